@@ -1,0 +1,163 @@
+/*
+ * cvg.h -- C-ABI of the B200 color-pair search (libcolorvibe_gpu.so).
+ *
+ * Drop-in boundary for the reference hot path `colorvibe::batch_search`
+ * (reference proj/include/colorvibe/search.hpp:126-130, src/search.cpp:403-456)
+ * and its pybind binding `colorvibe.batch_search` (proj/bindings/module.cpp:121-131).
+ * One `cvg_search` call evaluates a whole batch of searches -- the loop the
+ * reference runs one call at a time in feasibility_matrix
+ * (src/feasibility.cpp:261-292) and the bench sweep (src/bench.cpp:18-34).
+ *
+ * Plain C types only: no torch, no C++ in any signature.  All functions are
+ * thread-safe; a context may be shared by threads (calls on one context are
+ * serialized internally).  Errors are reported as status codes plus a
+ * thread-local message (cvg_last_error); the C++ wrapper maps CVG_EINVAL to
+ * std::invalid_argument and everything else to std::runtime_error, the
+ * exception types the reference throws (search.cpp:22-30, 49-56, 92-111).
+ *
+ * There is no CPU fallback: if the CUDA kernels cannot run, calls fail with
+ * CVG_ECUDA.  Options the device path does not implement fail with
+ * CVG_EUNSUPPORTED instead of silently computing on the host.
+ */
+#ifndef CVG_H_
+#define CVG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CVG_API __attribute__((visibility("default")))
+
+/* status codes */
+#define CVG_OK 0
+#define CVG_EINVAL 1       /* invalid color / grid / thresholds / pattern (reference: invalid_argument) */
+#define CVG_ECUDA 2        /* CUDA runtime failure, no device, kernel image missing */
+#define CVG_ENOMEM 3       /* host or device allocation failed */
+#define CVG_EOVERFLOW 4    /* device pair buffer too small (counts are still valid) */
+#define CVG_EUNSUPPORTED 5 /* option combination not implemented on the device path */
+
+/* SearchOptions::delta_mode / delta_basis (search.hpp:81-96) */
+#define CVG_DELTA_QUANTIZED 0
+#define CVG_DELTA_CONTINUOUS 1
+#define CVG_BASIS_TARGET_SWING 0
+#define CVG_BASIS_FRAME_DIFF 1
+
+/* what a search returns */
+#define CVG_OUT_PAIRS 0  /* every passing pair, canonical (search, radius, angle) order */
+#define CVG_OUT_COUNTS 1 /* per-search pair count only */
+#define CVG_OUT_FIRST 2  /* per-search count + first pair in canonical order (per-pixel mode) */
+
+/* evaluation path (all give identical results) */
+#define CVG_PATH_FAST 0  /* FP32 with a proven error bound + FP64 repair of near-boundary values */
+#define CVG_PATH_EXACT 1 /* FP64 op-for-op restatement for every candidate (serial_search) */
+#define CVG_PATH_AUDIT 2 /* both; counts bound violations (tests) */
+
+typedef struct cvg_ctx cvg_ctx;
+typedef struct cvg_plan cvg_plan;
+
+/*
+ * A batch of searches over one explicit grid.  Search s is
+ * (target_rgb[3s..3s+2], pattern_bits[s], v_th[s], r_novib[s]); pattern bits
+ * are r<<2 | g<<1 | b ("101" == 5), BitPattern search.hpp:14-24.  The grid is
+ * VibrationGrid (search.hpp:39-53): radii >= 0 strictly increasing, angles in
+ * [0, 2pi) strictly increasing, radians.  n_radii * n_angles must be < 2^32.
+ */
+typedef struct {
+    int32_t n_searches;
+    const int32_t* target_rgb;   /* [n_searches * 3], codes in [0, 255] */
+    const int32_t* pattern_bits; /* [n_searches], 1..7 */
+    const double* v_th;          /* [n_searches], > 0 */
+    const double* r_novib;       /* [n_searches], (0, 1] */
+    int32_t n_radii;
+    const double* radii;
+    int32_t n_angles;
+    const double* angles;
+    int32_t delta_mode;         /* CVG_DELTA_* */
+    int32_t delta_basis;        /* CVG_BASIS_* */
+    const double* white_point;  /* [3] or NULL for d65_white() (color.cpp:13-20) */
+    int32_t output;             /* CVG_OUT_* */
+    int32_t path;               /* CVG_PATH_* */
+    int32_t workers;            /* accepted for API parity, ignored: results never depend on it */
+} cvg_search_desc;
+
+/*
+ * Host-side result (library-owned; release with cvg_result_free).
+ * Pair p: idx[p] = k * n_angles + m (radius index k, angle index m),
+ * codes[6p .. 6p+5] = plus r,g,b then minus r,g,b.  Pairs of search s are
+ * [offsets[s], offsets[s+1]).  FIRST mode fills first_idx/first_codes instead
+ * (first_idx = 0xFFFFFFFF when a search has no pair).
+ */
+typedef struct {
+    int32_t n_searches;
+    uint64_t n_pairs;
+    uint64_t* counts;      /* [n_searches] */
+    uint64_t* offsets;     /* [n_searches + 1] (PAIRS) */
+    uint32_t* idx;         /* [n_pairs] (PAIRS) */
+    uint8_t* codes;        /* [n_pairs * 6] (PAIRS) */
+    uint32_t* first_idx;   /* [n_searches] (FIRST) */
+    uint8_t* first_codes;  /* [n_searches * 6] (FIRST) */
+    /* diagnostics */
+    uint64_t n_candidates;
+    uint64_t n_band_repairs;  /* candidates whose band decision went to FP64 */
+    uint64_t n_code_repairs;  /* passing candidates whose codes went to FP64 */
+    uint64_t n_audit_violations; /* PATH_AUDIT: FP32 "certain" decisions that were wrong (must be 0) */
+    uint64_t n_class_mismatch;   /* band decision != classify_pair on exact codes (must be 0) */
+    float audit_max_ratio;       /* PATH_AUDIT: max |lin32 - lin64| / bound (must be < 1) */
+    float kernel_ms;             /* device time of the search kernels of this call */
+} cvg_result;
+
+/* ---- context ----------------------------------------------------------- */
+CVG_API int cvg_create(int device, cvg_ctx** out);
+CVG_API void cvg_destroy(cvg_ctx* ctx);
+CVG_API const char* cvg_last_error(void);
+CVG_API const char* cvg_version(void);
+
+/* ---- one-shot host API: host buffers in, host result out ------------------
+ * Validates exactly like the reference (messages included), prepares the
+ * per-target constants and glibc tables on the host, copies them to the
+ * device, runs the fused kernel, and copies counts + pairs back. */
+CVG_API int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out);
+CVG_API void cvg_result_free(cvg_result* res);
+
+/* ---- plan API: device-resident repeated runs (benchmarks, pipelines) -----
+ * cvg_plan_create does validation + host prep + upload once.  cvg_plan_run
+ * enqueues the search on `stream` (a cudaStream_t, 0 = legacy default) with
+ * inputs already in HBM; results stay on the device.  cvg_plan_sync waits
+ * and reports overflow (CVG_EOVERFLOW if pair capacity was short: counts are
+ * valid, rerun after cvg_plan_reserve).  cvg_plan_fetch copies results to a
+ * host cvg_result. */
+CVG_API int cvg_plan_create(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_plan** out);
+CVG_API void cvg_plan_destroy(cvg_plan* plan);
+CVG_API int cvg_plan_reserve(cvg_plan* plan, uint64_t pair_capacity);
+CVG_API int cvg_plan_run(cvg_plan* plan, void* stream);
+CVG_API int cvg_plan_sync(cvg_plan* plan, uint64_t* n_pairs);
+CVG_API int cvg_plan_fetch(cvg_plan* plan, cvg_result* out);
+/* device pointers of the plan's outputs (valid until the plan is destroyed) */
+CVG_API int cvg_plan_device_outputs(cvg_plan* plan, uint64_t** counts, uint32_t** idx,
+                                    uint8_t** codes, uint64_t* capacity);
+/* number of kernel launches one cvg_plan_run enqueues */
+CVG_API int cvg_plan_launches(const cvg_plan* plan);
+CVG_API uint64_t cvg_plan_candidates(const cvg_plan* plan);
+
+/* ---- host-side scalar helpers of the reference API (color.hpp:34-66) ------
+ * Exact host conversions (same glibc pow/cbrt as the reference); used by the
+ * C++ / Python API surface, never by the search itself. */
+CVG_API int cvg_srgb_to_lab(const int32_t rgb[3], const double* white_point, double lab[3]);
+CVG_API int cvg_lab_to_srgb_clipped(const double lab[3], const double* white_point, int32_t rgb[3]);
+/* returns 1 if in gamut (rgb filled), 0 if not, negative status on error */
+CVG_API int cvg_lab_to_srgb(const double lab[3], const double* white_point, int32_t rgb[3]);
+CVG_API void cvg_d65_white(double out[3]);
+CVG_API void cvg_quant_thresholds(double out[256]);
+
+/* FP32 FFMA issue-rate microbenchmark (roofline denominator); returns
+ * lane-FFMA per second measured on `device`, 0 on failure. */
+CVG_API double cvg_measure_ffma_peak(int device, float* ms_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CVG_H_ */

@@ -1,0 +1,180 @@
+"""ctypes loaders for the parity checkers -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+arm may import this module.  The product package never does.
+
+* ``Oracle``    -- oracle/build/libcv_oracle.so, our C restatement
+                   (oracle/cv_oracle.c) of the reference search.
+* ``Reference`` -- oracle/_ref/libcolorvibe_ref_v{3,4}.so, the reference's own
+                   src/color.cpp + src/search.cpp behind oracle/ref_shim.cpp.
+
+Both return searches as (idx uint32[n], codes uint8[n, 6], deltas f64[n, 3]),
+idx = k * n_angles + m in canonical (radius, angle) order (search.cpp:448-455).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int32)
+_up = C.POINTER(C.c_uint32)
+_bp = C.POINTER(C.c_uint8)
+_u64p = C.POINTER(C.c_uint64)
+
+
+def build() -> None:
+    """Runs oracle/Makefile (reference targets skipped when sources absent)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+def _cpu_has_avx512() -> bool:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    return " avx512f " in line + " "
+    except OSError:
+        pass
+    return False
+
+
+def _ptr(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+class _Lib:
+    prefix = ""
+
+    def __init__(self, path: str):
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"parity checker not built: {path} (run oracle/Makefile)")
+        self.path = path
+        self.lib = C.CDLL(path)
+        p = self.prefix
+        f = getattr(self.lib, p + "search")
+        f.restype = C.c_int64
+        f.argtypes = [_ip, C.c_int, C.c_double, C.c_double, _dp, C.c_int, _dp, C.c_int,
+                      C.c_int, C.c_int, _dp, C.c_int, C.c_int, _up, _bp, _dp, C.c_int64]
+        self._search = f
+        for name in ("thresholds", "xyz_to_rgb", "white"):
+            getattr(self.lib, p + name).restype = None
+        getattr(self.lib, p + "table_code").restype = C.c_int
+        getattr(self.lib, p + "table_code").argtypes = [C.c_double]
+        getattr(self.lib, p + "quantize").restype = C.c_int
+        getattr(self.lib, p + "quantize").argtypes = [C.c_double]
+
+    # -- known-answer constants ------------------------------------------
+    def thresholds(self) -> np.ndarray:
+        out = np.zeros(256, np.float64)
+        getattr(self.lib, self.prefix + "thresholds")(_ptr(out, _dp))
+        return out
+
+    def xyz_to_rgb(self) -> np.ndarray:
+        out = np.zeros(9, np.float64)
+        getattr(self.lib, self.prefix + "xyz_to_rgb")(_ptr(out, _dp))
+        return out.reshape(3, 3)
+
+    def white(self) -> np.ndarray:
+        out = np.zeros(3, np.float64)
+        getattr(self.lib, self.prefix + "white")(_ptr(out, _dp))
+        return out
+
+    def table_code(self, x: float) -> int:
+        return getattr(self.lib, self.prefix + "table_code")(float(x))
+
+    def quantize(self, x: float) -> int:
+        return getattr(self.lib, self.prefix + "quantize")(float(x))
+
+    def srgb_to_lab(self, rgb) -> np.ndarray:
+        t = np.ascontiguousarray(rgb, np.int32)
+        out = np.zeros(3, np.float64)
+        getattr(self.lib, self.prefix + "srgb_to_lab")(*self._lab_args(t, out))
+        return out
+
+    def _lab_args(self, t, out):
+        return (_ptr(t, _ip), _ptr(out, _dp))
+
+    # -- one search ----------------------------------------------------------
+    def search(self, rgb, pattern_bits: int, v_th: float, r_novib: float, radii, angles,
+               delta_mode: int = 0, delta_basis: int = 0, white=None, method: int = 1,
+               workers: int = 1, want_deltas: bool = True):
+        t = np.ascontiguousarray(rgb, np.int32)
+        r = np.ascontiguousarray(radii, np.float64)
+        a = np.ascontiguousarray(angles, np.float64)
+        wp = None if white is None else np.ascontiguousarray(white, np.float64)
+        args = [_ptr(t, _ip), int(pattern_bits), float(v_th), float(r_novib),
+                _ptr(r, _dp), len(r), _ptr(a, _dp), len(a), int(delta_mode),
+                int(delta_basis), _ptr(wp, _dp), int(method), int(workers)]
+        n = self._search(*args, None, None, None, 0)
+        if n < 0:
+            raise ValueError(self.last_error())
+        idx = np.zeros(n, np.uint32)
+        codes = np.zeros((n, 6), np.uint8)
+        deltas = np.zeros((n, 3), np.float64) if want_deltas else None
+        if n:
+            n2 = self._search(*args, _ptr(idx, _up), _ptr(codes, _bp),
+                              _ptr(deltas, _dp), n)
+            assert n2 == n
+        return idx, codes, deltas
+
+    def last_error(self) -> str:
+        return "invalid argument"
+
+
+class Oracle(_Lib):
+    prefix = "cvo_"
+
+    def __init__(self, path: str | None = None):
+        super().__init__(path or os.path.join(HERE, "build", "libcv_oracle.so"))
+        self.lib.cvo_srgb_to_lab.argtypes = [_ip, _dp, _dp]
+        self.lib.cvo_lab_to_linear.argtypes = [_dp, _dp, _dp]
+
+    def _lab_args(self, t, out):
+        return (_ptr(t, _ip), None, _ptr(out, _dp))
+
+    def lab_to_linear(self, lab, white=None) -> np.ndarray:
+        l = np.ascontiguousarray(lab, np.float64)
+        out = np.zeros(3, np.float64)
+        wp = None if white is None else np.ascontiguousarray(white, np.float64)
+        self.lib.cvo_lab_to_linear(_ptr(l, _dp), _ptr(wp, _dp), _ptr(out, _dp))
+        return out
+
+
+class Reference(_Lib):
+    prefix = "cvr_"
+
+    def __init__(self, path: str | None = None):
+        if path is None:
+            v = "v4" if _cpu_has_avx512() else "v3"
+            path = os.path.join(HERE, "_ref", f"libcolorvibe_ref_{v}.so")
+        super().__init__(path)
+        self.lib.cvr_last_error.restype = C.c_char_p
+        self.lib.cvr_srgb_to_lab.argtypes = [_ip, _dp]
+        f = self.lib.cvr_search_many
+        f.restype = C.c_int64
+        f.argtypes = [C.c_int, _ip, _ip, _dp, _dp, _dp, C.c_int, _dp, C.c_int, C.c_int, _u64p]
+
+    def last_error(self) -> str:
+        return self.lib.cvr_last_error().decode()
+
+    def search_many(self, rgb, patterns, v_th, r_novib, radii, angles, workers: int = 0):
+        """Reference batch_search once per search (feasibility.cpp:273-275); counts only."""
+        t = np.ascontiguousarray(rgb, np.int32).reshape(-1, 3)
+        p = np.ascontiguousarray(patterns, np.int32)
+        v = np.ascontiguousarray(v_th, np.float64)
+        q = np.ascontiguousarray(r_novib, np.float64)
+        r = np.ascontiguousarray(radii, np.float64)
+        a = np.ascontiguousarray(angles, np.float64)
+        counts = np.zeros(len(t), np.uint64)
+        n = self.lib.cvr_search_many(len(t), _ptr(t, _ip), _ptr(p, _ip), _ptr(v, _dp),
+                                     _ptr(q, _dp), _ptr(r, _dp), len(r), _ptr(a, _dp),
+                                     len(a), int(workers), _ptr(counts, _u64p))
+        if n < 0:
+            raise ValueError(self.last_error())
+        return counts

@@ -1,0 +1,390 @@
+// bindings.cpp -- Python module `_core`, mirroring the reference binding
+// (proj/bindings/module.cpp:18-131: the types and the search functions) plus
+// a NumPy batch interface and device-resident plans for pipelines/benchmarks.
+// batch_search releases the GIL like the reference (module.cpp:121-131).
+#include <pybind11/numpy.h>
+#include <pybind11/operators.h>
+#include <pybind11/pybind11.h>
+#include <pybind11/stl.h>
+
+#include <numbers>
+#include <sstream>
+#include <stdexcept>
+
+#include "../../include/cvg.h"
+#include "colorvibe/search.hpp"
+
+namespace py = pybind11;
+using namespace colorvibe;
+
+namespace {
+
+void check(int status) {
+    if (status == CVG_OK) return;
+    const std::string msg = cvg_last_error();
+    if (status == CVG_EINVAL) throw std::invalid_argument(msg);
+    throw std::runtime_error(msg);
+}
+
+// Owns a cvg_result; NumPy arrays view its buffers (zero copy).
+struct ResultHolder {
+    cvg_result r{};
+    ~ResultHolder() { cvg_result_free(&r); }
+};
+
+int out_mode(const std::string& s) {
+    if (s == "pairs") return CVG_OUT_PAIRS;
+    if (s == "counts") return CVG_OUT_COUNTS;
+    if (s == "first") return CVG_OUT_FIRST;
+    throw std::invalid_argument("output must be 'pairs', 'counts' or 'first'");
+}
+
+int path_mode(const std::string& s) {
+    if (s == "fast") return CVG_PATH_FAST;
+    if (s == "exact") return CVG_PATH_EXACT;
+    if (s == "audit") return CVG_PATH_AUDIT;
+    throw std::invalid_argument("path must be 'fast', 'exact' or 'audit'");
+}
+
+using I32 = py::array_t<int32_t, py::array::c_style | py::array::forcecast>;
+using F64 = py::array_t<double, py::array::c_style | py::array::forcecast>;
+
+// Arrays kept alive for the duration of a descriptor's use.
+struct Desc {
+    I32 rgb, bits;
+    F64 vth, rn, radii, angles;
+    std::vector<double> wp;
+    cvg_search_desc d{};
+
+    Desc(I32 rgb_, I32 bits_, F64 vth_, F64 rn_, F64 radii_, F64 angles_, int mode, int basis, py::object white,
+         const std::string& output, const std::string& path)
+        : rgb(std::move(rgb_)), bits(std::move(bits_)), vth(std::move(vth_)), rn(std::move(rn_)),
+          radii(std::move(radii_)), angles(std::move(angles_)) {
+        const py::ssize_t n = bits.size();
+        if (rgb.size() != 3 * n || vth.size() != n || rn.size() != n) {
+            throw std::invalid_argument("targets must be (n, 3); patterns, v_th, r_novib must be (n,)");
+        }
+        d.n_searches = static_cast<int32_t>(n);
+        d.target_rgb = rgb.data();
+        d.pattern_bits = bits.data();
+        d.v_th = vth.data();
+        d.r_novib = rn.data();
+        d.n_radii = static_cast<int32_t>(radii.size());
+        d.radii = radii.data();
+        d.n_angles = static_cast<int32_t>(angles.size());
+        d.angles = angles.data();
+        d.delta_mode = mode;
+        d.delta_basis = basis;
+        if (!white.is_none()) {
+            wp = white.cast<std::vector<double>>();
+            if (wp.size() != 3) throw std::invalid_argument("white_point must have 3 entries");
+            d.white_point = wp.data();
+        }
+        d.output = out_mode(output);
+        d.path = path_mode(path);
+    }
+};
+
+py::dict result_dict(std::shared_ptr<ResultHolder> h, int output) {
+    py::object base = py::cast(h);
+    const cvg_result& r = h->r;
+    py::dict out;
+    const py::ssize_t n = r.n_searches;
+    py::array_t<uint64_t> counts(n);
+    std::copy(r.counts, r.counts + n, counts.mutable_data());
+    out["counts"] = counts;
+    out["n_pairs"] = r.n_pairs;
+    if (output == CVG_OUT_PAIRS) {
+        py::array_t<uint64_t> offs(n + 1);
+        std::copy(r.offsets, r.offsets + n + 1, offs.mutable_data());
+        out["offsets"] = offs;
+        const py::ssize_t np_ = static_cast<py::ssize_t>(r.n_pairs);
+        if (np_) {
+            out["idx"] = py::array_t<uint32_t>({np_}, {sizeof(uint32_t)}, r.idx, base);
+            out["codes"] = py::array_t<uint8_t>({np_, py::ssize_t(6)}, {py::ssize_t(6), py::ssize_t(1)}, r.codes, base);
+        } else {
+            out["idx"] = py::array_t<uint32_t>(0);
+            out["codes"] = py::array_t<uint8_t>(std::vector<py::ssize_t>{0, 6});
+        }
+    } else if (output == CVG_OUT_FIRST) {
+        if (n) {
+            out["first_idx"] = py::array_t<uint32_t>({n}, {sizeof(uint32_t)}, r.first_idx, base);
+            out["first_codes"] = py::array_t<uint8_t>({n, py::ssize_t(6)}, {py::ssize_t(6), py::ssize_t(1)}, r.first_codes, base);
+        } else {
+            out["first_idx"] = py::array_t<uint32_t>(0);
+            out["first_codes"] = py::array_t<uint8_t>(std::vector<py::ssize_t>{0, 6});
+        }
+    }
+    py::dict stats;
+    stats["candidates"] = r.n_candidates;
+    stats["band_repairs"] = r.n_band_repairs;
+    stats["code_repairs"] = r.n_code_repairs;
+    stats["audit_violations"] = r.n_audit_violations;
+    stats["class_mismatch"] = r.n_class_mismatch;
+    stats["audit_max_ratio"] = r.audit_max_ratio;
+    stats["kernel_ms"] = r.kernel_ms;
+    out["stats"] = stats;
+    return out;
+}
+
+struct Context {
+    cvg_ctx* ctx = nullptr;
+    explicit Context(int device) { check(cvg_create(device, &ctx)); }
+    ~Context() { cvg_destroy(ctx); }
+};
+
+struct Plan {
+    std::shared_ptr<Context> ctx;
+    std::unique_ptr<Desc> desc;
+    cvg_plan* plan = nullptr;
+    int output = 0;
+    ~Plan() { cvg_plan_destroy(plan); }
+};
+
+}  // namespace
+
+PYBIND11_MODULE(_core, m) {
+    m.doc() = "B200 color-vibration pair search (drop-in for colorvibe._core search API)";
+
+    // ---- reference types (module.cpp:18-104) ----
+    py::class_<SrgbColor>(m, "SrgbColor")
+        .def(py::init<int, int, int>(), py::arg("r"), py::arg("g"), py::arg("b"))
+        .def_readwrite("r", &SrgbColor::r)
+        .def_readwrite("g", &SrgbColor::g)
+        .def_readwrite("b", &SrgbColor::b)
+        .def(py::self == py::self)
+        .def("__repr__", [](const SrgbColor& c) {
+            std::ostringstream s;
+            s << "SrgbColor(" << c.r << ", " << c.g << ", " << c.b << ")";
+            return s.str();
+        });
+
+    py::class_<LabColor>(m, "LabColor")
+        .def(py::init<double, double, double>(), py::arg("l"), py::arg("a"), py::arg("b"))
+        .def_readwrite("l", &LabColor::l)
+        .def_readwrite("a", &LabColor::a)
+        .def_readwrite("b", &LabColor::b)
+        .def("__repr__", [](const LabColor& c) {
+            std::ostringstream s;
+            s << "LabColor(" << c.l << ", " << c.a << ", " << c.b << ")";
+            return s.str();
+        });
+
+    py::class_<WhitePoint>(m, "WhitePoint")
+        .def(py::init<double, double, double>(), py::arg("x"), py::arg("y"), py::arg("z"))
+        .def_readwrite("x", &WhitePoint::x)
+        .def_readwrite("y", &WhitePoint::y)
+        .def_readwrite("z", &WhitePoint::z);
+
+    py::class_<BitPattern>(m, "BitPattern")
+        .def(py::init([](const std::string& s) { return BitPattern::parse(s); }), py::arg("bits"))
+        .def_static("parse", &BitPattern::parse)
+        .def_readwrite("r", &BitPattern::r)
+        .def_readwrite("g", &BitPattern::g)
+        .def_readwrite("b", &BitPattern::b)
+        .def("any", &BitPattern::any)
+        .def(py::self == py::self)
+        .def("__str__", &BitPattern::str)
+        .def("__repr__", [](const BitPattern& p) { return "BitPattern(\"" + p.str() + "\")"; });
+
+    py::class_<Thresholds>(m, "Thresholds")
+        .def(py::init<double, double>(), py::arg("v_th"), py::arg("r_novib"))
+        .def_readwrite("v_th", &Thresholds::v_th)
+        .def_readwrite("r_novib", &Thresholds::r_novib)
+        .def("low_band", &Thresholds::low_band)
+        .def("validate", &Thresholds::validate);
+
+    py::class_<VibrationGrid>(m, "VibrationGrid")
+        .def(py::init<>())
+        .def_static("uniform", &VibrationGrid::uniform, py::arg("radius_min"), py::arg("radius_max"),
+                    py::arg("radius_step"), py::arg("angle_min_deg"), py::arg("angle_max_deg"),
+                    py::arg("angle_step_deg"))
+        .def_static("standard", &VibrationGrid::standard)
+        .def_readwrite("radii", &VibrationGrid::radii)
+        .def_readwrite("angles", &VibrationGrid::angles)
+        .def("candidate_count", &VibrationGrid::candidate_count)
+        .def("validate", &VibrationGrid::validate);
+
+    py::class_<ChannelDeltas>(m, "ChannelDeltas")
+        .def(py::init<double, double, double>(), py::arg("dr") = 0.0, py::arg("dg") = 0.0, py::arg("db") = 0.0)
+        .def_readonly("dr", &ChannelDeltas::dr)
+        .def_readonly("dg", &ChannelDeltas::dg)
+        .def_readonly("db", &ChannelDeltas::db)
+        .def(py::self == py::self)
+        .def("__repr__", [](const ChannelDeltas& d) {
+            std::ostringstream s;
+            s << "ChannelDeltas(" << d.dr << ", " << d.dg << ", " << d.db << ")";
+            return s.str();
+        });
+
+    py::class_<ColorPair>(m, "ColorPair")
+        .def(py::init<>())
+        .def_readonly("target", &ColorPair::target)
+        .def_readonly("plus", &ColorPair::plus)
+        .def_readonly("minus", &ColorPair::minus)
+        .def_readonly("radius", &ColorPair::radius)
+        .def_readonly("angle", &ColorPair::angle)
+        .def_readonly("deltas", &ColorPair::deltas)
+        .def(py::self == py::self)
+        .def_property_readonly("angle_deg", [](const ColorPair& p) { return p.angle * 180.0 / std::numbers::pi; })
+        .def("__repr__", [](const ColorPair& p) {
+            std::ostringstream s;
+            s << "ColorPair(r=" << p.radius << ", angle=" << p.angle << ", plus=(" << p.plus.r << "," << p.plus.g
+              << "," << p.plus.b << "), minus=(" << p.minus.r << "," << p.minus.g << "," << p.minus.b << "))";
+            return s.str();
+        });
+
+    py::enum_<DeltaMode>(m, "DeltaMode")
+        .value("QUANTIZED", DeltaMode::Quantized)
+        .value("CONTINUOUS", DeltaMode::Continuous);
+    py::enum_<DeltaBasis>(m, "DeltaBasis")
+        .value("TARGET_SWING", DeltaBasis::TargetSwing)
+        .value("FRAME_DIFF", DeltaBasis::FrameDiff);
+
+    py::class_<SearchOptions>(m, "SearchOptions")
+        .def(py::init<>())
+        .def_readwrite("delta_mode", &SearchOptions::delta_mode)
+        .def_readwrite("delta_basis", &SearchOptions::delta_basis)
+        .def_readwrite("workers", &SearchOptions::workers)
+        .def_readwrite("white_point", &SearchOptions::white_point);
+
+    py::class_<SearchSpec>(m, "SearchSpec")
+        .def(py::init<SrgbColor, BitPattern, Thresholds>(), py::arg("target"), py::arg("pattern"),
+             py::arg("thresholds"))
+        .def_readwrite("target", &SearchSpec::target)
+        .def_readwrite("pattern", &SearchSpec::pattern)
+        .def_readwrite("thresholds", &SearchSpec::thresholds);
+
+    // ---- reference functions (module.cpp:106-139) ----
+    m.def("d65_white", &d65_white, py::return_value_policy::copy);
+    m.def("srgb_to_lab", [](const SrgbColor& c) { return srgb_to_lab(c); }, py::arg("color"));
+    m.def("lab_to_srgb", [](const LabColor& c) { return lab_to_srgb(c); }, py::arg("color"),
+          "Returns None when the color falls outside the sRGB gamut");
+    m.def("lab_to_srgb_clipped", [](const LabColor& c) { return lab_to_srgb_clipped(c); }, py::arg("color"),
+          "Clamps out-of-gamut channels before quantizing");
+    m.def("in_gamut", [](const LabColor& c) { return in_gamut(c); }, py::arg("color"));
+    m.def("srgb_to_linear", &srgb_to_linear, py::arg("code"));
+    m.def("displaced_pair", &displaced_pair, py::arg("target"), py::arg("radius"), py::arg("angle"));
+    m.def(
+        "serial_search",
+        [](const SrgbColor& target, const VibrationGrid& grid, const BitPattern& pattern, const Thresholds& th,
+           int workers) {
+            SearchOptions opts;
+            opts.workers = workers;
+            return serial_search(target, grid, pattern, th, opts);
+        },
+        py::arg("target"), py::arg("grid"), py::arg("pattern"), py::arg("thresholds"), py::arg("workers") = 0,
+        py::call_guard<py::gil_scoped_release>());
+    m.def(
+        "batch_search",
+        [](const SrgbColor& target, const VibrationGrid& grid, const BitPattern& pattern, const Thresholds& th,
+           int workers) {
+            SearchOptions opts;
+            opts.workers = workers;
+            return batch_search(target, grid, pattern, th, opts);
+        },
+        py::arg("target"), py::arg("grid"), py::arg("pattern"), py::arg("thresholds"), py::arg("workers") = 0,
+        py::call_guard<py::gil_scoped_release>());
+    // Options-aware forms of the C++ API (search.hpp:126-130 take SearchOptions).
+    m.def("batch_search_opts", &batch_search, py::arg("target"), py::arg("grid"), py::arg("pattern"),
+          py::arg("thresholds"), py::arg("options"), py::call_guard<py::gil_scoped_release>());
+    m.def("serial_search_opts", &serial_search, py::arg("target"), py::arg("grid"), py::arg("pattern"),
+          py::arg("thresholds"), py::arg("options"), py::call_guard<py::gil_scoped_release>());
+    m.def("batch_search_many", &batch_search_many, py::arg("specs"), py::arg("grid"),
+          py::arg("options") = SearchOptions{}, py::call_guard<py::gil_scoped_release>());
+    m.def("batch_count_many", &batch_count_many, py::arg("specs"), py::arg("grid"),
+          py::arg("options") = SearchOptions{}, py::call_guard<py::gil_scoped_release>());
+    m.def("channel_deltas", &channel_deltas, py::arg("target"), py::arg("plus"), py::arg("minus"));
+    m.def("frame_deltas", &frame_deltas, py::arg("plus"), py::arg("minus"));
+    m.def("classify_pair", &classify_pair, py::arg("deltas"), py::arg("pattern"), py::arg("thresholds"),
+          "True when every channel delta satisfies its bit's band");
+    m.def("classification_margin", &classification_margin, py::arg("pair"), py::arg("thresholds"));
+    m.def("select_best", &select_best, py::arg("pairs"), py::arg("thresholds"), py::return_value_policy::copy);
+
+    // ---- low-level C-ABI access (NumPy in / NumPy out) ----
+    m.def("version", [] { return std::string(cvg_version()); });
+    m.def("quant_thresholds", [] {
+        py::array_t<double> a(256);
+        cvg_quant_thresholds(a.mutable_data());
+        return a;
+    });
+    m.def("measure_ffma_peak", [](int device) {
+        float ms = 0.f;
+        const double v = cvg_measure_ffma_peak(device, &ms);
+        return py::make_tuple(v, ms);
+    }, py::arg("device") = 0);
+
+    py::class_<Context, std::shared_ptr<Context>>(m, "Context")
+        .def(py::init<int>(), py::arg("device") = 0)
+        .def(
+            "search",
+            [](std::shared_ptr<Context> self, I32 rgb, I32 bits, F64 vth, F64 rn, F64 radii, F64 angles,
+               const std::string& output, const std::string& path, int mode, int basis, py::object white) {
+                Desc d(std::move(rgb), std::move(bits), std::move(vth), std::move(rn), std::move(radii),
+                       std::move(angles), mode, basis, white, output, path);
+                auto h = std::make_shared<ResultHolder>();
+                int st;
+                {
+                    py::gil_scoped_release nogil;
+                    st = cvg_search(self->ctx, &d.d, &h->r);
+                }
+                check(st);
+                return result_dict(h, d.d.output);
+            },
+            py::arg("targets"), py::arg("patterns"), py::arg("v_th"), py::arg("r_novib"), py::arg("radii"),
+            py::arg("angles"), py::arg("output") = "pairs", py::arg("path") = "fast", py::arg("delta_mode") = 0,
+            py::arg("delta_basis") = 0, py::arg("white_point") = py::none())
+        .def(
+            "plan",
+            [](std::shared_ptr<Context> self, I32 rgb, I32 bits, F64 vth, F64 rn, F64 radii, F64 angles,
+               const std::string& output, const std::string& path, int mode, int basis, py::object white) {
+                auto p = std::make_unique<Plan>();
+                p->ctx = self;
+                p->desc = std::make_unique<Desc>(std::move(rgb), std::move(bits), std::move(vth), std::move(rn),
+                                                 std::move(radii), std::move(angles), mode, basis, white, output, path);
+                p->output = p->desc->d.output;
+                check(cvg_plan_create(self->ctx, &p->desc->d, &p->plan));
+                return p;
+            },
+            py::arg("targets"), py::arg("patterns"), py::arg("v_th"), py::arg("r_novib"), py::arg("radii"),
+            py::arg("angles"), py::arg("output") = "pairs", py::arg("path") = "fast", py::arg("delta_mode") = 0,
+            py::arg("delta_basis") = 0, py::arg("white_point") = py::none());
+
+    py::class_<ResultHolder, std::shared_ptr<ResultHolder>>(m, "_Result");
+
+    py::class_<Plan>(m, "Plan")
+        .def("run", [](Plan& p, uintptr_t stream) { check(cvg_plan_run(p.plan, reinterpret_cast<void*>(stream))); },
+             py::arg("stream") = 0)
+        .def("sync", [](Plan& p) {
+            uint64_t n = 0;
+            int st;
+            {
+                py::gil_scoped_release nogil;
+                st = cvg_plan_sync(p.plan, &n);
+            }
+            check(st);
+            return n;
+        })
+        .def("reserve", [](Plan& p, uint64_t cap) { check(cvg_plan_reserve(p.plan, cap)); })
+        .def("fetch", [](Plan& p) {
+            auto h = std::make_shared<ResultHolder>();
+            int st;
+            {
+                py::gil_scoped_release nogil;
+                st = cvg_plan_fetch(p.plan, &h->r);
+            }
+            check(st);
+            return result_dict(h, p.output);
+        })
+        .def_property_readonly("launches", [](const Plan& p) { return cvg_plan_launches(p.plan); })
+        .def_property_readonly("candidates", [](const Plan& p) { return cvg_plan_candidates(p.plan); })
+        .def("device_outputs", [](Plan& p) {
+            uint64_t* counts = nullptr;
+            uint32_t* idx = nullptr;
+            uint8_t* codes = nullptr;
+            uint64_t cap = 0;
+            check(cvg_plan_device_outputs(p.plan, &counts, &idx, &codes, &cap));
+            return py::make_tuple(reinterpret_cast<uintptr_t>(counts), reinterpret_cast<uintptr_t>(idx),
+                                  reinterpret_cast<uintptr_t>(codes), cap);
+        });
+}

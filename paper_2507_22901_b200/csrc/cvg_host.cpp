@@ -1,0 +1,961 @@
+// cvg_host.cpp -- host side of libcolorvibe_gpu.so: the C-ABI in include/cvg.h.
+//
+// Compiled with the reference's FP flags (-ffp-contract=off, no errno/traps)
+// so every double computed here -- target Lab (glibc pow/cbrt), per-angle
+// sin/cos (glibc), the quantization threshold table (bisection over glibc
+// pow), the per-target hoisted constants -- carries the same bits as the
+// reference (src/color.cpp:57-70, src/search.cpp:341-370, 414-419,
+// src/convert_kernel.hpp:123-146).  Those are one-off per-call tables; every
+// candidate is evaluated on the GPU (cvg_kernels.cu).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <numbers>
+#include <string>
+#include <vector>
+
+#include "../../include/cvg.h"
+#include "cvg_internal.h"
+#include "cvg_layout.h"
+
+using cvg::LaunchArgs;
+using cvg::SearchConst;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(CVG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CVG_CUDA(call)                                  \
+    do {                                                \
+        cudaError_t _e = (call);                        \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// Pinned constants and scalar conversions (restating convert_kernel.hpp).
+
+struct Mat3 {
+    double m[3][3];
+};
+
+constexpr Mat3 kRgbToXyz{{{0.4124, 0.3576, 0.1805}, {0.2126, 0.7152, 0.0722}, {0.0193, 0.1192, 0.9505}}};
+
+// Adjugate over determinant with the reference's association
+// (convert_kernel.hpp:27-43), evaluated at compile time.
+constexpr Mat3 adjugate_inverse(const Mat3& a) {
+    const auto& m = a.m;
+    const double c00 = m[1][1] * m[2][2] - m[1][2] * m[2][1];
+    const double c01 = m[1][0] * m[2][2] - m[1][2] * m[2][0];
+    const double c02 = m[1][0] * m[2][1] - m[1][1] * m[2][0];
+    const double det = m[0][0] * c00 - m[0][1] * c01 + m[0][2] * c02;
+    Mat3 r{};
+    r.m[0][0] = c00 / det;
+    r.m[0][1] = (m[0][2] * m[2][1] - m[0][1] * m[2][2]) / det;
+    r.m[0][2] = (m[0][1] * m[1][2] - m[0][2] * m[1][1]) / det;
+    r.m[1][0] = (m[1][2] * m[2][0] - m[1][0] * m[2][2]) / det;
+    r.m[1][1] = (m[0][0] * m[2][2] - m[0][2] * m[2][0]) / det;
+    r.m[1][2] = (m[0][2] * m[1][0] - m[0][0] * m[1][2]) / det;
+    r.m[2][0] = c02 / det;
+    r.m[2][1] = (m[0][1] * m[2][0] - m[0][0] * m[2][1]) / det;
+    r.m[2][2] = (m[0][0] * m[1][1] - m[0][1] * m[1][0]) / det;
+    return r;
+}
+
+constexpr Mat3 kXyzToRgb = adjugate_inverse(kRgbToXyz);
+constexpr double kEps = 216.0 / 24389.0;
+constexpr double kKappa = 24389.0 / 27.0;
+constexpr double kInvKappa = 27.0 / 24389.0;
+constexpr double kInv500 = 1.0 / 500.0;
+constexpr double kInv200 = 1.0 / 200.0;
+constexpr double kGamutEps = 1e-12;
+constexpr double kTwoPi = 2.0 * std::numbers::pi;
+
+double f_lab(double t) { return t > kEps ? std::cbrt(t) : (kKappa * t + 16.0) / 116.0; }
+
+double f_lab_inv(double u) {
+    const double u3 = (u * u) * u;
+    return u3 > kEps ? u3 : (116.0 * u - 16.0) * kInvKappa;
+}
+
+double eotf(double u) { return u <= 0.04045 ? u / 12.92 : std::pow((u + 0.055) / 1.055, 2.4); }
+double oetf(double x) { return x <= 0.0031308 ? 12.92 * x : 1.055 * std::pow(x, 1.0 / 2.4) - 0.055; }
+
+int quantize(double linear) {
+    const double x = linear < 0.0 ? 0.0 : (linear > 1.0 ? 1.0 : linear);
+    return static_cast<int>(std::floor(255.0 * oetf(x) + 0.5));
+}
+
+const double* white_or_d65(const double* wp) {
+    static const double d65[3] = {(kRgbToXyz.m[0][0] + kRgbToXyz.m[0][1]) + kRgbToXyz.m[0][2],
+                                  (kRgbToXyz.m[1][0] + kRgbToXyz.m[1][1]) + kRgbToXyz.m[1][2],
+                                  (kRgbToXyz.m[2][0] + kRgbToXyz.m[2][1]) + kRgbToXyz.m[2][2]};
+    return wp ? wp : d65;
+}
+
+void to_lab(const int32_t c[3], const double* wp, double lab[3]) {
+    const double rl = eotf(c[0] / 255.0), gl = eotf(c[1] / 255.0), bl = eotf(c[2] / 255.0);
+    const auto& m = kRgbToXyz.m;
+    const double x = (m[0][0] * rl + m[0][1] * gl) + m[0][2] * bl;
+    const double y = (m[1][0] * rl + m[1][1] * gl) + m[1][2] * bl;
+    const double z = (m[2][0] * rl + m[2][1] * gl) + m[2][2] * bl;
+    const double fx = f_lab(x / wp[0]), fy = f_lab(y / wp[1]), fz = f_lab(z / wp[2]);
+    lab[0] = 116.0 * fy - 16.0;
+    lab[1] = 500.0 * (fx - fy);
+    lab[2] = 200.0 * (fy - fz);
+}
+
+void to_linear(const double lab[3], const double* wp, double lin[3]) {
+    const double fy = (lab[0] + 16.0) / 116.0;
+    const double fx = fy + lab[1] * kInv500;
+    const double fz = fy - lab[2] * kInv200;
+    const double x = wp[0] * f_lab_inv(fx), y = wp[1] * f_lab_inv(fy), z = wp[2] * f_lab_inv(fz);
+    const auto& m = kXyzToRgb.m;
+    for (int c = 0; c < 3; ++c) lin[c] = (m[c][0] * x + m[c][1] * y) + m[c][2] * z;
+}
+
+// Quantization thresholds: thr[c] = smallest double x with quantize(x) >= c,
+// found by bisection over the glibc-pow quantizer (convert_kernel.hpp:127-141).
+struct Tables {
+    double thr[256];
+    float thr_f[258];
+    uint8_t guess[cvg::kGuessBuckets + 1];
+    Tables() {
+        thr[0] = 0.0;
+        for (int code = 1; code <= 255; ++code) {
+            double lo = thr[code - 1], hi = 1.0;
+            while (std::nextafter(lo, 1.0) < hi) {
+                const double mid = 0.5 * (lo + hi);
+                (quantize(mid) >= code ? hi : lo) = mid;
+            }
+            thr[code] = hi;
+        }
+        thr_f[0] = -INFINITY;
+        for (int c = 1; c < 256; ++c) thr_f[c] = static_cast<float>(thr[c]);
+        thr_f[256] = INFINITY;
+        thr_f[257] = INFINITY;
+        for (int i = 0; i <= cvg::kGuessBuckets; ++i) guess[i] = static_cast<uint8_t>(code(i / 4096.0));
+    }
+    int code(double x) const {
+        if (x <= 0.0) return 0;
+        if (x >= 1.0) return 255;
+        return static_cast<int>(std::upper_bound(thr + 1, thr + 256, x) - thr) - 1;
+    }
+};
+
+const Tables& tables() {
+    static const Tables t;
+    return t;
+}
+
+// ---------------------------------------------------------------------------
+// Validation, mirroring the reference's checks and messages
+// (color.cpp:27-39, search.cpp:22-30, 49-56, 92-111).
+
+int validate_color(const int32_t* c) {
+    if (c[0] < 0 || c[0] > 255 || c[1] < 0 || c[1] > 255 || c[2] < 0 || c[2] > 255) {
+        return fail(CVG_EINVAL, "sRGB channel code outside [0, 255]: (" + std::to_string(c[0]) + ", " +
+                                    std::to_string(c[1]) + ", " + std::to_string(c[2]) + ")");
+    }
+    return CVG_OK;
+}
+
+int validate_grid(const double* radii, int nr, const double* angles, int na) {
+    if (nr < 0 || na < 0 || (nr > 0 && !radii) || (na > 0 && !angles)) {
+        return fail(CVG_EINVAL, "grid arrays missing");
+    }
+    for (int i = 0; i < nr; ++i) {
+        if (!(std::isfinite(radii[i]) && radii[i] >= 0.0)) return fail(CVG_EINVAL, "grid radii must be non-negative");
+        if (i > 0 && !(radii[i] > radii[i - 1])) return fail(CVG_EINVAL, "grid radii must be strictly increasing");
+    }
+    for (int i = 0; i < na; ++i) {
+        if (!(std::isfinite(angles[i]) && angles[i] >= 0.0 && angles[i] < kTwoPi)) {
+            return fail(CVG_EINVAL, "grid angles must lie in [0, 2pi)");
+        }
+        if (i > 0 && !(angles[i] > angles[i - 1])) return fail(CVG_EINVAL, "grid angles must be strictly increasing");
+    }
+    return CVG_OK;
+}
+
+int validate_thresholds(double v_th, double r_novib) {
+    if (!(std::isfinite(v_th) && v_th > 0.0)) return fail(CVG_EINVAL, "v_th must be positive");
+    if (!(std::isfinite(r_novib) && r_novib > 0.0 && r_novib <= 1.0)) return fail(CVG_EINVAL, "r_novib must be in (0, 1]");
+    return CVG_OK;
+}
+
+int validate_desc(const cvg_search_desc* d) {
+    if (!d) return fail(CVG_EINVAL, "null search descriptor");
+    if (d->n_searches < 0) return fail(CVG_EINVAL, "n_searches must be >= 0");
+    if (d->n_searches > 0 && (!d->target_rgb || !d->pattern_bits || !d->v_th || !d->r_novib)) {
+        return fail(CVG_EINVAL, "search arrays missing");
+    }
+    if (d->delta_mode != CVG_DELTA_QUANTIZED && d->delta_mode != CVG_DELTA_CONTINUOUS) {
+        return fail(CVG_EINVAL, "unknown delta_mode");
+    }
+    if (d->delta_basis != CVG_BASIS_TARGET_SWING && d->delta_basis != CVG_BASIS_FRAME_DIFF) {
+        return fail(CVG_EINVAL, "unknown delta_basis");
+    }
+    if (d->output < CVG_OUT_PAIRS || d->output > CVG_OUT_FIRST) return fail(CVG_EINVAL, "unknown output mode");
+    if (d->path < CVG_PATH_FAST || d->path > CVG_PATH_AUDIT) return fail(CVG_EINVAL, "unknown path");
+    // Per search in the reference order: target, grid, thresholds, pattern.
+    int grid_checked = 0;
+    for (int s = 0; s < d->n_searches; ++s) {
+        if (int e = validate_color(d->target_rgb + 3 * s)) return e;
+        if (!grid_checked) {
+            if (int e = validate_grid(d->radii, d->n_radii, d->angles, d->n_angles)) return e;
+            grid_checked = 1;
+        }
+        if (int e = validate_thresholds(d->v_th[s], d->r_novib[s])) return e;
+        const int p = d->pattern_bits[s];
+        if (p < 0 || p > 7) return fail(CVG_EINVAL, "bit pattern must be three binary digits");
+        if (p == 0) return fail(CVG_EINVAL, "bit pattern has no set bits");
+    }
+    if (!grid_checked) {
+        if (int e = validate_grid(d->radii, d->n_radii, d->angles, d->n_angles)) return e;
+    }
+    if (static_cast<uint64_t>(d->n_radii) * static_cast<uint64_t>(d->n_angles) >= (1ull << 32)) {
+        return fail(CVG_EINVAL, "grid too large: n_radii * n_angles must be < 2^32");
+    }
+    if (d->delta_mode == CVG_DELTA_CONTINUOUS) {
+        return fail(CVG_EUNSUPPORTED,
+                    "DeltaMode::Continuous is not implemented on the device path (no CPU fallback)");
+    }
+    return CVG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Per-search constants and the FP32 error bound.
+
+float round_up_f(double x) {
+    if (std::isinf(x)) return static_cast<float>(x);
+    float f = static_cast<float>(x);
+    if (static_cast<double>(f) < x) f = std::nextafter(f, INFINITY);
+    return f;
+}
+
+float round_down_f(double x) {
+    if (std::isinf(x)) return static_cast<float>(x);
+    float f = static_cast<float>(x);
+    if (static_cast<double>(f) > x) f = std::nextafter(f, -INFINITY);
+    return f;
+}
+
+struct BoundTerms {
+    double err;  // |g32 - f^-1(f)| bound
+    double gmax; // max |f^-1(f)|
+};
+
+// Forward error of g = f^-1(f) computed in FP32 as in fast_linear():
+// f = fma(+-r, s', f0) with r, s', f0 rounded to float, then either
+// (f*f)*f or fma(f, K1, -K2).  u = 2^-24 (round to nearest).
+BoundTerms finv_bound(double f0, double rmax_scaled) {
+    const double u = std::ldexp(1.0, -24);
+    const double F0 = std::fabs(f0);
+    const double ef = 3.01 * u * rmax_scaled + 2.01 * u * F0;  // |f32 - f|
+    const double fm = F0 + rmax_scaled;                        // max |f|
+    const double cube_err = 3.0 * fm * fm * ef + 3.0 * fm * ef * ef + ef * ef * ef +
+                            2.01 * u * (fm + ef) * (fm + ef) * (fm + ef);
+    const double k1 = 3132.0 / 24389.0, k2 = 432.0 / 24389.0;
+    const double lin_err = k1 * ef + 2.01 * u * (k1 * fm + k2) + 2.0 * u * k1 * ef;
+    BoundTerms b;
+    b.err = std::max(cube_err, lin_err);
+    b.gmax = std::max(fm * fm * fm, k1 * fm + k2);
+    return b;
+}
+
+void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, const Tables& T,
+                       SearchConst& S) {
+    std::memset(&S, 0, sizeof(S));
+    const double* wp = white_or_d65(d->white_point);
+    const int32_t* t = d->target_rgb + 3 * s;
+    double lab[3];
+    to_lab(t, wp, lab);
+    // search.cpp:345-355
+    const auto& m = kXyzToRgb.m;
+    const double fy = (lab[0] + 16.0) / 116.0;
+    const double yv = wp[1] * f_lab_inv(fy);
+    S.fy = fy;
+    S.ta = lab[1];
+    S.tb = lab[2];
+    S.wx = wp[0];
+    S.wz = wp[2];
+    for (int c = 0; c < 3; ++c) S.cy64[c] = m[c][1] * yv;
+
+    const int bits[3] = {(d->pattern_bits[s] >> 2) & 1, (d->pattern_bits[s] >> 1) & 1, d->pattern_bits[s] & 1};
+    const double v_th = d->v_th[s];
+    const double low = v_th * d->r_novib[s];
+    const int k1 = v_th >= 255.0 ? 256 : static_cast<int>(v_th) + 1;
+    const int q0 = low >= 255.0 ? 255 : static_cast<int>(low);
+    S.k1 = k1;
+    S.q0 = q0;
+    S.flags = static_cast<uint32_t>(bits[0] | (bits[1] << 1) | (bits[2] << 2));
+    if (d->delta_basis == CVG_BASIS_FRAME_DIFF) S.flags |= 1u << 8;
+    for (int c = 0; c < 3; ++c) S.t[c] = t[c];
+    // make_bands (search.cpp:291-329): exact only for Quantized x TargetSwing.
+    for (int c = 0; c < 3; ++c) {
+        if (mode != cvg::kModeBand) {
+            S.lo[c] = -HUGE_VAL;
+            S.hi[c] = HUGE_VAL;
+        } else if (bits[c]) {
+            S.lo[c] = t[c] - k1 + 1 >= 1 ? T.thr[t[c] - k1 + 1] : -HUGE_VAL;
+            S.hi[c] = t[c] + k1 <= 255 ? T.thr[t[c] + k1] : HUGE_VAL;
+        } else {
+            S.lo[c] = t[c] - q0 >= 1 ? T.thr[t[c] - q0] : -HUGE_VAL;
+            S.hi[c] = t[c] + q0 + 1 <= 255 ? T.thr[t[c] + q0 + 1] : HUGE_VAL;
+        }
+    }
+
+    // FP32 constants.
+    const double fx0 = fy + lab[1] * kInv500;
+    const double fz0 = fy - lab[2] * kInv200;
+    S.fx0 = static_cast<float>(fx0);
+    S.fz0 = static_cast<float>(fz0);
+    const double u0 = 6.0 / 29.0;
+    const double rc = std::min((fx0 - u0) * 500.0, (fz0 - u0) * 200.0) * (1.0 - 1e-6) - 1e-6;
+    S.rcube = rc > 0.0 ? round_down_f(rc) : -1.0f;
+    const double u = std::ldexp(1.0, -24);
+    const BoundTerms bx = finv_bound(fx0, rmax * kInv500);
+    const BoundTerms bz = finv_bound(fz0, rmax * kInv200);
+    for (int c = 0; c < 3; ++c) {
+        const double mx = m[c][0] * wp[0], mz = m[c][2] * wp[2], cy = S.cy64[c];
+        S.mx[c] = static_cast<float>(mx);
+        S.mz[c] = static_cast<float>(mz);
+        S.cy[c] = static_cast<float>(cy);
+        const double amx = std::fabs(mx), amz = std::fabs(mz), acy = std::fabs(cy);
+        const double inner_max = amz * bz.gmax + acy;
+        const double e_inner = amz * bz.err * (1 + u) + u * amz * bz.gmax + u * acy + u * (inner_max + amz * bz.err);
+        const double lin_max = amx * bx.gmax + inner_max;
+        const double e_lin = amx * bx.err * (1 + u) + u * amx * bx.gmax + e_inner + u * (lin_max + amx * bx.err);
+        const double eps = 1.05 * e_lin + 1e-12;
+        S.eps[c] = round_up_f(eps);
+        S.eps_code[c] = round_up_f(eps + std::ldexp(1.0, -23));
+        S.lo_p[c] = round_up_f(S.lo[c] + eps);
+        S.lo_m[c] = round_down_f(S.lo[c] - eps);
+        S.hi_p[c] = round_up_f(S.hi[c] + eps);
+        S.hi_m[c] = round_down_f(S.hi[c] - eps);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Caching allocators (device and pinned host), per context.
+
+struct Pool {
+    bool device = true;
+    std::multimap<size_t, void*> free_blocks;
+    std::map<void*, size_t> sizes;
+    size_t cached = 0;
+
+    static size_t round(size_t n) {
+        const size_t g = 2u << 20;
+        return ((n ? n : 1) + g - 1) / g * g;
+    }
+
+    void* alloc(size_t n) {
+        n = round(n);
+        auto it = free_blocks.lower_bound(n);
+        if (it != free_blocks.end() && it->first <= 2 * n) {
+            void* p = it->second;
+            cached -= it->first;
+            free_blocks.erase(it);
+            return p;
+        }
+        void* p = nullptr;
+        cudaError_t e = device ? cudaMalloc(&p, n) : cudaMallocHost(&p, n);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            trim();
+            e = device ? cudaMalloc(&p, n) : cudaMallocHost(&p, n);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                return nullptr;
+            }
+        }
+        sizes[p] = n;
+        return p;
+    }
+
+    void release(void* p) {
+        if (!p) return;
+        auto it = sizes.find(p);
+        if (it == sizes.end()) return;
+        free_blocks.emplace(it->second, p);
+        cached += it->second;
+    }
+
+    void trim() {
+        for (auto& kv : free_blocks) {
+            if (device) cudaFree(kv.second); else cudaFreeHost(kv.second);
+            sizes.erase(kv.second);
+        }
+        free_blocks.clear();
+        cached = 0;
+    }
+
+    ~Pool() {
+        for (auto& kv : sizes) {
+            if (device) cudaFree(kv.first); else cudaFreeHost(kv.first);
+        }
+    }
+};
+
+}  // namespace
+
+struct cvg_ctx {
+    int device = 0;
+    int sms = 0;
+    cudaStream_t stream = nullptr;
+    std::recursive_mutex mu;
+    Pool dev;
+    Pool host;
+};
+
+struct cvg_plan {
+    cvg_ctx* ctx = nullptr;
+    int mode = 0, out = 0, path = 0;
+    int32_t n = 0, nr = 0, na = 0;
+    uint64_t candidates = 0;
+    int grid = 0;
+    bool empty = false;
+    LaunchArgs args{};
+    // device allocations (from ctx->dev)
+    void* d_const = nullptr;  // search consts + grid tables + thresholds
+    void* d_work = nullptr;   // status + ticket + counts + stats (memset per run)
+    size_t work_bytes = 0;
+    void* d_first = nullptr;
+    size_t first_bytes = 0;
+    void* d_out_idx = nullptr;
+    void* d_out_codes = nullptr;
+    uint64_t capacity = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    bool ran = false;
+    cudaStream_t last_stream = nullptr;
+};
+
+namespace {
+
+int ensure_device(cvg_ctx* ctx) {
+    CVG_CUDA(cudaSetDevice(ctx->device));
+    return CVG_OK;
+}
+
+void plan_free_outputs(cvg_plan* p) {
+    p->ctx->dev.release(p->d_out_idx);
+    p->ctx->dev.release(p->d_out_codes);
+    p->d_out_idx = p->d_out_codes = nullptr;
+    p->capacity = 0;
+}
+
+int plan_reserve(cvg_plan* p, uint64_t cap) {
+    if (p->out != cvg::kOutPairs || p->empty) return CVG_OK;
+    if (cap == 0) cap = 1;
+    if (cap == p->capacity && p->d_out_idx) return CVG_OK;
+    plan_free_outputs(p);
+    p->d_out_idx = p->ctx->dev.alloc(cap * sizeof(uint32_t));
+    p->d_out_codes = p->ctx->dev.alloc(cap * 6);
+    if (!p->d_out_idx || !p->d_out_codes) {
+        plan_free_outputs(p);
+        return fail(CVG_ENOMEM, "device allocation of the pair buffer failed");
+    }
+    p->capacity = cap;
+    p->args.out_idx = static_cast<uint32_t*>(p->d_out_idx);
+    p->args.out_codes = static_cast<uint8_t*>(p->d_out_codes);
+    p->args.capacity = cap;
+    return CVG_OK;
+}
+
+// Bump layout of several arrays inside one allocation (256-byte aligned).
+struct Layout {
+    size_t off = 0;
+    size_t take(size_t bytes) {
+        off = (off + 255) & ~size_t(255);
+        const size_t o = off;
+        off += bytes;
+        return o;
+    }
+};
+
+template <typename T>
+T* at(void* base, size_t off) {
+    return reinterpret_cast<T*>(static_cast<unsigned char*>(base) + off);
+}
+
+int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
+    const Tables& T = tables();
+    p->ctx = ctx;
+    p->mode = (d->delta_mode == CVG_DELTA_QUANTIZED && d->delta_basis == CVG_BASIS_TARGET_SWING) ? cvg::kModeBand
+                                                                                                 : cvg::kModeCodes;
+    p->out = d->output;
+    p->path = d->path;
+    p->n = d->n_searches;
+    p->nr = d->n_radii;
+    p->na = d->n_angles;
+    const uint64_t cps = static_cast<uint64_t>(p->nr) * static_cast<uint64_t>(p->na);
+    p->candidates = cps * static_cast<uint64_t>(p->n);
+    p->empty = p->candidates == 0;
+    if (p->empty) return CVG_OK;  // search.cpp:409-411
+
+    const uint32_t tps = static_cast<uint32_t>((cps + cvg::kTile - 1) / cvg::kTile);
+    const uint64_t n_tiles = static_cast<uint64_t>(tps) * static_cast<uint64_t>(p->n);
+    if (n_tiles >= (1ull << 31)) return fail(CVG_EINVAL, "batch too large for one plan (split the searches)");
+
+    // ---- host tables ----
+    std::vector<SearchConst> sc(p->n);
+    const double rmax = d->radii[p->nr - 1];
+    for (int s = 0; s < p->n; ++s) make_search_const(d, s, rmax, p->mode, T, sc[s]);
+    std::vector<float> radii_f(p->nr);
+    for (int k = 0; k < p->nr; ++k) radii_f[k] = static_cast<float>(d->radii[k]);
+    std::vector<float> trig_f(2 * static_cast<size_t>(p->na));
+    std::vector<double> trig_d(2 * static_cast<size_t>(p->na));
+    for (int j = 0; j < p->na; ++j) {  // search.cpp:414-419
+        const double sn = std::sin(d->angles[j]);
+        const double cs = std::cos(d->angles[j]);
+        trig_d[2 * j] = sn;
+        trig_d[2 * j + 1] = cs;
+        trig_f[2 * j] = static_cast<float>(sn * kInv500);
+        trig_f[2 * j + 1] = static_cast<float>(cs * kInv200);
+    }
+
+    // ---- one constant blob: [sc | radii_d | radii_f | trig_d | trig_f | thr_d | thr_f | guess] ----
+    Layout L;
+    const size_t o_sc = L.take(sizeof(SearchConst) * sc.size());
+    const size_t o_rd = L.take(sizeof(double) * p->nr);
+    const size_t o_rf = L.take(sizeof(float) * p->nr);
+    const size_t o_td = L.take(sizeof(double) * trig_d.size());
+    const size_t o_tf = L.take(sizeof(float) * trig_f.size());
+    const size_t o_thd = L.take(sizeof(double) * 256);
+    const size_t o_thf = L.take(sizeof(float) * 258);
+    const size_t o_gs = L.take(cvg::kGuessBuckets + 1);
+    const size_t bytes = L.off;
+    unsigned char* stage = static_cast<unsigned char*>(ctx->host.alloc(bytes));
+    p->d_const = ctx->dev.alloc(bytes);
+    if (!stage || !p->d_const) {
+        ctx->host.release(stage);
+        return fail(CVG_ENOMEM, "allocation of the search tables failed");
+    }
+    std::memcpy(stage + o_sc, sc.data(), sizeof(SearchConst) * sc.size());
+    std::memcpy(stage + o_rd, d->radii, sizeof(double) * p->nr);
+    std::memcpy(stage + o_rf, radii_f.data(), sizeof(float) * p->nr);
+    std::memcpy(stage + o_td, trig_d.data(), sizeof(double) * trig_d.size());
+    std::memcpy(stage + o_tf, trig_f.data(), sizeof(float) * trig_f.size());
+    std::memcpy(stage + o_thd, T.thr, sizeof(double) * 256);
+    std::memcpy(stage + o_thf, T.thr_f, sizeof(float) * 258);
+    std::memcpy(stage + o_gs, T.guess, cvg::kGuessBuckets + 1);
+    LaunchArgs& A = p->args;
+    std::memset(&A, 0, sizeof(A));
+    A.sc = at<const SearchConst>(p->d_const, o_sc);
+    A.radii_d = at<const double>(p->d_const, o_rd);
+    A.radii_f = at<const float>(p->d_const, o_rf);
+    A.trig_d = at<const double>(p->d_const, o_td);
+    A.trig_f = at<const float>(p->d_const, o_tf);
+    A.thr_d = at<const double>(p->d_const, o_thd);
+    A.thr_f = at<const float>(p->d_const, o_thf);
+    A.guess = at<const uint8_t>(p->d_const, o_gs);
+    cudaError_t e = cudaMemcpyAsync(p->d_const, stage, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    ctx->host.release(stage);
+    if (e != cudaSuccess) return cuda_fail(e, "upload of the search tables");
+
+    for (int i = 0; i < 9; ++i) A.minv[i] = kXyzToRgb.m[i / 3][i % 3];
+    A.n_searches = p->n;
+    A.nr = p->nr;
+    A.na = p->na;
+    A.aligned = (p->na % 32) == 0;
+    A.tiles_per_search = tps;
+    A.cand_per_search = static_cast<uint32_t>(cps);
+    A.na_magic = p->na > 1 ? (UINT64_MAX / static_cast<uint64_t>(p->na)) + 1 : 0;
+    A.n_tiles = n_tiles;
+
+    // ---- per-run workspace: status[n_tiles] | ticket | counts[n] | stats ----
+    Layout W;
+    const size_t o_st = W.take(sizeof(unsigned long long) * (p->out == cvg::kOutPairs ? n_tiles : 0));
+    const size_t o_tk = W.take(sizeof(unsigned int));
+    const size_t o_ct = W.take(sizeof(unsigned long long) * p->n);
+    const size_t o_ss = W.take(sizeof(cvg::Stats));
+    p->work_bytes = W.off;
+    p->d_work = ctx->dev.alloc(p->work_bytes);
+    if (!p->d_work) return fail(CVG_ENOMEM, "device allocation of the workspace failed");
+    A.status = at<unsigned long long>(p->d_work, o_st);
+    A.ticket = at<unsigned int>(p->d_work, o_tk);
+    A.counts = at<unsigned long long>(p->d_work, o_ct);
+    A.stats = at<cvg::Stats>(p->d_work, o_ss);
+    if (p->out == cvg::kOutFirst) {
+        Layout F;
+        const size_t o_fi = F.take(sizeof(uint32_t) * p->n);
+        const size_t o_fc = F.take(static_cast<size_t>(p->n) * 6);
+        p->first_bytes = F.off;
+        p->d_first = ctx->dev.alloc(p->first_bytes);
+        if (!p->d_first) return fail(CVG_ENOMEM, "device allocation of the first-pair buffer failed");
+        A.first_idx = at<uint32_t>(p->d_first, o_fi);
+        A.first_codes = at<uint8_t>(p->d_first, o_fc);
+    }
+
+    const int per_sm = cvg::search_blocks_per_sm(p->mode, p->out, p->path);
+    if (per_sm <= 0) {
+        cudaError_t le = cudaGetLastError();
+        return fail(CVG_ECUDA, std::string("search kernel cannot be resident on this device (") +
+                                   cudaGetErrorString(le) + "); sm_100a image required");
+    }
+    const uint64_t want = (n_tiles + cvg::kWarpsPerBlock - 1) / cvg::kWarpsPerBlock;
+    p->grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(per_sm) * ctx->sms, want));
+    if (p->grid < 1) p->grid = 1;
+    CVG_CUDA(cudaEventCreate(&p->ev0));
+    CVG_CUDA(cudaEventCreate(&p->ev1));
+
+    if (p->out == cvg::kOutPairs) {
+        // Initial capacity: every candidate when it fits in half the free memory.
+        size_t free_b = 0, total_b = 0;
+        cudaMemGetInfo(&free_b, &total_b);
+        const uint64_t fit = static_cast<uint64_t>(free_b / 2 / 10);
+        uint64_t cap = std::min<uint64_t>(p->candidates, std::max<uint64_t>(fit, 1u << 20));
+        if (int e2 = plan_reserve(p, cap)) return e2;
+    }
+    return CVG_OK;
+}
+
+void plan_release(cvg_plan* p) {
+    if (!p->ctx) return;
+    plan_free_outputs(p);
+    p->ctx->dev.release(p->d_const);
+    p->ctx->dev.release(p->d_work);
+    p->ctx->dev.release(p->d_first);
+    if (p->ev0) cudaEventDestroy(p->ev0);
+    if (p->ev1) cudaEventDestroy(p->ev1);
+}
+
+int plan_enqueue(cvg_plan* p, cudaStream_t st) {
+    p->last_stream = st;
+    p->ran = true;
+    if (p->empty) return CVG_OK;
+    CVG_CUDA(cudaMemsetAsync(p->d_work, 0, p->work_bytes, st));
+    if (p->out == cvg::kOutFirst) CVG_CUDA(cudaMemsetAsync(p->d_first, 0xff, static_cast<size_t>(p->n) * 4, st));
+    CVG_CUDA(cudaEventRecord(p->ev0, st));
+    CVG_CUDA(cvg::launch_search(p->args, p->mode, p->out, p->path, p->grid, st));
+    if (p->out == cvg::kOutFirst) CVG_CUDA(cvg::launch_first_codes(p->args, st));
+    CVG_CUDA(cudaEventRecord(p->ev1, st));
+    return CVG_OK;
+}
+
+struct HostStats {
+    cvg::Stats st{};
+    float ms = 0.f;
+};
+
+// Waits for the last run; copies counts and stats to host.
+int plan_collect(cvg_plan* p, std::vector<uint64_t>& counts, HostStats& hs) {
+    counts.assign(p->n, 0);
+    if (p->empty) return CVG_OK;
+    cudaStream_t st = p->last_stream;
+    CVG_CUDA(cudaMemcpyAsync(counts.data(), p->args.counts, sizeof(uint64_t) * p->n, cudaMemcpyDeviceToHost, st));
+    CVG_CUDA(cudaMemcpyAsync(&hs.st, p->args.stats, sizeof(cvg::Stats), cudaMemcpyDeviceToHost, st));
+    CVG_CUDA(cudaStreamSynchronize(st));
+    CVG_CUDA(cudaEventElapsedTime(&hs.ms, p->ev0, p->ev1));
+    return CVG_OK;
+}
+
+void result_zero(cvg_result* r) { std::memset(r, 0, sizeof(*r)); }
+
+int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
+    result_zero(r);
+    r->n_searches = p->n;
+    std::vector<uint64_t> counts;
+    HostStats hs;
+    if (int e = plan_collect(p, counts, hs)) return e;
+    uint64_t total = 0;
+    for (uint64_t c : counts) total += c;
+    if (p->out == cvg::kOutPairs && hs.st.overflow) {
+        if (!allow_rerun) {
+            r->n_pairs = total;
+            return fail(CVG_EOVERFLOW, "pair buffer too small; call cvg_plan_reserve and rerun");
+        }
+        if (int e = plan_reserve(p, total)) return e;
+        if (int e = plan_enqueue(p, p->last_stream)) return e;
+        return plan_fetch_impl(p, r, false);
+    }
+    cvg_ctx* ctx = p->ctx;
+    const size_t n = static_cast<size_t>(p->n);
+    r->counts = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (n ? n : 1)));
+    if (!r->counts) return fail(CVG_ENOMEM, "host allocation failed");
+    std::copy(counts.begin(), counts.end(), r->counts);
+    r->n_pairs = total;
+    r->n_candidates = p->candidates;
+    r->n_band_repairs = hs.st.band_repairs;
+    r->n_code_repairs = hs.st.code_repairs;
+    r->n_audit_violations = hs.st.audit_violations;
+    r->n_class_mismatch = hs.st.class_mismatch;
+    std::memcpy(&r->audit_max_ratio, &hs.st.audit_max_ratio_bits, sizeof(float));
+    r->kernel_ms = hs.ms;
+    if (p->out == cvg::kOutPairs) {
+        r->offsets = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (n + 1)));
+        if (!r->offsets) return fail(CVG_ENOMEM, "host allocation failed");
+        r->offsets[0] = 0;
+        for (size_t s = 0; s < n; ++s) r->offsets[s + 1] = r->offsets[s] + counts[s];
+        if (total) {
+            r->idx = static_cast<uint32_t*>(ctx->host.alloc(total * 4));
+            r->codes = static_cast<uint8_t*>(ctx->host.alloc(total * 6));
+            if (!r->idx || !r->codes) return fail(CVG_ENOMEM, "pinned host allocation failed");
+            cudaStream_t st = p->last_stream;
+            CVG_CUDA(cudaMemcpyAsync(r->idx, p->d_out_idx, total * 4, cudaMemcpyDeviceToHost, st));
+            CVG_CUDA(cudaMemcpyAsync(r->codes, p->d_out_codes, total * 6, cudaMemcpyDeviceToHost, st));
+            CVG_CUDA(cudaStreamSynchronize(st));
+        }
+    } else if (p->out == cvg::kOutFirst && n) {
+        r->first_idx = static_cast<uint32_t*>(ctx->host.alloc(n * 4));
+        r->first_codes = static_cast<uint8_t*>(ctx->host.alloc(n * 6));
+        if (!r->first_idx || !r->first_codes) return fail(CVG_ENOMEM, "pinned host allocation failed");
+        cudaStream_t st = p->last_stream;
+        CVG_CUDA(cudaMemcpyAsync(r->first_idx, p->args.first_idx, n * 4, cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaMemcpyAsync(r->first_codes, p->args.first_codes, n * 6, cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaStreamSynchronize(st));
+    }
+    return CVG_OK;
+}
+
+// cvg_result keeps a pointer to its context in a side table so that
+// cvg_result_free can return pinned blocks to the right pool.
+std::mutex g_owner_mu;
+std::map<const void*, cvg_ctx*> g_owner;
+
+void remember_owner(cvg_result* r, cvg_ctx* ctx) {
+    std::lock_guard<std::mutex> lk(g_owner_mu);
+    for (const void* ptr : {static_cast<const void*>(r->idx), static_cast<const void*>(r->codes),
+                            static_cast<const void*>(r->first_idx), static_cast<const void*>(r->first_codes)}) {
+        if (ptr) g_owner[ptr] = ctx;
+    }
+}
+
+}  // namespace
+
+// ============================================================================
+// C-ABI
+// ============================================================================
+
+extern "C" {
+
+const char* cvg_last_error(void) { return g_error.c_str(); }
+const char* cvg_version(void) { return "colorvibe-b200 0.1.0 (sm_100a)"; }
+
+int cvg_create(int device, cvg_ctx** out) {
+    if (!out) return fail(CVG_EINVAL, "null output pointer");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(CVG_ECUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+    }
+    if (device < 0 || device >= count) return fail(CVG_EINVAL, "device index out of range");
+    auto* ctx = new cvg_ctx();
+    ctx->device = device;
+    ctx->dev.device = true;
+    ctx->host.device = false;
+    e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete ctx;
+        return cuda_fail(e, "context creation");
+    }
+    (void)tables();
+    *out = ctx;
+    return CVG_OK;
+}
+
+void cvg_destroy(cvg_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    {
+        std::lock_guard<std::mutex> lk(g_owner_mu);
+        for (auto it = g_owner.begin(); it != g_owner.end();) {
+            it = it->second == ctx ? g_owner.erase(it) : std::next(it);
+        }
+    }
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int cvg_plan_create(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_plan** out) {
+    if (!ctx || !out) return fail(CVG_EINVAL, "null context or output pointer");
+    *out = nullptr;
+    if (int e = validate_desc(desc)) return e;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    if (int e = ensure_device(ctx)) return e;
+    auto* p = new cvg_plan();
+    if (int e = plan_build(ctx, desc, p)) {
+        plan_release(p);
+        delete p;
+        return e;
+    }
+    *out = p;
+    return CVG_OK;
+}
+
+void cvg_plan_destroy(cvg_plan* p) {
+    if (!p) return;
+    if (p->ctx) {
+        std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+        cudaSetDevice(p->ctx->device);
+        if (p->ran) cudaStreamSynchronize(p->last_stream);
+        plan_release(p);
+    }
+    delete p;
+}
+
+int cvg_plan_reserve(cvg_plan* p, uint64_t cap) {
+    if (!p) return fail(CVG_EINVAL, "null plan");
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    if (int e = ensure_device(p->ctx)) return e;
+    return plan_reserve(p, cap);
+}
+
+int cvg_plan_run(cvg_plan* p, void* stream) {
+    if (!p) return fail(CVG_EINVAL, "null plan");
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    if (int e = ensure_device(p->ctx)) return e;
+    return plan_enqueue(p, static_cast<cudaStream_t>(stream));
+}
+
+int cvg_plan_sync(cvg_plan* p, uint64_t* n_pairs) {
+    if (!p) return fail(CVG_EINVAL, "null plan");
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    if (int e = ensure_device(p->ctx)) return e;
+    std::vector<uint64_t> counts;
+    HostStats hs;
+    if (int e = plan_collect(p, counts, hs)) return e;
+    uint64_t total = 0;
+    for (uint64_t c : counts) total += c;
+    if (n_pairs) *n_pairs = total;
+    if (p->out == cvg::kOutPairs && hs.st.overflow) return fail(CVG_EOVERFLOW, "pair buffer too small");
+    return CVG_OK;
+}
+
+int cvg_plan_fetch(cvg_plan* p, cvg_result* out) {
+    if (!p || !out) return fail(CVG_EINVAL, "null plan or result");
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    if (int e = ensure_device(p->ctx)) return e;
+    const int e = plan_fetch_impl(p, out, false);
+    remember_owner(out, p->ctx);
+    if (e) cvg_result_free(out);
+    return e;
+}
+
+int cvg_plan_device_outputs(cvg_plan* p, uint64_t** counts, uint32_t** idx, uint8_t** codes, uint64_t* capacity) {
+    if (!p) return fail(CVG_EINVAL, "null plan");
+    if (counts) *counts = reinterpret_cast<uint64_t*>(p->args.counts);
+    if (idx) *idx = static_cast<uint32_t*>(p->d_out_idx);
+    if (codes) *codes = static_cast<uint8_t*>(p->d_out_codes);
+    if (capacity) *capacity = p->capacity;
+    return CVG_OK;
+}
+
+int cvg_plan_launches(const cvg_plan* p) {
+    if (!p || p->empty) return 0;
+    return p->out == cvg::kOutFirst ? 2 : 1;
+}
+
+uint64_t cvg_plan_candidates(const cvg_plan* p) { return p ? p->candidates : 0; }
+
+int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out) {
+    if (!ctx || !out) return fail(CVG_EINVAL, "null context or result");
+    result_zero(out);
+    if (int e = validate_desc(desc)) return e;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    if (int e = ensure_device(ctx)) return e;
+    cvg_plan plan;
+    int e = plan_build(ctx, desc, &plan);
+    if (!e) e = plan_enqueue(&plan, ctx->stream);
+    if (!e) e = plan_fetch_impl(&plan, out, true);
+    if (plan.ran) cudaStreamSynchronize(ctx->stream);
+    plan_release(&plan);
+    plan.ctx = nullptr;
+    remember_owner(out, ctx);
+    if (e) cvg_result_free(out);
+    return e;
+}
+
+void cvg_result_free(cvg_result* r) {
+    if (!r) return;
+    std::free(r->counts);
+    std::free(r->offsets);
+    for (void* ptr : {static_cast<void*>(r->idx), static_cast<void*>(r->codes), static_cast<void*>(r->first_idx),
+                      static_cast<void*>(r->first_codes)}) {
+        if (!ptr) continue;
+        cvg_ctx* owner = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(g_owner_mu);
+            auto it = g_owner.find(ptr);
+            if (it != g_owner.end()) {
+                owner = it->second;
+                g_owner.erase(it);
+            }
+        }
+        if (owner) {
+            std::lock_guard<std::recursive_mutex> lk(owner->mu);
+            owner->host.release(ptr);
+        }
+    }
+    std::memset(r, 0, sizeof(*r));
+}
+
+int cvg_srgb_to_lab(const int32_t rgb[3], const double* wp, double lab[3]) {
+    if (!rgb || !lab) return fail(CVG_EINVAL, "null argument");
+    if (int e = validate_color(rgb)) return e;
+    to_lab(rgb, white_or_d65(wp), lab);
+    return CVG_OK;
+}
+
+static int validate_lab(const double lab[3]) {
+    if (!(std::isfinite(lab[0]) && std::isfinite(lab[1]) && std::isfinite(lab[2])) || lab[0] < 0.0 || lab[0] > 100.0) {
+        return fail(CVG_EINVAL, "Lab color with L* outside [0, 100]");
+    }
+    return CVG_OK;
+}
+
+int cvg_lab_to_srgb_clipped(const double lab[3], const double* wp, int32_t rgb[3]) {
+    if (!rgb || !lab) return fail(CVG_EINVAL, "null argument");
+    if (int e = validate_lab(lab)) return e;
+    double lin[3];
+    to_linear(lab, white_or_d65(wp), lin);
+    for (int c = 0; c < 3; ++c) rgb[c] = quantize(lin[c]);
+    return CVG_OK;
+}
+
+int cvg_lab_to_srgb(const double lab[3], const double* wp, int32_t rgb[3]) {
+    if (!rgb || !lab) return -fail(CVG_EINVAL, "null argument");
+    if (validate_lab(lab)) return -CVG_EINVAL;
+    double lin[3];
+    to_linear(lab, white_or_d65(wp), lin);
+    for (int c = 0; c < 3; ++c) {
+        if (!(lin[c] >= -kGamutEps && lin[c] <= 1.0 + kGamutEps)) return 0;
+    }
+    for (int c = 0; c < 3; ++c) rgb[c] = quantize(lin[c]);
+    return 1;
+}
+
+void cvg_d65_white(double out[3]) {
+    const double* w = white_or_d65(nullptr);
+    out[0] = w[0];
+    out[1] = w[1];
+    out[2] = w[2];
+}
+
+void cvg_quant_thresholds(double out[256]) { std::memcpy(out, tables().thr, sizeof(double) * 256); }
+
+double cvg_measure_ffma_peak(int device, float* ms_out) { return cvg::measure_ffma_peak(device, ms_out); }
+
+}  // extern "C"

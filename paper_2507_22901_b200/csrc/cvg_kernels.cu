@@ -1,0 +1,623 @@
+// cvg_kernels.cu -- fused color-pair search for B200 (sm_100a).
+//
+// One persistent kernel per batch of searches.  Each warp claims 2048-
+// candidate tiles (a contiguous range of one search's canonical index
+// i = k*na + m) from a global ticket and, per tile:
+//
+//   phase 1  synthesizes every candidate in registers from (target, r_k,
+//            theta_m) -- no per-candidate HBM traffic besides the L1/L2-
+//            resident trig table -- runs the Lab -> linear RGB conversion and
+//            the band test of the reference batch path (search.cpp:230-278,
+//            291-329) in FP32 with a proven per-channel error bound, and sends
+//            the rare candidates whose decision lies inside that bound through
+//            the FP64 op-for-op restatement (bit-identical to the reference).
+//            Passing candidates are compacted into a per-warp shared-memory
+//            list with ballot/popc (the reference's pass-2 extraction,
+//            search.cpp:379-397).
+//   look-back  the warp publishes its tile count and reads its predecessors'
+//            (decoupled look-back), giving the tile's output offset in the
+//            global canonical order -- one pass, no count kernel, and output
+//            order independent of scheduling (search.cpp:448-455, test
+//            tests/test_search.cpp:206-235).
+//   phase 2  the warp walks its compacted list 32 pairs at a time (all lanes
+//            busy), recomputes the six linear values, quantizes them through
+//            the float threshold table with the same bound (FP64 repair when
+//            unsure) and writes idx + 6 code bytes with coalesced stores.
+//
+// Result: per-search counts and pair lists bit-identical to the reference.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "cvg_internal.h"
+#include "cvg_layout.h"
+
+namespace cvg {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// Reference constants (convert_kernel.hpp:50-60), evaluated in double.
+constexpr double kLabEpsilon = 216.0 / 24389.0;
+constexpr double kInvKappa = 27.0 / 24389.0;
+constexpr double kInv500 = 1.0 / 500.0;
+constexpr double kInv200 = 1.0 / 200.0;
+
+// FP32 fast-path constants: f^-1(u) = u^3 above u0 = 6/29, else the tangent
+// line (116u - 16) * 27/24389 = K1*u - K2 (the two branches are C1-tangent at
+// u0, so a branch flip next to u0 costs O(du^2), covered by the bound).
+constexpr float kU0f = 6.0f / 29.0f;
+constexpr float kK1f = 3132.0f / 24389.0f;
+constexpr float kK2f = 432.0f / 24389.0f;
+
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPrefix = 2ull << 62;
+constexpr unsigned long long kValueMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t div_na(uint32_t i, const LaunchArgs& A) {
+    return A.na == 1 ? i : static_cast<uint32_t>(__umul64hi(static_cast<uint64_t>(i), A.na_magic));
+}
+
+// ------------------------------------------------------------------------
+// Per-search constants held in registers for a tile.
+struct Consts {
+    float fx0, fz0, rcube;
+    float mx[3], mz[3], cy[3];
+    float lo_p[3], lo_m[3], hi_p[3], hi_m[3];
+    float ec[3];
+    uint32_t flags;
+};
+
+__device__ __forceinline__ void load_consts(const SearchConst* S, Consts& c) {
+    c.fx0 = __ldg(&S->fx0);
+    c.fz0 = __ldg(&S->fz0);
+    c.rcube = __ldg(&S->rcube);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        c.mx[q] = __ldg(&S->mx[q]);
+        c.mz[q] = __ldg(&S->mz[q]);
+        c.cy[q] = __ldg(&S->cy[q]);
+        c.lo_p[q] = __ldg(&S->lo_p[q]);
+        c.lo_m[q] = __ldg(&S->lo_m[q]);
+        c.hi_p[q] = __ldg(&S->hi_p[q]);
+        c.hi_m[q] = __ldg(&S->hi_m[q]);
+        c.ec[q] = __ldg(&S->eps_code[q]);
+    }
+    c.flags = __ldg(&S->flags);
+}
+
+// ------------------------------------------------------------------------
+// FP64 exact path: op-for-op restatement of the reference batch row
+// (search.cpp:243-262 with convert_kernel.hpp:70-73), no contraction.
+
+__device__ __forceinline__ double finv_exact(double u) {
+    const double u3 = __dmul_rn(__dmul_rn(u, u), u);
+    return u3 > kLabEpsilon ? u3 : __dmul_rn(__dsub_rn(__dmul_rn(116.0, u), 16.0), kInvKappa);
+}
+
+__device__ __noinline__ void exact_linear(const SearchConst* S, const LaunchArgs& A, uint32_t k,
+                                          uint32_t m, double* lp, double* lm) {
+    const double r = __ldg(&A.radii_d[k]);
+    const double s = __ldg(&A.trig_d[2 * m]);
+    const double c = __ldg(&A.trig_d[2 * m + 1]);
+    const double fy = __ldg(&S->fy), ta = __ldg(&S->ta), tb = __ldg(&S->tb);
+    const double wx = __ldg(&S->wx), wz = __ldg(&S->wz);
+    const double da = __dmul_rn(r, s);
+    const double db = __dmul_rn(r, c);
+    const double fxp = __dadd_rn(fy, __dmul_rn(__dadd_rn(ta, da), kInv500));
+    const double fzp = __dsub_rn(fy, __dmul_rn(__dadd_rn(tb, db), kInv200));
+    const double xp = __dmul_rn(wx, finv_exact(fxp));
+    const double zp = __dmul_rn(wz, finv_exact(fzp));
+    const double fxm = __dadd_rn(fy, __dmul_rn(__dsub_rn(ta, da), kInv500));
+    const double fzm = __dsub_rn(fy, __dmul_rn(__dsub_rn(tb, db), kInv200));
+    const double xm = __dmul_rn(wx, finv_exact(fxm));
+    const double zm = __dmul_rn(wz, finv_exact(fzm));
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const double cy = __ldg(&S->cy64[q]);
+        lp[q] = __dadd_rn(__dadd_rn(__dmul_rn(A.minv[3 * q], xp), cy), __dmul_rn(A.minv[3 * q + 2], zp));
+        lm[q] = __dadd_rn(__dadd_rn(__dmul_rn(A.minv[3 * q], xm), cy), __dmul_rn(A.minv[3 * q + 2], zm));
+    }
+}
+
+// QuantTable::code (convert_kernel.hpp:148-154): largest c with x >= thr[c].
+__device__ __forceinline__ int code_exact(double x, const double* thr) {
+    if (x <= 0.0) return 0;
+    if (x >= 1.0) return 255;
+    int c = 0;
+#pragma unroll
+    for (int step = 128; step; step >>= 1) {
+        if (x >= thr[c + step]) c += step;
+    }
+    return c;
+}
+
+// Band predicate of pass1_row (search.cpp:267-276) on exact values.
+__device__ __forceinline__ bool exact_band(const SearchConst* S, const double* lp, const double* lm,
+                                           uint32_t flags) {
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const double lo = __ldg(&S->lo[q]), hi = __ldg(&S->hi[q]);
+        const bool in = (lp[q] >= lo) & (lp[q] < hi) & (lm[q] >= lo) & (lm[q] < hi);
+        const bool loud = (flags >> q) & 1;
+        ok &= in != loud;
+    }
+    return ok;
+}
+
+// classify_pair (search.cpp:146-157) on integer codes, with the integer form
+// of the thresholds (d > v_th <=> d >= k1, d <= low <=> d <= q0).
+__device__ __forceinline__ bool classify_codes(const SearchConst* S, const int* cp, const int* cm,
+                                               uint32_t flags) {
+    const bool frame_diff = (flags >> 8) & 1;
+    const int k1 = __ldg(&S->k1), q0 = __ldg(&S->q0);
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const int t = __ldg(&S->t[q]);
+        int d;
+        if (frame_diff) {
+            d = abs(cp[q] - cm[q]);
+        } else {
+            d = max(abs(cp[q] - t), abs(cm[q] - t));
+        }
+        const bool loud = (flags >> q) & 1;
+        ok &= loud ? (d >= k1) : (d <= q0);
+    }
+    return ok;
+}
+
+// ------------------------------------------------------------------------
+// FP32 fast path.
+
+template <bool kCubeOnly>
+__device__ __forceinline__ float finv_fast(float f) {
+    const float c3 = __fmul_rn(__fmul_rn(f, f), f);
+    if (kCubeOnly) return c3;
+    const float l = fmaf(f, kK1f, -kK2f);
+    return f > kU0f ? c3 : l;
+}
+
+template <bool kCubeOnly>
+__device__ __forceinline__ void fast_linear(const Consts& C, float r, float2 sc, float* vp, float* vm) {
+    const float fxp = fmaf(r, sc.x, C.fx0);
+    const float fxm = fmaf(-r, sc.x, C.fx0);
+    const float fzp = fmaf(-r, sc.y, C.fz0);
+    const float fzm = fmaf(r, sc.y, C.fz0);
+    const float gxp = finv_fast<kCubeOnly>(fxp);
+    const float gxm = finv_fast<kCubeOnly>(fxm);
+    const float gzp = finv_fast<kCubeOnly>(fzp);
+    const float gzm = finv_fast<kCubeOnly>(fzm);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        vp[q] = fmaf(C.mx[q], gxp, fmaf(C.mz[q], gzp, C.cy[q]));
+        vm[q] = fmaf(C.mx[q], gxm, fmaf(C.mz[q], gzm, C.cy[q]));
+    }
+}
+
+// Band test with margins: returns certain pass; sets unsure when no channel
+// certainly fails and some channel is undecided.
+__device__ __forceinline__ bool fast_band(const Consts& C, const float* vp, const float* vm, bool& unsure) {
+    bool pass = true, fail = false;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const float vmin = fminf(vp[q], vm[q]);
+        const float vmax = fmaxf(vp[q], vm[q]);
+        const bool cin = (vmin >= C.lo_p[q]) & (vmax < C.hi_m[q]);
+        const bool maybe = (vmin >= C.lo_m[q]) & (vmax < C.hi_p[q]);
+        const bool loud = (C.flags >> q) & 1;
+        pass &= loud ? !maybe : cin;
+        fail |= loud ? cin : !maybe;
+    }
+    unsure = !pass & !fail;
+    return pass;
+}
+
+// Linear value -> code through the float table, verified against the bound:
+// ok iff thr[c] + E < x < thr[c+1] - E, which proves code(x64) == c.
+__device__ __forceinline__ int code_fast(float x, float E, const float* tf, const uint8_t* guess, bool& ok) {
+    int i = __float2int_rz(x * static_cast<float>(kGuessBuckets));
+    i = min(max(i, 0), kGuessBuckets);
+    const int g = guess[i];
+    const int c = g + (x >= tf[g + 1]);
+    ok = (__fsub_rn(x, tf[c]) > E) & (__fsub_rn(tf[c + 1], x) > E);
+    return c;
+}
+
+struct Smem {
+    uint16_t list[kWarpsPerBlock][kTile];
+    double thr_d[256];
+    float thr_f[258];  // [0] = -inf, [c] = float(thr[c]), [256] = +inf
+    uint8_t guess[kGuessBuckets + 16];
+};
+
+// Codes of the six endpoint channels for one candidate, exact.
+template <int kPath>
+__device__ __forceinline__ void candidate_codes(const Smem& sm, const SearchConst* S, const Consts& C,
+                                                const LaunchArgs& A, uint32_t k, uint32_t m, bool active,
+                                                int* cp, int* cm, unsigned long long& repairs,
+                                                unsigned long long& violations, float& max_ratio) {
+    bool need_exact = true;
+    if (kPath != kPathExact) {
+        float vp[3], vm[3];
+        const float r = __ldg(&A.radii_f[k]);
+        const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + m);
+        fast_linear<false>(C, r, sc, vp, vm);
+        bool all_ok = true;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            bool ok1, ok2;
+            cp[q] = code_fast(vp[q], C.ec[q], sm.thr_f, sm.guess, ok1);
+            cm[q] = code_fast(vm[q], C.ec[q], sm.thr_f, sm.guess, ok2);
+            all_ok &= ok1 & ok2;
+        }
+        if (kPath == kPathAudit) {
+            double lp[3], lm[3];
+            exact_linear(S, A, k, m, lp, lm);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const int ep = code_exact(lp[q], sm.thr_d), em = code_exact(lm[q], sm.thr_d);
+                if (all_ok && active && (ep != cp[q] || em != cm[q])) ++violations;
+                const float eps = __ldg(&S->eps[q]);
+                max_ratio = fmaxf(max_ratio, static_cast<float>(fabs(static_cast<double>(vp[q]) - lp[q]) / eps));
+                max_ratio = fmaxf(max_ratio, static_cast<float>(fabs(static_cast<double>(vm[q]) - lm[q]) / eps));
+                cp[q] = ep;
+                cm[q] = em;
+            }
+            need_exact = false;
+            if (!all_ok && active) ++repairs;
+        } else {
+            need_exact = !all_ok;
+            if (__any_sync(kFull, need_exact) == 0) return;
+            if (need_exact && active) ++repairs;
+        }
+    }
+    if (need_exact) {
+        double lp[3], lm[3];
+        exact_linear(S, A, k, m, lp, lm);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            cp[q] = code_exact(lp[q], sm.thr_d);
+            cm[q] = code_exact(lm[q], sm.thr_d);
+        }
+    }
+}
+
+// Phase-1 decision for one candidate.
+template <int kMode, int kPath, bool kCubeOnly>
+__device__ __forceinline__ bool candidate_pass(const Smem& sm, const SearchConst* S, const Consts& C,
+                                               const LaunchArgs& A, uint32_t k, uint32_t m, float r,
+                                               bool active, unsigned long long& repairs,
+                                               unsigned long long& violations, float& max_ratio) {
+    if (kMode == kModeCodes) {
+        int cp[3], cm[3];
+        candidate_codes<kPath>(sm, S, C, A, k, m, active, cp, cm, repairs, violations, max_ratio);
+        return active && classify_codes(S, cp, cm, C.flags);
+    }
+    if (kPath == kPathExact) {
+        double lp[3], lm[3];
+        exact_linear(S, A, k, m, lp, lm);
+        return active && exact_band(S, lp, lm, C.flags);
+    }
+    float vp[3], vm[3];
+    const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + m);
+    fast_linear<kCubeOnly>(C, r, sc, vp, vm);
+    bool unsure;
+    bool pass = fast_band(C, vp, vm, unsure);
+    if (kPath == kPathAudit) {
+        double lp[3], lm[3];
+        exact_linear(S, A, k, m, lp, lm);
+        const bool ex = exact_band(S, lp, lm, C.flags);
+        if (active && !unsure && ex != pass) ++violations;
+        if (active && unsure) ++repairs;
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const float eps = __ldg(&S->eps[q]);
+            max_ratio = fmaxf(max_ratio, static_cast<float>(fabs(static_cast<double>(vp[q]) - lp[q]) / eps));
+            max_ratio = fmaxf(max_ratio, static_cast<float>(fabs(static_cast<double>(vm[q]) - lm[q]) / eps));
+        }
+        return active && ex;
+    }
+    if (__any_sync(kFull, unsure)) {
+        if (unsure) {
+            double lp[3], lm[3];
+            exact_linear(S, A, k, m, lp, lm);
+            pass = exact_band(S, lp, lm, C.flags);
+            if (active) ++repairs;
+        }
+    }
+    return active && pass;
+}
+
+// Decoupled look-back over the warp tiles (global canonical order).
+__device__ __forceinline__ unsigned long long lookback(unsigned long long* status, uint32_t t, uint32_t cnt,
+                                                       int lane) {
+    if (lane == 0) st_relaxed(&status[t], (t == 0 ? kFlagPrefix : kFlagAgg) | cnt);
+    if (t == 0) return 0;
+    unsigned long long excl = 0;
+    long long j = static_cast<long long>(t) - 1;
+    while (true) {
+        const long long idx = j - lane;
+        const unsigned long long v = idx >= 0 ? ld_relaxed(&status[idx]) : kFlagPrefix;
+        const unsigned flag = static_cast<unsigned>(v >> 62);
+        const unsigned pmask = __ballot_sync(kFull, flag == 2);
+        const unsigned zmask = __ballot_sync(kFull, flag == 0);
+        const unsigned stop = pmask ? static_cast<unsigned>(__ffs(pmask) - 1) : 31u;
+        const unsigned need = stop == 31u ? kFull : ((2u << stop) - 1u);
+        if (zmask & need) {
+            __nanosleep(64);
+            continue;
+        }
+        unsigned long long val = static_cast<unsigned>(lane) <= stop ? (v & kValueMask) : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(kFull, val, o);
+        excl += val;
+        if (pmask) break;
+        j -= 32;
+    }
+    if (lane == 0) st_relaxed(&status[t], kFlagPrefix | (excl + cnt));
+    return excl;
+}
+
+template <int kMode, int kOut, int kPath>
+__global__ void __launch_bounds__(kBlock, 3) search_kernel(const LaunchArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    for (int i = threadIdx.x; i < 256; i += kBlock) sm.thr_d[i] = A.thr_d[i];
+    for (int i = threadIdx.x; i < 258; i += kBlock) sm.thr_f[i] = A.thr_f[i];
+    for (int i = threadIdx.x; i <= kGuessBuckets; i += kBlock) sm.guess[i] = A.guess[i];
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    uint16_t* list = sm.list[warp];
+    const unsigned lane_lt = (1u << lane) - 1u;
+
+    unsigned long long repairs = 0, code_repairs = 0, violations = 0, mismatch = 0, overflow = 0;
+    float max_ratio = 0.f;
+
+    while (true) {
+        uint32_t t = 0;
+        if (lane == 0) t = atomicAdd(A.ticket, 1u);
+        t = __shfl_sync(kFull, t, 0);
+        if (t >= A.n_tiles) break;
+        const uint32_t s = t / A.tiles_per_search;
+        const uint32_t lt = t - s * A.tiles_per_search;
+        const SearchConst* S = A.sc + s;
+        Consts C;
+        load_consts(S, C);
+        const uint32_t i0 = lt * static_cast<uint32_t>(kTile);
+        const uint32_t i1 = min(i0 + static_cast<uint32_t>(kTile), A.cand_per_search);
+
+        // ---------------- phase 1: decide every candidate of the tile -------
+        uint32_t cnt = 0;
+        if (A.aligned) {
+            uint32_t k = div_na(i0, A);
+            uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
+            uint32_t i = i0;
+            while (i < i1) {
+                const uint32_t seg_end = min(i1, i + (static_cast<uint32_t>(A.na) - m0));
+                const float r = __ldg(&A.radii_f[k]);
+                const bool cube_only = r < C.rcube;
+                for (uint32_t base = i; base < seg_end; base += 32) {
+                    const uint32_t m = m0 + (base - i) + lane;
+                    bool pass;
+                    if (cube_only) {
+                        pass = candidate_pass<kMode, kPath, true>(sm, S, C, A, k, m, r, true, repairs,
+                                                                  violations, max_ratio);
+                    } else {
+                        pass = candidate_pass<kMode, kPath, false>(sm, S, C, A, k, m, r, true, repairs,
+                                                                   violations, max_ratio);
+                    }
+                    const unsigned b = __ballot_sync(kFull, pass);
+                    if (pass) list[cnt + __popc(b & lane_lt)] = static_cast<uint16_t>(base - i0 + lane);
+                    cnt += __popc(b);
+                }
+                i = seg_end;
+                m0 = 0;
+                ++k;
+            }
+        } else {
+            for (uint32_t base = i0; base < i1; base += 32) {
+                const bool active = base + lane < i1;
+                const uint32_t i = active ? base + lane : i1 - 1;
+                const uint32_t k = div_na(i, A);
+                const uint32_t m = i - k * static_cast<uint32_t>(A.na);
+                const float r = __ldg(&A.radii_f[k]);
+                const bool pass = candidate_pass<kMode, kPath, false>(sm, S, C, A, k, m, r, active, repairs,
+                                                                      violations, max_ratio);
+                const unsigned b = __ballot_sync(kFull, pass);
+                if (pass) list[cnt + __popc(b & lane_lt)] = static_cast<uint16_t>(i - i0);
+                cnt += __popc(b);
+            }
+        }
+        __syncwarp();
+
+        // ---------------- publish -------------------------------------------
+        if (kOut == kOutCounts || kOut == kOutFirst) {
+            if (lane == 0 && cnt) {
+                atomicAdd(&A.counts[s], static_cast<unsigned long long>(cnt));
+                if (kOut == kOutFirst) atomicMin(&A.first_idx[s], i0 + list[0]);
+            }
+            continue;
+        }
+        const unsigned long long base_out = lookback(A.status, t, cnt, lane);
+        if (cnt == 0) continue;
+        if (lane == 0) atomicAdd(&A.counts[s], static_cast<unsigned long long>(cnt));
+        if (base_out + cnt > A.capacity) {
+            if (lane == 0) ++overflow;
+            continue;
+        }
+
+        // ---------------- phase 2: codes + coalesced writes ----------------
+        for (uint32_t p = 0; p < cnt; p += 32) {
+            const uint32_t q = p + lane;
+            const bool active = q < cnt;
+            const uint32_t i = i0 + list[active ? q : 0];
+            const uint32_t k = div_na(i, A);
+            const uint32_t m = i - k * static_cast<uint32_t>(A.na);
+            int cp[3], cm[3];
+            candidate_codes<kPath>(sm, S, C, A, k, m, active, cp, cm, code_repairs, violations, max_ratio);
+            if (active) {
+                if (kMode == kModeBand && !classify_codes(S, cp, cm, C.flags)) ++mismatch;
+                const unsigned long long o = base_out + q;
+                A.out_idx[o] = i;
+                uint16_t* c16 = reinterpret_cast<uint16_t*>(A.out_codes + 6 * o);
+                c16[0] = static_cast<uint16_t>(cp[0] | (cp[1] << 8));
+                c16[1] = static_cast<uint16_t>(cp[2] | (cm[0] << 8));
+                c16[2] = static_cast<uint16_t>(cm[1] | (cm[2] << 8));
+            }
+        }
+        __syncwarp();
+    }
+
+    // ---------------- statistics ---------------------------------------------
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        repairs += __shfl_xor_sync(kFull, repairs, o);
+        code_repairs += __shfl_xor_sync(kFull, code_repairs, o);
+        violations += __shfl_xor_sync(kFull, violations, o);
+        mismatch += __shfl_xor_sync(kFull, mismatch, o);
+        overflow += __shfl_xor_sync(kFull, overflow, o);
+        max_ratio = fmaxf(max_ratio, __shfl_xor_sync(kFull, max_ratio, o));
+    }
+    if (lane == 0) {
+        if (repairs) atomicAdd(&A.stats->band_repairs, repairs);
+        if (code_repairs) atomicAdd(&A.stats->code_repairs, code_repairs);
+        if (violations) atomicAdd(&A.stats->audit_violations, violations);
+        if (mismatch) atomicAdd(&A.stats->class_mismatch, mismatch);
+        if (overflow) atomicAdd(&A.stats->overflow, overflow);
+        if (max_ratio > 0.f) atomicMax(&A.stats->audit_max_ratio_bits, __float_as_uint(max_ratio));
+    }
+}
+
+// FIRST mode epilogue: exact codes of each search's first canonical pair.
+__global__ void first_codes_kernel(const LaunchArgs A) {
+    __shared__ double thr[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) thr[i] = A.thr_d[i];
+    __syncthreads();
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= A.n_searches) return;
+    const uint32_t i = A.first_idx[s];
+    uint8_t* out = A.first_codes + 6 * static_cast<size_t>(s);
+    if (i == 0xffffffffu) {
+        for (int q = 0; q < 6; ++q) out[q] = 0;
+        return;
+    }
+    const uint32_t k = div_na(i, A);
+    const uint32_t m = i - k * static_cast<uint32_t>(A.na);
+    double lp[3], lm[3];
+    exact_linear(A.sc + s, A, k, m, lp, lm);
+    for (int q = 0; q < 3; ++q) {
+        out[q] = static_cast<uint8_t>(code_exact(lp[q], thr));
+        out[3 + q] = static_cast<uint8_t>(code_exact(lm[q], thr));
+    }
+}
+
+// FP32 issue-rate microbenchmark: 8 independent FFMA chains per thread.
+__global__ void ffma_peak_kernel(float* out, int iters, float a, float b) {
+    float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
+    float x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+            x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+        }
+    }
+    const float r = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+    if (r == 1234.5f) out[0] = r;
+}
+
+template <int kMode, int kOut, int kPath>
+cudaError_t launch_t(const LaunchArgs& a, int grid, cudaStream_t st) {
+    // The dynamic shared-memory opt-in is set by occupancy_t (plan creation).
+    search_kernel<kMode, kOut, kPath><<<grid, kBlock, sizeof(Smem), st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int kMode, int kOut, int kPath>
+int occupancy_t() {
+    auto fn = search_kernel<kMode, kOut, kPath>;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Smem)));
+    int blocks = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kBlock, sizeof(Smem)) != cudaSuccess) return 0;
+    return blocks;
+}
+
+using LaunchFn = cudaError_t (*)(const LaunchArgs&, int, cudaStream_t);
+using OccFn = int (*)();
+
+#define CVG_ROW(M, P) \
+    {launch_t<M, kOutPairs, P>, launch_t<M, kOutCounts, P>, launch_t<M, kOutFirst, P>}
+#define CVG_OCC(M, P) {occupancy_t<M, kOutPairs, P>, occupancy_t<M, kOutCounts, P>, occupancy_t<M, kOutFirst, P>}
+
+const LaunchFn kLaunch[2][3][3] = {
+    {CVG_ROW(kModeBand, kPathFast), CVG_ROW(kModeBand, kPathExact), CVG_ROW(kModeBand, kPathAudit)},
+    {CVG_ROW(kModeCodes, kPathFast), CVG_ROW(kModeCodes, kPathExact), CVG_ROW(kModeCodes, kPathAudit)},
+};
+const OccFn kOcc[2][3][3] = {
+    {CVG_OCC(kModeBand, kPathFast), CVG_OCC(kModeBand, kPathExact), CVG_OCC(kModeBand, kPathAudit)},
+    {CVG_OCC(kModeCodes, kPathFast), CVG_OCC(kModeCodes, kPathExact), CVG_OCC(kModeCodes, kPathAudit)},
+};
+
+}  // namespace
+
+cudaError_t launch_search(const LaunchArgs& a, int mode, int out, int path, int grid, cudaStream_t st) {
+    return kLaunch[mode][path][out](a, grid, st);
+}
+
+int search_blocks_per_sm(int mode, int out, int path) { return kOcc[mode][path][out](); }
+
+cudaError_t launch_first_codes(const LaunchArgs& a, cudaStream_t st) {
+    const int threads = 128;
+    const int blocks = (a.n_searches + threads - 1) / threads;
+    if (blocks == 0) return cudaSuccess;
+    first_codes_kernel<<<blocks, threads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+size_t search_smem_bytes() { return sizeof(Smem); }
+
+double measure_ffma_peak(int device, float* ms_out) {
+    if (cudaSetDevice(device) != cudaSuccess) return 0.0;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    float* out = nullptr;
+    if (cudaMalloc(&out, sizeof(float)) != cudaSuccess) return 0.0;
+    const int threads = 256, blocks = sms * 8, iters = 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    ffma_peak_kernel<<<blocks, threads>>>(out, 64, 0.999f, 0.001f);  // warm-up
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        cudaEventRecord(e0);
+        ffma_peak_kernel<<<blocks, threads>>>(out, iters, 0.999f, 0.001f);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    if (cudaGetLastError() != cudaSuccess) return 0.0;
+    if (ms_out) *ms_out = best;
+    const double ffma = static_cast<double>(blocks) * threads * iters * 16.0 * 8.0;
+    return ffma / (best * 1e-3);
+}
+
+}  // namespace cvg

@@ -1,0 +1,90 @@
+// cvg_layout.h -- HBM data layout shared by the host library (g++) and the
+// CUDA kernels (nvcc).  Plain structs only.
+#pragma once
+
+#include <cstdint>
+
+namespace cvg {
+
+// Candidates per warp tile: the unit of the ordered (decoupled look-back)
+// compaction.  A tile is a contiguous range of one search's canonical
+// (radius-major, angle-minor) candidate index.
+constexpr int kTile = 2048;
+constexpr int kWarpsPerBlock = 8;
+constexpr int kBlock = 32 * kWarpsPerBlock;
+constexpr int kGuessBuckets = 4096;  // code-guess buckets over linear [0, 1]
+
+// Per-search constants, one 256-byte record per (target, pattern, thresholds).
+// The FP32 half feeds the fast path; the FP64 half is the bit-exact restatement
+// of the reference hoisting (search.cpp:341-370) used by the repair path.
+struct alignas(16) SearchConst {
+    // --- FP32 fast path -------------------------------------------------
+    float fx0;         // Fy + a/500   (fx of both endpoints = fx0 +- r*sin/500)
+    float fz0;         // Fy - b/200   (fz = fz0 -+ r*cos/200)
+    float rcube;       // rows with r < rcube never leave the cube branch of f^-1
+    float mx[3];       // Minv[c][0] * wx
+    float mz[3];       // Minv[c][2] * wz
+    float cy[3];       // Minv[c][1] * wy * f^-1(Fy)
+    float eps[3];      // proven bound |lin32 - lin64| per channel (linear units)
+    float lo_p[3];     // band lower edge + eps
+    float lo_m[3];     // band lower edge - eps
+    float hi_p[3];     // band upper edge + eps
+    float hi_m[3];     // band upper edge - eps
+    float eps_code[3]; // eps + float rounding of the code thresholds
+    uint32_t flags;    // bit c (c=0,1,2 -> r,g,b): loud channel (pattern bit set)
+    int32_t t[3];      // target codes
+    int32_t k1;        // d > v_th   <=> d >= k1 (integer deltas); 256 = never
+    int32_t q0;        // d <= low   <=> d <= q0
+    // --- FP64 exact path (bit-identical to the reference) ----------------
+    double fy, ta, tb, wx, wz;
+    double cy64[3];
+    double lo[3], hi[3];
+};
+static_assert(sizeof(SearchConst) == 256, "SearchConst layout");
+
+// Device statistics block.
+struct Stats {
+    unsigned long long band_repairs;
+    unsigned long long code_repairs;
+    unsigned long long audit_violations;
+    unsigned long long class_mismatch;
+    unsigned long long overflow;
+    unsigned int audit_max_ratio_bits;  // float bits, atomicMax on non-negative floats
+    unsigned int pad;
+};
+
+enum Mode : int { kModeBand = 0, kModeCodes = 1 };
+enum Out : int { kOutPairs = 0, kOutCounts = 1, kOutFirst = 2 };
+enum Path : int { kPathFast = 0, kPathExact = 1, kPathAudit = 2 };
+
+// Everything one launch needs (passed by value as the kernel parameter).
+struct LaunchArgs {
+    const SearchConst* sc;     // [n_searches]
+    const float* radii_f;      // [nr]
+    const double* radii_d;     // [nr]
+    const float* trig_f;       // [na][2] = (sin/500, cos/200) as float
+    const double* trig_d;      // [na][2] = (sin, cos), glibc doubles (search.cpp:414-419)
+    const double* thr_d;       // [256] QuantTable thresholds (convert_kernel.hpp:123-141)
+    const float* thr_f;        // [257] thresholds rounded to float, [256] = +inf
+    const uint8_t* guess;      // [kGuessBuckets + 1] code(i / 4096)
+    double minv[9];            // kXyzToRgb (convert_kernel.hpp:47), row-major
+    int32_t n_searches;
+    int32_t nr;
+    int32_t na;
+    int32_t aligned;           // na % 32 == 0: a 32-candidate chunk never straddles rows
+    uint32_t tiles_per_search;
+    uint32_t cand_per_search;  // nr * na (< 2^32)
+    uint64_t na_magic;         // ceil(2^64 / na): k = umul64hi(i, na_magic)
+    uint64_t n_tiles;
+    unsigned long long* status;  // [n_tiles] look-back words (flag << 62 | value)
+    unsigned int* ticket;        // dynamic tile counter
+    unsigned long long* counts;  // [n_searches]
+    uint32_t* out_idx;           // [capacity]
+    uint8_t* out_codes;          // [capacity * 6]
+    uint64_t capacity;
+    uint32_t* first_idx;         // [n_searches] (FIRST)
+    uint8_t* first_codes;        // [n_searches * 6] (FIRST)
+    Stats* stats;
+};
+
+}  // namespace cvg

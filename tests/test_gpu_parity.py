@@ -1,0 +1,325 @@
+"""GPU parity: the fused sm_100a search vs the CPU oracle / reference goldens.
+
+Bar: bit-exact (integer/byte work).  Per-search counts and every emitted
+(idx = k*na+m, plus rgb, minus rgb) record must equal the oracle's on the same
+inputs; full-size configs are checked against reference-generated golden
+counts/hashes and size-independent properties.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from cvtest_util import golden, sha_records
+from paper_2507_22901_b200 import workloads as W
+from paper_2507_22901_b200.workloads import uniform_grid
+
+pytestmark = pytest.mark.gpu
+
+
+def run(ctx, wl, output="pairs", path="fast", basis=0, white=None, mode=0):
+    return ctx.search(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, output=output,
+                      path=path, delta_basis=basis, white_point=white, delta_mode=mode)
+
+
+def split(res, s):
+    a, b = int(res["offsets"][s]), int(res["offsets"][s + 1])
+    return res["idx"][a:b], res["codes"][a:b]
+
+
+def oracle_records(oracle, wl, s, basis=0, white=None, workers=4):
+    idx, codes, _ = oracle.search(wl.targets[s], int(wl.patterns[s]), wl.v_th[s], wl.r_novib[s], wl.radii,
+                                  wl.angles, delta_basis=basis, white=white, method=1, workers=workers,
+                                  want_deltas=False)
+    return idx, codes
+
+
+def assert_clean(res, path):
+    st = res["stats"]
+    assert st["class_mismatch"] == 0
+    if path == "audit":
+        assert st["audit_violations"] == 0
+        assert st["audit_max_ratio"] < 1.0, st
+
+
+@pytest.mark.parametrize("path", ["fast", "exact", "audit"])
+def test_cfg0_bit_exact(ctx, oracle, path):
+    wl = W.cfg0()
+    res = run(ctx, wl, path=path)
+    g = golden("workloads.json")["cfg0"]
+    assert res["n_pairs"] == g["total"] == 4802
+    idx, codes = split(res, 0)
+    oi, oc = oracle_records(oracle, wl, 0)
+    assert np.array_equal(idx, oi)
+    assert np.array_equal(codes, oc)
+    assert sha_records(idx, codes) == g["sha256"]
+    assert_clean(res, path)
+
+
+@pytest.mark.parametrize("basis", [0, 1])
+@pytest.mark.parametrize("path", ["fast", "exact", "audit"])
+def test_reference_small_grid_cases(ctx, path, basis):
+    """tests/test_search.cpp:177-204 cases, one launch for all of them."""
+    radii, angles = uniform_grid(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
+    cases = [c for c in golden("small_cases.json") if c["basis"] == basis]
+    res = ctx.search(np.array([c["target"] for c in cases], np.int32),
+                     np.array([W.bits(c["pattern"]) for c in cases], np.int32),
+                     np.array([c["v_th"] for c in cases]), np.array([c["r_novib"] for c in cases]),
+                     radii, angles, path=path, delta_basis=basis)
+    for s, c in enumerate(cases):
+        idx, codes = split(res, s)
+        assert len(idx) == c["count"], c
+        assert sha_records(idx, codes) == c["sha256"], c
+    assert_clean(res, path)
+
+
+@pytest.mark.parametrize("path", ["fast", "audit"])
+def test_cfg1_full_sweep(ctx, path):
+    wl = W.cfg1()
+    res = run(ctx, wl, path=path)
+    g = golden("workloads.json")["cfg1"]
+    assert res["counts"].tolist() == g["counts"]
+    assert res["n_pairs"] == g["total"] == 3785016
+    assert sha_records(res["idx"], res["codes"]) == g["sha256"]
+    assert_clean(res, path)
+
+
+def test_cfg1_counts_mode_matches_pairs(ctx):
+    wl = W.cfg1()
+    res = run(ctx, wl, output="counts")
+    assert res["counts"].tolist() == golden("workloads.json")["cfg1"]["counts"]
+
+
+def test_cfg3_dense_targets(ctx):
+    wl = W.cfg3()
+    res = run(ctx, wl)
+    g = golden("workloads.json")["cfg3"]
+    assert res["counts"].tolist() == g["counts"]
+    assert sha_records(res["idx"], res["codes"]) == g["sha256"]
+    assert_clean(res, "fast")
+
+
+def test_cfg4_first_pair_mode_crop(ctx):
+    g = golden("workloads.json")["cfg4_256x144"]
+    wl = W.cfg4(g["width"], g["height"])
+    res = run(ctx, wl, output="first")
+    import hashlib
+
+    m = hashlib.sha256()
+    m.update(res["counts"].astype(np.uint64).tobytes())
+    m.update(np.ascontiguousarray(res["first_idx"], np.uint32).tobytes())
+    m.update(np.ascontiguousarray(res["first_codes"], np.uint8).tobytes())
+    assert int(res["counts"].sum()) == g["total"]
+    assert m.hexdigest() == g["sha256"]
+
+
+@pytest.mark.slow
+def test_cfg2_fine_grid_counts_and_rows(ctx, oracle):
+    wl = W.cfg2()
+    res = run(ctx, wl)
+    g = golden("workloads.json").get("cfg2")
+    if g:
+        assert res["counts"].tolist() == g["counts"]
+    assert_clean(res, "fast")
+    na = len(wl.angles)
+    rows = [0, 1, 777, 2048, 4095]
+    for s in (0, 3, 8):
+        idx, codes = split(res, s)
+        assert np.all(np.diff(idx.astype(np.int64)) > 0)  # canonical order, no duplicates
+        sub = W.Workload("sub", wl.targets[s:s + 1], wl.patterns[s:s + 1], wl.v_th[s:s + 1],
+                         wl.r_novib[s:s + 1], wl.radii[rows], wl.angles)
+        oi, oc = oracle_records(oracle, sub, 0, workers=8)
+        k = idx // na
+        sel = np.isin(k, rows)
+        kk = np.searchsorted(np.array(rows), k[sel])
+        assert np.array_equal(kk * na + idx[sel] % na, oi)
+        assert np.array_equal(codes[sel], oc)
+
+
+# ---- reference API through the Python binding (test_search.cpp pins) -------
+
+def test_python_api_serial_equals_batch_and_oracle(cv, ctx, oracle):
+    grid = cv.VibrationGrid.uniform(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
+    for t in ([170, 170, 170], [240, 240, 240], [100, 100, 240], [240, 100, 240], [8, 8, 8]):
+        for p in ("100", "001", "101", "110", "111"):
+            th = cv.Thresholds(50.0, 0.5)
+            s = cv.serial_search(cv.SrgbColor(*t), grid, cv.BitPattern(p), th)
+            b = cv.batch_search(cv.SrgbColor(*t), grid, cv.BitPattern(p), th)
+            assert s == b
+            oi, oc, od = oracle.search(t, W.bits(p), 50.0, 0.5, grid.radii, grid.angles, method=0)
+            assert len(b) == len(oi)
+            for pair, i, c, d in zip(b, oi, oc, od):
+                assert pair.radius == grid.radii[i // len(grid.angles)]
+                assert pair.angle == grid.angles[i % len(grid.angles)]
+                assert [pair.plus.r, pair.plus.g, pair.plus.b, pair.minus.r, pair.minus.g, pair.minus.b] == c.tolist()
+                assert [pair.deltas.dr, pair.deltas.dg, pair.deltas.db] == d.tolist()
+                assert (pair.target.r, pair.target.g, pair.target.b) == tuple(t)
+
+
+def test_worker_count_independence(cv, ctx):
+    grid = cv.VibrationGrid.uniform(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
+    args = (cv.SrgbColor(170, 170, 170), grid, cv.BitPattern("101"), cv.Thresholds(50.0, 0.5))
+    base = cv.batch_search(*args, workers=1)
+    assert base
+    for w in (2, 3, 5, 16, 64):
+        assert cv.batch_search(*args, workers=w) == base
+
+
+def test_canonical_order_and_reverification(cv, ctx):
+    grid = cv.VibrationGrid.uniform(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
+    th = cv.Thresholds(50.0, 0.5)
+    pairs = cv.batch_search(cv.SrgbColor(240, 240, 240), grid, cv.BitPattern("110"), th)
+    assert len(pairs) > 1
+    for a, b in zip(pairs, pairs[1:]):
+        assert a.radius < b.radius or (a.radius == b.radius and a.angle < b.angle)
+    lab = cv.srgb_to_lab(cv.SrgbColor(240, 240, 240))
+    for p in pairs:
+        lp, lm = cv.displaced_pair(lab, p.radius, p.angle)
+        assert cv.lab_to_srgb_clipped(lp) == p.plus
+        assert cv.lab_to_srgb_clipped(lm) == p.minus
+        assert cv.channel_deltas(p.target, p.plus, p.minus) == p.deltas
+        assert cv.classify_pair(p.deltas, cv.BitPattern("110"), th)
+        assert lp.l == lab.l and lm.l == lab.l
+
+
+def test_zero_radius_never_pairs(cv, ctx):
+    grid = cv.VibrationGrid()
+    grid.radii = [0.0]
+    grid.angles = cv.VibrationGrid.uniform(1.0, 91.0, 10.0, 0.0, 350.0, 10.0).angles
+    for p in ("100", "010", "001", "110", "101", "011", "111"):
+        args = (cv.SrgbColor(170, 170, 170), grid, cv.BitPattern(p), cv.Thresholds(50.0, 0.5))
+        assert cv.serial_search(*args) == []
+        assert cv.batch_search(*args) == []
+
+
+def test_relaxing_r_novib_only_adds_pairs(cv, ctx):
+    grid = cv.VibrationGrid.uniform(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
+    for t in ((170, 170, 170), (100, 100, 240)):
+        for p in ("100", "101", "111"):
+            for v in (50.0, 100.0):
+                sets = []
+                for rn in (0.125, 0.25, 0.5):
+                    pairs = cv.batch_search(cv.SrgbColor(*t), grid, cv.BitPattern(p), cv.Thresholds(v, rn))
+                    sets.append({(x.radius, x.angle) for x in pairs})
+                assert sets[0] <= sets[1] <= sets[2]
+
+
+def test_frame_diff_basis(cv, ctx):
+    grid = cv.VibrationGrid.uniform(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
+    opts = cv.SearchOptions()
+    opts.delta_basis = cv.DeltaBasis.FRAME_DIFF
+    args = (cv.SrgbColor(170, 170, 170), grid, cv.BitPattern("101"), cv.Thresholds(50.0, 0.5))
+    fd = cv.batch_search_opts(*args, opts)
+    assert fd
+    for p in fd:
+        assert p.deltas == cv.frame_deltas(p.plus, p.minus)
+    assert fd == cv.serial_search_opts(*args, opts)
+    assert len(fd) != len(cv.batch_search(*args))
+
+
+def test_continuous_mode_fails_loudly(cv, ctx):
+    grid = cv.VibrationGrid.uniform(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
+    opts = cv.SearchOptions()
+    opts.delta_mode = cv.DeltaMode.CONTINUOUS
+    with pytest.raises(RuntimeError, match="Continuous"):
+        cv.batch_search_opts(cv.SrgbColor(170, 170, 170), grid, cv.BitPattern("101"), cv.Thresholds(50.0, 0.5),
+                             opts)
+
+
+def test_batch_many_equals_single(cv, ctx):
+    grid = cv.VibrationGrid.uniform(1.0, 60.0, 3.0, 0.0, 357.0, 3.0)
+    specs = [cv.SearchSpec(cv.SrgbColor(*t), cv.BitPattern(p), cv.Thresholds(v, r))
+             for t in ((100, 100, 100), (240, 100, 240)) for p in ("101", "111") for v, r in ((50, .5), (100, .25))]
+    many = cv.batch_search_many(specs, grid)
+    counts = cv.batch_count_many(specs, grid)
+    for sp, got, n in zip(specs, many, counts):
+        assert got == cv.batch_search(sp.target, grid, sp.pattern, sp.thresholds)
+        assert n == len(got)
+
+
+def test_concurrent_callers(cv, ctx):
+    grid = cv.VibrationGrid.uniform(1.0, 91.0, 5.0, 0.0, 355.0, 5.0)
+    args = (cv.SrgbColor(170, 170, 170), grid, cv.BitPattern("101"), cv.Thresholds(50.0, 0.5))
+    want = cv.batch_search(*args)
+    out = [None] * 6
+
+    def work(i):
+        out[i] = cv.batch_search(*args)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(6)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert all(o == want for o in out)
+
+
+# ---- edge cases -------------------------------------------------------------
+
+EDGE_GRIDS = {
+    "na1": (W.radii(50, 2.0), np.array([0.3])),
+    "na7": (W.radii(33, 3.0), W.angles(7)),
+    "na33": (W.radii(70, 1.5), W.angles(33)),
+    "nr1": (np.array([40.0]), W.angles(4096)),
+    "huge_r": (W.radii(16, 70.0), W.angles(512)),
+    "tiny_r": (W.radii(64, 1e-3), W.angles(96)),
+}
+EDGE_TARGETS = [[0, 0, 0], [255, 255, 255], [8, 8, 8], [255, 0, 0], [0, 255, 255], [1, 254, 128], [128, 128, 128]]
+
+
+@pytest.mark.parametrize("gname", sorted(EDGE_GRIDS))
+@pytest.mark.parametrize("path", ["fast", "audit"])
+def test_edge_grids_vs_oracle(ctx, oracle, gname, path):
+    radii, angles = EDGE_GRIDS[gname]
+    t, p, v, r = [], [], [], []
+    for tg in EDGE_TARGETS:
+        for pat, vt, rn in ((7, 50.0, 0.5), (5, 100.0, 0.25), (2, 20.0, 1.0), (1, 300.0, 0.5), (6, 0.5, 1.0)):
+            t.append(tg); p.append(pat); v.append(vt); r.append(rn)
+    wl = W.Workload("edge", np.array(t, np.int32), np.array(p, np.int32), np.array(v), np.array(r), radii, angles)
+    for basis in (0, 1):
+        res = run(ctx, wl, path=path, basis=basis)
+        for s in range(wl.n_searches):
+            idx, codes = split(res, s)
+            oi, oc = oracle_records(oracle, wl, s, basis=basis, workers=1)
+            assert np.array_equal(idx, oi), (gname, s, basis)
+            assert np.array_equal(codes, oc), (gname, s, basis)
+        assert_clean(res, path)
+
+
+def test_custom_white_point(ctx, oracle):
+    wp = [0.9642, 1.0, 0.8251]
+    wl = W.Workload("wp", np.array([[120, 60, 200], [30, 200, 90]], np.int32), np.array([5, 7], np.int32),
+                    np.array([50.0, 40.0]), np.array([0.5, 0.5]), W.radii(80, 1.25), W.angles(360))
+    res = run(ctx, wl, white=wp, path="audit")
+    for s in range(2):
+        idx, codes = split(res, s)
+        oi, oc = oracle_records(oracle, wl, s, white=wp)
+        assert np.array_equal(idx, oi) and np.array_equal(codes, oc)
+    assert_clean(res, "audit")
+
+
+def test_empty_grid_and_empty_batch(ctx):
+    wl = W.cfg0()
+    res = ctx.search(wl.targets, wl.patterns, wl.v_th, wl.r_novib, np.zeros(0), wl.angles)
+    assert res["n_pairs"] == 0 and res["counts"].tolist() == [0]
+    res = ctx.search(np.zeros((0, 3), np.int32), np.zeros(0, np.int32), np.zeros(0), np.zeros(0), wl.radii,
+                     wl.angles)
+    assert res["n_pairs"] == 0
+
+
+def test_plan_overflow_then_reserve(ctx):
+    wl = W.cfg1()
+    plan = ctx.plan(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles)
+    plan.reserve(1000)  # far too small: counts stay valid, the pairs overflow
+    plan.run()
+    with pytest.raises(RuntimeError, match="too small"):
+        plan.sync()
+    plan.reserve(3785016)
+    plan.run()
+    assert plan.sync() == 3785016
+    res = plan.fetch()
+    assert sha_records(res["idx"], res["codes"]) == golden("workloads.json")["cfg1"]["sha256"]
+    for _ in range(3):  # repeated runs reuse the device buffers
+        plan.run()
+    assert plan.sync() == 3785016
+    assert plan.launches == 1
