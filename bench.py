@@ -1,0 +1,346 @@
+#!/usr/bin/env python3
+"""Benchmark: candidate color pairs evaluated per second on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1] [--impl ours|reference]
+
+One step = one pass of the hot path (colorvibe::batch_search, reference
+src/search.cpp:403-456) over one batch of synthetic input: by default
+BASELINE.json configs[1], the 756-search sweep on the 256 x 1024 grid
+(198,180,864 candidates), evaluated in ONE launch of the fused kernel.
+
+Prints ONE JSON line (rank 0):
+  value   -- Gcand/s with inputs resident in HBM (device plan; CUDA events on
+             the launching stream around each step, L2 flushed between steps)
+  e2e     -- same metric through the C-ABI host call `cvg_search` (host
+             arrays in; per-target prep, H2D, kernel, D2H of counts + every
+             pair record out), wall-clocked per call
+  roofline-- FP32-issue roofline of the fused kernel (SURVEY.md §8(d):
+             W = 50 FP32 instructions per candidate) vs the FFMA issue peak
+             measured in this run
+  cpu_baseline -- the reference's own batch_search (oracle/_ref, built from
+             the reference sources) on all host cores, same workload
+
+Multi-GPU (torchrun, one process per GPU): weak scaling -- every rank
+evaluates its own full copy of the workload; there is no data-path exchange
+(the searches are independent), value = all ranks' candidates / max-over-
+ranks device time.  `--impl reference` runs the reference CPU arm on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+W_INSTR = 50  # algorithmic FP32 instructions per candidate
+METRIC = "candidate color pairs evaluated/sec"
+UNIT = "Gcand/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg3"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def workload(name):
+    from paper_2507_22901_b200 import workloads as W
+
+    return W.ALL[name]()
+
+
+def config_dict(wl, n, extra=None):
+    d = {"workload": f"{wl.name} (BASELINE.json configs[{wl.name[-1]}])", "searches": wl.n_searches,
+         "grid": f"{len(wl.radii)} radii x {len(wl.angles)} angles", "candidates_per_step": wl.candidates,
+         "targets": "Table-1 colors" if wl.name in ("cfg0", "cfg1", "cfg2") else "16^3 lattice",
+         "parallelism": f"replicas{n}" if n > 1 else "single", "l2": "flushed between steps (256 MiB write)"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+# ---------------------------------------------------------------------------
+# clocks under load (pynvml, sampled in a thread)
+
+class ClockSampler:
+    def __init__(self, device: int, period: float = 0.01):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._ok = True
+        except Exception:  # noqa: BLE001
+            pass
+        self.period = period
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    REASONS = {
+        "sw_power_cap": 0x4, "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80, "applications_clocks_setting": 0x2,
+    }
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                break
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._ok:
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._ok:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+
+def cpu_reference_arm(wl, steps, warmup, cores=None):
+    """The reference's own batch_search (oracle/_ref) once per search, all host
+    threads, full workload per step.  Returns (Gcand/s, seconds/step, cores)."""
+    from oracle.oracle import Reference
+
+    ref = Reference()
+    cores = cores or os.cpu_count() or 1
+    for _ in range(warmup):
+        ref.search_many(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, workers=cores)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        counts = ref.search_many(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, workers=cores)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    return wl.candidates * steps / total / 1e9, total / steps, cores, int(counts.sum()), ref.path
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    wl = workload(args.config)
+    steps = max(1, min(args.steps, 20))
+    warm = max(0, min(args.warmup, 2))
+    v, sec, cores, pairs, path = cpu_reference_arm(wl, steps, warm)
+    out = {
+        "metric": METRIC, "value": round(v, 6), "unit": UNIT, "n_gpus": 0, "steps": steps, "warmup": warm,
+        "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": config_dict(wl, 1, {"cpu": cpu_model(), "library": os.path.relpath(path, ROOT)}),
+        "pairs_per_step": pairs,
+        "cpu_baseline": {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"full {wl.name}: {wl.n_searches} reference batch_search calls per step, "
+                                   f"workers={cores}"},
+        "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def ncu_traffic():
+    """dram bytes per launch of the search kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2507_22901_b200 as cv
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = workload(args.config)
+    ctx = cv.Context(local)
+    stream = torch.cuda.current_stream()
+
+    # ---------------- device-resident plan: `value` ----------------
+    plan = ctx.plan(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles)
+    plan.run(stream.cuda_stream)
+    n_pairs = plan.sync()
+    plan.reserve(max(n_pairs, 1))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(args.warmup):
+        flush.zero_()
+        plan.run(stream.cuda_stream)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush outside the timed events
+            starts[i].record(stream)
+            plan.run(stream.cuda_stream)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    got = plan.sync()
+    assert got == n_pairs, (got, n_pairs)
+    kms = plan.last_kernel_ms()  # search kernel alone (last step)
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = wl.candidates * world * args.steps / (max_ms * 1e-3) / 1e9
+
+    # per-launch kernel time over the timed steps: events inside the plan
+    # cover only the search kernel; re-measure a few steps for the roofline
+    kern = []
+    for _ in range(min(args.steps, 20)):
+        flush.zero_()
+        plan.run(stream.cuda_stream)
+        kern.append(plan.last_kernel_ms())
+    kern_ms = statistics.median(kern)
+
+    # ---------------- e2e through the C-ABI host call ----------------
+    e2e_steps = args.e2e_steps or max(3, min(args.steps, 20))
+    res = ctx.search(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles)  # warm the pools
+    assert int(res["n_pairs"]) == n_pairs
+    h2d = int(res["stats"]["h2d_bytes"])
+    d2h = int(res["stats"]["d2h_bytes"])
+    del res
+    if dist:
+        dist.barrier()
+    e2e_times = []
+    for _ in range(e2e_steps):
+        t0 = time.perf_counter()
+        r = ctx.search(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles)
+        _ = int(r["n_pairs"])
+        e2e_times.append(time.perf_counter() - t0)
+        del r
+    e2e_s = sum(e2e_times)
+    t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        # verification gather (outside every timed region): per-search counts of all ranks
+        res = plan.fetch()
+        c = torch.tensor(res["counts"].astype(np.int64), device="cuda")
+        allc = [torch.empty_like(c) for _ in range(world)]
+        dist.all_gather(allc, c)
+        assert all(torch.equal(x, allc[0]) for x in allc)
+    e2e_value = wl.candidates * world * e2e_steps / float(t.item()) / 1e9
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---------------- roofline ----------------
+    peak_lane, _ = cv.measure_ffma_peak(local)
+    achieved = wl.candidates * W_INSTR / (kern_ms * 1e-3) / 1e12
+    peak = peak_lane / 1e12
+    roofline = {"bound": "fp32_issue", "achieved": round(achieved, 3), "peak": round(peak, 3),
+                "unit": "Tinstr/s", "frac": round(achieved / peak, 4) if peak else None,
+                "traffic": ncu_traffic(), "kernel_ms": round(kern_ms, 4),
+                "instr_per_candidate": W_INSTR,
+                "peak_source": "FFMA issue microbenchmark measured in this run (cvg_measure_ffma_peak)",
+                "hbm": {"bytes_per_launch": n_pairs * 10 + wl.n_searches * 8,
+                        "achieved_gbs": round((n_pairs * 10 + wl.n_searches * 8) / (kern_ms * 1e-3) / 1e9, 2)}}
+
+    # ---------------- CPU baseline (reference, bounded sample) ----------------
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            v, sec, cores, pairs, _ = cpu_reference_arm(wl, 2, 1)
+            cpu = {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "reference",
+                   "sample": f"full {wl.name} ({wl.n_searches} searches), best of 2 after 1 warm-up, "
+                             f"workers={cores}, {cpu_model()}",
+                   "pairs": pairs, "s_per_step": round(sec, 4)}
+            assert pairs == n_pairs, (pairs, n_pairs)
+        except FileNotFoundError as e:
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    out = {
+        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64repair", "data": "synthetic",
+        "config": config_dict(wl, world, {"pairs_per_step": n_pairs}),
+        "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "s_per_step": round(float(t.item()) / e2e_steps, 5), "steps": e2e_steps,
+                "api": "cvg_search (C-ABI host call)"},
+        "gpu_launches": plan.launches * args.steps,
+        "clocks": clk.summary(),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -107,6 +107,8 @@ typedef struct {
     uint64_t n_class_mismatch;   /* band decision != classify_pair on exact codes (must be 0) */
     float audit_max_ratio;       /* PATH_AUDIT: max |lin32 - lin64| / bound (must be < 1) */
     float kernel_ms;             /* device time of the search kernels of this call */
+    uint64_t h2d_bytes;          /* host->device bytes this call copied (tables + constants) */
+    uint64_t d2h_bytes;          /* device->host bytes this call copied (counts, stats, pairs) */
 } cvg_result;
 
 /* ---- context ----------------------------------------------------------- */
@@ -138,6 +140,10 @@ CVG_API int cvg_plan_fetch(cvg_plan* plan, cvg_result* out);
 /* device pointers of the plan's outputs (valid until the plan is destroyed) */
 CVG_API int cvg_plan_device_outputs(cvg_plan* plan, uint64_t** counts, uint32_t** idx,
                                     uint8_t** codes, uint64_t* capacity);
+/* device time (ms) of the search kernel(s) of the plan's last completed run */
+CVG_API int cvg_plan_last_kernel_ms(cvg_plan* plan, float* ms);
+/* bytes of device-resident input the plan uploaded (constants + grid tables) */
+CVG_API uint64_t cvg_plan_input_bytes(const cvg_plan* plan);
 /* number of kernel launches one cvg_plan_run enqueues */
 CVG_API int cvg_plan_launches(const cvg_plan* plan);
 CVG_API uint64_t cvg_plan_candidates(const cvg_plan* plan);

@@ -123,6 +123,8 @@ py::dict result_dict(std::shared_ptr<ResultHolder> h, int output) {
     stats["class_mismatch"] = r.n_class_mismatch;
     stats["audit_max_ratio"] = r.audit_max_ratio;
     stats["kernel_ms"] = r.kernel_ms;
+    stats["h2d_bytes"] = r.h2d_bytes;
+    stats["d2h_bytes"] = r.d2h_bytes;
     out["stats"] = stats;
     return out;
 }
@@ -378,6 +380,12 @@ PYBIND11_MODULE(_core, m) {
         })
         .def_property_readonly("launches", [](const Plan& p) { return cvg_plan_launches(p.plan); })
         .def_property_readonly("candidates", [](const Plan& p) { return cvg_plan_candidates(p.plan); })
+        .def_property_readonly("input_bytes", [](const Plan& p) { return cvg_plan_input_bytes(p.plan); })
+        .def("last_kernel_ms", [](Plan& p) {
+            float ms = 0.f;
+            check(cvg_plan_last_kernel_ms(p.plan, &ms));
+            return ms;
+        })
         .def("device_outputs", [](Plan& p) {
             uint64_t* counts = nullptr;
             uint32_t* idx = nullptr;

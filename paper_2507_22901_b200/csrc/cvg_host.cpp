@@ -444,6 +444,7 @@ struct cvg_plan {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     bool ran = false;
     cudaStream_t last_stream = nullptr;
+    uint64_t input_bytes = 0;
 };
 
 namespace {
@@ -541,6 +542,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     const size_t o_thf = L.take(sizeof(float) * 258);
     const size_t o_gs = L.take(cvg::kGuessBuckets + 1);
     const size_t bytes = L.off;
+    p->input_bytes = bytes;
     unsigned char* stage = static_cast<unsigned char*>(ctx->host.alloc(bytes));
     p->d_const = ctx->dev.alloc(bytes);
     if (!stage || !p->d_const) {
@@ -699,7 +701,10 @@ int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
     r->n_class_mismatch = hs.st.class_mismatch;
     std::memcpy(&r->audit_max_ratio, &hs.st.audit_max_ratio_bits, sizeof(float));
     r->kernel_ms = hs.ms;
+    r->h2d_bytes = p->input_bytes;
+    r->d2h_bytes = sizeof(uint64_t) * n + sizeof(cvg::Stats);
     if (p->out == cvg::kOutPairs) {
+        r->d2h_bytes += total * 10;
         r->offsets = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (n + 1)));
         if (!r->offsets) return fail(CVG_ENOMEM, "host allocation failed");
         r->offsets[0] = 0;
@@ -714,6 +719,7 @@ int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
             CVG_CUDA(cudaStreamSynchronize(st));
         }
     } else if (p->out == cvg::kOutFirst && n) {
+        r->d2h_bytes += n * 10;
         r->first_idx = static_cast<uint32_t*>(ctx->host.alloc(n * 4));
         r->first_codes = static_cast<uint8_t*>(ctx->host.alloc(n * 6));
         if (!r->first_idx || !r->first_codes) return fail(CVG_ENOMEM, "pinned host allocation failed");
@@ -862,6 +868,18 @@ int cvg_plan_device_outputs(cvg_plan* p, uint64_t** counts, uint32_t** idx, uint
     if (capacity) *capacity = p->capacity;
     return CVG_OK;
 }
+
+int cvg_plan_last_kernel_ms(cvg_plan* p, float* ms) {
+    if (!p || !ms) return fail(CVG_EINVAL, "null plan or output");
+    *ms = 0.f;
+    if (p->empty || !p->ran) return CVG_OK;
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    CVG_CUDA(cudaEventSynchronize(p->ev1));
+    CVG_CUDA(cudaEventElapsedTime(ms, p->ev0, p->ev1));
+    return CVG_OK;
+}
+
+uint64_t cvg_plan_input_bytes(const cvg_plan* p) { return p ? p->input_bytes : 0; }
 
 int cvg_plan_launches(const cvg_plan* p) {
     if (!p || p->empty) return 0;

@@ -34,6 +34,18 @@ def oracle_records(oracle, wl, s, basis=0, white=None, workers=4):
     return idx, codes
 
 
+def sha_by_search(res):
+    """Hash in the fixture's layout: per search, its idx bytes then its codes bytes."""
+    import hashlib
+
+    m = hashlib.sha256()
+    for s in range(len(res["counts"])):
+        idx, codes = split(res, s)
+        m.update(np.ascontiguousarray(idx, np.uint32).tobytes())
+        m.update(np.ascontiguousarray(codes, np.uint8).tobytes())
+    return m.hexdigest()
+
+
 def assert_clean(res, path):
     st = res["stats"]
     assert st["class_mismatch"] == 0
@@ -80,7 +92,7 @@ def test_cfg1_full_sweep(ctx, path):
     g = golden("workloads.json")["cfg1"]
     assert res["counts"].tolist() == g["counts"]
     assert res["n_pairs"] == g["total"] == 3785016
-    assert sha_records(res["idx"], res["codes"]) == g["sha256"]
+    assert sha_by_search(res) == g["sha256"]
     assert_clean(res, path)
 
 
@@ -95,7 +107,7 @@ def test_cfg3_dense_targets(ctx):
     res = run(ctx, wl)
     g = golden("workloads.json")["cfg3"]
     assert res["counts"].tolist() == g["counts"]
-    assert sha_records(res["idx"], res["codes"]) == g["sha256"]
+    assert sha_by_search(res) == g["sha256"]
     assert_clean(res, "fast")
 
 
@@ -318,7 +330,7 @@ def test_plan_overflow_then_reserve(ctx):
     plan.run()
     assert plan.sync() == 3785016
     res = plan.fetch()
-    assert sha_records(res["idx"], res["codes"]) == golden("workloads.json")["cfg1"]["sha256"]
+    assert sha_by_search(res) == golden("workloads.json")["cfg1"]["sha256"]
     for _ in range(3):  # repeated runs reuse the device buffers
         plan.run()
     assert plan.sync() == 3785016
