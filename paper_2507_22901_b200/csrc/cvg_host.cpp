@@ -331,24 +331,48 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
     const double u = std::ldexp(1.0, -24);
     const BoundTerms bx = finv_bound(fx0, rmax * kInv500);
     const BoundTerms bz = finv_bound(fz0, rmax * kInv200);
+    double eps_band = 0.0, vbound = 0.0;
     for (int c = 0; c < 3; ++c) {
         const double mx = m[c][0] * wp[0], mz = m[c][2] * wp[2], cy = S.cy64[c];
+        const double amx = std::fabs(mx), amz = std::fabs(mz);
+        // Forward error of lin = fma(mx, gx, fma(mz, gz, add)) for an additive
+        // constant `add` (cy for codes, cy - centre for the band statistic).
+        auto lin_err = [&](double add_exact, double add_rounding) {
+            const double aadd = std::fabs(add_exact);
+            const double inner_max = amz * bz.gmax + aadd;
+            const double e_inner = amz * bz.err * (1 + u) + u * amz * bz.gmax + add_rounding + u * (inner_max + amz * bz.err);
+            const double lin_max = amx * bx.gmax + inner_max;
+            return std::pair<double, double>(amx * bx.err * (1 + u) + u * amx * bx.gmax + e_inner +
+                                                 u * (lin_max + amx * bx.err),
+                                             lin_max);
+        };
         S.mx[c] = static_cast<float>(mx);
         S.mz[c] = static_cast<float>(mz);
         S.cy[c] = static_cast<float>(cy);
-        const double amx = std::fabs(mx), amz = std::fabs(mz), acy = std::fabs(cy);
-        const double inner_max = amz * bz.gmax + acy;
-        const double e_inner = amz * bz.err * (1 + u) + u * amz * bz.gmax + u * acy + u * (inner_max + amz * bz.err);
-        const double lin_max = amx * bx.gmax + inner_max;
-        const double e_lin = amx * bx.err * (1 + u) + u * amx * bx.gmax + e_inner + u * (lin_max + amx * bx.err);
+        const auto [e_lin, lin_max] = lin_err(cy, u * std::fabs(cy));
         const double eps = 1.05 * e_lin + 1e-12;
         S.eps[c] = round_up_f(eps);
         S.eps_code[c] = round_up_f(eps + std::ldexp(1.0, -23));
-        S.lo_p[c] = round_up_f(S.lo[c] + eps);
-        S.lo_m[c] = round_down_f(S.lo[c] - eps);
-        S.hi_p[c] = round_up_f(S.hi[c] + eps);
-        S.hi_m[c] = round_down_f(S.hi[c] - eps);
+        // Band statistic: with centre cc and half-width hh of [lo, hi] (an
+        // infinite edge replaced by -+L, L > every |lin| on the grid, which
+        // leaves the test unchanged), a channel is inside iff
+        // max(|vp - cc|, |vm - cc|) <= hh.  g = sg * (max - hh) < 0 iff the
+        // channel passes (quiet: both inside; loud: not both inside).
+        const double L = lin_max + e_lin + 1.0;
+        vbound = std::max(vbound, L);
+        const double lo = std::isinf(S.lo[c]) ? -L : S.lo[c];
+        const double hi = std::isinf(S.hi[c]) ? L : S.hi[c];
+        const double cc = 0.5 * (lo + hi), hh = 0.5 * (hi - lo);
+        const double sg = bits[c] ? -1.0 : 1.0;
+        S.cyc[c] = static_cast<float>(cy - cc);
+        S.sg[c] = static_cast<float>(sg);
+        S.nsh[c] = static_cast<float>(-sg * hh);
+        const auto [e_d, d_max] = lin_err(cy - cc, u * std::fabs(cy - cc) + 1e-15);
+        const double e_g = e_d + u * hh + u * (d_max + e_d + hh) + 1e-15;
+        eps_band = std::max(eps_band, 1.05 * e_g + 1e-12);
     }
+    S.eps_band = round_up_f(eps_band);
+    S.vbound = static_cast<float>(vbound);
 }
 
 // ---------------------------------------------------------------------------
@@ -520,7 +544,8 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     for (int s = 0; s < p->n; ++s) make_search_const(d, s, rmax, p->mode, T, sc[s]);
     std::vector<float> radii_f(p->nr);
     for (int k = 0; k < p->nr; ++k) radii_f[k] = static_cast<float>(d->radii[k]);
-    std::vector<float> trig_f(2 * static_cast<size_t>(p->na));
+    // float trig table padded by 64 entries: the hot loop prefetches one chunk ahead
+    std::vector<float> trig_f(2 * (static_cast<size_t>(p->na) + 64), 0.0f);
     std::vector<double> trig_d(2 * static_cast<size_t>(p->na));
     for (int j = 0; j < p->na; ++j) {  // search.cpp:414-419
         const double sn = std::sin(d->angles[j]);

@@ -69,12 +69,10 @@ __device__ __forceinline__ uint32_t div_na(uint32_t i, const LaunchArgs& A) {
 }
 
 // ------------------------------------------------------------------------
-// Per-search constants held in registers for a tile.
+// Per-search constants held in registers for a tile (phase 1).
 struct Consts {
-    float fx0, fz0, rcube;
-    float mx[3], mz[3], cy[3];
-    float lo_p[3], lo_m[3], hi_p[3], hi_m[3];
-    float ec[3];
+    float fx0, fz0, rcube, eps_band;
+    float mx[3], mz[3], cyc[3], sg[3], nsh[3];
     uint32_t flags;
 };
 
@@ -82,18 +80,34 @@ __device__ __forceinline__ void load_consts(const SearchConst* S, Consts& c) {
     c.fx0 = __ldg(&S->fx0);
     c.fz0 = __ldg(&S->fz0);
     c.rcube = __ldg(&S->rcube);
+    c.eps_band = __ldg(&S->eps_band);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        c.mx[q] = __ldg(&S->mx[q]);
+        c.mz[q] = __ldg(&S->mz[q]);
+        c.cyc[q] = __ldg(&S->cyc[q]);
+        c.sg[q] = __ldg(&S->sg[q]);
+        c.nsh[q] = __ldg(&S->nsh[q]);
+    }
+    c.flags = __ldg(&S->flags);
+}
+
+// Constants for the code path (phase 2 and CODES mode).
+struct CodeConsts {
+    float fx0, fz0;
+    float mx[3], mz[3], cy[3], ec[3];
+};
+
+__device__ __forceinline__ void load_code_consts(const SearchConst* S, CodeConsts& c) {
+    c.fx0 = __ldg(&S->fx0);
+    c.fz0 = __ldg(&S->fz0);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         c.mx[q] = __ldg(&S->mx[q]);
         c.mz[q] = __ldg(&S->mz[q]);
         c.cy[q] = __ldg(&S->cy[q]);
-        c.lo_p[q] = __ldg(&S->lo_p[q]);
-        c.lo_m[q] = __ldg(&S->lo_m[q]);
-        c.hi_p[q] = __ldg(&S->hi_p[q]);
-        c.hi_m[q] = __ldg(&S->hi_m[q]);
         c.ec[q] = __ldg(&S->eps_code[q]);
     }
-    c.flags = __ldg(&S->flags);
 }
 
 // ------------------------------------------------------------------------
@@ -189,39 +203,44 @@ __device__ __forceinline__ float finv_fast(float f) {
     return f > kU0f ? c3 : l;
 }
 
+// The six linear endpoint values (plus: vp, minus: vm) minus an additive
+// offset folded into `add` (cy for the values themselves, cy - centre for the
+// band statistic).  f = f0 +- r*s' is one FFMA; f^-1 two FMULs (+ select).
 template <bool kCubeOnly>
-__device__ __forceinline__ void fast_linear(const Consts& C, float r, float2 sc, float* vp, float* vm) {
-    const float fxp = fmaf(r, sc.x, C.fx0);
-    const float fxm = fmaf(-r, sc.x, C.fx0);
-    const float fzp = fmaf(-r, sc.y, C.fz0);
-    const float fzm = fmaf(r, sc.y, C.fz0);
+__device__ __forceinline__ void fast_linear(float fx0, float fz0, const float* mx, const float* mz, const float* add,
+                                            float r, float2 sc, float* vp, float* vm) {
+    const float fxp = fmaf(r, sc.x, fx0);
+    const float fxm = fmaf(-r, sc.x, fx0);
+    const float fzp = fmaf(-r, sc.y, fz0);
+    const float fzm = fmaf(r, sc.y, fz0);
     const float gxp = finv_fast<kCubeOnly>(fxp);
     const float gxm = finv_fast<kCubeOnly>(fxm);
     const float gzp = finv_fast<kCubeOnly>(fzp);
     const float gzm = finv_fast<kCubeOnly>(fzm);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-        vp[q] = fmaf(C.mx[q], gxp, fmaf(C.mz[q], gzp, C.cy[q]));
-        vm[q] = fmaf(C.mx[q], gxm, fmaf(C.mz[q], gzm, C.cy[q]));
+        vp[q] = fmaf(mx[q], gxp, fmaf(mz[q], gzp, add[q]));
+        vm[q] = fmaf(mx[q], gxm, fmaf(mz[q], gzm, add[q]));
     }
 }
 
-// Band test with margins: returns certain pass; sets unsure when no channel
-// certainly fails and some channel is undecided.
-__device__ __forceinline__ bool fast_band(const Consts& C, const float* vp, const float* vm, bool& unsure) {
-    bool pass = true, fail = false;
+// Band statistic of the reference band test (search.cpp:267-276,
+// make_bands 291-329).  With dp/dm = endpoint value minus the band centre,
+// g_c = sg_c * (max(|dp|, |dm|) - h_c) is negative iff channel c passes
+// (quiet: both endpoints inside the band; loud: not both inside), so the
+// candidate passes iff G = max_c g_c < 0.  |G32 - G| <= eps_band (host
+// proof), hence G < -eps certainly passes, G > eps certainly fails and only
+// |G| <= eps goes to the FP64 path.  7 ALU-pipe ops per candidate.
+__device__ __forceinline__ bool fast_band(const Consts& C, const float* dp, const float* dm, bool& unsure) {
+    float G = 0.f;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-        const float vmin = fminf(vp[q], vm[q]);
-        const float vmax = fmaxf(vp[q], vm[q]);
-        const bool cin = (vmin >= C.lo_p[q]) & (vmax < C.hi_m[q]);
-        const bool maybe = (vmin >= C.lo_m[q]) & (vmax < C.hi_p[q]);
-        const bool loud = (C.flags >> q) & 1;
-        pass &= loud ? !maybe : cin;
-        fail |= loud ? cin : !maybe;
+        const float M = fmaxf(fabsf(dp[q]), fabsf(dm[q]));
+        const float g = fmaf(C.sg[q], M, C.nsh[q]);
+        G = q == 0 ? g : fmaxf(G, g);
     }
-    unsure = !pass & !fail;
-    return pass;
+    unsure = fabsf(G) <= C.eps_band;
+    return G < -C.eps_band;
 }
 
 // Linear value -> code through the float table, verified against the bound:
@@ -242,18 +261,34 @@ struct Smem {
     uint8_t guess[kGuessBuckets + 16];
 };
 
-// Codes of the six endpoint channels for one candidate, exact.
+struct Counters {
+    unsigned long long repairs = 0, code_repairs = 0, violations = 0, mismatch = 0, overflow = 0;
+    float max_ratio = 0.f;
+};
+
+__device__ __forceinline__ void audit_ratio(const SearchConst* S, const float* vp, const float* vm, const double* lp,
+                                            const double* lm, float& max_ratio) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const double eps = __ldg(&S->eps[q]);
+        max_ratio = fmaxf(max_ratio, static_cast<float>(fabs(static_cast<double>(vp[q]) - lp[q]) / eps));
+        max_ratio = fmaxf(max_ratio, static_cast<float>(fabs(static_cast<double>(vm[q]) - lm[q]) / eps));
+    }
+}
+
+// Codes of the six endpoint channels of candidate (k, m), exact: FP32 value
+// + table lookup verified against the bound, FP64 for unverified lanes.
+// Called by all 32 lanes (warp votes inside).
 template <int kPath>
-__device__ __forceinline__ void candidate_codes(const Smem& sm, const SearchConst* S, const Consts& C,
+__device__ __forceinline__ void candidate_codes(const Smem& sm, const SearchConst* S, const CodeConsts& C,
                                                 const LaunchArgs& A, uint32_t k, uint32_t m, bool active,
-                                                int* cp, int* cm, unsigned long long& repairs,
-                                                unsigned long long& violations, float& max_ratio) {
+                                                int* cp, int* cm, unsigned long long& repairs, Counters& ct) {
     bool need_exact = true;
     if (kPath != kPathExact) {
         float vp[3], vm[3];
         const float r = __ldg(&A.radii_f[k]);
         const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + m);
-        fast_linear<false>(C, r, sc, vp, vm);
+        fast_linear<false>(C.fx0, C.fz0, C.mx, C.mz, C.cy, r, sc, vp, vm);
         bool all_ok = true;
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
@@ -265,23 +300,24 @@ __device__ __forceinline__ void candidate_codes(const Smem& sm, const SearchCons
         if (kPath == kPathAudit) {
             double lp[3], lm[3];
             exact_linear(S, A, k, m, lp, lm);
+            bool wrong = false;
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
                 const int ep = code_exact(lp[q], sm.thr_d), em = code_exact(lm[q], sm.thr_d);
-                if (all_ok && active && (ep != cp[q] || em != cm[q])) ++violations;
-                const float eps = __ldg(&S->eps[q]);
-                max_ratio = fmaxf(max_ratio, static_cast<float>(fabs(static_cast<double>(vp[q]) - lp[q]) / eps));
-                max_ratio = fmaxf(max_ratio, static_cast<float>(fabs(static_cast<double>(vm[q]) - lm[q]) / eps));
+                wrong |= (ep != cp[q]) | (em != cm[q]);
                 cp[q] = ep;
                 cm[q] = em;
             }
-            need_exact = false;
-            if (!all_ok && active) ++repairs;
-        } else {
-            need_exact = !all_ok;
-            if (__any_sync(kFull, need_exact) == 0) return;
-            if (need_exact && active) ++repairs;
+            if (active) {
+                ct.violations += all_ok && wrong;
+                repairs += !all_ok;
+                audit_ratio(S, vp, vm, lp, lm, ct.max_ratio);
+            }
+            return;
         }
+        need_exact = !all_ok;
+        if (!__any_sync(kFull, need_exact)) return;
+        if (need_exact && active) ++repairs;
     }
     if (need_exact) {
         double lp[3], lm[3];
@@ -294,15 +330,14 @@ __device__ __forceinline__ void candidate_codes(const Smem& sm, const SearchCons
     }
 }
 
-// Phase-1 decision for one candidate.
-template <int kMode, int kPath, bool kCubeOnly>
+// Phase-1 decision of one candidate, any mode/path (the generic loop).
+template <int kMode, int kPath>
 __device__ __forceinline__ bool candidate_pass(const Smem& sm, const SearchConst* S, const Consts& C,
-                                               const LaunchArgs& A, uint32_t k, uint32_t m, float r,
-                                               bool active, unsigned long long& repairs,
-                                               unsigned long long& violations, float& max_ratio) {
+                                               const CodeConsts& CC, const LaunchArgs& A, uint32_t k, uint32_t m,
+                                               bool active, Counters& ct) {
     if (kMode == kModeCodes) {
         int cp[3], cm[3];
-        candidate_codes<kPath>(sm, S, C, A, k, m, active, cp, cm, repairs, violations, max_ratio);
+        candidate_codes<kPath>(sm, S, CC, A, k, m, active, cp, cm, ct.repairs, ct);
         return active && classify_codes(S, cp, cm, C.flags);
     }
     if (kPath == kPathExact) {
@@ -310,45 +345,83 @@ __device__ __forceinline__ bool candidate_pass(const Smem& sm, const SearchConst
         exact_linear(S, A, k, m, lp, lm);
         return active && exact_band(S, lp, lm, C.flags);
     }
-    float vp[3], vm[3];
+    const float r = __ldg(&A.radii_f[k]);
     const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + m);
-    fast_linear<kCubeOnly>(C, r, sc, vp, vm);
+    float dp[3], dm[3];
+    fast_linear<false>(C.fx0, C.fz0, C.mx, C.mz, C.cyc, r, sc, dp, dm);
     bool unsure;
-    bool pass = fast_band(C, vp, vm, unsure);
+    bool pass = fast_band(C, dp, dm, unsure);
     if (kPath == kPathAudit) {
         double lp[3], lm[3];
         exact_linear(S, A, k, m, lp, lm);
         const bool ex = exact_band(S, lp, lm, C.flags);
-        if (active && !unsure && ex != pass) ++violations;
-        if (active && unsure) ++repairs;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            const float eps = __ldg(&S->eps[q]);
-            max_ratio = fmaxf(max_ratio, static_cast<float>(fabs(static_cast<double>(vp[q]) - lp[q]) / eps));
-            max_ratio = fmaxf(max_ratio, static_cast<float>(fabs(static_cast<double>(vm[q]) - lm[q]) / eps));
+        if (active) {
+            ct.violations += !unsure && ex != pass;
+            ct.repairs += unsure;
+            float vp[3], vm[3];
+            fast_linear<false>(CC.fx0, CC.fz0, CC.mx, CC.mz, CC.cy, r, sc, vp, vm);
+            audit_ratio(S, vp, vm, lp, lm, ct.max_ratio);
         }
         return active && ex;
     }
-    if (__any_sync(kFull, unsure)) {
-        if (unsure) {
-            double lp[3], lm[3];
-            exact_linear(S, A, k, m, lp, lm);
-            pass = exact_band(S, lp, lm, C.flags);
-            if (active) ++repairs;
-        }
+    if (__any_sync(kFull, unsure) && unsure) {
+        double lp[3], lm[3];
+        exact_linear(S, A, k, m, lp, lm);
+        pass = exact_band(S, lp, lm, C.flags);
+        if (active) ++ct.repairs;
     }
     return active && pass;
 }
 
-// Decoupled look-back over the warp tiles (global canonical order).
+// Hot loop: FAST path, band mode, `nch` full 32-candidate chunks of radius
+// row k starting at angle m0 (na % 32 == 0 so chunks never straddle rows).
+// Per candidate: 1 LDG (L1-resident trig), 27 FMA-pipe + 7 ALU-pipe ops; the
+// vote below is taken only when some lane passes or is unsure.
+template <bool kCubeOnly>
+__device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
+                                         float r, uint32_t m0, uint32_t nch, uint32_t off, uint16_t* list,
+                                         uint32_t& cnt, Counters& ct, unsigned lane, unsigned lane_lt) {
+    const float2* tp = reinterpret_cast<const float2*>(A.trig_f) + m0 + lane;
+    uint32_t m = m0 + lane;
+    off += lane;
+    float2 next = __ldg(tp);
+#pragma unroll 2
+    for (uint32_t c = 0; c < nch; ++c) {
+        const float2 sc = next;
+        next = __ldg(tp + 32);  // prefetch; the table is padded by 64 entries
+        float dp[3], dm[3];
+        fast_linear<kCubeOnly>(C.fx0, C.fz0, C.mx, C.mz, C.cyc, r, sc, dp, dm);
+        bool unsure;
+        bool pass = fast_band(C, dp, dm, unsure);
+        if (__any_sync(kFull, pass | unsure)) {
+            if (unsure) {
+                double lp[3], lm[3];
+                exact_linear(S, A, k, m, lp, lm);
+                pass = exact_band(S, lp, lm, C.flags);
+                ++ct.repairs;
+            }
+            const unsigned b = __ballot_sync(kFull, pass);
+            if (pass) list[cnt + __popc(b & lane_lt)] = static_cast<uint16_t>(off);
+            cnt += __popc(b);
+        }
+        tp += 32;
+        m += 32;
+        off += 32;
+    }
+}
+
+// Decoupled look-back over the warp tiles (global canonical order).  Tile
+// status word: flag (2 bits: 1 aggregate, 2 inclusive prefix) << 62 | value.
+// Tiles are claimed in order from a ticket, so every predecessor belongs to a
+// running warp and the spin terminates.
 __device__ __forceinline__ unsigned long long lookback(unsigned long long* status, uint32_t t, uint32_t cnt,
-                                                       int lane) {
+                                                       unsigned lane) {
     if (lane == 0) st_relaxed(&status[t], (t == 0 ? kFlagPrefix : kFlagAgg) | cnt);
     if (t == 0) return 0;
     unsigned long long excl = 0;
     long long j = static_cast<long long>(t) - 1;
     while (true) {
-        const long long idx = j - lane;
+        const long long idx = j - static_cast<long long>(lane);
         const unsigned long long v = idx >= 0 ? ld_relaxed(&status[idx]) : kFlagPrefix;
         const unsigned flag = static_cast<unsigned>(v >> 62);
         const unsigned pmask = __ballot_sync(kFull, flag == 2);
@@ -359,7 +432,7 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* statu
             __nanosleep(64);
             continue;
         }
-        unsigned long long val = static_cast<unsigned>(lane) <= stop ? (v & kValueMask) : 0ull;
+        unsigned long long val = lane <= stop ? (v & kValueMask) : 0ull;
 #pragma unroll
         for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(kFull, val, o);
         excl += val;
@@ -379,13 +452,11 @@ __global__ void __launch_bounds__(kBlock, 3) search_kernel(const LaunchArgs A) {
     for (int i = threadIdx.x; i <= kGuessBuckets; i += kBlock) sm.guess[i] = A.guess[i];
     __syncthreads();
 
-    const int lane = threadIdx.x & 31;
+    const unsigned lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     uint16_t* list = sm.list[warp];
     const unsigned lane_lt = (1u << lane) - 1u;
-
-    unsigned long long repairs = 0, code_repairs = 0, violations = 0, mismatch = 0, overflow = 0;
-    float max_ratio = 0.f;
+    Counters ct;
 
     while (true) {
         uint32_t t = 0;
@@ -395,51 +466,43 @@ __global__ void __launch_bounds__(kBlock, 3) search_kernel(const LaunchArgs A) {
         const uint32_t s = t / A.tiles_per_search;
         const uint32_t lt = t - s * A.tiles_per_search;
         const SearchConst* S = A.sc + s;
-        Consts C;
-        load_consts(S, C);
         const uint32_t i0 = lt * static_cast<uint32_t>(kTile);
         const uint32_t i1 = min(i0 + static_cast<uint32_t>(kTile), A.cand_per_search);
 
         // ---------------- phase 1: decide every candidate of the tile -------
         uint32_t cnt = 0;
-        if (A.aligned) {
-            uint32_t k = div_na(i0, A);
-            uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
-            uint32_t i = i0;
-            while (i < i1) {
-                const uint32_t seg_end = min(i1, i + (static_cast<uint32_t>(A.na) - m0));
-                const float r = __ldg(&A.radii_f[k]);
-                const bool cube_only = r < C.rcube;
-                for (uint32_t base = i; base < seg_end; base += 32) {
-                    const uint32_t m = m0 + (base - i) + lane;
-                    bool pass;
-                    if (cube_only) {
-                        pass = candidate_pass<kMode, kPath, true>(sm, S, C, A, k, m, r, true, repairs,
-                                                                  violations, max_ratio);
+        {
+            Consts C;
+            load_consts(S, C);
+            if (kMode == kModeBand && kPath == kPathFast && A.aligned) {
+                uint32_t k = div_na(i0, A);
+                uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
+                uint32_t i = i0;
+                while (i < i1) {
+                    const uint32_t seg = min(i1 - i, static_cast<uint32_t>(A.na) - m0);
+                    const float r = __ldg(&A.radii_f[k]);
+                    if (r < C.rcube) {
+                        band_row<true>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, ct, lane, lane_lt);
                     } else {
-                        pass = candidate_pass<kMode, kPath, false>(sm, S, C, A, k, m, r, true, repairs,
-                                                                   violations, max_ratio);
+                        band_row<false>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, ct, lane, lane_lt);
                     }
+                    i += seg;
+                    m0 = 0;
+                    ++k;
+                }
+            } else {
+                CodeConsts CC;
+                load_code_consts(S, CC);
+                for (uint32_t base = i0; base < i1; base += 32) {
+                    const bool active = base + lane < i1;
+                    const uint32_t i = active ? base + lane : i1 - 1;
+                    const uint32_t k = div_na(i, A);
+                    const uint32_t m = i - k * static_cast<uint32_t>(A.na);
+                    const bool pass = candidate_pass<kMode, kPath>(sm, S, C, CC, A, k, m, active, ct);
                     const unsigned b = __ballot_sync(kFull, pass);
-                    if (pass) list[cnt + __popc(b & lane_lt)] = static_cast<uint16_t>(base - i0 + lane);
+                    if (pass) list[cnt + __popc(b & lane_lt)] = static_cast<uint16_t>(i - i0);
                     cnt += __popc(b);
                 }
-                i = seg_end;
-                m0 = 0;
-                ++k;
-            }
-        } else {
-            for (uint32_t base = i0; base < i1; base += 32) {
-                const bool active = base + lane < i1;
-                const uint32_t i = active ? base + lane : i1 - 1;
-                const uint32_t k = div_na(i, A);
-                const uint32_t m = i - k * static_cast<uint32_t>(A.na);
-                const float r = __ldg(&A.radii_f[k]);
-                const bool pass = candidate_pass<kMode, kPath, false>(sm, S, C, A, k, m, r, active, repairs,
-                                                                      violations, max_ratio);
-                const unsigned b = __ballot_sync(kFull, pass);
-                if (pass) list[cnt + __popc(b & lane_lt)] = static_cast<uint16_t>(i - i0);
-                cnt += __popc(b);
             }
         }
         __syncwarp();
@@ -456,11 +519,14 @@ __global__ void __launch_bounds__(kBlock, 3) search_kernel(const LaunchArgs A) {
         if (cnt == 0) continue;
         if (lane == 0) atomicAdd(&A.counts[s], static_cast<unsigned long long>(cnt));
         if (base_out + cnt > A.capacity) {
-            if (lane == 0) ++overflow;
+            if (lane == 0) ++ct.overflow;
             continue;
         }
 
         // ---------------- phase 2: codes + coalesced writes ----------------
+        const uint32_t flags = __ldg(&S->flags);
+        CodeConsts CC;
+        load_code_consts(S, CC);
         for (uint32_t p = 0; p < cnt; p += 32) {
             const uint32_t q = p + lane;
             const bool active = q < cnt;
@@ -468,9 +534,9 @@ __global__ void __launch_bounds__(kBlock, 3) search_kernel(const LaunchArgs A) {
             const uint32_t k = div_na(i, A);
             const uint32_t m = i - k * static_cast<uint32_t>(A.na);
             int cp[3], cm[3];
-            candidate_codes<kPath>(sm, S, C, A, k, m, active, cp, cm, code_repairs, violations, max_ratio);
+            candidate_codes<kPath>(sm, S, CC, A, k, m, active, cp, cm, ct.code_repairs, ct);
             if (active) {
-                if (kMode == kModeBand && !classify_codes(S, cp, cm, C.flags)) ++mismatch;
+                if (kMode == kModeBand && !classify_codes(S, cp, cm, flags)) ++ct.mismatch;
                 const unsigned long long o = base_out + q;
                 A.out_idx[o] = i;
                 uint16_t* c16 = reinterpret_cast<uint16_t*>(A.out_codes + 6 * o);
@@ -485,20 +551,20 @@ __global__ void __launch_bounds__(kBlock, 3) search_kernel(const LaunchArgs A) {
     // ---------------- statistics ---------------------------------------------
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-        repairs += __shfl_xor_sync(kFull, repairs, o);
-        code_repairs += __shfl_xor_sync(kFull, code_repairs, o);
-        violations += __shfl_xor_sync(kFull, violations, o);
-        mismatch += __shfl_xor_sync(kFull, mismatch, o);
-        overflow += __shfl_xor_sync(kFull, overflow, o);
-        max_ratio = fmaxf(max_ratio, __shfl_xor_sync(kFull, max_ratio, o));
+        ct.repairs += __shfl_xor_sync(kFull, ct.repairs, o);
+        ct.code_repairs += __shfl_xor_sync(kFull, ct.code_repairs, o);
+        ct.violations += __shfl_xor_sync(kFull, ct.violations, o);
+        ct.mismatch += __shfl_xor_sync(kFull, ct.mismatch, o);
+        ct.overflow += __shfl_xor_sync(kFull, ct.overflow, o);
+        ct.max_ratio = fmaxf(ct.max_ratio, __shfl_xor_sync(kFull, ct.max_ratio, o));
     }
     if (lane == 0) {
-        if (repairs) atomicAdd(&A.stats->band_repairs, repairs);
-        if (code_repairs) atomicAdd(&A.stats->code_repairs, code_repairs);
-        if (violations) atomicAdd(&A.stats->audit_violations, violations);
-        if (mismatch) atomicAdd(&A.stats->class_mismatch, mismatch);
-        if (overflow) atomicAdd(&A.stats->overflow, overflow);
-        if (max_ratio > 0.f) atomicMax(&A.stats->audit_max_ratio_bits, __float_as_uint(max_ratio));
+        if (ct.repairs) atomicAdd(&A.stats->band_repairs, ct.repairs);
+        if (ct.code_repairs) atomicAdd(&A.stats->code_repairs, ct.code_repairs);
+        if (ct.violations) atomicAdd(&A.stats->audit_violations, ct.violations);
+        if (ct.mismatch) atomicAdd(&A.stats->class_mismatch, ct.mismatch);
+        if (ct.overflow) atomicAdd(&A.stats->overflow, ct.overflow);
+        if (ct.max_ratio > 0.f) atomicMax(&A.stats->audit_max_ratio_bits, __float_as_uint(ct.max_ratio));
     }
 }
 

@@ -20,17 +20,19 @@ constexpr int kGuessBuckets = 4096;  // code-guess buckets over linear [0, 1]
 struct alignas(16) SearchConst {
     // --- FP32 fast path -------------------------------------------------
     float fx0;         // Fy + a/500   (fx of both endpoints = fx0 +- r*sin/500)
-    float fz0;         // Fy - b/200   (fz = fz0 -+ r*cos/200)
+    float fz0;         // Fz = Fy - b/200 (fz = fz0 -+ r*cos/200)
     float rcube;       // rows with r < rcube never leave the cube branch of f^-1
+    float eps_band;    // bound on |G32 - G| of the band statistic G (see cvg_kernels.cu)
     float mx[3];       // Minv[c][0] * wx
     float mz[3];       // Minv[c][2] * wz
     float cy[3];       // Minv[c][1] * wy * f^-1(Fy)
+    float cyc[3];      // cy - band centre: the matrix FFMAs then yield v - centre
+    float sg[3];       // +1 quiet channel (0 bit), -1 loud channel (1 bit)
+    float nsh[3];      // -sg * band half-width
     float eps[3];      // proven bound |lin32 - lin64| per channel (linear units)
-    float lo_p[3];     // band lower edge + eps
-    float lo_m[3];     // band lower edge - eps
-    float hi_p[3];     // band upper edge + eps
-    float hi_m[3];     // band upper edge - eps
     float eps_code[3]; // eps + float rounding of the code thresholds
+    float vbound;      // max |lin| over the grid (+1): stands in for infinite band edges
+    uint32_t reserved;
     uint32_t flags;    // bit c (c=0,1,2 -> r,g,b): loud channel (pattern bit set)
     int32_t t[3];      // target codes
     int32_t k1;        // d > v_th   <=> d >= k1 (integer deltas); 256 = never
