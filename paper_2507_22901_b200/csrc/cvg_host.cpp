@@ -462,6 +462,7 @@ struct cvg_plan {
     size_t work_bytes = 0;
     void* d_first = nullptr;
     size_t first_bytes = 0;
+    void* d_scratch = nullptr;
     void* d_out_idx = nullptr;
     void* d_out_codes = nullptr;
     uint64_t capacity = 0;
@@ -607,19 +608,34 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     A.na_magic = p->na > 1 ? (UINT64_MAX / static_cast<uint64_t>(p->na)) + 1 : 0;
     A.n_tiles = n_tiles;
 
-    // ---- per-run workspace: status[n_tiles] | ticket | counts[n] | stats ----
+    // ---- per-run workspace --------------------------------------------------
+    // zeroed each run:  status[n_scan_blocks] | tickets[4] | counts[n] | stats
+    // written each run: tile_count[n_tiles] | tile_base[n_tiles] | total   (PAIRS)
+    const bool pairs = p->out == cvg::kOutPairs;
+    const uint64_t scan_blocks = pairs ? (n_tiles + cvg::kScanTile - 1) / cvg::kScanTile : 0;
     Layout W;
-    const size_t o_st = W.take(sizeof(unsigned long long) * (p->out == cvg::kOutPairs ? n_tiles : 0));
-    const size_t o_tk = W.take(sizeof(unsigned int));
+    const size_t o_st = W.take(sizeof(unsigned long long) * scan_blocks);
+    const size_t o_tk = W.take(sizeof(unsigned int) * 4);
     const size_t o_ct = W.take(sizeof(unsigned long long) * p->n);
     const size_t o_ss = W.take(sizeof(cvg::Stats));
-    p->work_bytes = W.off;
-    p->d_work = ctx->dev.alloc(p->work_bytes);
+    p->work_bytes = W.off;  // memset span
+    const size_t o_tc = W.take(sizeof(uint32_t) * (pairs ? n_tiles : 0));
+    const size_t o_tb = W.take(sizeof(unsigned long long) * (pairs ? n_tiles : 0));
+    const size_t o_to = W.take(sizeof(unsigned long long));
+    p->d_work = ctx->dev.alloc(W.off);
     if (!p->d_work) return fail(CVG_ENOMEM, "device allocation of the workspace failed");
     A.status = at<unsigned long long>(p->d_work, o_st);
     A.ticket = at<unsigned int>(p->d_work, o_tk);
     A.counts = at<unsigned long long>(p->d_work, o_ct);
     A.stats = at<cvg::Stats>(p->d_work, o_ss);
+    A.tile_count = at<uint32_t>(p->d_work, o_tc);
+    A.tile_base = at<unsigned long long>(p->d_work, o_tb);
+    A.total = at<unsigned long long>(p->d_work, o_to);
+    if (pairs) {
+        p->d_scratch = ctx->dev.alloc(static_cast<size_t>(n_tiles) * cvg::kTile * sizeof(uint16_t));
+        if (!p->d_scratch) return fail(CVG_ENOMEM, "device allocation of the tile lists failed");
+        A.scratch = static_cast<uint16_t*>(p->d_scratch);
+    }
     if (p->out == cvg::kOutFirst) {
         Layout F;
         const size_t o_fi = F.take(sizeof(uint32_t) * p->n);
@@ -660,6 +676,7 @@ void plan_release(cvg_plan* p) {
     p->ctx->dev.release(p->d_const);
     p->ctx->dev.release(p->d_work);
     p->ctx->dev.release(p->d_first);
+    p->ctx->dev.release(p->d_scratch);
     if (p->ev0) cudaEventDestroy(p->ev0);
     if (p->ev1) cudaEventDestroy(p->ev1);
 }
@@ -908,7 +925,7 @@ uint64_t cvg_plan_input_bytes(const cvg_plan* p) { return p ? p->input_bytes : 0
 
 int cvg_plan_launches(const cvg_plan* p) {
     if (!p || p->empty) return 0;
-    return p->out == cvg::kOutFirst ? 2 : 1;
+    return p->out == cvg::kOutPairs ? 3 : p->out == cvg::kOutFirst ? 2 : 1;
 }
 
 uint64_t cvg_plan_candidates(const cvg_plan* p) { return p ? p->candidates : 0; }

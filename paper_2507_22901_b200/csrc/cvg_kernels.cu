@@ -254,17 +254,44 @@ __device__ __forceinline__ int code_fast(float x, float E, const float* tf, cons
     return c;
 }
 
+// Shared tables: exact and float quantization thresholds + code guesses.
 struct Smem {
-    uint16_t list[kWarpsPerBlock][kTile];
     double thr_d[256];
     float thr_f[258];  // [0] = -inf, [c] = float(thr[c]), [256] = +inf
     uint8_t guess[kGuessBuckets + 16];
 };
 
+__device__ __forceinline__ void load_tables(Smem& sm, const LaunchArgs& A) {
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sm.thr_d[i] = A.thr_d[i];
+    for (int i = threadIdx.x; i < 258; i += blockDim.x) sm.thr_f[i] = A.thr_f[i];
+    for (int i = threadIdx.x; i <= kGuessBuckets; i += blockDim.x) sm.guess[i] = A.guess[i];
+    __syncthreads();
+}
+
 struct Counters {
     unsigned long long repairs = 0, code_repairs = 0, violations = 0, mismatch = 0, overflow = 0;
     float max_ratio = 0.f;
 };
+
+__device__ __forceinline__ void flush_counters(Counters& ct, const LaunchArgs& A, unsigned lane) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        ct.repairs += __shfl_xor_sync(kFull, ct.repairs, o);
+        ct.code_repairs += __shfl_xor_sync(kFull, ct.code_repairs, o);
+        ct.violations += __shfl_xor_sync(kFull, ct.violations, o);
+        ct.mismatch += __shfl_xor_sync(kFull, ct.mismatch, o);
+        ct.overflow += __shfl_xor_sync(kFull, ct.overflow, o);
+        ct.max_ratio = fmaxf(ct.max_ratio, __shfl_xor_sync(kFull, ct.max_ratio, o));
+    }
+    if (lane == 0) {
+        if (ct.repairs) atomicAdd(&A.stats->band_repairs, ct.repairs);
+        if (ct.code_repairs) atomicAdd(&A.stats->code_repairs, ct.code_repairs);
+        if (ct.violations) atomicAdd(&A.stats->audit_violations, ct.violations);
+        if (ct.mismatch) atomicAdd(&A.stats->class_mismatch, ct.mismatch);
+        if (ct.overflow) atomicAdd(&A.stats->overflow, ct.overflow);
+        if (ct.max_ratio > 0.f) atomicMax(&A.stats->audit_max_ratio_bits, __float_as_uint(ct.max_ratio));
+    }
+}
 
 __device__ __forceinline__ void audit_ratio(const SearchConst* S, const float* vp, const float* vm, const double* lp,
                                             const double* lm, float& max_ratio) {
@@ -373,14 +400,30 @@ __device__ __forceinline__ bool candidate_pass(const Smem& sm, const SearchConst
     return active && pass;
 }
 
+// Appends the passing lanes of one 32-candidate chunk to the tile's list
+// (PAIRS: ordered offsets in global scratch; FIRST: remembers the first).
+template <int kOut>
+__device__ __forceinline__ void append(bool pass, uint32_t off, uint16_t* list, uint32_t& cnt, uint32_t& first,
+                                       unsigned lane_lt) {
+    const unsigned b = __ballot_sync(kFull, pass);
+    if (kOut == kOutPairs) {
+        if (pass) list[cnt + __popc(b & lane_lt)] = static_cast<uint16_t>(off);
+    } else if (kOut == kOutFirst) {
+        if (cnt == 0 && b) first = __shfl_sync(kFull, off, __ffs(b) - 1);
+    }
+    cnt += __popc(b);
+}
+
 // Hot loop: FAST path, band mode, `nch` full 32-candidate chunks of radius
 // row k starting at angle m0 (na % 32 == 0 so chunks never straddle rows).
-// Per candidate: 1 LDG (L1-resident trig), 27 FMA-pipe + 7 ALU-pipe ops; the
-// vote below is taken only when some lane passes or is unsure.
-template <bool kCubeOnly>
+// Per candidate: 1 LDG (L1-resident trig, prefetched one chunk ahead),
+// 27 FMA-pipe + 7 ALU-pipe ops; the vote branch is taken only when some lane
+// passes or is unsure.
+template <bool kCubeOnly, int kOut>
 __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
                                          float r, uint32_t m0, uint32_t nch, uint32_t off, uint16_t* list,
-                                         uint32_t& cnt, Counters& ct, unsigned lane, unsigned lane_lt) {
+                                         uint32_t& cnt, uint32_t& first, Counters& ct, unsigned lane,
+                                         unsigned lane_lt) {
     const float2* tp = reinterpret_cast<const float2*>(A.trig_f) + m0 + lane;
     uint32_t m = m0 + lane;
     off += lane;
@@ -400,9 +443,7 @@ __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, 
                 pass = exact_band(S, lp, lm, C.flags);
                 ++ct.repairs;
             }
-            const unsigned b = __ballot_sync(kFull, pass);
-            if (pass) list[cnt + __popc(b & lane_lt)] = static_cast<uint16_t>(off);
-            cnt += __popc(b);
+            append<kOut>(pass, off, list, cnt, first, lane_lt);
         }
         tp += 32;
         m += 32;
@@ -410,162 +451,199 @@ __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, 
     }
 }
 
-// Decoupled look-back over the warp tiles (global canonical order).  Tile
-// status word: flag (2 bits: 1 aggregate, 2 inclusive prefix) << 62 | value.
-// Tiles are claimed in order from a ticket, so every predecessor belongs to a
-// running warp and the spin terminates.
-__device__ __forceinline__ unsigned long long lookback(unsigned long long* status, uint32_t t, uint32_t cnt,
-                                                       unsigned lane) {
-    if (lane == 0) st_relaxed(&status[t], (t == 0 ? kFlagPrefix : kFlagAgg) | cnt);
-    if (t == 0) return 0;
-    unsigned long long excl = 0;
-    long long j = static_cast<long long>(t) - 1;
-    while (true) {
-        const long long idx = j - static_cast<long long>(lane);
-        const unsigned long long v = idx >= 0 ? ld_relaxed(&status[idx]) : kFlagPrefix;
-        const unsigned flag = static_cast<unsigned>(v >> 62);
-        const unsigned pmask = __ballot_sync(kFull, flag == 2);
-        const unsigned zmask = __ballot_sync(kFull, flag == 0);
-        const unsigned stop = pmask ? static_cast<unsigned>(__ffs(pmask) - 1) : 31u;
-        const unsigned need = stop == 31u ? kFull : ((2u << stop) - 1u);
-        if (zmask & need) {
-            __nanosleep(64);
-            continue;
-        }
-        unsigned long long val = lane <= stop ? (v & kValueMask) : 0ull;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(kFull, val, o);
-        excl += val;
-        if (pmask) break;
-        j -= 32;
-    }
-    if (lane == 0) st_relaxed(&status[t], kFlagPrefix | (excl + cnt));
-    return excl;
-}
-
+// K1: decide every candidate.  Warps claim 2048-candidate tiles (contiguous
+// canonical ranges of one search) from a ticket, prefetching the next ticket.
+// PAIRS: tile count + ordered passing offsets to scratch; COUNTS: per-search
+// counts; FIRST: counts + first passing index.
 template <int kMode, int kOut, int kPath>
-__global__ void __launch_bounds__(kBlock, 3) search_kernel(const LaunchArgs A) {
+__global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    for (int i = threadIdx.x; i < 256; i += kBlock) sm.thr_d[i] = A.thr_d[i];
-    for (int i = threadIdx.x; i < 258; i += kBlock) sm.thr_f[i] = A.thr_f[i];
-    for (int i = threadIdx.x; i <= kGuessBuckets; i += kBlock) sm.guess[i] = A.guess[i];
-    __syncthreads();
-
+    load_tables(sm, A);
     const unsigned lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    uint16_t* list = sm.list[warp];
     const unsigned lane_lt = (1u << lane) - 1u;
     Counters ct;
 
-    while (true) {
-        uint32_t t = 0;
-        if (lane == 0) t = atomicAdd(A.ticket, 1u);
-        t = __shfl_sync(kFull, t, 0);
-        if (t >= A.n_tiles) break;
+    uint32_t t_claim = 0;
+    if (lane == 0) t_claim = atomicAdd(&A.ticket[0], 1u);
+    uint32_t t = __shfl_sync(kFull, t_claim, 0);
+    while (t < A.n_tiles) {
+        if (lane == 0) t_claim = atomicAdd(&A.ticket[0], 1u);  // next tile, consumed at the end
         const uint32_t s = t / A.tiles_per_search;
         const uint32_t lt = t - s * A.tiles_per_search;
         const SearchConst* S = A.sc + s;
         const uint32_t i0 = lt * static_cast<uint32_t>(kTile);
         const uint32_t i1 = min(i0 + static_cast<uint32_t>(kTile), A.cand_per_search);
-
-        // ---------------- phase 1: decide every candidate of the tile -------
-        uint32_t cnt = 0;
-        {
-            Consts C;
-            load_consts(S, C);
-            if (kMode == kModeBand && kPath == kPathFast && A.aligned) {
-                uint32_t k = div_na(i0, A);
-                uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
-                uint32_t i = i0;
-                while (i < i1) {
-                    const uint32_t seg = min(i1 - i, static_cast<uint32_t>(A.na) - m0);
-                    const float r = __ldg(&A.radii_f[k]);
-                    if (r < C.rcube) {
-                        band_row<true>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, ct, lane, lane_lt);
-                    } else {
-                        band_row<false>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, ct, lane, lane_lt);
-                    }
-                    i += seg;
-                    m0 = 0;
-                    ++k;
+        uint16_t* list = kOut == kOutPairs ? A.scratch + static_cast<size_t>(t) * kTile : nullptr;
+        uint32_t cnt = 0, first = 0;
+        Consts C;
+        load_consts(S, C);
+        if (kMode == kModeBand && kPath == kPathFast && A.aligned) {
+            uint32_t k = div_na(i0, A);
+            uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
+            uint32_t i = i0;
+            while (i < i1) {
+                const uint32_t seg = min(i1 - i, static_cast<uint32_t>(A.na) - m0);
+                const float r = __ldg(&A.radii_f[k]);
+                if (r < C.rcube) {
+                    band_row<true, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);
+                } else {
+                    band_row<false, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);
                 }
-            } else {
-                CodeConsts CC;
-                load_code_consts(S, CC);
-                for (uint32_t base = i0; base < i1; base += 32) {
-                    const bool active = base + lane < i1;
-                    const uint32_t i = active ? base + lane : i1 - 1;
-                    const uint32_t k = div_na(i, A);
-                    const uint32_t m = i - k * static_cast<uint32_t>(A.na);
-                    const bool pass = candidate_pass<kMode, kPath>(sm, S, C, CC, A, k, m, active, ct);
-                    const unsigned b = __ballot_sync(kFull, pass);
-                    if (pass) list[cnt + __popc(b & lane_lt)] = static_cast<uint16_t>(i - i0);
-                    cnt += __popc(b);
-                }
+                i += seg;
+                m0 = 0;
+                ++k;
+            }
+        } else {
+            CodeConsts CC;
+            load_code_consts(S, CC);
+            for (uint32_t base = i0; base < i1; base += 32) {
+                const bool active = base + lane < i1;
+                const uint32_t i = active ? base + lane : i1 - 1;
+                const uint32_t k = div_na(i, A);
+                const uint32_t m = i - k * static_cast<uint32_t>(A.na);
+                const bool pass = candidate_pass<kMode, kPath>(sm, S, C, CC, A, k, m, active, ct);
+                append<kOut>(pass, i - i0, list, cnt, first, lane_lt);
             }
         }
-        __syncwarp();
-
-        // ---------------- publish -------------------------------------------
-        if (kOut == kOutCounts || kOut == kOutFirst) {
-            if (lane == 0 && cnt) {
-                atomicAdd(&A.counts[s], static_cast<unsigned long long>(cnt));
-                if (kOut == kOutFirst) atomicMin(&A.first_idx[s], i0 + list[0]);
-            }
-            continue;
+        if (lane == 0) {
+            if (kOut == kOutPairs) A.tile_count[t] = cnt;
+            if (cnt) atomicAdd(&A.counts[s], static_cast<unsigned long long>(cnt));
+            if (kOut == kOutFirst && cnt) atomicMin(&A.first_idx[s], i0 + first);
         }
-        const unsigned long long base_out = lookback(A.status, t, cnt, lane);
-        if (cnt == 0) continue;
-        if (lane == 0) atomicAdd(&A.counts[s], static_cast<unsigned long long>(cnt));
-        if (base_out + cnt > A.capacity) {
-            if (lane == 0) ++ct.overflow;
-            continue;
-        }
-
-        // ---------------- phase 2: codes + coalesced writes ----------------
-        const uint32_t flags = __ldg(&S->flags);
-        CodeConsts CC;
-        load_code_consts(S, CC);
-        for (uint32_t p = 0; p < cnt; p += 32) {
-            const uint32_t q = p + lane;
-            const bool active = q < cnt;
-            const uint32_t i = i0 + list[active ? q : 0];
-            const uint32_t k = div_na(i, A);
-            const uint32_t m = i - k * static_cast<uint32_t>(A.na);
-            int cp[3], cm[3];
-            candidate_codes<kPath>(sm, S, CC, A, k, m, active, cp, cm, ct.code_repairs, ct);
-            if (active) {
-                if (kMode == kModeBand && !classify_codes(S, cp, cm, flags)) ++ct.mismatch;
-                const unsigned long long o = base_out + q;
-                A.out_idx[o] = i;
-                uint16_t* c16 = reinterpret_cast<uint16_t*>(A.out_codes + 6 * o);
-                c16[0] = static_cast<uint16_t>(cp[0] | (cp[1] << 8));
-                c16[1] = static_cast<uint16_t>(cp[2] | (cm[0] << 8));
-                c16[2] = static_cast<uint16_t>(cm[1] | (cm[2] << 8));
-            }
-        }
-        __syncwarp();
+        t = __shfl_sync(kFull, t_claim, 0);
     }
+    flush_counters(ct, A, lane);
+}
 
-    // ---------------- statistics ---------------------------------------------
+// K2: exclusive scan of tile_count -> tile_base (single pass, chained scan
+// with decoupled look-back over kScanTile-tile blocks claimed from a ticket).
+__global__ void __launch_bounds__(kBlock) scan_kernel(const LaunchArgs A) {
+    __shared__ uint32_t s_block;
+    __shared__ unsigned long long s_warp[kWarpsPerBlock];
+    __shared__ unsigned long long s_prefix;
+    if (threadIdx.x == 0) s_block = atomicAdd(&A.ticket[1], 1u);
+    __syncthreads();
+    const uint32_t b = s_block;
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t base = static_cast<uint64_t>(b) * kScanTile + static_cast<uint64_t>(threadIdx.x) * kScanItems;
+    uint32_t v[kScanItems];
+    unsigned long long sum = 0;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        ct.repairs += __shfl_xor_sync(kFull, ct.repairs, o);
-        ct.code_repairs += __shfl_xor_sync(kFull, ct.code_repairs, o);
-        ct.violations += __shfl_xor_sync(kFull, ct.violations, o);
-        ct.mismatch += __shfl_xor_sync(kFull, ct.mismatch, o);
-        ct.overflow += __shfl_xor_sync(kFull, ct.overflow, o);
-        ct.max_ratio = fmaxf(ct.max_ratio, __shfl_xor_sync(kFull, ct.max_ratio, o));
+    for (int j = 0; j < kScanItems; ++j) {
+        v[j] = base + j < A.n_tiles ? A.tile_count[base + j] : 0u;
+        sum += v[j];
     }
-    if (lane == 0) {
-        if (ct.repairs) atomicAdd(&A.stats->band_repairs, ct.repairs);
-        if (ct.code_repairs) atomicAdd(&A.stats->code_repairs, ct.code_repairs);
-        if (ct.violations) atomicAdd(&A.stats->audit_violations, ct.violations);
-        if (ct.mismatch) atomicAdd(&A.stats->class_mismatch, ct.mismatch);
-        if (ct.overflow) atomicAdd(&A.stats->overflow, ct.overflow);
-        if (ct.max_ratio > 0.f) atomicMax(&A.stats->audit_max_ratio_bits, __float_as_uint(ct.max_ratio));
+    unsigned long long incl = sum;  // warp inclusive scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= static_cast<unsigned>(o)) incl += y;
     }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    unsigned long long warp_off = 0, block_sum = 0;
+    for (int w = 0; w < kWarpsPerBlock; ++w) {
+        if (w < static_cast<int>(warp)) warp_off += s_warp[w];
+        block_sum += s_warp[w];
+    }
+    if (warp == 0) {
+        unsigned long long excl = 0;
+        if (b == 0) {
+            if (lane == 0) st_relaxed(&A.status[0], kFlagPrefix | block_sum);
+        } else {
+            if (lane == 0) st_relaxed(&A.status[b], kFlagAgg | block_sum);
+            long long j = static_cast<long long>(b) - 1;
+            while (true) {
+                const long long idx = j - static_cast<long long>(lane);
+                const unsigned long long w = idx >= 0 ? ld_relaxed(&A.status[idx]) : kFlagPrefix;
+                const unsigned flag = static_cast<unsigned>(w >> 62);
+                const unsigned pmask = __ballot_sync(kFull, flag == 2);
+                const unsigned zmask = __ballot_sync(kFull, flag == 0);
+                const unsigned stop = pmask ? static_cast<unsigned>(__ffs(pmask) - 1) : 31u;
+                const unsigned need = stop == 31u ? kFull : ((2u << stop) - 1u);
+                if (zmask & need) {
+                    __nanosleep(32);
+                    continue;
+                }
+                unsigned long long val = lane <= stop ? (w & kValueMask) : 0ull;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) val += __shfl_xor_sync(kFull, val, o);
+                excl += val;
+                if (pmask) break;
+                j -= 32;
+            }
+            if (lane == 0) st_relaxed(&A.status[b], kFlagPrefix | (excl + block_sum));
+        }
+        if (lane == 0) s_prefix = excl;
+    }
+    __syncthreads();
+    unsigned long long run = s_prefix + warp_off + (incl - sum);
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        if (base + j < A.n_tiles) A.tile_base[base + j] = run;
+        run += v[j];
+    }
+    if (base < A.n_tiles && base + kScanItems >= A.n_tiles) *A.total = run;
+}
+
+// K3: codes + coalesced writes of every passing pair at its final offset.
+// Warps claim groups of 32 tiles; lanes read the group's counts/bases once.
+template <int kMode, int kPath>
+__global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    load_tables(sm, A);
+    const unsigned lane = threadIdx.x & 31;
+    Counters ct;
+    while (true) {
+        uint32_t g = 0;
+        if (lane == 0) g = atomicAdd(&A.ticket[2], 1u);
+        g = __shfl_sync(kFull, g, 0);
+        const uint64_t t0 = static_cast<uint64_t>(g) * 32;
+        if (t0 >= A.n_tiles) break;
+        const uint64_t tl = t0 + lane;
+        const uint32_t my_cnt = tl < A.n_tiles ? A.tile_count[tl] : 0u;
+        const unsigned long long my_base = tl < A.n_tiles ? A.tile_base[tl] : 0ull;
+        unsigned todo = __ballot_sync(kFull, my_cnt != 0);
+        while (todo) {
+            const int j = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint32_t t = static_cast<uint32_t>(t0) + j;
+            const uint32_t cnt = __shfl_sync(kFull, my_cnt, j);
+            const unsigned long long base = __shfl_sync(kFull, my_base, j);
+            if (base + cnt > A.capacity) {
+                if (lane == 0) ++ct.overflow;
+                continue;
+            }
+            const uint32_t s = t / A.tiles_per_search;
+            const uint32_t i0 = (t - s * A.tiles_per_search) * static_cast<uint32_t>(kTile);
+            const SearchConst* S = A.sc + s;
+            const uint32_t flags = __ldg(&S->flags);
+            CodeConsts CC;
+            load_code_consts(S, CC);
+            const uint16_t* list = A.scratch + static_cast<size_t>(t) * kTile;
+            for (uint32_t p = 0; p < cnt; p += 32) {
+                const uint32_t q = p + lane;
+                const bool active = q < cnt;
+                const uint32_t i = i0 + list[active ? q : 0];
+                const uint32_t k = div_na(i, A);
+                const uint32_t m = i - k * static_cast<uint32_t>(A.na);
+                int cp[3], cm[3];
+                candidate_codes<kPath>(sm, S, CC, A, k, m, active, cp, cm, ct.code_repairs, ct);
+                if (active) {
+                    if (kMode == kModeBand && !classify_codes(S, cp, cm, flags)) ++ct.mismatch;
+                    const unsigned long long o = base + q;
+                    A.out_idx[o] = i;
+                    uint16_t* c16 = reinterpret_cast<uint16_t*>(A.out_codes + 6 * o);
+                    c16[0] = static_cast<uint16_t>(cp[0] | (cp[1] << 8));
+                    c16[1] = static_cast<uint16_t>(cp[2] | (cm[0] << 8));
+                    c16[2] = static_cast<uint16_t>(cm[1] | (cm[2] << 8));
+                }
+            }
+        }
+    }
+    flush_counters(ct, A, lane);
 }
 
 // FIRST mode epilogue: exact codes of each search's first canonical pair.
@@ -608,25 +686,33 @@ __global__ void ffma_peak_kernel(float* out, int iters, float a, float b) {
 
 template <int kMode, int kOut, int kPath>
 cudaError_t launch_t(const LaunchArgs& a, int grid, cudaStream_t st) {
-    // The dynamic shared-memory opt-in is set by occupancy_t (plan creation).
-    search_kernel<kMode, kOut, kPath><<<grid, kBlock, sizeof(Smem), st>>>(a);
+    // The dynamic shared-memory sizes are opted into by occupancy_t (plan creation).
+    phase1_kernel<kMode, kOut, kPath><<<grid, kBlock, sizeof(Smem), st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || kOut != kOutPairs) return e;
+    const unsigned scan_blocks = static_cast<unsigned>((a.n_tiles + kScanTile - 1) / kScanTile);
+    scan_kernel<<<scan_blocks, kBlock, 0, st>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    emit_kernel<kMode, kPath><<<grid, kBlock, sizeof(Smem), st>>>(a);
     return cudaGetLastError();
 }
 
 template <int kMode, int kOut, int kPath>
 int occupancy_t() {
-    auto fn = search_kernel<kMode, kOut, kPath>;
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Smem)));
+    auto f1 = phase1_kernel<kMode, kOut, kPath>;
+    auto f3 = emit_kernel<kMode, kPath>;
+    cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Smem)));
+    cudaFuncSetAttribute(f3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Smem)));
     int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kBlock, sizeof(Smem)) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f1, kBlock, sizeof(Smem)) != cudaSuccess) return 0;
     return blocks;
 }
 
 using LaunchFn = cudaError_t (*)(const LaunchArgs&, int, cudaStream_t);
 using OccFn = int (*)();
 
-#define CVG_ROW(M, P) \
-    {launch_t<M, kOutPairs, P>, launch_t<M, kOutCounts, P>, launch_t<M, kOutFirst, P>}
+#define CVG_ROW(M, P) {launch_t<M, kOutPairs, P>, launch_t<M, kOutCounts, P>, launch_t<M, kOutFirst, P>}
 #define CVG_OCC(M, P) {occupancy_t<M, kOutPairs, P>, occupancy_t<M, kOutCounts, P>, occupancy_t<M, kOutFirst, P>}
 
 const LaunchFn kLaunch[2][3][3] = {

@@ -13,6 +13,8 @@ constexpr int kTile = 2048;
 constexpr int kWarpsPerBlock = 8;
 constexpr int kBlock = 32 * kWarpsPerBlock;
 constexpr int kGuessBuckets = 4096;  // code-guess buckets over linear [0, 1]
+constexpr int kScanItems = 8;        // tile counts per thread in the offset scan
+constexpr int kScanTile = kBlock * kScanItems;
 
 // Per-search constants, one 256-byte record per (target, pattern, thresholds).
 // The FP32 half feeds the fast path; the FP64 half is the bit-exact restatement
@@ -78,9 +80,13 @@ struct LaunchArgs {
     uint32_t cand_per_search;  // nr * na (< 2^32)
     uint64_t na_magic;         // ceil(2^64 / na): k = umul64hi(i, na_magic)
     uint64_t n_tiles;
-    unsigned long long* status;  // [n_tiles] look-back words (flag << 62 | value)
-    unsigned int* ticket;        // dynamic tile counter
-    unsigned long long* counts;  // [n_searches]
+    unsigned long long* status;    // [n_scan_blocks] chained-scan status words (flag << 62 | value)
+    unsigned int* ticket;          // [4]: phase-1 tiles, scan blocks, emit tile groups
+    unsigned long long* counts;    // [n_searches]
+    uint32_t* tile_count;          // [n_tiles] passing candidates per tile (PAIRS)
+    unsigned long long* tile_base; // [n_tiles] exclusive prefix of tile_count (PAIRS)
+    uint16_t* scratch;             // [n_tiles * kTile] per-tile passing offsets (PAIRS)
+    unsigned long long* total;     // [1] sum of tile_count (PAIRS)
     uint32_t* out_idx;           // [capacity]
     uint8_t* out_codes;          // [capacity * 6]
     uint64_t capacity;
