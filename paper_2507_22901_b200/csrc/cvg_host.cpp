@@ -545,8 +545,8 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     for (int s = 0; s < p->n; ++s) make_search_const(d, s, rmax, p->mode, T, sc[s]);
     std::vector<float> radii_f(p->nr);
     for (int k = 0; k < p->nr; ++k) radii_f[k] = static_cast<float>(d->radii[k]);
-    // float trig table padded by 64 entries: the hot loop prefetches one chunk ahead
-    std::vector<float> trig_f(2 * (static_cast<size_t>(p->na) + 64), 0.0f);
+    // float trig table padded by 128 entries: the hot loop prefetches two chunks ahead
+    std::vector<float> trig_f(2 * (static_cast<size_t>(p->na) + 128), 0.0f);
     std::vector<double> trig_d(2 * static_cast<size_t>(p->na));
     for (int j = 0; j < p->na; ++j) {  // search.cpp:414-419
         const double sn = std::sin(d->angles[j]);
@@ -622,6 +622,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     const size_t o_tc = W.take(sizeof(uint32_t) * (pairs ? n_tiles : 0));
     const size_t o_tb = W.take(sizeof(unsigned long long) * (pairs ? n_tiles : 0));
     const size_t o_to = W.take(sizeof(unsigned long long));
+    const size_t o_wl = W.take(sizeof(uint32_t) * (pairs ? n_tiles : 0));
     p->d_work = ctx->dev.alloc(W.off);
     if (!p->d_work) return fail(CVG_ENOMEM, "device allocation of the workspace failed");
     A.status = at<unsigned long long>(p->d_work, o_st);
@@ -631,6 +632,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     A.tile_count = at<uint32_t>(p->d_work, o_tc);
     A.tile_base = at<unsigned long long>(p->d_work, o_tb);
     A.total = at<unsigned long long>(p->d_work, o_to);
+    A.worklist = at<uint32_t>(p->d_work, o_wl);
     if (pairs) {
         p->d_scratch = ctx->dev.alloc(static_cast<size_t>(n_tiles) * cvg::kTile * sizeof(uint16_t));
         if (!p->d_scratch) return fail(CVG_ENOMEM, "device allocation of the tile lists failed");

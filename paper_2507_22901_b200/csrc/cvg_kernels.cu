@@ -414,40 +414,71 @@ __device__ __forceinline__ void append(bool pass, uint32_t off, uint16_t* list, 
     cnt += __popc(b);
 }
 
+// Slow path of one chunk (some lane passes or is unsure): FP64 repair of the
+// unsure lanes, then the ordered append.
+template <int kOut>
+__device__ __forceinline__ void band_settle(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
+                                            uint32_t m, float G, uint32_t off, uint16_t* list, uint32_t& cnt,
+                                            uint32_t& first, Counters& ct, unsigned lane_lt) {
+    bool pass = G < -C.eps_band;
+    if (fabsf(G) <= C.eps_band) {
+        double lp[3], lm[3];
+        exact_linear(S, A, k, m, lp, lm);
+        pass = exact_band(S, lp, lm, C.flags);
+        ++ct.repairs;
+    }
+    append<kOut>(pass, off, list, cnt, first, lane_lt);
+}
+
+// Band statistic G of one candidate (see fast_band).
+template <bool kCubeOnly>
+__device__ __forceinline__ float band_g(const Consts& C, float r, float2 sc) {
+    float dp[3], dm[3];
+    fast_linear<kCubeOnly>(C.fx0, C.fz0, C.mx, C.mz, C.cyc, r, sc, dp, dm);
+    float G = 0.f;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const float M = fmaxf(fabsf(dp[q]), fabsf(dm[q]));
+        const float g = fmaf(C.sg[q], M, C.nsh[q]);
+        G = q == 0 ? g : fmaxf(G, g);
+    }
+    return G;
+}
+
 // Hot loop: FAST path, band mode, `nch` full 32-candidate chunks of radius
 // row k starting at angle m0 (na % 32 == 0 so chunks never straddle rows).
-// Per candidate: 1 LDG (L1-resident trig, prefetched one chunk ahead),
-// 27 FMA-pipe + 7 ALU-pipe ops; the vote branch is taken only when some lane
-// passes or is unsure.
+// Two chunks per iteration share one vote (ILP across chunks); per
+// candidate: 1 LDG (L1-resident trig, prefetched two chunks ahead), 27 FMA-
+// pipe + 5 ALU-pipe ops + 1 compare.  A candidate needs attention only when
+// G <= eps (passes, or sits inside the error bound), which is rare.
 template <bool kCubeOnly, int kOut>
 __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
                                          float r, uint32_t m0, uint32_t nch, uint32_t off, uint16_t* list,
                                          uint32_t& cnt, uint32_t& first, Counters& ct, unsigned lane,
                                          unsigned lane_lt) {
     const float2* tp = reinterpret_cast<const float2*>(A.trig_f) + m0 + lane;
+    const float eps = C.eps_band;
     uint32_t m = m0 + lane;
     off += lane;
-    float2 next = __ldg(tp);
-#pragma unroll 2
-    for (uint32_t c = 0; c < nch; ++c) {
-        const float2 sc = next;
-        next = __ldg(tp + 32);  // prefetch; the table is padded by 64 entries
-        float dp[3], dm[3];
-        fast_linear<kCubeOnly>(C.fx0, C.fz0, C.mx, C.mz, C.cyc, r, sc, dp, dm);
-        bool unsure;
-        bool pass = fast_band(C, dp, dm, unsure);
-        if (__any_sync(kFull, pass | unsure)) {
-            if (unsure) {
-                double lp[3], lm[3];
-                exact_linear(S, A, k, m, lp, lm);
-                pass = exact_band(S, lp, lm, C.flags);
-                ++ct.repairs;
-            }
-            append<kOut>(pass, off, list, cnt, first, lane_lt);
+    float2 na_ = __ldg(tp), nb_ = __ldg(tp + 32);
+    uint32_t c = 0;
+    for (; c + 2 <= nch; c += 2) {
+        const float2 sa = na_, sb = nb_;
+        na_ = __ldg(tp + 64);  // prefetch; the table is padded by 64 entries
+        nb_ = __ldg(tp + 96);
+        const float Ga = band_g<kCubeOnly>(C, r, sa);
+        const float Gb = band_g<kCubeOnly>(C, r, sb);
+        if (__any_sync(kFull, (Ga <= eps) | (Gb <= eps))) {
+            band_settle<kOut>(S, C, A, k, m, Ga, off, list, cnt, first, ct, lane_lt);
+            band_settle<kOut>(S, C, A, k, m + 32, Gb, off + 32, list, cnt, first, ct, lane_lt);
         }
-        tp += 32;
-        m += 32;
-        off += 32;
+        tp += 64;
+        m += 64;
+        off += 64;
+    }
+    if (c < nch) {
+        const float Ga = band_g<kCubeOnly>(C, r, na_);
+        if (__any_sync(kFull, Ga <= eps)) band_settle<kOut>(S, C, A, k, m, Ga, off, list, cnt, first, ct, lane_lt);
     }
 }
 
@@ -507,7 +538,10 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
             }
         }
         if (lane == 0) {
-            if (kOut == kOutPairs) A.tile_count[t] = cnt;
+            if (kOut == kOutPairs) {
+                A.tile_count[t] = cnt;
+                if (cnt) A.worklist[atomicAdd(&A.ticket[3], 1u)] = t;
+            }
             if (cnt) atomicAdd(&A.counts[s], static_cast<unsigned long long>(cnt));
             if (kOut == kOutFirst && cnt) atomicMin(&A.first_idx[s], i0 + first);
         }
@@ -588,34 +622,27 @@ __global__ void __launch_bounds__(kBlock) scan_kernel(const LaunchArgs A) {
 }
 
 // K3: codes + coalesced writes of every passing pair at its final offset.
-// Warps claim groups of 32 tiles; lanes read the group's counts/bases once.
+// Warps claim non-empty tiles from the phase-1 worklist (next claim
+// prefetched), so a warp's work is at most one tile (<= 64 chunks).
 template <int kMode, int kPath>
 __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     load_tables(sm, A);
     const unsigned lane = threadIdx.x & 31;
+    const uint32_t n_work = *reinterpret_cast<volatile unsigned int*>(&A.ticket[3]);
     Counters ct;
-    while (true) {
-        uint32_t g = 0;
-        if (lane == 0) g = atomicAdd(&A.ticket[2], 1u);
-        g = __shfl_sync(kFull, g, 0);
-        const uint64_t t0 = static_cast<uint64_t>(g) * 32;
-        if (t0 >= A.n_tiles) break;
-        const uint64_t tl = t0 + lane;
-        const uint32_t my_cnt = tl < A.n_tiles ? A.tile_count[tl] : 0u;
-        const unsigned long long my_base = tl < A.n_tiles ? A.tile_base[tl] : 0ull;
-        unsigned todo = __ballot_sync(kFull, my_cnt != 0);
-        while (todo) {
-            const int j = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const uint32_t t = static_cast<uint32_t>(t0) + j;
-            const uint32_t cnt = __shfl_sync(kFull, my_cnt, j);
-            const unsigned long long base = __shfl_sync(kFull, my_base, j);
-            if (base + cnt > A.capacity) {
-                if (lane == 0) ++ct.overflow;
-                continue;
-            }
+    uint32_t q_claim = 0;
+    if (lane == 0) q_claim = atomicAdd(&A.ticket[2], 1u);
+    uint32_t q = __shfl_sync(kFull, q_claim, 0);
+    while (q < n_work) {
+        if (lane == 0) q_claim = atomicAdd(&A.ticket[2], 1u);
+        const uint32_t t = A.worklist[q];
+        const uint32_t cnt = A.tile_count[t];
+        const unsigned long long base = A.tile_base[t];
+        if (base + cnt > A.capacity) {
+            if (lane == 0) ++ct.overflow;
+        } else {
             const uint32_t s = t / A.tiles_per_search;
             const uint32_t i0 = (t - s * A.tiles_per_search) * static_cast<uint32_t>(kTile);
             const SearchConst* S = A.sc + s;
@@ -624,16 +651,16 @@ __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
             load_code_consts(S, CC);
             const uint16_t* list = A.scratch + static_cast<size_t>(t) * kTile;
             for (uint32_t p = 0; p < cnt; p += 32) {
-                const uint32_t q = p + lane;
-                const bool active = q < cnt;
-                const uint32_t i = i0 + list[active ? q : 0];
+                const uint32_t qq = p + lane;
+                const bool active = qq < cnt;
+                const uint32_t i = i0 + list[active ? qq : 0];
                 const uint32_t k = div_na(i, A);
                 const uint32_t m = i - k * static_cast<uint32_t>(A.na);
                 int cp[3], cm[3];
                 candidate_codes<kPath>(sm, S, CC, A, k, m, active, cp, cm, ct.code_repairs, ct);
                 if (active) {
                     if (kMode == kModeBand && !classify_codes(S, cp, cm, flags)) ++ct.mismatch;
-                    const unsigned long long o = base + q;
+                    const unsigned long long o = base + qq;
                     A.out_idx[o] = i;
                     uint16_t* c16 = reinterpret_cast<uint16_t*>(A.out_codes + 6 * o);
                     c16[0] = static_cast<uint16_t>(cp[0] | (cp[1] << 8));
@@ -642,6 +669,7 @@ __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
                 }
             }
         }
+        q = __shfl_sync(kFull, q_claim, 0);
     }
     flush_counters(ct, A, lane);
 }

@@ -9,7 +9,7 @@ namespace cvg {
 // Candidates per warp tile: the unit of the ordered (decoupled look-back)
 // compaction.  A tile is a contiguous range of one search's canonical
 // (radius-major, angle-minor) candidate index.
-constexpr int kTile = 2048;
+constexpr int kTile = 4096;
 constexpr int kWarpsPerBlock = 8;
 constexpr int kBlock = 32 * kWarpsPerBlock;
 constexpr int kGuessBuckets = 4096;  // code-guess buckets over linear [0, 1]
@@ -81,11 +81,12 @@ struct LaunchArgs {
     uint64_t na_magic;         // ceil(2^64 / na): k = umul64hi(i, na_magic)
     uint64_t n_tiles;
     unsigned long long* status;    // [n_scan_blocks] chained-scan status words (flag << 62 | value)
-    unsigned int* ticket;          // [4]: phase-1 tiles, scan blocks, emit tile groups
+    unsigned int* ticket;          // [4]: phase-1 tiles, scan blocks, emit worklist, worklist size
     unsigned long long* counts;    // [n_searches]
     uint32_t* tile_count;          // [n_tiles] passing candidates per tile (PAIRS)
     unsigned long long* tile_base; // [n_tiles] exclusive prefix of tile_count (PAIRS)
     uint16_t* scratch;             // [n_tiles * kTile] per-tile passing offsets (PAIRS)
+    uint32_t* worklist;            // [n_tiles] ids of non-empty tiles, any order (PAIRS)
     unsigned long long* total;     // [1] sum of tile_count (PAIRS)
     uint32_t* out_idx;           // [capacity]
     uint8_t* out_codes;          // [capacity * 6]
