@@ -331,48 +331,48 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
     const double u = std::ldexp(1.0, -24);
     const BoundTerms bx = finv_bound(fx0, rmax * kInv500);
     const BoundTerms bz = finv_bound(fz0, rmax * kInv200);
-    double eps_band = 0.0, vbound = 0.0;
+    double eps_band = 0.0;
     for (int c = 0; c < 3; ++c) {
         const double mx = m[c][0] * wp[0], mz = m[c][2] * wp[2], cy = S.cy64[c];
-        const double amx = std::fabs(mx), amz = std::fabs(mz);
-        // Forward error of lin = fma(mx, gx, fma(mz, gz, add)) for an additive
-        // constant `add` (cy for codes, cy - centre for the band statistic).
-        auto lin_err = [&](double add_exact, double add_rounding) {
-            const double aadd = std::fabs(add_exact);
-            const double inner_max = amz * bz.gmax + aadd;
-            const double e_inner = amz * bz.err * (1 + u) + u * amz * bz.gmax + add_rounding + u * (inner_max + amz * bz.err);
-            const double lin_max = amx * bx.gmax + inner_max;
-            return std::pair<double, double>(amx * bx.err * (1 + u) + u * amx * bx.gmax + e_inner +
-                                                 u * (lin_max + amx * bx.err),
+        // Forward error of fma(cx, gx, fma(cz, gz, add)) with float-rounded
+        // constants (|cx|, |cz| magnitudes, `add` exact value).  Returns
+        // (bound, max |result|).
+        auto lin_err = [&](double acx, double acz, double add) {
+            const double aadd = std::fabs(add);
+            const double inner_max = acz * bz.gmax + aadd;
+            const double e_inner = acz * bz.err * (1 + u) + u * acz * bz.gmax + u * aadd + u * (inner_max + acz * bz.err);
+            const double lin_max = acx * bx.gmax + inner_max;
+            return std::pair<double, double>(acx * bx.err * (1 + u) + u * acx * bx.gmax + e_inner +
+                                                 u * (lin_max + acx * bx.err),
                                              lin_max);
         };
         S.mx[c] = static_cast<float>(mx);
         S.mz[c] = static_cast<float>(mz);
         S.cy[c] = static_cast<float>(cy);
-        const auto [e_lin, lin_max] = lin_err(cy, u * std::fabs(cy));
+        const auto [e_lin, lin_max] = lin_err(std::fabs(mx), std::fabs(mz), cy);
         const double eps = 1.05 * e_lin + 1e-12;
         S.eps[c] = round_up_f(eps);
         S.eps_code[c] = round_up_f(eps + std::ldexp(1.0, -23));
-        // Band statistic: with centre cc and half-width hh of [lo, hi] (an
-        // infinite edge replaced by -+L, L > every |lin| on the grid, which
-        // leaves the test unchanged), a channel is inside iff
-        // max(|vp - cc|, |vm - cc|) <= hh.  g = sg * (max - hh) < 0 iff the
-        // channel passes (quiet: both inside; loud: not both inside).
+        // Band form.  With centre cc and half-width hh of [lo, hi] (an
+        // infinite edge replaced by -+L, L above every |lin| on the grid,
+        // which leaves the test unchanged), channel c is inside iff
+        // M' = max(|vp - cc|, |vm - cc|) / hh <= 1: the matrix constants are
+        // pre-divided by hh so the kernel gets (v - cc) / hh directly.
         const double L = lin_max + e_lin + 1.0;
-        vbound = std::max(vbound, L);
         const double lo = std::isinf(S.lo[c]) ? -L : S.lo[c];
         const double hi = std::isinf(S.hi[c]) ? L : S.hi[c];
         const double cc = 0.5 * (lo + hi), hh = 0.5 * (hi - lo);
-        const double sg = bits[c] ? -1.0 : 1.0;
-        S.cyc[c] = static_cast<float>(cy - cc);
-        S.sg[c] = static_cast<float>(sg);
-        S.nsh[c] = static_cast<float>(-sg * hh);
-        const auto [e_d, d_max] = lin_err(cy - cc, u * std::fabs(cy - cc) + 1e-15);
-        const double e_g = e_d + u * hh + u * (d_max + e_d + hh) + 1e-15;
-        eps_band = std::max(eps_band, 1.05 * e_g + 1e-12);
+        S.mxs[c] = static_cast<float>(mx / hh);
+        S.mzs[c] = static_cast<float>(mz / hh);
+        S.cys[c] = static_cast<float>((cy - cc) / hh);
+        const auto [e_d, d_max] = lin_err(std::fabs(mx / hh), std::fabs(mz / hh), (cy - cc) / hh);
+        const double e_m = 1.05 * (e_d + 4 * std::ldexp(1.0, -53) * (d_max + 2.0)) + 1e-12 / hh;
+        // g_c = sg_c * (M'_c - 1) is one FFMA with exact +-1: adds u * |g|.
+        const double e_g = e_m + std::ldexp(1.0, -24) * (d_max + e_m + 1.0);
+        S.sg[c] = bits[c] ? -1.0f : 1.0f;
+        eps_band = std::max(eps_band, 1.01 * e_g);
     }
     S.eps_band = round_up_f(eps_band);
-    S.vbound = static_cast<float>(vbound);
 }
 
 // ---------------------------------------------------------------------------
@@ -537,7 +537,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
 
     const uint32_t tps = static_cast<uint32_t>((cps + cvg::kTile - 1) / cvg::kTile);
     const uint64_t n_tiles = static_cast<uint64_t>(tps) * static_cast<uint64_t>(p->n);
-    if (n_tiles >= (1ull << 31)) return fail(CVG_EINVAL, "batch too large for one plan (split the searches)");
+    if (n_tiles >= (1ull << 28)) return fail(CVG_EINVAL, "batch too large for one plan (split the searches)");
 
     // ---- host tables ----
     std::vector<SearchConst> sc(p->n);
@@ -557,6 +557,15 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
         trig_f[2 * j + 1] = static_cast<float>(cs * kInv200);
     }
 
+    // per 32-angle chunk: max |sin|/500 and max |cos|/200 (rounded up), padded
+    const size_t n_chunks = static_cast<size_t>(p->na) / 32 + 4;
+    std::vector<float> chunk_bound(2 * n_chunks, 0.0f);
+    for (int j = 0; j < p->na; ++j) {
+        float* b = &chunk_bound[2 * (j / 32)];
+        b[0] = std::max(b[0], round_up_f(std::fabs(trig_d[2 * j]) * kInv500 * (1.0 + 1e-12)));
+        b[1] = std::max(b[1], round_up_f(std::fabs(trig_d[2 * j + 1]) * kInv200 * (1.0 + 1e-12)));
+    }
+
     // ---- one constant blob: [sc | radii_d | radii_f | trig_d | trig_f | thr_d | thr_f | guess] ----
     Layout L;
     const size_t o_sc = L.take(sizeof(SearchConst) * sc.size());
@@ -564,6 +573,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     const size_t o_rf = L.take(sizeof(float) * p->nr);
     const size_t o_td = L.take(sizeof(double) * trig_d.size());
     const size_t o_tf = L.take(sizeof(float) * trig_f.size());
+    const size_t o_cb = L.take(sizeof(float) * chunk_bound.size());
     const size_t o_thd = L.take(sizeof(double) * 256);
     const size_t o_thf = L.take(sizeof(float) * 258);
     const size_t o_gs = L.take(cvg::kGuessBuckets + 1);
@@ -580,6 +590,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     std::memcpy(stage + o_rf, radii_f.data(), sizeof(float) * p->nr);
     std::memcpy(stage + o_td, trig_d.data(), sizeof(double) * trig_d.size());
     std::memcpy(stage + o_tf, trig_f.data(), sizeof(float) * trig_f.size());
+    std::memcpy(stage + o_cb, chunk_bound.data(), sizeof(float) * chunk_bound.size());
     std::memcpy(stage + o_thd, T.thr, sizeof(double) * 256);
     std::memcpy(stage + o_thf, T.thr_f, sizeof(float) * 258);
     std::memcpy(stage + o_gs, T.guess, cvg::kGuessBuckets + 1);
@@ -590,6 +601,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     A.radii_f = at<const float>(p->d_const, o_rf);
     A.trig_d = at<const double>(p->d_const, o_td);
     A.trig_f = at<const float>(p->d_const, o_tf);
+    A.chunk_bound = at<const float>(p->d_const, o_cb);
     A.thr_d = at<const double>(p->d_const, o_thd);
     A.thr_f = at<const float>(p->d_const, o_thf);
     A.guess = at<const uint8_t>(p->d_const, o_gs);
@@ -622,7 +634,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     const size_t o_tc = W.take(sizeof(uint32_t) * (pairs ? n_tiles : 0));
     const size_t o_tb = W.take(sizeof(unsigned long long) * (pairs ? n_tiles : 0));
     const size_t o_to = W.take(sizeof(unsigned long long));
-    const size_t o_wl = W.take(sizeof(uint32_t) * (pairs ? n_tiles : 0));
+    const size_t o_wl = W.take(sizeof(uint32_t) * (pairs ? n_tiles * (cvg::kTile / cvg::kEmitSpan) : 0));
     p->d_work = ctx->dev.alloc(W.off);
     if (!p->d_work) return fail(CVG_ENOMEM, "device allocation of the workspace failed");
     A.status = at<unsigned long long>(p->d_work, o_st);

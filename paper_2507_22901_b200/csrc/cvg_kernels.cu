@@ -49,6 +49,9 @@ constexpr double kInv200 = 1.0 / 200.0;
 constexpr float kU0f = 6.0f / 29.0f;
 constexpr float kK1f = 3132.0f / 24389.0f;
 constexpr float kK2f = 432.0f / 24389.0f;
+// Chunk-level cube test margin: f > u0 + 1e-5 keeps every candidate of the
+// chunk on the cube branch with room for the FP32 rounding of the test.
+constexpr float kU0Safe = 6.0f / 29.0f + 1e-5f;
 
 constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagPrefix = 2ull << 62;
@@ -69,10 +72,10 @@ __device__ __forceinline__ uint32_t div_na(uint32_t i, const LaunchArgs& A) {
 }
 
 // ------------------------------------------------------------------------
-// Per-search constants held in registers for a tile (phase 1).
+// Per-search constants held in registers for a tile (phase 1, band form).
 struct Consts {
-    float fx0, fz0, rcube, eps_band;
-    float mx[3], mz[3], cyc[3], sg[3], nsh[3];
+    float fx0, fz0, rcube, eps;
+    float mxs[3], mzs[3], cys[3], sg[3];
     uint32_t flags;
 };
 
@@ -80,14 +83,13 @@ __device__ __forceinline__ void load_consts(const SearchConst* S, Consts& c) {
     c.fx0 = __ldg(&S->fx0);
     c.fz0 = __ldg(&S->fz0);
     c.rcube = __ldg(&S->rcube);
-    c.eps_band = __ldg(&S->eps_band);
+    c.eps = __ldg(&S->eps_band);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-        c.mx[q] = __ldg(&S->mx[q]);
-        c.mz[q] = __ldg(&S->mz[q]);
-        c.cyc[q] = __ldg(&S->cyc[q]);
+        c.mxs[q] = __ldg(&S->mxs[q]);
+        c.mzs[q] = __ldg(&S->mzs[q]);
+        c.cys[q] = __ldg(&S->cys[q]);
         c.sg[q] = __ldg(&S->sg[q]);
-        c.nsh[q] = __ldg(&S->nsh[q]);
     }
     c.flags = __ldg(&S->flags);
 }
@@ -225,22 +227,20 @@ __device__ __forceinline__ void fast_linear(float fx0, float fz0, const float* m
 }
 
 // Band statistic of the reference band test (search.cpp:267-276,
-// make_bands 291-329).  With dp/dm = endpoint value minus the band centre,
-// g_c = sg_c * (max(|dp|, |dm|) - h_c) is negative iff channel c passes
-// (quiet: both endpoints inside the band; loud: not both inside), so the
-// candidate passes iff G = max_c g_c < 0.  |G32 - G| <= eps_band (host
-// proof), hence G < -eps certainly passes, G > eps certainly fails and only
-// |G| <= eps goes to the FP64 path.  7 ALU-pipe ops per candidate.
-__device__ __forceinline__ bool fast_band(const Consts& C, const float* dp, const float* dm, bool& unsure) {
-    float G = 0.f;
+// make_bands 291-329).  With the matrix rows pre-divided by the band half-
+// width h_c and offset by the band centre, channel c of a candidate yields
+// M'_c = max(|vp_c - centre_c|, |vm_c - centre_c|) / h_c: a quiet channel
+// passes iff M'_c <= 1 (both endpoints inside), a loud one iff M'_c > 1, so
+// with sg_c = +1 (quiet) / -1 (loud), g_c = sg_c * (M'_c - 1) is negative iff
+// channel c passes and the candidate passes iff G = max_c g_c < 0.
+// |G32 - G| <= eps (host proof), hence G < -eps certainly passes, G > eps
+// certainly fails, and only |G| <= eps goes to the FP64 path.  A candidate
+// needs attention at all only if G <= eps.  6 ALU + 3 FMA-pipe ops.
+__device__ __forceinline__ float band_G(const Consts& C, const float* dp, const float* dm) {
+    float g[3];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        const float M = fmaxf(fabsf(dp[q]), fabsf(dm[q]));
-        const float g = fmaf(C.sg[q], M, C.nsh[q]);
-        G = q == 0 ? g : fmaxf(G, g);
-    }
-    unsure = fabsf(G) <= C.eps_band;
-    return G < -C.eps_band;
+    for (int q = 0; q < 3; ++q) g[q] = fmaf(C.sg[q], fmaxf(fabsf(dp[q]), fabsf(dm[q])), -C.sg[q]);
+    return fmaxf(fmaxf(g[0], g[1]), g[2]);
 }
 
 // Linear value -> code through the float table, verified against the bound:
@@ -375,9 +375,10 @@ __device__ __forceinline__ bool candidate_pass(const Smem& sm, const SearchConst
     const float r = __ldg(&A.radii_f[k]);
     const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + m);
     float dp[3], dm[3];
-    fast_linear<false>(C.fx0, C.fz0, C.mx, C.mz, C.cyc, r, sc, dp, dm);
-    bool unsure;
-    bool pass = fast_band(C, dp, dm, unsure);
+    fast_linear<false>(C.fx0, C.fz0, C.mxs, C.mzs, C.cys, r, sc, dp, dm);
+    const float G = band_G(C, dp, dm);
+    bool pass = G < -C.eps;
+    const bool unsure = fabsf(G) <= C.eps;
     if (kPath == kPathAudit) {
         double lp[3], lm[3];
         exact_linear(S, A, k, m, lp, lm);
@@ -414,14 +415,14 @@ __device__ __forceinline__ void append(bool pass, uint32_t off, uint16_t* list, 
     cnt += __popc(b);
 }
 
-// Slow path of one chunk (some lane passes or is unsure): FP64 repair of the
+// Slow path of one chunk (some lane needs attention): FP64 repair of the
 // unsure lanes, then the ordered append.
 template <int kOut>
 __device__ __forceinline__ void band_settle(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
                                             uint32_t m, float G, uint32_t off, uint16_t* list, uint32_t& cnt,
                                             uint32_t& first, Counters& ct, unsigned lane_lt) {
-    bool pass = G < -C.eps_band;
-    if (fabsf(G) <= C.eps_band) {
+    bool pass = G < -C.eps;
+    if (fabsf(G) <= C.eps) {
         double lp[3], lm[3];
         exact_linear(S, A, k, m, lp, lm);
         pass = exact_band(S, lp, lm, C.flags);
@@ -430,55 +431,58 @@ __device__ __forceinline__ void band_settle(const SearchConst* S, const Consts& 
     append<kOut>(pass, off, list, cnt, first, lane_lt);
 }
 
-// Band statistic G of one candidate (see fast_band).
 template <bool kCubeOnly>
-__device__ __forceinline__ float band_g(const Consts& C, float r, float2 sc) {
+__device__ __forceinline__ float band_chunk(const Consts& C, float r, float2 sc) {
     float dp[3], dm[3];
-    fast_linear<kCubeOnly>(C.fx0, C.fz0, C.mx, C.mz, C.cyc, r, sc, dp, dm);
-    float G = 0.f;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        const float M = fmaxf(fabsf(dp[q]), fabsf(dm[q]));
-        const float g = fmaf(C.sg[q], M, C.nsh[q]);
-        G = q == 0 ? g : fmaxf(G, g);
-    }
-    return G;
+    fast_linear<kCubeOnly>(C.fx0, C.fz0, C.mxs, C.mzs, C.cys, r, sc, dp, dm);
+    return band_G(C, dp, dm);
 }
 
 // Hot loop: FAST path, band mode, `nch` full 32-candidate chunks of radius
-// row k starting at angle m0 (na % 32 == 0 so chunks never straddle rows).
-// Two chunks per iteration share one vote (ILP across chunks); per
-// candidate: 1 LDG (L1-resident trig, prefetched two chunks ahead), 27 FMA-
-// pipe + 5 ALU-pipe ops + 1 compare.  A candidate needs attention only when
-// G <= eps (passes, or sits inside the error bound), which is rare.
-template <bool kCubeOnly, int kOut>
+// row k starting at angle m0 (na % 32 == 0: chunks never straddle rows).  Two
+// chunks per iteration share one vote (ILP across chunks).  Per candidate:
+// 1 LDG (L1-resident trig, prefetched two chunks ahead), 27 FMA-pipe ops
+// (4 f, 8 cube, 12 matrix, 3 sign) + 6 min/max + 1 compare.  Rows that may
+// cross the linear branch of f^-1 (r >= rcube) decide per chunk pair, from
+// the chunks' max |sin|/|cos|, whether the cube branch still holds.
+template <bool kCubeRow, int kOut>
 __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
                                          float r, uint32_t m0, uint32_t nch, uint32_t off, uint16_t* list,
                                          uint32_t& cnt, uint32_t& first, Counters& ct, unsigned lane,
                                          unsigned lane_lt) {
-    const float2* tp = reinterpret_cast<const float2*>(A.trig_f) + m0 + lane;
-    const float eps = C.eps_band;
-    uint32_t m = m0 + lane;
-    off += lane;
-    float2 na_ = __ldg(tp), nb_ = __ldg(tp + 32);
-    uint32_t c = 0;
-    for (; c + 2 <= nch; c += 2) {
+    const float2* const t0 = reinterpret_cast<const float2*>(A.trig_f) + m0 + lane;
+    const uint32_t dend = 32u * (nch & ~1u);
+    float2 na_ = __ldg(t0), nb_ = __ldg(t0 + 32);
+    uint32_t d = 0;
+    for (; d != dend; d += 64) {
         const float2 sa = na_, sb = nb_;
-        na_ = __ldg(tp + 64);  // prefetch; the table is padded by 64 entries
-        nb_ = __ldg(tp + 96);
-        const float Ga = band_g<kCubeOnly>(C, r, sa);
-        const float Gb = band_g<kCubeOnly>(C, r, sb);
-        if (__any_sync(kFull, (Ga <= eps) | (Gb <= eps))) {
-            band_settle<kOut>(S, C, A, k, m, Ga, off, list, cnt, first, ct, lane_lt);
-            band_settle<kOut>(S, C, A, k, m + 32, Gb, off + 32, list, cnt, first, ct, lane_lt);
+        na_ = __ldg(t0 + d + 64);  // prefetch; the table is padded by 128 entries
+        nb_ = __ldg(t0 + d + 96);
+        float Ga, Gb;
+        bool cube = kCubeRow;
+        if (!kCubeRow) {
+            const float2* cb = reinterpret_cast<const float2*>(A.chunk_bound) + ((m0 + d) >> 5);
+            const float2 ba = __ldg(cb), bb = __ldg(cb + 1);
+            cube = (fmaf(-r, fmaxf(ba.x, bb.x), C.fx0) > kU0Safe) & (fmaf(-r, fmaxf(ba.y, bb.y), C.fz0) > kU0Safe);
         }
-        tp += 64;
-        m += 64;
-        off += 64;
+        if (cube) {
+            Ga = band_chunk<true>(C, r, sa);
+            Gb = band_chunk<true>(C, r, sb);
+        } else {
+            Ga = band_chunk<false>(C, r, sa);
+            Gb = band_chunk<false>(C, r, sb);
+        }
+        if (__any_sync(kFull, fminf(Ga, Gb) <= C.eps)) {
+            band_settle<kOut>(S, C, A, k, m0 + lane + d, Ga, off + lane + d, list, cnt, first, ct, lane_lt);
+            band_settle<kOut>(S, C, A, k, m0 + lane + d + 32, Gb, off + lane + d + 32, list, cnt, first, ct,
+                              lane_lt);
+        }
     }
-    if (c < nch) {
-        const float Ga = band_g<kCubeOnly>(C, r, na_);
-        if (__any_sync(kFull, Ga <= eps)) band_settle<kOut>(S, C, A, k, m, Ga, off, list, cnt, first, ct, lane_lt);
+    if (nch & 1u) {
+        const float Ga = band_chunk<kCubeRow>(C, r, na_);
+        if (__any_sync(kFull, Ga <= C.eps)) {
+            band_settle<kOut>(S, C, A, k, m0 + lane + d, Ga, off + lane + d, list, cnt, first, ct, lane_lt);
+        }
     }
 }
 
@@ -540,7 +544,12 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         if (lane == 0) {
             if (kOut == kOutPairs) {
                 A.tile_count[t] = cnt;
-                if (cnt) A.worklist[atomicAdd(&A.ticket[3], 1u)] = t;
+                // emit work items: (tile, 256-pair sub-range), any order
+                const uint32_t subs = (cnt + kEmitSpan - 1) / kEmitSpan;
+                if (subs) {
+                    const uint32_t w = atomicAdd(&A.ticket[3], subs);
+                    for (uint32_t j = 0; j < subs; ++j) A.worklist[w + j] = (t << 4) | j;
+                }
             }
             if (cnt) atomicAdd(&A.counts[s], static_cast<unsigned long long>(cnt));
             if (kOut == kOutFirst && cnt) atomicMin(&A.first_idx[s], i0 + first);
@@ -622,8 +631,9 @@ __global__ void __launch_bounds__(kBlock) scan_kernel(const LaunchArgs A) {
 }
 
 // K3: codes + coalesced writes of every passing pair at its final offset.
-// Warps claim non-empty tiles from the phase-1 worklist (next claim
-// prefetched), so a warp's work is at most one tile (<= 64 chunks).
+// Warps claim (tile, 256-pair sub-range) items from the phase-1 worklist
+// (next claim prefetched), so no warp holds more than 8 chunks of work; the
+// item's list entries are loaded up front (8 per lane, one coalesced wave).
 template <int kMode, int kPath>
 __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -637,29 +647,40 @@ __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
     uint32_t q = __shfl_sync(kFull, q_claim, 0);
     while (q < n_work) {
         if (lane == 0) q_claim = atomicAdd(&A.ticket[2], 1u);
-        const uint32_t t = A.worklist[q];
-        const uint32_t cnt = A.tile_count[t];
-        const unsigned long long base = A.tile_base[t];
+        const uint32_t item = A.worklist[q];
+        const uint32_t t = item >> 4;
+        const uint32_t p0 = (item & 15u) * kEmitSpan;
+        const uint32_t cnt = min(A.tile_count[t] - p0, static_cast<uint32_t>(kEmitSpan));
+        const unsigned long long base = A.tile_base[t] + p0;
+        const uint16_t* list = A.scratch + static_cast<size_t>(t) * kTile + p0;
+        uint16_t offs[kEmitSpan / 32];
+#pragma unroll
+        for (int j = 0; j < kEmitSpan / 32; ++j) {
+            const uint32_t qq = j * 32 + lane;
+            offs[j] = qq < cnt ? list[qq] : list[0];
+        }
         if (base + cnt > A.capacity) {
             if (lane == 0) ++ct.overflow;
         } else {
             const uint32_t s = t / A.tiles_per_search;
             const uint32_t i0 = (t - s * A.tiles_per_search) * static_cast<uint32_t>(kTile);
             const SearchConst* S = A.sc + s;
-            const uint32_t flags = __ldg(&S->flags);
             CodeConsts CC;
             load_code_consts(S, CC);
-            const uint16_t* list = A.scratch + static_cast<size_t>(t) * kTile;
-            for (uint32_t p = 0; p < cnt; p += 32) {
-                const uint32_t qq = p + lane;
+#pragma unroll
+            for (int j = 0; j < kEmitSpan / 32; ++j) {
+                if (static_cast<uint32_t>(j) * 32 >= cnt) break;
+                const uint32_t qq = j * 32 + lane;
                 const bool active = qq < cnt;
-                const uint32_t i = i0 + list[active ? qq : 0];
+                const uint32_t i = i0 + offs[j];
                 const uint32_t k = div_na(i, A);
                 const uint32_t m = i - k * static_cast<uint32_t>(A.na);
                 int cp[3], cm[3];
                 candidate_codes<kPath>(sm, S, CC, A, k, m, active, cp, cm, ct.code_repairs, ct);
                 if (active) {
-                    if (kMode == kModeBand && !classify_codes(S, cp, cm, flags)) ++ct.mismatch;
+                    if (kMode == kModeBand && kPath != kPathFast && !classify_codes(S, cp, cm, __ldg(&S->flags))) {
+                        ++ct.mismatch;
+                    }
                     const unsigned long long o = base + qq;
                     A.out_idx[o] = i;
                     uint16_t* c16 = reinterpret_cast<uint16_t*>(A.out_codes + 6 * o);

@@ -13,6 +13,7 @@ constexpr int kTile = 4096;
 constexpr int kWarpsPerBlock = 8;
 constexpr int kBlock = 32 * kWarpsPerBlock;
 constexpr int kGuessBuckets = 4096;  // code-guess buckets over linear [0, 1]
+constexpr int kEmitSpan = 256;      // pairs per emit work item (tile sub-range)
 constexpr int kScanItems = 8;        // tile counts per thread in the offset scan
 constexpr int kScanTile = kBlock * kScanItems;
 
@@ -24,17 +25,16 @@ struct alignas(16) SearchConst {
     float fx0;         // Fy + a/500   (fx of both endpoints = fx0 +- r*sin/500)
     float fz0;         // Fz = Fy - b/200 (fz = fz0 -+ r*cos/200)
     float rcube;       // rows with r < rcube never leave the cube branch of f^-1
-    float eps_band;    // bound on |G32 - G| of the band statistic G (see cvg_kernels.cu)
+    float eps_band;    // bound on |G32 - G| of the band statistic (see cvg_kernels.cu)
     float mx[3];       // Minv[c][0] * wx
     float mz[3];       // Minv[c][2] * wz
     float cy[3];       // Minv[c][1] * wy * f^-1(Fy)
-    float cyc[3];      // cy - band centre: the matrix FFMAs then yield v - centre
+    float mxs[3];      // band form: mx / h_c          (h_c: band half-width)
+    float mzs[3];      //            mz / h_c
+    float cys[3];      //            (cy - centre_c) / h_c
     float sg[3];       // +1 quiet channel (0 bit), -1 loud channel (1 bit)
-    float nsh[3];      // -sg * band half-width
     float eps[3];      // proven bound |lin32 - lin64| per channel (linear units)
     float eps_code[3]; // eps + float rounding of the code thresholds
-    float vbound;      // max |lin| over the grid (+1): stands in for infinite band edges
-    uint32_t reserved;
     uint32_t flags;    // bit c (c=0,1,2 -> r,g,b): loud channel (pattern bit set)
     int32_t t[3];      // target codes
     int32_t k1;        // d > v_th   <=> d >= k1 (integer deltas); 256 = never
@@ -44,7 +44,7 @@ struct alignas(16) SearchConst {
     double cy64[3];
     double lo[3], hi[3];
 };
-static_assert(sizeof(SearchConst) == 256, "SearchConst layout");
+static_assert(sizeof(SearchConst) == 272, "SearchConst layout");
 
 // Device statistics block.
 struct Stats {
@@ -68,6 +68,7 @@ struct LaunchArgs {
     const double* radii_d;     // [nr]
     const float* trig_f;       // [na][2] = (sin/500, cos/200) as float
     const double* trig_d;      // [na][2] = (sin, cos), glibc doubles (search.cpp:414-419)
+    const float* chunk_bound;  // [na/32 + 4][2] max |sin|/500, max |cos|/200 per 32-angle chunk (rounded up)
     const double* thr_d;       // [256] QuantTable thresholds (convert_kernel.hpp:123-141)
     const float* thr_f;        // [257] thresholds rounded to float, [256] = +inf
     const uint8_t* guess;      // [kGuessBuckets + 1] code(i / 4096)
@@ -86,7 +87,7 @@ struct LaunchArgs {
     uint32_t* tile_count;          // [n_tiles] passing candidates per tile (PAIRS)
     unsigned long long* tile_base; // [n_tiles] exclusive prefix of tile_count (PAIRS)
     uint16_t* scratch;             // [n_tiles * kTile] per-tile passing offsets (PAIRS)
-    uint32_t* worklist;            // [n_tiles] ids of non-empty tiles, any order (PAIRS)
+    uint32_t* worklist;            // [n_tiles * kTile / kEmitSpan] emit items tile << 4 | sub, any order
     unsigned long long* total;     // [1] sum of tile_count (PAIRS)
     uint32_t* out_idx;           // [capacity]
     uint8_t* out_codes;          // [capacity * 6]
