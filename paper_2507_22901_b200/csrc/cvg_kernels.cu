@@ -442,46 +442,34 @@ __device__ __forceinline__ float band_chunk(const Consts& C, float r, float2 sc)
 // row k starting at angle m0 (na % 32 == 0: chunks never straddle rows).  Two
 // chunks per iteration share one vote (ILP across chunks).  Per candidate:
 // 1 LDG (L1-resident trig, prefetched two chunks ahead), 27 FMA-pipe ops
-// (4 f, 8 cube, 12 matrix, 3 sign) + 6 min/max + 1 compare.  Rows that may
-// cross the linear branch of f^-1 (r >= rcube) decide per chunk pair, from
-// the chunks' max |sin|/|cos|, whether the cube branch still holds.
-template <bool kCubeRow, int kOut>
+// (4 f, 8 cube, 12 matrix, 3 sign) + 7 min/max + 1 compare.  kCubeOnly rows
+// (r < rcube) never reach the linear branch of f^-1; the others select.
+template <bool kCubeOnly, int kOut>
 __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
                                          float r, uint32_t m0, uint32_t nch, uint32_t off, uint16_t* list,
                                          uint32_t& cnt, uint32_t& first, Counters& ct, unsigned lane,
                                          unsigned lane_lt) {
-    const float2* const t0 = reinterpret_cast<const float2*>(A.trig_f) + m0 + lane;
-    const uint32_t dend = 32u * (nch & ~1u);
-    float2 na_ = __ldg(t0), nb_ = __ldg(t0 + 32);
-    uint32_t d = 0;
-    for (; d != dend; d += 64) {
+    const float2* __restrict__ trig = reinterpret_cast<const float2*>(A.trig_f);
+    const uint32_t mb = m0 + lane;
+    uint32_t ix = mb;
+    const uint32_t iend = mb + 32u * (nch & ~1u);
+    float2 na_ = __ldg(trig + ix), nb_ = __ldg(trig + ix + 32);
+    for (; ix != iend; ix += 64) {
         const float2 sa = na_, sb = nb_;
-        na_ = __ldg(t0 + d + 64);  // prefetch; the table is padded by 128 entries
-        nb_ = __ldg(t0 + d + 96);
-        float Ga, Gb;
-        bool cube = kCubeRow;
-        if (!kCubeRow) {
-            const float2* cb = reinterpret_cast<const float2*>(A.chunk_bound) + ((m0 + d) >> 5);
-            const float2 ba = __ldg(cb), bb = __ldg(cb + 1);
-            cube = (fmaf(-r, fmaxf(ba.x, bb.x), C.fx0) > kU0Safe) & (fmaf(-r, fmaxf(ba.y, bb.y), C.fz0) > kU0Safe);
-        }
-        if (cube) {
-            Ga = band_chunk<true>(C, r, sa);
-            Gb = band_chunk<true>(C, r, sb);
-        } else {
-            Ga = band_chunk<false>(C, r, sa);
-            Gb = band_chunk<false>(C, r, sb);
-        }
+        na_ = __ldg(trig + ix + 64);  // prefetch; the table is padded by 128 entries
+        nb_ = __ldg(trig + ix + 96);
+        const float Ga = band_chunk<kCubeOnly>(C, r, sa);
+        const float Gb = band_chunk<kCubeOnly>(C, r, sb);
         if (__any_sync(kFull, fminf(Ga, Gb) <= C.eps)) {
-            band_settle<kOut>(S, C, A, k, m0 + lane + d, Ga, off + lane + d, list, cnt, first, ct, lane_lt);
-            band_settle<kOut>(S, C, A, k, m0 + lane + d + 32, Gb, off + lane + d + 32, list, cnt, first, ct,
-                              lane_lt);
+            const uint32_t d = ix - mb;
+            band_settle<kOut>(S, C, A, k, ix, Ga, off + lane + d, list, cnt, first, ct, lane_lt);
+            band_settle<kOut>(S, C, A, k, ix + 32, Gb, off + lane + d + 32, list, cnt, first, ct, lane_lt);
         }
     }
     if (nch & 1u) {
-        const float Ga = band_chunk<kCubeRow>(C, r, na_);
+        const float Ga = band_chunk<kCubeOnly>(C, r, na_);
         if (__any_sync(kFull, Ga <= C.eps)) {
-            band_settle<kOut>(S, C, A, k, m0 + lane + d, Ga, off + lane + d, list, cnt, first, ct, lane_lt);
+            band_settle<kOut>(S, C, A, k, ix, Ga, off + lane + (ix - mb), list, cnt, first, ct, lane_lt);
         }
     }
 }
@@ -633,7 +621,7 @@ __global__ void __launch_bounds__(kBlock) scan_kernel(const LaunchArgs A) {
 // K3: codes + coalesced writes of every passing pair at its final offset.
 // Warps claim (tile, 256-pair sub-range) items from the phase-1 worklist
 // (next claim prefetched), so no warp holds more than 8 chunks of work; the
-// item's list entries are loaded up front (8 per lane, one coalesced wave).
+// item's list entries are read one chunk ahead.
 template <int kMode, int kPath>
 __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -653,12 +641,6 @@ __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
         const uint32_t cnt = min(A.tile_count[t] - p0, static_cast<uint32_t>(kEmitSpan));
         const unsigned long long base = A.tile_base[t] + p0;
         const uint16_t* list = A.scratch + static_cast<size_t>(t) * kTile + p0;
-        uint16_t offs[kEmitSpan / 32];
-#pragma unroll
-        for (int j = 0; j < kEmitSpan / 32; ++j) {
-            const uint32_t qq = j * 32 + lane;
-            offs[j] = qq < cnt ? list[qq] : list[0];
-        }
         if (base + cnt > A.capacity) {
             if (lane == 0) ++ct.overflow;
         } else {
@@ -667,12 +649,13 @@ __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
             const SearchConst* S = A.sc + s;
             CodeConsts CC;
             load_code_consts(S, CC);
-#pragma unroll
-            for (int j = 0; j < kEmitSpan / 32; ++j) {
-                if (static_cast<uint32_t>(j) * 32 >= cnt) break;
-                const uint32_t qq = j * 32 + lane;
+            uint32_t next = list[lane < cnt ? lane : 0];
+#pragma unroll 1
+            for (uint32_t p = 0; p < cnt; p += 32) {
+                const uint32_t qq = p + lane;
                 const bool active = qq < cnt;
-                const uint32_t i = i0 + offs[j];
+                const uint32_t i = i0 + next;
+                if (p + 32 < cnt) next = list[qq + 32 < cnt ? qq + 32 : p + 32];  // one chunk ahead
                 const uint32_t k = div_na(i, A);
                 const uint32_t m = i - k * static_cast<uint32_t>(A.na);
                 int cp[3], cm[3];
