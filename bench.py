@@ -267,13 +267,15 @@ def run_ours(args):
     del res
     if dist:
         dist.barrier()
-    e2e_times = []
+    e2e_times, phases = [], []
     for _ in range(e2e_steps):
         t0 = time.perf_counter()
         r = ctx.search(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles)
         _ = int(r["n_pairs"])
         e2e_times.append(time.perf_counter() - t0)
+        phases.append({k: r["stats"][k] for k in ("prep_ms", "h2d_ms", "device_ms", "d2h_ms", "total_ms")})
         del r
+    phase_med = {k: round(statistics.median(p[k] for p in phases), 4) for k in phases[0]}
     e2e_s = sum(e2e_times)
     t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
     if dist:
@@ -323,7 +325,7 @@ def run_ours(args):
         "config": config_dict(wl, world, {"pairs_per_step": n_pairs}),
         "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "s_per_step": round(float(t.item()) / e2e_steps, 5), "steps": e2e_steps,
-                "api": "cvg_search (C-ABI host call)"},
+                "api": "cvg_search (C-ABI host call)", "breakdown_ms": phase_med},
         "gpu_launches": plan.launches * args.steps,
         "clocks": clk.summary(),
         "roofline": roofline,

@@ -109,6 +109,10 @@ typedef struct {
     float kernel_ms;             /* device time of the search kernels of this call */
     uint64_t h2d_bytes;          /* host->device bytes this call copied (tables + constants) */
     uint64_t d2h_bytes;          /* device->host bytes this call copied (counts, stats, pairs) */
+    /* wall-clock breakdown of a cvg_search call (ms): host prep (validation,
+     * glibc tables, per-target constants), H2D upload, launch -> counts on
+     * host, pair D2H, whole call */
+    float prep_ms, h2d_ms, device_ms, d2h_ms, total_ms;
 } cvg_result;
 
 /* ---- context ----------------------------------------------------------- */

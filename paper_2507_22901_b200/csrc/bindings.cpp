@@ -125,6 +125,11 @@ py::dict result_dict(std::shared_ptr<ResultHolder> h, int output) {
     stats["kernel_ms"] = r.kernel_ms;
     stats["h2d_bytes"] = r.h2d_bytes;
     stats["d2h_bytes"] = r.d2h_bytes;
+    stats["prep_ms"] = r.prep_ms;
+    stats["h2d_ms"] = r.h2d_ms;
+    stats["device_ms"] = r.device_ms;
+    stats["d2h_ms"] = r.d2h_ms;
+    stats["total_ms"] = r.total_ms;
     out["stats"] = stats;
     return out;
 }

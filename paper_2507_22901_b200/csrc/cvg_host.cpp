@@ -11,9 +11,11 @@
 
 #include <algorithm>
 #include <cfloat>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -31,6 +33,10 @@ using cvg::SearchConst;
 namespace {
 
 thread_local std::string g_error;
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 int fail(int code, const std::string& msg) {
     g_error = msg;
@@ -470,6 +476,7 @@ struct cvg_plan {
     bool ran = false;
     cudaStream_t last_stream = nullptr;
     uint64_t input_bytes = 0;
+    double t_prep_end = 0, t_upload_end = 0;
 };
 
 namespace {
@@ -579,6 +586,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     const size_t o_gs = L.take(cvg::kGuessBuckets + 1);
     const size_t bytes = L.off;
     p->input_bytes = bytes;
+    p->t_prep_end = now_ms();
     unsigned char* stage = static_cast<unsigned char*>(ctx->host.alloc(bytes));
     p->d_const = ctx->dev.alloc(bytes);
     if (!stage || !p->d_const) {
@@ -609,12 +617,14 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
     ctx->host.release(stage);
     if (e != cudaSuccess) return cuda_fail(e, "upload of the search tables");
+    p->t_upload_end = now_ms();
 
     for (int i = 0; i < 9; ++i) A.minv[i] = kXyzToRgb.m[i / 3][i % 3];
     A.n_searches = p->n;
     A.nr = p->nr;
     A.na = p->na;
     A.aligned = (p->na % 32) == 0;
+    A.emit_exact = std::getenv("CVG_EMIT_EXACT") ? std::atoi(std::getenv("CVG_EMIT_EXACT")) : 0;
     A.tiles_per_search = tps;
     A.cand_per_search = static_cast<uint32_t>(cps);
     A.na_magic = p->na > 1 ? (UINT64_MAX / static_cast<uint64_t>(p->na)) + 1 : 0;
@@ -733,6 +743,7 @@ int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
     std::vector<uint64_t> counts;
     HostStats hs;
     if (int e = plan_collect(p, counts, hs)) return e;
+    const double t_counts = now_ms();
     uint64_t total = 0;
     for (uint64_t c : counts) total += c;
     if (p->out == cvg::kOutPairs && hs.st.overflow) {
@@ -774,6 +785,7 @@ int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
             CVG_CUDA(cudaMemcpyAsync(r->codes, p->d_out_codes, total * 6, cudaMemcpyDeviceToHost, st));
             CVG_CUDA(cudaStreamSynchronize(st));
         }
+        r->d2h_ms = static_cast<float>(now_ms() - t_counts);
     } else if (p->out == cvg::kOutFirst && n) {
         r->d2h_bytes += n * 10;
         r->first_idx = static_cast<uint32_t*>(ctx->host.alloc(n * 4));
@@ -950,10 +962,19 @@ int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out) {
     if (int e = validate_desc(desc)) return e;
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     if (int e = ensure_device(ctx)) return e;
+    const double t0 = now_ms();
     cvg_plan plan;
     int e = plan_build(ctx, desc, &plan);
+    const double t_built = now_ms();
     if (!e) e = plan_enqueue(&plan, ctx->stream);
     if (!e) e = plan_fetch_impl(&plan, out, true);
+    if (!e) {
+        const double t1 = now_ms();
+        out->prep_ms = static_cast<float>((plan.t_prep_end ? plan.t_prep_end : t_built) - t0);
+        out->h2d_ms = static_cast<float>(plan.t_upload_end ? plan.t_upload_end - plan.t_prep_end : 0.0);
+        out->total_ms = static_cast<float>(t1 - t0);
+        out->device_ms = static_cast<float>(t1 - t_built - out->d2h_ms);
+    }
     if (plan.ran) cudaStreamSynchronize(ctx->stream);
     plan_release(&plan);
     plan.ctx = nullptr;

@@ -659,7 +659,11 @@ __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
                 const uint32_t k = div_na(i, A);
                 const uint32_t m = i - k * static_cast<uint32_t>(A.na);
                 int cp[3], cm[3];
-                candidate_codes<kPath>(sm, S, CC, A, k, m, active, cp, cm, ct.code_repairs, ct);
+                if (kPath == kPathFast && A.emit_exact) {
+                    candidate_codes<kPathExact>(sm, S, CC, A, k, m, active, cp, cm, ct.code_repairs, ct);
+                } else {
+                    candidate_codes<kPath>(sm, S, CC, A, k, m, active, cp, cm, ct.code_repairs, ct);
+                }
                 if (active) {
                     if (kMode == kModeBand && kPath != kPathFast && !classify_codes(S, cp, cm, __ldg(&S->flags))) {
                         ++ct.mismatch;

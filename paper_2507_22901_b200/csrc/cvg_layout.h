@@ -77,6 +77,7 @@ struct LaunchArgs {
     int32_t nr;
     int32_t na;
     int32_t aligned;           // na % 32 == 0: a 32-candidate chunk never straddles rows
+    int32_t emit_exact;        // emit codes through the FP64 path (experiment knob, CVG_EMIT_EXACT)
     uint32_t tiles_per_search;
     uint32_t cand_per_search;  // nr * na (< 2^32)
     uint64_t na_magic;         // ceil(2^64 / na): k = umul64hi(i, na_magic)

@@ -89,7 +89,14 @@ def summarize_report(path, blocks):
                 cur["h"] = r
             elif cur and "h" in cur and len(r) == len(cur["h"]):
                 cur["rows"].append(dict(zip(cur["h"], r)))
-        for kk, b in zip(kernels, per):
+        # the source page lists kernels in ID order (names are formatted
+        # differently from the details page); keep the first listing of each
+        seen, uniq = set(), []
+        for b in per:
+            if b["name"] not in seen and b["rows"]:
+                seen.add(b["name"])
+                uniq.append(b)
+        for kk, b in zip(sorted(kernels, key=lambda k: int(k["id"])), uniq):
             data = b["rows"]
             tot = sum(int(d["Instructions Executed"]) for d in data) or 1
             stalls = {s: sum(int(d.get("stall_" + s, 0) or 0) for d in data) for s in STALLS}

@@ -96,6 +96,41 @@ __global__ void k_mix(float* out, const float* in, int iters) {
     if (r == 1234.5f) out[0] = r;
 }
 
+// FP64: dependent chains of DFMA (reg,reg,reg) and DMUL/DADD pairs
+__global__ void k_dfma(float* out, const float* in, int iters) {
+    double x[CHAINS], y[CHAINS], z[CHAINS];
+    for (int c = 0; c < CHAINS; ++c) {
+        x[c] = threadIdx.x + c;
+        y[c] = in[(threadIdx.x + c) & 255];
+        z[c] = in[(threadIdx.x * 5 + c) & 255];
+    }
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int u = 0; u < UNROLL; ++u)
+#pragma unroll
+            for (int c = 0; c < CHAINS; ++c) x[c] = fma(x[c], y[c], z[c]);
+    double r = 0;
+    for (int c = 0; c < CHAINS; ++c) r += x[c];
+    if (r == 1234.5) out[0] = (float)r;
+}
+
+__global__ void k_dmul_dadd(float* out, const float* in, int iters) {
+    double x[CHAINS], y[CHAINS], z[CHAINS];
+    for (int c = 0; c < CHAINS; ++c) {
+        x[c] = threadIdx.x + c;
+        y[c] = in[(threadIdx.x + c) & 255];
+        z[c] = in[(threadIdx.x * 5 + c) & 255];
+    }
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int u = 0; u < UNROLL / 2; ++u)
+#pragma unroll
+            for (int c = 0; c < CHAINS; ++c) x[c] = __dadd_rn(__dmul_rn(x[c], y[c]), z[c]);
+    double r = 0;
+    for (int c = 0; c < CHAINS; ++c) r += x[c];
+    if (r == 1234.5) out[0] = (float)r;
+}
+
 template <typename F>
 double time_kernel(F launch, double ops) {
     cudaEvent_t e0, e1;
@@ -129,12 +164,14 @@ int main() {
     const int blocks = sms * 8, threads = 256, iters = 2048;
     const double lanes = double(blocks) * threads * iters;
     const double per_clk_sm = 1.0 / (sms * clk_khz * 1e3);
-    struct R { const char* name; double v; } res[5];
+    struct R { const char* name; double v; } res[7];
     res[0] = {"ffma_reg_const_const", time_kernel([&] { k_ffma_rcc<<<blocks, threads>>>(out, iters, 0.999f, 1e-3f); }, lanes * UNROLL * CHAINS)};
     res[1] = {"ffma_reg_reg_reg", time_kernel([&] { k_ffma_rrr<<<blocks, threads>>>(out, in, iters); }, lanes * UNROLL * CHAINS)};
     res[2] = {"fmul_reg_reg", time_kernel([&] { k_fmul_rr<<<blocks, threads>>>(out, in, iters); }, lanes * UNROLL * CHAINS)};
     res[3] = {"fmnmx_abs", time_kernel([&] { k_fmnmx<<<blocks, threads>>>(out, in, iters); }, lanes * UNROLL * CHAINS)};
     res[4] = {"mix_3ffma_1fmnmx", time_kernel([&] { k_mix<<<blocks, threads>>>(out, in, iters); }, lanes * UNROLL * CHAINS)};
+    res[5] = {"dfma_reg", time_kernel([&] { k_dfma<<<blocks, threads>>>(out, in, iters / 8); }, lanes / 8 * UNROLL * CHAINS)};
+    res[6] = {"dmul_dadd_ops", time_kernel([&] { k_dmul_dadd<<<blocks, threads>>>(out, in, iters / 8); }, lanes / 8 * UNROLL * CHAINS)};
     printf("{\"sms\": %d, \"clock_attr_mhz\": %.0f", sms, clk_khz / 1e3);
     for (auto& r : res) printf(", \"%s_Tops\": %.3f, \"%s_per_sm_clk_at_attr\": %.1f", r.name, r.v / 1e12, r.name, r.v * per_clk_sm);
     printf("}\n");
