@@ -126,6 +126,8 @@ CVG_API const char* cvg_version(void);
  * per-target constants and glibc tables on the host, copies them to the
  * device, runs the fused kernel, and copies counts + pairs back. */
 CVG_API int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out);
+/* validation only (no device needed): CVG_OK or the status/message cvg_search would fail with */
+CVG_API int cvg_validate(const cvg_search_desc* desc);
 CVG_API void cvg_result_free(cvg_result* res);
 
 /* ---- plan API: device-resident repeated runs (benchmarks, pipelines) -----

@@ -225,7 +225,10 @@ PYBIND11_MODULE(_core, m) {
         });
 
     py::class_<ColorPair>(m, "ColorPair")
-        .def(py::init<>())
+        .def(py::init([](SrgbColor target, SrgbColor plus, SrgbColor minus, double radius, double angle,
+                         ChannelDeltas deltas) { return ColorPair{target, plus, minus, radius, angle, deltas}; }),
+             py::arg("target") = SrgbColor{}, py::arg("plus") = SrgbColor{}, py::arg("minus") = SrgbColor{},
+             py::arg("radius") = 0.0, py::arg("angle") = 0.0, py::arg("deltas") = ChannelDeltas{})
         .def_readonly("target", &ColorPair::target)
         .def_readonly("plus", &ColorPair::plus)
         .def_readonly("minus", &ColorPair::minus)

@@ -983,6 +983,8 @@ int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out) {
     return e;
 }
 
+int cvg_validate(const cvg_search_desc* desc) { return validate_desc(desc); }
+
 void cvg_result_free(cvg_result* r) {
     if (!r) return;
     std::free(r->counts);
