@@ -21,6 +21,7 @@
 #include <mutex>
 #include <numbers>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/cvg.h"
@@ -476,6 +477,7 @@ struct cvg_plan {
     bool ran = false;
     cudaStream_t last_stream = nullptr;
     uint64_t input_bytes = 0;
+    int32_t n_unique = 0;
     double t_prep_end = 0, t_upload_end = 0;
 };
 
@@ -527,6 +529,68 @@ T* at(void* base, size_t off) {
     return reinterpret_cast<T*>(static_cast<unsigned char*>(base) + off);
 }
 
+// sc_index[s] -> record of search s; uniq[u] -> first search with record u.
+// sc_index stays empty when every search is distinct (identity mapping).
+void dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, std::vector<int32_t>& uniq) {
+    const int n = d->n_searches;
+    sc_index.clear();
+    uniq.clear();
+    bool uniform = true;
+    for (int s = 1; s < n && uniform; ++s) {
+        uniform = d->pattern_bits[s] == d->pattern_bits[0] && d->v_th[s] == d->v_th[0] &&
+                  d->r_novib[s] == d->r_novib[0];
+    }
+    auto key24 = [&](int s) {
+        const int32_t* t = d->target_rgb + 3 * s;
+        return static_cast<uint32_t>(t[0]) << 16 | static_cast<uint32_t>(t[1]) << 8 | static_cast<uint32_t>(t[2]);
+    };
+    sc_index.resize(n);
+    if (uniform && n > 4096) {
+        // same classifier everywhere: a direct table over the 2^24 colors
+        std::vector<int32_t> table(1u << 24, -1);
+        for (int s = 0; s < n; ++s) {
+            int32_t& slot = table[key24(s)];
+            if (slot < 0) {
+                slot = static_cast<int32_t>(uniq.size());
+                uniq.push_back(s);
+            }
+            sc_index[s] = static_cast<uint32_t>(slot);
+        }
+    } else {
+        struct Key {
+            uint32_t rgb;
+            int32_t bits;
+            double v, r;
+            bool operator==(const Key& o) const {
+                return rgb == o.rgb && bits == o.bits && std::memcmp(&v, &o.v, 8) == 0 &&
+                       std::memcmp(&r, &o.r, 8) == 0;
+            }
+        };
+        struct Hash {
+            size_t operator()(const Key& k) const {
+                uint64_t a, b;
+                std::memcpy(&a, &k.v, 8);
+                std::memcpy(&b, &k.r, 8);
+                uint64_t h = (static_cast<uint64_t>(k.rgb) << 3 | static_cast<uint64_t>(k.bits)) * 0x9E3779B97F4A7C15ull;
+                h ^= a + 0x632BE59BD9B4E019ull + (h << 6) + (h >> 2);
+                h ^= b + 0x85157AF5ull + (h << 6) + (h >> 2);
+                return static_cast<size_t>(h);
+            }
+        };
+        std::unordered_map<Key, int32_t, Hash> seen;
+        seen.reserve(static_cast<size_t>(n) * 2);
+        for (int s = 0; s < n; ++s) {
+            const Key k{key24(s), d->pattern_bits[s], d->v_th[s], d->r_novib[s]};
+            auto [it, fresh] = seen.emplace(k, static_cast<int32_t>(uniq.size()));
+            if (fresh) uniq.push_back(s);
+            sc_index[s] = static_cast<uint32_t>(it->second);
+        }
+    }
+    if (static_cast<int>(uniq.size()) == n) {
+        sc_index.clear();  // all distinct: records are in search order
+    }
+}
+
 int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     const Tables& T = tables();
     p->ctx = ctx;
@@ -547,9 +611,16 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     if (n_tiles >= (1ull << 28)) return fail(CVG_EINVAL, "batch too large for one plan (split the searches)");
 
     // ---- host tables ----
-    std::vector<SearchConst> sc(p->n);
+    // Per-search constants, deduplicated: searches with the same (target,
+    // pattern, v_th, r_novib) share one record (per-pixel batches repeat
+    // colors); every candidate of every search is still evaluated.
+    std::vector<uint32_t> sc_index;
+    std::vector<int32_t> uniq;  // representative search of each record
+    dedup_searches(d, sc_index, uniq);
+    std::vector<SearchConst> sc(uniq.size());
     const double rmax = d->radii[p->nr - 1];
-    for (int s = 0; s < p->n; ++s) make_search_const(d, s, rmax, p->mode, T, sc[s]);
+    for (size_t u = 0; u < uniq.size(); ++u) make_search_const(d, uniq[u], rmax, p->mode, T, sc[u]);
+    p->n_unique = static_cast<int32_t>(uniq.size());
     std::vector<float> radii_f(p->nr);
     for (int k = 0; k < p->nr; ++k) radii_f[k] = static_cast<float>(d->radii[k]);
     // float trig table padded by 128 entries: the hot loop prefetches two chunks ahead
@@ -576,6 +647,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     // ---- one constant blob: [sc | radii_d | radii_f | trig_d | trig_f | thr_d | thr_f | guess] ----
     Layout L;
     const size_t o_sc = L.take(sizeof(SearchConst) * sc.size());
+    const size_t o_si = L.take(sizeof(uint32_t) * sc_index.size());
     const size_t o_rd = L.take(sizeof(double) * p->nr);
     const size_t o_rf = L.take(sizeof(float) * p->nr);
     const size_t o_td = L.take(sizeof(double) * trig_d.size());
@@ -594,6 +666,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
         return fail(CVG_ENOMEM, "allocation of the search tables failed");
     }
     std::memcpy(stage + o_sc, sc.data(), sizeof(SearchConst) * sc.size());
+    if (!sc_index.empty()) std::memcpy(stage + o_si, sc_index.data(), sizeof(uint32_t) * sc_index.size());
     std::memcpy(stage + o_rd, d->radii, sizeof(double) * p->nr);
     std::memcpy(stage + o_rf, radii_f.data(), sizeof(float) * p->nr);
     std::memcpy(stage + o_td, trig_d.data(), sizeof(double) * trig_d.size());
@@ -605,6 +678,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     LaunchArgs& A = p->args;
     std::memset(&A, 0, sizeof(A));
     A.sc = at<const SearchConst>(p->d_const, o_sc);
+    A.sc_index = sc_index.empty() ? nullptr : at<const uint32_t>(p->d_const, o_si);
     A.radii_d = at<const double>(p->d_const, o_rd);
     A.radii_f = at<const float>(p->d_const, o_rf);
     A.trig_d = at<const double>(p->d_const, o_td);

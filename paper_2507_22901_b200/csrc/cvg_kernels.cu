@@ -67,6 +67,10 @@ __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long 
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+__device__ __forceinline__ const SearchConst* search_const(const LaunchArgs& A, uint32_t s) {
+    return A.sc + (A.sc_index ? __ldg(&A.sc_index[s]) : s);
+}
+
 __device__ __forceinline__ uint32_t div_na(uint32_t i, const LaunchArgs& A) {
     return A.na == 1 ? i : static_cast<uint32_t>(__umul64hi(static_cast<uint64_t>(i), A.na_magic));
 }
@@ -494,7 +498,7 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         if (lane == 0) t_claim = atomicAdd(&A.ticket[0], 1u);  // next tile, consumed at the end
         const uint32_t s = t / A.tiles_per_search;
         const uint32_t lt = t - s * A.tiles_per_search;
-        const SearchConst* S = A.sc + s;
+        const SearchConst* S = search_const(A, s);
         const uint32_t i0 = lt * static_cast<uint32_t>(kTile);
         const uint32_t i1 = min(i0 + static_cast<uint32_t>(kTile), A.cand_per_search);
         uint16_t* list = kOut == kOutPairs ? A.scratch + static_cast<size_t>(t) * kTile : nullptr;
@@ -646,7 +650,7 @@ __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
         } else {
             const uint32_t s = t / A.tiles_per_search;
             const uint32_t i0 = (t - s * A.tiles_per_search) * static_cast<uint32_t>(kTile);
-            const SearchConst* S = A.sc + s;
+            const SearchConst* S = search_const(A, s);
             CodeConsts CC;
             load_code_consts(S, CC);
             uint32_t next = list[lane < cnt ? lane : 0];
@@ -698,7 +702,7 @@ __global__ void first_codes_kernel(const LaunchArgs A) {
     const uint32_t k = div_na(i, A);
     const uint32_t m = i - k * static_cast<uint32_t>(A.na);
     double lp[3], lm[3];
-    exact_linear(A.sc + s, A, k, m, lp, lm);
+    exact_linear(search_const(A, s), A, k, m, lp, lm);
     for (int q = 0; q < 3; ++q) {
         out[q] = static_cast<uint8_t>(code_exact(lp[q], thr));
         out[3 + q] = static_cast<uint8_t>(code_exact(lm[q], thr));

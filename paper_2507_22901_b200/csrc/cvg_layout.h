@@ -63,7 +63,8 @@ enum Path : int { kPathFast = 0, kPathExact = 1, kPathAudit = 2 };
 
 // Everything one launch needs (passed by value as the kernel parameter).
 struct LaunchArgs {
-    const SearchConst* sc;     // [n_searches]
+    const SearchConst* sc;     // [n_unique] per-search constant records
+    const uint32_t* sc_index;  // [n_searches] record of each search, nullptr = identity
     const float* radii_f;      // [nr]
     const double* radii_d;     // [nr]
     const float* trig_f;       // [na][2] = (sin/500, cos/200) as float

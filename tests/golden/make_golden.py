@@ -7,6 +7,7 @@ build container (where /root/reference exists):
 
     python tests/golden/make_golden.py            # everything but cfg2
     python tests/golden/make_golden.py --cfg2     # + cfg2 per-target counts (minutes)
+    python tests/golden/make_golden.py --cfg4     # + full-size cfg4 per-pixel count/first hash
 
 Outputs (all small, committed):
   known_answers.json    thresholds, kXyzToRgb, d65 white, target Lab, code probes
@@ -98,8 +99,8 @@ def workload_records(ref: Reference, wl: W.Workload, workers: int) -> dict:
 
 
 def cfg4_small(ref: Reference, width=256, height=144) -> dict:
-    """cfg4 pipeline on a reduced image (same generator): per-pixel count and
-    first canonical pair, memoized by color (results depend only on it)."""
+    """cfg4 pipeline (same generator, any size): per-pixel count and first
+    canonical pair, memoized by color (results depend only on it)."""
     img = W.voronoi_image(width, height)
     wl = W.cfg4(width, height)
     flat = img.reshape(-1, 3).astype(np.int32)
@@ -143,6 +144,7 @@ def aggregated_matrix(ref: Reference) -> str:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg2", action="store_true")
+    ap.add_argument("--cfg4", action="store_true", help="full 3840x2160 per-pixel config (memoized by color)")
     ap.add_argument("--workers", type=int, default=os.cpu_count() or 1)
     args = ap.parse_args()
     ref = Reference()
@@ -159,6 +161,8 @@ def main():
     wj["cfg1"] = workload_records(ref, W.cfg1(), args.workers)
     wj["cfg3"] = workload_records(ref, W.cfg3(), args.workers)
     wj["cfg4_256x144"] = cfg4_small(ref)
+    if args.cfg4:
+        wj["cfg4"] = cfg4_small(ref, 3840, 2160)
     if args.cfg2:
         wl = W.cfg2()
         counts = ref.search_many(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles,

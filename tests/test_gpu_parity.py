@@ -125,6 +125,40 @@ def test_cfg4_first_pair_mode_crop(ctx):
     assert m.hexdigest() == g["sha256"]
 
 
+def test_duplicate_searches_share_constants(ctx):
+    """Repeated (target, pattern, thresholds) share one constant record
+    (hash dedup path); every search still gets its own full result."""
+    wl = W.cfg1()
+    rep = W.Workload("rep", np.concatenate([wl.targets, wl.targets[::-1]]),
+                     np.concatenate([wl.patterns, wl.patterns[::-1]]), np.concatenate([wl.v_th, wl.v_th[::-1]]),
+                     np.concatenate([wl.r_novib, wl.r_novib[::-1]]), wl.radii, wl.angles)
+    res = run(ctx, rep)
+    g = golden("workloads.json")["cfg1"]["counts"]
+    assert res["counts"].tolist() == g + g[::-1]
+    n = wl.n_searches
+    for s in (0, 100, 755):
+        a_idx, a_codes = split(res, s)
+        b_idx, b_codes = split(res, 2 * n - 1 - s)
+        assert np.array_equal(a_idx, b_idx) and np.array_equal(a_codes, b_codes)
+
+
+@pytest.mark.slow
+def test_cfg4_full_image_first_pair(ctx):
+    g = golden("workloads.json").get("cfg4")
+    if not g:
+        pytest.skip("cfg4 golden not generated")
+    wl = W.cfg4()
+    res = run(ctx, wl, output="first")
+    import hashlib
+
+    m = hashlib.sha256()
+    m.update(res["counts"].astype(np.uint64).tobytes())
+    m.update(np.ascontiguousarray(res["first_idx"], np.uint32).tobytes())
+    m.update(np.ascontiguousarray(res["first_codes"], np.uint8).tobytes())
+    assert int(res["counts"].sum()) == g["total"]
+    assert m.hexdigest() == g["sha256"]
+
+
 @pytest.mark.slow
 def test_cfg2_fine_grid_counts_and_rows(ctx, oracle):
     wl = W.cfg2()
