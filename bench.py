@@ -226,7 +226,7 @@ def run_ours(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dist = None
-    if world > 1:
+    if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:  # under torchrun: NCCL even for one rank
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))

@@ -140,7 +140,7 @@ void to_linear(const double lab[3], const double* wp, double lin[3]) {
 // found by bisection over the glibc-pow quantizer (convert_kernel.hpp:127-141).
 struct Tables {
     double thr[256];
-    float thr_f[258];
+    float thr3[256][4];  // {tf[g], tf[g+1], tf[g+2], 0}: tf[0] = -inf, tf[c] = float(thr[c]), tf[256..] = +inf
     uint8_t guess[cvg::kGuessBuckets + 1];
     Tables() {
         thr[0] = 0.0;
@@ -152,11 +152,19 @@ struct Tables {
             }
             thr[code] = hi;
         }
-        thr_f[0] = -INFINITY;
-        for (int c = 1; c < 256; ++c) thr_f[c] = static_cast<float>(thr[c]);
-        thr_f[256] = INFINITY;
-        thr_f[257] = INFINITY;
-        for (int i = 0; i <= cvg::kGuessBuckets; ++i) guess[i] = static_cast<uint8_t>(code(i / 4096.0));
+        float tf[258];
+        tf[0] = -INFINITY;
+        for (int c = 1; c < 256; ++c) tf[c] = static_cast<float>(thr[c]);
+        tf[256] = tf[257] = INFINITY;
+        for (int g = 0; g < 256; ++g) {
+            thr3[g][0] = tf[g];
+            thr3[g][1] = tf[g + 1];
+            thr3[g][2] = tf[g + 2];
+            thr3[g][3] = 0.0f;
+        }
+        // Round-to-nearest buckets: bucket i holds x * 4096 in [i - 1/2, i + 1/2);
+        // guess = code at the bucket's lower edge (<= 1 threshold per bucket).
+        for (int i = 0; i <= cvg::kGuessBuckets; ++i) guess[i] = static_cast<uint8_t>(code((i - 0.5) / 4096.0));
     }
     int code(double x) const {
         if (x <= 0.0) return 0;
@@ -644,7 +652,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
         b[1] = std::max(b[1], round_up_f(std::fabs(trig_d[2 * j + 1]) * kInv200 * (1.0 + 1e-12)));
     }
 
-    // ---- one constant blob: [sc | radii_d | radii_f | trig_d | trig_f | thr_d | thr_f | guess] ----
+    // ---- one constant blob: [sc | sc_index | radii | trig | chunk bounds | thresholds | guess] ----
     Layout L;
     const size_t o_sc = L.take(sizeof(SearchConst) * sc.size());
     const size_t o_si = L.take(sizeof(uint32_t) * sc_index.size());
@@ -654,7 +662,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     const size_t o_tf = L.take(sizeof(float) * trig_f.size());
     const size_t o_cb = L.take(sizeof(float) * chunk_bound.size());
     const size_t o_thd = L.take(sizeof(double) * 256);
-    const size_t o_thf = L.take(sizeof(float) * 258);
+    const size_t o_thf = L.take(sizeof(float) * 256 * 4);
     const size_t o_gs = L.take(cvg::kGuessBuckets + 1);
     const size_t bytes = L.off;
     p->input_bytes = bytes;
@@ -673,7 +681,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     std::memcpy(stage + o_tf, trig_f.data(), sizeof(float) * trig_f.size());
     std::memcpy(stage + o_cb, chunk_bound.data(), sizeof(float) * chunk_bound.size());
     std::memcpy(stage + o_thd, T.thr, sizeof(double) * 256);
-    std::memcpy(stage + o_thf, T.thr_f, sizeof(float) * 258);
+    std::memcpy(stage + o_thf, T.thr3, sizeof(float) * 256 * 4);
     std::memcpy(stage + o_gs, T.guess, cvg::kGuessBuckets + 1);
     LaunchArgs& A = p->args;
     std::memset(&A, 0, sizeof(A));
@@ -685,7 +693,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     A.trig_f = at<const float>(p->d_const, o_tf);
     A.chunk_bound = at<const float>(p->d_const, o_cb);
     A.thr_d = at<const double>(p->d_const, o_thd);
-    A.thr_f = at<const float>(p->d_const, o_thf);
+    A.thr3 = at<const float>(p->d_const, o_thf);
     A.guess = at<const uint8_t>(p->d_const, o_gs);
     cudaError_t e = cudaMemcpyAsync(p->d_const, stage, bytes, cudaMemcpyHostToDevice, ctx->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
@@ -698,7 +706,6 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     A.nr = p->nr;
     A.na = p->na;
     A.aligned = (p->na % 32) == 0;
-    A.emit_exact = std::getenv("CVG_EMIT_EXACT") ? std::atoi(std::getenv("CVG_EMIT_EXACT")) : 0;
     A.tiles_per_search = tps;
     A.cand_per_search = static_cast<uint32_t>(cps);
     A.na_magic = p->na > 1 ? (UINT64_MAX / static_cast<uint64_t>(p->na)) + 1 : 0;

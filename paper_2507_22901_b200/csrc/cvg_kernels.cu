@@ -247,27 +247,42 @@ __device__ __forceinline__ float band_G(const Consts& C, const float* dp, const 
     return fmaxf(fmaxf(g[0], g[1]), g[2]);
 }
 
-// Linear value -> code through the float table, verified against the bound:
-// ok iff thr[c] + E < x < thr[c+1] - E, which proves code(x64) == c.
-__device__ __forceinline__ int code_fast(float x, float E, const float* tf, const uint8_t* guess, bool& ok) {
-    int i = __float2int_rz(x * static_cast<float>(kGuessBuckets));
-    i = min(max(i, 0), kGuessBuckets);
-    const int g = guess[i];
-    const int c = g + (x >= tf[g + 1]);
-    ok = (__fsub_rn(x, tf[c]) > E) & (__fsub_rn(tf[c + 1], x) > E);
+// Linear value -> code through the float tables, verified against the bound:
+// the bucket of x (round-to-nearest, x saturated to [0, 1]) gives g; one
+// 16-byte load gives thr[g..g+2]; c = g + (x >= thr[g+1]); ok iff
+// thr[c] + E < x < thr[c+1] - E, which proves code(x64) == c.
+__device__ __forceinline__ int code_fast(float x, float E, const float4* t3, const uint8_t* guess, bool& ok) {
+    const float b = fmaf(__saturatef(x), static_cast<float>(kGuessBuckets), 8388608.0f);  // 2^23 + round(x * 4096)
+    const int g = guess[__float_as_int(b) - 0x4B000000];
+    const float4 T = t3[g];
+    const bool up = x >= T.y;
+    const float lo = up ? T.y : T.x;
+    const float hi = up ? T.z : T.y;
+    ok = (__fsub_rn(x, lo) > E) & (__fsub_rn(hi, x) > E);
+    return g + up;
+}
+
+// Exact code from a nearby guess (the FP32 code is off by at most one).
+__device__ __forceinline__ int code_exact_from(double x, int c, const double* thr) {
+    if (x <= 0.0) return 0;
+    if (x >= 1.0) return 255;
+    while (c < 255 && x >= thr[c + 1]) ++c;
+    while (c > 0 && x < thr[c]) --c;
     return c;
 }
 
 // Shared tables: exact and float quantization thresholds + code guesses.
 struct Smem {
+    float4 t3[256];     // {tf[g], tf[g+1], tf[g+2], 0}
     double thr_d[256];
-    float thr_f[258];  // [0] = -inf, [c] = float(thr[c]), [256] = +inf
     uint8_t guess[kGuessBuckets + 16];
 };
 
 __device__ __forceinline__ void load_tables(Smem& sm, const LaunchArgs& A) {
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) sm.thr_d[i] = A.thr_d[i];
-    for (int i = threadIdx.x; i < 258; i += blockDim.x) sm.thr_f[i] = A.thr_f[i];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+        sm.thr_d[i] = A.thr_d[i];
+        sm.t3[i] = reinterpret_cast<const float4*>(A.thr3)[i];
+    }
     for (int i = threadIdx.x; i <= kGuessBuckets; i += blockDim.x) sm.guess[i] = A.guess[i];
     __syncthreads();
 }
@@ -307,57 +322,76 @@ __device__ __forceinline__ void audit_ratio(const SearchConst* S, const float* v
     }
 }
 
-// Codes of the six endpoint channels of candidate (k, m), exact: FP32 value
-// + table lookup verified against the bound, FP64 for unverified lanes.
-// Called by all 32 lanes (warp votes inside).
+// Codes of the six endpoint channels of one candidate from its FP32 values,
+// exact: values whose code is not proven by the bound go to FP64 (all six
+// values recomputed op-for-op, codes walked from the FP32 guess).  Called by
+// all 32 lanes (warp vote inside).
+__device__ __forceinline__ void codes_fast(const Smem& sm, const SearchConst* S, const CodeConsts& C,
+                                           const LaunchArgs& A, uint32_t k, uint32_t m, float r, float2 sc,
+                                           bool active, int* cp, int* cm, unsigned long long& repairs) {
+    float vp[3], vm[3];
+    fast_linear<false>(C.fx0, C.fz0, C.mx, C.mz, C.cy, r, sc, vp, vm);
+    bool all_ok = true;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        bool ok1, ok2;
+        cp[q] = code_fast(vp[q], C.ec[q], sm.t3, sm.guess, ok1);
+        cm[q] = code_fast(vm[q], C.ec[q], sm.t3, sm.guess, ok2);
+        all_ok &= ok1 & ok2;
+    }
+    if (__any_sync(kFull, !all_ok) && !all_ok) {
+        double lp[3], lm[3];
+        exact_linear(S, A, k, m, lp, lm);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            cp[q] = code_exact_from(lp[q], cp[q], sm.thr_d);
+            cm[q] = code_exact_from(lm[q], cm[q], sm.thr_d);
+        }
+        if (active) ++repairs;
+    }
+}
+
+// Codes of candidate (k, m) for any path (EXACT: FP64 only; AUDIT: both,
+// counting FP32 codes that were "verified" but wrong).
 template <int kPath>
 __device__ __forceinline__ void candidate_codes(const Smem& sm, const SearchConst* S, const CodeConsts& C,
                                                 const LaunchArgs& A, uint32_t k, uint32_t m, bool active,
                                                 int* cp, int* cm, unsigned long long& repairs, Counters& ct) {
-    bool need_exact = true;
-    if (kPath != kPathExact) {
-        float vp[3], vm[3];
-        const float r = __ldg(&A.radii_f[k]);
-        const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + m);
-        fast_linear<false>(C.fx0, C.fz0, C.mx, C.mz, C.cy, r, sc, vp, vm);
-        bool all_ok = true;
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            bool ok1, ok2;
-            cp[q] = code_fast(vp[q], C.ec[q], sm.thr_f, sm.guess, ok1);
-            cm[q] = code_fast(vm[q], C.ec[q], sm.thr_f, sm.guess, ok2);
-            all_ok &= ok1 & ok2;
-        }
-        if (kPath == kPathAudit) {
-            double lp[3], lm[3];
-            exact_linear(S, A, k, m, lp, lm);
-            bool wrong = false;
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                const int ep = code_exact(lp[q], sm.thr_d), em = code_exact(lm[q], sm.thr_d);
-                wrong |= (ep != cp[q]) | (em != cm[q]);
-                cp[q] = ep;
-                cm[q] = em;
-            }
-            if (active) {
-                ct.violations += all_ok && wrong;
-                repairs += !all_ok;
-                audit_ratio(S, vp, vm, lp, lm, ct.max_ratio);
-            }
-            return;
-        }
-        need_exact = !all_ok;
-        if (!__any_sync(kFull, need_exact)) return;
-        if (need_exact && active) ++repairs;
+    const float r = __ldg(&A.radii_f[k]);
+    const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + m);
+    if (kPath == kPathFast) {
+        codes_fast(sm, S, C, A, k, m, r, sc, active, cp, cm, repairs);
+        return;
     }
-    if (need_exact) {
-        double lp[3], lm[3];
-        exact_linear(S, A, k, m, lp, lm);
+    double lp[3], lm[3];
+    exact_linear(S, A, k, m, lp, lm);
+    if (kPath == kPathExact) {
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             cp[q] = code_exact(lp[q], sm.thr_d);
             cm[q] = code_exact(lm[q], sm.thr_d);
         }
+        return;
+    }
+    float vp[3], vm[3];
+    fast_linear<false>(C.fx0, C.fz0, C.mx, C.mz, C.cy, r, sc, vp, vm);
+    bool all_ok = true, wrong = false;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        bool ok1, ok2;
+        const int fp = code_fast(vp[q], C.ec[q], sm.t3, sm.guess, ok1);
+        const int fm = code_fast(vm[q], C.ec[q], sm.t3, sm.guess, ok2);
+        all_ok &= ok1 & ok2;
+        cp[q] = code_exact(lp[q], sm.thr_d);
+        cm[q] = code_exact(lm[q], sm.thr_d);
+        wrong |= (ok1 && fp != cp[q]) | (ok2 && fm != cm[q]);
+        // the FP64 walk from the FP32 guess must agree with the binary search
+        wrong |= (code_exact_from(lp[q], fp, sm.thr_d) != cp[q]) | (code_exact_from(lm[q], fm, sm.thr_d) != cm[q]);
+    }
+    if (active) {
+        ct.violations += wrong;
+        repairs += !all_ok;
+        audit_ratio(S, vp, vm, lp, lm, ct.max_ratio);
     }
 }
 
@@ -627,7 +661,7 @@ __global__ void __launch_bounds__(kBlock) scan_kernel(const LaunchArgs A) {
 // (next claim prefetched), so no warp holds more than 8 chunks of work; the
 // item's list entries are read one chunk ahead.
 template <int kMode, int kPath>
-__global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
+__global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     load_tables(sm, A);
@@ -653,31 +687,62 @@ __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
             const SearchConst* S = search_const(A, s);
             CodeConsts CC;
             load_code_consts(S, CC);
-            uint32_t next = list[lane < cnt ? lane : 0];
+            if (kPath == kPathFast) {
+                // Software pipeline: list entries two iterations ahead, the
+                // candidate's radius/trig loads one iteration ahead.
+                const float2* trig = reinterpret_cast<const float2*>(A.trig_f);
+                const uint32_t last = cnt - 1;
+                uint32_t off_n = list[min(32 + lane, last)];
+                uint32_t i = i0 + list[min(lane, last)];
+                uint32_t k = div_na(i, A);
+                uint32_t m = i - k * static_cast<uint32_t>(A.na);
+                float r = __ldg(&A.radii_f[k]);
+                float2 sc = __ldg(trig + m);
 #pragma unroll 1
-            for (uint32_t p = 0; p < cnt; p += 32) {
-                const uint32_t qq = p + lane;
-                const bool active = qq < cnt;
-                const uint32_t i = i0 + next;
-                if (p + 32 < cnt) next = list[qq + 32 < cnt ? qq + 32 : p + 32];  // one chunk ahead
-                const uint32_t k = div_na(i, A);
-                const uint32_t m = i - k * static_cast<uint32_t>(A.na);
-                int cp[3], cm[3];
-                if (kPath == kPathFast && A.emit_exact) {
-                    candidate_codes<kPathExact>(sm, S, CC, A, k, m, active, cp, cm, ct.code_repairs, ct);
-                } else {
-                    candidate_codes<kPath>(sm, S, CC, A, k, m, active, cp, cm, ct.code_repairs, ct);
-                }
-                if (active) {
-                    if (kMode == kModeBand && kPath != kPathFast && !classify_codes(S, cp, cm, __ldg(&S->flags))) {
-                        ++ct.mismatch;
+                for (uint32_t p = 0; p < cnt; p += 32) {
+                    const uint32_t i_n = i0 + off_n;
+                    const uint32_t k_n = div_na(i_n, A);
+                    const uint32_t m_n = i_n - k_n * static_cast<uint32_t>(A.na);
+                    const float r_n = __ldg(&A.radii_f[k_n]);
+                    const float2 sc_n = __ldg(trig + m_n);
+                    off_n = list[min(p + 64 + lane, last)];
+                    const uint32_t qq = p + lane;
+                    const bool active = qq < cnt;
+                    int cp[3], cm[3];
+                    codes_fast(sm, S, CC, A, k, m, r, sc, active, cp, cm, ct.code_repairs);
+                    if (active) {
+                        const unsigned long long o = base + qq;
+                        A.out_idx[o] = i;
+                        uint16_t* c16 = reinterpret_cast<uint16_t*>(A.out_codes + 6 * o);
+                        c16[0] = static_cast<uint16_t>(cp[0] | (cp[1] << 8));
+                        c16[1] = static_cast<uint16_t>(cp[2] | (cm[0] << 8));
+                        c16[2] = static_cast<uint16_t>(cm[1] | (cm[2] << 8));
                     }
-                    const unsigned long long o = base + qq;
-                    A.out_idx[o] = i;
-                    uint16_t* c16 = reinterpret_cast<uint16_t*>(A.out_codes + 6 * o);
-                    c16[0] = static_cast<uint16_t>(cp[0] | (cp[1] << 8));
-                    c16[1] = static_cast<uint16_t>(cp[2] | (cm[0] << 8));
-                    c16[2] = static_cast<uint16_t>(cm[1] | (cm[2] << 8));
+                    i = i_n;
+                    k = k_n;
+                    m = m_n;
+                    r = r_n;
+                    sc = sc_n;
+                }
+            } else {
+#pragma unroll 1
+                for (uint32_t p = 0; p < cnt; p += 32) {
+                    const uint32_t qq = p + lane;
+                    const bool active = qq < cnt;
+                    const uint32_t i = i0 + list[active ? qq : 0];
+                    const uint32_t k = div_na(i, A);
+                    const uint32_t m = i - k * static_cast<uint32_t>(A.na);
+                    int cp[3], cm[3];
+                    candidate_codes<kPath>(sm, S, CC, A, k, m, active, cp, cm, ct.code_repairs, ct);
+                    if (active) {
+                        if (kMode == kModeBand && !classify_codes(S, cp, cm, __ldg(&S->flags))) ++ct.mismatch;
+                        const unsigned long long o = base + qq;
+                        A.out_idx[o] = i;
+                        uint16_t* c16 = reinterpret_cast<uint16_t*>(A.out_codes + 6 * o);
+                        c16[0] = static_cast<uint16_t>(cp[0] | (cp[1] << 8));
+                        c16[1] = static_cast<uint16_t>(cp[2] | (cm[0] << 8));
+                        c16[2] = static_cast<uint16_t>(cm[1] | (cm[2] << 8));
+                    }
                 }
             }
         }

@@ -71,14 +71,13 @@ struct LaunchArgs {
     const double* trig_d;      // [na][2] = (sin, cos), glibc doubles (search.cpp:414-419)
     const float* chunk_bound;  // [na/32 + 4][2] max |sin|/500, max |cos|/200 per 32-angle chunk (rounded up)
     const double* thr_d;       // [256] QuantTable thresholds (convert_kernel.hpp:123-141)
-    const float* thr_f;        // [257] thresholds rounded to float, [256] = +inf
-    const uint8_t* guess;      // [kGuessBuckets + 1] code(i / 4096)
+    const float* thr3;         // [256][4] {tf[g], tf[g+1], tf[g+2], 0}, tf = thresholds as float, tf[0] = -inf
+    const uint8_t* guess;      // [kGuessBuckets + 1] code((i - 1/2) / 4096): round-to-nearest buckets
     double minv[9];            // kXyzToRgb (convert_kernel.hpp:47), row-major
     int32_t n_searches;
     int32_t nr;
     int32_t na;
     int32_t aligned;           // na % 32 == 0: a 32-candidate chunk never straddles rows
-    int32_t emit_exact;        // emit codes through the FP64 path (experiment knob, CVG_EMIT_EXACT)
     uint32_t tiles_per_search;
     uint32_t cand_per_search;  // nr * na (< 2^32)
     uint64_t na_magic;         // ceil(2^64 / na): k = umul64hi(i, na_magic)
