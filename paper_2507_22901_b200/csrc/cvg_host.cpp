@@ -643,16 +643,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
         trig_f[2 * j + 1] = static_cast<float>(cs * kInv200);
     }
 
-    // per 32-angle chunk: max |sin|/500 and max |cos|/200 (rounded up), padded
-    const size_t n_chunks = static_cast<size_t>(p->na) / 32 + 4;
-    std::vector<float> chunk_bound(2 * n_chunks, 0.0f);
-    for (int j = 0; j < p->na; ++j) {
-        float* b = &chunk_bound[2 * (j / 32)];
-        b[0] = std::max(b[0], round_up_f(std::fabs(trig_d[2 * j]) * kInv500 * (1.0 + 1e-12)));
-        b[1] = std::max(b[1], round_up_f(std::fabs(trig_d[2 * j + 1]) * kInv200 * (1.0 + 1e-12)));
-    }
-
-    // ---- one constant blob: [sc | sc_index | radii | trig | chunk bounds | thresholds | guess] ----
+    // ---- one constant blob: [sc | sc_index | radii | trig | thresholds | guess] ----
     Layout L;
     const size_t o_sc = L.take(sizeof(SearchConst) * sc.size());
     const size_t o_si = L.take(sizeof(uint32_t) * sc_index.size());
@@ -660,7 +651,6 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     const size_t o_rf = L.take(sizeof(float) * p->nr);
     const size_t o_td = L.take(sizeof(double) * trig_d.size());
     const size_t o_tf = L.take(sizeof(float) * trig_f.size());
-    const size_t o_cb = L.take(sizeof(float) * chunk_bound.size());
     const size_t o_thd = L.take(sizeof(double) * 256);
     const size_t o_thf = L.take(sizeof(float) * 256 * 4);
     const size_t o_gs = L.take(cvg::kGuessBuckets + 1);
@@ -679,7 +669,6 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     std::memcpy(stage + o_rf, radii_f.data(), sizeof(float) * p->nr);
     std::memcpy(stage + o_td, trig_d.data(), sizeof(double) * trig_d.size());
     std::memcpy(stage + o_tf, trig_f.data(), sizeof(float) * trig_f.size());
-    std::memcpy(stage + o_cb, chunk_bound.data(), sizeof(float) * chunk_bound.size());
     std::memcpy(stage + o_thd, T.thr, sizeof(double) * 256);
     std::memcpy(stage + o_thf, T.thr3, sizeof(float) * 256 * 4);
     std::memcpy(stage + o_gs, T.guess, cvg::kGuessBuckets + 1);
@@ -691,7 +680,6 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     A.radii_f = at<const float>(p->d_const, o_rf);
     A.trig_d = at<const double>(p->d_const, o_td);
     A.trig_f = at<const float>(p->d_const, o_tf);
-    A.chunk_bound = at<const float>(p->d_const, o_cb);
     A.thr_d = at<const double>(p->d_const, o_thd);
     A.thr3 = at<const float>(p->d_const, o_thf);
     A.guess = at<const uint8_t>(p->d_const, o_gs);

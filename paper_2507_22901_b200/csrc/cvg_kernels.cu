@@ -49,9 +49,7 @@ constexpr double kInv200 = 1.0 / 200.0;
 constexpr float kU0f = 6.0f / 29.0f;
 constexpr float kK1f = 3132.0f / 24389.0f;
 constexpr float kK2f = 432.0f / 24389.0f;
-// Chunk-level cube test margin: f > u0 + 1e-5 keeps every candidate of the
-// chunk on the cube branch with room for the FP32 rounding of the test.
-constexpr float kU0Safe = 6.0f / 29.0f + 1e-5f;
+
 
 constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagPrefix = 2ull << 62;

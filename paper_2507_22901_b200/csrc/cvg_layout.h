@@ -69,7 +69,6 @@ struct LaunchArgs {
     const double* radii_d;     // [nr]
     const float* trig_f;       // [na][2] = (sin/500, cos/200) as float
     const double* trig_d;      // [na][2] = (sin, cos), glibc doubles (search.cpp:414-419)
-    const float* chunk_bound;  // [na/32 + 4][2] max |sin|/500, max |cos|/200 per 32-angle chunk (rounded up)
     const double* thr_d;       // [256] QuantTable thresholds (convert_kernel.hpp:123-141)
     const float* thr3;         // [256][4] {tf[g], tf[g+1], tf[g+2], 0}, tf = thresholds as float, tf[0] = -inf
     const uint8_t* guess;      // [kGuessBuckets + 1] code((i - 1/2) / 4096): round-to-nearest buckets
