@@ -457,6 +457,8 @@ struct Pool {
 struct cvg_ctx {
     int device = 0;
     int sms = 0;
+    size_t total_mem = 0;
+    std::vector<cudaEvent_t> events;  // recycled timing events
     cudaStream_t stream = nullptr;
     std::recursive_mutex mu;
     Pool dev;
@@ -485,6 +487,7 @@ struct cvg_plan {
     bool ran = false;
     cudaStream_t last_stream = nullptr;
     uint64_t input_bytes = 0;
+    void* stage = nullptr;  // pinned staging of the constant blob (held until the plan is released)
     int32_t n_unique = 0;
     double t_prep_end = 0, t_upload_end = 0;
 };
@@ -683,9 +686,10 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     A.thr_d = at<const double>(p->d_const, o_thd);
     A.thr3 = at<const float>(p->d_const, o_thf);
     A.guess = at<const uint8_t>(p->d_const, o_gs);
+    // No sync: the staging block stays with the plan until it is released,
+    // which happens after the stream has passed this copy.
+    p->stage = stage;
     cudaError_t e = cudaMemcpyAsync(p->d_const, stage, bytes, cudaMemcpyHostToDevice, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
-    ctx->host.release(stage);
     if (e != cudaSuccess) return cuda_fail(e, "upload of the search tables");
     p->t_upload_end = now_ms();
 
@@ -749,14 +753,18 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     const uint64_t want = (n_tiles + cvg::kWarpsPerBlock - 1) / cvg::kWarpsPerBlock;
     p->grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(per_sm) * ctx->sms, want));
     if (p->grid < 1) p->grid = 1;
-    CVG_CUDA(cudaEventCreate(&p->ev0));
-    CVG_CUDA(cudaEventCreate(&p->ev1));
+    for (cudaEvent_t* ev : {&p->ev0, &p->ev1}) {
+        if (!ctx->events.empty()) {
+            *ev = ctx->events.back();
+            ctx->events.pop_back();
+        } else {
+            CVG_CUDA(cudaEventCreate(ev));
+        }
+    }
 
     if (p->out == cvg::kOutPairs) {
         // Initial capacity: every candidate when it fits in half the free memory.
-        size_t free_b = 0, total_b = 0;
-        cudaMemGetInfo(&free_b, &total_b);
-        const uint64_t fit = static_cast<uint64_t>(free_b / 2 / 10);
+        const uint64_t fit = static_cast<uint64_t>(ctx->total_mem / 4 / 10);  // a quarter of HBM at most
         uint64_t cap = std::min<uint64_t>(p->candidates, std::max<uint64_t>(fit, 1u << 20));
         if (int e2 = plan_reserve(p, cap)) return e2;
     }
@@ -770,8 +778,12 @@ void plan_release(cvg_plan* p) {
     p->ctx->dev.release(p->d_work);
     p->ctx->dev.release(p->d_first);
     p->ctx->dev.release(p->d_scratch);
-    if (p->ev0) cudaEventDestroy(p->ev0);
-    if (p->ev1) cudaEventDestroy(p->ev1);
+    if (p->stage) cudaStreamSynchronize(p->ctx->stream);  // the constant upload may still be in flight
+    if (p->ev0) p->ctx->events.push_back(p->ev0);
+    if (p->ev1) p->ctx->events.push_back(p->ev1);
+    p->ev0 = p->ev1 = nullptr;
+    p->ctx->host.release(p->stage);
+    p->stage = nullptr;
 }
 
 int plan_enqueue(cvg_plan* p, cudaStream_t st) {
@@ -909,6 +921,10 @@ int cvg_create(int device, cvg_ctx** out) {
     e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+        size_t free_b = 0;
+        e = cudaMemGetInfo(&free_b, &ctx->total_mem);
+    }
     if (e != cudaSuccess) {
         delete ctx;
         return cuda_fail(e, "context creation");
@@ -928,6 +944,7 @@ void cvg_destroy(cvg_ctx* ctx) {
             it = it->second == ctx ? g_owner.erase(it) : std::next(it);
         }
     }
+    for (cudaEvent_t ev : ctx->events) cudaEventDestroy(ev);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
 }

@@ -98,13 +98,14 @@ __device__ __forceinline__ void load_consts(const SearchConst* S, Consts& c) {
 
 // Constants for the code path (phase 2 and CODES mode).
 struct CodeConsts {
-    float fx0, fz0;
+    float fx0, fz0, rcube;
     float mx[3], mz[3], cy[3], ec[3];
 };
 
 __device__ __forceinline__ void load_code_consts(const SearchConst* S, CodeConsts& c) {
     c.fx0 = __ldg(&S->fx0);
     c.fz0 = __ldg(&S->fz0);
+    c.rcube = __ldg(&S->rcube);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         c.mx[q] = __ldg(&S->mx[q]);
@@ -123,8 +124,8 @@ __device__ __forceinline__ double finv_exact(double u) {
     return u3 > kLabEpsilon ? u3 : __dmul_rn(__dsub_rn(__dmul_rn(116.0, u), 16.0), kInvKappa);
 }
 
-__device__ __noinline__ void exact_linear(const SearchConst* S, const LaunchArgs& A, uint32_t k,
-                                          uint32_t m, double* lp, double* lm) {
+__device__ __forceinline__ void exact_linear_inl(const SearchConst* S, const LaunchArgs& A, uint32_t k,
+                                                 uint32_t m, double* lp, double* lm) {
     const double r = __ldg(&A.radii_d[k]);
     const double s = __ldg(&A.trig_d[2 * m]);
     const double c = __ldg(&A.trig_d[2 * m + 1]);
@@ -146,6 +147,12 @@ __device__ __noinline__ void exact_linear(const SearchConst* S, const LaunchArgs
         lp[q] = __dadd_rn(__dadd_rn(__dmul_rn(A.minv[3 * q], xp), cy), __dmul_rn(A.minv[3 * q + 2], zp));
         lm[q] = __dadd_rn(__dadd_rn(__dmul_rn(A.minv[3 * q], xm), cy), __dmul_rn(A.minv[3 * q + 2], zm));
     }
+}
+
+// Out-of-line copy for the rare repair sites of the hot kernels.
+__device__ __noinline__ void exact_linear(const SearchConst* S, const LaunchArgs& A, uint32_t k, uint32_t m,
+                                          double* lp, double* lm) {
+    exact_linear_inl(S, A, k, m, lp, lm);
 }
 
 // QuantTable::code (convert_kernel.hpp:148-154): largest c with x >= thr[c].
@@ -328,7 +335,11 @@ __device__ __forceinline__ void codes_fast(const Smem& sm, const SearchConst* S,
                                            const LaunchArgs& A, uint32_t k, uint32_t m, float r, float2 sc,
                                            bool active, int* cp, int* cm, unsigned long long& repairs) {
     float vp[3], vm[3];
-    fast_linear<false>(C.fx0, C.fz0, C.mx, C.mz, C.cy, r, sc, vp, vm);
+    if (__all_sync(kFull, r < C.rcube)) {  // every lane's row stays on the cube branch
+        fast_linear<true>(C.fx0, C.fz0, C.mx, C.mz, C.cy, r, sc, vp, vm);
+    } else {
+        fast_linear<false>(C.fx0, C.fz0, C.mx, C.mz, C.cy, r, sc, vp, vm);
+    }
     bool all_ok = true;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -339,7 +350,7 @@ __device__ __forceinline__ void codes_fast(const Smem& sm, const SearchConst* S,
     }
     if (__any_sync(kFull, !all_ok) && !all_ok) {
         double lp[3], lm[3];
-        exact_linear(S, A, k, m, lp, lm);
+        exact_linear_inl(S, A, k, m, lp, lm);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             cp[q] = code_exact_from(lp[q], cp[q], sm.thr_d);
