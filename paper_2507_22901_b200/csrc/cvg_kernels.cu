@@ -701,18 +701,24 @@ __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
                 // candidate's radius/trig loads one iteration ahead.
                 const float2* trig = reinterpret_cast<const float2*>(A.trig_f);
                 const uint32_t last = cnt - 1;
+                // a tile inside one radius row (n_angles >= 4096): k is the
+                // tile's row for every pair, no per-pair division or radius load
+                const uint32_t kt = div_na(i0, A);
+                const uint32_t mt = i0 - kt * static_cast<uint32_t>(A.na);
+                const bool one_row = mt + static_cast<uint32_t>(kTile) <= static_cast<uint32_t>(A.na);
+                const float rt = __ldg(&A.radii_f[kt]);
                 uint32_t off_n = list[min(32 + lane, last)];
                 uint32_t i = i0 + list[min(lane, last)];
-                uint32_t k = div_na(i, A);
+                uint32_t k = one_row ? kt : div_na(i, A);
                 uint32_t m = i - k * static_cast<uint32_t>(A.na);
-                float r = __ldg(&A.radii_f[k]);
+                float r = one_row ? rt : __ldg(&A.radii_f[k]);
                 float2 sc = __ldg(trig + m);
 #pragma unroll 1
                 for (uint32_t p = 0; p < cnt; p += 32) {
                     const uint32_t i_n = i0 + off_n;
-                    const uint32_t k_n = div_na(i_n, A);
+                    const uint32_t k_n = one_row ? kt : div_na(i_n, A);
                     const uint32_t m_n = i_n - k_n * static_cast<uint32_t>(A.na);
-                    const float r_n = __ldg(&A.radii_f[k_n]);
+                    const float r_n = one_row ? rt : __ldg(&A.radii_f[k_n]);
                     const float2 sc_n = __ldg(trig + m_n);
                     off_n = list[min(p + 64 + lane, last)];
                     const uint32_t qq = p + lane;
