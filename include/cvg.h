@@ -39,7 +39,9 @@ extern "C" {
 #define CVG_EOVERFLOW 4    /* device pair buffer too small (counts are still valid) */
 #define CVG_EUNSUPPORTED 5 /* option combination not implemented on the device path */
 
-/* SearchOptions::delta_mode / delta_basis (search.hpp:81-96) */
+/* SearchOptions::delta_mode / delta_basis (search.hpp:81-96).  Supported:
+ * Quantized x {TargetSwing, FrameDiff}, Continuous x TargetSwing;
+ * Continuous x FrameDiff returns CVG_EUNSUPPORTED. */
 #define CVG_DELTA_QUANTIZED 0
 #define CVG_DELTA_CONTINUOUS 1
 #define CVG_BASIS_TARGET_SWING 0
@@ -162,6 +164,11 @@ CVG_API int cvg_lab_to_srgb_clipped(const double lab[3], const double* white_poi
 /* returns 1 if in gamut (rgb filled), 0 if not, negative status on error */
 CVG_API int cvg_lab_to_srgb(const double lab[3], const double* white_point, int32_t rgb[3]);
 CVG_API void cvg_d65_white(double out[3]);
+/* pre-quantization signal values 255*oetf(clamp(lin)) of both endpoints of the
+ * pair (radius, angle) around `lab` (search.cpp:113-123, convert_kernel.hpp:
+ * 109-112): materializes DeltaMode::Continuous deltas of emitted pairs */
+CVG_API int cvg_pair_signal(const double lab[3], double radius, double angle, const double* white_point,
+                            double sp[3], double sm[3]);
 CVG_API void cvg_quant_thresholds(double out[256]);
 
 /* FP32 FFMA issue-rate microbenchmark (roofline denominator); returns

@@ -90,6 +90,13 @@ std::vector<ColorPair> materialize(const cvg_result& r, size_t s, const SrgbColo
     out.reserve(e - b);
     const uint32_t na = static_cast<uint32_t>(grid.angles.size());
     const bool swing = opts.delta_basis == DeltaBasis::TargetSwing;
+    const bool continuous = opts.delta_mode == DeltaMode::Continuous;
+    const double wp[3] = {opts.white_point.x, opts.white_point.y, opts.white_point.z};
+    double lab[3] = {0, 0, 0};
+    if (continuous) {
+        const int32_t rgb[3] = {target.r, target.g, target.b};
+        check(cvg_srgb_to_lab(rgb, wp, lab));
+    }
     for (uint64_t p = b; p < e; ++p) {
         const uint32_t i = r.idx[p];
         const uint8_t* c = r.codes + 6 * p;
@@ -99,7 +106,18 @@ std::vector<ColorPair> materialize(const cvg_result& r, size_t s, const SrgbColo
         cp.minus = SrgbColor{c[3], c[4], c[5]};
         cp.radius = grid.radii[i / na];
         cp.angle = grid.angles[i % na];
-        cp.deltas = swing ? channel_deltas(target, cp.plus, cp.minus) : frame_deltas(cp.plus, cp.minus);
+        if (continuous) {
+            // continuous_deltas (search.cpp:161-180), TargetSwing basis
+            double sp[3], sm[3];
+            check(cvg_pair_signal(lab, cp.radius, cp.angle, wp, sp, sm));
+            const double t[3] = {static_cast<double>(target.r), static_cast<double>(target.g),
+                                 static_cast<double>(target.b)};
+            double d[3];
+            for (int c = 0; c < 3; ++c) d[c] = std::max(std::abs(sp[c] - t[c]), std::abs(sm[c] - t[c]));
+            cp.deltas = ChannelDeltas{d[0], d[1], d[2]};
+        } else {
+            cp.deltas = swing ? channel_deltas(target, cp.plus, cp.minus) : frame_deltas(cp.plus, cp.minus);
+        }
         out.push_back(cp);
     }
     return out;

@@ -20,6 +20,7 @@
 #include <map>
 #include <mutex>
 #include <numbers>
+#include <stdexcept>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -246,9 +247,10 @@ int validate_desc(const cvg_search_desc* d) {
     if (static_cast<uint64_t>(d->n_radii) * static_cast<uint64_t>(d->n_angles) >= (1ull << 32)) {
         return fail(CVG_EINVAL, "grid too large: n_radii * n_angles must be < 2^32");
     }
-    if (d->delta_mode == CVG_DELTA_CONTINUOUS) {
+    if (d->delta_mode == CVG_DELTA_CONTINUOUS && d->delta_basis == CVG_BASIS_FRAME_DIFF) {
         return fail(CVG_EUNSUPPORTED,
-                    "DeltaMode::Continuous is not implemented on the device path (no CPU fallback)");
+                    "DeltaMode::Continuous with DeltaBasis::FrameDiff is not implemented on the device path "
+                    "(no CPU fallback)");
     }
     return CVG_OK;
 }
@@ -268,6 +270,67 @@ float round_down_f(double x) {
     float f = static_cast<float>(x);
     if (static_cast<double>(f) > x) f = std::nextafter(f, -INFINITY);
     return f;
+}
+
+// Continuous-mode bands.  With s(x) = signal_value(x) = 255 * oetf(clamp(x))
+// (convert_kernel.hpp:109-112, glibc pow), the reference's per-endpoint
+// condition fabs(s(x) - t) <= T (search.cpp:171-179, 146-157) holds exactly
+// on an interval [a, b] of doubles because s is monotone non-decreasing.
+// a and b are found by bisection over the reference's own double
+// computation; the band handed to the kernel is [a, nextafter(b, +inf)).
+// Monotonicity is checked on 64 doubles either side of each bound.
+double signal_value(double linear) {
+    const double x = linear < 0.0 ? 0.0 : (linear > 1.0 ? 1.0 : linear);
+    return 255.0 * oetf(x);
+}
+
+struct SignalBand {
+    double lo, hi;
+};
+
+SignalBand signal_band(int target, double T) {
+    const double t = static_cast<double>(target);
+    auto low_ok = [&](double x) { return signal_value(x) - t >= -T; };   // true for x >= a
+    auto high_ok = [&](double x) { return signal_value(x) - t <= T; };   // true for x <= b
+    // smallest x in (0, 1] with low_ok, by bisection over doubles
+    auto first_true = [](auto pred) {
+        double lo = 0.0, hi = 1.0;  // pred(hi) assumed true, pred(lo) false
+        while (std::nextafter(lo, 1.0) < hi) {
+            const double mid = 0.5 * (lo + hi);
+            (pred(mid) ? hi : lo) = mid;
+        }
+        return hi;
+    };
+    SignalBand b;
+    if (low_ok(0.0)) {
+        b.lo = -HUGE_VAL;  // s(x) = 0 for x <= 0 already satisfies it
+    } else if (!low_ok(1.0)) {
+        return SignalBand{HUGE_VAL, HUGE_VAL};  // never inside (empty band)
+    } else {
+        b.lo = first_true(low_ok);
+    }
+    if (high_ok(1.0)) {
+        b.hi = HUGE_VAL;
+    } else if (!high_ok(0.0)) {
+        return SignalBand{HUGE_VAL, HUGE_VAL};
+    } else {
+        b.hi = first_true([&](double x) { return !high_ok(x); });  // first x above b
+    }
+    // monotonicity around each bound (pow is accurate to < 1 ulp; a violation
+    // here would mean the interval model does not hold)
+    for (double edge : {b.lo, b.hi}) {
+        if (std::isinf(edge)) continue;
+        double x = edge;
+        for (int i = 0; i < 64; ++i) x = std::nextafter(x, -1.0);
+        double prev = signal_value(x);
+        for (int i = 0; i < 128; ++i) {
+            x = std::nextafter(x, 2.0);
+            const double v = signal_value(x);
+            if (v < prev) throw std::runtime_error("signal_value not monotone near a band edge");
+            prev = v;
+        }
+    }
+    return b;
 }
 
 struct BoundTerms {
@@ -320,10 +383,18 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
     S.q0 = q0;
     S.flags = static_cast<uint32_t>(bits[0] | (bits[1] << 1) | (bits[2] << 2));
     if (d->delta_basis == CVG_BASIS_FRAME_DIFF) S.flags |= 1u << 8;
+    const bool continuous = d->delta_mode == CVG_DELTA_CONTINUOUS;
+    if (continuous) S.flags |= 1u << 9;  // bands on signal values: no integer-code self-check
     for (int c = 0; c < 3; ++c) S.t[c] = t[c];
     // make_bands (search.cpp:291-329): exact only for Quantized x TargetSwing.
     for (int c = 0; c < 3; ++c) {
-        if (mode != cvg::kModeBand) {
+        if (mode == cvg::kModeBand && continuous) {
+            // continuous_deltas (search.cpp:161-180): pass iff |s(x) - t| <= T
+            // for both endpoints (quiet, T = low) / not for both (loud, T = v_th)
+            const SignalBand b = signal_band(t[c], bits[c] ? v_th : low);
+            S.lo[c] = b.lo;
+            S.hi[c] = b.hi;
+        } else if (mode != cvg::kModeBand) {
             S.lo[c] = -HUGE_VAL;
             S.hi[c] = HUGE_VAL;
         } else if (bits[c]) {
@@ -374,8 +445,12 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
         // M' = max(|vp - cc|, |vm - cc|) / hh <= 1: the matrix constants are
         // pre-divided by hh so the kernel gets (v - cc) / hh directly.
         const double L = lin_max + e_lin + 1.0;
-        const double lo = std::isinf(S.lo[c]) ? -L : S.lo[c];
-        const double hi = std::isinf(S.hi[c]) ? L : S.hi[c];
+        double lo = std::isinf(S.lo[c]) ? -L : S.lo[c];
+        double hi = std::isinf(S.hi[c]) ? L : S.hi[c];
+        if (S.lo[c] == HUGE_VAL || !(S.lo[c] < S.hi[c])) {  // empty band: never inside
+            lo = L + 1.0;
+            hi = L + 2.0;
+        }
         const double cc = 0.5 * (lo + hi), hh = 0.5 * (hi - lo);
         S.mxs[c] = static_cast<float>(mx / hh);
         S.mzs[c] = static_cast<float>(mz / hh);
@@ -605,8 +680,9 @@ void dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, s
 int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     const Tables& T = tables();
     p->ctx = ctx;
-    p->mode = (d->delta_mode == CVG_DELTA_QUANTIZED && d->delta_basis == CVG_BASIS_TARGET_SWING) ? cvg::kModeBand
-                                                                                                 : cvg::kModeCodes;
+    // TargetSwing (quantized or continuous) is a per-endpoint interval test:
+    // band mode.  Quantized FrameDiff classifies on the codes of both endpoints.
+    p->mode = d->delta_basis == CVG_BASIS_TARGET_SWING ? cvg::kModeBand : cvg::kModeCodes;
     p->out = d->output;
     p->path = d->path;
     p->n = d->n_searches;
@@ -769,6 +845,16 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
         if (int e2 = plan_reserve(p, cap)) return e2;
     }
     return CVG_OK;
+}
+
+int plan_build_safe(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
+    try {
+        return plan_build(ctx, d, p);
+    } catch (const std::bad_alloc&) {
+        return fail(CVG_ENOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(CVG_EUNSUPPORTED, e.what());
+    }
 }
 
 void plan_release(cvg_plan* p) {
@@ -956,7 +1042,7 @@ int cvg_plan_create(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_plan** out) {
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     if (int e = ensure_device(ctx)) return e;
     auto* p = new cvg_plan();
-    if (int e = plan_build(ctx, desc, p)) {
+    if (int e = plan_build_safe(ctx, desc, p)) {
         plan_release(p);
         delete p;
         return e;
@@ -1050,7 +1136,7 @@ int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out) {
     if (int e = ensure_device(ctx)) return e;
     const double t0 = now_ms();
     cvg_plan plan;
-    int e = plan_build(ctx, desc, &plan);
+    int e = plan_build_safe(ctx, desc, &plan);
     const double t_built = now_ms();
     if (!e) e = plan_enqueue(&plan, ctx->stream);
     if (!e) e = plan_fetch_impl(&plan, out, true);
@@ -1128,6 +1214,25 @@ int cvg_lab_to_srgb(const double lab[3], const double* wp, int32_t rgb[3]) {
     }
     for (int c = 0; c < 3; ++c) rgb[c] = quantize(lin[c]);
     return 1;
+}
+
+int cvg_pair_signal(const double lab[3], double radius, double angle, const double* wp, double sp[3],
+                    double sm[3]) {
+    if (!lab || !sp || !sm) return fail(CVG_EINVAL, "null argument");
+    if (int e = validate_lab(lab)) return e;
+    // displaced_pair (search.cpp:113-123) -> lab_to_linear -> signal_value
+    const double da = radius * std::sin(angle);
+    const double db = radius * std::cos(angle);
+    const double plus[3] = {lab[0], lab[1] + da, lab[2] + db};
+    const double minus[3] = {lab[0], lab[1] - da, lab[2] - db};
+    double lp[3], lm[3];
+    to_linear(plus, white_or_d65(wp), lp);
+    to_linear(minus, white_or_d65(wp), lm);
+    for (int c = 0; c < 3; ++c) {
+        sp[c] = signal_value(lp[c]);
+        sm[c] = signal_value(lm[c]);
+    }
+    return CVG_OK;
 }
 
 void cvg_d65_white(double out[3]) {

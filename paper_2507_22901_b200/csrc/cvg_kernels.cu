@@ -750,7 +750,8 @@ __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
                     int cp[3], cm[3];
                     candidate_codes<kPath>(sm, S, CC, A, k, m, active, cp, cm, ct.code_repairs, ct);
                     if (active) {
-                        if (kMode == kModeBand && !classify_codes(S, cp, cm, __ldg(&S->flags))) ++ct.mismatch;
+                        const uint32_t fl = __ldg(&S->flags);
+                        if (kMode == kModeBand && !(fl & (1u << 9)) && !classify_codes(S, cp, cm, fl)) ++ct.mismatch;
                         const unsigned long long o = base + qq;
                         A.out_idx[o] = i;
                         uint16_t* c16 = reinterpret_cast<uint16_t*>(A.out_codes + 6 * o);

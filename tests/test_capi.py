@@ -92,13 +92,13 @@ GRID = W.uniform_grid(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
     (dict(rn=[0.0]), 1, "r_novib must be in (0, 1]"),
     (dict(rn=[1.5]), 1, "r_novib must be in (0, 1]"),
     (dict(patterns=[0]), 1, "bit pattern has no set bits"),
-    (dict(mode=1), 5, "Continuous"),
+    (dict(mode=1, basis=1), 5, "Continuous"),
 ])
 def test_validation_mirrors_reference(lib, case, status, msg):
     args = dict(targets=[[170, 170, 170]], patterns=[5], vth=[50.0], rn=[0.5], radii=GRID[0], angles=GRID[1])
     args.update(case)
     st, err = _validate(lib, args["targets"], args["patterns"], args["vth"], args["rn"], args["radii"],
-                        args["angles"], mode=args.get("mode", 0))
+                        args["angles"], mode=args.get("mode", 0), basis=args.get("basis", 0))
     assert st == status
     assert msg in err
 
@@ -107,6 +107,8 @@ def test_validation_accepts_reference_inputs(lib):
     st, _ = _validate(lib, [[170, 170, 170]], [5], [50.0], [0.5], GRID[0], GRID[1])
     assert st == 0
     st, _ = _validate(lib, [[170, 170, 170]], [5], [50.0], [0.5], [], [])  # empty grid is valid
+    assert st == 0
+    st, _ = _validate(lib, [[170, 170, 170]], [5], [50.0], [0.5], GRID[0], GRID[1], mode=1)  # continuous swing
     assert st == 0
 
 

@@ -263,10 +263,47 @@ def test_frame_diff_basis(cv, ctx):
     assert len(fd) != len(cv.batch_search(*args))
 
 
-def test_continuous_mode_fails_loudly(cv, ctx):
+@pytest.mark.parametrize("path", ["fast", "audit", "exact"])
+def test_continuous_target_swing_bit_exact(ctx, oracle, path):
+    """DeltaMode::Continuous x TargetSwing (search.cpp:161-180): signal-space
+    bands from the host bisection, decided on the device."""
+    radii, angles = uniform_grid(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
+    t, p, v, r = [], [], [], []
+    for tg in ([170, 170, 170], [240, 240, 240], [100, 100, 240], [240, 100, 240], [8, 8, 8], [0, 255, 30]):
+        for pat in (1, 4, 5, 6, 7):
+            for vt, rn in ((50.0, 0.5), (100.0, 0.25), (20.5, 0.333)):
+                t.append(tg); p.append(pat); v.append(vt); r.append(rn)
+    wl = W.Workload("cont", np.array(t, np.int32), np.array(p, np.int32), np.array(v), np.array(r), radii, angles)
+    res = run(ctx, wl, path=path, mode=1)
+    assert res["stats"]["audit_violations"] == 0
+    for s in range(wl.n_searches):
+        a, b = int(res["offsets"][s]), int(res["offsets"][s + 1])
+        oi, oc, _ = oracle.search(wl.targets[s], int(wl.patterns[s]), wl.v_th[s], wl.r_novib[s], radii, angles,
+                                  delta_mode=1, method=0, want_deltas=False)
+        assert np.array_equal(res["idx"][a:b], oi), s
+        assert np.array_equal(res["codes"][a:b], oc), s
+
+
+def test_continuous_api_deltas_match_oracle(cv, ctx, oracle):
+    grid = cv.VibrationGrid.uniform(1.0, 91.0, 5.0, 0.0, 355.0, 5.0)
+    opts = cv.SearchOptions()
+    opts.delta_mode = cv.DeltaMode.CONTINUOUS
+    for t, p in (([170, 170, 170], "101"), ([100, 100, 240], "111"), ([240, 100, 100], "100")):
+        got = cv.batch_search_opts(cv.SrgbColor(*t), grid, cv.BitPattern(p), cv.Thresholds(50.0, 0.5), opts)
+        assert got == cv.serial_search_opts(cv.SrgbColor(*t), grid, cv.BitPattern(p), cv.Thresholds(50.0, 0.5),
+                                            opts)
+        oi, oc, od = oracle.search(t, W.bits(p), 50.0, 0.5, grid.radii, grid.angles, delta_mode=1, method=0)
+        assert len(got) == len(oi)
+        for pair, c, d in zip(got, oc, od):
+            assert [pair.plus.r, pair.plus.g, pair.plus.b, pair.minus.r, pair.minus.g, pair.minus.b] == c.tolist()
+            assert [pair.deltas.dr, pair.deltas.dg, pair.deltas.db] == d.tolist()
+
+
+def test_continuous_frame_diff_fails_loudly(cv, ctx):
     grid = cv.VibrationGrid.uniform(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
     opts = cv.SearchOptions()
     opts.delta_mode = cv.DeltaMode.CONTINUOUS
+    opts.delta_basis = cv.DeltaBasis.FRAME_DIFF
     with pytest.raises(RuntimeError, match="Continuous"):
         cv.batch_search_opts(cv.SrgbColor(170, 170, 170), grid, cv.BitPattern("101"), cv.Thresholds(50.0, 0.5),
                              opts)
