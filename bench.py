@@ -207,13 +207,14 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
-def ncu_traffic():
-    """dram bytes per launch of the search kernel from the committed ncu summary."""
+def ncu_traffic(config="cfg1"):
+    """DRAM bytes (read + write) per launch of phase1_kernel from one committed
+    `ncu --set full` capture (profiles/ncu_summary.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        return d.get("dram_bytes_per_launch")
+        return d.get("phase1_dram_bytes_per_launch", {}).get(config)
     except (OSError, ValueError):
         return None
 
@@ -272,12 +273,14 @@ def run_ours(args):
 
     # per-launch kernel time over the timed steps: events inside the plan
     # cover only the search kernel; re-measure a few steps for the roofline
-    kern = []
+    kern, phases = [], []
     for _ in range(min(args.steps, 20)):
         flush.zero_()
         plan.run(stream.cuda_stream)
         kern.append(plan.last_kernel_ms())
+        phases.append(plan.last_phase_ms())
     kern_ms = statistics.median(kern)
+    phase_ms = [statistics.median(p[i] for p in phases) for i in range(3)]
 
     # ---------------- e2e through the C-ABI host call ----------------
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 20))
@@ -319,11 +322,18 @@ def run_ours(args):
     # count + first pair (8 + 4 + 6 B) per search (first)
     out_bytes = n_pairs * 10 + wl.n_searches * 8 if wl.output == "pairs" else wl.n_searches * 18
     peak_lane, _ = cv.measure_ffma_peak(local)
-    achieved = wl.candidates * W_INSTR / (kern_ms * 1e-3) / 1e12
+    # dominant kernel: phase 1 decides every candidate (the W = 50 algorithmic
+    # FP32 instructions of SURVEY §8d); the whole 3-kernel step is reported too
+    p1_ms = phase_ms[0] if phase_ms[0] > 0 else kern_ms
+    achieved = wl.candidates * W_INSTR / (p1_ms * 1e-3) / 1e12
     peak = peak_lane / 1e12
-    roofline = {"bound": "fp32_issue", "achieved": round(achieved, 3), "peak": round(peak, 3),
-                "unit": "Tinstr/s", "frac": round(achieved / peak, 4) if peak else None,
-                "traffic": ncu_traffic(), "kernel_ms": round(kern_ms, 4),
+    step_achieved = wl.candidates * W_INSTR / (kern_ms * 1e-3) / 1e12
+    roofline = {"bound": "fp32_issue", "kernel": "phase1_kernel", "achieved": round(achieved, 3),
+                "peak": round(peak, 3), "unit": "Tinstr/s", "frac": round(achieved / peak, 4) if peak else None,
+                "traffic": ncu_traffic(wl.name), "kernel_ms": round(p1_ms, 4),
+                "step_kernels_ms": {"phase1": round(phase_ms[0], 4), "scan": round(phase_ms[1], 4),
+                                    "emit": round(phase_ms[2], 4), "total": round(kern_ms, 4)},
+                "step_frac": round(step_achieved / peak, 4) if peak else None,
                 "instr_per_candidate": W_INSTR,
                 "peak_source": "FFMA issue microbenchmark measured in this run (cvg_measure_ffma_peak)",
                 "hbm": {"bytes_per_launch": out_bytes,

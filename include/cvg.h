@@ -150,6 +150,10 @@ CVG_API int cvg_plan_device_outputs(cvg_plan* plan, uint64_t** counts, uint32_t*
                                     uint8_t** codes, uint64_t* capacity);
 /* device time (ms) of the search kernel(s) of the plan's last completed run */
 CVG_API int cvg_plan_last_kernel_ms(cvg_plan* plan, float* ms);
+/* per-kernel device time (ms) of the last run: phase 1 (candidate decisions),
+ * offset scan, pair emit (scan/emit are 0 outside CVG_OUT_PAIRS; the FIRST
+ * epilogue is counted in phase 1) */
+CVG_API int cvg_plan_last_phase_ms(cvg_plan* plan, float* phase1_ms, float* scan_ms, float* emit_ms);
 /* bytes of device-resident input the plan uploaded (constants + grid tables) */
 CVG_API uint64_t cvg_plan_input_bytes(const cvg_plan* plan);
 /* number of kernel launches one cvg_plan_run enqueues */

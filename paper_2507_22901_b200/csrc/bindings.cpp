@@ -389,6 +389,11 @@ PYBIND11_MODULE(_core, m) {
         .def_property_readonly("launches", [](const Plan& p) { return cvg_plan_launches(p.plan); })
         .def_property_readonly("candidates", [](const Plan& p) { return cvg_plan_candidates(p.plan); })
         .def_property_readonly("input_bytes", [](const Plan& p) { return cvg_plan_input_bytes(p.plan); })
+        .def("last_phase_ms", [](Plan& p) {
+            float a = 0.f, b = 0.f, c = 0.f;
+            check(cvg_plan_last_phase_ms(p.plan, &a, &b, &c));
+            return py::make_tuple(a, b, c);
+        })
         .def("last_kernel_ms", [](Plan& p) {
             float ms = 0.f;
             check(cvg_plan_last_kernel_ms(p.plan, &ms));

@@ -559,6 +559,7 @@ struct cvg_plan {
     void* d_out_codes = nullptr;
     uint64_t capacity = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t marks[2] = {nullptr, nullptr};  // after phase 1, after the scan (PAIRS)
     bool ran = false;
     cudaStream_t last_stream = nullptr;
     uint64_t input_bytes = 0;
@@ -829,7 +830,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     const uint64_t want = (n_tiles + cvg::kWarpsPerBlock - 1) / cvg::kWarpsPerBlock;
     p->grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(per_sm) * ctx->sms, want));
     if (p->grid < 1) p->grid = 1;
-    for (cudaEvent_t* ev : {&p->ev0, &p->ev1}) {
+    for (cudaEvent_t* ev : {&p->ev0, &p->ev1, &p->marks[0], &p->marks[1]}) {
         if (!ctx->events.empty()) {
             *ev = ctx->events.back();
             ctx->events.pop_back();
@@ -865,9 +866,10 @@ void plan_release(cvg_plan* p) {
     p->ctx->dev.release(p->d_first);
     p->ctx->dev.release(p->d_scratch);
     if (p->stage) cudaStreamSynchronize(p->ctx->stream);  // the constant upload may still be in flight
-    if (p->ev0) p->ctx->events.push_back(p->ev0);
-    if (p->ev1) p->ctx->events.push_back(p->ev1);
-    p->ev0 = p->ev1 = nullptr;
+    for (cudaEvent_t* ev : {&p->ev0, &p->ev1, &p->marks[0], &p->marks[1]}) {
+        if (*ev) p->ctx->events.push_back(*ev);
+        *ev = nullptr;
+    }
     p->ctx->host.release(p->stage);
     p->stage = nullptr;
 }
@@ -879,7 +881,7 @@ int plan_enqueue(cvg_plan* p, cudaStream_t st) {
     CVG_CUDA(cudaMemsetAsync(p->d_work, 0, p->work_bytes, st));
     if (p->out == cvg::kOutFirst) CVG_CUDA(cudaMemsetAsync(p->d_first, 0xff, static_cast<size_t>(p->n) * 4, st));
     CVG_CUDA(cudaEventRecord(p->ev0, st));
-    CVG_CUDA(cvg::launch_search(p->args, p->mode, p->out, p->path, p->grid, st));
+    CVG_CUDA(cvg::launch_search(p->args, p->mode, p->out, p->path, p->grid, st, p->marks));
     if (p->out == cvg::kOutFirst) CVG_CUDA(cvg::launch_first_codes(p->args, st));
     CVG_CUDA(cudaEventRecord(p->ev1, st));
     return CVG_OK;
@@ -1120,6 +1122,20 @@ int cvg_plan_last_kernel_ms(cvg_plan* p, float* ms) {
 }
 
 uint64_t cvg_plan_input_bytes(const cvg_plan* p) { return p ? p->input_bytes : 0; }
+
+int cvg_plan_last_phase_ms(cvg_plan* p, float* phase1_ms, float* scan_ms, float* emit_ms) {
+    if (!p || !phase1_ms || !scan_ms || !emit_ms) return fail(CVG_EINVAL, "null plan or output");
+    *phase1_ms = *scan_ms = *emit_ms = 0.f;
+    if (p->empty || !p->ran) return CVG_OK;
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    CVG_CUDA(cudaEventSynchronize(p->ev1));
+    if (p->out != cvg::kOutPairs) return cudaEventElapsedTime(phase1_ms, p->ev0, p->ev1) == cudaSuccess
+                                             ? CVG_OK : fail(CVG_ECUDA, "event timing failed");
+    CVG_CUDA(cudaEventElapsedTime(phase1_ms, p->ev0, p->marks[0]));
+    CVG_CUDA(cudaEventElapsedTime(scan_ms, p->marks[0], p->marks[1]));
+    CVG_CUDA(cudaEventElapsedTime(emit_ms, p->marks[1], p->ev1));
+    return CVG_OK;
+}
 
 int cvg_plan_launches(const cvg_plan* p) {
     if (!p || p->empty) return 0;

@@ -11,7 +11,9 @@ namespace cvg {
 
 // Enqueues the fused search kernel (mode: kModeBand/kModeCodes, out: kOut*,
 // path: kPath*) with `grid` persistent blocks on `st`.
-cudaError_t launch_search(const LaunchArgs& a, int mode, int out, int path, int grid, cudaStream_t st);
+// `marks` (optional, 2 events) are recorded after phase 1 and after the scan.
+cudaError_t launch_search(const LaunchArgs& a, int mode, int out, int path, int grid, cudaStream_t st,
+                          cudaEvent_t* marks = nullptr);
 // Resident blocks per SM for that instantiation; also opts the kernel into its
 // dynamic shared memory size on the current device (call before launching).
 int search_blocks_per_sm(int mode, int out, int path);

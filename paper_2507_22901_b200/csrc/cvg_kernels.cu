@@ -806,15 +806,17 @@ __global__ void ffma_peak_kernel(float* out, int iters, float a, float b) {
 }
 
 template <int kMode, int kOut, int kPath>
-cudaError_t launch_t(const LaunchArgs& a, int grid, cudaStream_t st) {
+cudaError_t launch_t(const LaunchArgs& a, int grid, cudaStream_t st, cudaEvent_t* marks) {
     // The dynamic shared-memory sizes are opted into by occupancy_t (plan creation).
     phase1_kernel<kMode, kOut, kPath><<<grid, kBlock, sizeof(Smem), st>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || kOut != kOutPairs) return e;
+    if (marks) cudaEventRecord(marks[0], st);
     const unsigned scan_blocks = static_cast<unsigned>((a.n_tiles + kScanTile - 1) / kScanTile);
     scan_kernel<<<scan_blocks, kBlock, 0, st>>>(a);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (marks) cudaEventRecord(marks[1], st);
     emit_kernel<kMode, kPath><<<grid, kBlock, sizeof(Smem), st>>>(a);
     return cudaGetLastError();
 }
@@ -830,7 +832,7 @@ int occupancy_t() {
     return blocks;
 }
 
-using LaunchFn = cudaError_t (*)(const LaunchArgs&, int, cudaStream_t);
+using LaunchFn = cudaError_t (*)(const LaunchArgs&, int, cudaStream_t, cudaEvent_t*);
 using OccFn = int (*)();
 
 #define CVG_ROW(M, P) {launch_t<M, kOutPairs, P>, launch_t<M, kOutCounts, P>, launch_t<M, kOutFirst, P>}
@@ -847,8 +849,9 @@ const OccFn kOcc[2][3][3] = {
 
 }  // namespace
 
-cudaError_t launch_search(const LaunchArgs& a, int mode, int out, int path, int grid, cudaStream_t st) {
-    return kLaunch[mode][path][out](a, grid, st);
+cudaError_t launch_search(const LaunchArgs& a, int mode, int out, int path, int grid, cudaStream_t st,
+                          cudaEvent_t* marks) {
+    return kLaunch[mode][path][out](a, grid, st, marks);
 }
 
 int search_blocks_per_sm(int mode, int out, int path) { return kOcc[mode][path][out](); }
