@@ -417,7 +417,16 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
     const double u = std::ldexp(1.0, -24);
     const BoundTerms bx = finv_bound(fx0, rmax * kInv500);
     const BoundTerms bz = finv_bound(fz0, rmax * kInv200);
-    double eps_band = 0.0;
+    double eps_q = 0.0, eps_l = 0.0;
+    // band form channel slots: loud channels first (the kernel specializes on
+    // the loud count L and reads slots [0, L) as loud, [L, 3) as quiet)
+    int slot_of[3], n_loud = 0;
+    for (int c = 0; c < 3; ++c) n_loud += bits[c];
+    {
+        int nl = 0, nq = n_loud;
+        for (int c = 0; c < 3; ++c) slot_of[c] = bits[c] ? nl++ : nq++;
+    }
+    S.flags |= static_cast<uint32_t>(n_loud) << 10;
     for (int c = 0; c < 3; ++c) {
         const double mx = m[c][0] * wp[0], mz = m[c][2] * wp[2], cy = S.cy64[c];
         // Forward error of fma(cx, gx, fma(cz, gz, add)) with float-rounded
@@ -452,17 +461,18 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
             hi = L + 2.0;
         }
         const double cc = 0.5 * (lo + hi), hh = 0.5 * (hi - lo);
-        S.mxs[c] = static_cast<float>(mx / hh);
-        S.mzs[c] = static_cast<float>(mz / hh);
-        S.cys[c] = static_cast<float>((cy - cc) / hh);
+        const int j = slot_of[c];
+        S.mxs[j] = static_cast<float>(mx / hh);
+        S.mzs[j] = static_cast<float>(mz / hh);
+        S.cys[j] = static_cast<float>((cy - cc) / hh);
         const auto [e_d, d_max] = lin_err(std::fabs(mx / hh), std::fabs(mz / hh), (cy - cc) / hh);
         const double e_m = 1.05 * (e_d + 4 * std::ldexp(1.0, -53) * (d_max + 2.0)) + 1e-12 / hh;
-        // g_c = sg_c * (M'_c - 1) is one FFMA with exact +-1: adds u * |g|.
-        const double e_g = e_m + std::ldexp(1.0, -24) * (d_max + e_m + 1.0);
-        S.sg[c] = bits[c] ? -1.0f : 1.0f;
-        eps_band = std::max(eps_band, 1.01 * e_g);
+        (bits[c] ? eps_l : eps_q) = std::max(bits[c] ? eps_l : eps_q, e_m);
     }
-    S.eps_band = round_up_f(eps_band);
+    S.la = round_down_f(1.0 - eps_l);
+    S.lp = round_up_f(1.0 + eps_l);
+    S.qa = round_up_f(1.0 + eps_q);
+    S.qp = round_down_f(1.0 - eps_q);
 }
 
 // ---------------------------------------------------------------------------

@@ -74,10 +74,12 @@ __device__ __forceinline__ uint32_t div_na(uint32_t i, const LaunchArgs& A) {
 }
 
 // ------------------------------------------------------------------------
-// Per-search constants held in registers for a tile (phase 1, band form).
+// Per-search constants held in registers for a tile (phase 1, band form;
+// channel slots loud-first).
 struct Consts {
-    float fx0, fz0, rcube, eps;
-    float mxs[3], mzs[3], cys[3], sg[3];
+    float fx0, fz0, rcube;
+    float mxs[3], mzs[3], cys[3];
+    float la, qa, lp, qp;
     uint32_t flags;
 };
 
@@ -85,14 +87,16 @@ __device__ __forceinline__ void load_consts(const SearchConst* S, Consts& c) {
     c.fx0 = __ldg(&S->fx0);
     c.fz0 = __ldg(&S->fz0);
     c.rcube = __ldg(&S->rcube);
-    c.eps = __ldg(&S->eps_band);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         c.mxs[q] = __ldg(&S->mxs[q]);
         c.mzs[q] = __ldg(&S->mzs[q]);
         c.cys[q] = __ldg(&S->cys[q]);
-        c.sg[q] = __ldg(&S->sg[q]);
     }
+    c.la = __ldg(&S->la);
+    c.qa = __ldg(&S->qa);
+    c.lp = __ldg(&S->lp);
+    c.qp = __ldg(&S->qp);
     c.flags = __ldg(&S->flags);
 }
 
@@ -235,21 +239,48 @@ __device__ __forceinline__ void fast_linear(float fx0, float fz0, const float* m
     }
 }
 
-// Band statistic of the reference band test (search.cpp:267-276,
+// Band statistics of the reference band test (search.cpp:267-276,
 // make_bands 291-329).  With the matrix rows pre-divided by the band half-
 // width h_c and offset by the band centre, channel c of a candidate yields
 // M'_c = max(|vp_c - centre_c|, |vm_c - centre_c|) / h_c: a quiet channel
-// passes iff M'_c <= 1 (both endpoints inside), a loud one iff M'_c > 1, so
-// with sg_c = +1 (quiet) / -1 (loud), g_c = sg_c * (M'_c - 1) is negative iff
-// channel c passes and the candidate passes iff G = max_c g_c < 0.
-// |G32 - G| <= eps (host proof), hence G < -eps certainly passes, G > eps
-// certainly fails, and only |G| <= eps goes to the FP64 path.  A candidate
-// needs attention at all only if G <= eps.  6 ALU + 3 FMA-pipe ops.
-__device__ __forceinline__ float band_G(const Consts& C, const float* dp, const float* dm) {
-    float g[3];
+// passes iff M'_c <= 1 (both endpoints inside), a loud one iff M'_c > 1.  The
+// host orders the channel slots loud-first, so with L loud channels the
+// candidate passes iff minl = min over slots < L of M' > 1 and maxq = max
+// over slots >= L of M' <= 1.  |M'32 - M'| is bounded on the host, hence
+//   attention (no channel certainly fails): minl >= la and maxq <= qa
+//   certain pass:                            minl >  lp and maxq <  qp
+// and only attention-but-not-certain candidates go to the FP64 path.
+// kL = loud count (1..3), 0 = read it from the flags at run time.
+template <int kL>
+__device__ __forceinline__ void band_stats(const Consts& C, const float* dp, const float* dm, float& minl,
+                                           float& maxq) {
+    const int L = kL ? kL : static_cast<int>((C.flags >> 10) & 3u);
+    minl = INFINITY;
+    maxq = -INFINITY;
+    if (kL == 3) {
+        minl = fminf(fminf(fmaxf(fabsf(dp[0]), fabsf(dm[0])), fmaxf(fabsf(dp[1]), fabsf(dm[1]))),
+                     fmaxf(fabsf(dp[2]), fabsf(dm[2])));
+    } else if (kL == 2) {
+        minl = fminf(fmaxf(fabsf(dp[0]), fabsf(dm[0])), fmaxf(fabsf(dp[1]), fabsf(dm[1])));
+        maxq = fmaxf(fabsf(dp[2]), fabsf(dm[2]));
+    } else if (kL == 1) {
+        minl = fmaxf(fabsf(dp[0]), fabsf(dm[0]));
+        maxq = fmaxf(fmaxf(fabsf(dp[1]), fabsf(dm[1])), fmaxf(fabsf(dp[2]), fabsf(dm[2])));
+    } else {
 #pragma unroll
-    for (int q = 0; q < 3; ++q) g[q] = fmaf(C.sg[q], fmaxf(fabsf(dp[q]), fabsf(dm[q])), -C.sg[q]);
-    return fmaxf(fmaxf(g[0], g[1]), g[2]);
+        for (int q = 0; q < 3; ++q) {
+            const float M = fmaxf(fabsf(dp[q]), fabsf(dm[q]));
+            if (q < L) minl = fminf(minl, M); else maxq = fmaxf(maxq, M);
+        }
+    }
+}
+
+__device__ __forceinline__ bool band_attention(const Consts& C, float minl, float maxq) {
+    return (minl >= C.la) & (maxq <= C.qa);
+}
+
+__device__ __forceinline__ bool band_certain(const Consts& C, float minl, float maxq) {
+    return (minl > C.lp) & (maxq < C.qp);
 }
 
 // Linear value -> code through the float tables, verified against the bound:
@@ -423,9 +454,10 @@ __device__ __forceinline__ bool candidate_pass(const Smem& sm, const SearchConst
     const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + m);
     float dp[3], dm[3];
     fast_linear<false>(C.fx0, C.fz0, C.mxs, C.mzs, C.cys, r, sc, dp, dm);
-    const float G = band_G(C, dp, dm);
-    bool pass = G < -C.eps;
-    const bool unsure = fabsf(G) <= C.eps;
+    float minl, maxq;
+    band_stats<0>(C, dp, dm, minl, maxq);
+    bool pass = band_certain(C, minl, maxq);
+    const bool unsure = band_attention(C, minl, maxq) & !pass;
     if (kPath == kPathAudit) {
         double lp[3], lm[3];
         exact_linear(S, A, k, m, lp, lm);
@@ -466,10 +498,10 @@ __device__ __forceinline__ void append(bool pass, uint32_t off, uint16_t* list, 
 // unsure lanes, then the ordered append.
 template <int kOut>
 __device__ __forceinline__ void band_settle(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
-                                            uint32_t m, float G, uint32_t off, uint16_t* list, uint32_t& cnt,
-                                            uint32_t& first, Counters& ct, unsigned lane_lt) {
-    bool pass = G < -C.eps;
-    if (fabsf(G) <= C.eps) {
+                                            uint32_t m, float minl, float maxq, uint32_t off, uint16_t* list,
+                                            uint32_t& cnt, uint32_t& first, Counters& ct, unsigned lane_lt) {
+    bool pass = band_certain(C, minl, maxq);
+    if (band_attention(C, minl, maxq) & !pass) {
         double lp[3], lm[3];
         exact_linear(S, A, k, m, lp, lm);
         pass = exact_band(S, lp, lm, C.flags);
@@ -478,20 +510,20 @@ __device__ __forceinline__ void band_settle(const SearchConst* S, const Consts& 
     append<kOut>(pass, off, list, cnt, first, lane_lt);
 }
 
-template <bool kCubeOnly>
-__device__ __forceinline__ float band_chunk(const Consts& C, float r, float2 sc) {
+template <int kL, bool kCubeOnly>
+__device__ __forceinline__ void band_chunk(const Consts& C, float r, float2 sc, float& minl, float& maxq) {
     float dp[3], dm[3];
     fast_linear<kCubeOnly>(C.fx0, C.fz0, C.mxs, C.mzs, C.cys, r, sc, dp, dm);
-    return band_G(C, dp, dm);
+    band_stats<kL>(C, dp, dm, minl, maxq);
 }
 
-// Hot loop: FAST path, band mode, `nch` full 32-candidate chunks of radius
-// row k starting at angle m0 (na % 32 == 0: chunks never straddle rows).  Two
-// chunks per iteration share one vote (ILP across chunks).  Per candidate:
-// 1 LDG (L1-resident trig, prefetched two chunks ahead), 27 FMA-pipe ops
-// (4 f, 8 cube, 12 matrix, 3 sign) + 7 min/max + 1 compare.  kCubeOnly rows
-// (r < rcube) never reach the linear branch of f^-1; the others select.
-template <bool kCubeOnly, int kOut>
+// Hot loop: FAST path, band mode, kL loud channels, `nch` full 32-candidate
+// chunks of radius row k starting at angle m0 (na % 32 == 0: chunks never
+// straddle rows).  Two chunks per iteration share one vote (ILP across
+// chunks).  Per candidate: 1 LDG (L1-resident trig, prefetched two chunks
+// ahead), 24 FMA-pipe ops (4 f, 8 cube, 12 matrix) + 4 min/max + compares.
+// kCubeOnly rows (r < rcube) never reach the linear branch of f^-1.
+template <int kL, bool kCubeOnly, int kOut>
 __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
                                          float r, uint32_t m0, uint32_t nch, uint32_t off, uint16_t* list,
                                          uint32_t& cnt, uint32_t& first, Counters& ct, unsigned lane,
@@ -501,23 +533,47 @@ __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, 
     uint32_t ix = mb;
     const uint32_t iend = mb + 32u * (nch & ~1u);
     float2 na_ = __ldg(trig + ix), nb_ = __ldg(trig + ix + 32);
+#pragma unroll 1  // code size: 3 loud counts x 2 branch forms x 3 outputs share the I-cache
     for (; ix != iend; ix += 64) {
         const float2 sa = na_, sb = nb_;
         na_ = __ldg(trig + ix + 64);  // prefetch; the table is padded by 128 entries
         nb_ = __ldg(trig + ix + 96);
-        const float Ga = band_chunk<kCubeOnly>(C, r, sa);
-        const float Gb = band_chunk<kCubeOnly>(C, r, sb);
-        if (__any_sync(kFull, fminf(Ga, Gb) <= C.eps)) {
+        float la_, qa_, lb_, qb_;
+        band_chunk<kL, kCubeOnly>(C, r, sa, la_, qa_);
+        band_chunk<kL, kCubeOnly>(C, r, sb, lb_, qb_);
+        if (__any_sync(kFull, band_attention(C, la_, qa_) | band_attention(C, lb_, qb_))) {
             const uint32_t d = ix - mb;
-            band_settle<kOut>(S, C, A, k, ix, Ga, off + lane + d, list, cnt, first, ct, lane_lt);
-            band_settle<kOut>(S, C, A, k, ix + 32, Gb, off + lane + d + 32, list, cnt, first, ct, lane_lt);
+            band_settle<kOut>(S, C, A, k, ix, la_, qa_, off + lane + d, list, cnt, first, ct, lane_lt);
+            band_settle<kOut>(S, C, A, k, ix + 32, lb_, qb_, off + lane + d + 32, list, cnt, first, ct, lane_lt);
         }
     }
     if (nch & 1u) {
-        const float Ga = band_chunk<kCubeOnly>(C, r, na_);
-        if (__any_sync(kFull, Ga <= C.eps)) {
-            band_settle<kOut>(S, C, A, k, ix, Ga, off + lane + (ix - mb), list, cnt, first, ct, lane_lt);
+        float la_, qa_;
+        band_chunk<kL, kCubeOnly>(C, r, na_, la_, qa_);
+        if (__any_sync(kFull, band_attention(C, la_, qa_))) {
+            band_settle<kOut>(S, C, A, k, ix, la_, qa_, off + lane + (ix - mb), list, cnt, first, ct, lane_lt);
         }
+    }
+}
+
+template <int kL, int kOut>
+__device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t i0,
+                                          uint32_t i1, uint16_t* list, uint32_t& cnt, uint32_t& first, Counters& ct,
+                                          unsigned lane, unsigned lane_lt) {
+    uint32_t k = div_na(i0, A);
+    uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
+    uint32_t i = i0;
+    while (i < i1) {
+        const uint32_t seg = min(i1 - i, static_cast<uint32_t>(A.na) - m0);
+        const float r = __ldg(&A.radii_f[k]);
+        if (r < C.rcube) {
+            band_row<kL, true, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);
+        } else {
+            band_row<kL, false, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);
+        }
+        i += seg;
+        m0 = 0;
+        ++k;
     }
 }
 
@@ -549,20 +605,13 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         Consts C;
         load_consts(S, C);
         if (kMode == kModeBand && kPath == kPathFast && A.aligned) {
-            uint32_t k = div_na(i0, A);
-            uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
-            uint32_t i = i0;
-            while (i < i1) {
-                const uint32_t seg = min(i1 - i, static_cast<uint32_t>(A.na) - m0);
-                const float r = __ldg(&A.radii_f[k]);
-                if (r < C.rcube) {
-                    band_row<true, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);
-                } else {
-                    band_row<false, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);
-                }
-                i += seg;
-                m0 = 0;
-                ++k;
+            const uint32_t nl = (C.flags >> 10) & 3u;
+            if (nl == 3) {
+                band_tile<3, kOut>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
+            } else if (nl == 2) {
+                band_tile<2, kOut>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
+            } else {
+                band_tile<1, kOut>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
             }
         } else {
             CodeConsts CC;

@@ -25,17 +25,17 @@ struct alignas(16) SearchConst {
     float fx0;         // Fy + a/500   (fx of both endpoints = fx0 +- r*sin/500)
     float fz0;         // Fz = Fy - b/200 (fz = fz0 -+ r*cos/200)
     float rcube;       // rows with r < rcube never leave the cube branch of f^-1
-    float eps_band;    // bound on |G32 - G| of the band statistic (see cvg_kernels.cu)
+    float la;          // band attention: min over loud M' >= la (= 1 - eps_l, rounded down)
     float mx[3];       // Minv[c][0] * wx
     float mz[3];       // Minv[c][2] * wz
     float cy[3];       // Minv[c][1] * wy * f^-1(Fy)
-    float mxs[3];      // band form: mx / h_c          (h_c: band half-width)
+    float mxs[3];      // band form, channels permuted loud-first: mx / h_c   (h_c: band half-width)
     float mzs[3];      //            mz / h_c
     float cys[3];      //            (cy - centre_c) / h_c
-    float sg[3];       // +1 quiet channel (0 bit), -1 loud channel (1 bit)
+    float qa, qp, lp;  // attention: max quiet M' <= qa; certain pass: max quiet M' < qp and min loud M' > lp
     float eps[3];      // proven bound |lin32 - lin64| per channel (linear units)
     float eps_code[3]; // eps + float rounding of the code thresholds
-    uint32_t flags;    // bit c (c=0,1,2 -> r,g,b): loud channel (pattern bit set)
+    uint32_t flags;    // bit c (c=0,1,2 -> r,g,b): loud channel; bit 8 FrameDiff; bit 9 continuous; bits 10-11: loud count
     int32_t t[3];      // target codes
     int32_t k1;        // d > v_th   <=> d >= k1 (integer deltas); 256 = never
     int32_t q0;        // d <= low   <=> d <= q0
