@@ -22,6 +22,7 @@
 #include <numbers>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -214,6 +215,64 @@ int validate_thresholds(double v_th, double r_novib) {
     return CVG_OK;
 }
 
+// Runs f(0..n-1) on up to hardware_concurrency threads, at least `grain`
+// items each (contiguous ranges); inline for small n.  Exceptions are rethrown on the caller's thread.
+template <typename F>
+void parallel_for(size_t n, F&& f, size_t grain = 512) {
+    const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t workers = std::min<size_t>(hw, n / std::max<size_t>(grain, 1));
+    if (workers <= 1) {
+        for (size_t i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::vector<std::thread> pool;
+    std::exception_ptr err;
+    std::mutex err_mu;
+    for (size_t w = 0; w < workers; ++w) {
+        pool.emplace_back([&, w] {
+            try {
+                for (size_t i = n * w / workers; i < n * (w + 1) / workers; ++i) f(i);
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(err_mu);
+                if (!err) err = std::current_exception();
+            }
+        });
+    }
+    for (auto& t : pool) t.join();
+    if (err) std::rethrow_exception(err);
+}
+
+// True when every search of the batch is valid (colors in [0, 255],
+// 0 < v_th < inf, 0 < r_novib <= 1, pattern in 1..7).  Accumulates with
+// bitwise ORs so the compiler vectorizes it: ~1 ns per search.
+bool batch_clean_range(const cvg_search_desc* d, size_t lo, size_t hi) {
+    uint32_t bad = 0;
+    const int32_t* c = d->target_rgb;
+    for (size_t i = 3 * lo; i < 3 * hi; ++i) bad |= static_cast<uint32_t>(c[i]) > 255u;
+    const int32_t* pb = d->pattern_bits;
+    for (size_t i = lo; i < hi; ++i) bad |= static_cast<uint32_t>(pb[i] - 1) > 6u;
+    const double* v = d->v_th;
+    const double* r = d->r_novib;
+    for (size_t i = lo; i < hi; ++i) {
+        bad |= static_cast<uint32_t>(!(v[i] > 0.0)) | static_cast<uint32_t>(!(v[i] < HUGE_VAL)) |
+               static_cast<uint32_t>(!(r[i] > 0.0)) | static_cast<uint32_t>(!(r[i] <= 1.0));
+    }
+    return bad == 0;
+}
+
+bool batch_clean(const cvg_search_desc* d) {
+    const size_t n = static_cast<size_t>(d->n_searches);
+    const size_t chunk = 1u << 18;
+    const size_t parts = (n + chunk - 1) / chunk;
+    std::vector<char> ok(parts, 1);
+    parallel_for(
+        parts, [&](size_t c) { ok[c] = batch_clean_range(d, c * chunk, std::min(n, (c + 1) * chunk)); }, 1);
+    for (char o : ok) {
+        if (!o) return false;
+    }
+    return true;
+}
+
 int validate_desc(const cvg_search_desc* d) {
     if (!d) return fail(CVG_EINVAL, "null search descriptor");
     if (d->n_searches < 0) return fail(CVG_EINVAL, "n_searches must be >= 0");
@@ -228,6 +287,13 @@ int validate_desc(const cvg_search_desc* d) {
     }
     if (d->output < CVG_OUT_PAIRS || d->output > CVG_OUT_FIRST) return fail(CVG_EINVAL, "unknown output mode");
     if (d->path < CVG_PATH_FAST || d->path > CVG_PATH_AUDIT) return fail(CVG_EINVAL, "unknown path");
+    // Fast screen: branch-free, vectorizable pass over the whole batch.  Only
+    // if it finds a problem does the ordered per-search loop below run, to
+    // report the first failure with the reference's message and order.
+    if (batch_clean(d) && validate_grid(d->radii, d->n_radii, d->angles, d->n_angles) == CVG_OK) {
+        goto checked;
+    }
+    {
     // Per search in the reference order: target, grid, thresholds, pattern.
     int grid_checked = 0;
     for (int s = 0; s < d->n_searches; ++s) {
@@ -244,6 +310,8 @@ int validate_desc(const cvg_search_desc* d) {
     if (!grid_checked) {
         if (int e = validate_grid(d->radii, d->n_radii, d->angles, d->n_angles)) return e;
     }
+    }
+checked:
     if (static_cast<uint64_t>(d->n_radii) * static_cast<uint64_t>(d->n_angles) >= (1ull << 32)) {
         return fail(CVG_EINVAL, "grid too large: n_radii * n_angles must be < 2^32");
     }
@@ -643,15 +711,27 @@ void dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, s
     };
     sc_index.resize(n);
     if (uniform && n > 4096) {
-        // same classifier everywhere: a direct table over the 2^24 colors
-        std::vector<int32_t> table(1u << 24, -1);
+        // Same classifier everywhere: records keyed by the 24-bit color.
+        // Presence bitmap over the 2^24 colors (2 MB) + per-word rank, so the
+        // record id of a color is rank(color): no table to clear, cache-resident.
+        std::vector<uint64_t> bits(1u << 18, 0);
         for (int s = 0; s < n; ++s) {
-            int32_t& slot = table[key24(s)];
-            if (slot < 0) {
-                slot = static_cast<int32_t>(uniq.size());
-                uniq.push_back(s);
-            }
-            sc_index[s] = static_cast<uint32_t>(slot);
+            const uint32_t k = key24(s);
+            bits[k >> 6] |= 1ull << (k & 63);
+        }
+        std::vector<uint32_t> rank(1u << 18);
+        uint32_t acc = 0;
+        for (size_t w = 0; w < bits.size(); ++w) {
+            rank[w] = acc;
+            acc += static_cast<uint32_t>(__builtin_popcountll(bits[w]));
+        }
+        uniq.assign(acc, -1);
+        for (int s = 0; s < n; ++s) {
+            const uint32_t k = key24(s);
+            const uint32_t id =
+                rank[k >> 6] + static_cast<uint32_t>(__builtin_popcountll(bits[k >> 6] & ((1ull << (k & 63)) - 1)));
+            sc_index[s] = id;
+            if (uniq[id] < 0) uniq[id] = s;
         }
     } else {
         struct Key {
@@ -717,7 +797,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     dedup_searches(d, sc_index, uniq);
     std::vector<SearchConst> sc(uniq.size());
     const double rmax = d->radii[p->nr - 1];
-    for (size_t u = 0; u < uniq.size(); ++u) make_search_const(d, uniq[u], rmax, p->mode, T, sc[u]);
+    parallel_for(uniq.size(), [&](size_t u) { make_search_const(d, uniq[u], rmax, p->mode, T, sc[u]); });
     p->n_unique = static_cast<int32_t>(uniq.size());
     std::vector<float> radii_f(p->nr);
     for (int k = 0; k < p->nr; ++k) radii_f[k] = static_cast<float>(d->radii[k]);
