@@ -90,14 +90,10 @@ py::dict result_dict(std::shared_ptr<ResultHolder> h, int output) {
     const cvg_result& r = h->r;
     py::dict out;
     const py::ssize_t n = r.n_searches;
-    py::array_t<uint64_t> counts(n);
-    std::copy(r.counts, r.counts + n, counts.mutable_data());
-    out["counts"] = counts;
+    out["counts"] = py::array_t<uint64_t>({n}, {sizeof(uint64_t)}, r.counts, base);  // pinned, zero-copy
     out["n_pairs"] = r.n_pairs;
     if (output == CVG_OUT_PAIRS) {
-        py::array_t<uint64_t> offs(n + 1);
-        std::copy(r.offsets, r.offsets + n + 1, offs.mutable_data());
-        out["offsets"] = offs;
+        out["offsets"] = py::array_t<uint64_t>({n + 1}, {sizeof(uint64_t)}, r.offsets, base);
         const py::ssize_t np_ = static_cast<py::ssize_t>(r.n_pairs);
         if (np_) {
             out["idx"] = py::array_t<uint32_t>({np_}, {sizeof(uint32_t)}, r.idx, base);

@@ -642,6 +642,7 @@ struct cvg_plan {
     cudaStream_t last_stream = nullptr;
     uint64_t input_bytes = 0;
     void* stage = nullptr;  // pinned staging of the constant blob (held until the plan is released)
+    uint64_t* h_counts = nullptr;  // pinned per-search counts for cvg_plan_sync
     int32_t n_unique = 0;
     double t_prep_end = 0, t_upload_end = 0;
 };
@@ -700,12 +701,26 @@ void dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, s
     const int n = d->n_searches;
     sc_index.clear();
     uniq.clear();
+    if (n <= 0) return;
+    // uniform classifier? (chunked so the 8M-search screen runs on all cores)
+    const size_t parts = n >= (1 << 20) ? 64 : 1;
+    std::vector<char> same(parts, 1);
+    parallel_for(
+        parts,
+        [&](size_t c) {
+            const size_t lo = std::max<size_t>(1, n * c / parts), hi = n * (c + 1) / parts;
+            const int32_t b0 = d->pattern_bits[0];
+            const double v0 = d->v_th[0], r0 = d->r_novib[0];
+            bool ok = true;
+            for (size_t s = lo; s < hi; ++s) {
+                ok &= (d->pattern_bits[s] == b0) & (d->v_th[s] == v0) & (d->r_novib[s] == r0);
+            }
+            same[c] = ok;
+        },
+        1);
     bool uniform = true;
-    for (int s = 1; s < n && uniform; ++s) {
-        uniform = d->pattern_bits[s] == d->pattern_bits[0] && d->v_th[s] == d->v_th[0] &&
-                  d->r_novib[s] == d->r_novib[0];
-    }
-    auto key24 = [&](int s) {
+    for (char c : same) uniform = uniform && c;
+    auto key24 = [&](size_t s) {
         const int32_t* t = d->target_rgb + 3 * s;
         return static_cast<uint32_t>(t[0]) << 16 | static_cast<uint32_t>(t[1]) << 8 | static_cast<uint32_t>(t[2]);
     };
@@ -714,25 +729,46 @@ void dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, s
         // Same classifier everywhere: records keyed by the 24-bit color.
         // Presence bitmap over the 2^24 colors (2 MB) + per-word rank, so the
         // record id of a color is rank(color): no table to clear, cache-resident.
+        // Both passes run chunked over all cores; the representative of a
+        // record is its first search (atomic min), so the result is
+        // independent of the thread count.
         std::vector<uint64_t> bits(1u << 18, 0);
-        for (int s = 0; s < n; ++s) {
-            const uint32_t k = key24(s);
-            bits[k >> 6] |= 1ull << (k & 63);
-        }
+        const size_t chunks = n >= (1 << 20) ? 64 : 1;
+        parallel_for(
+            chunks,
+            [&](size_t c) {
+                for (size_t s = n * c / chunks; s < n * (c + 1) / chunks; ++s) {
+                    const uint32_t k = key24(s);
+                    const uint64_t m = 1ull << (k & 63);
+                    if (!(__atomic_load_n(&bits[k >> 6], __ATOMIC_RELAXED) & m)) {
+                        __atomic_fetch_or(&bits[k >> 6], m, __ATOMIC_RELAXED);
+                    }
+                }
+            },
+            1);
         std::vector<uint32_t> rank(1u << 18);
         uint32_t acc = 0;
         for (size_t w = 0; w < bits.size(); ++w) {
             rank[w] = acc;
             acc += static_cast<uint32_t>(__builtin_popcountll(bits[w]));
         }
-        uniq.assign(acc, -1);
-        for (int s = 0; s < n; ++s) {
-            const uint32_t k = key24(s);
-            const uint32_t id =
-                rank[k >> 6] + static_cast<uint32_t>(__builtin_popcountll(bits[k >> 6] & ((1ull << (k & 63)) - 1)));
-            sc_index[s] = id;
-            if (uniq[id] < 0) uniq[id] = s;
-        }
+        uniq.assign(acc, INT32_MAX);
+        parallel_for(
+            chunks,
+            [&](size_t c) {
+                for (size_t s = n * c / chunks; s < n * (c + 1) / chunks; ++s) {
+                    const uint32_t k = key24(s);
+                    const uint32_t id = rank[k >> 6] +
+                                        static_cast<uint32_t>(__builtin_popcountll(bits[k >> 6] & ((1ull << (k & 63)) - 1)));
+                    sc_index[s] = id;
+                    int32_t cur = __atomic_load_n(&uniq[id], __ATOMIC_RELAXED);
+                    const int32_t me = static_cast<int32_t>(s);
+                    while (me < cur &&
+                           !__atomic_compare_exchange_n(&uniq[id], &cur, me, true, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
+                    }
+                }
+            },
+            1);
     } else {
         struct Key {
             uint32_t rgb;
@@ -757,7 +793,7 @@ void dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, s
         std::unordered_map<Key, int32_t, Hash> seen;
         seen.reserve(static_cast<size_t>(n) * 2);
         for (int s = 0; s < n; ++s) {
-            const Key k{key24(s), d->pattern_bits[s], d->v_th[s], d->r_novib[s]};
+            const Key k{key24(static_cast<size_t>(s)), d->pattern_bits[s], d->v_th[s], d->r_novib[s]};
             auto [it, fresh] = seen.emplace(k, static_cast<int32_t>(uniq.size()));
             if (fresh) uniq.push_back(s);
             sc_index[s] = static_cast<uint32_t>(it->second);
@@ -834,7 +870,16 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
         return fail(CVG_ENOMEM, "allocation of the search tables failed");
     }
     std::memcpy(stage + o_sc, sc.data(), sizeof(SearchConst) * sc.size());
-    if (!sc_index.empty()) std::memcpy(stage + o_si, sc_index.data(), sizeof(uint32_t) * sc_index.size());
+    if (!sc_index.empty()) {
+        const size_t m = sc_index.size(), parts = m >= (1u << 20) ? 16 : 1;
+        parallel_for(
+            parts,
+            [&](size_t c) {
+                const size_t lo = m * c / parts, hi = m * (c + 1) / parts;
+                std::memcpy(stage + o_si + 4 * lo, sc_index.data() + lo, 4 * (hi - lo));
+            },
+            1);
+    }
     std::memcpy(stage + o_rd, d->radii, sizeof(double) * p->nr);
     std::memcpy(stage + o_rf, radii_f.data(), sizeof(float) * p->nr);
     std::memcpy(stage + o_td, trig_d.data(), sizeof(double) * trig_d.size());
@@ -962,6 +1007,8 @@ void plan_release(cvg_plan* p) {
     }
     p->ctx->host.release(p->stage);
     p->stage = nullptr;
+    p->ctx->host.release(p->h_counts);
+    p->h_counts = nullptr;
 }
 
 int plan_enqueue(cvg_plan* p, cudaStream_t st) {
@@ -982,16 +1029,34 @@ struct HostStats {
     float ms = 0.f;
 };
 
-// Waits for the last run; copies counts and stats to host.
-int plan_collect(cvg_plan* p, std::vector<uint64_t>& counts, HostStats& hs) {
-    counts.assign(p->n, 0);
-    if (p->empty) return CVG_OK;
+// Waits for the last run; copies counts (into pinned `counts`) and stats to host.
+int plan_collect(cvg_plan* p, uint64_t* counts, HostStats& hs) {
+    if (p->empty) {
+        if (p->n) std::memset(counts, 0, sizeof(uint64_t) * p->n);
+        return CVG_OK;
+    }
     cudaStream_t st = p->last_stream;
-    CVG_CUDA(cudaMemcpyAsync(counts.data(), p->args.counts, sizeof(uint64_t) * p->n, cudaMemcpyDeviceToHost, st));
+    CVG_CUDA(cudaMemcpyAsync(counts, p->args.counts, sizeof(uint64_t) * p->n, cudaMemcpyDeviceToHost, st));
     CVG_CUDA(cudaMemcpyAsync(&hs.st, p->args.stats, sizeof(cvg::Stats), cudaMemcpyDeviceToHost, st));
     CVG_CUDA(cudaStreamSynchronize(st));
     CVG_CUDA(cudaEventElapsedTime(&hs.ms, p->ev0, p->ev1));
     return CVG_OK;
+}
+
+uint64_t sum_counts(const uint64_t* c, size_t n) {
+    const size_t parts = n >= (1u << 20) ? 16 : 1;
+    std::vector<uint64_t> part(parts, 0);
+    parallel_for(
+        parts,
+        [&](size_t k) {
+            uint64_t acc = 0;
+            for (size_t i = n * k / parts; i < n * (k + 1) / parts; ++i) acc += c[i];
+            part[k] = acc;
+        },
+        1);
+    uint64_t t = 0;
+    for (uint64_t v : part) t += v;
+    return t;
 }
 
 void result_zero(cvg_result* r) { std::memset(r, 0, sizeof(*r)); }
@@ -999,12 +1064,15 @@ void result_zero(cvg_result* r) { std::memset(r, 0, sizeof(*r)); }
 int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
     result_zero(r);
     r->n_searches = p->n;
-    std::vector<uint64_t> counts;
+    cvg_ctx* ctx = p->ctx;
+    const size_t n = static_cast<size_t>(p->n);
+    // counts land straight in the pinned block that becomes r->counts
+    r->counts = static_cast<uint64_t*>(ctx->host.alloc(sizeof(uint64_t) * (n ? n : 1)));
+    if (!r->counts) return fail(CVG_ENOMEM, "pinned host allocation failed");
     HostStats hs;
-    if (int e = plan_collect(p, counts, hs)) return e;
+    if (int e = plan_collect(p, r->counts, hs)) return e;
     const double t_counts = now_ms();
-    uint64_t total = 0;
-    for (uint64_t c : counts) total += c;
+    const uint64_t total = sum_counts(r->counts, n);
     if (p->out == cvg::kOutPairs && hs.st.overflow) {
         if (!allow_rerun) {
             r->n_pairs = total;
@@ -1012,13 +1080,9 @@ int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
         }
         if (int e = plan_reserve(p, total)) return e;
         if (int e = plan_enqueue(p, p->last_stream)) return e;
+        ctx->host.release(r->counts);
         return plan_fetch_impl(p, r, false);
     }
-    cvg_ctx* ctx = p->ctx;
-    const size_t n = static_cast<size_t>(p->n);
-    r->counts = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (n ? n : 1)));
-    if (!r->counts) return fail(CVG_ENOMEM, "host allocation failed");
-    std::copy(counts.begin(), counts.end(), r->counts);
     r->n_pairs = total;
     r->n_candidates = p->candidates;
     r->n_band_repairs = hs.st.band_repairs;
@@ -1034,7 +1098,7 @@ int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
         r->offsets = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (n + 1)));
         if (!r->offsets) return fail(CVG_ENOMEM, "host allocation failed");
         r->offsets[0] = 0;
-        for (size_t s = 0; s < n; ++s) r->offsets[s + 1] = r->offsets[s] + counts[s];
+        for (size_t s = 0; s < n; ++s) r->offsets[s + 1] = r->offsets[s] + r->counts[s];
         if (total) {
             r->idx = static_cast<uint32_t*>(ctx->host.alloc(total * 4));
             r->codes = static_cast<uint8_t*>(ctx->host.alloc(total * 6));
@@ -1065,7 +1129,8 @@ std::map<const void*, cvg_ctx*> g_owner;
 
 void remember_owner(cvg_result* r, cvg_ctx* ctx) {
     std::lock_guard<std::mutex> lk(g_owner_mu);
-    for (const void* ptr : {static_cast<const void*>(r->idx), static_cast<const void*>(r->codes),
+    for (const void* ptr : {static_cast<const void*>(r->counts), static_cast<const void*>(r->idx),
+                            static_cast<const void*>(r->codes),
                             static_cast<const void*>(r->first_idx), static_cast<const void*>(r->first_codes)}) {
         if (ptr) g_owner[ptr] = ctx;
     }
@@ -1172,11 +1237,13 @@ int cvg_plan_sync(cvg_plan* p, uint64_t* n_pairs) {
     if (!p) return fail(CVG_EINVAL, "null plan");
     std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
     if (int e = ensure_device(p->ctx)) return e;
-    std::vector<uint64_t> counts;
+    if (!p->h_counts) {
+        p->h_counts = static_cast<uint64_t*>(p->ctx->host.alloc(sizeof(uint64_t) * (p->n ? p->n : 1)));
+        if (!p->h_counts) return fail(CVG_ENOMEM, "pinned host allocation failed");
+    }
     HostStats hs;
-    if (int e = plan_collect(p, counts, hs)) return e;
-    uint64_t total = 0;
-    for (uint64_t c : counts) total += c;
+    if (int e = plan_collect(p, p->h_counts, hs)) return e;
+    const uint64_t total = sum_counts(p->h_counts, static_cast<size_t>(p->n));
     if (n_pairs) *n_pairs = total;
     if (p->out == cvg::kOutPairs && hs.st.overflow) return fail(CVG_EOVERFLOW, "pair buffer too small");
     return CVG_OK;
@@ -1265,9 +1332,8 @@ int cvg_validate(const cvg_search_desc* desc) { return validate_desc(desc); }
 
 void cvg_result_free(cvg_result* r) {
     if (!r) return;
-    std::free(r->counts);
     std::free(r->offsets);
-    for (void* ptr : {static_cast<void*>(r->idx), static_cast<void*>(r->codes), static_cast<void*>(r->first_idx),
+    for (void* ptr : {static_cast<void*>(r->counts), static_cast<void*>(r->idx), static_cast<void*>(r->codes), static_cast<void*>(r->first_idx),
                       static_cast<void*>(r->first_codes)}) {
         if (!ptr) continue;
         cvg_ctx* owner = nullptr;
