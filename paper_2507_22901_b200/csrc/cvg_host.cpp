@@ -9,7 +9,12 @@
 // candidate is evaluated on the GPU (cvg_kernels.cu).
 #include <cuda_runtime.h>
 
+#include <unistd.h>
+
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
 #include <cfloat>
 #include <chrono>
 #include <cmath>
@@ -215,30 +220,127 @@ int validate_thresholds(double v_th, double r_novib) {
     return CVG_OK;
 }
 
-// Runs f(0..n-1) on up to hardware_concurrency threads, at least `grain`
-// items each (contiguous ranges); inline for small n.  Exceptions are rethrown on the caller's thread.
+// Process-wide worker threads for parallel_for: spawning threads per call
+// costs ~10 us each, more than the host work of a sweep-sized batch.  The
+// caller takes part; nested calls and calls from a forked child run inline.
+class WorkerPool {
+public:
+    static WorkerPool& get() {
+        static WorkerPool pool;
+        return pool;
+    }
+    size_t width() const { return workers_.size() + 1; }
+
+    // job(w) for w in [0, n_jobs) on the pool and the calling thread
+    void run(size_t n_jobs, const std::function<void(size_t)>& job) {
+        if (n_jobs <= 1 || workers_.empty() || in_job_ || getpid() != pid_) {
+            for (size_t w = 0; w < n_jobs; ++w) job(w);
+            return;
+        }
+        std::lock_guard<std::mutex> one(run_mu_);  // one batch at a time
+        Batch b;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            b = Batch{++generation_, static_cast<uint32_t>(n_jobs), &job};
+            batch_ = b;
+            pending_ = n_jobs;
+            state_.store(b.gen << 32);
+        }
+        cv_.notify_all();
+        work(b);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_cv_.wait(lk, [&] { return pending_ == 0; });
+    }
+
+private:
+    struct Batch {
+        uint64_t gen = 0;
+        uint32_t n = 0;
+        const std::function<void(size_t)>* job = nullptr;
+    };
+    WorkerPool() : pid_(getpid()) {
+        const size_t hw = std::max(1u, std::thread::hardware_concurrency());
+        for (size_t i = 0; i + 1 < std::min<size_t>(hw, 64); ++i) {
+            workers_.emplace_back([this] { loop(); });
+        }
+    }
+    ~WorkerPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+    // Claims jobs of batch b only: state_ = generation << 32 | next job, so a
+    // worker holding an older batch can never take a job of a newer one.
+    void work(const Batch& b) {
+        in_job_ = true;
+        size_t done = 0;
+        uint64_t st = state_.load();
+        for (;;) {
+            if ((st >> 32) != (b.gen & 0xffffffffu) || (st & 0xffffffffu) >= b.n) break;
+            if (!state_.compare_exchange_weak(st, st + 1)) continue;
+            (*b.job)(static_cast<size_t>(st & 0xffffffffu));
+            ++done;
+            st = state_.load();
+        }
+        in_job_ = false;
+        if (done) {
+            std::lock_guard<std::mutex> lk(mu_);
+            pending_ -= done;
+            if (pending_ == 0) done_cv_.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            Batch b;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || generation_ != seen; });
+                if (stop_) return;
+                seen = generation_;
+                b = batch_;
+            }
+            work(b);
+        }
+    }
+
+    pid_t pid_;
+    std::vector<std::thread> workers_;
+    std::mutex run_mu_, mu_;
+    std::condition_variable cv_, done_cv_;
+    Batch batch_;
+    size_t pending_ = 0;
+    std::atomic<uint64_t> state_{0};
+    uint64_t generation_ = 0;
+    bool stop_ = false;
+    static thread_local bool in_job_;
+};
+thread_local bool WorkerPool::in_job_ = false;
+
+// Runs f(0..n-1) on the worker pool, at least `grain` items per job
+// (contiguous ranges); inline for small n.  Exceptions are rethrown on the
+// caller's thread.
 template <typename F>
 void parallel_for(size_t n, F&& f, size_t grain = 512) {
-    const size_t hw = std::max(1u, std::thread::hardware_concurrency());
-    const size_t workers = std::min<size_t>(hw, n / std::max<size_t>(grain, 1));
-    if (workers <= 1) {
+    WorkerPool& pool = WorkerPool::get();
+    const size_t jobs = std::min<size_t>(pool.width(), n / std::max<size_t>(grain, 1));
+    if (jobs <= 1) {
         for (size_t i = 0; i < n; ++i) f(i);
         return;
     }
-    std::vector<std::thread> pool;
     std::exception_ptr err;
     std::mutex err_mu;
-    for (size_t w = 0; w < workers; ++w) {
-        pool.emplace_back([&, w] {
-            try {
-                for (size_t i = n * w / workers; i < n * (w + 1) / workers; ++i) f(i);
-            } catch (...) {
-                std::lock_guard<std::mutex> lk(err_mu);
-                if (!err) err = std::current_exception();
-            }
-        });
-    }
-    for (auto& t : pool) t.join();
+    pool.run(jobs, [&](size_t w) {
+        try {
+            for (size_t i = n * w / jobs; i < n * (w + 1) / jobs; ++i) f(i);
+        } catch (...) {
+            std::lock_guard<std::mutex> lk(err_mu);
+            if (!err) err = std::current_exception();
+        }
+    });
     if (err) std::rethrow_exception(err);
 }
 
@@ -613,7 +715,13 @@ struct cvg_ctx {
     size_t total_mem = 0;
     std::vector<cudaEvent_t> events;  // recycled timing events
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;  // D2H of finished chunks while later chunks compute
+    cudaStream_t tail_stream = nullptr;  // per-range counts/totals of a pipelined search
     std::recursive_mutex mu;
+    // pair total of the last pipelined search of the same shape: sizes the
+    // pinned result so repeated searches never grow it
+    uint64_t hint_sig[4] = {0, 0, 0, 0};
+    uint64_t hint_pairs = 0;
     Pool dev;
     Pool host;
 };
@@ -804,7 +912,33 @@ void dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, s
     }
 }
 
-int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
+// Grid tables shared by every search (and every range of a pipelined search).
+struct GridTables {
+    std::vector<float> radii_f;
+    std::vector<float> trig_f;   // (sin/500, cos/200) per angle, padded by 128 entries
+    std::vector<double> trig_d;  // (sin, cos) per angle
+};
+
+GridTables make_grid_tables(const cvg_search_desc* d) {
+    GridTables g;
+    g.radii_f.resize(d->n_radii);
+    for (int k = 0; k < d->n_radii; ++k) g.radii_f[k] = static_cast<float>(d->radii[k]);
+    // float trig table padded by 128 entries: the hot loop prefetches two chunks ahead
+    g.trig_f.assign(2 * (static_cast<size_t>(d->n_angles) + 128), 0.0f);
+    g.trig_d.resize(2 * static_cast<size_t>(d->n_angles));
+    for (int j = 0; j < d->n_angles; ++j) {  // search.cpp:414-419
+        const double sn = std::sin(d->angles[j]);
+        const double cs = std::cos(d->angles[j]);
+        g.trig_d[2 * j] = sn;
+        g.trig_d[2 * j + 1] = cs;
+        g.trig_f[2 * j] = static_cast<float>(sn * kInv500);
+        g.trig_f[2 * j + 1] = static_cast<float>(cs * kInv200);
+    }
+    return g;
+}
+
+int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTables* grid = nullptr,
+               const SearchConst* pre = nullptr) {
     const Tables& T = tables();
     p->ctx = ctx;
     // TargetSwing (quantized or continuous) is a per-endpoint interval test:
@@ -829,29 +963,31 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     // pattern, v_th, r_novib) share one record (per-pixel batches repeat
     // colors); every candidate of every search is still evaluated.
     std::vector<uint32_t> sc_index;
-    std::vector<int32_t> uniq;  // representative search of each record
-    dedup_searches(d, sc_index, uniq);
-    std::vector<SearchConst> sc(uniq.size());
-    const double rmax = d->radii[p->nr - 1];
-    parallel_for(uniq.size(), [&](size_t u) { make_search_const(d, uniq[u], rmax, p->mode, T, sc[u]); });
-    p->n_unique = static_cast<int32_t>(uniq.size());
-    std::vector<float> radii_f(p->nr);
-    for (int k = 0; k < p->nr; ++k) radii_f[k] = static_cast<float>(d->radii[k]);
-    // float trig table padded by 128 entries: the hot loop prefetches two chunks ahead
-    std::vector<float> trig_f(2 * (static_cast<size_t>(p->na) + 128), 0.0f);
-    std::vector<double> trig_d(2 * static_cast<size_t>(p->na));
-    for (int j = 0; j < p->na; ++j) {  // search.cpp:414-419
-        const double sn = std::sin(d->angles[j]);
-        const double cs = std::cos(d->angles[j]);
-        trig_d[2 * j] = sn;
-        trig_d[2 * j + 1] = cs;
-        trig_f[2 * j] = static_cast<float>(sn * kInv500);
-        trig_f[2 * j + 1] = static_cast<float>(cs * kInv200);
+    std::vector<SearchConst> sc_own;
+    const SearchConst* sc_ptr = pre;  // one record per search, built by the caller
+    size_t n_sc = static_cast<size_t>(p->n);
+    if (!pre) {
+        std::vector<int32_t> uniq;  // representative search of each record
+        dedup_searches(d, sc_index, uniq);
+        sc_own.resize(uniq.size());
+        const double rmax = d->radii[p->nr - 1];
+        parallel_for(uniq.size(), [&](size_t u) { make_search_const(d, uniq[u], rmax, p->mode, T, sc_own[u]); });
+        sc_ptr = sc_own.data();
+        n_sc = sc_own.size();
     }
+    p->n_unique = static_cast<int32_t>(n_sc);
+    GridTables own;
+    if (!grid) {
+        own = make_grid_tables(d);
+        grid = &own;
+    }
+    const std::vector<float>& radii_f = grid->radii_f;
+    const std::vector<float>& trig_f = grid->trig_f;
+    const std::vector<double>& trig_d = grid->trig_d;
 
     // ---- one constant blob: [sc | sc_index | radii | trig | thresholds | guess] ----
     Layout L;
-    const size_t o_sc = L.take(sizeof(SearchConst) * sc.size());
+    const size_t o_sc = L.take(sizeof(SearchConst) * n_sc);
     const size_t o_si = L.take(sizeof(uint32_t) * sc_index.size());
     const size_t o_rd = L.take(sizeof(double) * p->nr);
     const size_t o_rf = L.take(sizeof(float) * p->nr);
@@ -869,7 +1005,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
         ctx->host.release(stage);
         return fail(CVG_ENOMEM, "allocation of the search tables failed");
     }
-    std::memcpy(stage + o_sc, sc.data(), sizeof(SearchConst) * sc.size());
+    std::memcpy(stage + o_sc, sc_ptr, sizeof(SearchConst) * n_sc);
     if (!sc_index.empty()) {
         const size_t m = sc_index.size(), parts = m >= (1u << 20) ? 16 : 1;
         parallel_for(
@@ -925,10 +1061,10 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     const size_t o_tk = W.take(sizeof(unsigned int) * 4);
     const size_t o_ct = W.take(sizeof(unsigned long long) * p->n);
     const size_t o_ss = W.take(sizeof(cvg::Stats));
+    const size_t o_to = W.take(sizeof(unsigned long long));  // stats+total read back as one ChunkTail
     p->work_bytes = W.off;  // memset span
     const size_t o_tc = W.take(sizeof(uint32_t) * (pairs ? n_tiles : 0));
     const size_t o_tb = W.take(sizeof(unsigned long long) * (pairs ? n_tiles : 0));
-    const size_t o_to = W.take(sizeof(unsigned long long));
     const size_t o_wl = W.take(sizeof(uint32_t) * (pairs ? n_tiles * (cvg::kTile / cvg::kEmitSpan) : 0));
     p->d_work = ctx->dev.alloc(W.off);
     if (!p->d_work) return fail(CVG_ENOMEM, "device allocation of the workspace failed");
@@ -983,9 +1119,10 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
     return CVG_OK;
 }
 
-int plan_build_safe(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p) {
+int plan_build_safe(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTables* grid = nullptr,
+                    const SearchConst* pre = nullptr) {
     try {
-        return plan_build(ctx, d, p);
+        return plan_build(ctx, d, p, grid, pre);
     } catch (const std::bad_alloc&) {
         return fail(CVG_ENOMEM, "host allocation failed");
     } catch (const std::exception& e) {
@@ -1136,6 +1273,302 @@ void remember_owner(cvg_result* r, cvg_ctx* ctx) {
     }
 }
 
+
+// ---- pipelined PAIRS search ------------------------------------------------
+// The end-to-end cost of a large PAIRS search is the PCIe read-back of 10
+// bytes per pair (cfg1: 38 MB, 0.69 ms at ~55 GB/s) after the device work.
+// Splitting the batch into K search ranges lets chunk c's read-back (copy
+// stream) overlap chunk c+1's build and kernels (compute stream); the
+// host learns chunk c's pair total from a 8-byte tail copy behind its
+// kernels and appends its pairs to one contiguous pinned result.
+int pipeline_chunks(const cvg_search_desc* d) {
+    if (d->output != CVG_OUT_PAIRS || d->n_searches < 2) return 1;
+    const uint64_t cands = static_cast<uint64_t>(d->n_searches) * static_cast<uint64_t>(d->n_radii) *
+                           static_cast<uint64_t>(d->n_angles);
+    static const int forced = [] {
+        const char* e = std::getenv("CVG_PIPELINE_K");  // tuning override; 1 disables pipelining
+        return e ? std::atoi(e) : 0;
+    }();
+    uint64_t k;
+    if (forced > 0) {
+        k = static_cast<uint64_t>(forced);
+    } else {
+        // each range pays ~80 us of kernel tail and the last range's read-back
+        // overlaps nothing; measured optimum (tools/sweep_pipeline.sh):
+        // cfg1 (198M candidates) K=2, cfg3 (1.07G) K=4..6
+        if (cands < (1ull << 26)) return 1;
+        k = cands < (1ull << 29) ? 2 : (cands < (1ull << 31) ? 4 : 6);
+    }
+    return static_cast<int>(std::min<uint64_t>(k, static_cast<uint64_t>(d->n_searches)));
+}
+
+// Range boundaries growing linearly (sizes 1:2:...:K): the first range is
+// small so the read-back starts early; the later ranges carry the bulk.
+std::vector<size_t> ramp_bounds(size_t n, int K) {
+    std::vector<size_t> lo(K + 1);
+    static const bool even = std::getenv("CVG_PIPELINE_EVEN") != nullptr;  // tuning override
+    if (even) {
+        for (int c = 0; c <= K; ++c) lo[c] = n * c / K;
+        return lo;
+    }
+    const size_t den = static_cast<size_t>(K) * (K + 1) / 2;
+    for (int c = 0; c <= K; ++c) {
+        const size_t num = static_cast<size_t>(c) * (c + 1) / 2;
+        lo[c] = std::max(static_cast<size_t>(c), std::min(n - (K - c), n * num / den));
+    }
+    return lo;
+}
+
+struct ChunkTail {
+    union {
+        cvg::Stats st;
+        unsigned char pad[256];
+    };
+    unsigned long long total;
+};
+static_assert(sizeof(cvg::Stats) <= 256 && offsetof(ChunkTail, total) == 256, "ChunkTail mirrors the workspace");
+
+struct PinnedPairs {
+    cvg_ctx* ctx;
+    uint32_t* idx = nullptr;
+    uint8_t* codes = nullptr;
+    uint64_t cap = 0;
+
+    // grows to `need` pairs keeping the first `used` (waits for in-flight copies)
+    bool ensure(uint64_t need, uint64_t want, uint64_t used) {
+        if (need <= cap) return true;
+        const uint64_t ncap = std::max(need, want);
+        auto* ni = static_cast<uint32_t*>(ctx->host.alloc(ncap * 4));
+        auto* nc = static_cast<uint8_t*>(ctx->host.alloc(ncap * 6));
+        if (!ni || !nc) {
+            ctx->host.release(ni);
+            ctx->host.release(nc);
+            return false;
+        }
+        if (used) {
+            cudaStreamSynchronize(ctx->copy_stream);
+            const size_t parts = used >= (1u << 20) ? 16 : 1;
+            parallel_for(
+                parts,
+                [&](size_t c) {
+                    const size_t lo = used * c / parts, hi = used * (c + 1) / parts;
+                    std::memcpy(ni + lo, idx + lo, 4 * (hi - lo));
+                    std::memcpy(nc + 6 * lo, codes + 6 * lo, 6 * (hi - lo));
+                },
+                1);
+        }
+        ctx->host.release(idx);
+        ctx->host.release(codes);
+        idx = ni;
+        codes = nc;
+        cap = ncap;
+        return true;
+    }
+};
+
+int search_pipelined(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, int K) {
+    const double t0 = now_ms();
+    const size_t n = static_cast<size_t>(d->n_searches);
+    const uint64_t cps = static_cast<uint64_t>(d->n_radii) * static_cast<uint64_t>(d->n_angles);
+    const GridTables grid = make_grid_tables(d);
+    // every record up front, on all cores (ranges are too small to thread well)
+    std::vector<SearchConst> recs(n);
+    {
+        const Tables& T = tables();
+        const int mode = d->delta_basis == CVG_BASIS_TARGET_SWING ? cvg::kModeBand : cvg::kModeCodes;
+        const double rmax = d->radii[d->n_radii - 1];
+        parallel_for(n, [&](size_t s) { make_search_const(d, static_cast<int>(s), rmax, mode, T, recs[s]); }, 64);
+    }
+    const double t_recs = now_ms();
+    r->n_searches = d->n_searches;
+    r->counts = static_cast<uint64_t*>(ctx->host.alloc(sizeof(uint64_t) * n));
+    r->offsets = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (n + 1)));
+    auto* tails = static_cast<ChunkTail*>(ctx->host.alloc(sizeof(ChunkTail) * K));
+    if (!r->counts || !r->offsets || !tails) {
+        ctx->host.release(tails);
+        return fail(CVG_ENOMEM, "host allocation failed");
+    }
+    std::vector<cvg_plan> plans(K);
+    const std::vector<size_t> lo = ramp_bounds(n, K);
+    std::vector<cudaEvent_t> done(K, nullptr), kdone(K, nullptr);  // tails landed / kernels finished
+    PinnedPairs out{ctx};
+    const uint64_t sig[4] = {n, cps, static_cast<uint64_t>(d->delta_basis), static_cast<uint64_t>(d->path)};
+    const bool hinted = std::equal(sig, sig + 4, ctx->hint_sig);
+    uint64_t used = 0;
+    double prep = t_recs - t0, h2d = 0, t_last_done = 0;
+    cvg::Stats agg{};
+    float agg_ratio = 0.f, kernel_ms = 0.f;
+    int err = CVG_OK;
+    static const bool trace = std::getenv("CVG_TRACE") != nullptr;
+    std::vector<cudaEvent_t> copied(trace ? K : 0, nullptr);
+    for (auto& e : copied) cudaEventCreate(&e);
+    std::vector<std::pair<const char*, double>> tl;
+    auto mark = [&](const char* what) {
+        if (trace) tl.emplace_back(what, now_ms() - t0);
+    };
+
+    auto enqueue_tail = [&](int c) -> int {
+        // counts and [stats | total] of the range on the tail stream: the
+        // compute stream goes on with the next range, never queued behind
+        // a pair copy on the D2H engine
+        cvg_plan& p = plans[c];
+        cudaStream_t st = ctx->tail_stream;
+        CVG_CUDA(cudaEventRecord(kdone[c], ctx->stream));
+        CVG_CUDA(cudaStreamWaitEvent(st, kdone[c], 0));
+        CVG_CUDA(cudaMemcpyAsync(r->counts + lo[c], p.args.counts, sizeof(uint64_t) * (lo[c + 1] - lo[c]),
+                                 cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaMemcpyAsync(&tails[c], p.args.stats, sizeof(ChunkTail), cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaEventRecord(done[c], st));
+        return CVG_OK;
+    };
+    auto drain = [&](int c) -> int {
+        cvg_plan& p = plans[c];
+        mark("drain");
+        CVG_CUDA(cudaEventSynchronize(done[c]));
+        mark("done");
+        if (tails[c].st.overflow) {  // device pair buffer too small: rerun this range at its exact size
+            if (int e = plan_reserve(&p, tails[c].total)) return e;
+            if (int e = plan_enqueue(&p, ctx->stream)) return e;
+            if (int e = enqueue_tail(c)) return e;
+            CVG_CUDA(cudaEventSynchronize(done[c]));
+        }
+        t_last_done = now_ms();
+        const uint64_t tc = tails[c].total;
+        const uint64_t seen = cps * lo[c + 1];  // candidates through this chunk
+        const uint64_t extrap = (used + tc) * ((cps * n + seen - 1) / seen) + (used + tc) / 4 + (1u << 16);
+        const uint64_t want = hinted ? std::max(ctx->hint_pairs, used + tc) : extrap;
+        if (!out.ensure(used + tc, std::min<uint64_t>(want, cps * n), used)) {
+            return fail(CVG_ENOMEM, "pinned host allocation failed");
+        }
+        if (tc) {
+            CVG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, done[c], 0));
+            CVG_CUDA(cudaMemcpyAsync(out.idx + used, p.d_out_idx, tc * 4, cudaMemcpyDeviceToHost, ctx->copy_stream));
+            CVG_CUDA(cudaMemcpyAsync(out.codes + 6 * used, p.d_out_codes, tc * 6, cudaMemcpyDeviceToHost,
+                                     ctx->copy_stream));
+        }
+        if (trace) cudaEventRecord(copied[c], ctx->copy_stream);
+        mark("issued");
+        used += tc;
+        const cvg::Stats& s = tails[c].st;
+        agg.band_repairs += s.band_repairs;
+        agg.code_repairs += s.code_repairs;
+        agg.audit_violations += s.audit_violations;
+        agg.class_mismatch += s.class_mismatch;
+        float ratio;
+        std::memcpy(&ratio, &s.audit_max_ratio_bits, sizeof(float));
+        agg_ratio = std::max(agg_ratio, ratio);
+        float ms = 0.f;
+        CVG_CUDA(cudaEventElapsedTime(&ms, p.ev0, p.ev1));
+        kernel_ms += ms;
+        return CVG_OK;
+    };
+
+    mark("grid");
+    int next = 0;  // first range not yet drained
+    for (int c = 0; c < K && !err; ++c) {
+        cvg_search_desc sub = *d;
+        sub.n_searches = static_cast<int32_t>(lo[c + 1] - lo[c]);
+        sub.target_rgb = d->target_rgb + 3 * lo[c];
+        sub.pattern_bits = d->pattern_bits + lo[c];
+        sub.v_th = d->v_th + lo[c];
+        sub.r_novib = d->r_novib + lo[c];
+        const double tb = now_ms();
+        err = plan_build_safe(ctx, &sub, &plans[c], &grid, recs.data() + lo[c]);
+        if (err) break;
+        prep += (plans[c].t_prep_end ? plans[c].t_prep_end : now_ms()) - tb;
+        h2d += plans[c].t_upload_end ? plans[c].t_upload_end - plans[c].t_prep_end : 0.0;
+        for (cudaEvent_t* ev : {&done[c], &kdone[c]}) {
+            if (!ctx->events.empty()) {
+                *ev = ctx->events.back();
+                ctx->events.pop_back();
+            } else if (cudaEventCreate(ev) != cudaSuccess) {
+                err = fail(CVG_ECUDA, "event creation failed");
+            }
+        }
+        if (err) break;
+        mark("built");
+        err = plan_enqueue(&plans[c], ctx->stream);
+        if (!err) err = enqueue_tail(c);
+        mark("enqueued");
+        // start the read-back of every finished range without blocking the builds
+        while (!err && next < c) {
+            const cudaError_t q = cudaEventQuery(done[next]);
+            if (q == cudaErrorNotReady) {
+                cudaGetLastError();  // not an error: the range is still running
+                break;
+            }
+            err = q == cudaSuccess ? drain(next++) : cuda_fail(q, "range completion");
+        }
+    }
+    while (!err && next < K) err = drain(next++);
+    if (!err) {
+        cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+        if (ce != cudaSuccess) err = cuda_fail(ce, "pair read-back");
+    }
+    const double t1 = now_ms();
+    if (!err) {
+        r->idx = used ? out.idx : nullptr;
+        r->codes = used ? out.codes : nullptr;
+        if (!used) {
+            ctx->host.release(out.idx);
+            ctx->host.release(out.codes);
+        }
+        r->offsets[0] = 0;
+        for (size_t s = 0; s < n; ++s) r->offsets[s + 1] = r->offsets[s] + r->counts[s];
+        r->n_pairs = used;
+        r->n_candidates = cps * n;
+        r->n_band_repairs = agg.band_repairs;
+        r->n_code_repairs = agg.code_repairs;
+        r->n_audit_violations = agg.audit_violations;
+        r->n_class_mismatch = agg.class_mismatch;
+        r->audit_max_ratio = agg_ratio;
+        r->kernel_ms = kernel_ms;
+        uint64_t in_bytes = 0;
+        for (const cvg_plan& p : plans) in_bytes += p.input_bytes;
+        r->h2d_bytes = in_bytes;
+        r->d2h_bytes = sizeof(uint64_t) * n + (sizeof(ChunkTail)) * K + used * 10;
+        r->prep_ms = static_cast<float>(prep);
+        r->h2d_ms = static_cast<float>(h2d);
+        r->device_ms = static_cast<float>(t_last_done - t0 - prep - h2d);
+        r->d2h_ms = static_cast<float>(t1 - t_last_done);
+        r->total_ms = static_cast<float>(t1 - t0);
+        std::copy(sig, sig + 4, ctx->hint_sig);
+        ctx->hint_pairs = used;
+    } else {
+        cudaStreamSynchronize(ctx->copy_stream);
+        ctx->host.release(out.idx);
+        ctx->host.release(out.codes);
+    }
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->tail_stream);
+    if (trace) {
+        mark("end");
+        std::string line = "[cvg trace] K=" + std::to_string(K);
+        for (auto& [w, t] : tl) line += std::string(" ") + w + "@" + std::to_string(t).substr(0, 6);
+        for (int c = 0; c < K && !err; ++c) {
+            float a = 0, b = 0, x = 0, m0 = 0, m1 = 0;
+            cudaEventElapsedTime(&a, plans[0].ev0, plans[c].ev0);
+            cudaEventElapsedTime(&b, plans[0].ev0, plans[c].ev1);
+            cudaEventElapsedTime(&x, plans[0].ev0, copied[c]);
+            cudaEventElapsedTime(&m0, plans[c].ev0, plans[c].marks[0]);
+            cudaEventElapsedTime(&m1, plans[c].ev0, plans[c].marks[1]);
+            line += " | r" + std::to_string(c) + " n=" + std::to_string(lo[c + 1] - lo[c]) + " pairs=" +
+                    std::to_string(tails[c].total) + " gpu " + std::to_string(a).substr(0, 5) + "-" +
+                    std::to_string(b).substr(0, 5) + " (p1 " + std::to_string(m0).substr(0, 5) + " scan@" +
+                    std::to_string(m1).substr(0, 5) + ") copied@" + std::to_string(x).substr(0, 5);
+        }
+        std::fprintf(stderr, "%s\n", line.c_str());
+        for (auto& e : copied) cudaEventDestroy(e);
+    }
+    for (int c = 0; c < K; ++c) {
+        if (done[c]) ctx->events.push_back(done[c]);
+        if (kdone[c]) ctx->events.push_back(kdone[c]);
+        if (plans[c].ctx) plan_release(&plans[c]);
+    }
+    ctx->host.release(tails);
+    return err;
+}
+
 }  // namespace
 
 // ============================================================================
@@ -1164,6 +1597,8 @@ int cvg_create(int device, cvg_ctx** out) {
     e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->tail_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) {
         size_t free_b = 0;
         e = cudaMemGetInfo(&free_b, &ctx->total_mem);
@@ -1187,8 +1622,12 @@ void cvg_destroy(cvg_ctx* ctx) {
             it = it->second == ctx ? g_owner.erase(it) : std::next(it);
         }
     }
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamSynchronize(ctx->tail_stream);
     for (cudaEvent_t ev : ctx->events) cudaEventDestroy(ev);
     cudaStreamDestroy(ctx->stream);
+    cudaStreamDestroy(ctx->copy_stream);
+    cudaStreamDestroy(ctx->tail_stream);
     delete ctx;
 }
 
@@ -1307,6 +1746,19 @@ int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out) {
     if (int e = validate_desc(desc)) return e;
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     if (int e = ensure_device(ctx)) return e;
+    if (const int K = pipeline_chunks(desc); K > 1) {
+        int e;
+        try {
+            e = search_pipelined(ctx, desc, out, K);
+        } catch (const std::bad_alloc&) {
+            e = fail(CVG_ENOMEM, "host allocation failed");
+        } catch (const std::exception& ex) {
+            e = fail(CVG_EUNSUPPORTED, ex.what());
+        }
+        remember_owner(out, ctx);
+        if (e) cvg_result_free(out);
+        return e;
+    }
     const double t0 = now_ms();
     cvg_plan plan;
     int e = plan_build_safe(ctx, desc, &plan);

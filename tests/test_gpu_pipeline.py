@@ -1,0 +1,76 @@
+"""The pipelined PAIRS read-back (cvg_host.cpp search_pipelined): batches of
+>= 2^25 candidates are split into search ranges whose pairs are copied back
+while later ranges compute.  The result must equal the single-plan result
+bit for bit, including when the pinned result has to grow (early ranges
+with few pairs, late ranges with many) and when ranges are empty.
+"""
+import numpy as np
+import pytest
+
+from paper_2507_22901_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+def single_plan(ctx, targets, pats, vt, rn, radii, angles, step):
+    """The same batch as sub-batches below the pipelining threshold."""
+    idx, codes, counts = [], [], []
+    for a in range(0, len(pats), step):
+        r = ctx.search(targets[a:a + step], pats[a:a + step], vt[a:a + step], rn[a:a + step], radii, angles)
+        assert r["n_pairs"] == 0 or len(r["idx"]) == r["n_pairs"]
+        idx.append(r["idx"].copy())
+        codes.append(r["codes"].copy())
+        counts.append(r["counts"].copy())
+    return np.concatenate(idx), np.concatenate(codes), np.concatenate(counts)
+
+
+@pytest.mark.parametrize("order", ["sparse_first", "dense_first", "mixed"])
+def test_pipelined_equals_single_plan(ctx, order):
+    rng = np.random.default_rng({"sparse_first": 1, "dense_first": 2, "mixed": 3}[order])
+    radii, angles = W.radii(256, 1.0), W.angles(1024)
+    n = 320  # 83.9M candidates -> 2 ranges (sizes 1:2)
+    targets = rng.integers(0, 256, (n, 3)).astype(np.int32)
+    pats = rng.integers(1, 8, n).astype(np.int32)
+    vt = rng.choice([5.0, 20.0, 50.0], n)
+    rn = np.full(n, 0.5)
+    if order == "sparse_first":
+        vt[: n // 2] = 254.9  # almost nothing passes in the first range
+    elif order == "dense_first":
+        vt[n // 2:] = 254.9
+    got = ctx.search(targets, pats, vt, rn, radii, angles)
+    want_idx, want_codes, want_counts = single_plan(ctx, targets, pats, vt, rn, radii, angles, 64)
+    assert np.array_equal(got["counts"], want_counts)
+    assert got["n_pairs"] == len(want_idx)
+    assert np.array_equal(got["offsets"][1:], np.cumsum(want_counts))
+    assert np.array_equal(got["idx"], want_idx)
+    assert np.array_equal(got["codes"], want_codes)
+    assert got["stats"]["class_mismatch"] == 0
+    # a repeat of the same shape takes the hinted capacity path
+    again = ctx.search(targets, pats, vt, rn, radii, angles)
+    assert np.array_equal(again["idx"], want_idx) and np.array_equal(again["codes"], want_codes)
+
+
+def test_pipelined_no_pairs(ctx):
+    radii, angles = W.radii(256, 1.0), W.angles(1024)
+    n = 300  # 78.6M candidates -> 2 ranges
+    targets = np.zeros((n, 3), np.int32)
+    res = ctx.search(targets, np.full(n, 7, np.int32), np.full(n, 300.0), np.full(n, 0.5), radii, angles)
+    assert res["n_pairs"] == 0 and len(res["idx"]) == 0 and res["counts"].sum() == 0
+    assert np.all(res["offsets"] == 0)
+
+
+def test_pipelined_many_ranges_audit(ctx, oracle):
+    """6 ranges; sampled searches checked against the oracle on the audit path."""
+    rng = np.random.default_rng(9)
+    radii, angles = W.radii(128, 0.5), W.angles(512)
+    n = 40000  # 2.6G candidates -> 6 ranges
+    targets = rng.integers(0, 256, (n, 3)).astype(np.int32)
+    pats = rng.integers(1, 8, n).astype(np.int32)
+    vt = rng.choice([10.0, 30.0, 60.0], n)
+    rn = rng.choice([0.5, 0.25], n)
+    res = ctx.search(targets, pats, vt, rn, radii, angles, path="audit")
+    assert res["stats"]["audit_violations"] == 0
+    for s in rng.choice(n, 12, replace=False):
+        a, b = int(res["offsets"][s]), int(res["offsets"][s + 1])
+        oi, oc, _ = oracle.search(targets[s], int(pats[s]), vt[s], rn[s], radii, angles, method=1, want_deltas=False)
+        assert np.array_equal(res["idx"][a:b], oi) and np.array_equal(res["codes"][a:b], oc), s
