@@ -33,10 +33,10 @@ def _free_port():
     return p
 
 
-def _small_batch():
+def _small_batch(n_targets=3):
     radii, angles = W.uniform_grid(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
     t, p, v, r = [], [], [], []
-    for tg in ([170, 170, 170], [240, 100, 240], [100, 100, 240]):
+    for tg in ([170, 170, 170], [240, 100, 240], [100, 100, 240])[:n_targets]:
         for pat in (5, 7, 4):
             for vt, rn in ((50.0, 0.5), (100.0, 0.25)):
                 t.append(tg); p.append(pat); v.append(vt); r.append(rn)
@@ -62,7 +62,7 @@ def _oracle_search(shard):
             "codes": np.concatenate(codes) if codes else np.zeros((0, 6), np.uint8)}
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, by="auto", n_targets=3):
     import torch.distributed as dist
 
     from paper_2507_22901_b200.distributed import gather_pairs, search_sharded
@@ -70,23 +70,26 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        wl = _small_batch()
-        res = search_sharded(wl, _oracle_search)
+        wl = _small_batch(n_targets)
+        res = search_sharded(wl, _oracle_search, by=by)
         got = gather_pairs(res)
-        q.put((rank, res.counts.tolist(), res.global_pair_offset,
+        q.put((rank, res.counts.tolist(), res.global_pair_offset if res.by == "searches" else None,
                None if got is None else (got[0].tolist(), got[1].tolist())))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_gloo_shards_equal_single_process(world):
+@pytest.mark.parametrize("world,by,n_targets", [(2, "auto", 3), (2, "rows", 3), (2, "auto", 1)])
+def test_gloo_shards_equal_single_process(world, by, n_targets):
+    """Search ranges (18 searches) and radius-row slices (forced, and auto
+    for a 6-search batch: < 4 searches per rank) give the single-process
+    result in canonical order."""
     import multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, by, n_targets)) for r in range(world)]
     for p in procs:
         p.start()
     outs = [q.get(timeout=120) for _ in range(world)]
@@ -94,11 +97,22 @@ def test_gloo_shards_equal_single_process(world):
         p.join(timeout=60)
         assert p.exitcode == 0
     outs.sort()
-    full = _oracle_search(_small_batch())
+    full = _oracle_search(_small_batch(n_targets))
     for rank, counts, off, _ in outs:
         assert counts == full["counts"].tolist()
-        lo, _ = shard_range(len(counts), rank, world)
-        assert off == int(np.sum(full["counts"][:lo]))
+        if off is not None:
+            lo, _ = shard_range(len(counts), rank, world)
+            assert off == int(np.sum(full["counts"][:lo]))
     idx, codes = outs[0][3]
     assert idx == full["idx"].tolist()
     assert codes == full["codes"].tolist()
+
+
+def test_partition_rule():
+    from paper_2507_22901_b200.distributed import partition
+
+    assert partition(756, 256, 8) == "searches"   # cfg1
+    assert partition(9, 4096, 8) == "rows"        # cfg2
+    assert partition(1, 256, 8) == "rows"         # cfg0
+    assert partition(1, 256, 1) == "searches"
+    assert partition(4, 3, 8) == "searches"       # fewer rows than ranks
