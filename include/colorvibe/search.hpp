@@ -82,7 +82,7 @@ struct ColorPair {
 
 enum class DeltaMode {
     Quantized,   // deltas between 8-bit codes (default)
-    Continuous,  // pre-quantization deltas (not on the device path: throws)
+    Continuous,  // pre-quantization deltas (device path for TargetSwing; FrameDiff throws)
 };
 
 enum class DeltaBasis {

@@ -179,6 +179,38 @@ CVG_API void cvg_quant_thresholds(double out[256]);
  * lane-FFMA per second measured on `device`, 0 on failure. */
 CVG_API double cvg_measure_ffma_peak(int device, float* ms_out);
 
+/* ---- codec image passes (reference src/codec.cpp:65-165) -------------------
+ * Rasters are 8-bit RGB, interleaved, row-major, width*height*3 bytes
+ * (image.hpp:12-14).  A layout is n_blocks block_w x block_h rectangles with
+ * top-left corners xy[2i], xy[2i+1]; they must lie inside the image and must
+ * not overlap (BlockLayout::validate, codec.cpp:25-54: CVG_EINVAL with the
+ * reference's message otherwise).
+ *
+ * `mem` says where the raster and sum pointers live:
+ *   CVG_MEM_HOST    host memory; the call copies in and out and returns when done;
+ *   CVG_MEM_DEVICE  device memory of the context's device; the passes are
+ *                   enqueued on `stream` (a cudaStream_t, 0 = legacy default)
+ *                   and the call returns without waiting.
+ * xy / plus_rgb / minus_rgb are always host arrays. */
+#define CVG_MEM_HOST 0
+#define CVG_MEM_DEVICE 1
+
+/* embed_blocks' painting (codec.cpp:65-99, paint :58-64): frame_a = base with
+ * every block filled with plus_rgb[3i..3i+2], frame_b the same with minus_rgb.
+ * Pixels outside the blocks are copied unchanged.  One pass over the image. */
+CVG_API int cvg_paint_blocks(cvg_ctx* ctx, const uint8_t* base, uint8_t* frame_a, uint8_t* frame_b, int32_t width,
+                             int32_t height, int32_t block_w, int32_t block_h, int32_t n_blocks, const int32_t* xy,
+                             const uint8_t* plus_rgb, const uint8_t* minus_rgb, int32_t mem, void* stream);
+
+/* decode_blocks' reduction (codec.cpp:124-137): per block, exact integer sums
+ * of each channel over the block's pixels in both frames.
+ * sums[6i..6i+5] = (a.r, a.g, a.b, b.r, b.g, b.b).  The reference's double
+ * accumulation of 8-bit values is exact below 2^53, so these sums equal its
+ * sum_a / sum_b bit for bit once converted to double. */
+CVG_API int cvg_block_sums(cvg_ctx* ctx, const uint8_t* frame_a, const uint8_t* frame_b, int32_t width,
+                           int32_t height, int32_t block_w, int32_t block_h, int32_t n_blocks, const int32_t* xy,
+                           uint64_t* sums, int32_t mem, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -7,6 +7,9 @@ arm may import this module.  The product package never does.
                    (oracle/cv_oracle.c) of the reference search.
 * ``Reference`` -- oracle/_ref/libcolorvibe_ref_v{3,4}.so, the reference's own
                    src/color.cpp + src/search.cpp behind oracle/ref_shim.cpp.
+* ``RefCodec``  -- oracle/_ref/libcolorvibe_ref_codec.so, the reference's own
+                   src/codec.cpp (+ search/color/util) behind
+                   oracle/ref_codec_shim.cpp.
 
 Both return searches as (idx uint32[n], codes uint8[n, 6], deltas f64[n, 3]),
 idx = k * n_angles + m in canonical (radius, angle) order (search.cpp:448-455).
@@ -178,3 +181,92 @@ class Reference(_Lib):
         if n < 0:
             raise ValueError(self.last_error())
         return counts
+
+
+class RefCodec:
+    """The reference codec (codec.cpp) through oracle/ref_codec_shim.cpp."""
+
+    def __init__(self, path: str | None = None):
+        path = path or os.path.join(HERE, "_ref", "libcolorvibe_ref_codec.so")
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"reference codec not built: {path} (run oracle/Makefile)")
+        self.path = path
+        self.lib = C.CDLL(path)
+        self.lib.cvrc_last_error.restype = C.c_char_p
+        self.lib.cvrc_embed.argtypes = [_bp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip, _ip,
+                                        C.POINTER(C.c_char_p), C.c_double, C.c_double, C.c_double, _dp, C.c_int,
+                                        _dp, C.c_int, C.c_int, _bp, _bp]
+        self.lib.cvrc_decode.argtypes = [_bp, _bp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         _ip, _ip, _ip, C.c_double, C.c_double, _ip, _ip, _dp]
+        self.lib.cvrc_layout_json.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _ip, C.POINTER(C.c_char_p),
+                                              C.c_double, C.c_double, C.c_char_p, C.c_int]
+        self.lib.cvrc_report_json.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _ip, C.POINTER(C.c_char_p),
+                                              C.c_double, C.c_double, _ip, _ip, _dp, C.c_char_p, C.c_int]
+
+    @staticmethod
+    def _layout(xy, rgb, bits, names):
+        xy = np.ascontiguousarray(xy, np.int32).reshape(-1, 2)
+        rgb = np.ascontiguousarray(rgb, np.int32).reshape(-1, 3)
+        bits = np.ascontiguousarray(bits, np.int32).reshape(-1)
+        cnames = None
+        if names is not None:
+            cnames = (C.c_char_p * len(names))(*[n.encode() for n in names])
+        return xy, rgb, bits, cnames
+
+    def _raise(self, rc):
+        msg = self.lib.cvrc_last_error().decode()
+        if rc == 1:
+            raise ValueError(msg)
+        raise RuntimeError(msg)
+
+    def embed(self, base, bw, bh, xy, rgb, bits, v_th, r_novib, radii, angles, names=None, refresh_hz=60.0,
+              basis=0):
+        base = np.ascontiguousarray(base, np.uint8)
+        h, w = base.shape[:2]
+        xy, rgb, bits, cnames = self._layout(xy, rgb, bits, names)
+        r = np.ascontiguousarray(radii, np.float64)
+        a = np.ascontiguousarray(angles, np.float64)
+        fa = np.zeros_like(base)
+        fb = np.zeros_like(base)
+        rc = self.lib.cvrc_embed(_ptr(base, _bp), w, h, bw, bh, len(xy), _ptr(xy, _ip), _ptr(rgb, _ip),
+                                 _ptr(bits, _ip), cnames, v_th, r_novib, refresh_hz, _ptr(r, _dp), len(r),
+                                 _ptr(a, _dp), len(a), basis, _ptr(fa, _bp), _ptr(fb, _bp))
+        if rc:
+            self._raise(rc)
+        return fa, fb
+
+    def decode(self, fa, fb, bw, bh, xy, rgb, bits, v_th, r_novib):
+        fa = np.ascontiguousarray(fa, np.uint8)
+        fb = np.ascontiguousarray(fb, np.uint8)
+        xy, rgb, bits, _ = self._layout(xy, rgb, bits, None)
+        n = len(xy)
+        st = np.zeros(n, np.int32)
+        pat = np.zeros(n, np.int32)
+        md = np.zeros((n, 3), np.float64)
+        rc = self.lib.cvrc_decode(_ptr(fa, _bp), _ptr(fb, _bp), fa.shape[1], fa.shape[0], fb.shape[1], fb.shape[0],
+                                  bw, bh, n, _ptr(xy, _ip), _ptr(rgb, _ip), _ptr(bits, _ip), v_th, r_novib,
+                                  _ptr(st, _ip), _ptr(pat, _ip), _ptr(md, _dp))
+        if rc:
+            self._raise(rc)
+        return st, pat, md
+
+    def layout_json(self, bw, bh, xy, rgb, bits, names, v_th, r_novib) -> str:
+        xy, rgb, bits, cnames = self._layout(xy, rgb, bits, names)
+        buf = C.create_string_buffer(1 << 20)
+        n = self.lib.cvrc_layout_json(bw, bh, len(xy), _ptr(xy, _ip), _ptr(rgb, _ip), _ptr(bits, _ip), cnames,
+                                      v_th, r_novib, buf, len(buf))
+        if n < 0:
+            self._raise(1)
+        return buf.value.decode()
+
+    def report_json(self, bw, bh, xy, rgb, bits, names, v_th, r_novib, status, pattern, mean_deltas) -> str:
+        xy, rgb, bits, cnames = self._layout(xy, rgb, bits, names)
+        st = np.ascontiguousarray(status, np.int32)
+        pat = np.ascontiguousarray(pattern, np.int32)
+        md = np.ascontiguousarray(mean_deltas, np.float64)
+        buf = C.create_string_buffer(1 << 20)
+        n = self.lib.cvrc_report_json(bw, bh, len(xy), _ptr(xy, _ip), _ptr(rgb, _ip), _ptr(bits, _ip), cnames,
+                                      v_th, r_novib, _ptr(st, _ip), _ptr(pat, _ip), _ptr(md, _dp), buf, len(buf))
+        if n < 0:
+            self._raise(1)
+        return buf.value.decode()

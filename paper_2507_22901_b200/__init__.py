@@ -8,6 +8,12 @@ ChannelDeltas, ColorPair, DeltaMode, DeltaBasis) and functions
 serial_search, batch_search, channel_deltas, frame_deltas, classify_pair,
 select_best), backed by the fused sm_100a kernel in csrc/cvg_kernels.cu.
 
+The codec surface (module.cpp:216-296): Image, DisplayParams, BlockSpec,
+BlockLayout, FramePair, BlockStatus, BlockResult, make_testcard,
+embed_blocks, decode_blocks, layout_to_json, decode_report_json (+
+layout_from_json); painting and block sums run on the device
+(csrc/cvg_codec.cu).
+
 Extras for batched/pipeline use: `Context.search(...)` (NumPy in, NumPy out,
 one launch for many searches), `Context.plan(...)` (device-resident repeated
 runs), `batch_search_many`, `batch_count_many`.
@@ -32,6 +38,25 @@ except ImportError as _e:  # pragma: no cover - exercised only on a broken build
 
 from ._core import (  # noqa: E402
     BitPattern,
+    BlockLayout,
+    BlockResult,
+    BlockSpec,
+    BlockStatus,
+    DisplayParams,
+    FramePair,
+    Image,
+    Sidecar,
+    block_sums_device,
+    block_sums_host,
+    decode_blocks,
+    decode_report_json,
+    embed_blocks,
+    embed_blocks_opts,
+    layout_from_json,
+    layout_to_json,
+    make_testcard,
+    paint_blocks_device,
+    paint_blocks_host,
     ChannelDeltas,
     ColorPair,
     Context,
@@ -77,6 +102,10 @@ __all__ = [
     "classification_margin", "classify_pair", "d65_white", "displaced_pair", "frame_deltas", "in_gamut",
     "lab_to_srgb", "lab_to_srgb_clipped", "measure_ffma_peak", "quant_thresholds", "select_best",
     "serial_search", "serial_search_opts", "srgb_to_lab", "srgb_to_linear", "version", "LIBRARY_PATH",
+    "BlockLayout", "BlockResult", "BlockSpec", "BlockStatus", "DisplayParams", "FramePair", "Image", "Sidecar",
+    "block_sums_device", "block_sums_host", "decode_blocks", "decode_report_json", "embed_blocks",
+    "embed_blocks_opts", "layout_from_json", "layout_to_json", "make_testcard", "paint_blocks_device",
+    "paint_blocks_host",
 ]
 
 __version__ = "0.1.0"

@@ -35,6 +35,9 @@ HEADERS = [os.path.join(CSRC, h) for h in ("cvg_layout.h", "cvg_internal.h")] + 
     os.path.join(INCLUDE, "cvg.h"),
     os.path.join(INCLUDE, "colorvibe", "color.hpp"),
     os.path.join(INCLUDE, "colorvibe", "search.hpp"),
+    os.path.join(INCLUDE, "colorvibe", "image.hpp"),
+    os.path.join(INCLUDE, "colorvibe", "codec.hpp"),
+    os.path.join(CSRC, "colorvibe_detail.h"),
 ]
 
 
@@ -63,12 +66,19 @@ def _objects() -> list[tuple[str, list[str], list[str], str | None]]:
          [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xptxas", "-v", "-Xcompiler", "-fPIC",
           "-I" + INCLUDE, "-c", src("cvg_kernels.cu"), "-o", o("cvg_kernels.o")],
          o("ptxas.log")),
+        (o("cvg_codec.o"), [src("cvg_codec.cu")] + HEADERS,
+         [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xptxas", "-v", "-Xcompiler", "-fPIC",
+          "-I" + INCLUDE, "-c", src("cvg_codec.cu"), "-o", o("cvg_codec.o")],
+         o("ptxas_codec.log")),
         (o("cvg_host.o"), [src("cvg_host.cpp")] + HEADERS,
          ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + CUDA_INC, "-I" + INCLUDE,
           "-c", src("cvg_host.cpp"), "-o", o("cvg_host.o")], None),
         (o("colorvibe_api.o"), [src("colorvibe_api.cpp")] + HEADERS,
          ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + INCLUDE,
           "-c", src("colorvibe_api.cpp"), "-o", o("colorvibe_api.o")], None),
+        (o("codec_api.o"), [src("codec_api.cpp")] + HEADERS,
+         ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + INCLUDE,
+          "-c", src("codec_api.cpp"), "-o", o("codec_api.o")], None),
     ]
 
 

@@ -12,6 +12,7 @@
 #include <stdexcept>
 
 #include "../../include/cvg.h"
+#include "colorvibe/codec.hpp"
 #include "colorvibe/search.hpp"
 
 namespace py = pybind11;
@@ -357,6 +358,193 @@ PYBIND11_MODULE(_core, m) {
             py::arg("delta_basis") = 0, py::arg("white_point") = py::none());
 
     py::class_<ResultHolder, std::shared_ptr<ResultHolder>>(m, "_Result");
+
+    // ---- codec (module.cpp:216-296; codec.hpp, image.hpp) ----
+    py::class_<Image>(m, "Image", py::buffer_protocol())
+        .def_static("solid", &Image::solid, py::arg("width"), py::arg("height"), py::arg("fill"))
+        .def_static("from_array", [](py::array_t<uint8_t, py::array::c_style | py::array::forcecast> a) {
+            if (a.ndim() != 3 || a.shape(2) != 3) throw std::invalid_argument("expected an (height, width, 3) uint8 array");
+            Image img;
+            img.height = static_cast<int>(a.shape(0));
+            img.width = static_cast<int>(a.shape(1));
+            img.pixels.assign(a.data(), a.data() + a.size());
+            return img;
+        }, py::arg("array"))
+        .def_readonly("width", &Image::width)
+        .def_readonly("height", &Image::height)
+        .def("get", &Image::get, py::arg("x"), py::arg("y"))
+        .def("set", &Image::set, py::arg("x"), py::arg("y"), py::arg("color"))
+        .def(py::self == py::self)
+        // (height, width, 3) uint8 view of the pixels (no copy)
+        .def_property_readonly("pixels", [](py::object self) {
+            Image& img = self.cast<Image&>();
+            return py::array_t<uint8_t>({static_cast<py::ssize_t>(img.height), static_cast<py::ssize_t>(img.width),
+                                         py::ssize_t(3)},
+                                        {static_cast<py::ssize_t>(3 * img.width), py::ssize_t(3), py::ssize_t(1)},
+                                        img.pixels.data(), self);
+        });
+
+    py::class_<DisplayParams>(m, "DisplayParams")
+        .def(py::init<>())
+        .def(py::init([](double hz) {
+                 DisplayParams d;
+                 d.refresh_hz = hz;
+                 return d;
+             }),
+             py::arg("refresh_hz"))
+        .def_readwrite("refresh_hz", &DisplayParams::refresh_hz)
+        .def_readwrite("ccff_hz", &DisplayParams::ccff_hz)
+        .def("validate", &DisplayParams::validate);
+
+    py::class_<BlockSpec>(m, "BlockSpec")
+        .def(py::init<>())
+        .def(py::init([](int x, int y, std::string name, SrgbColor color, BitPattern pattern) {
+                 return BlockSpec{x, y, std::move(name), color, pattern};
+             }),
+             py::arg("x"), py::arg("y"), py::arg("color_name"), py::arg("color"), py::arg("pattern"))
+        .def_readwrite("x", &BlockSpec::x)
+        .def_readwrite("y", &BlockSpec::y)
+        .def_readwrite("color_name", &BlockSpec::color_name)
+        .def_readwrite("color", &BlockSpec::color)
+        .def_readwrite("pattern", &BlockSpec::pattern);
+
+    py::class_<BlockLayout>(m, "BlockLayout")
+        .def(py::init<>())
+        .def_readwrite("block_width", &BlockLayout::block_width)
+        .def_readwrite("block_height", &BlockLayout::block_height)
+        .def_readwrite("blocks", &BlockLayout::blocks)
+        .def("validate", &BlockLayout::validate, py::arg("image_width"), py::arg("image_height"));
+
+    py::class_<FramePair>(m, "FramePair")
+        .def(py::init<>())
+        .def_readwrite("frame_a", &FramePair::frame_a)
+        .def_readwrite("frame_b", &FramePair::frame_b)
+        .def_readwrite("layout", &FramePair::layout);
+
+    py::enum_<BlockStatus>(m, "BlockStatus")
+        .value("PATTERN", BlockStatus::Pattern)
+        .value("NO_SIGNAL", BlockStatus::NoSignal)
+        .value("AMBIGUOUS", BlockStatus::Ambiguous);
+
+    py::class_<BlockResult>(m, "BlockResult")
+        .def(py::init([](BlockStatus st, BitPattern p, std::array<double, 3> md) { return BlockResult{st, p, md}; }),
+             py::arg("status") = BlockStatus::NoSignal, py::arg("pattern") = BitPattern{},
+             py::arg("mean_deltas") = std::array<double, 3>{0.0, 0.0, 0.0})
+        .def_readonly("status", &BlockResult::status)
+        .def_readonly("pattern", &BlockResult::pattern)
+        .def_readonly("mean_deltas", &BlockResult::mean_deltas);
+
+    py::class_<Sidecar>(m, "Sidecar")
+        .def_readonly("layout", &Sidecar::layout)
+        .def_readonly("thresholds", &Sidecar::thresholds);
+
+    m.def(
+        "make_testcard",
+        [](const SrgbColor& color, const BitPattern& pattern, const Thresholds& th, const VibrationGrid& grid,
+           const DisplayParams& disp, int width, int height, int workers) {
+            SearchOptions opts;
+            opts.workers = workers;
+            return make_testcard(color, pattern, th, grid, disp, width, height, opts);
+        },
+        py::arg("color"), py::arg("pattern"), py::arg("thresholds"), py::arg("grid"), py::arg("display"),
+        py::arg("width"), py::arg("height"), py::arg("workers") = 0, py::call_guard<py::gil_scoped_release>());
+    m.def(
+        "embed_blocks",
+        [](const Image& base, const BlockLayout& layout, const Thresholds& th, const VibrationGrid& grid,
+           const DisplayParams& disp, int workers) {
+            SearchOptions opts;
+            opts.workers = workers;
+            return embed_blocks(base, layout, th, grid, disp, opts);
+        },
+        py::arg("base"), py::arg("layout"), py::arg("thresholds"), py::arg("grid"), py::arg("display"),
+        py::arg("workers") = 0, py::call_guard<py::gil_scoped_release>());
+    m.def("embed_blocks_opts", &embed_blocks, py::arg("base"), py::arg("layout"), py::arg("thresholds"),
+          py::arg("grid"), py::arg("display"), py::arg("options"), py::call_guard<py::gil_scoped_release>());
+    m.def("decode_blocks", &decode_blocks, py::arg("frames"), py::arg("thresholds"),
+          py::call_guard<py::gil_scoped_release>());
+    m.def("layout_to_json", &layout_to_json, py::arg("layout"), py::arg("thresholds"));
+    m.def("layout_from_json", &layout_from_json, py::arg("text"));
+    m.def("decode_report_json", &decode_report_json, py::arg("layout"), py::arg("thresholds"), py::arg("results"));
+
+    // ---- codec passes on device memory (C-ABI, pointers as ints) ----
+    m.def(
+        "paint_blocks_device",
+        [](std::shared_ptr<Context> ctx, uintptr_t base, uintptr_t fa, uintptr_t fb, int width, int height, int bw,
+           int bh, py::array_t<int32_t, py::array::c_style | py::array::forcecast> xy,
+           py::array_t<uint8_t, py::array::c_style | py::array::forcecast> plus,
+           py::array_t<uint8_t, py::array::c_style | py::array::forcecast> minus, uintptr_t stream) {
+            const auto n = static_cast<int32_t>(xy.size() / 2);
+            if (xy.size() != 2 * n || plus.size() != 3 * n || minus.size() != 3 * n) {
+                throw std::invalid_argument("xy must be (n, 2); plus and minus (n, 3)");
+            }
+            check(cvg_paint_blocks(ctx->ctx, reinterpret_cast<const uint8_t*>(base), reinterpret_cast<uint8_t*>(fa),
+                                   reinterpret_cast<uint8_t*>(fb), width, height, bw, bh, n, xy.data(), plus.data(),
+                                   minus.data(), CVG_MEM_DEVICE, reinterpret_cast<void*>(stream)));
+        },
+        py::arg("ctx"), py::arg("base"), py::arg("frame_a"), py::arg("frame_b"), py::arg("width"), py::arg("height"),
+        py::arg("block_w"), py::arg("block_h"), py::arg("xy"), py::arg("plus"), py::arg("minus"),
+        py::arg("stream") = 0);
+    m.def(
+        "block_sums_device",
+        [](std::shared_ptr<Context> ctx, uintptr_t fa, uintptr_t fb, int width, int height, int bw, int bh,
+           py::array_t<int32_t, py::array::c_style | py::array::forcecast> xy, uintptr_t sums, uintptr_t stream) {
+            const auto n = static_cast<int32_t>(xy.size() / 2);
+            if (xy.size() != 2 * n) throw std::invalid_argument("xy must be (n, 2)");
+            check(cvg_block_sums(ctx->ctx, reinterpret_cast<const uint8_t*>(fa), reinterpret_cast<const uint8_t*>(fb),
+                                 width, height, bw, bh, n, xy.data(), reinterpret_cast<uint64_t*>(sums),
+                                 CVG_MEM_DEVICE, reinterpret_cast<void*>(stream)));
+        },
+        py::arg("ctx"), py::arg("frame_a"), py::arg("frame_b"), py::arg("width"), py::arg("height"),
+        py::arg("block_w"), py::arg("block_h"), py::arg("xy"), py::arg("sums"), py::arg("stream") = 0);
+    m.def(
+        "paint_blocks_host",
+        [](std::shared_ptr<Context> ctx, py::array_t<uint8_t, py::array::c_style | py::array::forcecast> base, int bw,
+           int bh, py::array_t<int32_t, py::array::c_style | py::array::forcecast> xy,
+           py::array_t<uint8_t, py::array::c_style | py::array::forcecast> plus,
+           py::array_t<uint8_t, py::array::c_style | py::array::forcecast> minus) {
+            if (base.ndim() != 3 || base.shape(2) != 3) throw std::invalid_argument("base must be (height, width, 3)");
+            const auto n = static_cast<int32_t>(xy.size() / 2);
+            if (xy.size() != 2 * n || plus.size() != 3 * n || minus.size() != 3 * n) {
+                throw std::invalid_argument("xy must be (n, 2); plus and minus (n, 3)");
+            }
+            py::array_t<uint8_t> a({base.shape(0), base.shape(1), py::ssize_t(3)});
+            py::array_t<uint8_t> b({base.shape(0), base.shape(1), py::ssize_t(3)});
+            int st;
+            {
+                py::gil_scoped_release nogil;
+                st = cvg_paint_blocks(ctx->ctx, base.data(), a.mutable_data(), b.mutable_data(),
+                                      static_cast<int32_t>(base.shape(1)), static_cast<int32_t>(base.shape(0)), bw, bh,
+                                      n, xy.data(), plus.data(), minus.data(), CVG_MEM_HOST, nullptr);
+            }
+            check(st);
+            return py::make_tuple(a, b);
+        },
+        py::arg("ctx"), py::arg("base"), py::arg("block_w"), py::arg("block_h"), py::arg("xy"), py::arg("plus"),
+        py::arg("minus"));
+    m.def(
+        "block_sums_host",
+        [](std::shared_ptr<Context> ctx, py::array_t<uint8_t, py::array::c_style | py::array::forcecast> fa,
+           py::array_t<uint8_t, py::array::c_style | py::array::forcecast> fb, int bw, int bh,
+           py::array_t<int32_t, py::array::c_style | py::array::forcecast> xy) {
+            if (fa.ndim() != 3 || fa.shape(2) != 3 || fb.ndim() != 3 || fb.shape(0) != fa.shape(0) ||
+                fb.shape(1) != fa.shape(1) || fb.shape(2) != 3) {
+                throw std::invalid_argument("frames must both be (height, width, 3)");
+            }
+            const auto n = static_cast<int32_t>(xy.size() / 2);
+            if (xy.size() != 2 * n) throw std::invalid_argument("xy must be (n, 2)");
+            py::array_t<uint64_t> sums({static_cast<py::ssize_t>(n), py::ssize_t(6)});
+            int st;
+            {
+                py::gil_scoped_release nogil;
+                st = cvg_block_sums(ctx->ctx, fa.data(), fb.data(), static_cast<int32_t>(fa.shape(1)),
+                                    static_cast<int32_t>(fa.shape(0)), bw, bh, n, xy.data(), sums.mutable_data(),
+                                    CVG_MEM_HOST, nullptr);
+            }
+            check(st);
+            return sums;
+        },
+        py::arg("ctx"), py::arg("frame_a"), py::arg("frame_b"), py::arg("block_w"), py::arg("block_h"),
+        py::arg("xy"));
 
     py::class_<Plan>(m, "Plan")
         .def("run", [](Plan& p, uintptr_t stream) { check(cvg_plan_run(p.plan, reinterpret_cast<void*>(stream))); },

@@ -12,10 +12,11 @@
 
 #include "../../include/cvg.h"
 #include "colorvibe/search.hpp"
+#include "colorvibe_detail.h"
 
 namespace colorvibe {
 
-namespace {
+namespace detail {
 
 [[noreturn]] void throw_status(int status) {
     const std::string msg = cvg_last_error();
@@ -41,11 +42,6 @@ cvg_ctx* default_ctx() {
     if (status != CVG_OK) throw std::runtime_error("colorvibe: no usable CUDA device: " + error);
     return ctx;
 }
-
-struct ResultGuard {
-    cvg_result r{};
-    ~ResultGuard() { cvg_result_free(&r); }
-};
 
 int pattern_bits(const BitPattern& p) { return (p.r ? 4 : 0) | (p.g ? 2 : 0) | (p.b ? 1 : 0); }
 
@@ -122,6 +118,12 @@ std::vector<ColorPair> materialize(const cvg_result& r, size_t s, const SrgbColo
     }
     return out;
 }
+
+}  // namespace detail
+
+using namespace detail;
+
+namespace {
 
 void validate_one(const SrgbColor& target, const VibrationGrid& grid, const BitPattern& pattern,
                   const Thresholds& th) {

@@ -28,6 +28,7 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <tuple>
 #include <unordered_map>
 #include <vector>
 
@@ -722,6 +723,12 @@ struct cvg_ctx {
     // pinned result so repeated searches never grow it
     uint64_t hint_sig[4] = {0, 0, 0, 0};
     uint64_t hint_pairs = 0;
+    // codec passes: the layout tables of the last call (device) and the event
+    // after its kernels; the next call's stream waits on it before reuse
+    void* codec_blob = nullptr;
+    size_t codec_blob_bytes = 0;
+    cudaEvent_t codec_done = nullptr;
+    bool codec_pending = false;
     Pool dev;
     Pool host;
 };
@@ -1624,6 +1631,11 @@ void cvg_destroy(cvg_ctx* ctx) {
     }
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamSynchronize(ctx->tail_stream);
+    if (ctx->codec_done) {
+        cudaEventSynchronize(ctx->codec_done);
+        cudaEventDestroy(ctx->codec_done);
+    }
+    if (ctx->codec_blob) cudaFree(ctx->codec_blob);
     for (cudaEvent_t ev : ctx->events) cudaEventDestroy(ev);
     cudaStreamDestroy(ctx->stream);
     cudaStreamDestroy(ctx->copy_stream);
@@ -1869,5 +1881,220 @@ void cvg_d65_white(double out[3]) {
 void cvg_quant_thresholds(double out[256]) { std::memcpy(out, tables().thr, sizeof(double) * 256); }
 
 double cvg_measure_ffma_peak(int device, float* ms_out) { return cvg::measure_ffma_peak(device, ms_out); }
+
+}  // extern "C"
+
+// ============================================================================
+// Codec passes (include/cvg.h; kernels in cvg_codec.cu).
+namespace {
+
+// Per-row span table of a block layout (CSR over rows, x0 sorted), with the
+// reference's BlockLayout::validate checks (codec.cpp:25-54).  Equal-size
+// blocks overlap iff two of them share a row with overlapping x ranges, and
+// then two neighbours in that row's sorted list overlap: one pass over the
+// sorted rows replaces the reference's all-pairs test.
+struct SpanCsr {
+    std::vector<int32_t> row_ptr, x0, blk;
+};
+
+int layout_spans(int32_t width, int32_t height, int32_t bw, int32_t bh, int32_t n, const int32_t* xy, SpanCsr& t) {
+    if (width <= 0 || height <= 0) return fail(CVG_EINVAL, "image dimensions must be positive");
+    if (bw <= 0 || bh <= 0) return fail(CVG_EINVAL, "layout: block size must be positive");
+    if (n < 0 || (n > 0 && !xy)) return fail(CVG_EINVAL, "layout: block positions missing");
+    for (int32_t i = 0; i < n; ++i) {
+        const int64_t x = xy[2 * i], y = xy[2 * i + 1];
+        if (x < 0 || y < 0 || x + bw > width || y + bh > height) {
+            return fail(CVG_EINVAL, "layout: block " + std::to_string(i) + " exceeds image bounds");
+        }
+    }
+    t.row_ptr.assign(static_cast<size_t>(height) + 1, 0);
+    for (int32_t i = 0; i < n; ++i) {
+        for (int32_t r = 0; r < bh; ++r) ++t.row_ptr[xy[2 * i + 1] + r + 1];
+    }
+    for (int32_t y = 0; y < height; ++y) t.row_ptr[y + 1] += t.row_ptr[y];
+    const size_t spans = static_cast<size_t>(t.row_ptr[height]);
+    t.x0.resize(spans);
+    t.blk.resize(spans);
+    std::vector<int32_t> fill(t.row_ptr.begin(), t.row_ptr.end() - 1);
+    for (int32_t i = 0; i < n; ++i) {
+        for (int32_t r = 0; r < bh; ++r) {
+            const int32_t k = fill[xy[2 * i + 1] + r]++;
+            t.x0[k] = xy[2 * i];
+            t.blk[k] = i;
+        }
+    }
+    std::vector<std::pair<int32_t, int32_t>> row;
+    for (int32_t y = 0; y < height; ++y) {
+        const int32_t s = t.row_ptr[y], e = t.row_ptr[y + 1];
+        if (e - s < 2) continue;
+        bool sorted = true;
+        for (int32_t k = s + 1; k < e; ++k) sorted = sorted && t.x0[k - 1] <= t.x0[k];
+        if (!sorted) {
+            row.clear();
+            for (int32_t k = s; k < e; ++k) row.emplace_back(t.x0[k], t.blk[k]);
+            std::sort(row.begin(), row.end());
+            for (int32_t k = s; k < e; ++k) std::tie(t.x0[k], t.blk[k]) = row[k - s];
+        }
+        for (int32_t k = s + 1; k < e; ++k) {
+            if (t.x0[k - 1] + bw > t.x0[k]) {
+                const int32_t a = std::min(t.blk[k - 1], t.blk[k]), b = std::max(t.blk[k - 1], t.blk[k]);
+                return fail(CVG_EINVAL, "layout: blocks " + std::to_string(a) + " and " + std::to_string(b) +
+                                            " overlap");
+            }
+        }
+    }
+    return CVG_OK;
+}
+
+// Uploads the codec tables (pageable source: the driver stages the bytes
+// before cudaMemcpyAsync returns) into the context's codec buffer on `st`,
+// after the previous codec call's kernels are done with it.
+int codec_upload(cvg_ctx* ctx, const std::vector<unsigned char>& blob, cudaStream_t st, unsigned char** dev) {
+    if (!ctx->codec_done) CVG_CUDA(cudaEventCreateWithFlags(&ctx->codec_done, cudaEventDisableTiming));
+    if (blob.size() > ctx->codec_blob_bytes) {
+        if (ctx->codec_pending) CVG_CUDA(cudaEventSynchronize(ctx->codec_done));
+        if (ctx->codec_blob) CVG_CUDA(cudaFree(ctx->codec_blob));
+        ctx->codec_blob = nullptr;
+        ctx->codec_blob_bytes = 0;
+        const size_t bytes = std::max<size_t>(blob.size(), 1u << 16);
+        CVG_CUDA(cudaMalloc(&ctx->codec_blob, bytes));
+        ctx->codec_blob_bytes = bytes;
+    } else if (ctx->codec_pending) {
+        CVG_CUDA(cudaStreamWaitEvent(st, ctx->codec_done, 0));
+    }
+    if (!blob.empty()) CVG_CUDA(cudaMemcpyAsync(ctx->codec_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
+    *dev = static_cast<unsigned char*>(ctx->codec_blob);
+    return CVG_OK;
+}
+
+int codec_finish(cvg_ctx* ctx, cudaStream_t st) {
+    CVG_CUDA(cudaEventRecord(ctx->codec_done, st));
+    ctx->codec_pending = true;
+    return CVG_OK;
+}
+
+template <typename T>
+size_t blob_put(std::vector<unsigned char>& blob, const T* p, size_t n) {
+    const size_t off = (blob.size() + 255) & ~size_t(255);
+    blob.resize(off + sizeof(T) * n);
+    if (n) std::memcpy(blob.data() + off, p, sizeof(T) * n);
+    return off;
+}
+
+// Device scratch for host-memory rasters (from the context's pool).
+struct DevScratch {
+    cvg_ctx* ctx;
+    std::vector<void*> blocks;
+    ~DevScratch() {
+        for (void* b : blocks) ctx->dev.release(b);
+    }
+    void* get(size_t bytes) {
+        void* p = ctx->dev.alloc(bytes);
+        if (p) blocks.push_back(p);
+        return p;
+    }
+};
+
+int codec_common(cvg_ctx* ctx, int32_t mem, const void* a, const void* b, const void* c) {
+    if (!ctx) return fail(CVG_EINVAL, "null context");
+    if (mem != CVG_MEM_HOST && mem != CVG_MEM_DEVICE) return fail(CVG_EINVAL, "mem must be CVG_MEM_HOST or CVG_MEM_DEVICE");
+    if (!a || !b || !c) return fail(CVG_EINVAL, "null raster pointer");
+    return ensure_device(ctx);
+}
+
+}  // namespace
+
+extern "C" {
+
+int cvg_paint_blocks(cvg_ctx* ctx, const uint8_t* base, uint8_t* frame_a, uint8_t* frame_b, int32_t width,
+                     int32_t height, int32_t block_w, int32_t block_h, int32_t n_blocks, const int32_t* xy,
+                     const uint8_t* plus_rgb, const uint8_t* minus_rgb, int32_t mem, void* stream) {
+    if (int e = codec_common(ctx, mem, base, frame_a, frame_b)) return e;
+    if (n_blocks > 0 && (!plus_rgb || !minus_rgb)) return fail(CVG_EINVAL, "block colors missing");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    try {
+        SpanCsr t;
+        if (int e = layout_spans(width, height, block_w, block_h, n_blocks, xy, t)) return e;
+        std::vector<unsigned char> blob;
+        const size_t o_rp = blob_put(blob, t.row_ptr.data(), t.row_ptr.size());
+        const size_t o_x0 = blob_put(blob, t.x0.data(), t.x0.size());
+        const size_t o_bk = blob_put(blob, t.blk.data(), t.blk.size());
+        const size_t o_pl = blob_put(blob, plus_rgb, 3 * static_cast<size_t>(std::max(n_blocks, 0)));
+        const size_t o_mi = blob_put(blob, minus_rgb, 3 * static_cast<size_t>(std::max(n_blocks, 0)));
+        const bool dev_mem = mem == CVG_MEM_DEVICE;
+        cudaStream_t st = dev_mem ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        unsigned char* d = nullptr;
+        if (int e = codec_upload(ctx, blob, st, &d)) return e;
+        const size_t bytes = 3 * static_cast<size_t>(width) * static_cast<size_t>(height);
+        DevScratch scratch{ctx};
+        const uint8_t* d_base = base;
+        uint8_t *d_a = frame_a, *d_b = frame_b;
+        if (!dev_mem) {
+            auto* db = static_cast<uint8_t*>(scratch.get(bytes));
+            d_a = static_cast<uint8_t*>(scratch.get(bytes));
+            d_b = static_cast<uint8_t*>(scratch.get(bytes));
+            if (!db || !d_a || !d_b) return fail(CVG_ENOMEM, "device allocation of the frames failed");
+            CVG_CUDA(cudaMemcpyAsync(db, base, bytes, cudaMemcpyHostToDevice, st));
+            d_base = db;
+        }
+        CVG_CUDA(cvg::launch_paint(d_base, d_a, d_b, width, height, reinterpret_cast<const int32_t*>(d + o_rp),
+                                   reinterpret_cast<const int32_t*>(d + o_x0),
+                                   reinterpret_cast<const int32_t*>(d + o_bk), block_w, d + o_pl, d + o_mi, ctx->sms,
+                                   st));
+        if (int e = codec_finish(ctx, st)) return e;
+        if (!dev_mem) {
+            CVG_CUDA(cudaMemcpyAsync(frame_a, d_a, bytes, cudaMemcpyDeviceToHost, st));
+            CVG_CUDA(cudaMemcpyAsync(frame_b, d_b, bytes, cudaMemcpyDeviceToHost, st));
+            CVG_CUDA(cudaStreamSynchronize(st));
+        }
+        return CVG_OK;
+    } catch (const std::bad_alloc&) {
+        return fail(CVG_ENOMEM, "host allocation failed");
+    }
+}
+
+int cvg_block_sums(cvg_ctx* ctx, const uint8_t* frame_a, const uint8_t* frame_b, int32_t width, int32_t height,
+                   int32_t block_w, int32_t block_h, int32_t n_blocks, const int32_t* xy, uint64_t* sums,
+                   int32_t mem, void* stream) {
+    if (int e = codec_common(ctx, mem, frame_a, frame_b, n_blocks > 0 ? static_cast<const void*>(sums) : frame_a)) {
+        return e;
+    }
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    try {
+        SpanCsr t;
+        if (int e = layout_spans(width, height, block_w, block_h, n_blocks, xy, t)) return e;
+        if (n_blocks == 0) return CVG_OK;
+        std::vector<unsigned char> blob;
+        const size_t o_xy = blob_put(blob, xy, 2 * static_cast<size_t>(n_blocks));
+        const bool dev_mem = mem == CVG_MEM_DEVICE;
+        cudaStream_t st = dev_mem ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        unsigned char* d = nullptr;
+        if (int e = codec_upload(ctx, blob, st, &d)) return e;
+        const size_t bytes = 3 * static_cast<size_t>(width) * static_cast<size_t>(height);
+        DevScratch scratch{ctx};
+        const uint8_t *d_a = frame_a, *d_b = frame_b;
+        auto* d_sums = reinterpret_cast<unsigned long long*>(sums);
+        if (!dev_mem) {
+            auto* da = static_cast<uint8_t*>(scratch.get(bytes));
+            auto* db = static_cast<uint8_t*>(scratch.get(bytes));
+            d_sums = static_cast<unsigned long long*>(scratch.get(sizeof(uint64_t) * 6 * n_blocks));
+            if (!da || !db || !d_sums) return fail(CVG_ENOMEM, "device allocation of the frames failed");
+            CVG_CUDA(cudaMemcpyAsync(da, frame_a, bytes, cudaMemcpyHostToDevice, st));
+            CVG_CUDA(cudaMemcpyAsync(db, frame_b, bytes, cudaMemcpyHostToDevice, st));
+            d_a = da;
+            d_b = db;
+        }
+        CVG_CUDA(cvg::launch_block_sums(d_a, d_b, width, block_w, block_h, n_blocks,
+                                        reinterpret_cast<const int32_t*>(d + o_xy), d_sums, ctx->sms, st));
+        if (int e = codec_finish(ctx, st)) return e;
+        if (!dev_mem) {
+            CVG_CUDA(cudaMemcpyAsync(sums, d_sums, sizeof(uint64_t) * 6 * n_blocks, cudaMemcpyDeviceToHost, st));
+            CVG_CUDA(cudaStreamSynchronize(st));
+        }
+        return CVG_OK;
+    } catch (const std::bad_alloc&) {
+        return fail(CVG_ENOMEM, "host allocation failed");
+    }
+}
 
 }  // extern "C"

@@ -50,3 +50,13 @@ def ctx(cv):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return cv.Context(0)
+
+
+@pytest.fixture(scope="session")
+def ref_codec():
+    from oracle.oracle import RefCodec
+
+    try:
+        return RefCodec()
+    except FileNotFoundError as e:
+        pytest.skip(f"reference codec build absent: {e}")
