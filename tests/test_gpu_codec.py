@@ -138,8 +138,9 @@ def random_layout(rng, w, h, bw, bh, n_max):
     return xy
 
 
-FEASIBLE = [((170, 170, 170), "101"), ((240, 240, 240), "001"), ((100, 100, 240), "110"), ((30, 30, 30), "111"),
-            ((240, 100, 240), "101"), ((100, 240, 100), "010"), ((170, 170, 170), "111"), ((240, 240, 100), "100")]
+# feasible at (50, 0.5) on the matrix grid (pair counts 28, 10, 14, 10, 4, 8 by the oracle)
+FEASIBLE = [((170, 170, 170), "101"), ((240, 240, 240), "001"), ((100, 100, 240), "110"),
+            ((240, 100, 240), "101"), ((170, 170, 170), "111"), ((240, 240, 100), "100")]
 
 
 @pytest.mark.parametrize("w,h,bw,bh,n,seed", [(64, 48, 8, 8, 12, 1), (61, 37, 5, 7, 10, 2), (130, 66, 13, 3, 40, 3),
