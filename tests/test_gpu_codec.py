@@ -176,8 +176,9 @@ def test_embed_decode_match_reference(cv, ctx, ref_codec, w, h, bw, bh, n, seed)
 def test_embed_frame_diff_matches_reference(cv, ctx, ref_codec):
     rng = np.random.default_rng(11)
     base = rng.integers(0, 256, (40, 40, 3)).astype(np.uint8)
-    specs = [(0, 0, "a", (170, 170, 170), "101"), (20, 0, "b", (240, 240, 240), "011"),
-             (0, 20, "c", (100, 100, 240), "110")]
+    # feasible under FrameDiff at (50, 0.5) (oracle pair counts 26, 6, 14)
+    specs = [(0, 0, "a", (170, 170, 170), "101"), (20, 0, "b", (240, 240, 240), "001"),
+             (0, 20, "c", (240, 100, 100), "110")]
     opts = cv.SearchOptions()
     opts.delta_basis = cv.DeltaBasis.FRAME_DIFF
     g = grid(cv)
