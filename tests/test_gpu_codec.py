@@ -231,7 +231,7 @@ def test_device_passes_4k_many_blocks(cv, ctx):
     h, w, bw, bh = 2160, 3840, 16, 16
     base = rng.integers(0, 256, (h, w, 3)).astype(np.uint8)
     xy = [(x, y) for y in range(0, h - bh + 1, 64) for x in range(0, w - bw + 1, 48)]
-    xy += [(3, 5), (23, 5), (2001, 2139)]
+    xy += [(3, 20), (23, 20), (2001, 2139)]  # unaligned x, between grid rows
     xy = np.array(xy, np.int32)
     plus = rng.integers(0, 256, (len(xy), 3)).astype(np.uint8)
     minus = rng.integers(0, 256, (len(xy), 3)).astype(np.uint8)
