@@ -59,6 +59,7 @@ extern "C" {
 
 typedef struct cvg_ctx cvg_ctx;
 typedef struct cvg_plan cvg_plan;
+typedef struct cvg_layout cvg_layout;
 
 /*
  * A batch of searches over one explicit grid.  Search s is
@@ -210,6 +211,21 @@ CVG_API int cvg_paint_blocks(cvg_ctx* ctx, const uint8_t* base, uint8_t* frame_a
 CVG_API int cvg_block_sums(cvg_ctx* ctx, const uint8_t* frame_a, const uint8_t* frame_b, int32_t width,
                            int32_t height, int32_t block_w, int32_t block_h, int32_t n_blocks, const int32_t* xy,
                            uint64_t* sums, int32_t mem, void* stream);
+
+/* Prepared layouts for repeated passes over one geometry (a video stream, a
+ * benchmark): validation and the per-row span table are built and uploaded
+ * once; each pass is then one kernel launch (plus a copy of the 6 B/block
+ * colors for painting).  Same semantics as the one-shot calls above, which
+ * are a prepared layout used once. */
+CVG_API int cvg_layout_create(cvg_ctx* ctx, int32_t width, int32_t height, int32_t block_w, int32_t block_h,
+                              int32_t n_blocks, const int32_t* xy, cvg_layout** out);
+CVG_API void cvg_layout_destroy(cvg_layout* layout);
+CVG_API int cvg_layout_paint(cvg_layout* layout, const uint8_t* base, uint8_t* frame_a, uint8_t* frame_b,
+                             const uint8_t* plus_rgb, const uint8_t* minus_rgb, int32_t mem, void* stream);
+CVG_API int cvg_layout_block_sums(cvg_layout* layout, const uint8_t* frame_a, const uint8_t* frame_b, uint64_t* sums,
+                                  int32_t mem, void* stream);
+/* kernel launches one cvg_layout_paint / cvg_layout_block_sums enqueues */
+CVG_API int cvg_layout_launches(const cvg_layout* layout, int32_t pass);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ one launch for many searches), `Context.plan(...)` (device-resident repeated
 runs), `batch_search_many`, `batch_count_many`.
 
 There is no CPU fallback.  Importing requires the in-tree native build
-(`python -m paper_2507_22901_b200.build`); searches require a CUDA device and
+(`python paper_2507_22901_b200/build.py`); searches require a CUDA device and
 raise RuntimeError otherwise.
 """
 from __future__ import annotations
@@ -33,7 +33,7 @@ try:
 except ImportError as _e:  # pragma: no cover - exercised only on a broken build
     raise ImportError(
         "paper_2507_22901_b200: native extension not built "
-        f"({_e}); run `python -m paper_2507_22901_b200.build`"
+        f"({_e}); run `python paper_2507_22901_b200/build.py`"
     ) from _e
 
 from ._core import (  # noqa: E402
@@ -45,6 +45,7 @@ from ._core import (  # noqa: E402
     DisplayParams,
     FramePair,
     Image,
+    Layout,
     Sidecar,
     block_sums_device,
     block_sums_host,
@@ -102,7 +103,7 @@ __all__ = [
     "classification_margin", "classify_pair", "d65_white", "displaced_pair", "frame_deltas", "in_gamut",
     "lab_to_srgb", "lab_to_srgb_clipped", "measure_ffma_peak", "quant_thresholds", "select_best",
     "serial_search", "serial_search_opts", "srgb_to_lab", "srgb_to_linear", "version", "LIBRARY_PATH",
-    "BlockLayout", "BlockResult", "BlockSpec", "BlockStatus", "DisplayParams", "FramePair", "Image", "Sidecar",
+    "BlockLayout", "BlockResult", "BlockSpec", "BlockStatus", "DisplayParams", "FramePair", "Image", "Layout", "Sidecar",
     "block_sums_device", "block_sums_host", "decode_blocks", "decode_report_json", "embed_blocks",
     "embed_blocks_opts", "layout_from_json", "layout_to_json", "make_testcard", "paint_blocks_device",
     "paint_blocks_host",

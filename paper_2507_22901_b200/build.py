@@ -5,7 +5,7 @@ Produces, next to this file:
                         CUDA kernels for sm_100a, static cudart
   _core.<abi>.so        pybind11 module linked against libcolorvibe_gpu.so
 
-Usage: python -m paper_2507_22901_b200.build   (or __graft_entry__.build()).
+Usage: python paper_2507_22901_b200/build.py   (or __graft_entry__.build()).
 Rebuilds only what is out of date (mtime based).
 """
 from __future__ import annotations

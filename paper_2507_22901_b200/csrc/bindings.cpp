@@ -496,6 +496,41 @@ PYBIND11_MODULE(_core, m) {
         },
         py::arg("ctx"), py::arg("frame_a"), py::arg("frame_b"), py::arg("width"), py::arg("height"),
         py::arg("block_w"), py::arg("block_h"), py::arg("xy"), py::arg("sums"), py::arg("stream") = 0);
+    struct Layout {
+        std::shared_ptr<Context> ctx;
+        cvg_layout* L = nullptr;
+        ~Layout() { cvg_layout_destroy(L); }
+    };
+    py::class_<Layout, std::shared_ptr<Layout>>(m, "Layout")
+        .def(py::init([](std::shared_ptr<Context> ctx, int width, int height, int bw, int bh,
+                         py::array_t<int32_t, py::array::c_style | py::array::forcecast> xy) {
+                 auto l = std::make_shared<Layout>();
+                 l->ctx = ctx;
+                 const auto n = static_cast<int32_t>(xy.size() / 2);
+                 if (xy.size() != 2 * n) throw std::invalid_argument("xy must be (n, 2)");
+                 check(cvg_layout_create(ctx->ctx, width, height, bw, bh, n, xy.data(), &l->L));
+                 return l;
+             }),
+             py::arg("ctx"), py::arg("width"), py::arg("height"), py::arg("block_w"), py::arg("block_h"), py::arg("xy"))
+        .def("paint_device",
+             [](Layout& l, uintptr_t base, uintptr_t fa, uintptr_t fb,
+                py::array_t<uint8_t, py::array::c_style | py::array::forcecast> plus,
+                py::array_t<uint8_t, py::array::c_style | py::array::forcecast> minus, uintptr_t stream) {
+                 check(cvg_layout_paint(l.L, reinterpret_cast<const uint8_t*>(base), reinterpret_cast<uint8_t*>(fa),
+                                        reinterpret_cast<uint8_t*>(fb), plus.data(), minus.data(), CVG_MEM_DEVICE,
+                                        reinterpret_cast<void*>(stream)));
+             },
+             py::arg("base"), py::arg("frame_a"), py::arg("frame_b"), py::arg("plus"), py::arg("minus"),
+             py::arg("stream") = 0)
+        .def("block_sums_device",
+             [](Layout& l, uintptr_t fa, uintptr_t fb, uintptr_t sums, uintptr_t stream) {
+                 check(cvg_layout_block_sums(l.L, reinterpret_cast<const uint8_t*>(fa), reinterpret_cast<const uint8_t*>(fb),
+                                             reinterpret_cast<uint64_t*>(sums), CVG_MEM_DEVICE,
+                                             reinterpret_cast<void*>(stream)));
+             },
+             py::arg("frame_a"), py::arg("frame_b"), py::arg("sums"), py::arg("stream") = 0)
+        .def("launches", [](const Layout& l, int pass) { return cvg_layout_launches(l.L, pass); }, py::arg("pass_") = 0);
+
     m.def(
         "paint_blocks_host",
         [](std::shared_ptr<Context> ctx, py::array_t<uint8_t, py::array::c_style | py::array::forcecast> base, int bw,

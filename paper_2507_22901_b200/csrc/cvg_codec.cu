@@ -43,94 +43,132 @@ __device__ __forceinline__ int first_span_after(const SpanTable& t, int s, int e
     return s;
 }
 
+// Painting.  One CTA per image row (grid-stride over rows), so rows without
+// blocks -- most of a carrier -- are a plain 16-byte copy per thread with
+// fully coalesced loads and stores, no per-pixel work.  In a row with
+// blocks, each 16-byte chunk covers pixels px0..px0+5 (3 bytes each); its
+// byte k belongs to pixel (phase + k) / 3 and channel (phase + k) % 3 with
+// phase = chunk % 3 (16 = 1 mod 3), so the merge is unrolled per phase with
+// compile-time byte positions.  Block colors come packed as r | g << 8 |
+// b << 16 words.  Needs 3 * width % 16 == 0 (rows start on 16 bytes).
 __device__ __forceinline__ uint32_t put_byte(uint32_t w, int byte, uint32_t v) {
     const int sh = 8 * byte;
-    return (w & ~(0xffu << sh)) | (v << sh);
+    return (w & ~(0xffu << sh)) | ((v & 0xffu) << sh);
 }
 
-// 4 pixels (12 bytes = 3 words) per thread; needs width % 4 == 0 so every
-// group starts on a word boundary inside one row.
-__global__ void __launch_bounds__(256) paint4_kernel(const uint32_t* __restrict__ base, uint32_t* __restrict__ fa,
-                                                     uint32_t* __restrict__ fb, int width, int height, SpanTable t,
-                                                     const uint8_t* __restrict__ plus,
-                                                     const uint8_t* __restrict__ minus) {
-    const int gpr = width >> 2;
-    const long long total = static_cast<long long>(gpr) * height;
-    for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < total;
-         g += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const uint32_t w0 = __ldcs(base + 3 * g), w1 = __ldcs(base + 3 * g + 1), w2 = __ldcs(base + 3 * g + 2);
-        const int y = static_cast<int>(g / gpr);
-        const int x = static_cast<int>(g - static_cast<long long>(y) * gpr) << 2;
-        const int s = __ldg(&t.row_ptr[y]), e = __ldg(&t.row_ptr[y + 1]);
-        uint32_t a[3] = {w0, w1, w2}, b[3] = {w0, w1, w2};
-        if (s != e) {
-            int j = first_span_after(t, s, e, x);
+template <int kPhase>
+__device__ __forceinline__ void merge_chunk(uint32_t (&a)[4], uint32_t (&b)[4], const int (&blk)[6],
+                                            const uint32_t (&pc)[6], const uint32_t (&mc)[6]) {
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                while (j < e && __ldg(&t.x0[j]) + t.bw <= x + p) ++j;
-                if (j < e && __ldg(&t.x0[j]) <= x + p) {
-                    const int k = __ldg(&t.blk[j]);
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const int byte = 3 * p + c;  // compile-time after unrolling
-                        a[byte >> 2] = put_byte(a[byte >> 2], byte & 3, __ldg(&plus[3 * k + c]));
-                        b[byte >> 2] = put_byte(b[byte >> 2], byte & 3, __ldg(&minus[3 * k + c]));
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            __stcs(fa + 3 * g + q, a[q]);
-            __stcs(fb + 3 * g + q, b[q]);
+    for (int k = 0; k < 16; ++k) {
+        const int q = (kPhase + k) / 3, ch = (kPhase + k) % 3;
+        if (blk[q] >= 0) {
+            a[k >> 2] = put_byte(a[k >> 2], k & 3, pc[q] >> (8 * ch));
+            b[k >> 2] = put_byte(b[k >> 2], k & 3, mc[q] >> (8 * ch));
         }
     }
 }
 
-// Any width: one pixel per thread.
+__global__ void __launch_bounds__(256) paint16_kernel(const uint4* __restrict__ base, uint4* __restrict__ fa,
+                                                      uint4* __restrict__ fb, int width, int height, SpanTable t,
+                                                      const uint32_t* __restrict__ plus,
+                                                      const uint32_t* __restrict__ minus) {
+    const int cpr = (3 * width) >> 4;  // 16-byte chunks per row
+    for (int y = blockIdx.x; y < height; y += gridDim.x) {
+        const int s = __ldg(&t.row_ptr[y]), e = __ldg(&t.row_ptr[y + 1]);
+        const size_t row0 = static_cast<size_t>(y) * cpr;
+        if (s == e) {
+            for (int c = threadIdx.x; c < cpr; c += blockDim.x) {
+                const uint4 v = __ldcs(base + row0 + c);
+                __stcs(fa + row0 + c, v);
+                __stcs(fb + row0 + c, v);
+            }
+            continue;
+        }
+        int j = -1;  // span cursor: this thread's chunks come in increasing x
+        for (int c = threadIdx.x; c < cpr; c += blockDim.x) {
+            const uint4 v = __ldcs(base + row0 + c);
+            const int px0 = (c << 4) / 3, px1 = ((c << 4) + 15) / 3;
+            if (j < 0) {
+                j = first_span_after(t, s, e, px0);
+            } else {
+                while (j < e && __ldg(&t.x0[j]) + t.bw <= px0) ++j;
+            }
+            if (j >= e || __ldg(&t.x0[j]) > px1) {  // no block touches this chunk
+                __stcs(fa + row0 + c, v);
+                __stcs(fb + row0 + c, v);
+                continue;
+            }
+            int blk[6];
+            uint32_t pc[6], mc[6];
+            int jj = j;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                const int px = px0 + q;
+                while (jj < e && __ldg(&t.x0[jj]) + t.bw <= px) ++jj;
+                const bool in = px <= px1 && jj < e && __ldg(&t.x0[jj]) <= px;
+                blk[q] = in ? __ldg(&t.blk[jj]) : -1;
+                pc[q] = in ? __ldg(&plus[blk[q]]) : 0u;
+                mc[q] = in ? __ldg(&minus[blk[q]]) : 0u;
+            }
+            uint32_t a[4] = {v.x, v.y, v.z, v.w}, b[4] = {v.x, v.y, v.z, v.w};
+            const int phase = c % 3;
+            if (phase == 0) {
+                merge_chunk<0>(a, b, blk, pc, mc);
+            } else if (phase == 1) {
+                merge_chunk<1>(a, b, blk, pc, mc);
+            } else {
+                merge_chunk<2>(a, b, blk, pc, mc);
+            }
+            __stcs(fa + row0 + c, make_uint4(a[0], a[1], a[2], a[3]));
+            __stcs(fb + row0 + c, make_uint4(b[0], b[1], b[2], b[3]));
+        }
+    }
+}
+
+// Any width: one CTA per row, one pixel per thread.
 __global__ void __launch_bounds__(256) paint1_kernel(const uint8_t* __restrict__ base, uint8_t* __restrict__ fa,
                                                      uint8_t* __restrict__ fb, int width, int height, SpanTable t,
-                                                     const uint8_t* __restrict__ plus,
-                                                     const uint8_t* __restrict__ minus) {
-    const long long total = static_cast<long long>(width) * height;
-    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const int y = static_cast<int>(i / width);
-        const int x = static_cast<int>(i - static_cast<long long>(y) * width);
+                                                     const uint32_t* __restrict__ plus,
+                                                     const uint32_t* __restrict__ minus) {
+    for (int y = blockIdx.x; y < height; y += gridDim.x) {
         const int s = __ldg(&t.row_ptr[y]), e = __ldg(&t.row_ptr[y + 1]);
-        int k = -1;
-        if (s != e) {
-            const int j = first_span_after(t, s, e, x);
-            if (j < e && __ldg(&t.x0[j]) <= x) k = __ldg(&t.blk[j]);
-        }
+        const size_t row0 = 3 * static_cast<size_t>(y) * width;
+        int j = -1;
+        for (int x = threadIdx.x; x < width; x += blockDim.x) {
+            int k = -1;
+            if (s != e) {
+                if (j < 0) {
+                    j = first_span_after(t, s, e, x);
+                } else {
+                    while (j < e && __ldg(&t.x0[j]) + t.bw <= x) ++j;
+                }
+                if (j < e && __ldg(&t.x0[j]) <= x) k = __ldg(&t.blk[j]);
+            }
+            const size_t i = row0 + 3 * static_cast<size_t>(x);
+            const uint32_t pw = k < 0 ? 0u : __ldg(&plus[k]), mw = k < 0 ? 0u : __ldg(&minus[k]);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const uint8_t v = base[3 * i + c];
-            fa[3 * i + c] = k < 0 ? v : plus[3 * k + c];
-            fb[3 * i + c] = k < 0 ? v : minus[3 * k + c];
+            for (int c = 0; c < 3; ++c) {
+                const uint8_t v = base[i + c];
+                fa[i + c] = k < 0 ? v : static_cast<uint8_t>(pw >> (8 * c));
+                fb[i + c] = k < 0 ? v : static_cast<uint8_t>(mw >> (8 * c));
+            }
         }
     }
 }
 
-// Block sums.  One CTA of 192 threads (a multiple of 3) per (block, row
-// slice).  A row segment of a block is split into an unaligned head and
-// tail (<= 3 bytes each, done bytewise) and a word-aligned middle.  Byte 0
-// of word w belongs to channel (4w) % 3 = w % 3, and a thread strides by
-// 192 words, so each thread sees one fixed byte->channel phase: it adds the
-// words' even and odd bytes into two packed 16-bit-lane accumulators (two
-// instructions per word and frame) and unpacks them into channels per row.
-constexpr int kSumThreads = 192;
+// Block sums.  CTAs of 8 warps per (block, row slice); a warp sums one row
+// segment of the block at a time, lanes over its 4-byte words (byte 0 of
+// word w is channel w % 3, since 4 = 1 mod 3) plus the unaligned head and
+// tail bytes, in exact integers; then warp shuffles, one shared atomic per
+// warp and channel, and one global atomic per CTA and channel.
+constexpr int kSumThreads = 256;
 
-__device__ __forceinline__ void unpack_add(uint32_t even, uint32_t odd, int phase, unsigned long long* ch) {
-    // bytes 0..3 of the words -> channels (phase + k) % 3
-    const uint32_t s[4] = {even & 0xffffu, odd & 0xffffu, even >> 16, odd >> 16};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int c = (phase + k) % 3;
-        ch[0] += c == 0 ? s[k] : 0u;
-        ch[1] += c == 1 ? s[k] : 0u;
-        ch[2] += c == 2 ? s[k] : 0u;
-    }
+__device__ __forceinline__ void add_word(uint32_t v, int phase, unsigned long long (&ch)[3]) {
+    const uint32_t x0 = (v & 0xffu) + (v >> 24), x1 = (v >> 8) & 0xffu, x2 = (v >> 16) & 0xffu;
+    ch[0] += phase == 0 ? x0 : (phase == 1 ? x2 : x1);
+    ch[1] += phase == 0 ? x1 : (phase == 1 ? x0 : x2);
+    ch[2] += phase == 0 ? x2 : (phase == 1 ? x1 : x0);
 }
 
 __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* __restrict__ fa,
@@ -143,41 +181,27 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
     __syncthreads();
     const int blk = blockIdx.x;
     const int bx = __ldg(&xy[2 * blk]), by = __ldg(&xy[2 * blk + 1]);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned long long ca[3] = {0, 0, 0}, cb[3] = {0, 0, 0};
     const uint32_t* wa = reinterpret_cast<const uint32_t*>(fa);
     const uint32_t* wb = reinterpret_cast<const uint32_t*>(fb);
-    for (int r = blockIdx.y; r < block_h; r += gridDim.y) {
+    for (int r = blockIdx.y * (kSumThreads / 32) + warp; r < block_h; r += gridDim.y * (kSumThreads / 32)) {
         const long long s = 3 * (static_cast<long long>(by + r) * width + bx);  // segment [s, e)
         const long long e = s + 3ll * block_w;
-        const long long ws = (s + 3) >> 2, we = e >> 2;  // whole words inside the segment
-        if (ws < we) {
-            const int phase = static_cast<int>((ws + threadIdx.x) % 3);
-            uint32_t ea = 0, oa = 0, eb = 0, ob = 0;
-            int n = 0;
-            for (long long w = ws + threadIdx.x; w < we; w += kSumThreads) {
-                const uint32_t va = __ldcs(wa + w), vb = __ldcs(wb + w);
-                ea += va & 0x00ff00ffu;
-                oa += (va >> 8) & 0x00ff00ffu;
-                eb += vb & 0x00ff00ffu;
-                ob += (vb >> 8) & 0x00ff00ffu;
-                if (++n == 256) {  // 16-bit lanes hold 257 bytes of 255
-                    unpack_add(ea, oa, phase, ca);
-                    unpack_add(eb, ob, phase, cb);
-                    ea = oa = eb = ob = 0;
-                    n = 0;
-                }
-            }
-            unpack_add(ea, oa, phase, ca);
-            unpack_add(eb, ob, phase, cb);
+        long long ws = (s + 3) >> 2, we = e >> 2;  // whole words inside the segment
+        if (ws > we) ws = we;
+        for (long long w = ws + lane; w < we; w += 32) {
+            const int phase = static_cast<int>(w % 3);
+            add_word(__ldcs(wa + w), phase, ca);
+            add_word(__ldcs(wb + w), phase, cb);
         }
-        // head bytes [s, 4*ws) and tail bytes [4*we, e) (all bytes when the
-        // segment holds no whole word)
+        // head [s, 4 ws) and tail [4 we, e) bytes (the whole segment when it
+        // holds no whole word)
         const long long h_end = ws < we ? 4 * ws : e;
         const long long t_beg = ws < we ? 4 * we : e;
         const int n_head = static_cast<int>(h_end - s), n_tail = static_cast<int>(e - t_beg);
-        const int tid = threadIdx.x;
-        if (tid < n_head + n_tail) {
-            const long long i = tid < n_head ? s + tid : t_beg + (tid - n_head);
+        for (int k = lane; k < n_head + n_tail; k += 32) {
+            const long long i = k < n_head ? s + k : t_beg + (k - n_head);
             const int c = static_cast<int>(i % 3);
             const unsigned long long va = fa[i], vb = fb[i];
             ca[0] += c == 0 ? va : 0ull;
@@ -188,7 +212,6 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
             cb[2] += c == 2 ? vb : 0ull;
         }
     }
-    // CTA reduction: warp shuffles, then one shared atomic per warp and channel
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         for (int o = 16; o; o >>= 1) {
@@ -196,40 +219,31 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
             cb[c] += __shfl_xor_sync(0xffffffffu, cb[c], o);
         }
     }
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            atomicAdd(&red[c], ca[c]);
-            atomicAdd(&red[3 + c], cb[c]);
+            if (ca[c]) atomicAdd(&red[c], ca[c]);
+            if (cb[c]) atomicAdd(&red[3 + c], cb[c]);
         }
     }
     __syncthreads();
     if (threadIdx.x < 6 && red[threadIdx.x]) atomicAdd(&sums[6 * blk + threadIdx.x], red[threadIdx.x]);
 }
 
-int grid_for(long long items, int threads, int sms) {
-    const long long want = (items + threads - 1) / threads;
-    const long long cap = static_cast<long long>(sms) * 16;  // 16 x 256 threads per SM: full occupancy
-    return static_cast<int>(want < cap ? (want > 0 ? want : 1) : cap);
-}
-
 }  // namespace
 
 cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int width, int height,
                          const int32_t* row_ptr, const int32_t* x0, const int32_t* blk, int block_w,
-                         const uint8_t* plus, const uint8_t* minus, int sms, cudaStream_t st) {
+                         const uint32_t* plus, const uint32_t* minus, int sms, cudaStream_t st) {
     const SpanTable t{row_ptr, x0, blk, block_w};
-    const bool words = width % 4 == 0 && (reinterpret_cast<uintptr_t>(base) & 3) == 0 &&
-                       (reinterpret_cast<uintptr_t>(fa) & 3) == 0 && (reinterpret_cast<uintptr_t>(fb) & 3) == 0;
-    if (words) {
-        const long long groups = static_cast<long long>(width / 4) * height;
-        paint4_kernel<<<grid_for(groups, 256, sms), 256, 0, st>>>(reinterpret_cast<const uint32_t*>(base),
-                                                                 reinterpret_cast<uint32_t*>(fa),
-                                                                 reinterpret_cast<uint32_t*>(fb), width, height, t,
-                                                                 plus, minus);
+    const int grid = height < sms * 8 ? height : sms * 8;  // 8 x 256 threads per SM, rows grid-strided
+    const bool vec = (3 * width) % 16 == 0 && ((reinterpret_cast<uintptr_t>(base) | reinterpret_cast<uintptr_t>(fa) |
+                                                reinterpret_cast<uintptr_t>(fb)) & 15) == 0;
+    if (vec) {
+        paint16_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(base), reinterpret_cast<uint4*>(fa),
+                                             reinterpret_cast<uint4*>(fb), width, height, t, plus, minus);
     } else {
-        const long long px = static_cast<long long>(width) * height;
-        paint1_kernel<<<grid_for(px, 256, sms), 256, 0, st>>>(base, fa, fb, width, height, t, plus, minus);
+        paint1_kernel<<<grid, 256, 0, st>>>(base, fa, fb, width, height, t, plus, minus);
     }
     return cudaGetLastError();
 }
@@ -237,14 +251,17 @@ cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int widt
 cudaError_t launch_block_sums(const uint8_t* fa, const uint8_t* fb, int width, int block_w, int block_h,
                               int n_blocks, const int32_t* xy, unsigned long long* sums, int sms, cudaStream_t st) {
     if (n_blocks <= 0) return cudaSuccess;
+    if ((reinterpret_cast<uintptr_t>(fa) | reinterpret_cast<uintptr_t>(fb)) & 3) return cudaErrorMisalignedAddress;
     cudaError_t e = cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * 6 * static_cast<size_t>(n_blocks), st);
     if (e != cudaSuccess) return e;
-    // enough CTAs for ~8 per SM in total, row slices of each block
+    // row slices of 8 rows per CTA, at most what fills ~8 CTAs per SM in total
+    const long long rows8 = (block_h + 7) / 8;
     const long long want = (static_cast<long long>(sms) * 8 + n_blocks - 1) / n_blocks;
-    int slices = static_cast<int>(want < block_h ? (want > 0 ? want : 1) : block_h);
+    long long slices = want < rows8 ? want : rows8;
+    if (slices < 1) slices = 1;
     if (slices > 65535) slices = 65535;
-    if ((reinterpret_cast<uintptr_t>(fa) & 3) || (reinterpret_cast<uintptr_t>(fb) & 3)) return cudaErrorMisalignedAddress;
-    block_sums_kernel<<<dim3(n_blocks, slices), kSumThreads, 0, st>>>(fa, fb, width, block_w, block_h, xy, sums);
+    block_sums_kernel<<<dim3(n_blocks, static_cast<unsigned>(slices)), kSumThreads, 0, st>>>(fa, fb, width, block_w,
+                                                                                             block_h, xy, sums);
     return cudaGetLastError();
 }
 

@@ -723,15 +723,13 @@ struct cvg_ctx {
     // pinned result so repeated searches never grow it
     uint64_t hint_sig[4] = {0, 0, 0, 0};
     uint64_t hint_pairs = 0;
-    // codec passes: the layout tables of the last call (device) and the event
-    // after its kernels; the next call's stream waits on it before reuse
-    void* codec_blob = nullptr;
-    size_t codec_blob_bytes = 0;
-    cudaEvent_t codec_done = nullptr;
-    bool codec_pending = false;
+    // scratch layout of the one-shot codec calls (cvg_paint_blocks / cvg_block_sums)
+    cvg_layout* codec_layout = nullptr;
     Pool dev;
     Pool host;
 };
+
+void layout_free(cvg_layout* L);  // codec section below
 
 struct cvg_plan {
     cvg_ctx* ctx = nullptr;
@@ -1631,11 +1629,7 @@ void cvg_destroy(cvg_ctx* ctx) {
     }
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamSynchronize(ctx->tail_stream);
-    if (ctx->codec_done) {
-        cudaEventSynchronize(ctx->codec_done);
-        cudaEventDestroy(ctx->codec_done);
-    }
-    if (ctx->codec_blob) cudaFree(ctx->codec_blob);
+    layout_free(ctx->codec_layout);
     for (cudaEvent_t ev : ctx->events) cudaEventDestroy(ev);
     cudaStreamDestroy(ctx->stream);
     cudaStreamDestroy(ctx->copy_stream);
@@ -1946,33 +1940,6 @@ int layout_spans(int32_t width, int32_t height, int32_t bw, int32_t bh, int32_t 
     return CVG_OK;
 }
 
-// Uploads the codec tables (pageable source: the driver stages the bytes
-// before cudaMemcpyAsync returns) into the context's codec buffer on `st`,
-// after the previous codec call's kernels are done with it.
-int codec_upload(cvg_ctx* ctx, const std::vector<unsigned char>& blob, cudaStream_t st, unsigned char** dev) {
-    if (!ctx->codec_done) CVG_CUDA(cudaEventCreateWithFlags(&ctx->codec_done, cudaEventDisableTiming));
-    if (blob.size() > ctx->codec_blob_bytes) {
-        if (ctx->codec_pending) CVG_CUDA(cudaEventSynchronize(ctx->codec_done));
-        if (ctx->codec_blob) CVG_CUDA(cudaFree(ctx->codec_blob));
-        ctx->codec_blob = nullptr;
-        ctx->codec_blob_bytes = 0;
-        const size_t bytes = std::max<size_t>(blob.size(), 1u << 16);
-        CVG_CUDA(cudaMalloc(&ctx->codec_blob, bytes));
-        ctx->codec_blob_bytes = bytes;
-    } else if (ctx->codec_pending) {
-        CVG_CUDA(cudaStreamWaitEvent(st, ctx->codec_done, 0));
-    }
-    if (!blob.empty()) CVG_CUDA(cudaMemcpyAsync(ctx->codec_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
-    *dev = static_cast<unsigned char*>(ctx->codec_blob);
-    return CVG_OK;
-}
-
-int codec_finish(cvg_ctx* ctx, cudaStream_t st) {
-    CVG_CUDA(cudaEventRecord(ctx->codec_done, st));
-    ctx->codec_pending = true;
-    return CVG_OK;
-}
-
 template <typename T>
 size_t blob_put(std::vector<unsigned char>& blob, const T* p, size_t n) {
     const size_t off = (blob.size() + 255) & ~size_t(255);
@@ -1995,6 +1962,142 @@ struct DevScratch {
     }
 };
 
+}  // namespace
+
+// A block layout on the device: span table, positions and the packed block
+// colors of the last paint, in one allocation.  `done` follows the last pass
+// that read it; anything that rewrites the tables first makes its stream wait
+// on it (or waits on the host when the allocation must grow).
+struct cvg_layout {
+    cvg_ctx* ctx = nullptr;
+    int32_t width = 0, height = 0, bw = 0, bh = 0, n = 0;
+    unsigned char* d = nullptr;
+    size_t cap = 0;
+    size_t o_rp = 0, o_x0 = 0, o_bk = 0, o_xy = 0, o_pl = 0, o_mi = 0;
+    cudaEvent_t done = nullptr;
+    bool pending = false;
+};
+
+namespace {
+
+int layout_reserve(cvg_layout* L, size_t bytes, cudaStream_t st) {
+    if (!L->done) CVG_CUDA(cudaEventCreateWithFlags(&L->done, cudaEventDisableTiming));
+    if (bytes > L->cap) {
+        if (L->pending) CVG_CUDA(cudaEventSynchronize(L->done));
+        if (L->d) CVG_CUDA(cudaFree(L->d));
+        L->d = nullptr;
+        L->cap = 0;
+        const size_t cap = std::max<size_t>(bytes, 1u << 16);
+        CVG_CUDA(cudaMalloc(reinterpret_cast<void**>(&L->d), cap));
+        L->cap = cap;
+    } else if (L->pending) {
+        CVG_CUDA(cudaStreamWaitEvent(st, L->done, 0));
+    }
+    return CVG_OK;
+}
+
+// Validates the geometry, builds the span table and uploads it on `st`
+// (pageable source: the driver stages the bytes before the call returns).
+int layout_prepare(cvg_layout* L, int32_t width, int32_t height, int32_t bw, int32_t bh, int32_t n,
+                   const int32_t* xy, cudaStream_t st) {
+    SpanCsr t;
+    if (int e = layout_spans(width, height, bw, bh, n, xy, t)) return e;
+    std::vector<unsigned char> blob;
+    L->o_rp = blob_put(blob, t.row_ptr.data(), t.row_ptr.size());
+    L->o_x0 = blob_put(blob, t.x0.data(), t.x0.size());
+    L->o_bk = blob_put(blob, t.blk.data(), t.blk.size());
+    L->o_xy = blob_put(blob, xy, 2 * static_cast<size_t>(n));
+    L->o_pl = (blob.size() + 255) & ~size_t(255);  // colors: written by each paint
+    L->o_mi = L->o_pl + ((4 * static_cast<size_t>(n) + 255) & ~size_t(255));
+    const size_t total = L->o_mi + 4 * static_cast<size_t>(n);
+    if (int e = layout_reserve(L, total, st)) return e;
+    CVG_CUDA(cudaMemcpyAsync(L->d, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
+    L->width = width;
+    L->height = height;
+    L->bw = bw;
+    L->bh = bh;
+    L->n = n;
+    return CVG_OK;
+}
+
+int layout_colors(cvg_layout* L, const uint8_t* plus, const uint8_t* minus, cudaStream_t st) {
+    if (L->n == 0) return CVG_OK;
+    if (!plus || !minus) return fail(CVG_EINVAL, "block colors missing");
+    std::vector<uint32_t> w(2 * static_cast<size_t>(L->n));
+    for (int32_t i = 0; i < L->n; ++i) {
+        w[i] = plus[3 * i] | (uint32_t(plus[3 * i + 1]) << 8) | (uint32_t(plus[3 * i + 2]) << 16);
+        w[L->n + i] = minus[3 * i] | (uint32_t(minus[3 * i + 1]) << 8) | (uint32_t(minus[3 * i + 2]) << 16);
+    }
+    if (L->pending) CVG_CUDA(cudaStreamWaitEvent(st, L->done, 0));
+    CVG_CUDA(cudaMemcpyAsync(L->d + L->o_pl, w.data(), 4 * static_cast<size_t>(L->n), cudaMemcpyHostToDevice, st));
+    CVG_CUDA(cudaMemcpyAsync(L->d + L->o_mi, w.data() + L->n, 4 * static_cast<size_t>(L->n), cudaMemcpyHostToDevice,
+                             st));
+    return CVG_OK;
+}
+
+int layout_finish(cvg_layout* L, cudaStream_t st) {
+    CVG_CUDA(cudaEventRecord(L->done, st));
+    L->pending = true;
+    return CVG_OK;
+}
+
+int paint_pass(cvg_layout* L, const uint8_t* base, uint8_t* fa, uint8_t* fb, const uint8_t* plus,
+               const uint8_t* minus, int32_t mem, cudaStream_t st) {
+    cvg_ctx* ctx = L->ctx;
+    if (int e = layout_colors(L, plus, minus, st)) return e;
+    const size_t bytes = 3 * static_cast<size_t>(L->width) * static_cast<size_t>(L->height);
+    DevScratch scratch{ctx};
+    const uint8_t* d_base = base;
+    uint8_t *d_a = fa, *d_b = fb;
+    if (mem == CVG_MEM_HOST) {
+        auto* db = static_cast<uint8_t*>(scratch.get(bytes));
+        d_a = static_cast<uint8_t*>(scratch.get(bytes));
+        d_b = static_cast<uint8_t*>(scratch.get(bytes));
+        if (!db || !d_a || !d_b) return fail(CVG_ENOMEM, "device allocation of the frames failed");
+        CVG_CUDA(cudaMemcpyAsync(db, base, bytes, cudaMemcpyHostToDevice, st));
+        d_base = db;
+    }
+    CVG_CUDA(cvg::launch_paint(d_base, d_a, d_b, L->width, L->height, reinterpret_cast<const int32_t*>(L->d + L->o_rp),
+                               reinterpret_cast<const int32_t*>(L->d + L->o_x0),
+                               reinterpret_cast<const int32_t*>(L->d + L->o_bk), L->bw,
+                               reinterpret_cast<const uint32_t*>(L->d + L->o_pl),
+                               reinterpret_cast<const uint32_t*>(L->d + L->o_mi), ctx->sms, st));
+    if (int e = layout_finish(L, st)) return e;
+    if (mem == CVG_MEM_HOST) {
+        CVG_CUDA(cudaMemcpyAsync(fa, d_a, bytes, cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaMemcpyAsync(fb, d_b, bytes, cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaStreamSynchronize(st));
+    }
+    return CVG_OK;
+}
+
+int sums_pass(cvg_layout* L, const uint8_t* fa, const uint8_t* fb, uint64_t* sums, int32_t mem, cudaStream_t st) {
+    if (L->n == 0) return CVG_OK;
+    cvg_ctx* ctx = L->ctx;
+    const size_t bytes = 3 * static_cast<size_t>(L->width) * static_cast<size_t>(L->height);
+    DevScratch scratch{ctx};
+    const uint8_t *d_a = fa, *d_b = fb;
+    auto* d_sums = reinterpret_cast<unsigned long long*>(sums);
+    if (mem == CVG_MEM_HOST) {
+        auto* da = static_cast<uint8_t*>(scratch.get(bytes));
+        auto* db = static_cast<uint8_t*>(scratch.get(bytes));
+        d_sums = static_cast<unsigned long long*>(scratch.get(sizeof(uint64_t) * 6 * L->n));
+        if (!da || !db || !d_sums) return fail(CVG_ENOMEM, "device allocation of the frames failed");
+        CVG_CUDA(cudaMemcpyAsync(da, fa, bytes, cudaMemcpyHostToDevice, st));
+        CVG_CUDA(cudaMemcpyAsync(db, fb, bytes, cudaMemcpyHostToDevice, st));
+        d_a = da;
+        d_b = db;
+    }
+    CVG_CUDA(cvg::launch_block_sums(d_a, d_b, L->width, L->bw, L->bh, L->n,
+                                    reinterpret_cast<const int32_t*>(L->d + L->o_xy), d_sums, ctx->sms, st));
+    if (int e = layout_finish(L, st)) return e;
+    if (mem == CVG_MEM_HOST) {
+        CVG_CUDA(cudaMemcpyAsync(sums, d_sums, sizeof(uint64_t) * 6 * L->n, cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaStreamSynchronize(st));
+    }
+    return CVG_OK;
+}
+
 int codec_common(cvg_ctx* ctx, int32_t mem, const void* a, const void* b, const void* c) {
     if (!ctx) return fail(CVG_EINVAL, "null context");
     if (mem != CVG_MEM_HOST && mem != CVG_MEM_DEVICE) return fail(CVG_EINVAL, "mem must be CVG_MEM_HOST or CVG_MEM_DEVICE");
@@ -2002,7 +2105,24 @@ int codec_common(cvg_ctx* ctx, int32_t mem, const void* a, const void* b, const 
     return ensure_device(ctx);
 }
 
+cvg_layout* scratch_layout(cvg_ctx* ctx) {
+    if (!ctx->codec_layout) {
+        ctx->codec_layout = new cvg_layout();
+        ctx->codec_layout->ctx = ctx;
+    }
+    return ctx->codec_layout;
+}
+
 }  // namespace
+
+void layout_free(cvg_layout* L) {
+    if (!L) return;
+    cudaSetDevice(L->ctx->device);
+    if (L->pending) cudaEventSynchronize(L->done);
+    if (L->done) cudaEventDestroy(L->done);
+    if (L->d) cudaFree(L->d);
+    delete L;
+}
 
 extern "C" {
 
@@ -2010,44 +2130,12 @@ int cvg_paint_blocks(cvg_ctx* ctx, const uint8_t* base, uint8_t* frame_a, uint8_
                      int32_t height, int32_t block_w, int32_t block_h, int32_t n_blocks, const int32_t* xy,
                      const uint8_t* plus_rgb, const uint8_t* minus_rgb, int32_t mem, void* stream) {
     if (int e = codec_common(ctx, mem, base, frame_a, frame_b)) return e;
-    if (n_blocks > 0 && (!plus_rgb || !minus_rgb)) return fail(CVG_EINVAL, "block colors missing");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     try {
-        SpanCsr t;
-        if (int e = layout_spans(width, height, block_w, block_h, n_blocks, xy, t)) return e;
-        std::vector<unsigned char> blob;
-        const size_t o_rp = blob_put(blob, t.row_ptr.data(), t.row_ptr.size());
-        const size_t o_x0 = blob_put(blob, t.x0.data(), t.x0.size());
-        const size_t o_bk = blob_put(blob, t.blk.data(), t.blk.size());
-        const size_t o_pl = blob_put(blob, plus_rgb, 3 * static_cast<size_t>(std::max(n_blocks, 0)));
-        const size_t o_mi = blob_put(blob, minus_rgb, 3 * static_cast<size_t>(std::max(n_blocks, 0)));
-        const bool dev_mem = mem == CVG_MEM_DEVICE;
-        cudaStream_t st = dev_mem ? static_cast<cudaStream_t>(stream) : ctx->stream;
-        unsigned char* d = nullptr;
-        if (int e = codec_upload(ctx, blob, st, &d)) return e;
-        const size_t bytes = 3 * static_cast<size_t>(width) * static_cast<size_t>(height);
-        DevScratch scratch{ctx};
-        const uint8_t* d_base = base;
-        uint8_t *d_a = frame_a, *d_b = frame_b;
-        if (!dev_mem) {
-            auto* db = static_cast<uint8_t*>(scratch.get(bytes));
-            d_a = static_cast<uint8_t*>(scratch.get(bytes));
-            d_b = static_cast<uint8_t*>(scratch.get(bytes));
-            if (!db || !d_a || !d_b) return fail(CVG_ENOMEM, "device allocation of the frames failed");
-            CVG_CUDA(cudaMemcpyAsync(db, base, bytes, cudaMemcpyHostToDevice, st));
-            d_base = db;
-        }
-        CVG_CUDA(cvg::launch_paint(d_base, d_a, d_b, width, height, reinterpret_cast<const int32_t*>(d + o_rp),
-                                   reinterpret_cast<const int32_t*>(d + o_x0),
-                                   reinterpret_cast<const int32_t*>(d + o_bk), block_w, d + o_pl, d + o_mi, ctx->sms,
-                                   st));
-        if (int e = codec_finish(ctx, st)) return e;
-        if (!dev_mem) {
-            CVG_CUDA(cudaMemcpyAsync(frame_a, d_a, bytes, cudaMemcpyDeviceToHost, st));
-            CVG_CUDA(cudaMemcpyAsync(frame_b, d_b, bytes, cudaMemcpyDeviceToHost, st));
-            CVG_CUDA(cudaStreamSynchronize(st));
-        }
-        return CVG_OK;
+        cudaStream_t st = mem == CVG_MEM_DEVICE ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        cvg_layout* L = scratch_layout(ctx);
+        if (int e = layout_prepare(L, width, height, block_w, block_h, n_blocks, xy, st)) return e;
+        return paint_pass(L, base, frame_a, frame_b, plus_rgb, minus_rgb, mem, st);
     } catch (const std::bad_alloc&) {
         return fail(CVG_ENOMEM, "host allocation failed");
     }
@@ -2061,40 +2149,79 @@ int cvg_block_sums(cvg_ctx* ctx, const uint8_t* frame_a, const uint8_t* frame_b,
     }
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     try {
-        SpanCsr t;
-        if (int e = layout_spans(width, height, block_w, block_h, n_blocks, xy, t)) return e;
-        if (n_blocks == 0) return CVG_OK;
-        std::vector<unsigned char> blob;
-        const size_t o_xy = blob_put(blob, xy, 2 * static_cast<size_t>(n_blocks));
-        const bool dev_mem = mem == CVG_MEM_DEVICE;
-        cudaStream_t st = dev_mem ? static_cast<cudaStream_t>(stream) : ctx->stream;
-        unsigned char* d = nullptr;
-        if (int e = codec_upload(ctx, blob, st, &d)) return e;
-        const size_t bytes = 3 * static_cast<size_t>(width) * static_cast<size_t>(height);
-        DevScratch scratch{ctx};
-        const uint8_t *d_a = frame_a, *d_b = frame_b;
-        auto* d_sums = reinterpret_cast<unsigned long long*>(sums);
-        if (!dev_mem) {
-            auto* da = static_cast<uint8_t*>(scratch.get(bytes));
-            auto* db = static_cast<uint8_t*>(scratch.get(bytes));
-            d_sums = static_cast<unsigned long long*>(scratch.get(sizeof(uint64_t) * 6 * n_blocks));
-            if (!da || !db || !d_sums) return fail(CVG_ENOMEM, "device allocation of the frames failed");
-            CVG_CUDA(cudaMemcpyAsync(da, frame_a, bytes, cudaMemcpyHostToDevice, st));
-            CVG_CUDA(cudaMemcpyAsync(db, frame_b, bytes, cudaMemcpyHostToDevice, st));
-            d_a = da;
-            d_b = db;
-        }
-        CVG_CUDA(cvg::launch_block_sums(d_a, d_b, width, block_w, block_h, n_blocks,
-                                        reinterpret_cast<const int32_t*>(d + o_xy), d_sums, ctx->sms, st));
-        if (int e = codec_finish(ctx, st)) return e;
-        if (!dev_mem) {
-            CVG_CUDA(cudaMemcpyAsync(sums, d_sums, sizeof(uint64_t) * 6 * n_blocks, cudaMemcpyDeviceToHost, st));
-            CVG_CUDA(cudaStreamSynchronize(st));
-        }
-        return CVG_OK;
+        cudaStream_t st = mem == CVG_MEM_DEVICE ? static_cast<cudaStream_t>(stream) : ctx->stream;
+        cvg_layout* L = scratch_layout(ctx);
+        if (int e = layout_prepare(L, width, height, block_w, block_h, n_blocks, xy, st)) return e;
+        return sums_pass(L, frame_a, frame_b, sums, mem, st);
     } catch (const std::bad_alloc&) {
         return fail(CVG_ENOMEM, "host allocation failed");
     }
+}
+
+int cvg_layout_create(cvg_ctx* ctx, int32_t width, int32_t height, int32_t block_w, int32_t block_h, int32_t n_blocks,
+                      const int32_t* xy, cvg_layout** out) {
+    if (!ctx || !out) return fail(CVG_EINVAL, "null context or output pointer");
+    *out = nullptr;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    if (int e = ensure_device(ctx)) return e;
+    auto* L = new (std::nothrow) cvg_layout();
+    if (!L) return fail(CVG_ENOMEM, "host allocation failed");
+    L->ctx = ctx;
+    int e;
+    try {
+        e = layout_prepare(L, width, height, block_w, block_h, n_blocks, xy, ctx->stream);
+    } catch (const std::bad_alloc&) {
+        e = fail(CVG_ENOMEM, "host allocation failed");
+    }
+    if (!e) {
+        const cudaError_t ce = cudaStreamSynchronize(ctx->stream);
+        if (ce != cudaSuccess) e = cuda_fail(ce, "layout upload");
+    }
+    if (e) {
+        layout_free(L);
+        return e;
+    }
+    *out = L;
+    return CVG_OK;
+}
+
+void cvg_layout_destroy(cvg_layout* L) {
+    if (!L) return;
+    std::lock_guard<std::recursive_mutex> lk(L->ctx->mu);
+    layout_free(L);
+}
+
+int cvg_layout_paint(cvg_layout* L, const uint8_t* base, uint8_t* frame_a, uint8_t* frame_b, const uint8_t* plus_rgb,
+                     const uint8_t* minus_rgb, int32_t mem, void* stream) {
+    if (!L) return fail(CVG_EINVAL, "null layout");
+    if (int e = codec_common(L->ctx, mem, base, frame_a, frame_b)) return e;
+    std::lock_guard<std::recursive_mutex> lk(L->ctx->mu);
+    try {
+        cudaStream_t st = mem == CVG_MEM_DEVICE ? static_cast<cudaStream_t>(stream) : L->ctx->stream;
+        return paint_pass(L, base, frame_a, frame_b, plus_rgb, minus_rgb, mem, st);
+    } catch (const std::bad_alloc&) {
+        return fail(CVG_ENOMEM, "host allocation failed");
+    }
+}
+
+int cvg_layout_block_sums(cvg_layout* L, const uint8_t* frame_a, const uint8_t* frame_b, uint64_t* sums, int32_t mem,
+                          void* stream) {
+    if (!L) return fail(CVG_EINVAL, "null layout");
+    if (int e = codec_common(L->ctx, mem, frame_a, frame_b, L->n > 0 ? static_cast<const void*>(sums) : frame_a)) {
+        return e;
+    }
+    std::lock_guard<std::recursive_mutex> lk(L->ctx->mu);
+    try {
+        cudaStream_t st = mem == CVG_MEM_DEVICE ? static_cast<cudaStream_t>(stream) : L->ctx->stream;
+        return sums_pass(L, frame_a, frame_b, sums, mem, st);
+    } catch (const std::bad_alloc&) {
+        return fail(CVG_ENOMEM, "host allocation failed");
+    }
+}
+
+int cvg_layout_launches(const cvg_layout* L, int32_t pass) {
+    if (!L) return 0;
+    return pass == 0 ? 1 : (L->n > 0 ? 1 : 0);  // paint: 1 kernel; sums: 1 kernel (+ a memset)
 }
 
 }  // extern "C"
