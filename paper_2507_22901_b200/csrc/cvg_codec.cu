@@ -69,59 +69,86 @@ __device__ __forceinline__ void merge_chunk(uint32_t (&a)[4], uint32_t (&b)[4], 
     }
 }
 
+// Warp tasks: a task is 128 consecutive 16-byte chunks (2 KB) of one row;
+// lane l takes chunks l, l+32, l+64, l+96, all four loads issued before any
+// store (4 x 16 B in flight per lane).  Row spans are warp-uniform; a lane's
+// span cursor only moves forward across its chunks.
+constexpr int kTaskChunks = 128;
+
+template <int kPhase>
+__device__ __forceinline__ uint4 merge_pixels(uint4 v, int px0, int px1, int& j, int e, const SpanTable& t,
+                                              const uint32_t* __restrict__ colors, uint4& other,
+                                              const uint32_t* __restrict__ colors2) {
+    int blk[6];
+    uint32_t pc[6], mc[6];
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        const int px = px0 + q;
+        while (j < e && __ldg(&t.x0[j]) + t.bw <= px) ++j;
+        const bool in = px <= px1 && j < e && __ldg(&t.x0[j]) <= px;
+        blk[q] = in ? __ldg(&t.blk[j]) : -1;
+        pc[q] = in ? __ldg(&colors[blk[q]]) : 0u;
+        mc[q] = in ? __ldg(&colors2[blk[q]]) : 0u;
+    }
+    uint32_t a[4] = {v.x, v.y, v.z, v.w}, b[4] = {v.x, v.y, v.z, v.w};
+    merge_chunk<kPhase>(a, b, blk, pc, mc);
+    other = make_uint4(b[0], b[1], b[2], b[3]);
+    return make_uint4(a[0], a[1], a[2], a[3]);
+}
+
 __global__ void __launch_bounds__(256) paint16_kernel(const uint4* __restrict__ base, uint4* __restrict__ fa,
                                                       uint4* __restrict__ fb, int width, int height, SpanTable t,
                                                       const uint32_t* __restrict__ plus,
                                                       const uint32_t* __restrict__ minus) {
     const int cpr = (3 * width) >> 4;  // 16-byte chunks per row
-    for (int y = blockIdx.x; y < height; y += gridDim.x) {
-        const int s = __ldg(&t.row_ptr[y]), e = __ldg(&t.row_ptr[y + 1]);
+    const int tpr = (cpr + kTaskChunks - 1) / kTaskChunks;
+    const long long tasks = static_cast<long long>(tpr) * height;
+    const int lane = threadIdx.x & 31;
+    const long long nwarps = static_cast<long long>(gridDim.x) * (blockDim.x >> 5);
+    for (long long task = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; task < tasks;
+         task += nwarps) {
+        const int y = static_cast<int>(task / tpr);
+        const int c0 = static_cast<int>(task - static_cast<long long>(y) * tpr) * kTaskChunks + lane;
         const size_t row0 = static_cast<size_t>(y) * cpr;
-        if (s == e) {
-            for (int c = threadIdx.x; c < cpr; c += blockDim.x) {
-                const uint4 v = __ldcs(base + row0 + c);
-                __stcs(fa + row0 + c, v);
-                __stcs(fb + row0 + c, v);
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int c = c0 + 32 * u;
+            if (c < cpr) v[u] = __ldcs(base + row0 + c);
+        }
+        const int s = __ldg(&t.row_ptr[y]), e = __ldg(&t.row_ptr[y + 1]);
+        if (s == e) {  // no block crosses this row: a copy
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int c = c0 + 32 * u;
+                if (c < cpr) {
+                    __stcs(fa + row0 + c, v[u]);
+                    __stcs(fb + row0 + c, v[u]);
+                }
             }
             continue;
         }
-        int j = -1;  // span cursor: this thread's chunks come in increasing x
-        for (int c = threadIdx.x; c < cpr; c += blockDim.x) {
-            const uint4 v = __ldcs(base + row0 + c);
-            const int px0 = (c << 4) / 3, px1 = ((c << 4) + 15) / 3;
-            if (j < 0) {
-                j = first_span_after(t, s, e, px0);
-            } else {
-                while (j < e && __ldg(&t.x0[j]) + t.bw <= px0) ++j;
-            }
-            if (j >= e || __ldg(&t.x0[j]) > px1) {  // no block touches this chunk
-                __stcs(fa + row0 + c, v);
-                __stcs(fb + row0 + c, v);
-                continue;
-            }
-            int blk[6];
-            uint32_t pc[6], mc[6];
-            int jj = j;
+        int j = c0 < cpr ? first_span_after(t, s, e, (c0 << 4) / 3) : e;
 #pragma unroll
-            for (int q = 0; q < 6; ++q) {
-                const int px = px0 + q;
-                while (jj < e && __ldg(&t.x0[jj]) + t.bw <= px) ++jj;
-                const bool in = px <= px1 && jj < e && __ldg(&t.x0[jj]) <= px;
-                blk[q] = in ? __ldg(&t.blk[jj]) : -1;
-                pc[q] = in ? __ldg(&plus[blk[q]]) : 0u;
-                mc[q] = in ? __ldg(&minus[blk[q]]) : 0u;
+        for (int u = 0; u < 4; ++u) {
+            const int c = c0 + 32 * u;
+            if (c >= cpr) break;
+            const int px0 = (c << 4) / 3, px1 = ((c << 4) + 15) / 3;
+            while (j < e && __ldg(&t.x0[j]) + t.bw <= px0) ++j;
+            uint4 ra = v[u], rb = v[u];
+            if (j < e && __ldg(&t.x0[j]) <= px1) {  // a block touches this chunk
+                int jj = j;
+                const int phase = c % 3;
+                if (phase == 0) {
+                    ra = merge_pixels<0>(v[u], px0, px1, jj, e, t, plus, rb, minus);
+                } else if (phase == 1) {
+                    ra = merge_pixels<1>(v[u], px0, px1, jj, e, t, plus, rb, minus);
+                } else {
+                    ra = merge_pixels<2>(v[u], px0, px1, jj, e, t, plus, rb, minus);
+                }
             }
-            uint32_t a[4] = {v.x, v.y, v.z, v.w}, b[4] = {v.x, v.y, v.z, v.w};
-            const int phase = c % 3;
-            if (phase == 0) {
-                merge_chunk<0>(a, b, blk, pc, mc);
-            } else if (phase == 1) {
-                merge_chunk<1>(a, b, blk, pc, mc);
-            } else {
-                merge_chunk<2>(a, b, blk, pc, mc);
-            }
-            __stcs(fa + row0 + c, make_uint4(a[0], a[1], a[2], a[3]));
-            __stcs(fb + row0 + c, make_uint4(b[0], b[1], b[2], b[3]));
+            __stcs(fa + row0 + c, ra);
+            __stcs(fb + row0 + c, rb);
         }
     }
 }
@@ -157,23 +184,37 @@ __global__ void __launch_bounds__(256) paint1_kernel(const uint8_t* __restrict__
     }
 }
 
-// Block sums.  CTAs of 8 warps per (block, row slice); a warp sums one row
-// segment of the block at a time, lanes over its 4-byte words (byte 0 of
-// word w is channel w % 3, since 4 = 1 mod 3) plus the unaligned head and
-// tail bytes, in exact integers; then warp shuffles, one shared atomic per
-// warp and channel, and one global atomic per CTA and channel.
+// Block sums.  A CTA takes one block (or a slice of its rows) and flattens
+// it into (row, 16-byte chunk) items, so every thread issues independent
+// 16-byte loads however narrow the block is.  Byte i of the chunk starting
+// at byte offset 16c belongs to channel (c + i) % 3 (16 = 1 mod 3): bytes are
+// summed into three chunk-relative accumulators with compile-time indices and
+// rotated into r, g, b once per chunk.  Chunks that straddle the block's row
+// segment [s, e) mask their bytes; a chunk running past the end of the image
+// is read bytewise.  Sums are exact integers.
 constexpr int kSumThreads = 256;
 
-__device__ __forceinline__ void add_word(uint32_t v, int phase, unsigned long long (&ch)[3]) {
-    const uint32_t x0 = (v & 0xffu) + (v >> 24), x1 = (v >> 8) & 0xffu, x2 = (v >> 16) & 0xffu;
-    ch[0] += phase == 0 ? x0 : (phase == 1 ? x2 : x1);
-    ch[1] += phase == 0 ? x1 : (phase == 1 ? x0 : x2);
-    ch[2] += phase == 0 ? x2 : (phase == 1 ? x1 : x0);
+__device__ __forceinline__ void rotate_add(const uint32_t (&rel)[3], int phase, unsigned long long (&ch)[3]) {
+    ch[0] += phase == 0 ? rel[0] : (phase == 1 ? rel[2] : rel[1]);
+    ch[1] += phase == 0 ? rel[1] : (phase == 1 ? rel[0] : rel[2]);
+    ch[2] += phase == 0 ? rel[2] : (phase == 1 ? rel[1] : rel[0]);
+}
+
+__device__ __forceinline__ void sum_chunk(uint4 v, long long o, long long s, long long e, bool full,
+                                          uint32_t (&rel)[3]) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    rel[0] = rel[1] = rel[2] = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        uint32_t byte = (w[i >> 2] >> (8 * (i & 3))) & 0xffu;
+        if (!full) byte = (o + i >= s && o + i < e) ? byte : 0u;
+        rel[i % 3] += byte;
+    }
 }
 
 __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* __restrict__ fa,
                                                                  const uint8_t* __restrict__ fb, int width,
-                                                                 int block_w, int block_h,
+                                                                 int block_w, int block_h, long long total_bytes,
                                                                  const int32_t* __restrict__ xy,
                                                                  unsigned long long* __restrict__ sums) {
     __shared__ unsigned long long red[6];
@@ -181,35 +222,40 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
     __syncthreads();
     const int blk = blockIdx.x;
     const int bx = __ldg(&xy[2 * blk]), by = __ldg(&xy[2 * blk + 1]);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int cpr = (3 * block_w + 15) / 16 + 1;  // chunks a row segment can touch
+    const int r0 = static_cast<int>((static_cast<long long>(block_h) * blockIdx.y) / gridDim.y);
+    const int r1 = static_cast<int>((static_cast<long long>(block_h) * (blockIdx.y + 1)) / gridDim.y);
+    const long long items = static_cast<long long>(r1 - r0) * cpr;
     unsigned long long ca[3] = {0, 0, 0}, cb[3] = {0, 0, 0};
-    const uint32_t* wa = reinterpret_cast<const uint32_t*>(fa);
-    const uint32_t* wb = reinterpret_cast<const uint32_t*>(fb);
-    for (int r = blockIdx.y * (kSumThreads / 32) + warp; r < block_h; r += gridDim.y * (kSumThreads / 32)) {
-        const long long s = 3 * (static_cast<long long>(by + r) * width + bx);  // segment [s, e)
+    const uint4* va4 = reinterpret_cast<const uint4*>(fa);
+    const uint4* vb4 = reinterpret_cast<const uint4*>(fb);
+    for (long long it = threadIdx.x; it < items; it += kSumThreads) {
+        const int r = r0 + static_cast<int>(it / cpr);
+        const int k = static_cast<int>(it - static_cast<long long>(r - r0) * cpr);
+        const long long s = 3 * (static_cast<long long>(by + r) * width + bx);
         const long long e = s + 3ll * block_w;
-        long long ws = (s + 3) >> 2, we = e >> 2;  // whole words inside the segment
-        if (ws > we) ws = we;
-        for (long long w = ws + lane; w < we; w += 32) {
-            const int phase = static_cast<int>(w % 3);
-            add_word(__ldcs(wa + w), phase, ca);
-            add_word(__ldcs(wb + w), phase, cb);
-        }
-        // head [s, 4 ws) and tail [4 we, e) bytes (the whole segment when it
-        // holds no whole word)
-        const long long h_end = ws < we ? 4 * ws : e;
-        const long long t_beg = ws < we ? 4 * we : e;
-        const int n_head = static_cast<int>(h_end - s), n_tail = static_cast<int>(e - t_beg);
-        for (int k = lane; k < n_head + n_tail; k += 32) {
-            const long long i = k < n_head ? s + k : t_beg + (k - n_head);
-            const int c = static_cast<int>(i % 3);
-            const unsigned long long va = fa[i], vb = fb[i];
-            ca[0] += c == 0 ? va : 0ull;
-            ca[1] += c == 1 ? va : 0ull;
-            ca[2] += c == 2 ? va : 0ull;
-            cb[0] += c == 0 ? vb : 0ull;
-            cb[1] += c == 1 ? vb : 0ull;
-            cb[2] += c == 2 ? vb : 0ull;
+        const long long c = (s >> 4) + k;
+        const long long o = c << 4;
+        if (o >= e) continue;
+        const int phase = static_cast<int>(c % 3);
+        uint32_t rel[3];
+        if (o + 16 <= total_bytes) {
+            const bool full = o >= s && o + 16 <= e;
+            sum_chunk(__ldcs(va4 + c), o, s, e, full, rel);
+            rotate_add(rel, phase, ca);
+            sum_chunk(__ldcs(vb4 + c), o, s, e, full, rel);
+            rotate_add(rel, phase, cb);
+        } else {  // the image's last partial chunk
+            for (long long i = (o > s ? o : s); i < e; ++i) {
+                const int ch = static_cast<int>(i % 3);
+                const unsigned long long x = fa[i], y = fb[i];
+                ca[0] += ch == 0 ? x : 0ull;
+                ca[1] += ch == 1 ? x : 0ull;
+                ca[2] += ch == 2 ? x : 0ull;
+                cb[0] += ch == 0 ? y : 0ull;
+                cb[1] += ch == 1 ? y : 0ull;
+                cb[2] += ch == 2 ? y : 0ull;
+            }
         }
     }
 #pragma unroll
@@ -219,7 +265,7 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
             cb[c] += __shfl_xor_sync(0xffffffffu, cb[c], o);
         }
     }
-    if (lane == 0) {
+    if ((threadIdx.x & 31) == 0) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             if (ca[c]) atomicAdd(&red[c], ca[c]);
@@ -236,7 +282,7 @@ cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int widt
                          const int32_t* row_ptr, const int32_t* x0, const int32_t* blk, int block_w,
                          const uint32_t* plus, const uint32_t* minus, int sms, cudaStream_t st) {
     const SpanTable t{row_ptr, x0, blk, block_w};
-    const int grid = height < sms * 8 ? height : sms * 8;  // 8 x 256 threads per SM, rows grid-strided
+    const int grid = height < sms * 8 ? height : sms * 8;  // 8 x 256 threads per SM
     const bool vec = (3 * width) % 16 == 0 && ((reinterpret_cast<uintptr_t>(base) | reinterpret_cast<uintptr_t>(fa) |
                                                 reinterpret_cast<uintptr_t>(fb)) & 15) == 0;
     if (vec) {
@@ -248,20 +294,20 @@ cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int widt
     return cudaGetLastError();
 }
 
-cudaError_t launch_block_sums(const uint8_t* fa, const uint8_t* fb, int width, int block_w, int block_h,
+cudaError_t launch_block_sums(const uint8_t* fa, const uint8_t* fb, int width, int height, int block_w, int block_h,
                               int n_blocks, const int32_t* xy, unsigned long long* sums, int sms, cudaStream_t st) {
+    const long long total_bytes = 3ll * width * height;
     if (n_blocks <= 0) return cudaSuccess;
-    if ((reinterpret_cast<uintptr_t>(fa) | reinterpret_cast<uintptr_t>(fb)) & 3) return cudaErrorMisalignedAddress;
+    if ((reinterpret_cast<uintptr_t>(fa) | reinterpret_cast<uintptr_t>(fb)) & 15) return cudaErrorMisalignedAddress;
     cudaError_t e = cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * 6 * static_cast<size_t>(n_blocks), st);
     if (e != cudaSuccess) return e;
-    // row slices of 8 rows per CTA, at most what fills ~8 CTAs per SM in total
-    const long long rows8 = (block_h + 7) / 8;
+    // row slices so that ~8 CTAs per SM are in flight in total
     const long long want = (static_cast<long long>(sms) * 8 + n_blocks - 1) / n_blocks;
-    long long slices = want < rows8 ? want : rows8;
+    long long slices = want < block_h ? want : block_h;
     if (slices < 1) slices = 1;
     if (slices > 65535) slices = 65535;
-    block_sums_kernel<<<dim3(n_blocks, static_cast<unsigned>(slices)), kSumThreads, 0, st>>>(fa, fb, width, block_w,
-                                                                                             block_h, xy, sums);
+    block_sums_kernel<<<dim3(n_blocks, static_cast<unsigned>(slices)), kSumThreads, 0, st>>>(
+        fa, fb, width, block_w, block_h, total_bytes, xy, sums);
     return cudaGetLastError();
 }
 

@@ -2088,7 +2088,7 @@ int sums_pass(cvg_layout* L, const uint8_t* fa, const uint8_t* fb, uint64_t* sum
         d_a = da;
         d_b = db;
     }
-    CVG_CUDA(cvg::launch_block_sums(d_a, d_b, L->width, L->bw, L->bh, L->n,
+    CVG_CUDA(cvg::launch_block_sums(d_a, d_b, L->width, L->height, L->bw, L->bh, L->n,
                                     reinterpret_cast<const int32_t*>(L->d + L->o_xy), d_sums, ctx->sms, st));
     if (int e = layout_finish(L, st)) return e;
     if (mem == CVG_MEM_HOST) {

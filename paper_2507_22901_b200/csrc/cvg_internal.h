@@ -27,7 +27,7 @@ size_t search_smem_bytes();
 cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int width, int height,
                          const int32_t* row_ptr, const int32_t* x0, const int32_t* blk, int block_w,
                          const uint32_t* plus, const uint32_t* minus, int sms, cudaStream_t st);
-cudaError_t launch_block_sums(const uint8_t* fa, const uint8_t* fb, int width, int block_w, int block_h,
+cudaError_t launch_block_sums(const uint8_t* fa, const uint8_t* fb, int width, int height, int block_w, int block_h,
                               int n_blocks, const int32_t* xy, unsigned long long* sums, int sms, cudaStream_t st);
 double measure_ffma_peak(int device, float* ms_out);
 
