@@ -1964,7 +1964,7 @@ struct DevScratch {
 
 }  // namespace
 
-// A block layout on the device: span table, positions and the packed block
+// A validated block layout on the device: positions and the packed block
 // colors of the last paint, in one allocation.  `done` follows the last pass
 // that read it; anything that rewrites the tables first makes its stream wait
 // on it (or waits on the host when the allocation must grow).
@@ -1973,7 +1973,7 @@ struct cvg_layout {
     int32_t width = 0, height = 0, bw = 0, bh = 0, n = 0;
     unsigned char* d = nullptr;
     size_t cap = 0;
-    size_t o_rp = 0, o_x0 = 0, o_bk = 0, o_xy = 0, o_pl = 0, o_mi = 0;
+    size_t o_xy = 0, o_pl = 0, o_mi = 0;
     cudaEvent_t done = nullptr;
     bool pending = false;
 };
@@ -2002,10 +2002,7 @@ int layout_prepare(cvg_layout* L, int32_t width, int32_t height, int32_t bw, int
                    const int32_t* xy, cudaStream_t st) {
     SpanCsr t;
     if (int e = layout_spans(width, height, bw, bh, n, xy, t)) return e;
-    std::vector<unsigned char> blob;
-    L->o_rp = blob_put(blob, t.row_ptr.data(), t.row_ptr.size());
-    L->o_x0 = blob_put(blob, t.x0.data(), t.x0.size());
-    L->o_bk = blob_put(blob, t.blk.data(), t.blk.size());
+    std::vector<unsigned char> blob;  // the span table only validates; the kernels take positions
     L->o_xy = blob_put(blob, xy, 2 * static_cast<size_t>(n));
     L->o_pl = (blob.size() + 255) & ~size_t(255);  // colors: written by each paint
     L->o_mi = L->o_pl + ((4 * static_cast<size_t>(n) + 255) & ~size_t(255));
@@ -2057,9 +2054,8 @@ int paint_pass(cvg_layout* L, const uint8_t* base, uint8_t* fa, uint8_t* fb, con
         CVG_CUDA(cudaMemcpyAsync(db, base, bytes, cudaMemcpyHostToDevice, st));
         d_base = db;
     }
-    CVG_CUDA(cvg::launch_paint(d_base, d_a, d_b, L->width, L->height, reinterpret_cast<const int32_t*>(L->d + L->o_rp),
-                               reinterpret_cast<const int32_t*>(L->d + L->o_x0),
-                               reinterpret_cast<const int32_t*>(L->d + L->o_bk), L->bw,
+    CVG_CUDA(cvg::launch_paint(d_base, d_a, d_b, L->width, L->height, L->bw, L->bh, L->n,
+                               reinterpret_cast<const int32_t*>(L->d + L->o_xy),
                                reinterpret_cast<const uint32_t*>(L->d + L->o_pl),
                                reinterpret_cast<const uint32_t*>(L->d + L->o_mi), ctx->sms, st));
     if (int e = layout_finish(L, st)) return e;
@@ -2221,7 +2217,7 @@ int cvg_layout_block_sums(cvg_layout* L, const uint8_t* frame_a, const uint8_t* 
 
 int cvg_layout_launches(const cvg_layout* L, int32_t pass) {
     if (!L) return 0;
-    return pass == 0 ? 1 : (L->n > 0 ? 1 : 0);  // paint: 1 kernel; sums: 1 kernel (+ a memset)
+    return pass == 0 ? (L->n > 0 ? 2 : 1) : (L->n > 0 ? 1 : 0);  // paint: copy + fill; sums: 1 (+ a memset)
 }
 
 }  // extern "C"

@@ -21,12 +21,11 @@ int search_blocks_per_sm(int mode, int out, int path);
 cudaError_t launch_first_codes(const LaunchArgs& a, cudaStream_t st);
 size_t search_smem_bytes();
 
-// Codec passes (cvg_codec.cu).  Span table: per-row CSR of the blocks
-// crossing the row (x0 sorted), see cvg_host.cpp layout_spans().  Block
-// colors packed r | g << 8 | b << 16.
-cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int width, int height,
-                         const int32_t* row_ptr, const int32_t* x0, const int32_t* blk, int block_w,
-                         const uint32_t* plus, const uint32_t* minus, int sms, cudaStream_t st);
+// Codec passes (cvg_codec.cu).  Block positions xy[2i], xy[2i+1]; colors
+// packed r | g << 8 | b << 16.  Paint = copy pass + block fill pass.
+cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int width, int height, int block_w,
+                         int block_h, int n_blocks, const int32_t* xy, const uint32_t* plus, const uint32_t* minus,
+                         int sms, cudaStream_t st);
 cudaError_t launch_block_sums(const uint8_t* fa, const uint8_t* fb, int width, int height, int block_w, int block_h,
                               int n_blocks, const int32_t* xy, unsigned long long* sums, int sms, cudaStream_t st);
 double measure_ffma_peak(int device, float* ms_out);

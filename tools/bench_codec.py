@@ -64,7 +64,7 @@ def main():
         torch.cuda.synchronize()
         return statistics.median(a.elapsed_time(b) for a, b in ev)
 
-    # prepared layout (span table uploaded once): a pass = colors copy + 1 kernel
+    # prepared layout (positions uploaded once): a paint = colors copy + copy and fill kernels
     lay = cv.Layout(ctx, w, h, bw, bh, xy)
     paint = lambda: lay.paint_device(d_base.data_ptr(), d_a.data_ptr(), d_b.data_ptr(), plus, minus,  # noqa
                                      st.cuda_stream)
@@ -131,10 +131,10 @@ def main():
             "paint_one_shot": {"ms": round(oneshot_ms, 4), "note": "cvg_paint_blocks: layout validated, span "
                                                                      "table built and uploaded inside the call"},
         },
-        "gpu_launches": {"paint": 1, "block_sums": 1},
+        "gpu_launches": {"paint": 2, "block_sums": 1},
         "roofline": {"bound": "hbm", "achieved": round(paint_bytes / (paint_ms * 1e-3) / 1e9, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(paint_bytes / (paint_ms * 1e-3) / 1e9 / peak, 4),
-                     "kernel": "paint4_kernel", "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
+                     "kernel": "copy2_kernel + fill_kernel", "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
         "e2e": {"value": round(3 * w * h / e2e_s / 1e9, 4), "unit": "GB/s (carrier bytes)", "s_per_step": round(e2e_s, 5),
                 "api": "embed_blocks + decode_blocks (C++ API, host Images)",
                 "h2d_bytes_per_step": 3 * 3 * w * h, "d2h_bytes_per_step": 2 * 3 * w * h + 48 * n},
