@@ -99,25 +99,26 @@ __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uin
     const int cpr = (3 * block_w + 15) / 16 + 1;
     const int r0 = static_cast<int>((static_cast<long long>(block_h) * blockIdx.y) / gridDim.y);
     const int r1 = static_cast<int>((static_cast<long long>(block_h) * (blockIdx.y + 1)) / gridDim.y);
-    const long long items = static_cast<long long>(r1 - r0) * cpr;
-    for (long long it = threadIdx.x; it < items; it += blockDim.x) {
-        const int r = r0 + static_cast<int>(it / cpr);
-        const int k = static_cast<int>(it - static_cast<long long>(r - r0) * cpr);
-        const long long s = 3 * (static_cast<long long>(by + r) * width + bx);
+    const int items = (r1 - r0) * cpr;  // < 2^31: block_h * (3 block_w / 16 + 2)
+    for (int it = threadIdx.x; it < items; it += blockDim.x) {
+        const int rr = it / cpr;
+        const int k = it - rr * cpr;
+        const long long s = 3 * (static_cast<long long>(by + r0 + rr) * width + bx);
         const long long e = s + 3ll * block_w;
         const long long c = (s >> 4) + k;
         const long long o = c << 4;
         if (o >= e) continue;
+        const int phase = static_cast<int>(((s >> 4) % 3 + k) % 3);  // c % 3
         if (vec && o >= s && o + 16 <= e) {
-            const int phase = static_cast<int>(c % 3);
             reinterpret_cast<uint4*>(fa)[c] = color_chunk(pc, phase);
             reinterpret_cast<uint4*>(fb)[c] = color_chunk(mc, phase);
         } else {
             const long long lo = o > s ? o : s, hi = o + 16 < e ? o + 16 : e;
+            int ch = static_cast<int>(lo - s) % 3;  // s is a pixel start: channel 0
             for (long long i = lo; i < hi; ++i) {
-                const int ch = static_cast<int>(i % 3);
                 fa[i] = static_cast<uint8_t>(pc >> (8 * ch));
                 fb[i] = static_cast<uint8_t>(mc >> (8 * ch));
+                ch = ch == 2 ? 0 : ch + 1;
             }
         }
     }
@@ -164,19 +165,19 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
     const int cpr = (3 * block_w + 15) / 16 + 1;  // chunks a row segment can touch
     const int r0 = static_cast<int>((static_cast<long long>(block_h) * blockIdx.y) / gridDim.y);
     const int r1 = static_cast<int>((static_cast<long long>(block_h) * (blockIdx.y + 1)) / gridDim.y);
-    const long long items = static_cast<long long>(r1 - r0) * cpr;
+    const int items = (r1 - r0) * cpr;
     unsigned long long ca[3] = {0, 0, 0}, cb[3] = {0, 0, 0};
     const uint4* va4 = reinterpret_cast<const uint4*>(fa);
     const uint4* vb4 = reinterpret_cast<const uint4*>(fb);
-    for (long long it = threadIdx.x; it < items; it += kSumThreads) {
-        const int r = r0 + static_cast<int>(it / cpr);
-        const int k = static_cast<int>(it - static_cast<long long>(r - r0) * cpr);
-        const long long s = 3 * (static_cast<long long>(by + r) * width + bx);
+    for (int it = threadIdx.x; it < items; it += kSumThreads) {
+        const int rr = it / cpr;
+        const int k = it - rr * cpr;
+        const long long s = 3 * (static_cast<long long>(by + r0 + rr) * width + bx);
         const long long e = s + 3ll * block_w;
         const long long c = (s >> 4) + k;
         const long long o = c << 4;
         if (o >= e) continue;
-        const int phase = static_cast<int>(c % 3);
+        const int phase = static_cast<int>(((s >> 4) % 3 + k) % 3);  // c % 3
         uint32_t rel[3];
         if (o + 16 <= total_bytes) {
             const bool full = o >= s && o + 16 <= e;
@@ -185,8 +186,9 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
             sum_chunk(__ldcs(vb4 + c), o, s, e, full, rel);
             rotate_add(rel, phase, cb);
         } else {  // the image's last partial chunk
-            for (long long i = (o > s ? o : s); i < e; ++i) {
-                const int ch = static_cast<int>(i % 3);
+            const long long lo = o > s ? o : s;
+            int ch = static_cast<int>(lo - s) % 3;
+            for (long long i = lo; i < e; ++i) {
                 const unsigned long long x = fa[i], y = fb[i];
                 ca[0] += ch == 0 ? x : 0ull;
                 ca[1] += ch == 1 ? x : 0ull;
@@ -194,6 +196,7 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
                 cb[0] += ch == 0 ? y : 0ull;
                 cb[1] += ch == 1 ? y : 0ull;
                 cb[2] += ch == 2 ? y : 0ull;
+                ch = ch == 2 ? 0 : ch + 1;
             }
         }
     }
