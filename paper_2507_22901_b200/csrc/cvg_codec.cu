@@ -24,12 +24,8 @@ namespace {
 // Painting, in two passes over device memory:
 //  1. copy2_kernel: frame_a = frame_b = base, a flat 16-byte copy (read once,
 //     write twice: the 9 B/pixel minimum) with four loads in flight per thread;
-//  2. fill_kernel: every block's rows.  A CTA flattens its block into
-//     (row, 16-byte chunk) items like the block sums below; a chunk inside the
-//     row segment is one 16-byte store of the color pattern (byte i of the
-//     chunk at offset 16c is channel (c + i) % 3), a chunk straddling the
-//     segment's ends is stored bytewise, so neighbouring blocks never write
-//     the same bytes.  Its stores hit the lines pass 1 just wrote (L2).
+//  2. fill_kernel: every block's row segments as coalesced 32-bit stores of
+//     the color pattern plus <= 6 unaligned edge bytes per row (below).
 // The fused alternative (one pass, a span lookup per chunk) measured slower:
 // its per-chunk lookups are dependent loads that stall the copy's stream of
 // independent loads.
@@ -45,14 +41,14 @@ __global__ void __launch_bounds__(256) copy2_kernel(const uint4* __restrict__ ba
         for (int u = 0; u < 4; ++u) v[u] = __ldcs(base + i + u * stride);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            __stcs(fa + i + u * stride, v[u]);
-            __stcs(fb + i + u * stride, v[u]);
+            fa[i + u * stride] = v[u];  // default policy: the fill pass merges into these lines in L2
+            fb[i + u * stride] = v[u];
         }
     }
     for (; i < n16; i += stride) {
         const uint4 v = __ldcs(base + i);
-        __stcs(fa + i, v);
-        __stcs(fb + i, v);
+        fa[i] = v;
+        fb[i] = v;
     }
     // the last n_bytes % 16 bytes
     const long long t = 16 * n16 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -71,54 +67,59 @@ __global__ void __launch_bounds__(256) copy2_bytes_kernel(const uint8_t* __restr
     }
 }
 
-// 16 pattern bytes of a color (r | g << 8 | b << 16) starting at channel `phase`
-__device__ __forceinline__ uint4 color_chunk(uint32_t rgb, int phase) {
-    // rot[k] = the color rotated to start at channel k, repeated: bytes c, c+1, c+2, c, ...
-    uint32_t w[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        uint32_t x = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int ch0 = (4 * q + i) % 3;  // channel at phase 0
-            const int ch = phase == 0 ? ch0 : (phase == 1 ? (ch0 + 1) % 3 : (ch0 + 2) % 3);
-            x |= ((rgb >> (8 * ch)) & 0xffu) << (8 * i);
-        }
-        w[q] = x;
-    }
-    return make_uint4(w[0], w[1], w[2], w[3]);
+// The 4-byte word of a color's repeating r,g,b pattern whose first byte is
+// channel `phase` (word w of the raster starts at channel (4w) % 3 = w % 3).
+__device__ __forceinline__ uint32_t color_word(uint32_t rgb, int phase) {
+    const uint32_t r = rgb & 0xffu, g = (rgb >> 8) & 0xffu, b = (rgb >> 16) & 0xffu;
+    const uint32_t w0 = r | g << 8 | b << 16 | r << 24;  // channels 0,1,2,0
+    const uint32_t w1 = g | b << 8 | r << 16 | g << 24;  // 1,2,0,1
+    const uint32_t w2 = b | r << 8 | g << 16 | b << 24;  // 2,0,1,2
+    return phase == 0 ? w0 : (phase == 1 ? w1 : w2);
 }
 
+// A CTA takes one block (or a slice of its rows) and flattens it into
+// (row, item) pairs: items [0, wpr) are the whole 4-byte words of the row
+// segment -- one coalesced 32-bit store per frame each --, items
+// [wpr, wpr + 6) its unaligned head and tail bytes (<= 3 each).  Every byte
+// written belongs to this block, so neighbouring blocks never race.
 __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uint8_t* __restrict__ fb, int width,
                                                    int block_w, int block_h, const int32_t* __restrict__ xy,
                                                    const uint32_t* __restrict__ plus,
-                                                   const uint32_t* __restrict__ minus, bool vec) {
+                                                   const uint32_t* __restrict__ minus) {
     const int blk = blockIdx.x;
     const int bx = __ldg(&xy[2 * blk]), by = __ldg(&xy[2 * blk + 1]);
     const uint32_t pc = __ldg(&plus[blk]), mc = __ldg(&minus[blk]);
-    const int cpr = (3 * block_w + 15) / 16 + 1;
+    const int wpr = (3 * block_w) / 4 + 1;  // whole words a row segment can hold
+    const int ipr = wpr + 6;
     const int r0 = static_cast<int>((static_cast<long long>(block_h) * blockIdx.y) / gridDim.y);
     const int r1 = static_cast<int>((static_cast<long long>(block_h) * (blockIdx.y + 1)) / gridDim.y);
-    const int items = (r1 - r0) * cpr;  // < 2^31: block_h * (3 block_w / 16 + 2)
+    const int items = (r1 - r0) * ipr;
+    uint32_t* wa = reinterpret_cast<uint32_t*>(fa);
+    uint32_t* wb = reinterpret_cast<uint32_t*>(fb);
     for (int it = threadIdx.x; it < items; it += blockDim.x) {
-        const int rr = it / cpr;
-        const int k = it - rr * cpr;
+        const int rr = it / ipr;
+        const int k = it - rr * ipr;
         const long long s = 3 * (static_cast<long long>(by + r0 + rr) * width + bx);
         const long long e = s + 3ll * block_w;
-        const long long c = (s >> 4) + k;
-        const long long o = c << 4;
-        if (o >= e) continue;
-        const int phase = static_cast<int>(((s >> 4) % 3 + k) % 3);  // c % 3
-        if (vec && o >= s && o + 16 <= e) {
-            reinterpret_cast<uint4*>(fa)[c] = color_chunk(pc, phase);
-            reinterpret_cast<uint4*>(fb)[c] = color_chunk(mc, phase);
+        long long ws = (s + 3) >> 2;
+        const long long we = e >> 2;
+        if (ws > we) ws = we;  // no whole word: all bytes go to the head
+        if (k < wpr) {
+            const long long w = ws + k;
+            if (w < we) {
+                const int phase = static_cast<int>(w % 3);
+                wa[w] = color_word(pc, phase);
+                wb[w] = color_word(mc, phase);
+            }
         } else {
-            const long long lo = o > s ? o : s, hi = o + 16 < e ? o + 16 : e;
-            int ch = static_cast<int>(lo - s) % 3;  // s is a pixel start: channel 0
-            for (long long i = lo; i < hi; ++i) {
+            const int q = k - wpr;  // 0..2 head, 3..5 tail
+            const long long h_end = ws < we ? 4 * ws : e;
+            const long long t_beg = ws < we ? 4 * we : e;
+            const long long i = q < 3 ? s + q : t_beg + (q - 3);
+            if ((q < 3 && i < h_end) || (q >= 3 && i < e)) {
+                const int ch = static_cast<int>((i - s) % 3);  // s is a pixel start
                 fa[i] = static_cast<uint8_t>(pc >> (8 * ch));
                 fb[i] = static_cast<uint8_t>(mc >> (8 * ch));
-                ch = ch == 2 ? 0 : ch + 1;
             }
         }
     }
@@ -235,13 +236,13 @@ cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int widt
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || n_blocks <= 0) return e;
-    const bool fvec = ((reinterpret_cast<uintptr_t>(fa) | reinterpret_cast<uintptr_t>(fb)) & 15) == 0;
     const long long want = (static_cast<long long>(sms) * 8 + n_blocks - 1) / n_blocks;
     long long slices = want < block_h ? want : block_h;
     if (slices < 1) slices = 1;
     if (slices > 65535) slices = 65535;
+    if ((reinterpret_cast<uintptr_t>(fa) | reinterpret_cast<uintptr_t>(fb)) & 3) return cudaErrorMisalignedAddress;
     fill_kernel<<<dim3(n_blocks, static_cast<unsigned>(slices)), 256, 0, st>>>(fa, fb, width, block_w, block_h, xy,
-                                                                               plus, minus, fvec);
+                                                                               plus, minus);
     return cudaGetLastError();
 }
 
