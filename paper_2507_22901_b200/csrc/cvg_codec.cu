@@ -77,47 +77,54 @@ __device__ __forceinline__ uint32_t color_word(uint32_t rgb, int phase) {
     return phase == 0 ? w0 : (phase == 1 ? w1 : w2);
 }
 
-// A CTA takes one block (or a slice of its rows) and flattens it into
-// (row, item) pairs: items [0, wpr) are the whole 4-byte words of the row
-// segment -- one coalesced 32-bit store per frame each --, items
-// [wpr, wpr + 6) its unaligned head and tail bytes (<= 3 each).  Every byte
-// written belongs to this block, so neighbouring blocks never race.
+// A CTA takes one block (or a slice of its rows); its threads form lane
+// groups of G (a power of two, about the words of one row segment), one
+// group per row, so narrow blocks still fill whole warps.  A group stores
+// the row segment's whole 4-byte words (coalesced 32-bit stores of the
+// pattern word of the word's phase) and its <= 3 + 3 unaligned head and tail
+// bytes.  Every byte written belongs to this block: neighbouring blocks
+// never race.  Row setup is 64-bit once per row; per-item work is 32-bit.
 __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uint8_t* __restrict__ fb, int width,
-                                                   int block_w, int block_h, const int32_t* __restrict__ xy,
-                                                   const uint32_t* __restrict__ plus,
+                                                   int block_w, int block_h, int group,
+                                                   const int32_t* __restrict__ xy, const uint32_t* __restrict__ plus,
                                                    const uint32_t* __restrict__ minus) {
     const int blk = blockIdx.x;
     const int bx = __ldg(&xy[2 * blk]), by = __ldg(&xy[2 * blk + 1]);
     const uint32_t pc = __ldg(&plus[blk]), mc = __ldg(&minus[blk]);
-    const int wpr = (3 * block_w) / 4 + 1;  // whole words a row segment can hold
-    const int ipr = wpr + 6;
+    const uint32_t pw[3] = {color_word(pc, 0), color_word(pc, 1), color_word(pc, 2)};
+    const uint32_t mw[3] = {color_word(mc, 0), color_word(mc, 1), color_word(mc, 2)};
     const int r0 = static_cast<int>((static_cast<long long>(block_h) * blockIdx.y) / gridDim.y);
     const int r1 = static_cast<int>((static_cast<long long>(block_h) * (blockIdx.y + 1)) / gridDim.y);
-    const int items = (r1 - r0) * ipr;
+    const int g = threadIdx.x / group, li = threadIdx.x - g * group, groups = blockDim.x / group;
     uint32_t* wa = reinterpret_cast<uint32_t*>(fa);
     uint32_t* wb = reinterpret_cast<uint32_t*>(fb);
-    for (int it = threadIdx.x; it < items; it += blockDim.x) {
-        const int rr = it / ipr;
-        const int k = it - rr * ipr;
-        const long long s = 3 * (static_cast<long long>(by + r0 + rr) * width + bx);
+    for (int r = r0 + g; r < r1; r += groups) {
+        const long long s = 3 * (static_cast<long long>(by + r) * width + bx);
         const long long e = s + 3ll * block_w;
         long long ws = (s + 3) >> 2;
         const long long we = e >> 2;
-        if (ws > we) ws = we;  // no whole word: all bytes go to the head
-        if (k < wpr) {
-            const long long w = ws + k;
-            if (w < we) {
-                const int phase = static_cast<int>(w % 3);
-                wa[w] = color_word(pc, phase);
-                wb[w] = color_word(mc, phase);
+        if (ws > we) ws = we;  // no whole word (1-pixel blocks): the 3 bytes are head bytes
+        const int nw = static_cast<int>(we - ws);
+        const int ph0 = static_cast<int>(ws % 3);
+        for (int k = li; k < nw; k += group) {
+            const int ph = (ph0 + k) % 3;
+            wa[ws + k] = ph == 0 ? pw[0] : (ph == 1 ? pw[1] : pw[2]);
+            wb[ws + k] = ph == 0 ? mw[0] : (ph == 1 ? mw[1] : mw[2]);
+        }
+        if (li < 6) {
+            const int nh = static_cast<int>((nw > 0 ? 4 * ws : e) - s);  // head bytes
+            const long long t_beg = nw > 0 ? 4 * we : e;
+            const int nt = static_cast<int>(e - t_beg);
+            long long i = -1;
+            int ch = 0;
+            if (li < 3 && li < nh) {
+                i = s + li;
+                ch = li;  // s starts a pixel
+            } else if (li >= 3 && li - 3 < nt) {
+                i = t_beg + (li - 3);
+                ch = static_cast<int>(t_beg - s + (li - 3)) % 3;
             }
-        } else {
-            const int q = k - wpr;  // 0..2 head, 3..5 tail
-            const long long h_end = ws < we ? 4 * ws : e;
-            const long long t_beg = ws < we ? 4 * we : e;
-            const long long i = q < 3 ? s + q : t_beg + (q - 3);
-            if ((q < 3 && i < h_end) || (q >= 3 && i < e)) {
-                const int ch = static_cast<int>((i - s) % 3);  // s is a pixel start
+            if (i >= 0) {
                 fa[i] = static_cast<uint8_t>(pc >> (8 * ch));
                 fb[i] = static_cast<uint8_t>(mc >> (8 * ch));
             }
@@ -125,9 +132,10 @@ __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uin
     }
 }
 
-// Block sums.  A CTA takes one block (or a slice of its rows) and flattens
-// it into (row, 16-byte chunk) items, so every thread issues independent
-// 16-byte loads however narrow the block is.  Byte i of the chunk starting
+// Block sums.  A CTA takes one block (or a slice of its rows); lane groups of
+// G (a power of two, about the 16-byte chunks of a row segment) take one row
+// each, so every thread issues independent 16-byte loads however narrow the
+// block is.  Byte i of the chunk starting
 // at byte offset 16c belongs to channel (c + i) % 3 (16 = 1 mod 3): bytes are
 // summed into three chunk-relative accumulators with compile-time indices and
 // rotated into r, g, b once per chunk.  Chunks that straddle the block's row
@@ -155,7 +163,8 @@ __device__ __forceinline__ void sum_chunk(uint4 v, long long o, long long s, lon
 
 __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* __restrict__ fa,
                                                                  const uint8_t* __restrict__ fb, int width,
-                                                                 int block_w, int block_h, long long total_bytes,
+                                                                 int block_w, int block_h, int group,
+                                                                 long long total_bytes,
                                                                  const int32_t* __restrict__ xy,
                                                                  unsigned long long* __restrict__ sums) {
     __shared__ unsigned long long red[6];
@@ -163,41 +172,41 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
     __syncthreads();
     const int blk = blockIdx.x;
     const int bx = __ldg(&xy[2 * blk]), by = __ldg(&xy[2 * blk + 1]);
-    const int cpr = (3 * block_w + 15) / 16 + 1;  // chunks a row segment can touch
     const int r0 = static_cast<int>((static_cast<long long>(block_h) * blockIdx.y) / gridDim.y);
     const int r1 = static_cast<int>((static_cast<long long>(block_h) * (blockIdx.y + 1)) / gridDim.y);
-    const int items = (r1 - r0) * cpr;
+    const int g = threadIdx.x / group, li = threadIdx.x - g * group, groups = kSumThreads / group;
     unsigned long long ca[3] = {0, 0, 0}, cb[3] = {0, 0, 0};
     const uint4* va4 = reinterpret_cast<const uint4*>(fa);
     const uint4* vb4 = reinterpret_cast<const uint4*>(fb);
-    for (int it = threadIdx.x; it < items; it += kSumThreads) {
-        const int rr = it / cpr;
-        const int k = it - rr * cpr;
-        const long long s = 3 * (static_cast<long long>(by + r0 + rr) * width + bx);
+    for (int r = r0 + g; r < r1; r += groups) {
+        const long long s = 3 * (static_cast<long long>(by + r) * width + bx);
         const long long e = s + 3ll * block_w;
-        const long long c = (s >> 4) + k;
-        const long long o = c << 4;
-        if (o >= e) continue;
-        const int phase = static_cast<int>(((s >> 4) % 3 + k) % 3);  // c % 3
-        uint32_t rel[3];
-        if (o + 16 <= total_bytes) {
-            const bool full = o >= s && o + 16 <= e;
-            sum_chunk(__ldcs(va4 + c), o, s, e, full, rel);
-            rotate_add(rel, phase, ca);
-            sum_chunk(__ldcs(vb4 + c), o, s, e, full, rel);
-            rotate_add(rel, phase, cb);
-        } else {  // the image's last partial chunk
-            const long long lo = o > s ? o : s;
-            int ch = static_cast<int>(lo - s) % 3;
-            for (long long i = lo; i < e; ++i) {
-                const unsigned long long x = fa[i], y = fb[i];
-                ca[0] += ch == 0 ? x : 0ull;
-                ca[1] += ch == 1 ? x : 0ull;
-                ca[2] += ch == 2 ? x : 0ull;
-                cb[0] += ch == 0 ? y : 0ull;
-                cb[1] += ch == 1 ? y : 0ull;
-                cb[2] += ch == 2 ? y : 0ull;
-                ch = ch == 2 ? 0 : ch + 1;
+        const long long c0 = s >> 4;
+        const int nc = static_cast<int>(((e + 15) >> 4) - c0);  // chunks touching [s, e)
+        const int ph0 = static_cast<int>(c0 % 3);
+        for (int k = li; k < nc; k += group) {
+            const long long c = c0 + k, o = c << 4;
+            uint32_t rel[3];
+            const int phase = (ph0 + k) % 3;  // channel of the chunk's first byte
+            if (o + 16 <= total_bytes) {
+                const bool full = o >= s && o + 16 <= e;
+                sum_chunk(__ldcs(va4 + c), o, s, e, full, rel);
+                rotate_add(rel, phase, ca);
+                sum_chunk(__ldcs(vb4 + c), o, s, e, full, rel);
+                rotate_add(rel, phase, cb);
+            } else {  // the image's last partial chunk
+                const long long lo = o > s ? o : s;
+                int ch = static_cast<int>(lo - s) % 3;
+                for (long long i = lo; i < e; ++i) {
+                    const unsigned long long x = fa[i], y = fb[i];
+                    ca[0] += ch == 0 ? x : 0ull;
+                    ca[1] += ch == 1 ? x : 0ull;
+                    ca[2] += ch == 2 ? x : 0ull;
+                    cb[0] += ch == 0 ? y : 0ull;
+                    cb[1] += ch == 1 ? y : 0ull;
+                    cb[2] += ch == 2 ? y : 0ull;
+                    ch = ch == 2 ? 0 : ch + 1;
+                }
             }
         }
     }
@@ -217,6 +226,13 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
     }
     __syncthreads();
     if (threadIdx.x < 6 && red[threadIdx.x]) atomicAdd(&sums[6 * blk + threadIdx.x], red[threadIdx.x]);
+}
+
+// Lanes per row: the power of two >= the items of a row segment, <= 32.
+int lane_group(int items) {
+    int g = 1;
+    while (g < items && g < 32) g <<= 1;
+    return g < 8 ? 8 : g;  // >= 6 lanes for the fill's edge bytes
 }
 
 }  // namespace
@@ -241,8 +257,8 @@ cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int widt
     if (slices < 1) slices = 1;
     if (slices > 65535) slices = 65535;
     if ((reinterpret_cast<uintptr_t>(fa) | reinterpret_cast<uintptr_t>(fb)) & 3) return cudaErrorMisalignedAddress;
-    fill_kernel<<<dim3(n_blocks, static_cast<unsigned>(slices)), 256, 0, st>>>(fa, fb, width, block_w, block_h, xy,
-                                                                               plus, minus);
+    fill_kernel<<<dim3(n_blocks, static_cast<unsigned>(slices)), 256, 0, st>>>(
+        fa, fb, width, block_w, block_h, lane_group((3 * block_w) / 4 + 1), xy, plus, minus);
     return cudaGetLastError();
 }
 
@@ -259,7 +275,7 @@ cudaError_t launch_block_sums(const uint8_t* fa, const uint8_t* fb, int width, i
     if (slices < 1) slices = 1;
     if (slices > 65535) slices = 65535;
     block_sums_kernel<<<dim3(n_blocks, static_cast<unsigned>(slices)), kSumThreads, 0, st>>>(
-        fa, fb, width, block_w, block_h, total_bytes, xy, sums);
+        fa, fb, width, block_w, block_h, lane_group((3 * block_w + 15) / 16 + 1), total_bytes, xy, sums);
     return cudaGetLastError();
 }
 
