@@ -83,7 +83,11 @@ __device__ __forceinline__ uint32_t color_word(uint32_t rgb, int phase) {
 // the row segment's whole 4-byte words (coalesced 32-bit stores of the
 // pattern word of the word's phase) and its <= 3 + 3 unaligned head and tail
 // bytes.  Every byte written belongs to this block: neighbouring blocks
-// never race.  Row setup is 64-bit once per row; per-item work is 32-bit.
+// never race.
+// kUniform (width % 4 == 0): a row is 3W = 0 mod 12 bytes, so every row of a
+// block has the same word alignment and phases; the geometry is set up once
+// and a row costs its stores and one address add.
+template <bool kUniform>
 __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uint8_t* __restrict__ fb, int width,
                                                    int block_w, int block_h, int group,
                                                    const int32_t* __restrict__ xy, const uint32_t* __restrict__ plus,
@@ -96,33 +100,56 @@ __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uin
     const int r0 = static_cast<int>((static_cast<long long>(block_h) * blockIdx.y) / gridDim.y);
     const int r1 = static_cast<int>((static_cast<long long>(block_h) * (blockIdx.y + 1)) / gridDim.y);
     const int g = threadIdx.x / group, li = threadIdx.x - g * group, groups = blockDim.x / group;
+    const int gmod3 = group % 3;
     uint32_t* wa = reinterpret_cast<uint32_t*>(fa);
     uint32_t* wb = reinterpret_cast<uint32_t*>(fb);
-    for (int r = r0 + g; r < r1; r += groups) {
-        const long long s = 3 * (static_cast<long long>(by + r) * width + bx);
+    // geometry of a row segment (for kUniform: of every row, relative to its start)
+    auto geometry = [&](long long s, long long& ws, int& nw, int& ph0, int& nh, long long& t_beg, int& nt) {
         const long long e = s + 3ll * block_w;
-        long long ws = (s + 3) >> 2;
+        ws = (s + 3) >> 2;
         const long long we = e >> 2;
         if (ws > we) ws = we;  // no whole word (1-pixel blocks): the 3 bytes are head bytes
-        const int nw = static_cast<int>(we - ws);
-        const int ph0 = static_cast<int>(ws % 3);
+        nw = static_cast<int>(we - ws);
+        ph0 = static_cast<int>(ws % 3);
+        nh = static_cast<int>((nw > 0 ? 4 * ws : e) - s);
+        t_beg = nw > 0 ? 4 * we : e;
+        nt = static_cast<int>(e - t_beg);
+    };
+    long long ws = 0, t_beg = 0;
+    int nw = 0, ph0 = 0, nh = 0, nt = 0, tch = 0;
+    const long long row_bytes = 3ll * width;
+    if (kUniform) {
+        const long long s0 = 3 * (static_cast<long long>(by) * width + bx);
+        geometry(s0, ws, nw, ph0, nh, t_beg, nt);
+        tch = static_cast<int>(t_beg - s0) % 3;
+    }
+    for (int r = r0 + g; r < r1; r += groups) {
+        const long long s = 3 * (static_cast<long long>(by + r) * width + bx);
+        long long wrow;
+        long long tb;
+        if (kUniform) {
+            wrow = ws + static_cast<long long>(r) * (row_bytes >> 2);
+            tb = t_beg + static_cast<long long>(r) * row_bytes;
+        } else {
+            geometry(s, wrow, nw, ph0, nh, tb, nt);
+            tch = static_cast<int>(tb - s) % 3;
+        }
+        int ph = (ph0 + li) % 3;
         for (int k = li; k < nw; k += group) {
-            const int ph = (ph0 + k) % 3;
-            wa[ws + k] = ph == 0 ? pw[0] : (ph == 1 ? pw[1] : pw[2]);
-            wb[ws + k] = ph == 0 ? mw[0] : (ph == 1 ? mw[1] : mw[2]);
+            wa[wrow + k] = ph == 0 ? pw[0] : (ph == 1 ? pw[1] : pw[2]);
+            wb[wrow + k] = ph == 0 ? mw[0] : (ph == 1 ? mw[1] : mw[2]);
+            ph += gmod3;
+            ph = ph >= 3 ? ph - 3 : ph;
         }
         if (li < 6) {
-            const int nh = static_cast<int>((nw > 0 ? 4 * ws : e) - s);  // head bytes
-            const long long t_beg = nw > 0 ? 4 * we : e;
-            const int nt = static_cast<int>(e - t_beg);
             long long i = -1;
             int ch = 0;
             if (li < 3 && li < nh) {
                 i = s + li;
                 ch = li;  // s starts a pixel
             } else if (li >= 3 && li - 3 < nt) {
-                i = t_beg + (li - 3);
-                ch = static_cast<int>(t_beg - s + (li - 3)) % 3;
+                i = tb + (li - 3);
+                ch = (tch + li - 3) % 3;
             }
             if (i >= 0) {
                 fa[i] = static_cast<uint8_t>(pc >> (8 * ch));
@@ -135,32 +162,46 @@ __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uin
 // Block sums.  A CTA takes one block (or a slice of its rows); lane groups of
 // G (a power of two, about the 16-byte chunks of a row segment) take one row
 // each, so every thread issues independent 16-byte loads however narrow the
-// block is.  Byte i of the chunk starting
-// at byte offset 16c belongs to channel (c + i) % 3 (16 = 1 mod 3): bytes are
-// summed into three chunk-relative accumulators with compile-time indices and
-// rotated into r, g, b once per chunk.  Chunks that straddle the block's row
-// segment [s, e) mask their bytes; a chunk running past the end of the image
-// is read bytewise.  Sums are exact integers.
+// block is.  A chunk's bytes are summed per channel with byte dot products
+// (dp4a against 0/1 selector words): byte i of the chunk at offset o is
+// channel o + i mod 3, and the selectors also drop bytes outside the row
+// segment.  kUniform (width % 16 == 0): every row of a block has the same
+// chunk alignment and phases, so a lane's selectors are built once.  Sums
+// are exact integers (32-bit lane partials flushed to 64 bits).
 constexpr int kSumThreads = 256;
 
-__device__ __forceinline__ void rotate_add(const uint32_t (&rel)[3], int phase, unsigned long long (&ch)[3]) {
-    ch[0] += phase == 0 ? rel[0] : (phase == 1 ? rel[2] : rel[1]);
-    ch[1] += phase == 0 ? rel[1] : (phase == 1 ? rel[0] : rel[2]);
-    ch[2] += phase == 0 ? rel[2] : (phase == 1 ? rel[1] : rel[0]);
-}
-
-__device__ __forceinline__ void sum_chunk(uint4 v, long long o, long long s, long long e, bool full,
-                                          uint32_t (&rel)[3]) {
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-    rel[0] = rel[1] = rel[2] = 0;
+// selector words of one chunk: sel[q][c] has 0x01 in the bytes of word q that
+// belong to channel c and lie in [s, e)
+__device__ __forceinline__ void chunk_selectors(long long o, long long s, long long e, uint32_t (&sel)[4][3]) {
+    const int ph = static_cast<int>(((o % 3) + 3) % 3);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        uint32_t byte = (w[i >> 2] >> (8 * (i & 3))) & 0xffu;
-        if (!full) byte = (o + i >= s && o + i < e) ? byte : 0u;
-        rel[i % 3] += byte;
+    for (int q = 0; q < 4; ++q) {
+        uint32_t m[3] = {0, 0, 0};
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const long long x = o + 4 * q + b;
+            const int ch = (ph + 4 * q + b) % 3;
+            const uint32_t bit = (x >= s && x < e) ? (1u << (8 * b)) : 0u;
+            m[0] |= ch == 0 ? bit : 0u;
+            m[1] |= ch == 1 ? bit : 0u;
+            m[2] |= ch == 2 ? bit : 0u;
+        }
+        sel[q][0] = m[0];
+        sel[q][1] = m[1];
+        sel[q][2] = m[2];
     }
 }
 
+__device__ __forceinline__ void dot_chunk(uint4 v, const uint32_t (&sel)[4][3], uint32_t (&acc)[3]) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c] = __dp4a(w[q], sel[q][c], acc[c]);
+    }
+}
+
+template <bool kUniform>
 __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* __restrict__ fa,
                                                                  const uint8_t* __restrict__ fb, int width,
                                                                  int block_w, int block_h, int group,
@@ -176,24 +217,44 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
     const int r1 = static_cast<int>((static_cast<long long>(block_h) * (blockIdx.y + 1)) / gridDim.y);
     const int g = threadIdx.x / group, li = threadIdx.x - g * group, groups = kSumThreads / group;
     unsigned long long ca[3] = {0, 0, 0}, cb[3] = {0, 0, 0};
+    uint32_t pa[3] = {0, 0, 0}, pb[3] = {0, 0, 0};
+    int pending = 0;
     const uint4* va4 = reinterpret_cast<const uint4*>(fa);
     const uint4* vb4 = reinterpret_cast<const uint4*>(fb);
+    const long long row_bytes = 3ll * width;
+    const long long s0 = 3 * (static_cast<long long>(by) * width + bx);
+    const int nc0 = static_cast<int>(((s0 + 3ll * block_w + 15) >> 4) - (s0 >> 4));
+    uint32_t sel0[4][3];
+    if (kUniform && li < nc0) chunk_selectors(((s0 >> 4) + li) << 4, s0, s0 + 3ll * block_w, sel0);
     for (int r = r0 + g; r < r1; r += groups) {
-        const long long s = 3 * (static_cast<long long>(by + r) * width + bx);
+        const long long s = s0 + static_cast<long long>(r) * row_bytes;
         const long long e = s + 3ll * block_w;
         const long long c0 = s >> 4;
-        const int nc = static_cast<int>(((e + 15) >> 4) - c0);  // chunks touching [s, e)
-        const int ph0 = static_cast<int>(c0 % 3);
+        const int nc = static_cast<int>(((e + 15) >> 4) - c0);
         for (int k = li; k < nc; k += group) {
             const long long c = c0 + k, o = c << 4;
-            uint32_t rel[3];
-            const int phase = (ph0 + k) % 3;  // channel of the chunk's first byte
             if (o + 16 <= total_bytes) {
-                const bool full = o >= s && o + 16 <= e;
-                sum_chunk(__ldcs(va4 + c), o, s, e, full, rel);
-                rotate_add(rel, phase, ca);
-                sum_chunk(__ldcs(vb4 + c), o, s, e, full, rel);
-                rotate_add(rel, phase, cb);
+                uint32_t sel[4][3];
+                if (kUniform && k == li) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                        for (int x = 0; x < 3; ++x) sel[q][x] = sel0[q][x];
+                    }
+                } else {
+                    chunk_selectors(o, s, e, sel);
+                }
+                dot_chunk(__ldcs(va4 + c), sel, pa);
+                dot_chunk(__ldcs(vb4 + c), sel, pb);
+                if (++pending == 65536) {  // 65536 chunks x 16 x 255 < 2^32
+#pragma unroll
+                    for (int x = 0; x < 3; ++x) {
+                        ca[x] += pa[x];
+                        cb[x] += pb[x];
+                        pa[x] = pb[x] = 0;
+                    }
+                    pending = 0;
+                }
             } else {  // the image's last partial chunk
                 const long long lo = o > s ? o : s;
                 int ch = static_cast<int>(lo - s) % 3;
@@ -209,6 +270,11 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
                 }
             }
         }
+    }
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+        ca[x] += pa[x];
+        cb[x] += pb[x];
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -257,8 +323,14 @@ cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int widt
     if (slices < 1) slices = 1;
     if (slices > 65535) slices = 65535;
     if ((reinterpret_cast<uintptr_t>(fa) | reinterpret_cast<uintptr_t>(fb)) & 3) return cudaErrorMisalignedAddress;
-    fill_kernel<<<dim3(n_blocks, static_cast<unsigned>(slices)), 256, 0, st>>>(
-        fa, fb, width, block_w, block_h, lane_group((3 * block_w) / 4 + 1), xy, plus, minus);
+    const int grp = lane_group((3 * block_w) / 4 + 1);
+    if (width % 4 == 0) {
+        fill_kernel<true><<<dim3(n_blocks, static_cast<unsigned>(slices)), 256, 0, st>>>(fa, fb, width, block_w,
+                                                                                         block_h, grp, xy, plus, minus);
+    } else {
+        fill_kernel<false><<<dim3(n_blocks, static_cast<unsigned>(slices)), 256, 0, st>>>(fa, fb, width, block_w,
+                                                                                          block_h, grp, xy, plus, minus);
+    }
     return cudaGetLastError();
 }
 
@@ -274,8 +346,15 @@ cudaError_t launch_block_sums(const uint8_t* fa, const uint8_t* fb, int width, i
     long long slices = want < block_h ? want : block_h;
     if (slices < 1) slices = 1;
     if (slices > 65535) slices = 65535;
-    block_sums_kernel<<<dim3(n_blocks, static_cast<unsigned>(slices)), kSumThreads, 0, st>>>(
-        fa, fb, width, block_w, block_h, lane_group((3 * block_w + 15) / 16 + 1), total_bytes, xy, sums);
+    const int grp = lane_group((3 * block_w + 15) / 16 + 1);
+    const dim3 grid(n_blocks, static_cast<unsigned>(slices));
+    if (width % 16 == 0) {
+        block_sums_kernel<true><<<grid, kSumThreads, 0, st>>>(fa, fb, width, block_w, block_h, grp, total_bytes, xy,
+                                                               sums);
+    } else {
+        block_sums_kernel<false><<<grid, kSumThreads, 0, st>>>(fa, fb, width, block_w, block_h, grp, total_bytes, xy,
+                                                                sums);
+    }
     return cudaGetLastError();
 }
 

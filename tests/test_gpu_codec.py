@@ -144,10 +144,12 @@ FEASIBLE = [((170, 170, 170), "101"), ((240, 240, 240), "001"), ((100, 100, 240)
 
 
 @pytest.mark.parametrize("w,h,bw,bh,n,seed", [(64, 48, 8, 8, 12, 1), (61, 37, 5, 7, 10, 2), (130, 66, 13, 3, 40, 3),
-                                               (33, 20, 33, 20, 1, 4), (256, 128, 1, 1, 300, 5)])
+                                               (33, 20, 33, 20, 1, 4), (256, 128, 1, 1, 300, 5),
+                                               (100, 40, 9, 5, 20, 6), (96, 64, 2, 17, 30, 7)])
 def test_embed_decode_match_reference(cv, ctx, ref_codec, w, h, bw, bh, n, seed):
-    """Random base images and layouts (odd widths -> the per-pixel kernel,
-    unaligned block x, 1x1 blocks, a full-image block)."""
+    """Random base images and layouts: widths with 3W mod 16 / mod 12 != 0
+    (the per-row geometry paths), unaligned block x, 1x1 and 2-pixel-wide
+    blocks, a full-image block."""
     rng = np.random.default_rng(seed)
     base = rng.integers(0, 256, (h, w, 3)).astype(np.uint8)
     xy = random_layout(rng, w, h, bw, bh, n)
