@@ -82,7 +82,7 @@ __device__ __forceinline__ uint32_t color_word(uint32_t rgb, int phase) {
 // group per row, so narrow blocks still fill whole warps.  A group stores
 // the row segment's whole 4-byte words (coalesced 32-bit stores of the
 // pattern word of the word's phase) and its <= 3 + 3 unaligned head and tail
-// bytes.  Every byte written belongs to this block: neighbouring blocks
+// bytes (a segment holding no whole word has <= 6 bytes, all written as head).  Every byte written belongs to this block: neighbouring blocks
 // never race.
 // kUniform (width % 4 == 0): a row is 3W = 0 mod 12 bytes, so every row of a
 // block has the same word alignment and phases; the geometry is set up once
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uin
         const long long e = s + 3ll * block_w;
         ws = (s + 3) >> 2;
         const long long we = e >> 2;
-        if (ws > we) ws = we;  // no whole word (1-pixel blocks): the 3 bytes are head bytes
+        if (ws > we) ws = we;  // no whole word (segments of <= 6 bytes): every byte is a head byte
         nw = static_cast<int>(we - ws);
         ph0 = static_cast<int>(ws % 3);
         nh = static_cast<int>((nw > 0 ? 4 * ws : e) - s);
@@ -144,7 +144,12 @@ __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uin
         if (li < 6) {
             long long i = -1;
             int ch = 0;
-            if (li < 3 && li < nh) {
+            if (nw == 0) {  // no whole word: <= 6 bytes (3 + 3 around a word boundary), all "head"
+                if (li < nh) {
+                    i = s + li;
+                    ch = li % 3;
+                }
+            } else if (li < 3 && li < nh) {
                 i = s + li;
                 ch = li;  // s starts a pixel
             } else if (li >= 3 && li - 3 < nt) {
