@@ -89,7 +89,7 @@ __device__ __forceinline__ uint32_t color_word(uint32_t rgb, int phase) {
 // and a row costs its stores and one address add.
 template <bool kUniform>
 __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uint8_t* __restrict__ fb, int width,
-                                                   int block_w, int block_h, int group,
+                                                   int block_w, int block_h, int rows_per_slice, int log2_group,
                                                    const int32_t* __restrict__ xy, const uint32_t* __restrict__ plus,
                                                    const uint32_t* __restrict__ minus) {
     const int blk = blockIdx.x;
@@ -97,9 +97,10 @@ __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uin
     const uint32_t pc = __ldg(&plus[blk]), mc = __ldg(&minus[blk]);
     const uint32_t pw[3] = {color_word(pc, 0), color_word(pc, 1), color_word(pc, 2)};
     const uint32_t mw[3] = {color_word(mc, 0), color_word(mc, 1), color_word(mc, 2)};
-    const int r0 = static_cast<int>((static_cast<long long>(block_h) * blockIdx.y) / gridDim.y);
-    const int r1 = static_cast<int>((static_cast<long long>(block_h) * (blockIdx.y + 1)) / gridDim.y);
-    const int g = threadIdx.x / group, li = threadIdx.x - g * group, groups = blockDim.x / group;
+    const int r0 = static_cast<int>(blockIdx.y) * rows_per_slice;
+    const int r1 = min(r0 + rows_per_slice, block_h);
+    const int group = 1 << log2_group;
+    const int g = threadIdx.x >> log2_group, li = threadIdx.x & (group - 1), groups = blockDim.x >> log2_group;
     const int gmod3 = group % 3;
     uint32_t* wa = reinterpret_cast<uint32_t*>(fa);
     uint32_t* wb = reinterpret_cast<uint32_t*>(fb);
@@ -209,8 +210,8 @@ __device__ __forceinline__ void dot_chunk(uint4 v, const uint32_t (&sel)[4][3], 
 template <bool kUniform>
 __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* __restrict__ fa,
                                                                  const uint8_t* __restrict__ fb, int width,
-                                                                 int block_w, int block_h, int group,
-                                                                 long long total_bytes,
+                                                                 int block_w, int block_h, int rows_per_slice,
+                                                                 int log2_group, long long total_bytes,
                                                                  const int32_t* __restrict__ xy,
                                                                  unsigned long long* __restrict__ sums) {
     __shared__ unsigned long long red[6];
@@ -218,9 +219,10 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
     __syncthreads();
     const int blk = blockIdx.x;
     const int bx = __ldg(&xy[2 * blk]), by = __ldg(&xy[2 * blk + 1]);
-    const int r0 = static_cast<int>((static_cast<long long>(block_h) * blockIdx.y) / gridDim.y);
-    const int r1 = static_cast<int>((static_cast<long long>(block_h) * (blockIdx.y + 1)) / gridDim.y);
-    const int g = threadIdx.x / group, li = threadIdx.x - g * group, groups = kSumThreads / group;
+    const int r0 = static_cast<int>(blockIdx.y) * rows_per_slice;
+    const int r1 = min(r0 + rows_per_slice, block_h);
+    const int group = 1 << log2_group;
+    const int g = threadIdx.x >> log2_group, li = threadIdx.x & (group - 1), groups = kSumThreads >> log2_group;
     unsigned long long ca[3] = {0, 0, 0}, cb[3] = {0, 0, 0};
     uint32_t pa[3] = {0, 0, 0}, pb[3] = {0, 0, 0};
     int pending = 0;
@@ -299,11 +301,23 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
     if (threadIdx.x < 6 && red[threadIdx.x]) atomicAdd(&sums[6 * blk + threadIdx.x], red[threadIdx.x]);
 }
 
-// Lanes per row: the power of two >= the items of a row segment, <= 32.
-int lane_group(int items) {
-    int g = 1;
-    while (g < items && g < 32) g <<= 1;
-    return g < 8 ? 8 : g;  // >= 6 lanes for the fill's edge bytes
+// log2 of the lanes per row: the power of two >= the items of a row
+// segment, in [8, 32] (>= 6 lanes for the fill's edge bytes).
+int lane_group_log2(int items) {
+    int l = 3;
+    while ((1 << l) < items && l < 5) ++l;
+    return l;
+}
+
+// Row slices of a block so that ~8 CTAs per SM are in flight in total.
+int rows_per_slice(int n_blocks, int block_h, int sms, unsigned* slices_out) {
+    const long long want = (static_cast<long long>(sms) * 8 + n_blocks - 1) / n_blocks;
+    long long slices = want < block_h ? want : block_h;
+    if (slices < 1) slices = 1;
+    if (slices > 65535) slices = 65535;
+    const int rps = static_cast<int>((block_h + slices - 1) / slices);
+    *slices_out = static_cast<unsigned>((block_h + rps - 1) / rps);
+    return rps;
 }
 
 }  // namespace
@@ -323,18 +337,15 @@ cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int widt
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || n_blocks <= 0) return e;
-    const long long want = (static_cast<long long>(sms) * 8 + n_blocks - 1) / n_blocks;
-    long long slices = want < block_h ? want : block_h;
-    if (slices < 1) slices = 1;
-    if (slices > 65535) slices = 65535;
+    unsigned slices = 1;
+    const int rps = rows_per_slice(n_blocks, block_h, sms, &slices);
     if ((reinterpret_cast<uintptr_t>(fa) | reinterpret_cast<uintptr_t>(fb)) & 3) return cudaErrorMisalignedAddress;
-    const int grp = lane_group((3 * block_w) / 4 + 1);
+    const int lg = lane_group_log2((3 * block_w) / 4 + 1);
+    const dim3 grid2(n_blocks, slices);
     if (width % 4 == 0) {
-        fill_kernel<true><<<dim3(n_blocks, static_cast<unsigned>(slices)), 256, 0, st>>>(fa, fb, width, block_w,
-                                                                                         block_h, grp, xy, plus, minus);
+        fill_kernel<true><<<grid2, 256, 0, st>>>(fa, fb, width, block_w, block_h, rps, lg, xy, plus, minus);
     } else {
-        fill_kernel<false><<<dim3(n_blocks, static_cast<unsigned>(slices)), 256, 0, st>>>(fa, fb, width, block_w,
-                                                                                          block_h, grp, xy, plus, minus);
+        fill_kernel<false><<<grid2, 256, 0, st>>>(fa, fb, width, block_w, block_h, rps, lg, xy, plus, minus);
     }
     return cudaGetLastError();
 }
@@ -346,19 +357,16 @@ cudaError_t launch_block_sums(const uint8_t* fa, const uint8_t* fb, int width, i
     if ((reinterpret_cast<uintptr_t>(fa) | reinterpret_cast<uintptr_t>(fb)) & 15) return cudaErrorMisalignedAddress;
     cudaError_t e = cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * 6 * static_cast<size_t>(n_blocks), st);
     if (e != cudaSuccess) return e;
-    // row slices so that ~8 CTAs per SM are in flight in total
-    const long long want = (static_cast<long long>(sms) * 8 + n_blocks - 1) / n_blocks;
-    long long slices = want < block_h ? want : block_h;
-    if (slices < 1) slices = 1;
-    if (slices > 65535) slices = 65535;
-    const int grp = lane_group((3 * block_w + 15) / 16 + 1);
-    const dim3 grid(n_blocks, static_cast<unsigned>(slices));
+    unsigned slices = 1;
+    const int rps = rows_per_slice(n_blocks, block_h, sms, &slices);
+    const int lg = lane_group_log2((3 * block_w + 15) / 16 + 1);
+    const dim3 grid(n_blocks, slices);
     if (width % 16 == 0) {
-        block_sums_kernel<true><<<grid, kSumThreads, 0, st>>>(fa, fb, width, block_w, block_h, grp, total_bytes, xy,
+        block_sums_kernel<true><<<grid, kSumThreads, 0, st>>>(fa, fb, width, block_w, block_h, rps, lg, total_bytes, xy,
                                                                sums);
     } else {
-        block_sums_kernel<false><<<grid, kSumThreads, 0, st>>>(fa, fb, width, block_w, block_h, grp, total_bytes, xy,
-                                                                sums);
+        block_sums_kernel<false><<<grid, kSumThreads, 0, st>>>(fa, fb, width, block_w, block_h, rps, lg, total_bytes,
+                                                                xy, sums);
     }
     return cudaGetLastError();
 }
