@@ -21,6 +21,8 @@
 namespace cvg {
 namespace {
 
+constexpr int kBlockThreads = 256;  // 8 warps; the fill and the block sums run one task per warp
+
 // Painting, in two passes over device memory:
 //  1. copy2_kernel: frame_a = frame_b = base, a flat 16-byte copy (read once,
 //     write twice: the 9 B/pixel minimum) with four loads in flight per thread;
@@ -77,7 +79,7 @@ __device__ __forceinline__ uint32_t color_word(uint32_t rgb, int phase) {
     return phase == 0 ? w0 : (phase == 1 ? w1 : w2);
 }
 
-// A CTA takes one block (or a slice of its rows); its threads form lane
+// A warp takes one block (or a slice of its rows); its lanes form
 // groups of G (a power of two, about the words of one row segment), one
 // group per row, so narrow blocks still fill whole warps.  A group stores
 // the row segment's whole 4-byte words (coalesced 32-bit stores of the
@@ -89,18 +91,21 @@ __device__ __forceinline__ uint32_t color_word(uint32_t rgb, int phase) {
 // and a row costs its stores and one address add.
 template <bool kUniform>
 __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uint8_t* __restrict__ fb, int width,
-                                                   int block_w, int block_h, int rows_per_slice, int log2_group,
-                                                   const int32_t* __restrict__ xy, const uint32_t* __restrict__ plus,
+                                                   int block_w, int block_h, int slices, int rows_per_slice,
+                                                   int log2_group, int n_tasks, const int32_t* __restrict__ xy,
+                                                   const uint32_t* __restrict__ plus,
                                                    const uint32_t* __restrict__ minus) {
-    const int blk = blockIdx.x;
+    const int task = static_cast<int>(blockIdx.x) * (kBlockThreads / 32) + static_cast<int>(threadIdx.x >> 5);
+    if (task >= n_tasks) return;
+    const int blk = task / slices, slice = task - blk * slices;
     const int bx = __ldg(&xy[2 * blk]), by = __ldg(&xy[2 * blk + 1]);
     const uint32_t pc = __ldg(&plus[blk]), mc = __ldg(&minus[blk]);
     const uint32_t pw[3] = {color_word(pc, 0), color_word(pc, 1), color_word(pc, 2)};
     const uint32_t mw[3] = {color_word(mc, 0), color_word(mc, 1), color_word(mc, 2)};
-    const int r0 = static_cast<int>(blockIdx.y) * rows_per_slice;
+    const int r0 = slice * rows_per_slice;
     const int r1 = min(r0 + rows_per_slice, block_h);
-    const int group = 1 << log2_group;
-    const int g = threadIdx.x >> log2_group, li = threadIdx.x & (group - 1), groups = blockDim.x >> log2_group;
+    const int group = 1 << log2_group, lane = threadIdx.x & 31;
+    const int g = lane >> log2_group, li = lane & (group - 1), groups = 32 >> log2_group;
     const int gmod3 = group % 3;
     uint32_t* wa = reinterpret_cast<uint32_t*>(fa);
     uint32_t* wb = reinterpret_cast<uint32_t*>(fb);
@@ -165,7 +170,7 @@ __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uin
     }
 }
 
-// Block sums.  A CTA takes one block (or a slice of its rows); lane groups of
+// Block sums.  A warp takes one block (or a slice of its rows); lane groups of
 // G (a power of two, about the 16-byte chunks of a row segment) take one row
 // each, so every thread issues independent 16-byte loads however narrow the
 // block is.  A chunk's bytes are summed per channel with byte dot products
@@ -174,7 +179,7 @@ __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uin
 // segment.  kUniform (width % 16 == 0): every row of a block has the same
 // chunk alignment and phases, so a lane's selectors are built once.  Sums
 // are exact integers (32-bit lane partials flushed to 64 bits).
-constexpr int kSumThreads = 256;
+constexpr int kSumThreads = kBlockThreads;
 
 // selector words of one chunk: sel[q][c] has 0x01 in the bytes of word q that
 // belong to channel c and lie in [s, e)
@@ -210,19 +215,19 @@ __device__ __forceinline__ void dot_chunk(uint4 v, const uint32_t (&sel)[4][3], 
 template <bool kUniform>
 __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* __restrict__ fa,
                                                                  const uint8_t* __restrict__ fb, int width,
-                                                                 int block_w, int block_h, int rows_per_slice,
-                                                                 int log2_group, long long total_bytes,
+                                                                 int block_w, int block_h, int slices,
+                                                                 int rows_per_slice, int log2_group, int n_tasks,
+                                                                 long long total_bytes,
                                                                  const int32_t* __restrict__ xy,
                                                                  unsigned long long* __restrict__ sums) {
-    __shared__ unsigned long long red[6];
-    if (threadIdx.x < 6) red[threadIdx.x] = 0;
-    __syncthreads();
-    const int blk = blockIdx.x;
+    const int task = static_cast<int>(blockIdx.x) * (kSumThreads / 32) + static_cast<int>(threadIdx.x >> 5);
+    if (task >= n_tasks) return;
+    const int blk = task / slices, slice = task - blk * slices;
     const int bx = __ldg(&xy[2 * blk]), by = __ldg(&xy[2 * blk + 1]);
-    const int r0 = static_cast<int>(blockIdx.y) * rows_per_slice;
+    const int r0 = slice * rows_per_slice;
     const int r1 = min(r0 + rows_per_slice, block_h);
-    const int group = 1 << log2_group;
-    const int g = threadIdx.x >> log2_group, li = threadIdx.x & (group - 1), groups = kSumThreads >> log2_group;
+    const int group = 1 << log2_group, lane = threadIdx.x & 31;
+    const int g = lane >> log2_group, li = lane & (group - 1), groups = 32 >> log2_group;
     unsigned long long ca[3] = {0, 0, 0}, cb[3] = {0, 0, 0};
     uint32_t pa[3] = {0, 0, 0}, pb[3] = {0, 0, 0};
     int pending = 0;
@@ -290,15 +295,13 @@ __global__ void __launch_bounds__(kSumThreads) block_sums_kernel(const uint8_t* 
             cb[c] += __shfl_xor_sync(0xffffffffu, cb[c], o);
         }
     }
-    if ((threadIdx.x & 31) == 0) {
+    if (lane == 0) {  // one atomic per warp task and channel
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            if (ca[c]) atomicAdd(&red[c], ca[c]);
-            if (cb[c]) atomicAdd(&red[3 + c], cb[c]);
+            if (ca[c]) atomicAdd(&sums[6 * blk + c], ca[c]);
+            if (cb[c]) atomicAdd(&sums[6 * blk + 3 + c], cb[c]);
         }
     }
-    __syncthreads();
-    if (threadIdx.x < 6 && red[threadIdx.x]) atomicAdd(&sums[6 * blk + threadIdx.x], red[threadIdx.x]);
 }
 
 // log2 of the lanes per row: the power of two >= the items of a row
@@ -309,12 +312,12 @@ int lane_group_log2(int items) {
     return l;
 }
 
-// Row slices of a block so that ~8 CTAs per SM are in flight in total.
+// Row slices of a block (one warp task each) so that >= 16 warps per SM are
+// in flight in total.
 int rows_per_slice(int n_blocks, int block_h, int sms, unsigned* slices_out) {
-    const long long want = (static_cast<long long>(sms) * 8 + n_blocks - 1) / n_blocks;
+    const long long want = (static_cast<long long>(sms) * 16 + n_blocks - 1) / n_blocks;
     long long slices = want < block_h ? want : block_h;
     if (slices < 1) slices = 1;
-    if (slices > 65535) slices = 65535;
     const int rps = static_cast<int>((block_h + slices - 1) / slices);
     *slices_out = static_cast<unsigned>((block_h + rps - 1) / rps);
     return rps;
@@ -341,11 +344,16 @@ cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int widt
     const int rps = rows_per_slice(n_blocks, block_h, sms, &slices);
     if ((reinterpret_cast<uintptr_t>(fa) | reinterpret_cast<uintptr_t>(fb)) & 3) return cudaErrorMisalignedAddress;
     const int lg = lane_group_log2((3 * block_w) / 4 + 1);
-    const dim3 grid2(n_blocks, slices);
+    const long long tasks = static_cast<long long>(n_blocks) * slices;
+    if (tasks > (1ll << 31) - 1) return cudaErrorInvalidConfiguration;
+    const int nt = static_cast<int>(tasks);
+    const unsigned grid2 = static_cast<unsigned>((tasks + 7) / 8);
     if (width % 4 == 0) {
-        fill_kernel<true><<<grid2, 256, 0, st>>>(fa, fb, width, block_w, block_h, rps, lg, xy, plus, minus);
+        fill_kernel<true><<<grid2, kBlockThreads, 0, st>>>(fa, fb, width, block_w, block_h, static_cast<int>(slices),
+                                                           rps, lg, nt, xy, plus, minus);
     } else {
-        fill_kernel<false><<<grid2, 256, 0, st>>>(fa, fb, width, block_w, block_h, rps, lg, xy, plus, minus);
+        fill_kernel<false><<<grid2, kBlockThreads, 0, st>>>(fa, fb, width, block_w, block_h, static_cast<int>(slices),
+                                                            rps, lg, nt, xy, plus, minus);
     }
     return cudaGetLastError();
 }
@@ -360,13 +368,17 @@ cudaError_t launch_block_sums(const uint8_t* fa, const uint8_t* fb, int width, i
     unsigned slices = 1;
     const int rps = rows_per_slice(n_blocks, block_h, sms, &slices);
     const int lg = lane_group_log2((3 * block_w + 15) / 16 + 1);
-    const dim3 grid(n_blocks, slices);
+    const long long tasks = static_cast<long long>(n_blocks) * slices;
+    if (tasks > (1ll << 31) - 1) return cudaErrorInvalidConfiguration;
+    const int nt = static_cast<int>(tasks);
+    const unsigned grid = static_cast<unsigned>((tasks + 7) / 8);
     if (width % 16 == 0) {
-        block_sums_kernel<true><<<grid, kSumThreads, 0, st>>>(fa, fb, width, block_w, block_h, rps, lg, total_bytes, xy,
-                                                               sums);
+        block_sums_kernel<true><<<grid, kSumThreads, 0, st>>>(fa, fb, width, block_w, block_h, static_cast<int>(slices),
+                                                               rps, lg, nt, total_bytes, xy, sums);
     } else {
-        block_sums_kernel<false><<<grid, kSumThreads, 0, st>>>(fa, fb, width, block_w, block_h, rps, lg, total_bytes,
-                                                                xy, sums);
+        block_sums_kernel<false><<<grid, kSumThreads, 0, st>>>(fa, fb, width, block_w, block_h,
+                                                                static_cast<int>(slices), rps, lg, nt, total_bytes, xy,
+                                                                sums);
     }
     return cudaGetLastError();
 }
