@@ -1976,6 +1976,8 @@ struct cvg_layout {
     size_t o_xy = 0, o_pl = 0, o_mi = 0;
     cudaEvent_t done = nullptr;
     bool pending = false;
+    std::vector<uint32_t> colors;  // packed colors the device holds (plus then minus)
+    bool colors_valid = false;
 };
 
 namespace {
@@ -2004,8 +2006,9 @@ int layout_prepare(cvg_layout* L, int32_t width, int32_t height, int32_t bw, int
     if (int e = layout_spans(width, height, bw, bh, n, xy, t)) return e;
     std::vector<unsigned char> blob;  // the span table only validates; the kernels take positions
     L->o_xy = blob_put(blob, xy, 2 * static_cast<size_t>(n));
-    L->o_pl = (blob.size() + 255) & ~size_t(255);  // colors: written by each paint
-    L->o_mi = L->o_pl + ((4 * static_cast<size_t>(n) + 255) & ~size_t(255));
+    L->o_pl = (blob.size() + 255) & ~size_t(255);  // colors: plus then minus, written by the paints
+    L->o_mi = L->o_pl + 4 * static_cast<size_t>(n);
+    L->colors_valid = false;
     const size_t total = L->o_mi + 4 * static_cast<size_t>(n);
     if (int e = layout_reserve(L, total, st)) return e;
     CVG_CUDA(cudaMemcpyAsync(L->d, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
@@ -2017,18 +2020,23 @@ int layout_prepare(cvg_layout* L, int32_t width, int32_t height, int32_t bw, int
     return CVG_OK;
 }
 
+// Packs the block colors and uploads them (one copy; plus then minus are
+// adjacent) unless they equal what the device already holds -- a codec
+// stream paints the same message frame after frame.
 int layout_colors(cvg_layout* L, const uint8_t* plus, const uint8_t* minus, cudaStream_t st) {
     if (L->n == 0) return CVG_OK;
     if (!plus || !minus) return fail(CVG_EINVAL, "block colors missing");
-    std::vector<uint32_t> w(2 * static_cast<size_t>(L->n));
-    for (int32_t i = 0; i < L->n; ++i) {
+    const size_t n = static_cast<size_t>(L->n);
+    std::vector<uint32_t> w(2 * n);
+    for (size_t i = 0; i < n; ++i) {
         w[i] = plus[3 * i] | (uint32_t(plus[3 * i + 1]) << 8) | (uint32_t(plus[3 * i + 2]) << 16);
-        w[L->n + i] = minus[3 * i] | (uint32_t(minus[3 * i + 1]) << 8) | (uint32_t(minus[3 * i + 2]) << 16);
+        w[n + i] = minus[3 * i] | (uint32_t(minus[3 * i + 1]) << 8) | (uint32_t(minus[3 * i + 2]) << 16);
     }
+    if (L->colors_valid && L->colors == w) return CVG_OK;
     if (L->pending) CVG_CUDA(cudaStreamWaitEvent(st, L->done, 0));
-    CVG_CUDA(cudaMemcpyAsync(L->d + L->o_pl, w.data(), 4 * static_cast<size_t>(L->n), cudaMemcpyHostToDevice, st));
-    CVG_CUDA(cudaMemcpyAsync(L->d + L->o_mi, w.data() + L->n, 4 * static_cast<size_t>(L->n), cudaMemcpyHostToDevice,
-                             st));
+    CVG_CUDA(cudaMemcpyAsync(L->d + L->o_pl, w.data(), 8 * n, cudaMemcpyHostToDevice, st));
+    L->colors.swap(w);
+    L->colors_valid = true;
     return CVG_OK;
 }
 

@@ -258,3 +258,29 @@ def test_host_passes_full_image_block(cv, ctx):
     assert (a == [1, 2, 3]).all() and (b == [250, 251, 252]).all()
     sums = cv.block_sums_host(ctx, base, base[::-1].copy(), 1918, 1080, xy)
     assert np.array_equal(sums, CO.block_sums(base, base[::-1].copy(), 1918, 1080, xy))
+
+
+def test_prepared_layout_repaints_and_sums(cv, ctx):
+    """A prepared Layout reused with new colors, then the same colors again
+    (the upload is skipped), and its block sums, against the NumPy oracle."""
+    import torch
+
+    rng = np.random.default_rng(23)
+    h, w, bw, bh = 120, 200, 12, 7
+    base = rng.integers(0, 256, (h, w, 3)).astype(np.uint8)
+    xy = np.array(random_layout(rng, w, h, bw, bh, 40), np.int32)
+    lay = cv.Layout(ctx, w, h, bw, bh, xy)
+    d_base = torch.from_numpy(base).cuda()
+    d_a, d_b = torch.empty_like(d_base), torch.empty_like(d_base)
+    d_sums = torch.zeros((len(xy), 6), dtype=torch.int64, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    for colors_seed in (1, 2, 2, 3):
+        crng = np.random.default_rng(colors_seed)
+        plus = crng.integers(0, 256, (len(xy), 3)).astype(np.uint8)
+        minus = crng.integers(0, 256, (len(xy), 3)).astype(np.uint8)
+        lay.paint_device(d_base.data_ptr(), d_a.data_ptr(), d_b.data_ptr(), plus, minus, st)
+        lay.block_sums_device(d_a.data_ptr(), d_b.data_ptr(), d_sums.data_ptr(), st)
+        torch.cuda.synchronize()
+        oa, ob = CO.paint(base, bw, bh, xy, plus, minus)
+        assert np.array_equal(d_a.cpu().numpy(), oa) and np.array_equal(d_b.cpu().numpy(), ob)
+        assert np.array_equal(d_sums.cpu().numpy().astype(np.uint64), CO.block_sums(oa, ob, bw, bh, xy))
