@@ -592,11 +592,18 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
 
     uint32_t t_claim = 0;
     if (lane == 0) t_claim = atomicAdd(&A.ticket[0], 1u);
-    uint32_t t = __shfl_sync(kFull, t_claim, 0);
-    while (t < A.n_tiles) {
+    uint32_t c = __shfl_sync(kFull, t_claim, 0);
+    while (c < A.n_tiles) {
         if (lane == 0) t_claim = atomicAdd(&A.ticket[0], 1u);  // next tile, consumed at the end
-        const uint32_t s = t / A.tiles_per_search;
-        const uint32_t lt = t - s * A.tiles_per_search;
+        // Claim order: outermost radius tiles of every search first, the
+        // innermost last.  Outer rows are the costly ones (they reach the
+        // linear branch of f^-1 and need more repairs), so the last round of
+        // claims -- the tail where warps run out of work -- is the cheapest.
+        // Tile t (search s, tile lt) keeps its storage slot s * tps + lt.
+        const uint32_t q = c / static_cast<uint32_t>(A.n_searches);
+        const uint32_t s = c - q * static_cast<uint32_t>(A.n_searches);
+        const uint32_t lt = A.tiles_per_search - 1 - q;
+        const uint32_t t = s * A.tiles_per_search + lt;
         const SearchConst* S = search_const(A, s);
         const uint32_t i0 = lt * static_cast<uint32_t>(kTile);
         const uint32_t i1 = min(i0 + static_cast<uint32_t>(kTile), A.cand_per_search);
@@ -638,7 +645,7 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
             if (cnt) atomicAdd(&A.counts[s], static_cast<unsigned long long>(cnt));
             if (kOut == kOutFirst && cnt) atomicMin(&A.first_idx[s], i0 + first);
         }
-        t = __shfl_sync(kFull, t_claim, 0);
+        c = __shfl_sync(kFull, t_claim, 0);
     }
     flush_counters(ct, A, lane);
 }
