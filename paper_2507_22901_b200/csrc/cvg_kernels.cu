@@ -311,6 +311,7 @@ __device__ __forceinline__ int code_exact_from(double x, int c, const double* th
 struct Smem {
     float4 t3[256];     // {tf[g], tf[g+1], tf[g+2], 0}
     double thr_d[256];
+    uint32_t first[kWarpsPerBlock];  // FIRST mode: tile offset of the warp's first passing candidate
     uint8_t guess[kGuessBuckets + 16];
 };
 
@@ -483,13 +484,15 @@ __device__ __forceinline__ bool candidate_pass(const Smem& sm, const SearchConst
 // Appends the passing lanes of one 32-candidate chunk to the tile's list
 // (PAIRS: ordered offsets in global scratch; FIRST: remembers the first).
 template <int kOut>
-__device__ __forceinline__ void append(bool pass, uint32_t off, uint16_t* list, uint32_t& cnt, uint32_t& first,
+__device__ __forceinline__ void append(bool pass, uint32_t off, uint16_t* list, uint32_t& cnt, uint32_t* first,
                                        unsigned lane_lt) {
     const unsigned b = __ballot_sync(kFull, pass);
     if (kOut == kOutPairs) {
         if (pass) list[cnt + __popc(b & lane_lt)] = static_cast<uint16_t>(off);
     } else if (kOut == kOutFirst) {
-        if (cnt == 0 && b) first = __shfl_sync(kFull, off, __ffs(b) - 1);
+        // the first passing lane of the tile's first passing chunk records its
+        // offset in shared memory (keeps a register free in the hot loop)
+        if (cnt == 0 && pass && (b & lane_lt) == 0) *first = off;
     }
     cnt += __popc(b);
 }
@@ -499,7 +502,7 @@ __device__ __forceinline__ void append(bool pass, uint32_t off, uint16_t* list, 
 template <int kOut>
 __device__ __forceinline__ void band_settle(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
                                             uint32_t m, float minl, float maxq, uint32_t off, uint16_t* list,
-                                            uint32_t& cnt, uint32_t& first, Counters& ct, unsigned lane_lt) {
+                                            uint32_t& cnt, uint32_t* first, Counters& ct, unsigned lane_lt) {
     bool pass = band_certain(C, minl, maxq);
     if (band_attention(C, minl, maxq) & !pass) {
         double lp[3], lm[3];
@@ -517,48 +520,66 @@ __device__ __forceinline__ void band_chunk(const Consts& C, float r, float2 sc, 
     band_stats<kL>(C, dp, dm, minl, maxq);
 }
 
+// Two chunks sharing one vote: the decisions of candidates ix and ix + 32.
+template <int kL, bool kCubeOnly, int kOut>
+__device__ __forceinline__ void band_pair(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
+                                          float r, float2 sa, float2 sb, uint32_t ix, uint32_t off, uint16_t* list,
+                                          uint32_t& cnt, uint32_t* first, Counters& ct, unsigned lane_lt) {
+    float la_, qa_, lb_, qb_;
+    band_chunk<kL, kCubeOnly>(C, r, sa, la_, qa_);
+    band_chunk<kL, kCubeOnly>(C, r, sb, lb_, qb_);
+    if (__any_sync(kFull, band_attention(C, la_, qa_) | band_attention(C, lb_, qb_))) {
+        band_settle<kOut>(S, C, A, k, ix, la_, qa_, off, list, cnt, first, ct, lane_lt);
+        band_settle<kOut>(S, C, A, k, ix + 32, lb_, qb_, off + 32, list, cnt, first, ct, lane_lt);
+    }
+}
+
 // Hot loop: FAST path, band mode, kL loud channels, `nch` full 32-candidate
 // chunks of radius row k starting at angle m0 (na % 32 == 0: chunks never
-// straddle rows).  Two chunks per iteration share one vote (ILP across
-// chunks).  Per candidate: 1 LDG (L1-resident trig, prefetched two chunks
-// ahead), 24 FMA-pipe ops (4 f, 8 cube, 12 matrix) + 4 min/max + compares.
+// straddle rows).  Two chunks per vote (ILP across chunks); the loop body
+// holds two such pairs with ping-pong prefetch registers (trig two chunks
+// ahead, L1-resident), so no register rotation per pair.  Per candidate:
+// 1 LDG, 24 FMA-pipe ops (4 f, 8 cube, 12 matrix) + 4 min/max + compares.
 // kCubeOnly rows (r < rcube) never reach the linear branch of f^-1.
 template <int kL, bool kCubeOnly, int kOut>
 __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
                                          float r, uint32_t m0, uint32_t nch, uint32_t off, uint16_t* list,
-                                         uint32_t& cnt, uint32_t& first, Counters& ct, unsigned lane,
+                                         uint32_t& cnt, uint32_t* first, Counters& ct, unsigned lane,
                                          unsigned lane_lt) {
     const float2* __restrict__ trig = reinterpret_cast<const float2*>(A.trig_f);
     const uint32_t mb = m0 + lane;
     uint32_t ix = mb;
+    const uint32_t off0 = off + lane - mb;  // candidate offset in the tile = off0 + ix
+    float2 a0 = __ldg(trig + ix), a1 = __ldg(trig + ix + 32);
+    if ((nch >> 1) & 1u) {  // peel one pair: the loop below takes pairs two at a time
+        const float2 b0 = __ldg(trig + ix + 64), b1 = __ldg(trig + ix + 96);
+        band_pair<kL, kCubeOnly, kOut>(S, C, A, k, r, a0, a1, ix, off0 + ix, list, cnt, first, ct, lane_lt);
+        ix += 64;
+        a0 = b0;
+        a1 = b1;
+    }
     const uint32_t iend = mb + 32u * (nch & ~1u);
-    float2 na_ = __ldg(trig + ix), nb_ = __ldg(trig + ix + 32);
 #pragma unroll 1  // code size: 3 loud counts x 2 branch forms x 3 outputs share the I-cache
-    for (; ix != iend; ix += 64) {
-        const float2 sa = na_, sb = nb_;
-        na_ = __ldg(trig + ix + 64);  // prefetch; the table is padded by 128 entries
-        nb_ = __ldg(trig + ix + 96);
-        float la_, qa_, lb_, qb_;
-        band_chunk<kL, kCubeOnly>(C, r, sa, la_, qa_);
-        band_chunk<kL, kCubeOnly>(C, r, sb, lb_, qb_);
-        if (__any_sync(kFull, band_attention(C, la_, qa_) | band_attention(C, lb_, qb_))) {
-            const uint32_t d = ix - mb;
-            band_settle<kOut>(S, C, A, k, ix, la_, qa_, off + lane + d, list, cnt, first, ct, lane_lt);
-            band_settle<kOut>(S, C, A, k, ix + 32, lb_, qb_, off + lane + d + 32, list, cnt, first, ct, lane_lt);
-        }
+    for (; ix != iend; ix += 128) {
+        const float2 b0 = __ldg(trig + ix + 64), b1 = __ldg(trig + ix + 96);  // the table is padded by 128
+        band_pair<kL, kCubeOnly, kOut>(S, C, A, k, r, a0, a1, ix, off0 + ix, list, cnt, first, ct, lane_lt);
+        a0 = __ldg(trig + ix + 128);
+        a1 = __ldg(trig + ix + 160);
+        band_pair<kL, kCubeOnly, kOut>(S, C, A, k, r, b0, b1, ix + 64, off0 + ix + 64, list, cnt, first, ct,
+                                       lane_lt);
     }
     if (nch & 1u) {
         float la_, qa_;
-        band_chunk<kL, kCubeOnly>(C, r, na_, la_, qa_);
+        band_chunk<kL, kCubeOnly>(C, r, a0, la_, qa_);
         if (__any_sync(kFull, band_attention(C, la_, qa_))) {
-            band_settle<kOut>(S, C, A, k, ix, la_, qa_, off + lane + (ix - mb), list, cnt, first, ct, lane_lt);
+            band_settle<kOut>(S, C, A, k, ix, la_, qa_, off0 + ix, list, cnt, first, ct, lane_lt);
         }
     }
 }
 
 template <int kL, int kOut>
 __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t i0,
-                                          uint32_t i1, uint16_t* list, uint32_t& cnt, uint32_t& first, Counters& ct,
+                                          uint32_t i1, uint16_t* list, uint32_t& cnt, uint32_t* first, Counters& ct,
                                           unsigned lane, unsigned lane_lt) {
     uint32_t k = div_na(i0, A);
     uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
@@ -608,7 +629,8 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         const uint32_t i0 = lt * static_cast<uint32_t>(kTile);
         const uint32_t i1 = min(i0 + static_cast<uint32_t>(kTile), A.cand_per_search);
         uint16_t* list = kOut == kOutPairs ? A.scratch + static_cast<size_t>(t) * kTile : nullptr;
-        uint32_t cnt = 0, first = 0;
+        uint32_t cnt = 0;
+        uint32_t* first = &sm.first[threadIdx.x >> 5];
         Consts C;
         load_consts(S, C);
         if (kMode == kModeBand && kPath == kPathFast && A.aligned) {
@@ -632,6 +654,7 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
                 append<kOut>(pass, i - i0, list, cnt, first, lane_lt);
             }
         }
+        if (kOut == kOutFirst) __syncwarp();  // *first was written by another lane
         if (lane == 0) {
             if (kOut == kOutPairs) {
                 A.tile_count[t] = cnt;
@@ -643,7 +666,7 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
                 }
             }
             if (cnt) atomicAdd(&A.counts[s], static_cast<unsigned long long>(cnt));
-            if (kOut == kOutFirst && cnt) atomicMin(&A.first_idx[s], i0 + first);
+            if (kOut == kOutFirst && cnt) atomicMin(&A.first_idx[s], i0 + *first);
         }
         c = __shfl_sync(kFull, t_claim, 0);
     }
