@@ -12,7 +12,6 @@
 #include <unistd.h>
 
 #include <algorithm>
-#include <array>
 #include <atomic>
 #include <condition_variable>
 #include <functional>
@@ -991,32 +990,10 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     const std::vector<float>& trig_f = grid->trig_f;
     const std::vector<double>& trig_d = grid->trig_d;
 
-    // Claim order within a tile round: searches grouped by loud count (band
-    // mode), so the warps resident on an SM mostly run one hot-loop
-    // specialization and share the instruction cache.
-    std::vector<uint32_t> claim;
-    static const bool group_claims = [] {
-        const char* e = std::getenv("CVG_CLAIM_GROUP");  // A/B switch; default on
-        return !e || std::atoi(e) != 0;
-    }();
-    if (group_claims && p->mode == cvg::kModeBand && p->n > 1) {
-        std::array<size_t, 4> bucket{};
-        for (int32_t i = 0; i < p->n; ++i) ++bucket[__builtin_popcount(d->pattern_bits[i] & 7)];
-        int kinds = 0;
-        for (size_t b : bucket) kinds += b > 0;
-        if (kinds > 1) {
-            std::array<size_t, 4> at{};
-            for (int b = 1; b < 4; ++b) at[b] = at[b - 1] + bucket[b - 1];
-            claim.resize(p->n);
-            for (int32_t i = 0; i < p->n; ++i) claim[at[__builtin_popcount(d->pattern_bits[i] & 7)]++] = i;
-        }
-    }
-
-    // ---- one constant blob: [sc | sc_index | claim | radii | trig | thresholds | guess] ----
+    // ---- one constant blob: [sc | sc_index | radii | trig | thresholds | guess] ----
     Layout L;
     const size_t o_sc = L.take(sizeof(SearchConst) * n_sc);
     const size_t o_si = L.take(sizeof(uint32_t) * sc_index.size());
-    const size_t o_co = L.take(sizeof(uint32_t) * claim.size());
     const size_t o_rd = L.take(sizeof(double) * p->nr);
     const size_t o_rf = L.take(sizeof(float) * p->nr);
     const size_t o_td = L.take(sizeof(double) * trig_d.size());
@@ -1044,7 +1021,6 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
             },
             1);
     }
-    if (!claim.empty()) std::memcpy(stage + o_co, claim.data(), sizeof(uint32_t) * claim.size());
     std::memcpy(stage + o_rd, d->radii, sizeof(double) * p->nr);
     std::memcpy(stage + o_rf, radii_f.data(), sizeof(float) * p->nr);
     std::memcpy(stage + o_td, trig_d.data(), sizeof(double) * trig_d.size());
@@ -1056,7 +1032,6 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     std::memset(&A, 0, sizeof(A));
     A.sc = at<const SearchConst>(p->d_const, o_sc);
     A.sc_index = sc_index.empty() ? nullptr : at<const uint32_t>(p->d_const, o_si);
-    A.claim_order = claim.empty() ? nullptr : at<const uint32_t>(p->d_const, o_co);
     A.radii_d = at<const double>(p->d_const, o_rd);
     A.radii_f = at<const float>(p->d_const, o_rf);
     A.trig_d = at<const double>(p->d_const, o_td);

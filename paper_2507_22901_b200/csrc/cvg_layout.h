@@ -65,7 +65,6 @@ enum Path : int { kPathFast = 0, kPathExact = 1, kPathAudit = 2 };
 struct LaunchArgs {
     const SearchConst* sc;     // [n_unique] per-search constant records
     const uint32_t* sc_index;  // [n_searches] record of each search, nullptr = identity
-    const uint32_t* claim_order;  // [n_searches] search claimed at position p of a tile round, nullptr = identity
     const float* radii_f;      // [nr]
     const double* radii_d;     // [nr]
     const float* trig_f;       // [na][2] = (sin/500, cos/200) as float
