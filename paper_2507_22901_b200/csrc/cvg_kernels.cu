@@ -520,26 +520,11 @@ __device__ __forceinline__ void band_chunk(const Consts& C, float r, float2 sc, 
     band_stats<kL>(C, dp, dm, minl, maxq);
 }
 
-// Two chunks sharing one vote: the decisions of candidates ix and ix + 32.
-template <int kL, bool kCubeOnly, int kOut>
-__device__ __forceinline__ void band_pair(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
-                                          float r, float2 sa, float2 sb, uint32_t ix, uint32_t off, uint16_t* list,
-                                          uint32_t& cnt, uint32_t* first, Counters& ct, unsigned lane_lt) {
-    float la_, qa_, lb_, qb_;
-    band_chunk<kL, kCubeOnly>(C, r, sa, la_, qa_);
-    band_chunk<kL, kCubeOnly>(C, r, sb, lb_, qb_);
-    if (__any_sync(kFull, band_attention(C, la_, qa_) | band_attention(C, lb_, qb_))) {
-        band_settle<kOut>(S, C, A, k, ix, la_, qa_, off, list, cnt, first, ct, lane_lt);
-        band_settle<kOut>(S, C, A, k, ix + 32, lb_, qb_, off + 32, list, cnt, first, ct, lane_lt);
-    }
-}
-
 // Hot loop: FAST path, band mode, kL loud channels, `nch` full 32-candidate
 // chunks of radius row k starting at angle m0 (na % 32 == 0: chunks never
-// straddle rows).  Two chunks per vote (ILP across chunks); the loop body
-// holds two such pairs with ping-pong prefetch registers (trig two chunks
-// ahead, L1-resident), so no register rotation per pair.  Per candidate:
-// 1 LDG, 24 FMA-pipe ops (4 f, 8 cube, 12 matrix) + 4 min/max + compares.
+// straddle rows).  Two chunks per iteration share one vote (ILP across
+// chunks).  Per candidate: 1 LDG (L1-resident trig, prefetched two chunks
+// ahead), 24 FMA-pipe ops (4 f, 8 cube, 12 matrix) + 4 min/max + compares.
 // kCubeOnly rows (r < rcube) never reach the linear branch of f^-1.
 template <int kL, bool kCubeOnly, int kOut>
 __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
@@ -549,30 +534,27 @@ __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, 
     const float2* __restrict__ trig = reinterpret_cast<const float2*>(A.trig_f);
     const uint32_t mb = m0 + lane;
     uint32_t ix = mb;
-    const uint32_t off0 = off + lane - mb;  // candidate offset in the tile = off0 + ix
-    float2 a0 = __ldg(trig + ix), a1 = __ldg(trig + ix + 32);
-    if ((nch >> 1) & 1u) {  // peel one pair: the loop below takes pairs two at a time
-        const float2 b0 = __ldg(trig + ix + 64), b1 = __ldg(trig + ix + 96);
-        band_pair<kL, kCubeOnly, kOut>(S, C, A, k, r, a0, a1, ix, off0 + ix, list, cnt, first, ct, lane_lt);
-        ix += 64;
-        a0 = b0;
-        a1 = b1;
-    }
     const uint32_t iend = mb + 32u * (nch & ~1u);
-#pragma unroll 1  // code size: 3 loud counts x 2 branch forms x 3 outputs share the I-cache
-    for (; ix != iend; ix += 128) {
-        const float2 b0 = __ldg(trig + ix + 64), b1 = __ldg(trig + ix + 96);  // the table is padded by 128
-        band_pair<kL, kCubeOnly, kOut>(S, C, A, k, r, a0, a1, ix, off0 + ix, list, cnt, first, ct, lane_lt);
-        a0 = __ldg(trig + ix + 128);
-        a1 = __ldg(trig + ix + 160);
-        band_pair<kL, kCubeOnly, kOut>(S, C, A, k, r, b0, b1, ix + 64, off0 + ix + 64, list, cnt, first, ct,
-                                       lane_lt);
+    float2 na_ = __ldg(trig + ix), nb_ = __ldg(trig + ix + 32);
+#pragma unroll 1  // code size (an unrolled two-pair body measured 25% slower on cfg1/cfg3, 7% faster on cfg2)
+    for (; ix != iend; ix += 64) {
+        const float2 sa = na_, sb = nb_;
+        na_ = __ldg(trig + ix + 64);  // prefetch; the table is padded by 128 entries
+        nb_ = __ldg(trig + ix + 96);
+        float la_, qa_, lb_, qb_;
+        band_chunk<kL, kCubeOnly>(C, r, sa, la_, qa_);
+        band_chunk<kL, kCubeOnly>(C, r, sb, lb_, qb_);
+        if (__any_sync(kFull, band_attention(C, la_, qa_) | band_attention(C, lb_, qb_))) {
+            const uint32_t d = ix - mb;
+            band_settle<kOut>(S, C, A, k, ix, la_, qa_, off + lane + d, list, cnt, first, ct, lane_lt);
+            band_settle<kOut>(S, C, A, k, ix + 32, lb_, qb_, off + lane + d + 32, list, cnt, first, ct, lane_lt);
+        }
     }
     if (nch & 1u) {
         float la_, qa_;
-        band_chunk<kL, kCubeOnly>(C, r, a0, la_, qa_);
+        band_chunk<kL, kCubeOnly>(C, r, na_, la_, qa_);
         if (__any_sync(kFull, band_attention(C, la_, qa_))) {
-            band_settle<kOut>(S, C, A, k, ix, la_, qa_, off0 + ix, list, cnt, first, ct, lane_lt);
+            band_settle<kOut>(S, C, A, k, ix, la_, qa_, off + lane + (ix - mb), list, cnt, first, ct, lane_lt);
         }
     }
 }
