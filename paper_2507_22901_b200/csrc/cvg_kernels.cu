@@ -598,14 +598,23 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
     uint32_t c = __shfl_sync(kFull, t_claim, 0);
     while (c < A.n_tiles) {
         if (lane == 0) t_claim = atomicAdd(&A.ticket[0], 1u);  // next tile, consumed at the end
-        // Claim order: outermost radius tiles of every search first, the
-        // innermost last.  Outer rows are the costly ones (they reach the
-        // linear branch of f^-1 and need more repairs), so the last round of
-        // claims -- the tail where warps run out of work -- is the cheapest.
-        // Tile t (search s, tile lt) keeps its storage slot s * tps + lt.
-        const uint32_t q = c / static_cast<uint32_t>(A.n_searches);
-        const uint32_t s = c - q * static_cast<uint32_t>(A.n_searches);
-        const uint32_t lt = A.tiles_per_search - 1 - q;
+        // Claim order for searches of many tiles: outermost radius tiles of
+        // every search first, the innermost last.  Outer rows are the costly
+        // ones (they reach the linear branch of f^-1 and need more repairs),
+        // so the last round of claims -- the tail where warps run out of
+        // work -- is the cheapest.  Searches of a few tiles (per-pixel
+        // batches) keep search order: a warp's consecutive tiles share the
+        // search's constants.  Tile t (search s, tile lt) keeps its storage
+        // slot s * tps + lt either way.
+        uint32_t s, lt;
+        if (A.tiles_per_search >= 16) {
+            const uint32_t q = c / static_cast<uint32_t>(A.n_searches);
+            s = c - q * static_cast<uint32_t>(A.n_searches);
+            lt = A.tiles_per_search - 1 - q;
+        } else {
+            s = c / A.tiles_per_search;
+            lt = c - s * A.tiles_per_search;
+        }
         const uint32_t t = s * A.tiles_per_search + lt;
         const SearchConst* S = search_const(A, s);
         const uint32_t i0 = lt * static_cast<uint32_t>(kTile);
