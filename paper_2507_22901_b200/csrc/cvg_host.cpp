@@ -718,6 +718,7 @@ struct cvg_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // D2H of finished chunks while later chunks compute
     cudaStream_t tail_stream = nullptr;  // per-range counts/totals of a pipelined search
+    cudaStream_t aux_stream = nullptr;   // second range view of split plans
     std::recursive_mutex mu;
     // pair total of the last pipelined search of the same shape: sizes the
     // pinned result so repeated searches never grow it
@@ -750,7 +751,11 @@ struct cvg_plan {
     void* d_out_codes = nullptr;
     uint64_t capacity = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    cudaEvent_t marks[2] = {nullptr, nullptr};  // after phase 1, after the scan (PAIRS)
+    // PAIRS: after phase 1, after the scan; split: [0] phase 1 of view a, [1]
+    // phase 1 of view b, [2] scan of view a (fork/join), [3] join of view b
+    cudaEvent_t marks[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool split = false;
+    LaunchArgs va{}, vb{};  // the two range views of a split plan
     bool ran = false;
     cudaStream_t last_stream = nullptr;
     uint64_t input_bytes = 0;
@@ -1057,16 +1062,35 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.n_tiles = n_tiles;
 
     // ---- per-run workspace --------------------------------------------------
-    // zeroed each run:  status[n_scan_blocks] | tickets[4] | counts[n] | stats
-    // written each run: tile_count[n_tiles] | tile_base[n_tiles] | total   (PAIRS)
+    // zeroed each run:  status[n_scan_blocks] | tickets[8] | counts[n] | stats | total | total_a | total_b
+    // written each run: tile_count[n_tiles] | tile_base[n_tiles] | worklist   (PAIRS)
     const bool pairs = p->out == cvg::kOutPairs;
-    const uint64_t scan_blocks = pairs ? (n_tiles + cvg::kScanTile - 1) / cvg::kScanTile : 0;
+    const int per_sm = cvg::search_blocks_per_sm(p->mode, p->out, p->path);
+    if (per_sm <= 0) {
+        cudaError_t le = cudaGetLastError();
+        return fail(CVG_ECUDA, std::string("search kernel cannot be resident on this device (") +
+                                   cudaGetErrorString(le) + "); sm_100a image required");
+    }
+    // Two range views on two streams (PAIRS): the second range's phase 1
+    // fills the first's tail, and the first's scan + emit fill the second's.
+    // Worth it when each range still has many tile rounds.
+    static const bool allow_split = [] {
+        const char* e = std::getenv("CVG_SPLIT");  // A/B switch; default on
+        return !e || std::atoi(e) != 0;
+    }();
+    const uint64_t resident_warps = static_cast<uint64_t>(per_sm) * ctx->sms * cvg::kWarpsPerBlock;
+    p->split = allow_split && pairs && p->n >= 2 && n_tiles >= 8 * resident_warps;
+    const uint32_t n_a = p->split ? static_cast<uint32_t>(p->n / 2) : static_cast<uint32_t>(p->n);
+    const uint64_t tiles_a = static_cast<uint64_t>(n_a) * tps, tiles_b = n_tiles - tiles_a;
+    const uint64_t scan_a = pairs ? (tiles_a + cvg::kScanTile - 1) / cvg::kScanTile : 0;
+    const uint64_t scan_b = p->split ? (tiles_b + cvg::kScanTile - 1) / cvg::kScanTile : 0;
     Layout W;
-    const size_t o_st = W.take(sizeof(unsigned long long) * scan_blocks);
-    const size_t o_tk = W.take(sizeof(unsigned int) * 4);
+    const size_t o_st = W.take(sizeof(unsigned long long) * (scan_a + scan_b));
+    const size_t o_tk = W.take(sizeof(unsigned int) * 8);
     const size_t o_ct = W.take(sizeof(unsigned long long) * p->n);
     const size_t o_ss = W.take(sizeof(cvg::Stats));
     const size_t o_to = W.take(sizeof(unsigned long long));  // stats+total read back as one ChunkTail
+    const size_t o_ta = W.take(sizeof(unsigned long long) * 2);  // per-view totals (split)
     p->work_bytes = W.off;  // memset span
     const size_t o_tc = W.take(sizeof(uint32_t) * (pairs ? n_tiles : 0));
     const size_t o_tb = W.take(sizeof(unsigned long long) * (pairs ? n_tiles : 0));
@@ -1081,6 +1105,11 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.tile_base = at<unsigned long long>(p->d_work, o_tb);
     A.total = at<unsigned long long>(p->d_work, o_to);
     A.worklist = at<uint32_t>(p->d_work, o_wl);
+    A.search_begin = 0;
+    A.range_searches = static_cast<uint32_t>(p->n);
+    A.tile_begin = 0;
+    A.base_offset = nullptr;
+    A.grand_total = nullptr;
     if (pairs) {
         p->d_scratch = ctx->dev.alloc(static_cast<size_t>(n_tiles) * cvg::kTile * sizeof(uint16_t));
         if (!p->d_scratch) return fail(CVG_ENOMEM, "device allocation of the tile lists failed");
@@ -1097,16 +1126,28 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         A.first_codes = at<uint8_t>(p->d_first, o_fc);
     }
 
-    const int per_sm = cvg::search_blocks_per_sm(p->mode, p->out, p->path);
-    if (per_sm <= 0) {
-        cudaError_t le = cudaGetLastError();
-        return fail(CVG_ECUDA, std::string("search kernel cannot be resident on this device (") +
-                                   cudaGetErrorString(le) + "); sm_100a image required");
+    if (p->split) {
+        unsigned long long* totals = at<unsigned long long>(p->d_work, o_ta);
+        p->va = A;
+        p->va.range_searches = n_a;
+        p->va.n_tiles = tiles_a;
+        p->va.total = totals;
+        p->vb = A;
+        p->vb.search_begin = n_a;
+        p->vb.range_searches = static_cast<uint32_t>(p->n) - n_a;
+        p->vb.tile_begin = tiles_a;
+        p->vb.n_tiles = tiles_b;
+        p->vb.status = A.status + scan_a;
+        p->vb.ticket = A.ticket + 4;
+        p->vb.total = totals + 1;
+        p->vb.worklist = A.worklist + tiles_a * (cvg::kTile / cvg::kEmitSpan);
+        p->vb.base_offset = totals;
+        p->vb.grand_total = A.total;
     }
     const uint64_t want = (n_tiles + cvg::kWarpsPerBlock - 1) / cvg::kWarpsPerBlock;
     p->grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(per_sm) * ctx->sms, want));
     if (p->grid < 1) p->grid = 1;
-    for (cudaEvent_t* ev : {&p->ev0, &p->ev1, &p->marks[0], &p->marks[1]}) {
+    for (cudaEvent_t* ev : {&p->ev0, &p->ev1, &p->marks[0], &p->marks[1], &p->marks[2], &p->marks[3]}) {
         if (!ctx->events.empty()) {
             *ev = ctx->events.back();
             ctx->events.pop_back();
@@ -1137,13 +1178,14 @@ int plan_build_safe(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const G
 
 void plan_release(cvg_plan* p) {
     if (!p->ctx) return;
+    if (p->ran && !p->empty && p->ev1) cudaEventSynchronize(p->ev1);  // buffers go back to the pool
     plan_free_outputs(p);
     p->ctx->dev.release(p->d_const);
     p->ctx->dev.release(p->d_work);
     p->ctx->dev.release(p->d_first);
     p->ctx->dev.release(p->d_scratch);
     if (p->stage) cudaStreamSynchronize(p->ctx->stream);  // the constant upload may still be in flight
-    for (cudaEvent_t* ev : {&p->ev0, &p->ev1, &p->marks[0], &p->marks[1]}) {
+    for (cudaEvent_t* ev : {&p->ev0, &p->ev1, &p->marks[0], &p->marks[1], &p->marks[2], &p->marks[3]}) {
         if (*ev) p->ctx->events.push_back(*ev);
         *ev = nullptr;
     }
@@ -1160,8 +1202,25 @@ int plan_enqueue(cvg_plan* p, cudaStream_t st) {
     CVG_CUDA(cudaMemsetAsync(p->d_work, 0, p->work_bytes, st));
     if (p->out == cvg::kOutFirst) CVG_CUDA(cudaMemsetAsync(p->d_first, 0xff, static_cast<size_t>(p->n) * 4, st));
     CVG_CUDA(cudaEventRecord(p->ev0, st));
-    CVG_CUDA(cvg::launch_search(p->args, p->mode, p->out, p->path, p->grid, st, p->marks));
-    if (p->out == cvg::kOutFirst) CVG_CUDA(cvg::launch_first_codes(p->args, st));
+    if (p->split) {
+        cudaStream_t aux = p->ctx->aux_stream;
+        CVG_CUDA(cudaStreamWaitEvent(aux, p->ev0, 0));
+        CVG_CUDA(cvg::launch_phase1(p->va, p->mode, p->out, p->path, p->grid, st));
+        CVG_CUDA(cudaEventRecord(p->marks[0], st));
+        CVG_CUDA(cvg::launch_phase1(p->vb, p->mode, p->out, p->path, p->grid, aux));
+        CVG_CUDA(cudaEventRecord(p->marks[1], aux));
+        CVG_CUDA(cvg::launch_scan(p->va, st));
+        CVG_CUDA(cudaEventRecord(p->marks[2], st));
+        CVG_CUDA(cvg::launch_emit(p->va, p->mode, p->path, p->grid, st));
+        CVG_CUDA(cvg::launch_scan(p->vb, aux));
+        CVG_CUDA(cudaStreamWaitEvent(aux, p->marks[2], 0));  // view b's pairs start after view a's total
+        CVG_CUDA(cvg::launch_emit(p->vb, p->mode, p->path, p->grid, aux));
+        CVG_CUDA(cudaEventRecord(p->marks[3], aux));
+        CVG_CUDA(cudaStreamWaitEvent(st, p->marks[3], 0));
+    } else {
+        CVG_CUDA(cvg::launch_search(p->args, p->mode, p->out, p->path, p->grid, st, p->marks));
+        if (p->out == cvg::kOutFirst) CVG_CUDA(cvg::launch_first_codes(p->args, st));
+    }
     CVG_CUDA(cudaEventRecord(p->ev1, st));
     return CVG_OK;
 }
@@ -1604,6 +1663,7 @@ int cvg_create(int device, cvg_ctx** out) {
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->tail_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) {
         size_t free_b = 0;
         e = cudaMemGetInfo(&free_b, &ctx->total_mem);
@@ -1629,11 +1689,13 @@ void cvg_destroy(cvg_ctx* ctx) {
     }
     cudaStreamSynchronize(ctx->copy_stream);
     cudaStreamSynchronize(ctx->tail_stream);
+    cudaStreamSynchronize(ctx->aux_stream);
     layout_free(ctx->codec_layout);
     for (cudaEvent_t ev : ctx->events) cudaEventDestroy(ev);
     cudaStreamDestroy(ctx->stream);
     cudaStreamDestroy(ctx->copy_stream);
     cudaStreamDestroy(ctx->tail_stream);
+    cudaStreamDestroy(ctx->aux_stream);
     delete ctx;
 }
 
@@ -1733,6 +1795,17 @@ int cvg_plan_last_phase_ms(cvg_plan* p, float* phase1_ms, float* scan_ms, float*
     CVG_CUDA(cudaEventSynchronize(p->ev1));
     if (p->out != cvg::kOutPairs) return cudaEventElapsedTime(phase1_ms, p->ev0, p->ev1) == cudaSuccess
                                              ? CVG_OK : fail(CVG_ECUDA, "event timing failed");
+    if (p->split) {
+        // phase 1 = until both views' phase 1 ended; scan + emit = the rest
+        // (view a's scan and emit overlap view b's phase 1 and are not split out)
+        float a = 0.f, b = 0.f, all = 0.f;
+        CVG_CUDA(cudaEventElapsedTime(&a, p->ev0, p->marks[0]));
+        CVG_CUDA(cudaEventElapsedTime(&b, p->ev0, p->marks[1]));
+        CVG_CUDA(cudaEventElapsedTime(&all, p->ev0, p->ev1));
+        *phase1_ms = std::max(a, b);
+        *emit_ms = all - *phase1_ms;
+        return CVG_OK;
+    }
     CVG_CUDA(cudaEventElapsedTime(phase1_ms, p->ev0, p->marks[0]));
     CVG_CUDA(cudaEventElapsedTime(scan_ms, p->marks[0], p->marks[1]));
     CVG_CUDA(cudaEventElapsedTime(emit_ms, p->marks[1], p->ev1));
@@ -1741,6 +1814,7 @@ int cvg_plan_last_phase_ms(cvg_plan* p, float* phase1_ms, float* scan_ms, float*
 
 int cvg_plan_launches(const cvg_plan* p) {
     if (!p || p->empty) return 0;
+    if (p->split) return 6;
     return p->out == cvg::kOutPairs ? 3 : p->out == cvg::kOutFirst ? 2 : 1;
 }
 

@@ -15,6 +15,10 @@ namespace cvg {
 // `marks` (optional, 2 events) are recorded after phase 1 and after the scan.
 cudaError_t launch_search(const LaunchArgs& a, int mode, int out, int path, int grid, cudaStream_t st,
                           cudaEvent_t* marks = nullptr);
+// The three PAIRS-mode kernels separately (range views on two streams).
+cudaError_t launch_phase1(const LaunchArgs& a, int mode, int out, int path, int grid, cudaStream_t st);
+cudaError_t launch_scan(const LaunchArgs& a, cudaStream_t st);
+cudaError_t launch_emit(const LaunchArgs& a, int mode, int path, int grid, cudaStream_t st);
 // Resident blocks per SM for that instantiation; also opts the kernel into its
 // dynamic shared memory size on the current device (call before launching).
 int search_blocks_per_sm(int mode, int out, int path);

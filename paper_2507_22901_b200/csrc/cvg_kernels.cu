@@ -608,12 +608,13 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         // slot s * tps + lt either way.
         uint32_t s, lt;
         if (A.tiles_per_search >= 16) {
-            const uint32_t q = c / static_cast<uint32_t>(A.n_searches);
-            s = c - q * static_cast<uint32_t>(A.n_searches);
+            const uint32_t q = c / A.range_searches;
+            s = A.search_begin + (c - q * A.range_searches);
             lt = A.tiles_per_search - 1 - q;
         } else {
-            s = c / A.tiles_per_search;
-            lt = c - s * A.tiles_per_search;
+            const uint32_t sr = c / A.tiles_per_search;
+            lt = c - sr * A.tiles_per_search;
+            s = A.search_begin + sr;
         }
         const uint32_t t = s * A.tiles_per_search + lt;
         const SearchConst* S = search_const(A, s);
@@ -679,7 +680,7 @@ __global__ void __launch_bounds__(kBlock) scan_kernel(const LaunchArgs A) {
     unsigned long long sum = 0;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        v[j] = base + j < A.n_tiles ? A.tile_count[base + j] : 0u;
+        v[j] = base + j < A.n_tiles ? A.tile_count[A.tile_begin + base + j] : 0u;
         sum += v[j];
     }
     unsigned long long incl = sum;  // warp inclusive scan
@@ -729,7 +730,7 @@ __global__ void __launch_bounds__(kBlock) scan_kernel(const LaunchArgs A) {
     unsigned long long run = s_prefix + warp_off + (incl - sum);
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        if (base + j < A.n_tiles) A.tile_base[base + j] = run;
+        if (base + j < A.n_tiles) A.tile_base[A.tile_begin + base + j] = run;
         run += v[j];
     }
     if (base < A.n_tiles && base + kScanItems >= A.n_tiles) *A.total = run;
@@ -746,6 +747,8 @@ __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
     load_tables(sm, A);
     const unsigned lane = threadIdx.x & 31;
     const uint32_t n_work = *reinterpret_cast<volatile unsigned int*>(&A.ticket[3]);
+    const unsigned long long base0 = A.base_offset ? *A.base_offset : 0ull;
+    if (A.grand_total && blockIdx.x == 0 && threadIdx.x == 0) *A.grand_total = base0 + *A.total;
     Counters ct;
     uint32_t q_claim = 0;
     if (lane == 0) q_claim = atomicAdd(&A.ticket[2], 1u);
@@ -756,7 +759,7 @@ __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
         const uint32_t t = item >> 4;
         const uint32_t p0 = (item & 15u) * kEmitSpan;
         const uint32_t cnt = min(A.tile_count[t] - p0, static_cast<uint32_t>(kEmitSpan));
-        const unsigned long long base = A.tile_base[t] + p0;
+        const unsigned long long base = base0 + A.tile_base[t] + p0;
         const uint16_t* list = A.scratch + static_cast<size_t>(t) * kTile + p0;
         if (base + cnt > A.capacity) {
             if (lane == 0) ++ct.overflow;
@@ -876,19 +879,34 @@ __global__ void ffma_peak_kernel(float* out, int iters, float a, float b) {
 }
 
 template <int kMode, int kOut, int kPath>
-cudaError_t launch_t(const LaunchArgs& a, int grid, cudaStream_t st, cudaEvent_t* marks) {
+cudaError_t phase1_t(const LaunchArgs& a, int grid, cudaStream_t st) {
     // The dynamic shared-memory sizes are opted into by occupancy_t (plan creation).
     phase1_kernel<kMode, kOut, kPath><<<grid, kBlock, sizeof(Smem), st>>>(a);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess || kOut != kOutPairs) return e;
-    if (marks) cudaEventRecord(marks[0], st);
-    const unsigned scan_blocks = static_cast<unsigned>((a.n_tiles + kScanTile - 1) / kScanTile);
-    scan_kernel<<<scan_blocks, kBlock, 0, st>>>(a);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    if (marks) cudaEventRecord(marks[1], st);
+    return cudaGetLastError();
+}
+
+template <int kMode, int kPath>
+cudaError_t emit_t(const LaunchArgs& a, int grid, cudaStream_t st) {
     emit_kernel<kMode, kPath><<<grid, kBlock, sizeof(Smem), st>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t scan_l(const LaunchArgs& a, cudaStream_t st) {
+    const unsigned scan_blocks = static_cast<unsigned>((a.n_tiles + kScanTile - 1) / kScanTile);
+    if (scan_blocks == 0) return cudaSuccess;
+    scan_kernel<<<scan_blocks, kBlock, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <int kMode, int kOut, int kPath>
+cudaError_t launch_t(const LaunchArgs& a, int grid, cudaStream_t st, cudaEvent_t* marks) {
+    cudaError_t e = phase1_t<kMode, kOut, kPath>(a, grid, st);
+    if (e != cudaSuccess || kOut != kOutPairs) return e;
+    if (marks) cudaEventRecord(marks[0], st);
+    e = scan_l(a, st);
+    if (e != cudaSuccess) return e;
+    if (marks) cudaEventRecord(marks[1], st);
+    return emit_t<kMode, kPath>(a, grid, st);
 }
 
 template <int kMode, int kOut, int kPath>
@@ -912,6 +930,16 @@ const LaunchFn kLaunch[2][3][3] = {
     {CVG_ROW(kModeBand, kPathFast), CVG_ROW(kModeBand, kPathExact), CVG_ROW(kModeBand, kPathAudit)},
     {CVG_ROW(kModeCodes, kPathFast), CVG_ROW(kModeCodes, kPathExact), CVG_ROW(kModeCodes, kPathAudit)},
 };
+using Phase1Fn = cudaError_t (*)(const LaunchArgs&, int, cudaStream_t);
+#define CVG_P1(M, P) {phase1_t<M, kOutPairs, P>, phase1_t<M, kOutCounts, P>, phase1_t<M, kOutFirst, P>}
+const Phase1Fn kPhase1[2][3][3] = {
+    {CVG_P1(kModeBand, kPathFast), CVG_P1(kModeBand, kPathExact), CVG_P1(kModeBand, kPathAudit)},
+    {CVG_P1(kModeCodes, kPathFast), CVG_P1(kModeCodes, kPathExact), CVG_P1(kModeCodes, kPathAudit)},
+};
+const Phase1Fn kEmit[2][3] = {
+    {emit_t<kModeBand, kPathFast>, emit_t<kModeBand, kPathExact>, emit_t<kModeBand, kPathAudit>},
+    {emit_t<kModeCodes, kPathFast>, emit_t<kModeCodes, kPathExact>, emit_t<kModeCodes, kPathAudit>},
+};
 const OccFn kOcc[2][3][3] = {
     {CVG_OCC(kModeBand, kPathFast), CVG_OCC(kModeBand, kPathExact), CVG_OCC(kModeBand, kPathAudit)},
     {CVG_OCC(kModeCodes, kPathFast), CVG_OCC(kModeCodes, kPathExact), CVG_OCC(kModeCodes, kPathAudit)},
@@ -925,6 +953,14 @@ cudaError_t launch_search(const LaunchArgs& a, int mode, int out, int path, int 
 }
 
 int search_blocks_per_sm(int mode, int out, int path) { return kOcc[mode][path][out](); }
+
+cudaError_t launch_phase1(const LaunchArgs& a, int mode, int out, int path, int grid, cudaStream_t st) {
+    return kPhase1[mode][path][out](a, grid, st);
+}
+cudaError_t launch_scan(const LaunchArgs& a, cudaStream_t st) { return scan_l(a, st); }
+cudaError_t launch_emit(const LaunchArgs& a, int mode, int path, int grid, cudaStream_t st) {
+    return kEmit[mode][path](a, grid, st);
+}
 
 cudaError_t launch_first_codes(const LaunchArgs& a, cudaStream_t st) {
     const int threads = 128;

@@ -80,7 +80,16 @@ struct LaunchArgs {
     uint32_t tiles_per_search;
     uint32_t cand_per_search;  // nr * na (< 2^32)
     uint64_t na_magic;         // ceil(2^64 / na): k = umul64hi(i, na_magic)
-    uint64_t n_tiles;
+    uint64_t n_tiles;              // tiles of this range view
+    // Range view: the launch covers searches [search_begin, search_begin +
+    // range_searches) = tiles [tile_begin, tile_begin + n_tiles).  A plan may
+    // run two views on two streams so that one range's scan and emit fill
+    // the other range's phase-1 tail; tile indices stay global.
+    uint32_t search_begin;
+    uint32_t range_searches;
+    uint64_t tile_begin;
+    const unsigned long long* base_offset;  // emit: pair positions start at *base_offset (nullptr = 0)
+    unsigned long long* grand_total;        // emit of the last view: *grand_total = *base_offset + *total
     unsigned long long* status;    // [n_scan_blocks] chained-scan status words (flag << 62 | value)
     unsigned int* ticket;          // [4]: phase-1 tiles, scan blocks, emit worklist, worklist size
     unsigned long long* counts;    // [n_searches]
