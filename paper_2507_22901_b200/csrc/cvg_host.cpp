@@ -1203,6 +1203,12 @@ int plan_enqueue(cvg_plan* p, cudaStream_t st) {
     if (p->out == cvg::kOutFirst) CVG_CUDA(cudaMemsetAsync(p->d_first, 0xff, static_cast<size_t>(p->n) * 4, st));
     CVG_CUDA(cudaEventRecord(p->ev0, st));
     if (p->split) {
+        // the views copy the output buffers, which cvg_plan_reserve may have replaced
+        for (LaunchArgs* v : {&p->va, &p->vb}) {
+            v->out_idx = p->args.out_idx;
+            v->out_codes = p->args.out_codes;
+            v->capacity = p->args.capacity;
+        }
         cudaStream_t aux = p->ctx->aux_stream;
         CVG_CUDA(cudaStreamWaitEvent(aux, p->ev0, 0));
         CVG_CUDA(cvg::launch_phase1(p->va, p->mode, p->out, p->path, p->grid, st));
@@ -1495,6 +1501,7 @@ int search_pipelined(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, int 
             if (int e = plan_enqueue(&p, ctx->stream)) return e;
             if (int e = enqueue_tail(c)) return e;
             CVG_CUDA(cudaEventSynchronize(done[c]));
+            if (tails[c].st.overflow) return fail(CVG_ECUDA, "pair buffer overflow after resizing");
         }
         t_last_done = now_ms();
         const uint64_t tc = tails[c].total;
