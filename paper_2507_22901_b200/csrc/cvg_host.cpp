@@ -1073,10 +1073,12 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     }
     // Two range views on two streams (PAIRS): the second range's phase 1
     // fills the first's tail, and the first's scan + emit fill the second's.
-    // Worth it when each range still has many tile rounds.
+    // Measured neutral on cfg1/cfg2/cfg3 (the second range's persistent
+    // blocks hold every slot until its own tail, so the first range's emit
+    // only starts there), hence off unless CVG_SPLIT=1.
     static const bool allow_split = [] {
-        const char* e = std::getenv("CVG_SPLIT");  // A/B switch; default on
-        return !e || std::atoi(e) != 0;
+        const char* e = std::getenv("CVG_SPLIT");
+        return e && std::atoi(e) != 0;
     }();
     const uint64_t resident_warps = static_cast<uint64_t>(per_sm) * ctx->sms * cvg::kWarpsPerBlock;
     p->split = allow_split && pairs && p->n >= 2 && n_tiles >= 8 * resident_warps;
