@@ -750,34 +750,17 @@ __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
     const unsigned long long base0 = A.base_offset ? *A.base_offset : 0ull;
     if (A.grand_total && blockIdx.x == 0 && threadIdx.x == 0) *A.grand_total = base0 + *A.total;
     Counters ct;
-    // Two claims in flight: while item q is processed, the next item's
-    // worklist entry is already loaded and its tile metadata, list head and
-    // search constants are prefetched into L1 (items average a few chunks,
-    // so their dependent metadata loads would otherwise dominate).
     uint32_t q_claim = 0;
-    if (lane == 0) q_claim = atomicAdd(&A.ticket[2], 2u);
+    if (lane == 0) q_claim = atomicAdd(&A.ticket[2], 1u);
     uint32_t q = __shfl_sync(kFull, q_claim, 0);
-    uint32_t q1 = q + 1;
-    uint32_t item_n = q < n_work ? A.worklist[q] : 0u;
     while (q < n_work) {
         if (lane == 0) q_claim = atomicAdd(&A.ticket[2], 1u);
-        const uint32_t item = item_n;
-        item_n = q1 < n_work ? A.worklist[q1] : 0u;
+        const uint32_t item = A.worklist[q];
         const uint32_t t = item >> 4;
         const uint32_t p0 = (item & 15u) * kEmitSpan;
         const uint32_t cnt = min(A.tile_count[t] - p0, static_cast<uint32_t>(kEmitSpan));
         const unsigned long long base = base0 + A.tile_base[t] + p0;
         const uint16_t* list = A.scratch + static_cast<size_t>(t) * kTile + p0;
-        if (q1 < n_work && lane < 4) {  // prefetch the next item's metadata and constants
-            const uint32_t t1 = item_n >> 4;
-            const uint32_t s1 = t1 / A.tiles_per_search;
-            const void* ptr = lane == 0 ? static_cast<const void*>(&A.tile_count[t1])
-                            : lane == 1 ? static_cast<const void*>(&A.tile_base[t1])
-                            : lane == 2 ? static_cast<const void*>(search_const(A, s1))
-                                        : static_cast<const void*>(A.scratch + static_cast<size_t>(t1) * kTile +
-                                                                   (item_n & 15u) * kEmitSpan);
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
-        }
         if (base + cnt > A.capacity) {
             if (lane == 0) ++ct.overflow;
         } else {
@@ -852,8 +835,7 @@ __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
                 }
             }
         }
-        q = q1;
-        q1 = __shfl_sync(kFull, q_claim, 0);
+        q = __shfl_sync(kFull, q_claim, 0);
     }
     flush_counters(ct, A, lane);
 }
