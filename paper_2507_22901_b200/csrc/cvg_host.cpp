@@ -1438,6 +1438,133 @@ struct PinnedPairs {
     }
 };
 
+// ---- pipelined COUNTS / FIRST search -----------------------------------------
+// Per-pixel batches (cfg4: 8.3M searches) spend ~13 ms of host prep and
+// ~3 ms of read-back around ~230 ms of kernels.  Split into K search ranges:
+// range c+1 is built on the host while range c computes, and range c's
+// counts (+ first pairs) are read back on the copy stream while later
+// ranges compute.  Only range 0's prep and the last range's read-back stay
+// exposed.  Every result array is sized up front (n searches).
+int fixed_chunks(const cvg_search_desc* d) {
+    if (d->output == CVG_OUT_PAIRS || d->n_searches < (1 << 20)) return 1;
+    static const int forced = [] {
+        const char* e = std::getenv("CVG_PIPELINE_K");
+        return e ? std::atoi(e) : 0;
+    }();
+    return forced > 0 ? std::min(forced, d->n_searches) : 4;
+}
+
+int search_ranges_fixed(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, int K) {
+    const double t0 = now_ms();
+    const size_t n = static_cast<size_t>(d->n_searches);
+    const uint64_t cps = static_cast<uint64_t>(d->n_radii) * static_cast<uint64_t>(d->n_angles);
+    const bool first = d->output == CVG_OUT_FIRST;
+    r->n_searches = d->n_searches;
+    r->counts = static_cast<uint64_t*>(ctx->host.alloc(sizeof(uint64_t) * n));
+    if (first) {
+        r->first_idx = static_cast<uint32_t*>(ctx->host.alloc(4 * n));
+        r->first_codes = static_cast<uint8_t*>(ctx->host.alloc(6 * n));
+    }
+    auto* tails = static_cast<ChunkTail*>(ctx->host.alloc(sizeof(ChunkTail) * K));
+    if (!r->counts || !tails || (first && (!r->first_idx || !r->first_codes))) {
+        ctx->host.release(tails);
+        return fail(CVG_ENOMEM, "pinned host allocation failed");
+    }
+    std::vector<cvg_plan> plans(K);
+    std::vector<cudaEvent_t> kdone(K, nullptr);
+    const GridTables grid = make_grid_tables(d);
+    double prep = 0, h2d = 0, t_first_enqueued = 0;
+    int err = CVG_OK;
+    for (int c = 0; c < K && !err; ++c) {
+        const size_t lo = n * c / K, hi = n * (c + 1) / K;
+        cvg_search_desc sub = *d;
+        sub.n_searches = static_cast<int32_t>(hi - lo);
+        sub.target_rgb = d->target_rgb + 3 * lo;
+        sub.pattern_bits = d->pattern_bits + lo;
+        sub.v_th = d->v_th + lo;
+        sub.r_novib = d->r_novib + lo;
+        const double tb = now_ms();
+        err = plan_build_safe(ctx, &sub, &plans[c], &grid);
+        if (err) break;
+        prep += (plans[c].t_prep_end ? plans[c].t_prep_end : now_ms()) - tb;
+        h2d += plans[c].t_upload_end ? plans[c].t_upload_end - plans[c].t_prep_end : 0.0;
+        if (!ctx->events.empty()) {
+            kdone[c] = ctx->events.back();
+            ctx->events.pop_back();
+        } else if (cudaEventCreate(&kdone[c]) != cudaSuccess) {
+            err = fail(CVG_ECUDA, "event creation failed");
+            break;
+        }
+        err = plan_enqueue(&plans[c], ctx->stream);
+        if (err) break;
+        if (c == 0) t_first_enqueued = now_ms();
+        const cvg_plan& p = plans[c];
+        auto copy = [&]() -> int {
+            cudaStream_t cs = ctx->copy_stream;
+            CVG_CUDA(cudaEventRecord(kdone[c], ctx->stream));
+            CVG_CUDA(cudaStreamWaitEvent(cs, kdone[c], 0));
+            CVG_CUDA(cudaMemcpyAsync(r->counts + lo, p.args.counts, sizeof(uint64_t) * (hi - lo),
+                                     cudaMemcpyDeviceToHost, cs));
+            CVG_CUDA(cudaMemcpyAsync(&tails[c], p.args.stats, sizeof(ChunkTail), cudaMemcpyDeviceToHost, cs));
+            if (first) {
+                CVG_CUDA(cudaMemcpyAsync(r->first_idx + lo, p.args.first_idx, 4 * (hi - lo), cudaMemcpyDeviceToHost,
+                                         cs));
+                CVG_CUDA(cudaMemcpyAsync(r->first_codes + 6 * lo, p.args.first_codes, 6 * (hi - lo),
+                                         cudaMemcpyDeviceToHost, cs));
+            }
+            return CVG_OK;
+        };
+        err = copy();
+    }
+    const double t_enqueued = now_ms();
+    if (!err) {
+        const cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+        if (ce != cudaSuccess) err = cuda_fail(ce, "result read-back");
+    }
+    const double t1 = now_ms();
+    if (!err) {
+        cvg::Stats agg{};
+        float ratio_max = 0.f, kernel_ms = 0.f;
+        uint64_t in_bytes = 0;
+        for (int c = 0; c < K; ++c) {
+            const cvg::Stats& st = tails[c].st;
+            agg.band_repairs += st.band_repairs;
+            agg.code_repairs += st.code_repairs;
+            agg.audit_violations += st.audit_violations;
+            agg.class_mismatch += st.class_mismatch;
+            float ratio;
+            std::memcpy(&ratio, &st.audit_max_ratio_bits, sizeof(float));
+            ratio_max = std::max(ratio_max, ratio);
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, plans[c].ev0, plans[c].ev1) == cudaSuccess) kernel_ms += ms;
+            in_bytes += plans[c].input_bytes;
+        }
+        r->n_pairs = sum_counts(r->counts, n);
+        r->n_candidates = cps * n;
+        r->n_band_repairs = agg.band_repairs;
+        r->n_code_repairs = agg.code_repairs;
+        r->n_audit_violations = agg.audit_violations;
+        r->n_class_mismatch = agg.class_mismatch;
+        r->audit_max_ratio = ratio_max;
+        r->kernel_ms = kernel_ms;
+        r->h2d_bytes = in_bytes;
+        r->d2h_bytes = (sizeof(uint64_t) + (first ? 10 : 0)) * n + sizeof(ChunkTail) * K;
+        r->prep_ms = static_cast<float>(prep);
+        r->h2d_ms = static_cast<float>(h2d);
+        r->device_ms = static_cast<float>(t1 - t_first_enqueued);  // ranges after the first overlap their prep
+        r->d2h_ms = 0.f;                                               // overlapped except the last range's
+        r->total_ms = static_cast<float>(t1 - t0);
+        (void)t_enqueued;
+    }
+    cudaStreamSynchronize(ctx->stream);
+    for (int c = 0; c < K; ++c) {
+        if (kdone[c]) ctx->events.push_back(kdone[c]);
+        if (plans[c].ctx) plan_release(&plans[c]);
+    }
+    ctx->host.release(tails);
+    return err;
+}
+
 int search_pipelined(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, int K) {
     const double t0 = now_ms();
     const size_t n = static_cast<size_t>(d->n_searches);
@@ -1835,10 +1962,11 @@ int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out) {
     if (int e = validate_desc(desc)) return e;
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     if (int e = ensure_device(ctx)) return e;
-    if (const int K = pipeline_chunks(desc); K > 1) {
+    if (const int K = std::max(pipeline_chunks(desc), fixed_chunks(desc)); K > 1) {
         int e;
         try {
-            e = search_pipelined(ctx, desc, out, K);
+            e = desc->output == CVG_OUT_PAIRS ? search_pipelined(ctx, desc, out, K)
+                                              : search_ranges_fixed(ctx, desc, out, K);
         } catch (const std::bad_alloc&) {
             e = fail(CVG_ENOMEM, "host allocation failed");
         } catch (const std::exception& ex) {

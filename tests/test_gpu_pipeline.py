@@ -74,3 +74,27 @@ def test_pipelined_many_ranges_audit(ctx, oracle):
         a, b = int(res["offsets"][s]), int(res["offsets"][s + 1])
         oi, oc, _ = oracle.search(targets[s], int(pats[s]), vt[s], rn[s], radii, angles, method=1, want_deltas=False)
         assert np.array_equal(res["idx"][a:b], oi) and np.array_equal(res["codes"][a:b], oc), s
+
+
+@pytest.mark.parametrize("output", ["first", "counts"])
+def test_ranged_counts_first_equal_single_plans(ctx, output):
+    """Per-pixel-size COUNTS / FIRST batches (>= 2^20 searches) run as 4
+    search ranges whose prep and read-back overlap the kernels
+    (cvg_host.cpp search_ranges_fixed); results equal sub-batch single plans."""
+    rng = np.random.default_rng(31)
+    n = (1 << 20) + 12345
+    radii, angles = W.radii(8, 6.0), W.angles(64)
+    targets = rng.integers(0, 256, (n, 3)).astype(np.int32)
+    pats = rng.integers(1, 8, n).astype(np.int32)
+    vt = rng.choice([20.0, 50.0], n)
+    rn = np.full(n, 0.5)
+    got = ctx.search(targets, pats, vt, rn, radii, angles, output=output)
+    step = 1 << 18
+    for a in range(0, n, step):
+        want = ctx.search(targets[a:a + step], pats[a:a + step], vt[a:a + step], rn[a:a + step], radii, angles,
+                          output=output)
+        assert np.array_equal(got["counts"][a:a + step], want["counts"])
+        if output == "first":
+            assert np.array_equal(got["first_idx"][a:a + step], want["first_idx"])
+            assert np.array_equal(got["first_codes"][a:a + step], want["first_codes"])
+    assert got["n_pairs"] == int(got["counts"].sum())
