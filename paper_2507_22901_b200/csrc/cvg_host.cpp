@@ -12,6 +12,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <condition_variable>
 #include <functional>
@@ -995,10 +996,36 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     const std::vector<float>& trig_f = grid->trig_f;
     const std::vector<double>& trig_d = grid->trig_d;
 
-    // ---- one constant blob: [sc | sc_index | radii | trig | thresholds | guess] ----
+    // Claim order (band mode, more than one loud count in the batch): all
+    // tiles of the searches with one loud count, then the next, so the warps
+    // resident together run one band_row specialization (instruction cache).
+    std::vector<uint32_t> claim;
+    std::array<uint32_t, 3> group_end{};
+    static const bool group_claims = [] {
+        const char* e = std::getenv("CVG_CLAIM_GROUP");  // A/B switch; default on
+        return !e || std::atoi(e) != 0;
+    }();
+    if (group_claims && p->mode == cvg::kModeBand && p->n > 1) {
+        std::array<uint32_t, 4> bucket{};
+        for (int32_t i = 0; i < p->n; ++i) ++bucket[__builtin_popcount(d->pattern_bits[i] & 7)];
+        int kinds = 0;
+        for (uint32_t b : bucket) kinds += b > 0;
+        if (kinds > 1) {
+            // positions: loud count 1 first ([0, group_end[0])), then 2, then 3
+            group_end[0] = bucket[1];
+            group_end[1] = bucket[1] + bucket[2];
+            group_end[2] = bucket[1] + bucket[2] + bucket[3];
+            std::array<uint32_t, 4> next{0, 0, group_end[0], group_end[1]};
+            claim.resize(p->n);
+            for (int32_t i = 0; i < p->n; ++i) claim[next[__builtin_popcount(d->pattern_bits[i] & 7)]++] = i;
+        }
+    }
+
+    // ---- one constant blob: [sc | sc_index | claim | radii | trig | thresholds | guess] ----
     Layout L;
     const size_t o_sc = L.take(sizeof(SearchConst) * n_sc);
     const size_t o_si = L.take(sizeof(uint32_t) * sc_index.size());
+    const size_t o_co = L.take(sizeof(uint32_t) * claim.size());
     const size_t o_rd = L.take(sizeof(double) * p->nr);
     const size_t o_rf = L.take(sizeof(float) * p->nr);
     const size_t o_td = L.take(sizeof(double) * trig_d.size());
@@ -1026,6 +1053,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
             },
             1);
     }
+    if (!claim.empty()) std::memcpy(stage + o_co, claim.data(), sizeof(uint32_t) * claim.size());
     std::memcpy(stage + o_rd, d->radii, sizeof(double) * p->nr);
     std::memcpy(stage + o_rf, radii_f.data(), sizeof(float) * p->nr);
     std::memcpy(stage + o_td, trig_d.data(), sizeof(double) * trig_d.size());
@@ -1037,6 +1065,8 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     std::memset(&A, 0, sizeof(A));
     A.sc = at<const SearchConst>(p->d_const, o_sc);
     A.sc_index = sc_index.empty() ? nullptr : at<const uint32_t>(p->d_const, o_si);
+    A.claim_order = claim.empty() ? nullptr : at<const uint32_t>(p->d_const, o_co);
+    for (int g = 0; g < 3; ++g) A.group_end[g] = group_end[g];
     A.radii_d = at<const double>(p->d_const, o_rd);
     A.radii_f = at<const float>(p->d_const, o_rf);
     A.trig_d = at<const double>(p->d_const, o_td);
@@ -1130,6 +1160,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
 
     if (p->split) {
         unsigned long long* totals = at<unsigned long long>(p->d_work, o_ta);
+        A.claim_order = nullptr;  // range views claim in search order
         p->va = A;
         p->va.range_searches = n_a;
         p->va.n_tiles = tiles_a;

@@ -607,7 +607,31 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         // search's constants.  Tile t (search s, tile lt) keeps its storage
         // slot s * tps + lt either way.
         uint32_t s, lt;
-        if (A.tiles_per_search >= 16) {
+        if (A.claim_order) {
+            // group g of loud-count-sorted positions, outer-first inside it
+            const uint32_t tps = A.tiles_per_search;
+            uint32_t g0 = 0, g1 = A.group_end[0];
+            if (c >= g1 * tps) {
+                g0 = g1;
+                g1 = A.group_end[1];
+                if (c >= g1 * tps) {
+                    g0 = g1;
+                    g1 = A.group_end[2];
+                }
+            }
+            const uint32_t cl = c - g0 * tps, ng = g1 - g0;
+            uint32_t pos;
+            if (tps >= 16) {
+                const uint32_t q = cl / ng;
+                pos = g0 + (cl - q * ng);
+                lt = tps - 1 - q;
+            } else {
+                const uint32_t sr = cl / tps;
+                lt = cl - sr * tps;
+                pos = g0 + sr;
+            }
+            s = __ldg(&A.claim_order[pos]);
+        } else if (A.tiles_per_search >= 16) {
             const uint32_t q = c / A.range_searches;
             s = A.search_begin + (c - q * A.range_searches);
             lt = A.tiles_per_search - 1 - q;

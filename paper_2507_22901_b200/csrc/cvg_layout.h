@@ -65,6 +65,12 @@ enum Path : int { kPathFast = 0, kPathExact = 1, kPathAudit = 2 };
 struct LaunchArgs {
     const SearchConst* sc;     // [n_unique] per-search constant records
     const uint32_t* sc_index;  // [n_searches] record of each search, nullptr = identity
+    // Claim order (band mode, mixed patterns): claim_order[p] is the search at
+    // position p; positions [group_end[g-1], group_end[g]) hold the searches
+    // of one loud count, claimed group after group so that concurrently
+    // resident warps run one hot-loop specialization.  nullptr = identity.
+    const uint32_t* claim_order;
+    uint32_t group_end[3];
     const float* radii_f;      // [nr]
     const double* radii_d;     // [nr]
     const float* trig_f;       // [na][2] = (sin/500, cos/200) as float
