@@ -536,7 +536,9 @@ __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, 
     uint32_t ix = mb;
     const uint32_t iend = mb + 32u * (nch & ~1u);
     float2 na_ = __ldg(trig + ix), nb_ = __ldg(trig + ix + 32);
-#pragma unroll 1  // code size (an unrolled two-pair body measured 25% slower on cfg1/cfg3, 7% faster on cfg2)
+#pragma unroll 1  // code size: an unrolled two-pair body (ping-pong prefetch, no register
+                  // rotation) measured, with loud-count-major claims: cfg1 -1.4%, cfg3 +4.4%,
+                  // cfg2 +8%; without them 25% slower (instruction cache).  Kept rolled for cfg1.
     for (; ix != iend; ix += 64) {
         const float2 sa = na_, sb = nb_;
         na_ = __ldg(trig + ix + 64);  // prefetch; the table is padded by 128 entries
