@@ -73,7 +73,8 @@ def config_dict(wl, n, extra=None):
          "grid": f"{len(wl.radii)} radii x {len(wl.angles)} angles", "candidates_per_step": wl.candidates,
          "targets": {"cfg3": "16^3 lattice", "cfg4": "3840x2160 Voronoi image, one search per pixel"}.get(
              wl.name, "Table-1 colors"), "output": wl.output,
-         "parallelism": f"replicas{n}" if n > 1 else "single", "l2": "flushed between steps (256 MiB write)"}
+         "parallelism": f"dp{n} (each rank its own {wl.name}-sized batch, no data-path collective)" if n > 1
+         else "single", "l2": "flushed between steps (256 MiB write)"}
     if extra:
         d.update(extra)
     return d
@@ -194,7 +195,8 @@ def run_reference(args):
     warm = max(0, min(args.warmup, 2))
     v, sec, cores, pairs, path = cpu_reference_arm(wl, steps, warm)
     out = {
-        "metric": METRIC, "value": round(v, 6), "unit": UNIT, "n_gpus": 0, "steps": steps, "warmup": warm,
+        "metric": METRIC, "value": round(v, 6), "unit": UNIT, "n_gpus": world, "device": "cpu (host cores)",
+        "steps": steps, "warmup": warm,
         "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": config_dict(wl, 1, {"cpu": cpu_model(), "library": os.path.relpath(path, ROOT)}),
