@@ -1993,7 +1993,17 @@ int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out) {
     if (int e = validate_desc(desc)) return e;
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     if (int e = ensure_device(ctx)) return e;
-    if (const int K = std::max(pipeline_chunks(desc), fixed_chunks(desc)); K > 1) {
+    // A plan holds < 2^28 tiles (32-bit tile ids with 16 emit items each):
+    // larger batches always run as search ranges, each well under the limit.
+    int K_min = 1;
+    {
+        const uint64_t cps = static_cast<uint64_t>(desc->n_radii) * static_cast<uint64_t>(desc->n_angles);
+        const uint64_t tiles = (cps + cvg::kTile - 1) / cvg::kTile * static_cast<uint64_t>(desc->n_searches);
+        const uint64_t per_range = 1ull << 26;  // ramp ranges reach 2/(K+1) of the batch
+        if (tiles >= per_range) K_min = static_cast<int>(std::min<uint64_t>((tiles + per_range - 1) / per_range,
+                                                                             static_cast<uint64_t>(desc->n_searches)));
+    }
+    if (const int K = std::max({pipeline_chunks(desc), fixed_chunks(desc), K_min}); K > 1) {
         int e;
         try {
             e = desc->output == CVG_OUT_PAIRS ? search_pipelined(ctx, desc, out, K)
