@@ -221,6 +221,65 @@ def ncu_traffic(config="cfg1"):
         return None
 
 
+def time_gather(dist, plan, wl, n_pairs, world, stream, reps=5):
+    """The multi-GPU exchange step of SURVEY §8(e), timed apart from the
+    search (scaling is weak: no collective in the timed step): NCCL
+    all_gather of every rank's per-search counts, and (PAIRS) of its packed
+    pair records (u32 idx + 6 code bytes, padded to the largest rank).  Device
+    events around each collective, max over ranks.  The gathered counts are
+    checked against the local ones (every rank ran the same batch)."""
+    import torch
+
+    n = wl.n_searches
+    counts = torch.empty(n, dtype=torch.int64, device="cuda")
+    pairs = wl.output == "pairs"
+    idx = torch.empty(max(n_pairs, 1), dtype=torch.int32, device="cuda") if pairs else None
+    codes = torch.empty((max(n_pairs, 1), 6), dtype=torch.uint8, device="cuda") if pairs else None
+    plan.run(stream.cuda_stream)
+    plan.sync()
+    plan.copy_outputs(counts.data_ptr(), idx.data_ptr() if pairs else 0, codes.data_ptr() if pairs else 0,
+                      n_pairs if pairs else 0, stream.cuda_stream)
+    sizes = torch.tensor([n_pairs], dtype=torch.int64, device="cuda")
+    out_c = [torch.empty_like(counts) for _ in range(world)]
+
+    def timed(fn):
+        ms = []
+        for _ in range(reps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms.append(a.elapsed_time(b))
+        v = torch.tensor([statistics.median(ms)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        return float(v.item())
+
+    out = {"collective": "NCCL all_gather over NVLink", "counts_bytes_per_rank": 8 * n,
+           "counts_all_gather_ms": round(timed(lambda: dist.all_gather(out_c, counts)), 4)}
+    assert all(torch.equal(x, counts) for x in out_c), "gathered counts differ between ranks"
+    if pairs:
+        all_sizes = [torch.empty_like(sizes) for _ in range(world)]
+        dist.all_gather(all_sizes, sizes)
+        width = int(max(int(x.item()) for x in all_sizes))
+        rec = torch.zeros((max(width, 1), 10), dtype=torch.uint8, device="cuda")
+        rec[:n_pairs, :4] = idx[:n_pairs].view(torch.uint8).view(-1, 4)
+        rec[:n_pairs, 4:] = codes[:n_pairs]
+        out_r = [torch.empty_like(rec) for _ in range(world)]
+
+        def pairs_gather():
+            dist.all_gather(all_sizes, sizes)
+            dist.all_gather(out_r, rec)
+
+        out["pairs_bytes_per_rank"] = 10 * n_pairs
+        out["pairs_all_gather_ms"] = round(timed(pairs_gather), 4)
+        out["pairs_all_gather_gbs"] = round(10 * n_pairs * world / (out["pairs_all_gather_ms"] * 1e-3) / 1e9, 1)
+        assert all(torch.equal(x[:n_pairs], rec[:n_pairs]) for x in out_r)
+    return out
+
+
 def run_ours(args):
     import torch
 
@@ -304,14 +363,10 @@ def run_ours(args):
     phase_med = {k: round(statistics.median(p[k] for p in phases), 4) for k in phases[0]}
     e2e_s = sum(e2e_times)
     t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    gather = None
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        # verification gather (outside every timed region): per-search counts of all ranks
-        res = plan.fetch()
-        c = torch.tensor(res["counts"].astype(np.int64)[:65536], device="cuda")
-        allc = [torch.empty_like(c) for _ in range(world)]
-        dist.all_gather(allc, c)
-        assert all(torch.equal(x, allc[0]) for x in allc)
+        gather = time_gather(dist, plan, wl, n_pairs, world, stream)
     e2e_value = wl.candidates * world * e2e_steps / float(t.item()) / 1e9
 
     if rank != 0:
@@ -364,6 +419,7 @@ def run_ours(args):
                 "s_per_step": round(float(t.item()) / e2e_steps, 5), "steps": e2e_steps,
                 "api": "cvg_search (C-ABI host call)", "breakdown_ms": phase_med},
         "gpu_launches": plan.launches * args.steps,
+        **({"gather": gather} if gather else {}),
         "clocks": clk.summary(),
         "roofline": roofline,
         "cpu_baseline": cpu,

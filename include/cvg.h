@@ -149,6 +149,12 @@ CVG_API int cvg_plan_fetch(cvg_plan* plan, cvg_result* out);
 /* device pointers of the plan's outputs (valid until the plan is destroyed) */
 CVG_API int cvg_plan_device_outputs(cvg_plan* plan, uint64_t** counts, uint32_t** idx,
                                     uint8_t** codes, uint64_t* capacity);
+/* Copies the last run's per-search counts (u64, n_searches), pair idx (u32)
+ * and codes (6 B) -- n_pairs of each, as cvg_plan_sync reported -- into
+ * caller device buffers, enqueued on `stream` (NULL pointers skip an array).
+ * For collectives on framework tensors (e.g. NCCL all_gather of results). */
+CVG_API int cvg_plan_copy_outputs(cvg_plan* plan, uint64_t* counts, uint32_t* idx, uint8_t* codes,
+                                  uint64_t n_pairs, void* stream);
 /* device time (ms) of the search kernel(s) of the plan's last completed run */
 CVG_API int cvg_plan_last_kernel_ms(cvg_plan* plan, float* ms);
 /* per-kernel device time (ms) of the last run: phase 1 (candidate decisions),

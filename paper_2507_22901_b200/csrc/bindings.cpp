@@ -618,6 +618,13 @@ PYBIND11_MODULE(_core, m) {
             check(cvg_plan_last_kernel_ms(p.plan, &ms));
             return ms;
         })
+        .def("copy_outputs",
+             [](Plan& p, uintptr_t counts, uintptr_t idx, uintptr_t codes, uint64_t n_pairs, uintptr_t stream) {
+                 check(cvg_plan_copy_outputs(p.plan, reinterpret_cast<uint64_t*>(counts),
+                                             reinterpret_cast<uint32_t*>(idx), reinterpret_cast<uint8_t*>(codes),
+                                             n_pairs, reinterpret_cast<void*>(stream)));
+             },
+             py::arg("counts"), py::arg("idx"), py::arg("codes"), py::arg("n_pairs"), py::arg("stream") = 0)
         .def("device_outputs", [](Plan& p) {
             uint64_t* counts = nullptr;
             uint32_t* idx = nullptr;

@@ -1933,6 +1933,24 @@ int cvg_plan_fetch(cvg_plan* p, cvg_result* out) {
     return e;
 }
 
+int cvg_plan_copy_outputs(cvg_plan* p, uint64_t* counts, uint32_t* idx, uint8_t* codes, uint64_t n_pairs,
+                          void* stream) {
+    if (!p) return fail(CVG_EINVAL, "null plan");
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    if (int e = ensure_device(p->ctx)) return e;
+    if (p->empty) return CVG_OK;
+    if ((idx || codes) && (p->out != cvg::kOutPairs || n_pairs > p->capacity)) {
+        return fail(CVG_EINVAL, "n_pairs exceeds the plan's pair buffer (or not a PAIRS plan)");
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (counts) {
+        CVG_CUDA(cudaMemcpyAsync(counts, p->args.counts, sizeof(uint64_t) * p->n, cudaMemcpyDeviceToDevice, st));
+    }
+    if (idx && n_pairs) CVG_CUDA(cudaMemcpyAsync(idx, p->d_out_idx, 4 * n_pairs, cudaMemcpyDeviceToDevice, st));
+    if (codes && n_pairs) CVG_CUDA(cudaMemcpyAsync(codes, p->d_out_codes, 6 * n_pairs, cudaMemcpyDeviceToDevice, st));
+    return CVG_OK;
+}
+
 int cvg_plan_device_outputs(cvg_plan* p, uint64_t** counts, uint32_t** idx, uint8_t** codes, uint64_t* capacity) {
     if (!p) return fail(CVG_EINVAL, "null plan");
     if (counts) *counts = reinterpret_cast<uint64_t*>(p->args.counts);
