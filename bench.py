@@ -28,6 +28,7 @@ ranks device time.  `--impl reference` runs the reference CPU arm on rank 0.
 from __future__ import annotations
 
 import argparse
+import contextlib
 import json
 import os
 import statistics
@@ -55,6 +56,20 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
+
+
+@contextlib.contextmanager
+def stdout_to_stderr():
+    """Points file descriptor 1 at stderr for the duration (C-level prints too)."""
+    sys.stdout.flush()
+    saved = os.dup(1)
+    try:
+        os.dup2(2, 1)
+        yield
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
 
 
 def dist_env():
@@ -291,7 +306,9 @@ def run_ours(args):
     if world > 1 or "TORCHELASTIC_RUN_ID" in os.environ:  # under torchrun: NCCL even for one rank
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        with stdout_to_stderr():  # NCCL prints its version banner on stdout; the JSON line must stand alone
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()  # communicator is created here: keep its banner off stdout too
     wl = workload(args.config)
     ctx = cv.Context(local)
     stream = torch.cuda.current_stream()
