@@ -561,77 +561,17 @@ __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, 
     }
 }
 
-// COUNTS / FIRST hot loop: no list to build, so certain passes are counted
-// per lane without a vote (cnt) and the first passing offset is kept per
-// lane (first); only candidates whose FP32 decision is unsure (|G| <= eps)
-// vote into the FP64 repair.  Both are reduced over the warp per tile.
-template <int kL, bool kCubeOnly, int kOut>
-__device__ __forceinline__ void band_row_count(const SearchConst* S, const Consts& C, const LaunchArgs& A,
-                                               uint32_t k, float r, uint32_t m0, uint32_t nch, uint32_t off,
-                                               uint32_t& cnt, uint32_t& first, Counters& ct, unsigned lane) {
-    const float2* __restrict__ trig = reinterpret_cast<const float2*>(A.trig_f);
-    const uint32_t mb = m0 + lane;
-    const uint32_t off0 = off + lane - mb;  // candidate offset in the tile = off0 + ix
-    uint32_t ix = mb;
-    const uint32_t iend = mb + 32u * (nch & ~1u);
-    float2 na_ = __ldg(trig + ix), nb_ = __ldg(trig + ix + 32);
-    auto settle = [&](uint32_t x, bool unsure, bool pass) {
-        if (unsure) {
-            double lp[3], lm[3];
-            exact_linear(S, A, k, x, lp, lm);
-            pass = exact_band(S, lp, lm, C.flags);
-            ++ct.repairs;
-        }
-        return pass;
-    };
-#pragma unroll 1
-    for (; ix != iend; ix += 64) {
-        const float2 sa = na_, sb = nb_;
-        na_ = __ldg(trig + ix + 64);  // prefetch; the table is padded by 128 entries
-        nb_ = __ldg(trig + ix + 96);
-        float la_, qa_, lb_, qb_;
-        band_chunk<kL, kCubeOnly>(C, r, sa, la_, qa_);
-        band_chunk<kL, kCubeOnly>(C, r, sb, lb_, qb_);
-        bool pa = band_certain(C, la_, qa_), pb = band_certain(C, lb_, qb_);
-        const bool ua = band_attention(C, la_, qa_) & !pa, ub = band_attention(C, lb_, qb_) & !pb;
-        if (__any_sync(kFull, ua | ub)) {
-            pa = settle(ix, ua, pa);
-            pb = settle(ix + 32, ub, pb);
-        }
-        cnt += static_cast<uint32_t>(pa) + static_cast<uint32_t>(pb);
-        if (kOut == kOutFirst) {
-            first = min(first, pa ? off0 + ix : 0xffffffffu);
-            first = min(first, pb ? off0 + ix + 32 : 0xffffffffu);
-        }
-    }
-    if (nch & 1u) {
-        float la_, qa_;
-        band_chunk<kL, kCubeOnly>(C, r, na_, la_, qa_);
-        bool pa = band_certain(C, la_, qa_);
-        const bool ua = band_attention(C, la_, qa_) & !pa;
-        if (__any_sync(kFull, ua)) pa = settle(ix, ua, pa);
-        cnt += static_cast<uint32_t>(pa);
-        if (kOut == kOutFirst) first = min(first, pa ? off0 + ix : 0xffffffffu);
-    }
-}
-
 template <int kL, int kOut>
 __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t i0,
-                                          uint32_t i1, uint16_t* list, uint32_t& cnt, uint32_t* first,
-                                          uint32_t& lane_first, Counters& ct, unsigned lane, unsigned lane_lt) {
+                                          uint32_t i1, uint16_t* list, uint32_t& cnt, uint32_t* first, Counters& ct,
+                                          unsigned lane, unsigned lane_lt) {
     uint32_t k = div_na(i0, A);
     uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
     uint32_t i = i0;
     while (i < i1) {
         const uint32_t seg = min(i1 - i, static_cast<uint32_t>(A.na) - m0);
         const float r = __ldg(&A.radii_f[k]);
-        if (kOut != kOutPairs) {  // per-lane cnt / lane_first, reduced by the caller
-            if (r < C.rcube) {
-                band_row_count<kL, true, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, cnt, lane_first, ct, lane);
-            } else {
-                band_row_count<kL, false, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, cnt, lane_first, ct, lane);
-            }
-        } else if (r < C.rcube) {
+        if (r < C.rcube) {
             band_row<kL, true, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);
         } else {
             band_row<kL, false, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);
@@ -713,20 +653,12 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         load_consts(S, C);
         if (kMode == kModeBand && kPath == kPathFast && A.aligned) {
             const uint32_t nl = (C.flags >> 10) & 3u;
-            uint32_t lane_first = 0xffffffffu;
             if (nl == 3) {
-                band_tile<3, kOut>(S, C, A, i0, i1, list, cnt, first, lane_first, ct, lane, lane_lt);
+                band_tile<3, kOut>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
             } else if (nl == 2) {
-                band_tile<2, kOut>(S, C, A, i0, i1, list, cnt, first, lane_first, ct, lane, lane_lt);
+                band_tile<2, kOut>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
             } else {
-                band_tile<1, kOut>(S, C, A, i0, i1, list, cnt, first, lane_first, ct, lane, lane_lt);
-            }
-            if (kOut != kOutPairs) {  // per-lane tallies -> tile count / first
-                cnt = __reduce_add_sync(kFull, cnt);
-                if (kOut == kOutFirst) {
-                    const uint32_t f = __reduce_min_sync(kFull, lane_first);
-                    if (lane == 0 && cnt) *first = f;
-                }
+                band_tile<1, kOut>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
             }
         } else {
             CodeConsts CC;
