@@ -184,7 +184,8 @@ class Reference(_Lib):
 
 
 class RefCodec:
-    """The reference codec (codec.cpp) through oracle/ref_codec_shim.cpp."""
+    """The reference codec (codec.cpp) and feasibility sweep (feasibility.cpp)
+    through oracle/ref_codec_shim.cpp."""
 
     def __init__(self, path: str | None = None):
         path = path or os.path.join(HERE, "_ref", "libcolorvibe_ref_codec.so")
@@ -202,6 +203,24 @@ class RefCodec:
                                               C.c_double, C.c_double, C.c_char_p, C.c_int]
         self.lib.cvrc_report_json.argtypes = [C.c_int, C.c_int, C.c_int, _ip, _ip, _ip, C.POINTER(C.c_char_p),
                                               C.c_double, C.c_double, _ip, _ip, _dp, C.c_char_p, C.c_int]
+        self.lib.cvrf_config_roundtrip.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_char_p]
+        self.lib.cvrf_export.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_int]
+
+    def config_roundtrip(self, text: str):
+        """(config_to_json(config_from_json(text)), config_hash) of the reference."""
+        buf, h = C.create_string_buffer(1 << 22), C.create_string_buffer(32)
+        n = self.lib.cvrf_config_roundtrip(text.encode(), buf, len(buf), h)
+        if n < 0:
+            self._raise(-n)
+        return buf.value.decode(), h.value.decode()
+
+    def export(self, text: str, fmt: str = "csv", aggregated: bool = True) -> str:
+        """export_matrix of the reference's own feasibility_matrix (CPU)."""
+        buf = C.create_string_buffer(1 << 24)
+        n = self.lib.cvrf_export(text.encode(), int(fmt == "json"), int(aggregated), buf, len(buf))
+        if n < 0:
+            self._raise(-n)
+        return buf.value.decode()
 
     @staticmethod
     def _layout(xy, rgb, bits, names):

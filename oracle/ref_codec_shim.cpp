@@ -1,8 +1,9 @@
 // ref_codec_shim.cpp -- TEST INFRASTRUCTURE ONLY.
 //
-// extern "C" wrapper over the UNMODIFIED reference codec (src/codec.cpp,
-// with src/search.cpp, src/color.cpp, src/util.cpp), compiled where those
-// sources lie by oracle/Makefile into oracle/_ref/libcolorvibe_ref_codec.so.
+// extern "C" wrapper over the UNMODIFIED reference codec and feasibility
+// sweep (src/codec.cpp, src/feasibility.cpp, with src/search.cpp,
+// src/color.cpp, src/util.cpp), compiled where those sources lie by
+// oracle/Makefile into oracle/_ref/libcolorvibe_ref_codec.so.
 // Nothing from the reference is copied into this repo.  image.cpp is not
 // compiled (it needs libpng); the one Image member the codec calls,
 // Image::solid, is restated below from its declaration (image.hpp).
@@ -15,6 +16,7 @@
 #include <vector>
 
 #include "colorvibe/codec.hpp"
+#include "colorvibe/feasibility.hpp"
 #include "colorvibe/image.hpp"
 
 namespace colorvibe {
@@ -155,6 +157,36 @@ int cvrc_report_json(int bw, int bh, int n, const int32_t* xy, const int32_t* rg
     if (rc) return -1;
     if (static_cast<int>(s.size()) < cap) std::memcpy(out, s.c_str(), s.size() + 1);
     return static_cast<int>(s.size());
+}
+
+// ---- feasibility.cpp: config JSON round trip, hash, matrix exports ----
+int copy_out(const std::string& s, char* out, int cap) {
+    if (static_cast<int>(s.size()) < cap) std::memcpy(out, s.c_str(), s.size() + 1);
+    return static_cast<int>(s.size());
+}
+
+// config_to_json(config_from_json(text)) (+ config_hash into hash[17])
+int cvrf_config_roundtrip(const char* text, char* out, int cap, char* hash) {
+    std::string s, h;
+    const int rc = guarded([&] {
+        const SearchConfig cfg = config_from_json(text);
+        s = config_to_json(cfg);
+        h = config_hash(cfg);
+    });
+    if (rc) return -rc;
+    std::memcpy(hash, h.c_str(), h.size() + 1);
+    return copy_out(s, out, cap);
+}
+
+// export_matrix(feasibility_matrix(config_from_json(text)), format, aggregated)
+int cvrf_export(const char* text, int json_format, int aggregated, char* out, int cap) {
+    std::string s;
+    const int rc = guarded([&] {
+        const FeasibilityMatrix m = feasibility_matrix(config_from_json(text));
+        s = export_matrix(m, json_format ? ExportFormat::Json : ExportFormat::Csv, aggregated != 0);
+    });
+    if (rc) return -rc;
+    return copy_out(s, out, cap);
 }
 
 }  // extern "C"

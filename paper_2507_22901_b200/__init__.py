@@ -8,6 +8,11 @@ ChannelDeltas, ColorPair, DeltaMode, DeltaBasis) and functions
 serial_search, batch_search, channel_deltas, frame_deltas, classify_pair,
 select_best), backed by the fused sm_100a kernel in csrc/cvg_kernels.cu.
 
+The feasibility sweep (module.cpp:140-191): NamedColor, SearchConfig,
+FeasibilityCell, FeasibilityMatrix, AggregateMatrix, feasibility_matrix (all
+cells in one launch), aggregate_any, export_matrix, config_from_json /
+config_to_json / config_hash.
+
 The codec surface (module.cpp:216-296): Image, DisplayParams, BlockSpec,
 BlockLayout, FramePair, BlockStatus, BlockResult, make_testcard,
 embed_blocks, decode_blocks, layout_to_json, decode_report_json (+
@@ -37,6 +42,18 @@ except ImportError as _e:  # pragma: no cover - exercised only on a broken build
     ) from _e
 
 from ._core import (  # noqa: E402
+    AggregateMatrix,
+    FeasibilityCell,
+    FeasibilityMatrix,
+    NamedColor,
+    SearchConfig,
+    aggregate_any,
+    config_from_json,
+    config_hash,
+    config_to_json,
+    export_matrix,
+    feasibility_matrix,
+    matrix_filename,
     BitPattern,
     BlockLayout,
     BlockResult,
@@ -106,7 +123,9 @@ __all__ = [
     "BlockLayout", "BlockResult", "BlockSpec", "BlockStatus", "DisplayParams", "FramePair", "Image", "Layout", "Sidecar",
     "block_sums_device", "block_sums_host", "decode_blocks", "decode_report_json", "embed_blocks",
     "embed_blocks_opts", "layout_from_json", "layout_to_json", "make_testcard", "paint_blocks_device",
-    "paint_blocks_host",
+    "paint_blocks_host", "AggregateMatrix", "FeasibilityCell", "FeasibilityMatrix", "NamedColor", "SearchConfig",
+    "aggregate_any", "config_from_json", "config_hash", "config_to_json", "export_matrix", "feasibility_matrix",
+    "matrix_filename",
 ]
 
 __version__ = "0.1.0"

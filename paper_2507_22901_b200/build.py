@@ -38,6 +38,8 @@ HEADERS = [os.path.join(CSRC, h) for h in ("cvg_layout.h", "cvg_internal.h")] + 
     os.path.join(INCLUDE, "colorvibe", "image.hpp"),
     os.path.join(INCLUDE, "colorvibe", "codec.hpp"),
     os.path.join(CSRC, "colorvibe_detail.h"),
+    os.path.join(CSRC, "json_lite.h"),
+    os.path.join(INCLUDE, "colorvibe", "feasibility.hpp"),
 ]
 
 
@@ -76,6 +78,9 @@ def _objects() -> list[tuple[str, list[str], list[str], str | None]]:
         (o("colorvibe_api.o"), [src("colorvibe_api.cpp")] + HEADERS,
          ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + INCLUDE,
           "-c", src("colorvibe_api.cpp"), "-o", o("colorvibe_api.o")], None),
+        (o("feasibility_api.o"), [src("feasibility_api.cpp")] + HEADERS,
+         ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + INCLUDE,
+          "-c", src("feasibility_api.cpp"), "-o", o("feasibility_api.o")], None),
         (o("codec_api.o"), [src("codec_api.cpp")] + HEADERS,
          ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + INCLUDE,
           "-c", src("codec_api.cpp"), "-o", o("codec_api.o")], None),

@@ -13,6 +13,7 @@
 
 #include "../../include/cvg.h"
 #include "colorvibe/codec.hpp"
+#include "colorvibe/feasibility.hpp"
 #include "colorvibe/search.hpp"
 
 namespace py = pybind11;
@@ -358,6 +359,67 @@ PYBIND11_MODULE(_core, m) {
             py::arg("delta_basis") = 0, py::arg("white_point") = py::none());
 
     py::class_<ResultHolder, std::shared_ptr<ResultHolder>>(m, "_Result");
+
+    // ---- feasibility sweep (module.cpp:140-191; feasibility.hpp) ----
+    py::class_<NamedColor>(m, "NamedColor")
+        .def(py::init<std::string, SrgbColor>(), py::arg("name"), py::arg("rgb"))
+        .def_readwrite("name", &NamedColor::name)
+        .def_readwrite("rgb", &NamedColor::rgb);
+
+    py::class_<SearchConfig>(m, "SearchConfig")
+        .def(py::init(&SearchConfig::defaults))
+        .def_static("defaults", &SearchConfig::defaults)
+        .def_static("benchmark_defaults", &SearchConfig::benchmark_defaults)
+        .def_readwrite("colors", &SearchConfig::colors)
+        .def_readwrite("patterns", &SearchConfig::patterns)
+        .def_readwrite("v_th_values", &SearchConfig::v_th_values)
+        .def_readwrite("r_novib_values", &SearchConfig::r_novib_values)
+        .def_readwrite("grid", &SearchConfig::grid)
+        .def_readwrite("white_point", &SearchConfig::white_point)
+        .def_readwrite("delta_mode", &SearchConfig::delta_mode)
+        .def_readwrite("delta_basis", &SearchConfig::delta_basis)
+        .def_readwrite("workers", &SearchConfig::workers)
+        .def("validate", &SearchConfig::validate)
+        .def("options", &SearchConfig::options)
+        .def("combo_count", &SearchConfig::combo_count);
+    m.def("config_from_json", &config_from_json, py::arg("text"));
+    m.def("config_to_json", &config_to_json, py::arg("config"));
+    m.def("config_hash", &config_hash, py::arg("config"));
+
+    py::class_<FeasibilityCell>(m, "FeasibilityCell")
+        .def_readonly("color_index", &FeasibilityCell::color_index)
+        .def_readonly("pattern_index", &FeasibilityCell::pattern_index)
+        .def_readonly("v_th_index", &FeasibilityCell::v_th_index)
+        .def_readonly("r_novib_index", &FeasibilityCell::r_novib_index)
+        .def_readonly("feasible", &FeasibilityCell::feasible)
+        .def_readonly("pair_count", &FeasibilityCell::pair_count)
+        .def_readonly("best_pair", &FeasibilityCell::best_pair);
+
+    py::class_<FeasibilityMatrix>(m, "FeasibilityMatrix")
+        .def_readonly("config", &FeasibilityMatrix::config)
+        .def_readonly("cells", &FeasibilityMatrix::cells)
+        .def("cell", &FeasibilityMatrix::cell, py::arg("color"), py::arg("pattern"), py::arg("v_th"),
+             py::arg("r_novib"), py::return_value_policy::reference_internal);
+
+    py::class_<AggregateMatrix>(m, "AggregateMatrix")
+        .def_readonly("patterns", &AggregateMatrix::patterns)
+        .def_readonly("colors", &AggregateMatrix::colors)
+        .def("at", &AggregateMatrix::at, py::arg("pattern"), py::arg("color"));
+
+    m.def("feasibility_matrix", &feasibility_matrix, py::arg("config"), py::call_guard<py::gil_scoped_release>());
+    m.def("aggregate_any", &aggregate_any, py::arg("matrix"));
+    m.def(
+        "export_matrix",
+        [](const FeasibilityMatrix& mat, const std::string& format, bool aggregated) {
+            return export_matrix(mat, parse_export_format(format), aggregated);
+        },
+        py::arg("matrix"), py::arg("format") = "csv", py::arg("aggregated") = true);
+    m.def(
+        "matrix_filename",
+        [](const std::string& format, bool aggregated) {
+            return matrix_filename(parse_export_format(format), aggregated);
+        },
+        py::arg("format"), py::arg("aggregated"));
 
     // ---- codec (module.cpp:216-296; codec.hpp, image.hpp) ----
     py::class_<Image>(m, "Image", py::buffer_protocol())

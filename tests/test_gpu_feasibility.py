@@ -1,0 +1,80 @@
+"""The feasibility sweep on the GPU (feasibility.hpp): every cell in one
+batched launch, exports byte-identical to the reference's own
+feasibility_matrix + export_matrix (oracle/_ref, run on CPU here), and the
+reference's test_feasibility.cpp device cases."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CONFIGS = [
+    '{"version": 1}',
+    '{"version": 1, "delta_basis": "frame_diff"}',
+    '{"version": 1, "white_point": [0.9642, 1.0, 0.8251], "v_th": [20, 60.5], "r_novib": [0.3]}',
+    '{"version": 1, "delta_mode": "continuous", "v_th": [50], "r_novib": [0.5]}',
+    '{"version": 1, "grid": {"radius": {"min": 0, "max": 100, "step": 1}, '
+    '"angle_deg": {"min": 0, "max": 359, "step": 1}}}',
+]
+
+
+@pytest.mark.parametrize("text", CONFIGS)
+@pytest.mark.parametrize("fmt,aggregated", [("csv", True), ("json", True), ("csv", False), ("json", False)])
+def test_exports_match_reference(cv, ctx, ref_codec, text, fmt, aggregated):
+    m = cv.feasibility_matrix(cv.config_from_json(text))
+    assert cv.export_matrix(m, fmt, aggregated) == ref_codec.export(text, fmt, aggregated)
+
+
+def tiny(cv):  # test_feasibility.cpp:20-29
+    cfg = cv.SearchConfig.defaults()
+    cfg.colors = [cfg.colors[1], cfg.colors[5]]
+    cfg.patterns = [cv.BitPattern("101"), cv.BitPattern("010")]
+    cfg.v_th_values = [50.0]
+    cfg.r_novib_values = [0.5]
+    return cfg
+
+
+def test_cells_match_serial_reference(cv, ctx):  # test_feasibility.cpp:103-123
+    cfg = tiny(cv)
+    m = cv.feasibility_matrix(cfg)
+    assert len(m.cells) == cfg.combo_count()
+    th = cv.Thresholds(50.0, 0.5)
+    for ci in range(2):
+        for pi in range(2):
+            oracle = cv.serial_search(cfg.colors[ci].rgb, cfg.grid, cfg.patterns[pi], th)
+            cell = m.cell(ci, pi, 0, 0)
+            assert cell.feasible == bool(oracle) and cell.pair_count == len(oracle)
+            assert (cell.best_pair is not None) == cell.feasible
+            if cell.best_pair is not None:
+                assert cell.best_pair == cv.select_best(oracle, th)
+
+
+def test_aggregate_is_or_over_thresholds(cv, ctx):  # test_feasibility.cpp:125-141
+    m = cv.feasibility_matrix(cv.SearchConfig.defaults())
+    agg = cv.aggregate_any(m)
+    assert len(agg.patterns) == 7 and len(agg.colors) == 9
+    for pi in range(7):
+        for ci in range(9):
+            assert agg.at(pi, ci) == any(m.cell(ci, pi, vi, ri).feasible for vi in range(4) for ri in range(3))
+
+
+def test_aggregated_export_golden_and_deterministic(cv, ctx):  # test_feasibility.cpp:143-154
+    from cvtest_util import golden
+
+    m = cv.feasibility_matrix(cv.SearchConfig.defaults())
+    csv = cv.export_matrix(m, "csv", True)
+    assert csv == golden("matrix_aggregated.csv")
+    m2 = cv.feasibility_matrix(cv.SearchConfig.defaults())
+    assert cv.export_matrix(m2, "csv", True) == csv
+    assert cv.export_matrix(m2, "json", True) == cv.export_matrix(m, "json", True)
+
+
+def test_full_export_rows(cv, ctx):  # test_feasibility.cpp:156-164
+    cfg = tiny(cv)
+    csv = cv.export_matrix(cv.feasibility_matrix(cfg), "csv", False)
+    assert csv.count("\n") == cfg.combo_count() + 1
+    assert csv.startswith("color,pattern,v_th,r_novib,feasible,pair_count")
+
+
+def test_benchmark_defaults_total(cv, ctx):
+    m = cv.feasibility_matrix(cv.SearchConfig.benchmark_defaults())
+    assert sum(c.pair_count for c in m.cells) == 408364  # SURVEY §6, run_benchmark parity pass
