@@ -28,6 +28,20 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # contraction in host code, so host-side tables carry the reference's bits.
 HOST_FP = ["-ffp-contract=off", "-fno-math-errno", "-fno-trapping-math"]
 
+# nlohmann json (header only, MIT) from the venv's cudnn_frontend copy: its
+# float formatter makes our JSON text match the reference's digit for digit
+# (json_lite.h falls back to shortest round-trip digits without it).
+def _nlohmann_dir() -> str | None:
+    for base in sysconfig.get_paths()["purelib"], sysconfig.get_paths()["platlib"]:
+        d = os.path.join(base, "include", "cudnn_frontend", "thirdparty", "nlohmann")
+        if os.path.exists(os.path.join(d, "json.hpp")):
+            return d
+    return None
+
+
+NLOHMANN = _nlohmann_dir()
+JSON_INC = ["-I" + NLOHMANN] if NLOHMANN else []
+
 LIB = os.path.join(PKG, "libcolorvibe_gpu.so")
 EXT = os.path.join(PKG, "_core" + sysconfig.get_config_var("EXT_SUFFIX"))
 
@@ -79,10 +93,10 @@ def _objects() -> list[tuple[str, list[str], list[str], str | None]]:
          ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + INCLUDE,
           "-c", src("colorvibe_api.cpp"), "-o", o("colorvibe_api.o")], None),
         (o("feasibility_api.o"), [src("feasibility_api.cpp")] + HEADERS,
-         ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + INCLUDE,
+         ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + INCLUDE, *JSON_INC,
           "-c", src("feasibility_api.cpp"), "-o", o("feasibility_api.o")], None),
         (o("codec_api.o"), [src("codec_api.cpp")] + HEADERS,
-         ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + INCLUDE,
+         ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + INCLUDE, *JSON_INC,
           "-c", src("codec_api.cpp"), "-o", o("codec_api.o")], None),
     ]
 

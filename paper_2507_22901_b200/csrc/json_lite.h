@@ -17,6 +17,15 @@
 #include <utility>
 #include <vector>
 
+// Float text: nlohmann's own Grisu2 (detail::to_chars) when its header is on
+// the include path (build.py adds the copy in the venv's cudnn_frontend), so
+// the digits match the reference even where Grisu2 is not shortest;
+// otherwise the shortest round-trip digits in the same layout.
+#if __has_include(<json.hpp>)
+#include <json.hpp>
+#define CVG_HAVE_NLOHMANN_TO_CHARS 1
+#endif
+
 namespace colorvibe::json {
 
 struct Json;
@@ -172,6 +181,13 @@ inline std::string get_string(const Json& j) {
 // layout (plain decimal for exponents in (-4, 15], else d.ddde+XX).
 inline std::string float_text(double v) {
     if (!std::isfinite(v)) return "null";
+#ifdef CVG_HAVE_NLOHMANN_TO_CHARS
+    {
+        char nb[64];
+        char* end = nlohmann::detail::to_chars(nb, nb + sizeof(nb), v);
+        return std::string(nb, end);
+    }
+#endif
     if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
     char buf[64];
     int prec = 0;
