@@ -43,6 +43,9 @@ except ImportError as _e:  # pragma: no cover - exercised only on a broken build
 
 from ._core import (  # noqa: E402
     AggregateMatrix,
+    BenchReport,
+    bench_report_json,
+    run_benchmark,
     FeasibilityCell,
     FeasibilityMatrix,
     NamedColor,
@@ -125,7 +128,7 @@ __all__ = [
     "embed_blocks_opts", "layout_from_json", "layout_to_json", "make_testcard", "paint_blocks_device",
     "paint_blocks_host", "AggregateMatrix", "FeasibilityCell", "FeasibilityMatrix", "NamedColor", "SearchConfig",
     "aggregate_any", "config_from_json", "config_hash", "config_to_json", "export_matrix", "feasibility_matrix",
-    "matrix_filename",
+    "matrix_filename", "BenchReport", "bench_report_json", "run_benchmark",
 ]
 
 __version__ = "0.1.0"

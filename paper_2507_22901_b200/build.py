@@ -54,6 +54,7 @@ HEADERS = [os.path.join(CSRC, h) for h in ("cvg_layout.h", "cvg_internal.h")] + 
     os.path.join(CSRC, "colorvibe_detail.h"),
     os.path.join(CSRC, "json_lite.h"),
     os.path.join(INCLUDE, "colorvibe", "feasibility.hpp"),
+    os.path.join(INCLUDE, "colorvibe", "bench.hpp"),
 ]
 
 

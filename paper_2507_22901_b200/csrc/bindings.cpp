@@ -12,6 +12,7 @@
 #include <stdexcept>
 
 #include "../../include/cvg.h"
+#include "colorvibe/bench.hpp"
 #include "colorvibe/codec.hpp"
 #include "colorvibe/feasibility.hpp"
 #include "colorvibe/search.hpp"
@@ -420,6 +421,23 @@ PYBIND11_MODULE(_core, m) {
             return matrix_filename(parse_export_format(format), aggregated);
         },
         py::arg("format"), py::arg("aggregated"));
+
+    py::class_<BenchReport>(m, "BenchReport")  // module.cpp:193-212
+        .def_readonly("config_hash", &BenchReport::config_hash)
+        .def_readonly("combos", &BenchReport::combos)
+        .def_readonly("candidates", &BenchReport::candidates)
+        .def_readonly("pairs_found", &BenchReport::pairs_found)
+        .def_readonly("repetitions", &BenchReport::repetitions)
+        .def_readonly("workers", &BenchReport::workers)
+        .def_readonly("serial_seconds", &BenchReport::serial_seconds)
+        .def_readonly("batch_seconds", &BenchReport::batch_seconds)
+        .def_readonly("batch_single_seconds", &BenchReport::batch_single_seconds)
+        .def_readonly("speedup", &BenchReport::speedup)
+        .def_readonly("speedup_single", &BenchReport::speedup_single)
+        .def_readonly("result_parity", &BenchReport::result_parity);
+    m.def("run_benchmark", &run_benchmark, py::arg("config"), py::arg("repetitions") = 3,
+          py::call_guard<py::gil_scoped_release>());
+    m.def("bench_report_json", &bench_report_json, py::arg("report"));
 
     // ---- codec (module.cpp:216-296; codec.hpp, image.hpp) ----
     py::class_<Image>(m, "Image", py::buffer_protocol())

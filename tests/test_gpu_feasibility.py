@@ -78,3 +78,37 @@ def test_full_export_rows(cv, ctx):  # test_feasibility.cpp:156-164
 def test_benchmark_defaults_total(cv, ctx):
     m = cv.feasibility_matrix(cv.SearchConfig.benchmark_defaults())
     assert sum(c.pair_count for c in m.cells) == 408364  # SURVEY §6, run_benchmark parity pass
+
+
+def bench_config(cv):  # test_bench.cpp:11-20
+    cfg = cv.SearchConfig.defaults()
+    cfg.colors = [cfg.colors[1]]
+    cfg.patterns = [cv.BitPattern("101"), cv.BitPattern("111")]
+    cfg.v_th_values = [50.0]
+    cfg.r_novib_values = [0.5]
+    cfg.grid = cv.VibrationGrid.uniform(1.0, 61.0, 20.0, 0.0, 315.0, 45.0)
+    return cfg
+
+
+def test_benchmark_small_workload(cv, ctx):  # test_bench.cpp:23-49
+    import json
+
+    cfg = bench_config(cv)
+    r = cv.run_benchmark(cfg, 2)
+    assert r.result_parity and r.combos == cfg.combo_count() and r.candidates == cfg.grid.candidate_count()
+    assert r.repetitions == 2 and r.workers >= 1
+    assert r.serial_seconds > 0 and r.batch_seconds > 0 and r.batch_single_seconds > 0
+    assert r.speedup == r.serial_seconds / r.batch_seconds
+    assert r.config_hash == cv.config_hash(cfg)
+    found = sum(len(cv.serial_search(cfg.colors[0].rgb, cfg.grid, p, cv.Thresholds(50.0, 0.5))) for p in cfg.patterns)
+    assert r.pairs_found == found
+    with pytest.raises(ValueError):
+        cv.run_benchmark(cfg, 0)
+    j = json.loads(cv.bench_report_json(r))
+    assert j["version"] == 1 and j["combos"] == r.combos and j["candidates_per_combo"] == r.candidates
+    assert j["result_parity"] is True and j["config_hash"] == r.config_hash
+
+
+def test_benchmark_defaults_parity_pass(cv, ctx):  # run_benchmark(benchmark_defaults) = 408,364
+    r = cv.run_benchmark(cv.SearchConfig.benchmark_defaults(), 1)
+    assert r.result_parity and r.pairs_found == 408364
