@@ -45,7 +45,7 @@ JSON_INC = ["-I" + NLOHMANN] if NLOHMANN else []
 LIB = os.path.join(PKG, "libcolorvibe_gpu.so")
 EXT = os.path.join(PKG, "_core" + sysconfig.get_config_var("EXT_SUFFIX"))
 
-HEADERS = [os.path.join(CSRC, h) for h in ("cvg_layout.h", "cvg_internal.h")] + [
+HEADERS = [os.path.join(CSRC, h) for h in ("cvg_layout.h", "cvg_internal.h", "cvg_host.h")] + [
     os.path.join(INCLUDE, "cvg.h"),
     os.path.join(INCLUDE, "colorvibe", "color.hpp"),
     os.path.join(INCLUDE, "colorvibe", "search.hpp"),
@@ -87,9 +87,10 @@ def _objects() -> list[tuple[str, list[str], list[str], str | None]]:
          [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xptxas", "-v", "-Xcompiler", "-fPIC",
           "-I" + INCLUDE, "-c", src("cvg_codec.cu"), "-o", o("cvg_codec.o")],
          o("ptxas_codec.log")),
-        (o("cvg_host.o"), [src("cvg_host.cpp")] + HEADERS,
-         ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + CUDA_INC, "-I" + INCLUDE,
-          "-c", src("cvg_host.cpp"), "-o", o("cvg_host.o")], None),
+        *[(o(f"{name}.o"), [src(f"{name}.cpp")] + HEADERS,
+           ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + CUDA_INC, "-I" + INCLUDE,
+            "-c", src(f"{name}.cpp"), "-o", o(f"{name}.o")], None)
+          for name in ("cvg_prep", "cvg_plan", "cvg_search", "cvg_codec_host")],
         (o("colorvibe_api.o"), [src("colorvibe_api.cpp")] + HEADERS,
          ["g++", "-std=c++20", "-O2", "-fPIC", *HOST_FP, "-Wall", "-I" + INCLUDE,
           "-c", src("colorvibe_api.cpp"), "-o", o("colorvibe_api.o")], None),

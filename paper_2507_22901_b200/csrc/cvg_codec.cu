@@ -7,7 +7,7 @@
 // chunks with every warp access coalesced, keep per-byte work to a few
 // integer instructions, and size their grids in multiples of the SM count.
 //
-// The host validates the layout (bounds, no overlaps: cvg_host.cpp
+// The host validates the layout (bounds, no overlaps: cvg_codec_host.cpp
 // layout_spans) and uploads the block positions and packed colors
 // (r | g << 8 | b << 16); the kernels address pixels by byte offset: the
 // pixel (x, y) occupies bytes 3 (y W + x) .. +2, so byte offset o is channel

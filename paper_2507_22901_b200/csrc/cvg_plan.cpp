@@ -1,0 +1,914 @@
+// cvg_plan.cpp -- plans (build once, run many) and the context, plan and
+// scalar parts of the C-ABI (include/cvg.h).
+#include "cvg_host.h"
+
+namespace cvg::host {
+
+thread_local std::string g_error;
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+int fail(int code, const std::string& msg) {
+    g_error = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(CVG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int ensure_device(cvg_ctx* ctx) {
+    CVG_CUDA(cudaSetDevice(ctx->device));
+    return CVG_OK;
+}
+
+void plan_free_outputs(cvg_plan* p) {
+    p->ctx->dev.release(p->d_out_idx);
+    p->ctx->dev.release(p->d_out_codes);
+    p->d_out_idx = p->d_out_codes = nullptr;
+    p->capacity = 0;
+}
+
+int plan_reserve(cvg_plan* p, uint64_t cap) {
+    if (p->out != cvg::kOutPairs || p->empty) return CVG_OK;
+    if (cap == 0) cap = 1;
+    if (cap == p->capacity && p->d_out_idx) return CVG_OK;
+    plan_free_outputs(p);
+    p->d_out_idx = p->ctx->dev.alloc(cap * sizeof(uint32_t));
+    p->d_out_codes = p->ctx->dev.alloc(cap * 6);
+    if (!p->d_out_idx || !p->d_out_codes) {
+        plan_free_outputs(p);
+        return fail(CVG_ENOMEM, "device allocation of the pair buffer failed");
+    }
+    p->capacity = cap;
+    p->args.out_idx = static_cast<uint32_t*>(p->d_out_idx);
+    p->args.out_codes = static_cast<uint8_t*>(p->d_out_codes);
+    p->args.capacity = cap;
+    return CVG_OK;
+}
+
+// Bump layout of several arrays inside one allocation (256-byte aligned).
+struct Layout {
+    size_t off = 0;
+    size_t take(size_t bytes) {
+        off = (off + 255) & ~size_t(255);
+        const size_t o = off;
+        off += bytes;
+        return o;
+    }
+};
+
+template <typename T>
+T* at(void* base, size_t off) {
+    return reinterpret_cast<T*>(static_cast<unsigned char*>(base) + off);
+}
+
+// sc_index[s] -> record of search s; uniq[u] -> first search with record u.
+// sc_index stays empty when every search is distinct (identity mapping).
+void dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, std::vector<int32_t>& uniq) {
+    const int n = d->n_searches;
+    sc_index.clear();
+    uniq.clear();
+    if (n <= 0) return;
+    // uniform classifier? (chunked so the 8M-search screen runs on all cores)
+    const size_t parts = n >= (1 << 20) ? 64 : 1;
+    std::vector<char> same(parts, 1);
+    parallel_for(
+        parts,
+        [&](size_t c) {
+            const size_t lo = std::max<size_t>(1, n * c / parts), hi = n * (c + 1) / parts;
+            const int32_t b0 = d->pattern_bits[0];
+            const double v0 = d->v_th[0], r0 = d->r_novib[0];
+            bool ok = true;
+            for (size_t s = lo; s < hi; ++s) {
+                ok &= (d->pattern_bits[s] == b0) & (d->v_th[s] == v0) & (d->r_novib[s] == r0);
+            }
+            same[c] = ok;
+        },
+        1);
+    bool uniform = true;
+    for (char c : same) uniform = uniform && c;
+    auto key24 = [&](size_t s) {
+        const int32_t* t = d->target_rgb + 3 * s;
+        return static_cast<uint32_t>(t[0]) << 16 | static_cast<uint32_t>(t[1]) << 8 | static_cast<uint32_t>(t[2]);
+    };
+    sc_index.resize(n);
+    if (uniform && n > 4096) {
+        // Same classifier everywhere: records keyed by the 24-bit color.
+        // Presence bitmap over the 2^24 colors (2 MB) + per-word rank, so the
+        // record id of a color is rank(color): no table to clear, cache-resident.
+        // Both passes run chunked over all cores; the representative of a
+        // record is its first search (atomic min), so the result is
+        // independent of the thread count.
+        std::vector<uint64_t> bits(1u << 18, 0);
+        const size_t chunks = n >= (1 << 20) ? 64 : 1;
+        parallel_for(
+            chunks,
+            [&](size_t c) {
+                for (size_t s = n * c / chunks; s < n * (c + 1) / chunks; ++s) {
+                    const uint32_t k = key24(s);
+                    const uint64_t m = 1ull << (k & 63);
+                    if (!(__atomic_load_n(&bits[k >> 6], __ATOMIC_RELAXED) & m)) {
+                        __atomic_fetch_or(&bits[k >> 6], m, __ATOMIC_RELAXED);
+                    }
+                }
+            },
+            1);
+        std::vector<uint32_t> rank(1u << 18);
+        uint32_t acc = 0;
+        for (size_t w = 0; w < bits.size(); ++w) {
+            rank[w] = acc;
+            acc += static_cast<uint32_t>(__builtin_popcountll(bits[w]));
+        }
+        uniq.assign(acc, INT32_MAX);
+        parallel_for(
+            chunks,
+            [&](size_t c) {
+                for (size_t s = n * c / chunks; s < n * (c + 1) / chunks; ++s) {
+                    const uint32_t k = key24(s);
+                    const uint32_t id = rank[k >> 6] +
+                                        static_cast<uint32_t>(__builtin_popcountll(bits[k >> 6] & ((1ull << (k & 63)) - 1)));
+                    sc_index[s] = id;
+                    int32_t cur = __atomic_load_n(&uniq[id], __ATOMIC_RELAXED);
+                    const int32_t me = static_cast<int32_t>(s);
+                    while (me < cur &&
+                           !__atomic_compare_exchange_n(&uniq[id], &cur, me, true, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
+                    }
+                }
+            },
+            1);
+    } else {
+        struct Key {
+            uint32_t rgb;
+            int32_t bits;
+            double v, r;
+            bool operator==(const Key& o) const {
+                return rgb == o.rgb && bits == o.bits && std::memcmp(&v, &o.v, 8) == 0 &&
+                       std::memcmp(&r, &o.r, 8) == 0;
+            }
+        };
+        struct Hash {
+            size_t operator()(const Key& k) const {
+                uint64_t a, b;
+                std::memcpy(&a, &k.v, 8);
+                std::memcpy(&b, &k.r, 8);
+                uint64_t h = (static_cast<uint64_t>(k.rgb) << 3 | static_cast<uint64_t>(k.bits)) * 0x9E3779B97F4A7C15ull;
+                h ^= a + 0x632BE59BD9B4E019ull + (h << 6) + (h >> 2);
+                h ^= b + 0x85157AF5ull + (h << 6) + (h >> 2);
+                return static_cast<size_t>(h);
+            }
+        };
+        std::unordered_map<Key, int32_t, Hash> seen;
+        seen.reserve(static_cast<size_t>(n) * 2);
+        for (int s = 0; s < n; ++s) {
+            const Key k{key24(static_cast<size_t>(s)), d->pattern_bits[s], d->v_th[s], d->r_novib[s]};
+            auto [it, fresh] = seen.emplace(k, static_cast<int32_t>(uniq.size()));
+            if (fresh) uniq.push_back(s);
+            sc_index[s] = static_cast<uint32_t>(it->second);
+        }
+    }
+    if (static_cast<int>(uniq.size()) == n) {
+        sc_index.clear();  // all distinct: records are in search order
+    }
+}
+
+GridTables make_grid_tables(const cvg_search_desc* d) {
+    GridTables g;
+    g.radii_f.resize(d->n_radii);
+    for (int k = 0; k < d->n_radii; ++k) g.radii_f[k] = static_cast<float>(d->radii[k]);
+    // float trig table padded by 128 entries: the hot loop prefetches two chunks ahead
+    g.trig_f.assign(2 * (static_cast<size_t>(d->n_angles) + 128), 0.0f);
+    g.trig_d.resize(2 * static_cast<size_t>(d->n_angles));
+    for (int j = 0; j < d->n_angles; ++j) {  // search.cpp:414-419
+        const double sn = std::sin(d->angles[j]);
+        const double cs = std::cos(d->angles[j]);
+        g.trig_d[2 * j] = sn;
+        g.trig_d[2 * j + 1] = cs;
+        g.trig_f[2 * j] = static_cast<float>(sn * kInv500);
+        g.trig_f[2 * j + 1] = static_cast<float>(cs * kInv200);
+    }
+    return g;
+}
+
+int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTables* grid = nullptr,
+               const SearchConst* pre = nullptr) {
+    const Tables& T = tables();
+    p->ctx = ctx;
+    // TargetSwing (quantized or continuous) is a per-endpoint interval test:
+    // band mode.  Quantized FrameDiff classifies on the codes of both endpoints.
+    p->mode = d->delta_basis == CVG_BASIS_TARGET_SWING ? cvg::kModeBand : cvg::kModeCodes;
+    p->out = d->output;
+    p->path = d->path;
+    p->n = d->n_searches;
+    p->nr = d->n_radii;
+    p->na = d->n_angles;
+    const uint64_t cps = static_cast<uint64_t>(p->nr) * static_cast<uint64_t>(p->na);
+    p->candidates = cps * static_cast<uint64_t>(p->n);
+    p->empty = p->candidates == 0;
+    if (p->empty) return CVG_OK;  // search.cpp:409-411
+
+    const uint32_t tps = static_cast<uint32_t>((cps + cvg::kTile - 1) / cvg::kTile);
+    const uint64_t n_tiles = static_cast<uint64_t>(tps) * static_cast<uint64_t>(p->n);
+    if (n_tiles >= (1ull << 28)) return fail(CVG_EINVAL, "batch too large for one plan (split the searches)");
+
+    // ---- host tables ----
+    // Per-search constants, deduplicated: searches with the same (target,
+    // pattern, v_th, r_novib) share one record (per-pixel batches repeat
+    // colors); every candidate of every search is still evaluated.
+    std::vector<uint32_t> sc_index;
+    std::vector<SearchConst> sc_own;
+    const SearchConst* sc_ptr = pre;  // one record per search, built by the caller
+    size_t n_sc = static_cast<size_t>(p->n);
+    if (!pre) {
+        std::vector<int32_t> uniq;  // representative search of each record
+        dedup_searches(d, sc_index, uniq);
+        sc_own.resize(uniq.size());
+        const double rmax = d->radii[p->nr - 1];
+        parallel_for(uniq.size(), [&](size_t u) { make_search_const(d, uniq[u], rmax, p->mode, T, sc_own[u]); });
+        sc_ptr = sc_own.data();
+        n_sc = sc_own.size();
+    }
+    p->n_unique = static_cast<int32_t>(n_sc);
+    GridTables own;
+    if (!grid) {
+        own = make_grid_tables(d);
+        grid = &own;
+    }
+    const std::vector<float>& radii_f = grid->radii_f;
+    const std::vector<float>& trig_f = grid->trig_f;
+    const std::vector<double>& trig_d = grid->trig_d;
+
+    // Claim order (band mode, more than one loud count in the batch): all
+    // tiles of the searches with one loud count, then the next, so the warps
+    // resident together run one band_row specialization (instruction cache).
+    std::vector<uint32_t> claim;
+    std::array<uint32_t, 3> group_end{};
+    static const bool group_claims = [] {
+        const char* e = std::getenv("CVG_CLAIM_GROUP");  // A/B switch; default on
+        return !e || std::atoi(e) != 0;
+    }();
+    if (group_claims && p->mode == cvg::kModeBand && p->n > 1) {
+        std::array<uint32_t, 4> bucket{};
+        for (int32_t i = 0; i < p->n; ++i) ++bucket[__builtin_popcount(d->pattern_bits[i] & 7)];
+        int kinds = 0;
+        for (uint32_t b : bucket) kinds += b > 0;
+        if (kinds > 1) {
+            // positions: loud count 1 first ([0, group_end[0])), then 2, then 3
+            group_end[0] = bucket[1];
+            group_end[1] = bucket[1] + bucket[2];
+            group_end[2] = bucket[1] + bucket[2] + bucket[3];
+            std::array<uint32_t, 4> next{0, 0, group_end[0], group_end[1]};
+            claim.resize(p->n);
+            for (int32_t i = 0; i < p->n; ++i) claim[next[__builtin_popcount(d->pattern_bits[i] & 7)]++] = i;
+        }
+    }
+
+    // ---- one constant blob: [sc | sc_index | claim | radii | trig | thresholds | guess] ----
+    Layout L;
+    const size_t o_sc = L.take(sizeof(SearchConst) * n_sc);
+    const size_t o_si = L.take(sizeof(uint32_t) * sc_index.size());
+    const size_t o_co = L.take(sizeof(uint32_t) * claim.size());
+    const size_t o_rd = L.take(sizeof(double) * p->nr);
+    const size_t o_rf = L.take(sizeof(float) * p->nr);
+    const size_t o_td = L.take(sizeof(double) * trig_d.size());
+    const size_t o_tf = L.take(sizeof(float) * trig_f.size());
+    const size_t o_thd = L.take(sizeof(double) * 256);
+    const size_t o_thf = L.take(sizeof(float) * 256 * 4);
+    const size_t o_gs = L.take(cvg::kGuessBuckets + 1);
+    const size_t bytes = L.off;
+    p->input_bytes = bytes;
+    p->t_prep_end = now_ms();
+    unsigned char* stage = static_cast<unsigned char*>(ctx->host.alloc(bytes));
+    p->d_const = ctx->dev.alloc(bytes);
+    if (!stage || !p->d_const) {
+        ctx->host.release(stage);
+        return fail(CVG_ENOMEM, "allocation of the search tables failed");
+    }
+    std::memcpy(stage + o_sc, sc_ptr, sizeof(SearchConst) * n_sc);
+    if (!sc_index.empty()) {
+        const size_t m = sc_index.size(), parts = m >= (1u << 20) ? 16 : 1;
+        parallel_for(
+            parts,
+            [&](size_t c) {
+                const size_t lo = m * c / parts, hi = m * (c + 1) / parts;
+                std::memcpy(stage + o_si + 4 * lo, sc_index.data() + lo, 4 * (hi - lo));
+            },
+            1);
+    }
+    if (!claim.empty()) std::memcpy(stage + o_co, claim.data(), sizeof(uint32_t) * claim.size());
+    std::memcpy(stage + o_rd, d->radii, sizeof(double) * p->nr);
+    std::memcpy(stage + o_rf, radii_f.data(), sizeof(float) * p->nr);
+    std::memcpy(stage + o_td, trig_d.data(), sizeof(double) * trig_d.size());
+    std::memcpy(stage + o_tf, trig_f.data(), sizeof(float) * trig_f.size());
+    std::memcpy(stage + o_thd, T.thr, sizeof(double) * 256);
+    std::memcpy(stage + o_thf, T.thr3, sizeof(float) * 256 * 4);
+    std::memcpy(stage + o_gs, T.guess, cvg::kGuessBuckets + 1);
+    LaunchArgs& A = p->args;
+    std::memset(&A, 0, sizeof(A));
+    A.sc = at<const SearchConst>(p->d_const, o_sc);
+    A.sc_index = sc_index.empty() ? nullptr : at<const uint32_t>(p->d_const, o_si);
+    A.claim_order = claim.empty() ? nullptr : at<const uint32_t>(p->d_const, o_co);
+    for (int g = 0; g < 3; ++g) A.group_end[g] = group_end[g];
+    A.radii_d = at<const double>(p->d_const, o_rd);
+    A.radii_f = at<const float>(p->d_const, o_rf);
+    A.trig_d = at<const double>(p->d_const, o_td);
+    A.trig_f = at<const float>(p->d_const, o_tf);
+    A.thr_d = at<const double>(p->d_const, o_thd);
+    A.thr3 = at<const float>(p->d_const, o_thf);
+    A.guess = at<const uint8_t>(p->d_const, o_gs);
+    // No sync: the staging block stays with the plan until it is released,
+    // which happens after the stream has passed this copy.
+    p->stage = stage;
+    cudaError_t e = cudaMemcpyAsync(p->d_const, stage, bytes, cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "upload of the search tables");
+    p->t_upload_end = now_ms();
+
+    for (int i = 0; i < 9; ++i) A.minv[i] = kXyzToRgb.m[i / 3][i % 3];
+    A.n_searches = p->n;
+    A.nr = p->nr;
+    A.na = p->na;
+    A.aligned = (p->na % 32) == 0;
+    A.tiles_per_search = tps;
+    A.cand_per_search = static_cast<uint32_t>(cps);
+    A.na_magic = p->na > 1 ? (UINT64_MAX / static_cast<uint64_t>(p->na)) + 1 : 0;
+    A.n_tiles = n_tiles;
+
+    // ---- per-run workspace --------------------------------------------------
+    // zeroed each run:  status[n_scan_blocks] | tickets[8] | counts[n] | stats | total | total_a | total_b
+    // written each run: tile_count[n_tiles] | tile_base[n_tiles] | worklist   (PAIRS)
+    const bool pairs = p->out == cvg::kOutPairs;
+    const int per_sm = cvg::search_blocks_per_sm(p->mode, p->out, p->path);
+    if (per_sm <= 0) {
+        cudaError_t le = cudaGetLastError();
+        return fail(CVG_ECUDA, std::string("search kernel cannot be resident on this device (") +
+                                   cudaGetErrorString(le) + "); sm_100a image required");
+    }
+    // Two range views on two streams (PAIRS): the second range's phase 1
+    // fills the first's tail, and the first's scan + emit fill the second's.
+    // Measured neutral on cfg1/cfg2/cfg3 (the second range's persistent
+    // blocks hold every slot until its own tail, so the first range's emit
+    // only starts there), hence off unless CVG_SPLIT=1.
+    static const bool allow_split = [] {
+        const char* e = std::getenv("CVG_SPLIT");
+        return e && std::atoi(e) != 0;
+    }();
+    const uint64_t resident_warps = static_cast<uint64_t>(per_sm) * ctx->sms * cvg::kWarpsPerBlock;
+    p->split = allow_split && pairs && p->n >= 2 && n_tiles >= 8 * resident_warps;
+    const uint32_t n_a = p->split ? static_cast<uint32_t>(p->n / 2) : static_cast<uint32_t>(p->n);
+    const uint64_t tiles_a = static_cast<uint64_t>(n_a) * tps, tiles_b = n_tiles - tiles_a;
+    const uint64_t scan_a = pairs ? (tiles_a + cvg::kScanTile - 1) / cvg::kScanTile : 0;
+    const uint64_t scan_b = p->split ? (tiles_b + cvg::kScanTile - 1) / cvg::kScanTile : 0;
+    Layout W;
+    const size_t o_st = W.take(sizeof(unsigned long long) * (scan_a + scan_b));
+    const size_t o_tk = W.take(sizeof(unsigned int) * 8);
+    const size_t o_ct = W.take(sizeof(unsigned long long) * p->n);
+    const size_t o_ss = W.take(sizeof(cvg::Stats));
+    const size_t o_to = W.take(sizeof(unsigned long long));  // stats+total read back as one ChunkTail
+    const size_t o_ta = W.take(sizeof(unsigned long long) * 2);  // per-view totals (split)
+    p->work_bytes = W.off;  // memset span
+    const size_t o_tc = W.take(sizeof(uint32_t) * (pairs ? n_tiles : 0));
+    const size_t o_tb = W.take(sizeof(unsigned long long) * (pairs ? n_tiles : 0));
+    const size_t o_wl = W.take(sizeof(uint32_t) * (pairs ? n_tiles * (cvg::kTile / cvg::kEmitSpan) : 0));
+    p->d_work = ctx->dev.alloc(W.off);
+    if (!p->d_work) return fail(CVG_ENOMEM, "device allocation of the workspace failed");
+    A.status = at<unsigned long long>(p->d_work, o_st);
+    A.ticket = at<unsigned int>(p->d_work, o_tk);
+    A.counts = at<unsigned long long>(p->d_work, o_ct);
+    A.stats = at<cvg::Stats>(p->d_work, o_ss);
+    A.tile_count = at<uint32_t>(p->d_work, o_tc);
+    A.tile_base = at<unsigned long long>(p->d_work, o_tb);
+    A.total = at<unsigned long long>(p->d_work, o_to);
+    A.worklist = at<uint32_t>(p->d_work, o_wl);
+    A.search_begin = 0;
+    A.range_searches = static_cast<uint32_t>(p->n);
+    A.tile_begin = 0;
+    A.base_offset = nullptr;
+    A.grand_total = nullptr;
+    if (pairs) {
+        p->d_scratch = ctx->dev.alloc(static_cast<size_t>(n_tiles) * cvg::kTile * sizeof(uint16_t));
+        if (!p->d_scratch) return fail(CVG_ENOMEM, "device allocation of the tile lists failed");
+        A.scratch = static_cast<uint16_t*>(p->d_scratch);
+    }
+    if (p->out == cvg::kOutFirst) {
+        Layout F;
+        const size_t o_fi = F.take(sizeof(uint32_t) * p->n);
+        const size_t o_fc = F.take(static_cast<size_t>(p->n) * 6);
+        p->first_bytes = F.off;
+        p->d_first = ctx->dev.alloc(p->first_bytes);
+        if (!p->d_first) return fail(CVG_ENOMEM, "device allocation of the first-pair buffer failed");
+        A.first_idx = at<uint32_t>(p->d_first, o_fi);
+        A.first_codes = at<uint8_t>(p->d_first, o_fc);
+    }
+
+    if (p->split) {
+        unsigned long long* totals = at<unsigned long long>(p->d_work, o_ta);
+        A.claim_order = nullptr;  // range views claim in search order
+        p->va = A;
+        p->va.range_searches = n_a;
+        p->va.n_tiles = tiles_a;
+        p->va.total = totals;
+        p->vb = A;
+        p->vb.search_begin = n_a;
+        p->vb.range_searches = static_cast<uint32_t>(p->n) - n_a;
+        p->vb.tile_begin = tiles_a;
+        p->vb.n_tiles = tiles_b;
+        p->vb.status = A.status + scan_a;
+        p->vb.ticket = A.ticket + 4;
+        p->vb.total = totals + 1;
+        p->vb.worklist = A.worklist + tiles_a * (cvg::kTile / cvg::kEmitSpan);
+        p->vb.base_offset = totals;
+        p->vb.grand_total = A.total;
+    }
+    const uint64_t want = (n_tiles + cvg::kWarpsPerBlock - 1) / cvg::kWarpsPerBlock;
+    p->grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(per_sm) * ctx->sms, want));
+    if (p->grid < 1) p->grid = 1;
+    for (cudaEvent_t* ev : {&p->ev0, &p->ev1, &p->marks[0], &p->marks[1], &p->marks[2], &p->marks[3]}) {
+        if (!ctx->events.empty()) {
+            *ev = ctx->events.back();
+            ctx->events.pop_back();
+        } else {
+            CVG_CUDA(cudaEventCreate(ev));
+        }
+    }
+
+    if (p->out == cvg::kOutPairs) {
+        // Initial capacity: every candidate when it fits in half the free memory.
+        const uint64_t fit = static_cast<uint64_t>(ctx->total_mem / 4 / 10);  // a quarter of HBM at most
+        uint64_t cap = std::min<uint64_t>(p->candidates, std::max<uint64_t>(fit, 1u << 20));
+        if (int e2 = plan_reserve(p, cap)) return e2;
+    }
+    return CVG_OK;
+}
+
+int plan_build_safe(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTables* grid,
+                    const SearchConst* pre) {
+    try {
+        return plan_build(ctx, d, p, grid, pre);
+    } catch (const std::bad_alloc&) {
+        return fail(CVG_ENOMEM, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(CVG_EUNSUPPORTED, e.what());
+    }
+}
+
+void plan_release(cvg_plan* p) {
+    if (!p->ctx) return;
+    if (p->ran && !p->empty && p->ev1) cudaEventSynchronize(p->ev1);  // buffers go back to the pool
+    plan_free_outputs(p);
+    p->ctx->dev.release(p->d_const);
+    p->ctx->dev.release(p->d_work);
+    p->ctx->dev.release(p->d_first);
+    p->ctx->dev.release(p->d_scratch);
+    if (p->stage) cudaStreamSynchronize(p->ctx->stream);  // the constant upload may still be in flight
+    for (cudaEvent_t* ev : {&p->ev0, &p->ev1, &p->marks[0], &p->marks[1], &p->marks[2], &p->marks[3]}) {
+        if (*ev) p->ctx->events.push_back(*ev);
+        *ev = nullptr;
+    }
+    p->ctx->host.release(p->stage);
+    p->stage = nullptr;
+    p->ctx->host.release(p->h_counts);
+    p->h_counts = nullptr;
+}
+
+int plan_enqueue(cvg_plan* p, cudaStream_t st) {
+    p->last_stream = st;
+    p->ran = true;
+    if (p->empty) return CVG_OK;
+    CVG_CUDA(cudaMemsetAsync(p->d_work, 0, p->work_bytes, st));
+    if (p->out == cvg::kOutFirst) CVG_CUDA(cudaMemsetAsync(p->d_first, 0xff, static_cast<size_t>(p->n) * 4, st));
+    CVG_CUDA(cudaEventRecord(p->ev0, st));
+    if (p->split) {
+        // the views copy the output buffers, which cvg_plan_reserve may have replaced
+        for (LaunchArgs* v : {&p->va, &p->vb}) {
+            v->out_idx = p->args.out_idx;
+            v->out_codes = p->args.out_codes;
+            v->capacity = p->args.capacity;
+        }
+        cudaStream_t aux = p->ctx->aux_stream;
+        CVG_CUDA(cudaStreamWaitEvent(aux, p->ev0, 0));
+        CVG_CUDA(cvg::launch_phase1(p->va, p->mode, p->out, p->path, p->grid, st));
+        CVG_CUDA(cudaEventRecord(p->marks[0], st));
+        CVG_CUDA(cvg::launch_phase1(p->vb, p->mode, p->out, p->path, p->grid, aux));
+        CVG_CUDA(cudaEventRecord(p->marks[1], aux));
+        CVG_CUDA(cvg::launch_scan(p->va, st));
+        CVG_CUDA(cudaEventRecord(p->marks[2], st));
+        CVG_CUDA(cvg::launch_emit(p->va, p->mode, p->path, p->grid, st));
+        CVG_CUDA(cvg::launch_scan(p->vb, aux));
+        CVG_CUDA(cudaStreamWaitEvent(aux, p->marks[2], 0));  // view b's pairs start after view a's total
+        CVG_CUDA(cvg::launch_emit(p->vb, p->mode, p->path, p->grid, aux));
+        CVG_CUDA(cudaEventRecord(p->marks[3], aux));
+        CVG_CUDA(cudaStreamWaitEvent(st, p->marks[3], 0));
+    } else {
+        CVG_CUDA(cvg::launch_search(p->args, p->mode, p->out, p->path, p->grid, st, p->marks));
+        if (p->out == cvg::kOutFirst) CVG_CUDA(cvg::launch_first_codes(p->args, st));
+    }
+    CVG_CUDA(cudaEventRecord(p->ev1, st));
+    return CVG_OK;
+}
+
+int plan_collect(cvg_plan* p, uint64_t* counts, HostStats& hs) {
+    if (p->empty) {
+        if (p->n) std::memset(counts, 0, sizeof(uint64_t) * p->n);
+        return CVG_OK;
+    }
+    cudaStream_t st = p->last_stream;
+    CVG_CUDA(cudaMemcpyAsync(counts, p->args.counts, sizeof(uint64_t) * p->n, cudaMemcpyDeviceToHost, st));
+    CVG_CUDA(cudaMemcpyAsync(&hs.st, p->args.stats, sizeof(cvg::Stats), cudaMemcpyDeviceToHost, st));
+    CVG_CUDA(cudaStreamSynchronize(st));
+    CVG_CUDA(cudaEventElapsedTime(&hs.ms, p->ev0, p->ev1));
+    return CVG_OK;
+}
+
+uint64_t sum_counts(const uint64_t* c, size_t n) {
+    const size_t parts = n >= (1u << 20) ? 16 : 1;
+    std::vector<uint64_t> part(parts, 0);
+    parallel_for(
+        parts,
+        [&](size_t k) {
+            uint64_t acc = 0;
+            for (size_t i = n * k / parts; i < n * (k + 1) / parts; ++i) acc += c[i];
+            part[k] = acc;
+        },
+        1);
+    uint64_t t = 0;
+    for (uint64_t v : part) t += v;
+    return t;
+}
+
+void result_zero(cvg_result* r) { std::memset(r, 0, sizeof(*r)); }
+
+int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
+    result_zero(r);
+    r->n_searches = p->n;
+    cvg_ctx* ctx = p->ctx;
+    const size_t n = static_cast<size_t>(p->n);
+    // counts land straight in the pinned block that becomes r->counts
+    r->counts = static_cast<uint64_t*>(ctx->host.alloc(sizeof(uint64_t) * (n ? n : 1)));
+    if (!r->counts) return fail(CVG_ENOMEM, "pinned host allocation failed");
+    HostStats hs;
+    if (int e = plan_collect(p, r->counts, hs)) return e;
+    const double t_counts = now_ms();
+    const uint64_t total = sum_counts(r->counts, n);
+    if (p->out == cvg::kOutPairs && hs.st.overflow) {
+        if (!allow_rerun) {
+            r->n_pairs = total;
+            return fail(CVG_EOVERFLOW, "pair buffer too small; call cvg_plan_reserve and rerun");
+        }
+        if (int e = plan_reserve(p, total)) return e;
+        if (int e = plan_enqueue(p, p->last_stream)) return e;
+        ctx->host.release(r->counts);
+        return plan_fetch_impl(p, r, false);
+    }
+    r->n_pairs = total;
+    r->n_candidates = p->candidates;
+    r->n_band_repairs = hs.st.band_repairs;
+    r->n_code_repairs = hs.st.code_repairs;
+    r->n_audit_violations = hs.st.audit_violations;
+    r->n_class_mismatch = hs.st.class_mismatch;
+    std::memcpy(&r->audit_max_ratio, &hs.st.audit_max_ratio_bits, sizeof(float));
+    r->kernel_ms = hs.ms;
+    r->h2d_bytes = p->input_bytes;
+    r->d2h_bytes = sizeof(uint64_t) * n + sizeof(cvg::Stats);
+    if (p->out == cvg::kOutPairs) {
+        r->d2h_bytes += total * 10;
+        r->offsets = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (n + 1)));
+        if (!r->offsets) return fail(CVG_ENOMEM, "host allocation failed");
+        r->offsets[0] = 0;
+        for (size_t s = 0; s < n; ++s) r->offsets[s + 1] = r->offsets[s] + r->counts[s];
+        if (total) {
+            r->idx = static_cast<uint32_t*>(ctx->host.alloc(total * 4));
+            r->codes = static_cast<uint8_t*>(ctx->host.alloc(total * 6));
+            if (!r->idx || !r->codes) return fail(CVG_ENOMEM, "pinned host allocation failed");
+            cudaStream_t st = p->last_stream;
+            CVG_CUDA(cudaMemcpyAsync(r->idx, p->d_out_idx, total * 4, cudaMemcpyDeviceToHost, st));
+            CVG_CUDA(cudaMemcpyAsync(r->codes, p->d_out_codes, total * 6, cudaMemcpyDeviceToHost, st));
+            CVG_CUDA(cudaStreamSynchronize(st));
+        }
+        r->d2h_ms = static_cast<float>(now_ms() - t_counts);
+    } else if (p->out == cvg::kOutFirst && n) {
+        r->d2h_bytes += n * 10;
+        r->first_idx = static_cast<uint32_t*>(ctx->host.alloc(n * 4));
+        r->first_codes = static_cast<uint8_t*>(ctx->host.alloc(n * 6));
+        if (!r->first_idx || !r->first_codes) return fail(CVG_ENOMEM, "pinned host allocation failed");
+        cudaStream_t st = p->last_stream;
+        CVG_CUDA(cudaMemcpyAsync(r->first_idx, p->args.first_idx, n * 4, cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaMemcpyAsync(r->first_codes, p->args.first_codes, n * 6, cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaStreamSynchronize(st));
+    }
+    return CVG_OK;
+}
+
+// cvg_result keeps a pointer to its context in a side table so that
+// cvg_result_free can return pinned blocks to the right pool.
+std::mutex g_owner_mu;
+std::map<const void*, cvg_ctx*> g_owner;
+
+void remember_owner(cvg_result* r, cvg_ctx* ctx) {
+    std::lock_guard<std::mutex> lk(g_owner_mu);
+    for (const void* ptr : {static_cast<const void*>(r->counts), static_cast<const void*>(r->idx),
+                            static_cast<const void*>(r->codes),
+                            static_cast<const void*>(r->first_idx), static_cast<const void*>(r->first_codes)}) {
+        if (ptr) g_owner[ptr] = ctx;
+    }
+}
+
+}  // namespace cvg::host
+
+// ============================================================================
+// C-ABI
+// ============================================================================
+
+using namespace cvg::host;
+
+extern "C" {
+
+const char* cvg_last_error(void) { return g_error.c_str(); }
+const char* cvg_version(void) { return "colorvibe-b200 0.1.0 (sm_100a)"; }
+
+int cvg_create(int device, cvg_ctx** out) {
+    if (!out) return fail(CVG_EINVAL, "null output pointer");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(CVG_ECUDA, std::string("no CUDA device available: ") + cudaGetErrorString(e));
+    }
+    if (device < 0 || device >= count) return fail(CVG_EINVAL, "device index out of range");
+    auto* ctx = new cvg_ctx();
+    ctx->device = device;
+    ctx->dev.device = true;
+    ctx->host.device = false;
+    e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->tail_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) {
+        size_t free_b = 0;
+        e = cudaMemGetInfo(&free_b, &ctx->total_mem);
+    }
+    if (e != cudaSuccess) {
+        delete ctx;
+        return cuda_fail(e, "context creation");
+    }
+    (void)tables();
+    *out = ctx;
+    return CVG_OK;
+}
+
+void cvg_destroy(cvg_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    {
+        std::lock_guard<std::mutex> lk(g_owner_mu);
+        for (auto it = g_owner.begin(); it != g_owner.end();) {
+            it = it->second == ctx ? g_owner.erase(it) : std::next(it);
+        }
+    }
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamSynchronize(ctx->tail_stream);
+    cudaStreamSynchronize(ctx->aux_stream);
+    layout_free(ctx->codec_layout);
+    for (cudaEvent_t ev : ctx->events) cudaEventDestroy(ev);
+    cudaStreamDestroy(ctx->stream);
+    cudaStreamDestroy(ctx->copy_stream);
+    cudaStreamDestroy(ctx->tail_stream);
+    cudaStreamDestroy(ctx->aux_stream);
+    delete ctx;
+}
+
+int cvg_plan_create(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_plan** out) {
+    if (!ctx || !out) return fail(CVG_EINVAL, "null context or output pointer");
+    *out = nullptr;
+    if (int e = validate_desc(desc)) return e;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    if (int e = ensure_device(ctx)) return e;
+    auto* p = new cvg_plan();
+    if (int e = plan_build_safe(ctx, desc, p)) {
+        plan_release(p);
+        delete p;
+        return e;
+    }
+    *out = p;
+    return CVG_OK;
+}
+
+void cvg_plan_destroy(cvg_plan* p) {
+    if (!p) return;
+    if (p->ctx) {
+        std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+        cudaSetDevice(p->ctx->device);
+        if (p->ran) cudaStreamSynchronize(p->last_stream);
+        plan_release(p);
+    }
+    delete p;
+}
+
+int cvg_plan_reserve(cvg_plan* p, uint64_t cap) {
+    if (!p) return fail(CVG_EINVAL, "null plan");
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    if (int e = ensure_device(p->ctx)) return e;
+    return plan_reserve(p, cap);
+}
+
+int cvg_plan_run(cvg_plan* p, void* stream) {
+    if (!p) return fail(CVG_EINVAL, "null plan");
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    if (int e = ensure_device(p->ctx)) return e;
+    return plan_enqueue(p, static_cast<cudaStream_t>(stream));
+}
+
+int cvg_plan_sync(cvg_plan* p, uint64_t* n_pairs) {
+    if (!p) return fail(CVG_EINVAL, "null plan");
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    if (int e = ensure_device(p->ctx)) return e;
+    if (!p->h_counts) {
+        p->h_counts = static_cast<uint64_t*>(p->ctx->host.alloc(sizeof(uint64_t) * (p->n ? p->n : 1)));
+        if (!p->h_counts) return fail(CVG_ENOMEM, "pinned host allocation failed");
+    }
+    HostStats hs;
+    if (int e = plan_collect(p, p->h_counts, hs)) return e;
+    const uint64_t total = sum_counts(p->h_counts, static_cast<size_t>(p->n));
+    if (n_pairs) *n_pairs = total;
+    if (p->out == cvg::kOutPairs && hs.st.overflow) return fail(CVG_EOVERFLOW, "pair buffer too small");
+    return CVG_OK;
+}
+
+int cvg_plan_fetch(cvg_plan* p, cvg_result* out) {
+    if (!p || !out) return fail(CVG_EINVAL, "null plan or result");
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    if (int e = ensure_device(p->ctx)) return e;
+    const int e = plan_fetch_impl(p, out, false);
+    remember_owner(out, p->ctx);
+    if (e) cvg_result_free(out);
+    return e;
+}
+
+int cvg_plan_copy_outputs(cvg_plan* p, uint64_t* counts, uint32_t* idx, uint8_t* codes, uint64_t n_pairs,
+                          void* stream) {
+    if (!p) return fail(CVG_EINVAL, "null plan");
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    if (int e = ensure_device(p->ctx)) return e;
+    if (p->empty) return CVG_OK;
+    if ((idx || codes) && (p->out != cvg::kOutPairs || n_pairs > p->capacity)) {
+        return fail(CVG_EINVAL, "n_pairs exceeds the plan's pair buffer (or not a PAIRS plan)");
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (counts) {
+        CVG_CUDA(cudaMemcpyAsync(counts, p->args.counts, sizeof(uint64_t) * p->n, cudaMemcpyDeviceToDevice, st));
+    }
+    if (idx && n_pairs) CVG_CUDA(cudaMemcpyAsync(idx, p->d_out_idx, 4 * n_pairs, cudaMemcpyDeviceToDevice, st));
+    if (codes && n_pairs) CVG_CUDA(cudaMemcpyAsync(codes, p->d_out_codes, 6 * n_pairs, cudaMemcpyDeviceToDevice, st));
+    return CVG_OK;
+}
+
+int cvg_plan_device_outputs(cvg_plan* p, uint64_t** counts, uint32_t** idx, uint8_t** codes, uint64_t* capacity) {
+    if (!p) return fail(CVG_EINVAL, "null plan");
+    if (counts) *counts = reinterpret_cast<uint64_t*>(p->args.counts);
+    if (idx) *idx = static_cast<uint32_t*>(p->d_out_idx);
+    if (codes) *codes = static_cast<uint8_t*>(p->d_out_codes);
+    if (capacity) *capacity = p->capacity;
+    return CVG_OK;
+}
+
+int cvg_plan_last_kernel_ms(cvg_plan* p, float* ms) {
+    if (!p || !ms) return fail(CVG_EINVAL, "null plan or output");
+    *ms = 0.f;
+    if (p->empty || !p->ran) return CVG_OK;
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    CVG_CUDA(cudaEventSynchronize(p->ev1));
+    CVG_CUDA(cudaEventElapsedTime(ms, p->ev0, p->ev1));
+    return CVG_OK;
+}
+
+uint64_t cvg_plan_input_bytes(const cvg_plan* p) { return p ? p->input_bytes : 0; }
+
+int cvg_plan_last_phase_ms(cvg_plan* p, float* phase1_ms, float* scan_ms, float* emit_ms) {
+    if (!p || !phase1_ms || !scan_ms || !emit_ms) return fail(CVG_EINVAL, "null plan or output");
+    *phase1_ms = *scan_ms = *emit_ms = 0.f;
+    if (p->empty || !p->ran) return CVG_OK;
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    CVG_CUDA(cudaEventSynchronize(p->ev1));
+    if (p->out != cvg::kOutPairs) return cudaEventElapsedTime(phase1_ms, p->ev0, p->ev1) == cudaSuccess
+                                             ? CVG_OK : fail(CVG_ECUDA, "event timing failed");
+    if (p->split) {
+        // phase 1 = until both views' phase 1 ended; scan + emit = the rest
+        // (view a's scan and emit overlap view b's phase 1 and are not split out)
+        float a = 0.f, b = 0.f, all = 0.f;
+        CVG_CUDA(cudaEventElapsedTime(&a, p->ev0, p->marks[0]));
+        CVG_CUDA(cudaEventElapsedTime(&b, p->ev0, p->marks[1]));
+        CVG_CUDA(cudaEventElapsedTime(&all, p->ev0, p->ev1));
+        *phase1_ms = std::max(a, b);
+        *emit_ms = all - *phase1_ms;
+        return CVG_OK;
+    }
+    CVG_CUDA(cudaEventElapsedTime(phase1_ms, p->ev0, p->marks[0]));
+    CVG_CUDA(cudaEventElapsedTime(scan_ms, p->marks[0], p->marks[1]));
+    CVG_CUDA(cudaEventElapsedTime(emit_ms, p->marks[1], p->ev1));
+    return CVG_OK;
+}
+
+int cvg_plan_launches(const cvg_plan* p) {
+    if (!p || p->empty) return 0;
+    if (p->split) return 6;
+    return p->out == cvg::kOutPairs ? 3 : p->out == cvg::kOutFirst ? 2 : 1;
+}
+
+uint64_t cvg_plan_candidates(const cvg_plan* p) { return p ? p->candidates : 0; }
+
+int cvg_validate(const cvg_search_desc* desc) { return validate_desc(desc); }
+
+void cvg_result_free(cvg_result* r) {
+    if (!r) return;
+    std::free(r->offsets);
+    for (void* ptr : {static_cast<void*>(r->counts), static_cast<void*>(r->idx), static_cast<void*>(r->codes), static_cast<void*>(r->first_idx),
+                      static_cast<void*>(r->first_codes)}) {
+        if (!ptr) continue;
+        cvg_ctx* owner = nullptr;
+        {
+            std::lock_guard<std::mutex> lk(g_owner_mu);
+            auto it = g_owner.find(ptr);
+            if (it != g_owner.end()) {
+                owner = it->second;
+                g_owner.erase(it);
+            }
+        }
+        if (owner) {
+            std::lock_guard<std::recursive_mutex> lk(owner->mu);
+            owner->host.release(ptr);
+        }
+    }
+    std::memset(r, 0, sizeof(*r));
+}
+
+int cvg_srgb_to_lab(const int32_t rgb[3], const double* wp, double lab[3]) {
+    if (!rgb || !lab) return fail(CVG_EINVAL, "null argument");
+    if (int e = validate_color(rgb)) return e;
+    to_lab(rgb, white_or_d65(wp), lab);
+    return CVG_OK;
+}
+
+static int validate_lab(const double lab[3]) {
+    if (!(std::isfinite(lab[0]) && std::isfinite(lab[1]) && std::isfinite(lab[2])) || lab[0] < 0.0 || lab[0] > 100.0) {
+        return fail(CVG_EINVAL, "Lab color with L* outside [0, 100]");
+    }
+    return CVG_OK;
+}
+
+int cvg_lab_to_srgb_clipped(const double lab[3], const double* wp, int32_t rgb[3]) {
+    if (!rgb || !lab) return fail(CVG_EINVAL, "null argument");
+    if (int e = validate_lab(lab)) return e;
+    double lin[3];
+    to_linear(lab, white_or_d65(wp), lin);
+    for (int c = 0; c < 3; ++c) rgb[c] = quantize(lin[c]);
+    return CVG_OK;
+}
+
+int cvg_lab_to_srgb(const double lab[3], const double* wp, int32_t rgb[3]) {
+    if (!rgb || !lab) return -fail(CVG_EINVAL, "null argument");
+    if (validate_lab(lab)) return -CVG_EINVAL;
+    double lin[3];
+    to_linear(lab, white_or_d65(wp), lin);
+    for (int c = 0; c < 3; ++c) {
+        if (!(lin[c] >= -kGamutEps && lin[c] <= 1.0 + kGamutEps)) return 0;
+    }
+    for (int c = 0; c < 3; ++c) rgb[c] = quantize(lin[c]);
+    return 1;
+}
+
+int cvg_pair_signal(const double lab[3], double radius, double angle, const double* wp, double sp[3],
+                    double sm[3]) {
+    if (!lab || !sp || !sm) return fail(CVG_EINVAL, "null argument");
+    if (int e = validate_lab(lab)) return e;
+    // displaced_pair (search.cpp:113-123) -> lab_to_linear -> signal_value
+    const double da = radius * std::sin(angle);
+    const double db = radius * std::cos(angle);
+    const double plus[3] = {lab[0], lab[1] + da, lab[2] + db};
+    const double minus[3] = {lab[0], lab[1] - da, lab[2] - db};
+    double lp[3], lm[3];
+    to_linear(plus, white_or_d65(wp), lp);
+    to_linear(minus, white_or_d65(wp), lm);
+    for (int c = 0; c < 3; ++c) {
+        sp[c] = signal_value(lp[c]);
+        sm[c] = signal_value(lm[c]);
+    }
+    return CVG_OK;
+}
+
+void cvg_d65_white(double out[3]) {
+    const double* w = white_or_d65(nullptr);
+    out[0] = w[0];
+    out[1] = w[1];
+    out[2] = w[2];
+}
+
+void cvg_quant_thresholds(double out[256]) { std::memcpy(out, tables().thr, sizeof(double) * 256); }
+
+double cvg_measure_ffma_peak(int device, float* ms_out) { return cvg::measure_ffma_peak(device, ms_out); }
+
+}  // extern "C"

@@ -1,0 +1,488 @@
+// cvg_search.cpp -- cvg_search: one host call over a batch of searches, and
+// its pipelined paths (search ranges whose host prep and read-back overlap
+// the kernels of other ranges).
+#include "cvg_host.h"
+
+namespace cvg::host {
+
+// ---- pipelined PAIRS search ------------------------------------------------
+// The end-to-end cost of a large PAIRS search is the PCIe read-back of 10
+// bytes per pair (cfg1: 38 MB, 0.69 ms at ~55 GB/s) after the device work.
+// Splitting the batch into K search ranges lets chunk c's read-back (copy
+// stream) overlap chunk c+1's build and kernels (compute stream); the
+// host learns chunk c's pair total from a 8-byte tail copy behind its
+// kernels and appends its pairs to one contiguous pinned result.
+int pipeline_chunks(const cvg_search_desc* d) {
+    if (d->output != CVG_OUT_PAIRS || d->n_searches < 2) return 1;
+    const uint64_t cands = static_cast<uint64_t>(d->n_searches) * static_cast<uint64_t>(d->n_radii) *
+                           static_cast<uint64_t>(d->n_angles);
+    static const int forced = [] {
+        const char* e = std::getenv("CVG_PIPELINE_K");  // tuning override; 1 disables pipelining
+        return e ? std::atoi(e) : 0;
+    }();
+    uint64_t k;
+    if (forced > 0) {
+        k = static_cast<uint64_t>(forced);
+    } else {
+        // each range pays ~80 us of kernel tail and the last range's read-back
+        // overlaps nothing; measured optimum (tools/sweep_pipeline.sh):
+        // cfg1 (198M candidates) K=2, cfg3 (1.07G) K=4..6
+        if (cands < (1ull << 26)) return 1;
+        k = cands < (1ull << 29) ? 2 : (cands < (1ull << 31) ? 4 : 6);
+    }
+    return static_cast<int>(std::min<uint64_t>(k, static_cast<uint64_t>(d->n_searches)));
+}
+
+// Range boundaries growing linearly (sizes 1:2:...:K): the first range is
+// small so the read-back starts early; the later ranges carry the bulk.
+std::vector<size_t> ramp_bounds(size_t n, int K) {
+    std::vector<size_t> lo(K + 1);
+    static const bool even = std::getenv("CVG_PIPELINE_EVEN") != nullptr;  // tuning override
+    if (even) {
+        for (int c = 0; c <= K; ++c) lo[c] = n * c / K;
+        return lo;
+    }
+    const size_t den = static_cast<size_t>(K) * (K + 1) / 2;
+    for (int c = 0; c <= K; ++c) {
+        const size_t num = static_cast<size_t>(c) * (c + 1) / 2;
+        lo[c] = std::max(static_cast<size_t>(c), std::min(n - (K - c), n * num / den));
+    }
+    return lo;
+}
+
+struct ChunkTail {
+    union {
+        cvg::Stats st;
+        unsigned char pad[256];
+    };
+    unsigned long long total;
+};
+static_assert(sizeof(cvg::Stats) <= 256 && offsetof(ChunkTail, total) == 256, "ChunkTail mirrors the workspace");
+
+struct PinnedPairs {
+    cvg_ctx* ctx;
+    uint32_t* idx = nullptr;
+    uint8_t* codes = nullptr;
+    uint64_t cap = 0;
+
+    // grows to `need` pairs keeping the first `used` (waits for in-flight copies)
+    bool ensure(uint64_t need, uint64_t want, uint64_t used) {
+        if (need <= cap) return true;
+        const uint64_t ncap = std::max(need, want);
+        auto* ni = static_cast<uint32_t*>(ctx->host.alloc(ncap * 4));
+        auto* nc = static_cast<uint8_t*>(ctx->host.alloc(ncap * 6));
+        if (!ni || !nc) {
+            ctx->host.release(ni);
+            ctx->host.release(nc);
+            return false;
+        }
+        if (used) {
+            cudaStreamSynchronize(ctx->copy_stream);
+            const size_t parts = used >= (1u << 20) ? 16 : 1;
+            parallel_for(
+                parts,
+                [&](size_t c) {
+                    const size_t lo = used * c / parts, hi = used * (c + 1) / parts;
+                    std::memcpy(ni + lo, idx + lo, 4 * (hi - lo));
+                    std::memcpy(nc + 6 * lo, codes + 6 * lo, 6 * (hi - lo));
+                },
+                1);
+        }
+        ctx->host.release(idx);
+        ctx->host.release(codes);
+        idx = ni;
+        codes = nc;
+        cap = ncap;
+        return true;
+    }
+};
+
+// ---- pipelined COUNTS / FIRST search -----------------------------------------
+// Per-pixel batches (cfg4: 8.3M searches) spend ~13 ms of host prep and
+// ~3 ms of read-back around ~230 ms of kernels.  Split into K search ranges:
+// range c+1 is built on the host while range c computes, and range c's
+// counts (+ first pairs) are read back on the copy stream while later
+// ranges compute.  Only range 0's prep and the last range's read-back stay
+// exposed.  Every result array is sized up front (n searches).
+int fixed_chunks(const cvg_search_desc* d) {
+    if (d->output == CVG_OUT_PAIRS || d->n_searches < (1 << 20)) return 1;
+    static const int forced = [] {
+        const char* e = std::getenv("CVG_PIPELINE_K");
+        return e ? std::atoi(e) : 0;
+    }();
+    return forced > 0 ? std::min(forced, d->n_searches) : 4;
+}
+
+int search_ranges_fixed(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, int K) {
+    const double t0 = now_ms();
+    const size_t n = static_cast<size_t>(d->n_searches);
+    const uint64_t cps = static_cast<uint64_t>(d->n_radii) * static_cast<uint64_t>(d->n_angles);
+    const bool first = d->output == CVG_OUT_FIRST;
+    r->n_searches = d->n_searches;
+    r->counts = static_cast<uint64_t*>(ctx->host.alloc(sizeof(uint64_t) * n));
+    if (first) {
+        r->first_idx = static_cast<uint32_t*>(ctx->host.alloc(4 * n));
+        r->first_codes = static_cast<uint8_t*>(ctx->host.alloc(6 * n));
+    }
+    auto* tails = static_cast<ChunkTail*>(ctx->host.alloc(sizeof(ChunkTail) * K));
+    if (!r->counts || !tails || (first && (!r->first_idx || !r->first_codes))) {
+        ctx->host.release(tails);
+        return fail(CVG_ENOMEM, "pinned host allocation failed");
+    }
+    std::vector<cvg_plan> plans(K);
+    std::vector<cudaEvent_t> kdone(K, nullptr);
+    const GridTables grid = make_grid_tables(d);
+    double prep = 0, h2d = 0, t_first_enqueued = 0;
+    int err = CVG_OK;
+    for (int c = 0; c < K && !err; ++c) {
+        const size_t lo = n * c / K, hi = n * (c + 1) / K;
+        cvg_search_desc sub = *d;
+        sub.n_searches = static_cast<int32_t>(hi - lo);
+        sub.target_rgb = d->target_rgb + 3 * lo;
+        sub.pattern_bits = d->pattern_bits + lo;
+        sub.v_th = d->v_th + lo;
+        sub.r_novib = d->r_novib + lo;
+        const double tb = now_ms();
+        err = plan_build_safe(ctx, &sub, &plans[c], &grid);
+        if (err) break;
+        prep += (plans[c].t_prep_end ? plans[c].t_prep_end : now_ms()) - tb;
+        h2d += plans[c].t_upload_end ? plans[c].t_upload_end - plans[c].t_prep_end : 0.0;
+        if (!ctx->events.empty()) {
+            kdone[c] = ctx->events.back();
+            ctx->events.pop_back();
+        } else if (cudaEventCreate(&kdone[c]) != cudaSuccess) {
+            err = fail(CVG_ECUDA, "event creation failed");
+            break;
+        }
+        err = plan_enqueue(&plans[c], ctx->stream);
+        if (err) break;
+        if (c == 0) t_first_enqueued = now_ms();
+        const cvg_plan& p = plans[c];
+        auto copy = [&]() -> int {
+            cudaStream_t cs = ctx->copy_stream;
+            CVG_CUDA(cudaEventRecord(kdone[c], ctx->stream));
+            CVG_CUDA(cudaStreamWaitEvent(cs, kdone[c], 0));
+            CVG_CUDA(cudaMemcpyAsync(r->counts + lo, p.args.counts, sizeof(uint64_t) * (hi - lo),
+                                     cudaMemcpyDeviceToHost, cs));
+            CVG_CUDA(cudaMemcpyAsync(&tails[c], p.args.stats, sizeof(ChunkTail), cudaMemcpyDeviceToHost, cs));
+            if (first) {
+                CVG_CUDA(cudaMemcpyAsync(r->first_idx + lo, p.args.first_idx, 4 * (hi - lo), cudaMemcpyDeviceToHost,
+                                         cs));
+                CVG_CUDA(cudaMemcpyAsync(r->first_codes + 6 * lo, p.args.first_codes, 6 * (hi - lo),
+                                         cudaMemcpyDeviceToHost, cs));
+            }
+            return CVG_OK;
+        };
+        err = copy();
+    }
+    const double t_enqueued = now_ms();
+    if (!err) {
+        const cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+        if (ce != cudaSuccess) err = cuda_fail(ce, "result read-back");
+    }
+    const double t1 = now_ms();
+    if (!err) {
+        cvg::Stats agg{};
+        float ratio_max = 0.f, kernel_ms = 0.f;
+        uint64_t in_bytes = 0;
+        for (int c = 0; c < K; ++c) {
+            const cvg::Stats& st = tails[c].st;
+            agg.band_repairs += st.band_repairs;
+            agg.code_repairs += st.code_repairs;
+            agg.audit_violations += st.audit_violations;
+            agg.class_mismatch += st.class_mismatch;
+            float ratio;
+            std::memcpy(&ratio, &st.audit_max_ratio_bits, sizeof(float));
+            ratio_max = std::max(ratio_max, ratio);
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, plans[c].ev0, plans[c].ev1) == cudaSuccess) kernel_ms += ms;
+            in_bytes += plans[c].input_bytes;
+        }
+        r->n_pairs = sum_counts(r->counts, n);
+        r->n_candidates = cps * n;
+        r->n_band_repairs = agg.band_repairs;
+        r->n_code_repairs = agg.code_repairs;
+        r->n_audit_violations = agg.audit_violations;
+        r->n_class_mismatch = agg.class_mismatch;
+        r->audit_max_ratio = ratio_max;
+        r->kernel_ms = kernel_ms;
+        r->h2d_bytes = in_bytes;
+        r->d2h_bytes = (sizeof(uint64_t) + (first ? 10 : 0)) * n + sizeof(ChunkTail) * K;
+        r->prep_ms = static_cast<float>(prep);
+        r->h2d_ms = static_cast<float>(h2d);
+        r->device_ms = static_cast<float>(t1 - t_first_enqueued);  // ranges after the first overlap their prep
+        r->d2h_ms = 0.f;                                               // overlapped except the last range's
+        r->total_ms = static_cast<float>(t1 - t0);
+        (void)t_enqueued;
+    }
+    cudaStreamSynchronize(ctx->stream);
+    for (int c = 0; c < K; ++c) {
+        if (kdone[c]) ctx->events.push_back(kdone[c]);
+        if (plans[c].ctx) plan_release(&plans[c]);
+    }
+    ctx->host.release(tails);
+    return err;
+}
+
+int search_pipelined(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, int K) {
+    const double t0 = now_ms();
+    const size_t n = static_cast<size_t>(d->n_searches);
+    const uint64_t cps = static_cast<uint64_t>(d->n_radii) * static_cast<uint64_t>(d->n_angles);
+    const GridTables grid = make_grid_tables(d);
+    // every record up front, on all cores (ranges are too small to thread well)
+    std::vector<SearchConst> recs(n);
+    {
+        const Tables& T = tables();
+        const int mode = d->delta_basis == CVG_BASIS_TARGET_SWING ? cvg::kModeBand : cvg::kModeCodes;
+        const double rmax = d->radii[d->n_radii - 1];
+        parallel_for(n, [&](size_t s) { make_search_const(d, static_cast<int>(s), rmax, mode, T, recs[s]); }, 64);
+    }
+    const double t_recs = now_ms();
+    r->n_searches = d->n_searches;
+    r->counts = static_cast<uint64_t*>(ctx->host.alloc(sizeof(uint64_t) * n));
+    r->offsets = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (n + 1)));
+    auto* tails = static_cast<ChunkTail*>(ctx->host.alloc(sizeof(ChunkTail) * K));
+    if (!r->counts || !r->offsets || !tails) {
+        ctx->host.release(tails);
+        return fail(CVG_ENOMEM, "host allocation failed");
+    }
+    std::vector<cvg_plan> plans(K);
+    const std::vector<size_t> lo = ramp_bounds(n, K);
+    std::vector<cudaEvent_t> done(K, nullptr), kdone(K, nullptr);  // tails landed / kernels finished
+    PinnedPairs out{ctx};
+    const uint64_t sig[4] = {n, cps, static_cast<uint64_t>(d->delta_basis), static_cast<uint64_t>(d->path)};
+    const bool hinted = std::equal(sig, sig + 4, ctx->hint_sig);
+    uint64_t used = 0;
+    double prep = t_recs - t0, h2d = 0, t_last_done = 0;
+    cvg::Stats agg{};
+    float agg_ratio = 0.f, kernel_ms = 0.f;
+    int err = CVG_OK;
+    static const bool trace = std::getenv("CVG_TRACE") != nullptr;
+    std::vector<cudaEvent_t> copied(trace ? K : 0, nullptr);
+    for (auto& e : copied) cudaEventCreate(&e);
+    std::vector<std::pair<const char*, double>> tl;
+    auto mark = [&](const char* what) {
+        if (trace) tl.emplace_back(what, now_ms() - t0);
+    };
+
+    auto enqueue_tail = [&](int c) -> int {
+        // counts and [stats | total] of the range on the tail stream: the
+        // compute stream goes on with the next range, never queued behind
+        // a pair copy on the D2H engine
+        cvg_plan& p = plans[c];
+        cudaStream_t st = ctx->tail_stream;
+        CVG_CUDA(cudaEventRecord(kdone[c], ctx->stream));
+        CVG_CUDA(cudaStreamWaitEvent(st, kdone[c], 0));
+        CVG_CUDA(cudaMemcpyAsync(r->counts + lo[c], p.args.counts, sizeof(uint64_t) * (lo[c + 1] - lo[c]),
+                                 cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaMemcpyAsync(&tails[c], p.args.stats, sizeof(ChunkTail), cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaEventRecord(done[c], st));
+        return CVG_OK;
+    };
+    auto drain = [&](int c) -> int {
+        cvg_plan& p = plans[c];
+        mark("drain");
+        CVG_CUDA(cudaEventSynchronize(done[c]));
+        mark("done");
+        if (tails[c].st.overflow) {  // device pair buffer too small: rerun this range at its exact size
+            if (int e = plan_reserve(&p, tails[c].total)) return e;
+            if (int e = plan_enqueue(&p, ctx->stream)) return e;
+            if (int e = enqueue_tail(c)) return e;
+            CVG_CUDA(cudaEventSynchronize(done[c]));
+            if (tails[c].st.overflow) return fail(CVG_ECUDA, "pair buffer overflow after resizing");
+        }
+        t_last_done = now_ms();
+        const uint64_t tc = tails[c].total;
+        const uint64_t seen = cps * lo[c + 1];  // candidates through this chunk
+        const uint64_t extrap = (used + tc) * ((cps * n + seen - 1) / seen) + (used + tc) / 4 + (1u << 16);
+        const uint64_t want = hinted ? std::max(ctx->hint_pairs, used + tc) : extrap;
+        if (!out.ensure(used + tc, std::min<uint64_t>(want, cps * n), used)) {
+            return fail(CVG_ENOMEM, "pinned host allocation failed");
+        }
+        if (tc) {
+            CVG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, done[c], 0));
+            CVG_CUDA(cudaMemcpyAsync(out.idx + used, p.d_out_idx, tc * 4, cudaMemcpyDeviceToHost, ctx->copy_stream));
+            CVG_CUDA(cudaMemcpyAsync(out.codes + 6 * used, p.d_out_codes, tc * 6, cudaMemcpyDeviceToHost,
+                                     ctx->copy_stream));
+        }
+        if (trace) cudaEventRecord(copied[c], ctx->copy_stream);
+        mark("issued");
+        used += tc;
+        const cvg::Stats& s = tails[c].st;
+        agg.band_repairs += s.band_repairs;
+        agg.code_repairs += s.code_repairs;
+        agg.audit_violations += s.audit_violations;
+        agg.class_mismatch += s.class_mismatch;
+        float ratio;
+        std::memcpy(&ratio, &s.audit_max_ratio_bits, sizeof(float));
+        agg_ratio = std::max(agg_ratio, ratio);
+        float ms = 0.f;
+        CVG_CUDA(cudaEventElapsedTime(&ms, p.ev0, p.ev1));
+        kernel_ms += ms;
+        return CVG_OK;
+    };
+
+    mark("grid");
+    int next = 0;  // first range not yet drained
+    for (int c = 0; c < K && !err; ++c) {
+        cvg_search_desc sub = *d;
+        sub.n_searches = static_cast<int32_t>(lo[c + 1] - lo[c]);
+        sub.target_rgb = d->target_rgb + 3 * lo[c];
+        sub.pattern_bits = d->pattern_bits + lo[c];
+        sub.v_th = d->v_th + lo[c];
+        sub.r_novib = d->r_novib + lo[c];
+        const double tb = now_ms();
+        err = plan_build_safe(ctx, &sub, &plans[c], &grid, recs.data() + lo[c]);
+        if (err) break;
+        prep += (plans[c].t_prep_end ? plans[c].t_prep_end : now_ms()) - tb;
+        h2d += plans[c].t_upload_end ? plans[c].t_upload_end - plans[c].t_prep_end : 0.0;
+        for (cudaEvent_t* ev : {&done[c], &kdone[c]}) {
+            if (!ctx->events.empty()) {
+                *ev = ctx->events.back();
+                ctx->events.pop_back();
+            } else if (cudaEventCreate(ev) != cudaSuccess) {
+                err = fail(CVG_ECUDA, "event creation failed");
+            }
+        }
+        if (err) break;
+        mark("built");
+        err = plan_enqueue(&plans[c], ctx->stream);
+        if (!err) err = enqueue_tail(c);
+        mark("enqueued");
+        // start the read-back of every finished range without blocking the builds
+        while (!err && next < c) {
+            const cudaError_t q = cudaEventQuery(done[next]);
+            if (q == cudaErrorNotReady) {
+                cudaGetLastError();  // not an error: the range is still running
+                break;
+            }
+            err = q == cudaSuccess ? drain(next++) : cuda_fail(q, "range completion");
+        }
+    }
+    while (!err && next < K) err = drain(next++);
+    if (!err) {
+        cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
+        if (ce != cudaSuccess) err = cuda_fail(ce, "pair read-back");
+    }
+    const double t1 = now_ms();
+    if (!err) {
+        r->idx = used ? out.idx : nullptr;
+        r->codes = used ? out.codes : nullptr;
+        if (!used) {
+            ctx->host.release(out.idx);
+            ctx->host.release(out.codes);
+        }
+        r->offsets[0] = 0;
+        for (size_t s = 0; s < n; ++s) r->offsets[s + 1] = r->offsets[s] + r->counts[s];
+        r->n_pairs = used;
+        r->n_candidates = cps * n;
+        r->n_band_repairs = agg.band_repairs;
+        r->n_code_repairs = agg.code_repairs;
+        r->n_audit_violations = agg.audit_violations;
+        r->n_class_mismatch = agg.class_mismatch;
+        r->audit_max_ratio = agg_ratio;
+        r->kernel_ms = kernel_ms;
+        uint64_t in_bytes = 0;
+        for (const cvg_plan& p : plans) in_bytes += p.input_bytes;
+        r->h2d_bytes = in_bytes;
+        r->d2h_bytes = sizeof(uint64_t) * n + (sizeof(ChunkTail)) * K + used * 10;
+        r->prep_ms = static_cast<float>(prep);
+        r->h2d_ms = static_cast<float>(h2d);
+        r->device_ms = static_cast<float>(t_last_done - t0 - prep - h2d);
+        r->d2h_ms = static_cast<float>(t1 - t_last_done);
+        r->total_ms = static_cast<float>(t1 - t0);
+        std::copy(sig, sig + 4, ctx->hint_sig);
+        ctx->hint_pairs = used;
+    } else {
+        cudaStreamSynchronize(ctx->copy_stream);
+        ctx->host.release(out.idx);
+        ctx->host.release(out.codes);
+    }
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->tail_stream);
+    if (trace) {
+        mark("end");
+        std::string line = "[cvg trace] K=" + std::to_string(K);
+        for (auto& [w, t] : tl) line += std::string(" ") + w + "@" + std::to_string(t).substr(0, 6);
+        for (int c = 0; c < K && !err; ++c) {
+            float a = 0, b = 0, x = 0, m0 = 0, m1 = 0;
+            cudaEventElapsedTime(&a, plans[0].ev0, plans[c].ev0);
+            cudaEventElapsedTime(&b, plans[0].ev0, plans[c].ev1);
+            cudaEventElapsedTime(&x, plans[0].ev0, copied[c]);
+            cudaEventElapsedTime(&m0, plans[c].ev0, plans[c].marks[0]);
+            cudaEventElapsedTime(&m1, plans[c].ev0, plans[c].marks[1]);
+            line += " | r" + std::to_string(c) + " n=" + std::to_string(lo[c + 1] - lo[c]) + " pairs=" +
+                    std::to_string(tails[c].total) + " gpu " + std::to_string(a).substr(0, 5) + "-" +
+                    std::to_string(b).substr(0, 5) + " (p1 " + std::to_string(m0).substr(0, 5) + " scan@" +
+                    std::to_string(m1).substr(0, 5) + ") copied@" + std::to_string(x).substr(0, 5);
+        }
+        std::fprintf(stderr, "%s\n", line.c_str());
+        for (auto& e : copied) cudaEventDestroy(e);
+    }
+    for (int c = 0; c < K; ++c) {
+        if (done[c]) ctx->events.push_back(done[c]);
+        if (kdone[c]) ctx->events.push_back(kdone[c]);
+        if (plans[c].ctx) plan_release(&plans[c]);
+    }
+    ctx->host.release(tails);
+    return err;
+}
+
+}  // namespace cvg::host
+
+using namespace cvg::host;
+
+extern "C" {
+
+int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out) {
+    if (!ctx || !out) return fail(CVG_EINVAL, "null context or result");
+    result_zero(out);
+    if (int e = validate_desc(desc)) return e;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    if (int e = ensure_device(ctx)) return e;
+    // A plan holds < 2^28 tiles (32-bit tile ids with 16 emit items each):
+    // larger batches always run as search ranges, each well under the limit.
+    int K_min = 1;
+    {
+        const uint64_t cps = static_cast<uint64_t>(desc->n_radii) * static_cast<uint64_t>(desc->n_angles);
+        const uint64_t tiles = (cps + cvg::kTile - 1) / cvg::kTile * static_cast<uint64_t>(desc->n_searches);
+        const uint64_t per_range = 1ull << 26;  // ramp ranges reach 2/(K+1) of the batch
+        if (tiles >= per_range) K_min = static_cast<int>(std::min<uint64_t>((tiles + per_range - 1) / per_range,
+                                                                             static_cast<uint64_t>(desc->n_searches)));
+    }
+    if (const int K = std::max({pipeline_chunks(desc), fixed_chunks(desc), K_min}); K > 1) {
+        int e;
+        try {
+            e = desc->output == CVG_OUT_PAIRS ? search_pipelined(ctx, desc, out, K)
+                                              : search_ranges_fixed(ctx, desc, out, K);
+        } catch (const std::bad_alloc&) {
+            e = fail(CVG_ENOMEM, "host allocation failed");
+        } catch (const std::exception& ex) {
+            e = fail(CVG_EUNSUPPORTED, ex.what());
+        }
+        remember_owner(out, ctx);
+        if (e) cvg_result_free(out);
+        return e;
+    }
+    const double t0 = now_ms();
+    cvg_plan plan;
+    int e = plan_build_safe(ctx, desc, &plan);
+    const double t_built = now_ms();
+    if (!e) e = plan_enqueue(&plan, ctx->stream);
+    if (!e) e = plan_fetch_impl(&plan, out, true);
+    if (!e) {
+        const double t1 = now_ms();
+        out->prep_ms = static_cast<float>((plan.t_prep_end ? plan.t_prep_end : t_built) - t0);
+        out->h2d_ms = static_cast<float>(plan.t_upload_end ? plan.t_upload_end - plan.t_prep_end : 0.0);
+        out->total_ms = static_cast<float>(t1 - t0);
+        out->device_ms = static_cast<float>(t1 - t_built - out->d2h_ms);
+    }
+    if (plan.ran) cudaStreamSynchronize(ctx->stream);
+    plan_release(&plan);
+    plan.ctx = nullptr;
+    remember_owner(out, ctx);
+    if (e) cvg_result_free(out);
+    return e;
+}
+
+}  // extern "C"

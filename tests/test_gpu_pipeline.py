@@ -1,4 +1,4 @@
-"""The pipelined PAIRS read-back (cvg_host.cpp search_pipelined): batches of
+"""The pipelined PAIRS read-back (cvg_search.cpp search_pipelined): batches of
 >= 2^25 candidates are split into search ranges whose pairs are copied back
 while later ranges compute.  The result must equal the single-plan result
 bit for bit, including when the pinned result has to grow (early ranges
@@ -80,7 +80,7 @@ def test_pipelined_many_ranges_audit(ctx, oracle):
 def test_ranged_counts_first_equal_single_plans(ctx, output):
     """Per-pixel-size COUNTS / FIRST batches (>= 2^20 searches) run as 4
     search ranges whose prep and read-back overlap the kernels
-    (cvg_host.cpp search_ranges_fixed); results equal sub-batch single plans."""
+    (cvg_search.cpp search_ranges_fixed); results equal sub-batch single plans."""
     rng = np.random.default_rng(31)
     n = (1 << 20) + 12345
     radii, angles = W.radii(8, 6.0), W.angles(64)
