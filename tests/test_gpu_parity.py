@@ -406,3 +406,26 @@ def test_plan_overflow_then_reserve(ctx):
         plan.run()
     assert plan.sync() == 3785016
     assert plan.launches == 3  # phase 1, offset scan, emit
+
+
+def test_huge_single_search_linearity(ctx):
+    """One search of 2^31 candidates (4096 radii x 524288 angles: candidate
+    indices k*na + m up to 2^31, 524288 tiles): COUNTS and FIRST over the full
+    grid equal the sum / first over four radius slices run as separate
+    searches (the pair set of a search is a disjoint union over its rows)."""
+    radii, angles = W.radii(4096, 0.03125), W.angles(524288)
+    t = np.array([[200, 60, 90]], np.int32)
+    p, v, r = np.array([5], np.int32), np.array([40.0]), np.array([0.5])
+    full = ctx.search(t, p, v, r, radii, angles, output="first")
+    total, first = 0, None
+    for q in range(4):
+        sl = radii[q * 1024:(q + 1) * 1024]
+        part = ctx.search(t, p, v, r, sl, angles, output="first")
+        c = int(part["counts"][0])
+        if c and first is None:
+            first = int(part["first_idx"][0]) + q * 1024 * len(angles)
+            first_codes = part["first_codes"][0].tolist()
+        total += c
+    assert int(full["counts"][0]) == total > 0
+    assert int(full["first_idx"][0]) == first
+    assert full["first_codes"][0].tolist() == first_codes
