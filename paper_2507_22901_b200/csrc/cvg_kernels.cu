@@ -78,6 +78,7 @@ __device__ __forceinline__ uint32_t div_na(uint32_t i, const LaunchArgs& A) {
 // channel slots loud-first).
 struct Consts {
     float fx0, fz0, rcube;
+    float cube[6];  // SearchConst::cube: {fx0^3, 3 fx0^2, 3 fx0, fz0^3, 3 fz0^2, 3 fz0}
     float mxs[3], mzs[3], cys[3];
     float la, qa, lp, qp;
     uint32_t flags;
@@ -87,6 +88,8 @@ __device__ __forceinline__ void load_consts(const SearchConst* S, Consts& c) {
     c.fx0 = __ldg(&S->fx0);
     c.fz0 = __ldg(&S->fz0);
     c.rcube = __ldg(&S->rcube);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) c.cube[q] = __ldg(&S->cube[q]);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         c.mxs[q] = __ldg(&S->mxs[q]);
@@ -252,27 +255,59 @@ __device__ __forceinline__ void fast_linear(float fx0, float fz0, const float* m
 // and only attention-but-not-certain candidates go to the FP64 path.
 // kL = loud count (1..3), 0 = read it from the flags at run time.
 template <int kL>
-__device__ __forceinline__ void band_stats(const Consts& C, const float* dp, const float* dm, float& minl,
-                                           float& maxq) {
+__device__ __forceinline__ void band_stats_m(const Consts& C, const float* M, float& minl, float& maxq) {
     const int L = kL ? kL : static_cast<int>((C.flags >> 10) & 3u);
     minl = INFINITY;
     maxq = -INFINITY;
     if (kL == 3) {
-        minl = fminf(fminf(fmaxf(fabsf(dp[0]), fabsf(dm[0])), fmaxf(fabsf(dp[1]), fabsf(dm[1]))),
-                     fmaxf(fabsf(dp[2]), fabsf(dm[2])));
+        minl = fminf(fminf(M[0], M[1]), M[2]);
     } else if (kL == 2) {
-        minl = fminf(fmaxf(fabsf(dp[0]), fabsf(dm[0])), fmaxf(fabsf(dp[1]), fabsf(dm[1])));
-        maxq = fmaxf(fabsf(dp[2]), fabsf(dm[2]));
+        minl = fminf(M[0], M[1]);
+        maxq = M[2];
     } else if (kL == 1) {
-        minl = fmaxf(fabsf(dp[0]), fabsf(dm[0]));
-        maxq = fmaxf(fmaxf(fabsf(dp[1]), fabsf(dm[1])), fmaxf(fabsf(dp[2]), fabsf(dm[2])));
+        minl = M[0];
+        maxq = fmaxf(M[1], M[2]);
     } else {
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-            const float M = fmaxf(fabsf(dp[q]), fabsf(dm[q]));
-            if (q < L) minl = fminf(minl, M); else maxq = fmaxf(maxq, M);
+            if (q < L) minl = fminf(minl, M[q]); else maxq = fmaxf(maxq, M[q]);
         }
     }
+}
+
+template <int kL>
+__device__ __forceinline__ void band_stats(const Consts& C, const float* dp, const float* dm, float& minl,
+                                           float& maxq) {
+    float M[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) M[q] = fmaxf(fabsf(dp[q]), fabsf(dm[q]));
+    band_stats_m<kL>(C, M, minl, maxq);
+}
+
+// Cube-only rows in sum/difference form: with d+- the two endpoint values of
+// a channel, A = (d+ + d-)/2 and B = (d+ - d-)/2 give M' = max(|d+|, |d-|)
+// = |A| + |B|, and for f+- = f0 +- U in the cube branch
+//   A = mxs (fx0^3 + 3 fx0 Ux^2) + mzs (fz0^3 + 3 fz0 Uz^2) + cys
+//   B = mxs Ux (3 fx0^2 + Ux^2)  - mzs Uz (3 fz0^2 + Uz^2)
+// (Ux = r sin/500, Uz = r cos/200): 10 ops for the cubes and 15 for the
+// three channels instead of 4 + 8 + 12 + 3 (static SASS of the two-chunk
+// loop body: 70 instructions instead of 74); the host bound (cube_bound,
+// make_search_const) covers this form.
+template <int kL>
+__device__ __forceinline__ void band_cube(const Consts& C, float r, float2 sc, float& minl, float& maxq) {
+    const float ux = __fmul_rn(r, sc.x), uz = __fmul_rn(r, sc.y);
+    const float ax = fmaf(__fmul_rn(ux, ux), C.cube[2], C.cube[0]);
+    const float az = fmaf(__fmul_rn(uz, uz), C.cube[5], C.cube[3]);
+    const float bx = __fmul_rn(ux, fmaf(ux, ux, C.cube[1]));
+    const float bz = __fmul_rn(uz, fmaf(uz, uz, C.cube[4]));
+    float M[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const float a = fmaf(C.mxs[q], ax, fmaf(C.mzs[q], az, C.cys[q]));
+        const float b = fmaf(C.mxs[q], bx, -__fmul_rn(C.mzs[q], bz));
+        M[q] = fabsf(a) + fabsf(b);
+    }
+    band_stats_m<kL>(C, M, minl, maxq);
 }
 
 __device__ __forceinline__ bool band_attention(const Consts& C, float minl, float maxq) {
@@ -463,6 +498,13 @@ __device__ __forceinline__ bool candidate_pass(const Smem& sm, const SearchConst
         double lp[3], lm[3];
         exact_linear(S, A, k, m, lp, lm);
         const bool ex = exact_band(S, lp, lm, C.flags);
+        if (r < C.rcube) {  // cube-only rows run the sum/difference form in the fast path
+            float l2, q2;
+            band_cube<0>(C, r, sc, l2, q2);
+            const bool pass2 = band_certain(C, l2, q2);
+            const bool unsure2 = band_attention(C, l2, q2) & !pass2;
+            if (active) ct.violations += !unsure2 && ex != pass2;
+        }
         if (active) {
             ct.violations += !unsure && ex != pass;
             ct.repairs += unsure;
@@ -515,17 +557,22 @@ __device__ __forceinline__ void band_settle(const SearchConst* S, const Consts& 
 
 template <int kL, bool kCubeOnly>
 __device__ __forceinline__ void band_chunk(const Consts& C, float r, float2 sc, float& minl, float& maxq) {
-    float dp[3], dm[3];
-    fast_linear<kCubeOnly>(C.fx0, C.fz0, C.mxs, C.mzs, C.cys, r, sc, dp, dm);
-    band_stats<kL>(C, dp, dm, minl, maxq);
+    if (kCubeOnly) {
+        band_cube<kL>(C, r, sc, minl, maxq);
+    } else {
+        float dp[3], dm[3];
+        fast_linear<false>(C.fx0, C.fz0, C.mxs, C.mzs, C.cys, r, sc, dp, dm);
+        band_stats<kL>(C, dp, dm, minl, maxq);
+    }
 }
 
 // Hot loop: FAST path, band mode, kL loud channels, `nch` full 32-candidate
 // chunks of radius row k starting at angle m0 (na % 32 == 0: chunks never
 // straddle rows).  Two chunks per iteration share one vote (ILP across
 // chunks).  Per candidate: 1 LDG (L1-resident trig, prefetched two chunks
-// ahead), 24 FMA-pipe ops (4 f, 8 cube, 12 matrix) + 4 min/max + compares.
-// kCubeOnly rows (r < rcube) never reach the linear branch of f^-1.
+// ahead), then either 24 FMA-pipe ops (4 f, 8 cube or linear, 12 matrix) + 4
+// min/max, or, in kCubeOnly rows (r < rcube: never the linear branch of
+// f^-1), the sum/difference form's 25 ops + 1-2 min/max (band_cube).
 template <int kL, bool kCubeOnly, int kOut>
 __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
                                          float r, uint32_t m0, uint32_t nch, uint32_t off, uint16_t* list,

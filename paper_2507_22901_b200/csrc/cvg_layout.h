@@ -17,7 +17,7 @@ constexpr int kEmitSpan = 256;      // pairs per emit work item (tile sub-range)
 constexpr int kScanItems = 8;        // tile counts per thread in the offset scan
 constexpr int kScanTile = kBlock * kScanItems;
 
-// Per-search constants, one 256-byte record per (target, pattern, thresholds).
+// Per-search constants, one 288-byte record per (target, pattern, thresholds).
 // The FP32 half feeds the fast path; the FP64 half is the bit-exact restatement
 // of the reference hoisting (search.cpp:341-370) used by the repair path.
 struct alignas(16) SearchConst {
@@ -32,6 +32,7 @@ struct alignas(16) SearchConst {
     float mxs[3];      // band form, channels permuted loud-first: mx / h_c   (h_c: band half-width)
     float mzs[3];      //            mz / h_c
     float cys[3];      //            (cy - centre_c) / h_c
+    float cube[6];     // cube-only rows, sum/difference form: {fx0^3, 3 fx0^2, 3 fx0, fz0^3, 3 fz0^2, 3 fz0}
     float qa, qp, lp;  // attention: max quiet M' <= qa; certain pass: max quiet M' < qp and min loud M' > lp
     float eps[3];      // proven bound |lin32 - lin64| per channel (linear units)
     float eps_code[3]; // eps + float rounding of the code thresholds
@@ -44,7 +45,7 @@ struct alignas(16) SearchConst {
     double cy64[3];
     double lo[3], hi[3];
 };
-static_assert(sizeof(SearchConst) == 272, "SearchConst layout");
+static_assert(sizeof(SearchConst) == 288, "SearchConst layout");
 
 // Device statistics block.
 struct Stats {

@@ -271,6 +271,35 @@ BoundTerms finv_bound(double f0, double rmax_scaled) {
     return b;
 }
 
+// Cube-only rows (every endpoint in the cube branch), sum/difference form as
+// in the kernel's band_cube(): with f+- = f0 +- U (U = r*s') the half-sum and
+// half-difference of the cubes are
+//   A = (f+^3 + f-^3)/2 = f0^3 + 3 f0 U^2   = fma(u*u, C3, C1)
+//   B = (f+^3 - f-^3)/2 = U (3 f0^2 + U^2)  = u * fma(u, u, C2),   u = r*s'
+// with C1 = fl(f0^3), C2 = fl(3 f0^2), C3 = fl(3 f0) rounded once from double
+// (1.01u each).  Forward errors (u = 2^-24):
+//   u:         3.01u |U|   (r, s' rounded to float, product)
+//   u*u:       7.04u U^2;   times C3: 8.06u relative to 3 F0 U^2
+//   A:         8.06u 3F0U^2 + 1.01u F0^3 + u |A|
+//   fma(u,u,C2): 6.03u U^2 + 3.03u F0^2 + u |T|,  T = U^2 + 3 F0^2
+//   B:         |u| etx + 3.01u |U| T + u |U| T
+struct CubeTerms {
+    BoundTerms a, b;
+};
+
+CubeTerms cube_bound(double f0, double umax) {
+    const double u = std::ldexp(1.0, -24);
+    const double F = std::fabs(f0), U = umax;
+    CubeTerms t;
+    t.a.gmax = F * F * F + 3.0 * F * U * U;
+    t.a.err = u * (9.07 * 3.0 * F * U * U + 2.02 * F * F * F);
+    const double T = U * U + 3.0 * F * F;
+    const double etx = u * (7.04 * U * U + 6.04 * F * F);
+    t.b.gmax = U * T;
+    t.b.err = U * (1.0 + 3.02 * u) * etx + 4.03 * u * U * T;
+    return t;
+}
+
 void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, const Tables& T,
                        SearchConst& S) {
     std::memset(&S, 0, sizeof(S));
@@ -332,6 +361,10 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
     const double u = std::ldexp(1.0, -24);
     const BoundTerms bx = finv_bound(fx0, rmax * kInv500);
     const BoundTerms bz = finv_bound(fz0, rmax * kInv200);
+    const CubeTerms cx = cube_bound(fx0, rmax * kInv500);
+    const CubeTerms cz = cube_bound(fz0, rmax * kInv200);
+    const double cube_c[6] = {fx0 * fx0 * fx0, 3.0 * fx0 * fx0, 3.0 * fx0, fz0 * fz0 * fz0, 3.0 * fz0 * fz0, 3.0 * fz0};
+    for (int i = 0; i < 6; ++i) S.cube[i] = static_cast<float>(cube_c[i]);
     double eps_q = 0.0, eps_l = 0.0;
     // band form channel slots: loud channels first (the kernel specializes on
     // the loud count L and reads slots [0, L) as loud, [L, 3) as quiet)
@@ -347,15 +380,16 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
         // Forward error of fma(cx, gx, fma(cz, gz, add)) with float-rounded
         // constants (|cx|, |cz| magnitudes, `add` exact value).  Returns
         // (bound, max |result|).
-        auto lin_err = [&](double acx, double acz, double add) {
+        auto lin_err_of = [&](const BoundTerms& gx, const BoundTerms& gz, double acx, double acz, double add) {
             const double aadd = std::fabs(add);
-            const double inner_max = acz * bz.gmax + aadd;
-            const double e_inner = acz * bz.err * (1 + u) + u * acz * bz.gmax + u * aadd + u * (inner_max + acz * bz.err);
-            const double lin_max = acx * bx.gmax + inner_max;
-            return std::pair<double, double>(acx * bx.err * (1 + u) + u * acx * bx.gmax + e_inner +
-                                                 u * (lin_max + acx * bx.err),
+            const double inner_max = acz * gz.gmax + aadd;
+            const double e_inner = acz * gz.err * (1 + u) + u * acz * gz.gmax + u * aadd + u * (inner_max + acz * gz.err);
+            const double lin_max = acx * gx.gmax + inner_max;
+            return std::pair<double, double>(acx * gx.err * (1 + u) + u * acx * gx.gmax + e_inner +
+                                                 u * (lin_max + acx * gx.err),
                                              lin_max);
         };
+        auto lin_err = [&](double acx, double acz, double add) { return lin_err_of(bx, bz, acx, acz, add); };
         S.mx[c] = static_cast<float>(mx);
         S.mz[c] = static_cast<float>(mz);
         S.cy[c] = static_cast<float>(cy);
@@ -381,7 +415,13 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
         S.mzs[j] = static_cast<float>(mz / hh);
         S.cys[j] = static_cast<float>((cy - cc) / hh);
         const auto [e_d, d_max] = lin_err(std::fabs(mx / hh), std::fabs(mz / hh), (cy - cc) / hh);
-        const double e_m = 1.05 * (e_d + 4 * std::ldexp(1.0, -53) * (d_max + 2.0)) + 1e-12 / hh;
+        // cube-only rows: M' = |A_c| + |B_c| with A_c = fma(mxs, Ax, fma(mzs, Az, cys)) and
+        // B_c = fma(mxs, Bx, -(mzs * Bz)) (the kernel's band_cube); the thresholds cover both forms
+        const auto [e_a, a_max] = lin_err_of(cx.a, cz.a, std::fabs(mx / hh), std::fabs(mz / hh), (cy - cc) / hh);
+        const auto [e_b, b_max] = lin_err_of(cx.b, cz.b, std::fabs(mx / hh), std::fabs(mz / hh), 0.0);
+        const double e_ab = e_a + e_b + u * (a_max + b_max + e_a + e_b);
+        const double m_max = std::max(d_max, a_max + b_max);
+        const double e_m = 1.05 * (std::max(e_d, e_ab) + 4 * std::ldexp(1.0, -53) * (m_max + 2.0)) + 1e-12 / hh;
         (bits[c] ? eps_l : eps_q) = std::max(bits[c] ? eps_l : eps_q, e_m);
     }
     S.la = round_down_f(1.0 - eps_l);

@@ -6,7 +6,8 @@ import subprocess
 import sys
 from collections import Counter
 
-obj = "paper_2507_22901_b200/_build/cvg_kernels.o"
+import os
+obj = os.environ.get("OBJ", "paper_2507_22901_b200/_build/cvg_kernels.o")
 pat = sys.argv[1] if len(sys.argv) > 1 else r"phase1_kernelILi0ELi0ELi0E"
 sass = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
 funcs = re.split(r"\n\s*Function : ", sass)
@@ -24,6 +25,31 @@ for i, (a, ins) in enumerate(lines):
         tgt = int(t.group(1), 16)
         if tgt < a and tgt in addr_idx:
             body = lines[addr_idx[tgt]:i + 1]
-            if 30 <= len(body) <= 200:
+            if 20 <= len(body) <= 400:
                 ops = Counter(x.split()[0].lstrip("@!P0123456789T ").split(".")[0] if not x.startswith("@") else x.split()[1].split(".")[0] for _, x in body)
                 print(f"loop {tgt:#x}-{a:#x}: {len(body)} instrs  {dict(ops.most_common(12))}")
+
+# Fast path of each hot loop: loop top .. the branch that skips the settle
+# (the first "@!P BRA" after a VOTE.ANY), plus that branch's target .. the
+# backward branch.
+print("fast paths (no candidate needs attention):")
+for i, (a, ins) in enumerate(lines):
+    t = re.search(r"0x([0-9a-f]+)", ins) if "BRA" in ins else None
+    if not t or int(t.group(1), 16) >= a or int(t.group(1), 16) not in addr_idx:
+        continue
+    top = addr_idx[int(t.group(1), 16)]
+    body = lines[top:i + 1]
+    if not (20 <= len(body) <= 400):
+        continue
+    vote = next((j for j in range(top, i) if lines[j][1].startswith("VOTE.ANY")), None)
+    if vote is None:
+        continue
+    skip = next((j for j in range(vote, i) if re.match(r"@!?P\d BRA", lines[j][1])), None)
+    if skip is None:
+        continue
+    tgt = int(re.search(r"0x([0-9a-f]+)", lines[skip][1]).group(1), 16)
+    if tgt not in addr_idx or tgt > a:
+        continue
+    path = lines[top:skip + 1] + lines[addr_idx[tgt]:i + 1]
+    ops = Counter(x.split()[1].split(".")[0] if x.startswith("@") else x.split()[0].split(".")[0] for _, x in path)
+    print(f"  loop {lines[top][0]:#x}: {len(path)} instrs  {dict(ops.most_common(14))}")
