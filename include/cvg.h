@@ -38,10 +38,13 @@ extern "C" {
 #define CVG_ENOMEM 3       /* host or device allocation failed */
 #define CVG_EOVERFLOW 4    /* device pair buffer too small (counts are still valid) */
 #define CVG_EUNSUPPORTED 5 /* option combination not implemented on the device path */
+#define CVG_EUNDECIDED 6   /* Continuous x FrameDiff: a decision depends on the last bits of glibc pow
+                              (|s(p) - s(m)| within ~1e-12 of a threshold); never observed, fails loudly */
 
-/* SearchOptions::delta_mode / delta_basis (search.hpp:81-96).  Supported:
- * Quantized x {TargetSwing, FrameDiff}, Continuous x TargetSwing;
- * Continuous x FrameDiff returns CVG_EUNSUPPORTED. */
+/* SearchOptions::delta_mode / delta_basis (search.hpp:81-96).  All four
+ * combinations run on the device.  Continuous x FrameDiff compares
+ * |s(p) - s(m)| of device-pow signal values against the thresholds with the
+ * device/glibc pow error margin; a decision inside it returns CVG_EUNDECIDED. */
 #define CVG_DELTA_QUANTIZED 0
 #define CVG_DELTA_CONTINUOUS 1
 #define CVG_BASIS_TARGET_SWING 0

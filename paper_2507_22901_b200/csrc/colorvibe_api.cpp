@@ -103,13 +103,15 @@ std::vector<ColorPair> materialize(const cvg_result& r, size_t s, const SrgbColo
         cp.radius = grid.radii[i / na];
         cp.angle = grid.angles[i % na];
         if (continuous) {
-            // continuous_deltas (search.cpp:161-180), TargetSwing basis
+            // continuous_deltas (search.cpp:161-180) on the host's glibc signal values
             double sp[3], sm[3];
             check(cvg_pair_signal(lab, cp.radius, cp.angle, wp, sp, sm));
             const double t[3] = {static_cast<double>(target.r), static_cast<double>(target.g),
                                  static_cast<double>(target.b)};
             double d[3];
-            for (int c = 0; c < 3; ++c) d[c] = std::max(std::abs(sp[c] - t[c]), std::abs(sm[c] - t[c]));
+            for (int c = 0; c < 3; ++c) {
+                d[c] = swing ? std::max(std::abs(sp[c] - t[c]), std::abs(sm[c] - t[c])) : std::abs(sp[c] - sm[c]);
+            }
             cp.deltas = ChannelDeltas{d[0], d[1], d[2]};
         } else {
             cp.deltas = swing ? channel_deltas(target, cp.plus, cp.minus) : frame_deltas(cp.plus, cp.minus);

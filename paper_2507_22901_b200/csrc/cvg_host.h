@@ -288,6 +288,19 @@ double signal_value(double linear);
 // the FP64 hoisted values of the reference (cvg_prep.cpp).
 void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, const Tables& T, SearchConst& S);
 
+// Kernel family of a search (cvg_layout.h Mode): TargetSwing (quantized or
+// continuous) is a per-endpoint interval test (band); Quantized FrameDiff
+// classifies on the codes of both endpoints; Continuous FrameDiff on the
+// difference of the two signal values.
+inline int search_mode(const cvg_search_desc* d) {
+    if (d->delta_basis == CVG_BASIS_TARGET_SWING) return cvg::kModeBand;
+    return d->delta_mode == CVG_DELTA_QUANTIZED ? cvg::kModeCodes : cvg::kModeSignal;
+}
+
+// CVG_EUNDECIDED with the count of continuous-FrameDiff decisions that fell
+// inside the device/glibc pow margin.
+int undecided_fail(unsigned long long n);
+
 // ---------------------------------------------------------------------------
 // Caching allocators (device and pinned host), per context.
 

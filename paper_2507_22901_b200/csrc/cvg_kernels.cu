@@ -188,6 +188,54 @@ __device__ __forceinline__ bool exact_band(const SearchConst* S, const double* l
     return ok;
 }
 
+// signal_value (convert_kernel.hpp:109-112) of an exact linear value, with
+// the radius `e` of |s_dev - s_ref| (s_ref: the reference's glibc result).
+// Clamped values and the linear branch of srgb_oetf (convert_kernel.hpp:81-83)
+// are op-for-op exact (e = 0).  On the pow branch the device pow differs from
+// glibc's by at most 2 (CUDA) + 0.52 (glibc) ulp of t <= 1; propagated through
+// 1.055*t - 0.055 and *255 (one rounding each, 1 ulp apart at most) that is
+// 255 * (1.055 * 3 * 2^-53 + 2 * 2^-52) + 2^-45 < 2.4e-13; e = 5e-13.
+__device__ __forceinline__ double signal_dev(double lin, double& e) {
+    const double x = lin < 0.0 ? 0.0 : (lin > 1.0 ? 1.0 : lin);
+    double y;
+    e = 0.0;
+    if (x <= 0.0031308) {
+        y = __dmul_rn(12.92, x);
+    } else {
+        const double t = pow(x, 1.0 / 2.4);
+        y = __dsub_rn(__dmul_rn(1.055, t), 0.055);
+        if (x != 1.0) e = 5e-13;  // pow(1, y) == 1 exactly on both sides
+    }
+    return __dmul_rn(255.0, y);
+}
+
+// classify_pair (search.cpp:146-157) on continuous FrameDiff deltas
+// |s(p) - s(m)| (continuous_deltas, search.cpp:161-173), decided with the
+// margin of signal_dev: d_dev within e_p + e_m + 2^-44 (rounding of the
+// difference, values < 256) of a threshold is undecided (counted; the call
+// then fails instead of guessing).  lo[c] holds the channel's threshold.
+__device__ __forceinline__ bool signal_pass(const SearchConst* S, const double* lp, const double* lm,
+                                            uint32_t flags, bool& undecided) {
+    bool ok = true;
+    undecided = false;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        double ep, em;
+        const double sp = signal_dev(lp[q], ep);
+        const double sm = signal_dev(lm[q], em);
+        const double d = fabs(__dsub_rn(sp, sm));
+        const double mg = ep + em > 0.0 ? ep + em + 0x1p-44 : 0.0;
+        const double T = __ldg(&S->lo[q]);
+        const bool loud = (flags >> q) & 1;
+        // loud: d > v_th; quiet: d <= low
+        const bool pass = loud ? d > T : d <= T;
+        const bool sure = loud ? (d - mg > T) | (d + mg <= T) : (d + mg <= T) | (d - mg > T);
+        ok &= pass;
+        undecided |= !sure;
+    }
+    return ok;
+}
+
 // classify_pair (search.cpp:146-157) on integer codes, with the integer form
 // of the thresholds (d > v_th <=> d >= k1, d <= low <=> d <= q0).
 __device__ __forceinline__ bool classify_codes(const SearchConst* S, const int* cp, const int* cm,
@@ -360,7 +408,7 @@ __device__ __forceinline__ void load_tables(Smem& sm, const LaunchArgs& A) {
 }
 
 struct Counters {
-    unsigned long long repairs = 0, code_repairs = 0, violations = 0, mismatch = 0, overflow = 0;
+    unsigned long long repairs = 0, code_repairs = 0, violations = 0, mismatch = 0, overflow = 0, undecided = 0;
     float max_ratio = 0.f;
 };
 
@@ -372,6 +420,7 @@ __device__ __forceinline__ void flush_counters(Counters& ct, const LaunchArgs& A
         ct.violations += __shfl_xor_sync(kFull, ct.violations, o);
         ct.mismatch += __shfl_xor_sync(kFull, ct.mismatch, o);
         ct.overflow += __shfl_xor_sync(kFull, ct.overflow, o);
+        ct.undecided += __shfl_xor_sync(kFull, ct.undecided, o);
         ct.max_ratio = fmaxf(ct.max_ratio, __shfl_xor_sync(kFull, ct.max_ratio, o));
     }
     if (lane == 0) {
@@ -380,6 +429,7 @@ __device__ __forceinline__ void flush_counters(Counters& ct, const LaunchArgs& A
         if (ct.violations) atomicAdd(&A.stats->audit_violations, ct.violations);
         if (ct.mismatch) atomicAdd(&A.stats->class_mismatch, ct.mismatch);
         if (ct.overflow) atomicAdd(&A.stats->overflow, ct.overflow);
+        if (ct.undecided) atomicAdd(&A.stats->undecided, ct.undecided);
         if (ct.max_ratio > 0.f) atomicMax(&A.stats->audit_max_ratio_bits, __float_as_uint(ct.max_ratio));
     }
 }
@@ -476,6 +526,14 @@ template <int kMode, int kPath>
 __device__ __forceinline__ bool candidate_pass(const Smem& sm, const SearchConst* S, const Consts& C,
                                                const CodeConsts& CC, const LaunchArgs& A, uint32_t k, uint32_t m,
                                                bool active, Counters& ct) {
+    if (kMode == kModeSignal) {  // every path: FP64 linear values + device pow with its margin
+        double lp[3], lm[3];
+        exact_linear(S, A, k, m, lp, lm);
+        bool undecided;
+        const bool pass = signal_pass(S, lp, lm, C.flags, undecided);
+        if (active) ct.undecided += undecided;
+        return active && pass;
+    }
     if (kMode == kModeCodes) {
         int cp[3], cm[3];
         candidate_codes<kPath>(sm, S, CC, A, k, m, active, cp, cm, ct.repairs, ct);
@@ -958,6 +1016,10 @@ cudaError_t phase1_t(const LaunchArgs& a, int grid, cudaStream_t st) {
     return cudaGetLastError();
 }
 
+// The emit pass of a mode/path pair (continuous FrameDiff decides in FP64 but
+// quantizes passing pairs on the FP32 code path with FP64 repair).
+constexpr int emit_path(int mode, int path) { return mode == kModeSignal ? kPathFast : path; }
+
 template <int kMode, int kPath>
 cudaError_t emit_t(const LaunchArgs& a, int grid, cudaStream_t st) {
     emit_kernel<kMode, kPath><<<grid, kBlock, sizeof(Smem), st>>>(a);
@@ -979,13 +1041,13 @@ cudaError_t launch_t(const LaunchArgs& a, int grid, cudaStream_t st, cudaEvent_t
     e = scan_l(a, st);
     if (e != cudaSuccess) return e;
     if (marks) cudaEventRecord(marks[1], st);
-    return emit_t<kMode, kPath>(a, grid, st);
+    return emit_t<kMode, emit_path(kMode, kPath)>(a, grid, st);
 }
 
 template <int kMode, int kOut, int kPath>
 int occupancy_t() {
     auto f1 = phase1_kernel<kMode, kOut, kPath>;
-    auto f3 = emit_kernel<kMode, kPath>;
+    auto f3 = emit_kernel<kMode, emit_path(kMode, kPath)>;
     cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Smem)));
     cudaFuncSetAttribute(f3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Smem)));
     int blocks = 0;
@@ -999,23 +1061,29 @@ using OccFn = int (*)();
 #define CVG_ROW(M, P) {launch_t<M, kOutPairs, P>, launch_t<M, kOutCounts, P>, launch_t<M, kOutFirst, P>}
 #define CVG_OCC(M, P) {occupancy_t<M, kOutPairs, P>, occupancy_t<M, kOutCounts, P>, occupancy_t<M, kOutFirst, P>}
 
-const LaunchFn kLaunch[2][3][3] = {
+const LaunchFn kLaunch[kModes][3][3] = {
     {CVG_ROW(kModeBand, kPathFast), CVG_ROW(kModeBand, kPathExact), CVG_ROW(kModeBand, kPathAudit)},
     {CVG_ROW(kModeCodes, kPathFast), CVG_ROW(kModeCodes, kPathExact), CVG_ROW(kModeCodes, kPathAudit)},
+    // continuous FrameDiff: one FP64 decision path (all three paths run it)
+    {CVG_ROW(kModeSignal, kPathExact), CVG_ROW(kModeSignal, kPathExact), CVG_ROW(kModeSignal, kPathExact)},
 };
 using Phase1Fn = cudaError_t (*)(const LaunchArgs&, int, cudaStream_t);
 #define CVG_P1(M, P) {phase1_t<M, kOutPairs, P>, phase1_t<M, kOutCounts, P>, phase1_t<M, kOutFirst, P>}
-const Phase1Fn kPhase1[2][3][3] = {
+const Phase1Fn kPhase1[kModes][3][3] = {
     {CVG_P1(kModeBand, kPathFast), CVG_P1(kModeBand, kPathExact), CVG_P1(kModeBand, kPathAudit)},
     {CVG_P1(kModeCodes, kPathFast), CVG_P1(kModeCodes, kPathExact), CVG_P1(kModeCodes, kPathAudit)},
+    {CVG_P1(kModeSignal, kPathExact), CVG_P1(kModeSignal, kPathExact), CVG_P1(kModeSignal, kPathExact)},
 };
-const Phase1Fn kEmit[2][3] = {
+const Phase1Fn kEmit[kModes][3] = {
     {emit_t<kModeBand, kPathFast>, emit_t<kModeBand, kPathExact>, emit_t<kModeBand, kPathAudit>},
     {emit_t<kModeCodes, kPathFast>, emit_t<kModeCodes, kPathExact>, emit_t<kModeCodes, kPathAudit>},
+    // codes of passing pairs: the FP32 code path with FP64 repair, as in the other modes
+    {emit_t<kModeSignal, kPathFast>, emit_t<kModeSignal, kPathFast>, emit_t<kModeSignal, kPathFast>},
 };
-const OccFn kOcc[2][3][3] = {
+const OccFn kOcc[kModes][3][3] = {
     {CVG_OCC(kModeBand, kPathFast), CVG_OCC(kModeBand, kPathExact), CVG_OCC(kModeBand, kPathAudit)},
     {CVG_OCC(kModeCodes, kPathFast), CVG_OCC(kModeCodes, kPathExact), CVG_OCC(kModeCodes, kPathAudit)},
+    {CVG_OCC(kModeSignal, kPathExact), CVG_OCC(kModeSignal, kPathExact), CVG_OCC(kModeSignal, kPathExact)},
 };
 
 }  // namespace

@@ -43,7 +43,7 @@ struct alignas(16) SearchConst {
     // --- FP64 exact path (bit-identical to the reference) ----------------
     double fy, ta, tb, wx, wz;
     double cy64[3];
-    double lo[3], hi[3];
+    double lo[3], hi[3];  // band edges (kModeBand); lo[c] = the channel's threshold, v_th or low (kModeSignal)
 };
 static_assert(sizeof(SearchConst) == 288, "SearchConst layout");
 
@@ -54,11 +54,17 @@ struct Stats {
     unsigned long long audit_violations;
     unsigned long long class_mismatch;
     unsigned long long overflow;
+    unsigned long long undecided;  // kModeSignal: decisions inside the device/glibc pow margin (call fails)
     unsigned int audit_max_ratio_bits;  // float bits, atomicMax on non-negative floats
     unsigned int pad;
 };
 
-enum Mode : int { kModeBand = 0, kModeCodes = 1 };
+// kModeBand: TargetSwing (quantized or continuous), interval test per endpoint;
+// kModeCodes: Quantized x FrameDiff, classify on the codes of both endpoints;
+// kModeSignal: Continuous x FrameDiff, classify on |s(p) - s(m)| of the
+// pre-rounding signal values (FP64 on the device, glibc-pow error margin).
+enum Mode : int { kModeBand = 0, kModeCodes = 1, kModeSignal = 2 };
+constexpr int kModes = 3;
 enum Out : int { kOutPairs = 0, kOutCounts = 1, kOutFirst = 2 };
 enum Path : int { kPathFast = 0, kPathExact = 1, kPathAudit = 2 };
 

@@ -196,9 +196,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
                const SearchConst* pre = nullptr) {
     const Tables& T = tables();
     p->ctx = ctx;
-    // TargetSwing (quantized or continuous) is a per-endpoint interval test:
-    // band mode.  Quantized FrameDiff classifies on the codes of both endpoints.
-    p->mode = d->delta_basis == CVG_BASIS_TARGET_SWING ? cvg::kModeBand : cvg::kModeCodes;
+    p->mode = search_mode(d);
     p->out = d->output;
     p->path = d->path;
     p->n = d->n_searches;
@@ -539,6 +537,12 @@ uint64_t sum_counts(const uint64_t* c, size_t n) {
 
 void result_zero(cvg_result* r) { std::memset(r, 0, sizeof(*r)); }
 
+int undecided_fail(unsigned long long n) {
+    return fail(CVG_EUNDECIDED, std::to_string(n) +
+                                    " continuous FrameDiff decision(s) lie within the device/glibc pow error "
+                                    "margin of a threshold; the device cannot prove the reference's result");
+}
+
 int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
     result_zero(r);
     r->n_searches = p->n;
@@ -551,6 +555,7 @@ int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
     if (int e = plan_collect(p, r->counts, hs)) return e;
     const double t_counts = now_ms();
     const uint64_t total = sum_counts(r->counts, n);
+    if (hs.st.undecided) return undecided_fail(hs.st.undecided);
     if (p->out == cvg::kOutPairs && hs.st.overflow) {
         if (!allow_rerun) {
             r->n_pairs = total;
@@ -735,6 +740,7 @@ int cvg_plan_sync(cvg_plan* p, uint64_t* n_pairs) {
     if (int e = plan_collect(p, p->h_counts, hs)) return e;
     const uint64_t total = sum_counts(p->h_counts, static_cast<size_t>(p->n));
     if (n_pairs) *n_pairs = total;
+    if (hs.st.undecided) return undecided_fail(hs.st.undecided);
     if (p->out == cvg::kOutPairs && hs.st.overflow) return fail(CVG_EOVERFLOW, "pair buffer too small");
     return CVG_OK;
 }

@@ -162,11 +162,6 @@ checked:
     if (static_cast<uint64_t>(d->n_radii) * static_cast<uint64_t>(d->n_angles) >= (1ull << 32)) {
         return fail(CVG_EINVAL, "grid too large: n_radii * n_angles must be < 2^32");
     }
-    if (d->delta_mode == CVG_DELTA_CONTINUOUS && d->delta_basis == CVG_BASIS_FRAME_DIFF) {
-        return fail(CVG_EUNSUPPORTED,
-                    "DeltaMode::Continuous with DeltaBasis::FrameDiff is not implemented on the device path "
-                    "(no CPU fallback)");
-    }
     return CVG_OK;
 }
 
@@ -245,6 +240,27 @@ SignalBand signal_band(int target, double T) {
             prev = v;
         }
     }
+    return b;
+}
+
+// signal_band depends only on (target code, threshold): a batch repeats few
+// pairs (cfg1: 9 targets x 16 thresholds over 756 searches), and each band
+// costs ~380 glibc pow calls, so bands are memoized process-wide.
+SignalBand signal_band_cached(int target, double T) {
+    static std::mutex mu;
+    static std::map<std::pair<int, uint64_t>, SignalBand> cache;
+    uint64_t bits;
+    std::memcpy(&bits, &T, sizeof(bits));
+    const std::pair<int, uint64_t> key(target, bits);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        const auto it = cache.find(key);
+        if (it != cache.end()) return it->second;
+    }
+    const SignalBand b = signal_band(target, T);
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() >= (1u << 16)) cache.clear();
+    cache.emplace(key, b);
     return b;
 }
 
@@ -332,10 +348,14 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
     for (int c = 0; c < 3; ++c) S.t[c] = t[c];
     // make_bands (search.cpp:291-329): exact only for Quantized x TargetSwing.
     for (int c = 0; c < 3; ++c) {
-        if (mode == cvg::kModeBand && continuous) {
+        if (mode == cvg::kModeSignal) {
+            // continuous FrameDiff (search.cpp:146-173): the channel's threshold on |s(p) - s(m)|
+            S.lo[c] = bits[c] ? v_th : low;
+            S.hi[c] = HUGE_VAL;
+        } else if (mode == cvg::kModeBand && continuous) {
             // continuous_deltas (search.cpp:161-180): pass iff |s(x) - t| <= T
             // for both endpoints (quiet, T = low) / not for both (loud, T = v_th)
-            const SignalBand b = signal_band(t[c], bits[c] ? v_th : low);
+            const SignalBand b = signal_band_cached(t[c], bits[c] ? v_th : low);
             S.lo[c] = b.lo;
             S.hi[c] = b.hi;
         } else if (mode != cvg::kModeBand) {

@@ -187,6 +187,7 @@ int search_ranges_fixed(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, i
         uint64_t in_bytes = 0;
         for (int c = 0; c < K; ++c) {
             const cvg::Stats& st = tails[c].st;
+            if (st.undecided && !err) err = undecided_fail(st.undecided);
             agg.band_repairs += st.band_repairs;
             agg.code_repairs += st.code_repairs;
             agg.audit_violations += st.audit_violations;
@@ -233,7 +234,7 @@ int search_pipelined(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, int 
     std::vector<SearchConst> recs(n);
     {
         const Tables& T = tables();
-        const int mode = d->delta_basis == CVG_BASIS_TARGET_SWING ? cvg::kModeBand : cvg::kModeCodes;
+        const int mode = search_mode(d);
         const double rmax = d->radii[d->n_radii - 1];
         parallel_for(n, [&](size_t s) { make_search_const(d, static_cast<int>(s), rmax, mode, T, recs[s]); }, 64);
     }
@@ -291,6 +292,7 @@ int search_pipelined(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, int 
             CVG_CUDA(cudaEventSynchronize(done[c]));
             if (tails[c].st.overflow) return fail(CVG_ECUDA, "pair buffer overflow after resizing");
         }
+        if (tails[c].st.undecided) return undecided_fail(tails[c].st.undecided);
         t_last_done = now_ms();
         const uint64_t tc = tails[c].total;
         const uint64_t seen = cps * lo[c + 1];  // candidates through this chunk

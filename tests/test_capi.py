@@ -92,7 +92,7 @@ GRID = W.uniform_grid(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
     (dict(rn=[0.0]), 1, "r_novib must be in (0, 1]"),
     (dict(rn=[1.5]), 1, "r_novib must be in (0, 1]"),
     (dict(patterns=[0]), 1, "bit pattern has no set bits"),
-    (dict(mode=1, basis=1), 5, "Continuous"),
+    (dict(mode=2), 1, "unknown delta_mode"),
 ])
 def test_validation_mirrors_reference(lib, case, status, msg):
     args = dict(targets=[[170, 170, 170]], patterns=[5], vth=[50.0], rn=[0.5], radii=GRID[0], angles=GRID[1])
@@ -110,6 +110,8 @@ def test_validation_accepts_reference_inputs(lib):
     assert st == 0
     st, _ = _validate(lib, [[170, 170, 170]], [5], [50.0], [0.5], GRID[0], GRID[1], mode=1)  # continuous swing
     assert st == 0
+    st, _ = _validate(lib, [[170, 170, 170]], [5], [50.0], [0.5], GRID[0], GRID[1], mode=1, basis=1)
+    assert st == 0  # continuous frame diff: runs on the device
 
 
 def test_create_without_device_fails_loudly(lib):

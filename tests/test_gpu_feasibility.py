@@ -12,6 +12,7 @@ CONFIGS = [
     '{"version": 1, "delta_basis": "frame_diff"}',
     '{"version": 1, "white_point": [0.9642, 1.0, 0.8251], "v_th": [20, 60.5], "r_novib": [0.3]}',
     '{"version": 1, "delta_mode": "continuous", "v_th": [50], "r_novib": [0.5]}',
+    '{"version": 1, "delta_mode": "continuous", "delta_basis": "frame_diff", "v_th": [50, 100], "r_novib": [0.5]}',
     '{"version": 1, "grid": {"radius": {"min": 0, "max": 100, "step": 1}, '
     '"angle_deg": {"min": 0, "max": 359, "step": 1}}}',
 ]

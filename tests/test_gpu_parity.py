@@ -299,14 +299,54 @@ def test_continuous_api_deltas_match_oracle(cv, ctx, oracle):
             assert [pair.deltas.dr, pair.deltas.dg, pair.deltas.db] == d.tolist()
 
 
-def test_continuous_frame_diff_fails_loudly(cv, ctx):
-    grid = cv.VibrationGrid.uniform(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
+@pytest.mark.parametrize("path", ["fast", "exact"])
+@pytest.mark.parametrize("out", ["pairs", "counts", "first"])
+def test_continuous_frame_diff_bit_exact(ctx, oracle, path, out):
+    """DeltaMode::Continuous x FrameDiff (search.cpp:146-173): |s(p) - s(m)|
+    of device-pow signal values, decided with the glibc-pow margin."""
+    radii, angles = uniform_grid(0.0, 128.0, 2.5, 0.0, 359.0, 1.0)
+    t, p, v, r = [], [], [], []
+    for tg in ([170, 170, 170], [240, 240, 240], [100, 100, 240], [240, 100, 240], [8, 8, 8], [0, 255, 30],
+               [255, 255, 255], [0, 0, 0]):
+        for pat in (1, 2, 4, 5, 6, 7):
+            for vt, rn in ((50.0, 0.5), (100.0, 0.25), (20.5, 0.333), (3.0, 1.0)):
+                t.append(tg); p.append(pat); v.append(vt); r.append(rn)
+    wl = W.Workload("cfd", np.array(t, np.int32), np.array(p, np.int32), np.array(v), np.array(r), radii, angles)
+    res = run(ctx, wl, path=path, mode=1, basis=1, output=out)
+    total = 0
+    for s in range(wl.n_searches):
+        oi, oc, _ = oracle.search(wl.targets[s], int(wl.patterns[s]), wl.v_th[s], wl.r_novib[s], radii, angles,
+                                  delta_mode=1, delta_basis=1, method=0, want_deltas=False)
+        total += len(oi)
+        assert res["counts"][s] == len(oi), s
+        if out == "pairs":
+            a, b = int(res["offsets"][s]), int(res["offsets"][s + 1])
+            assert np.array_equal(res["idx"][a:b], oi), s
+            assert np.array_equal(res["codes"][a:b], oc), s
+        elif out == "first" and len(oi):
+            assert res["first_idx"][s] == oi[0], s
+            assert np.array_equal(res["first_codes"][s], oc[0]), s
+    assert total > 1000
+
+
+def test_continuous_frame_diff_api(cv, ctx, oracle):
+    grid = cv.VibrationGrid.uniform(1.0, 91.0, 5.0, 0.0, 355.0, 5.0)
     opts = cv.SearchOptions()
     opts.delta_mode = cv.DeltaMode.CONTINUOUS
     opts.delta_basis = cv.DeltaBasis.FRAME_DIFF
-    with pytest.raises(RuntimeError, match="Continuous"):
-        cv.batch_search_opts(cv.SrgbColor(170, 170, 170), grid, cv.BitPattern("101"), cv.Thresholds(50.0, 0.5),
-                             opts)
+    n = 0
+    for t, p in (([170, 170, 170], "101"), ([100, 100, 240], "111"), ([240, 100, 100], "100"), ([8, 8, 8], "010")):
+        args = (cv.SrgbColor(*t), grid, cv.BitPattern(p), cv.Thresholds(50.0, 0.5))
+        got = cv.batch_search_opts(*args, opts)
+        assert got == cv.serial_search_opts(*args, opts)
+        oi, oc, od = oracle.search(t, W.bits(p), 50.0, 0.5, grid.radii, grid.angles, delta_mode=1, delta_basis=1,
+                                   method=0)
+        assert len(got) == len(oi)
+        n += len(got)
+        for pair, c, d in zip(got, oc, od):
+            assert [pair.plus.r, pair.plus.g, pair.plus.b, pair.minus.r, pair.minus.g, pair.minus.b] == c.tolist()
+            assert [pair.deltas.dr, pair.deltas.dg, pair.deltas.db] == d.tolist()
+    assert n > 0
 
 
 def test_batch_many_equals_single(cv, ctx):
