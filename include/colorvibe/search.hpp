@@ -82,7 +82,7 @@ struct ColorPair {
 
 enum class DeltaMode {
     Quantized,   // deltas between 8-bit codes (default)
-    Continuous,  // pre-quantization deltas (device path for TargetSwing; FrameDiff throws)
+    Continuous,  // pre-quantization deltas (device path for both bases)
 };
 
 enum class DeltaBasis {
