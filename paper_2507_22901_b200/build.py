@@ -24,6 +24,9 @@ BUILD = os.path.join(PKG, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CUDA_INC = "/usr/local/cuda/include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# experiment hook: extra -D flags for the search kernels (e.g. CVG_KERNEL_DEFS="-DCVG_GROUP=4");
+# the caller removes _build/cvg_kernels.o so that the object is rebuilt
+KERNEL_DEFS = os.environ.get("CVG_KERNEL_DEFS", "").split()
 # The reference's value-safe FP flags (proj/src/CMakeLists.txt:21-43): no FMA
 # contraction in host code, so host-side tables carry the reference's bits.
 HOST_FP = ["-ffp-contract=off", "-fno-math-errno", "-fno-trapping-math"]
@@ -80,7 +83,7 @@ def _objects() -> list[tuple[str, list[str], list[str], str | None]]:
     src = lambda n: os.path.join(CSRC, n)  # noqa: E731
     return [
         (o("cvg_kernels.o"), [src("cvg_kernels.cu")] + HEADERS,
-         [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xptxas", "-v", "-Xcompiler", "-fPIC",
+         [NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xptxas", "-v", "-Xcompiler", "-fPIC", *KERNEL_DEFS,
           "-I" + INCLUDE, "-c", src("cvg_kernels.cu"), "-o", o("cvg_kernels.o")],
          o("ptxas.log")),
         (o("cvg_codec.o"), [src("cvg_codec.cu")] + HEADERS,

@@ -29,6 +29,7 @@
 
 #include <cstdint>
 
+
 #include "cvg_internal.h"
 #include "cvg_layout.h"
 
@@ -626,40 +627,52 @@ __device__ __forceinline__ void band_chunk(const Consts& C, float r, float2 sc, 
 
 // Hot loop: FAST path, band mode, kL loud channels, `nch` full 32-candidate
 // chunks of radius row k starting at angle m0 (na % 32 == 0: chunks never
-// straddle rows).  Two chunks per iteration share one vote (ILP across
-// chunks).  Per candidate: 1 LDG (L1-resident trig, prefetched two chunks
-// ahead), then either 24 FMA-pipe ops (4 f, 8 cube or linear, 12 matrix) + 4
-// min/max, or, in kCubeOnly rows (r < rcube: never the linear branch of
-// f^-1), the sum/difference form's 25 ops + 1-2 min/max (band_cube).
+// straddle rows).  Four chunks per iteration share one vote and one loop
+// branch (ILP across chunks); their trig loads are issued together at the
+// top of the iteration (L1-resident table; other warps hide the latency).
+// Per candidate: 1 LDG, then either 24 FMA-pipe ops (4 f, 8 cube or linear,
+// 12 matrix) + 4 min/max, or, in kCubeOnly rows (r < rcube: never the
+// linear branch of f^-1), the sum/difference form's 25 ops + 1-2 min/max
+// (band_cube).  Measured against two chunks per vote with a two-chunk-ahead
+// prefetch (cfg1 / cfg3 / cfg2 / cfg4): 4 per vote +2.5 / +6.3 / +1.5 / +7.4%;
+// 2 per vote without prefetch +2 / +2.6 / -3.8%; 3: +0.7 / +2 / -1.9%;
+// 6: -7 / +5 / +2.5%; 8: -17 / +4 / +1.6%; 4 with a next-group prefetch
+// (register rotation): -6 / 0 / +1.8%.
 template <int kL, bool kCubeOnly, int kOut>
 __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
                                          float r, uint32_t m0, uint32_t nch, uint32_t off, uint16_t* list,
                                          uint32_t& cnt, uint32_t* first, Counters& ct, unsigned lane,
                                          unsigned lane_lt) {
+    constexpr uint32_t G = 4;
     const float2* __restrict__ trig = reinterpret_cast<const float2*>(A.trig_f);
     const uint32_t mb = m0 + lane;
     uint32_t ix = mb;
-    const uint32_t iend = mb + 32u * (nch & ~1u);
-    float2 na_ = __ldg(trig + ix), nb_ = __ldg(trig + ix + 32);
-#pragma unroll 1  // code size: an unrolled two-pair body (ping-pong prefetch, no register
-                  // rotation) measured, with loud-count-major claims: cfg1 -1.4%, cfg3 +4.4%,
-                  // cfg2 +8%; without them 25% slower (instruction cache).  Kept rolled for cfg1.
-    for (; ix != iend; ix += 64) {
-        const float2 sa = na_, sb = nb_;
-        na_ = __ldg(trig + ix + 64);  // prefetch; the table is padded by 128 entries
-        nb_ = __ldg(trig + ix + 96);
-        float la_, qa_, lb_, qb_;
-        band_chunk<kL, kCubeOnly>(C, r, sa, la_, qa_);
-        band_chunk<kL, kCubeOnly>(C, r, sb, lb_, qb_);
-        if (__any_sync(kFull, band_attention(C, la_, qa_) | band_attention(C, lb_, qb_))) {
+    const uint32_t iend = mb + 32u * (nch - nch % G);
+#pragma unroll 1
+    for (; ix != iend; ix += 32 * G) {
+        float2 sv[G];
+        float lv[G], qv[G];
+#pragma unroll
+        for (uint32_t g = 0; g < G; ++g) sv[g] = __ldg(trig + ix + 32 * g);
+        bool att = false;
+#pragma unroll
+        for (uint32_t g = 0; g < G; ++g) {
+            band_chunk<kL, kCubeOnly>(C, r, sv[g], lv[g], qv[g]);
+            att |= band_attention(C, lv[g], qv[g]);
+        }
+        if (__any_sync(kFull, att)) {
             const uint32_t d = ix - mb;
-            band_settle<kOut>(S, C, A, k, ix, la_, qa_, off + lane + d, list, cnt, first, ct, lane_lt);
-            band_settle<kOut>(S, C, A, k, ix + 32, lb_, qb_, off + lane + d + 32, list, cnt, first, ct, lane_lt);
+#pragma unroll
+            for (uint32_t g = 0; g < G; ++g) {
+                band_settle<kOut>(S, C, A, k, ix + 32 * g, lv[g], qv[g], off + lane + d + 32 * g, list, cnt, first, ct,
+                                  lane_lt);
+            }
         }
     }
-    if (nch & 1u) {
+#pragma unroll 1
+    for (uint32_t j = nch % G; j; --j, ix += 32) {
         float la_, qa_;
-        band_chunk<kL, kCubeOnly>(C, r, na_, la_, qa_);
+        band_chunk<kL, kCubeOnly>(C, r, __ldg(trig + ix), la_, qa_);
         if (__any_sync(kFull, band_attention(C, la_, qa_))) {
             band_settle<kOut>(S, C, A, k, ix, la_, qa_, off + lane + (ix - mb), list, cnt, first, ct, lane_lt);
         }

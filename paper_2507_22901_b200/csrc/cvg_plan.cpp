@@ -178,7 +178,7 @@ GridTables make_grid_tables(const cvg_search_desc* d) {
     GridTables g;
     g.radii_f.resize(d->n_radii);
     for (int k = 0; k < d->n_radii; ++k) g.radii_f[k] = static_cast<float>(d->radii[k]);
-    // float trig table padded by 128 entries: the hot loop prefetches two chunks ahead
+    // float trig table padded by 128 entries (loads of a partial last chunk stay in bounds)
     g.trig_f.assign(2 * (static_cast<size_t>(d->n_angles) + 128), 0.0f);
     g.trig_d.resize(2 * static_cast<size_t>(d->n_angles));
     for (int j = 0; j < d->n_angles; ++j) {  // search.cpp:414-419

@@ -39,7 +39,7 @@ for i, (a, ins) in enumerate(lines):
         continue
     top = addr_idx[int(t.group(1), 16)]
     body = lines[top:i + 1]
-    if not (20 <= len(body) <= 400):
+    if not (20 <= len(body) <= 3000):
         continue
     vote = next((j for j in range(top, i) if lines[j][1].startswith("VOTE.ANY")), None)
     if vote is None:
