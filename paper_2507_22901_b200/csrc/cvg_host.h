@@ -373,7 +373,7 @@ struct cvg_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;  // D2H of finished chunks while later chunks compute
     cudaStream_t tail_stream = nullptr;  // per-range counts/totals of a pipelined search
-    cudaStream_t aux_stream = nullptr;   // second range view of split plans
+    cudaStream_t aux_stream = nullptr;   // emits of a streamed search (concurrent with phase 1)
     std::recursive_mutex mu;
     // pair total of the last pipelined search of the same shape: sizes the
     // pinned result so repeated searches never grow it
@@ -406,11 +406,9 @@ struct cvg_plan {
     void* d_out_codes = nullptr;
     uint64_t capacity = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-    // PAIRS: after phase 1, after the scan; split: [0] phase 1 of view a, [1]
-    // phase 1 of view b, [2] scan of view a (fork/join), [3] join of view b
+    // PAIRS: [0] after phase 1, [1] after the scan (pipelined searches use [2], [3] per view)
     cudaEvent_t marks[4] = {nullptr, nullptr, nullptr, nullptr};
-    bool split = false;
-    LaunchArgs va{}, vb{};  // the two range views of a split plan
+    bool external_out = false;  // the caller supplies the pair buffers (streamed search): no reserve
     bool ran = false;
     cudaStream_t last_stream = nullptr;
     uint64_t input_bytes = 0;

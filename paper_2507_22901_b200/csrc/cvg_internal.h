@@ -18,7 +18,8 @@ cudaError_t launch_search(const LaunchArgs& a, int mode, int out, int path, int 
 // The three PAIRS-mode kernels separately (range views on two streams).
 cudaError_t launch_phase1(const LaunchArgs& a, int mode, int out, int path, int grid, cudaStream_t st);
 cudaError_t launch_scan(const LaunchArgs& a, cudaStream_t st);
-cudaError_t launch_emit(const LaunchArgs& a, int mode, int path, int grid, cudaStream_t st);
+// threads: any multiple of 32 up to kBlock (streamed searches run 128-thread emits beside phase 1)
+cudaError_t launch_emit(const LaunchArgs& a, int mode, int path, int grid, cudaStream_t st, int threads = kBlock);
 // Resident blocks per SM for that instantiation; also opts the kernel into its
 // dynamic shared memory size on the current device (call before launching).
 int search_blocks_per_sm(int mode, int out, int path);

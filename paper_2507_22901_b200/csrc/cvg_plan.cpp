@@ -140,33 +140,36 @@ void dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, s
             },
             1);
     } else {
-        struct Key {
-            uint32_t rgb;
-            int32_t bits;
-            double v, r;
-            bool operator==(const Key& o) const {
-                return rgb == o.rgb && bits == o.bits && std::memcmp(&v, &o.v, 8) == 0 &&
-                       std::memcmp(&r, &o.r, 8) == 0;
-            }
+        // Open-addressing table of search ids keyed by (color, pattern, v_th,
+        // r_novib) bits: no per-entry allocation (4096 searches: ~40 us
+        // instead of ~450 us with std::unordered_map).
+        auto same = [&](size_t a, size_t b) {
+            return key24(a) == key24(b) && d->pattern_bits[a] == d->pattern_bits[b] &&
+                   std::memcmp(&d->v_th[a], &d->v_th[b], 8) == 0 && std::memcmp(&d->r_novib[a], &d->r_novib[b], 8) == 0;
         };
-        struct Hash {
-            size_t operator()(const Key& k) const {
-                uint64_t a, b;
-                std::memcpy(&a, &k.v, 8);
-                std::memcpy(&b, &k.r, 8);
-                uint64_t h = (static_cast<uint64_t>(k.rgb) << 3 | static_cast<uint64_t>(k.bits)) * 0x9E3779B97F4A7C15ull;
-                h ^= a + 0x632BE59BD9B4E019ull + (h << 6) + (h >> 2);
-                h ^= b + 0x85157AF5ull + (h << 6) + (h >> 2);
-                return static_cast<size_t>(h);
-            }
+        auto hash = [&](size_t s) {
+            uint64_t a, b;
+            std::memcpy(&a, &d->v_th[s], 8);
+            std::memcpy(&b, &d->r_novib[s], 8);
+            uint64_t h = (static_cast<uint64_t>(key24(s)) << 3 | static_cast<uint64_t>(d->pattern_bits[s] & 7)) *
+                         0x9E3779B97F4A7C15ull;
+            h ^= (a + 0x632BE59BD9B4E019ull + (h << 6) + (h >> 2)) * 0xBF58476D1CE4E5B9ull;
+            h ^= (b + 0x85157AF5ull + (h << 6) + (h >> 2)) * 0x94D049BB133111EBull;
+            return h ^ (h >> 31);
         };
-        std::unordered_map<Key, int32_t, Hash> seen;
-        seen.reserve(static_cast<size_t>(n) * 2);
+        size_t cap = 16;
+        while (cap < 2 * static_cast<size_t>(n)) cap <<= 1;
+        std::vector<int32_t> slot(cap, -1);  // search id of the record's representative
         for (int s = 0; s < n; ++s) {
-            const Key k{key24(static_cast<size_t>(s)), d->pattern_bits[s], d->v_th[s], d->r_novib[s]};
-            auto [it, fresh] = seen.emplace(k, static_cast<int32_t>(uniq.size()));
-            if (fresh) uniq.push_back(s);
-            sc_index[s] = static_cast<uint32_t>(it->second);
+            size_t i = hash(static_cast<size_t>(s)) & (cap - 1);
+            while (slot[i] >= 0 && !same(static_cast<size_t>(slot[i]), static_cast<size_t>(s))) i = (i + 1) & (cap - 1);
+            if (slot[i] < 0) {
+                slot[i] = s;
+                sc_index[s] = static_cast<uint32_t>(uniq.size());
+                uniq.push_back(s);
+            } else {
+                sc_index[s] = sc_index[slot[i]];
+            }
         }
     }
     if (static_cast<int>(uniq.size()) == n) {
@@ -194,7 +197,23 @@ GridTables make_grid_tables(const cvg_search_desc* d) {
 
 int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTables* grid = nullptr,
                const SearchConst* pre = nullptr) {
+    const double tb0 = now_ms();
+    static const bool trace = std::getenv("CVG_TRACE") != nullptr;
+    std::vector<std::pair<const char*, double>> tl;
+    auto mark = [&](const char* w) {
+        if (trace) tl.emplace_back(w, now_ms() - tb0);
+    };
+    struct TraceOut {
+        std::vector<std::pair<const char*, double>>& tl;
+        ~TraceOut() {
+            if (tl.empty()) return;
+            std::string line = "[cvg build]";
+            for (auto& [w, t] : tl) line += std::string(" ") + w + "@" + std::to_string(t).substr(0, 6);
+            std::fprintf(stderr, "%s\n", line.c_str());
+        }
+    } trace_out{tl};
     const Tables& T = tables();
+    mark("tables");
     p->ctx = ctx;
     p->mode = search_mode(d);
     p->out = d->output;
@@ -215,19 +234,15 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     // Per-search constants, deduplicated: searches with the same (target,
     // pattern, v_th, r_novib) share one record (per-pixel batches repeat
     // colors); every candidate of every search is still evaluated.
+    // The records are built straight into the pinned staging block below.
     std::vector<uint32_t> sc_index;
-    std::vector<SearchConst> sc_own;
-    const SearchConst* sc_ptr = pre;  // one record per search, built by the caller
+    std::vector<int32_t> uniq;  // representative search of each record
     size_t n_sc = static_cast<size_t>(p->n);
     if (!pre) {
-        std::vector<int32_t> uniq;  // representative search of each record
         dedup_searches(d, sc_index, uniq);
-        sc_own.resize(uniq.size());
-        const double rmax = d->radii[p->nr - 1];
-        parallel_for(uniq.size(), [&](size_t u) { make_search_const(d, uniq[u], rmax, p->mode, T, sc_own[u]); });
-        sc_ptr = sc_own.data();
-        n_sc = sc_own.size();
+        n_sc = uniq.size();
     }
+    mark("dedup");
     p->n_unique = static_cast<int32_t>(n_sc);
     GridTables own;
     if (!grid) {
@@ -237,6 +252,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     const std::vector<float>& radii_f = grid->radii_f;
     const std::vector<float>& trig_f = grid->trig_f;
     const std::vector<double>& trig_d = grid->trig_d;
+    mark("grid");
 
     // Claim order (band mode, more than one loud count in the batch): all
     // tiles of the searches with one loud count, then the next, so the warps
@@ -284,7 +300,16 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         ctx->host.release(stage);
         return fail(CVG_ENOMEM, "allocation of the search tables failed");
     }
-    std::memcpy(stage + o_sc, sc_ptr, sizeof(SearchConst) * n_sc);
+    p->stage = stage;  // released with the plan (also if a record throws below)
+    mark("alloc");
+    if (pre) {
+        std::memcpy(stage + o_sc, pre, sizeof(SearchConst) * n_sc);
+    } else {
+        auto* recs = reinterpret_cast<SearchConst*>(stage + o_sc);
+        const double rmax = d->radii[p->nr - 1];
+        parallel_for(n_sc, [&](size_t u) { make_search_const(d, uniq[u], rmax, p->mode, T, recs[u]); }, 8);
+    }
+    mark("records");
     if (!sc_index.empty()) {
         const size_t m = sc_index.size(), parts = m >= (1u << 20) ? 16 : 1;
         parallel_for(
@@ -318,10 +343,10 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.guess = at<const uint8_t>(p->d_const, o_gs);
     // No sync: the staging block stays with the plan until it is released,
     // which happens after the stream has passed this copy.
-    p->stage = stage;
     cudaError_t e = cudaMemcpyAsync(p->d_const, stage, bytes, cudaMemcpyHostToDevice, ctx->stream);
     if (e != cudaSuccess) return cuda_fail(e, "upload of the search tables");
     p->t_upload_end = now_ms();
+    mark("upload");
 
     for (int i = 0; i < 9; ++i) A.minv[i] = kXyzToRgb.m[i / 3][i % 3];
     A.n_searches = p->n;
@@ -334,7 +359,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.n_tiles = n_tiles;
 
     // ---- per-run workspace --------------------------------------------------
-    // zeroed each run:  status[n_scan_blocks] | tickets[8] | counts[n] | stats | total | total_a | total_b
+    // zeroed each run:  status[n_scan_blocks] | tickets[8] | counts[n] | stats | total
     // written each run: tile_count[n_tiles] | tile_base[n_tiles] | worklist   (PAIRS)
     const bool pairs = p->out == cvg::kOutPairs;
     const int per_sm = cvg::search_blocks_per_sm(p->mode, p->out, p->path);
@@ -343,28 +368,13 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         return fail(CVG_ECUDA, std::string("search kernel cannot be resident on this device (") +
                                    cudaGetErrorString(le) + "); sm_100a image required");
     }
-    // Two range views on two streams (PAIRS): the second range's phase 1
-    // fills the first's tail, and the first's scan + emit fill the second's.
-    // Measured neutral on cfg1/cfg2/cfg3 (the second range's persistent
-    // blocks hold every slot until its own tail, so the first range's emit
-    // only starts there), hence off unless CVG_SPLIT=1.
-    static const bool allow_split = [] {
-        const char* e = std::getenv("CVG_SPLIT");
-        return e && std::atoi(e) != 0;
-    }();
-    const uint64_t resident_warps = static_cast<uint64_t>(per_sm) * ctx->sms * cvg::kWarpsPerBlock;
-    p->split = allow_split && pairs && p->n >= 2 && n_tiles >= 8 * resident_warps;
-    const uint32_t n_a = p->split ? static_cast<uint32_t>(p->n / 2) : static_cast<uint32_t>(p->n);
-    const uint64_t tiles_a = static_cast<uint64_t>(n_a) * tps, tiles_b = n_tiles - tiles_a;
-    const uint64_t scan_a = pairs ? (tiles_a + cvg::kScanTile - 1) / cvg::kScanTile : 0;
-    const uint64_t scan_b = p->split ? (tiles_b + cvg::kScanTile - 1) / cvg::kScanTile : 0;
+    const uint64_t scan_blocks = pairs ? (n_tiles + cvg::kScanTile - 1) / cvg::kScanTile : 0;
     Layout W;
-    const size_t o_st = W.take(sizeof(unsigned long long) * (scan_a + scan_b));
+    const size_t o_st = W.take(sizeof(unsigned long long) * scan_blocks);
     const size_t o_tk = W.take(sizeof(unsigned int) * 8);
     const size_t o_ct = W.take(sizeof(unsigned long long) * p->n);
     const size_t o_ss = W.take(sizeof(cvg::Stats));
     const size_t o_to = W.take(sizeof(unsigned long long));  // stats+total read back as one ChunkTail
-    const size_t o_ta = W.take(sizeof(unsigned long long) * 2);  // per-view totals (split)
     p->work_bytes = W.off;  // memset span
     const size_t o_tc = W.take(sizeof(uint32_t) * (pairs ? n_tiles : 0));
     const size_t o_tb = W.take(sizeof(unsigned long long) * (pairs ? n_tiles : 0));
@@ -400,27 +410,13 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         A.first_codes = at<uint8_t>(p->d_first, o_fc);
     }
 
-    if (p->split) {
-        unsigned long long* totals = at<unsigned long long>(p->d_work, o_ta);
-        A.claim_order = nullptr;  // range views claim in search order
-        p->va = A;
-        p->va.range_searches = n_a;
-        p->va.n_tiles = tiles_a;
-        p->va.total = totals;
-        p->vb = A;
-        p->vb.search_begin = n_a;
-        p->vb.range_searches = static_cast<uint32_t>(p->n) - n_a;
-        p->vb.tile_begin = tiles_a;
-        p->vb.n_tiles = tiles_b;
-        p->vb.status = A.status + scan_a;
-        p->vb.ticket = A.ticket + 4;
-        p->vb.total = totals + 1;
-        p->vb.worklist = A.worklist + tiles_a * (cvg::kTile / cvg::kEmitSpan);
-        p->vb.base_offset = totals;
-        p->vb.grand_total = A.total;
-    }
     const uint64_t want = (n_tiles + cvg::kWarpsPerBlock - 1) / cvg::kWarpsPerBlock;
-    p->grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(per_sm) * ctx->sms, want));
+    static const int cap_per_sm = [] {
+        const char* e = std::getenv("CVG_BLOCKS_PER_SM");  // tuning override (occupancy experiments)
+        return e ? std::atoi(e) : 0;
+    }();
+    const int use_per_sm = cap_per_sm > 0 ? std::min(cap_per_sm, per_sm) : per_sm;
+    p->grid = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(use_per_sm) * ctx->sms, want));
     if (p->grid < 1) p->grid = 1;
     for (cudaEvent_t* ev : {&p->ev0, &p->ev1, &p->marks[0], &p->marks[1], &p->marks[2], &p->marks[3]}) {
         if (!ctx->events.empty()) {
@@ -431,7 +427,8 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         }
     }
 
-    if (p->out == cvg::kOutPairs) {
+    mark("workspace");
+    if (p->out == cvg::kOutPairs && !p->external_out) {
         // Initial capacity: every candidate when it fits in half the free memory.
         const uint64_t fit = static_cast<uint64_t>(ctx->total_mem / 4 / 10);  // a quarter of HBM at most
         uint64_t cap = std::min<uint64_t>(p->candidates, std::max<uint64_t>(fit, 1u << 20));
@@ -477,31 +474,8 @@ int plan_enqueue(cvg_plan* p, cudaStream_t st) {
     CVG_CUDA(cudaMemsetAsync(p->d_work, 0, p->work_bytes, st));
     if (p->out == cvg::kOutFirst) CVG_CUDA(cudaMemsetAsync(p->d_first, 0xff, static_cast<size_t>(p->n) * 4, st));
     CVG_CUDA(cudaEventRecord(p->ev0, st));
-    if (p->split) {
-        // the views copy the output buffers, which cvg_plan_reserve may have replaced
-        for (LaunchArgs* v : {&p->va, &p->vb}) {
-            v->out_idx = p->args.out_idx;
-            v->out_codes = p->args.out_codes;
-            v->capacity = p->args.capacity;
-        }
-        cudaStream_t aux = p->ctx->aux_stream;
-        CVG_CUDA(cudaStreamWaitEvent(aux, p->ev0, 0));
-        CVG_CUDA(cvg::launch_phase1(p->va, p->mode, p->out, p->path, p->grid, st));
-        CVG_CUDA(cudaEventRecord(p->marks[0], st));
-        CVG_CUDA(cvg::launch_phase1(p->vb, p->mode, p->out, p->path, p->grid, aux));
-        CVG_CUDA(cudaEventRecord(p->marks[1], aux));
-        CVG_CUDA(cvg::launch_scan(p->va, st));
-        CVG_CUDA(cudaEventRecord(p->marks[2], st));
-        CVG_CUDA(cvg::launch_emit(p->va, p->mode, p->path, p->grid, st));
-        CVG_CUDA(cvg::launch_scan(p->vb, aux));
-        CVG_CUDA(cudaStreamWaitEvent(aux, p->marks[2], 0));  // view b's pairs start after view a's total
-        CVG_CUDA(cvg::launch_emit(p->vb, p->mode, p->path, p->grid, aux));
-        CVG_CUDA(cudaEventRecord(p->marks[3], aux));
-        CVG_CUDA(cudaStreamWaitEvent(st, p->marks[3], 0));
-    } else {
-        CVG_CUDA(cvg::launch_search(p->args, p->mode, p->out, p->path, p->grid, st, p->marks));
-        if (p->out == cvg::kOutFirst) CVG_CUDA(cvg::launch_first_codes(p->args, st));
-    }
+    CVG_CUDA(cvg::launch_search(p->args, p->mode, p->out, p->path, p->grid, st, p->marks));
+    if (p->out == cvg::kOutFirst) CVG_CUDA(cvg::launch_first_codes(p->args, st));
     CVG_CUDA(cudaEventRecord(p->ev1, st));
     return CVG_OK;
 }
@@ -802,17 +776,6 @@ int cvg_plan_last_phase_ms(cvg_plan* p, float* phase1_ms, float* scan_ms, float*
     CVG_CUDA(cudaEventSynchronize(p->ev1));
     if (p->out != cvg::kOutPairs) return cudaEventElapsedTime(phase1_ms, p->ev0, p->ev1) == cudaSuccess
                                              ? CVG_OK : fail(CVG_ECUDA, "event timing failed");
-    if (p->split) {
-        // phase 1 = until both views' phase 1 ended; scan + emit = the rest
-        // (view a's scan and emit overlap view b's phase 1 and are not split out)
-        float a = 0.f, b = 0.f, all = 0.f;
-        CVG_CUDA(cudaEventElapsedTime(&a, p->ev0, p->marks[0]));
-        CVG_CUDA(cudaEventElapsedTime(&b, p->ev0, p->marks[1]));
-        CVG_CUDA(cudaEventElapsedTime(&all, p->ev0, p->ev1));
-        *phase1_ms = std::max(a, b);
-        *emit_ms = all - *phase1_ms;
-        return CVG_OK;
-    }
     CVG_CUDA(cudaEventElapsedTime(phase1_ms, p->ev0, p->marks[0]));
     CVG_CUDA(cudaEventElapsedTime(scan_ms, p->marks[0], p->marks[1]));
     CVG_CUDA(cudaEventElapsedTime(emit_ms, p->marks[1], p->ev1));
@@ -821,7 +784,6 @@ int cvg_plan_last_phase_ms(cvg_plan* p, float* phase1_ms, float* scan_ms, float*
 
 int cvg_plan_launches(const cvg_plan* p) {
     if (!p || p->empty) return 0;
-    if (p->split) return 6;
     return p->out == cvg::kOutPairs ? 3 : p->out == cvg::kOutFirst ? 2 : 1;
 }
 

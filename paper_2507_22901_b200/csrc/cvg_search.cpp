@@ -225,209 +225,253 @@ int search_ranges_fixed(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, i
     return err;
 }
 
+// One plan for the whole batch (constants and grid tables uploaded once),
+// run as K search-range views back to back on the compute stream: phase 1,
+// scan and emit of view c, then view c+1 with no host work in between.  The
+// tail stream reads each view's counts and [stats | total] behind its emit;
+// the host then queues the copy of the view's pairs (one contiguous slice of
+// the canonical result, at the running total) on the copy stream, so the
+// D2H engine drains view c while views c+1.. compute.  Only the first
+// view's kernels and the last view's copy are exposed.
 int search_pipelined(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, int K) {
     const double t0 = now_ms();
     const size_t n = static_cast<size_t>(d->n_searches);
     const uint64_t cps = static_cast<uint64_t>(d->n_radii) * static_cast<uint64_t>(d->n_angles);
-    const GridTables grid = make_grid_tables(d);
-    // every record up front, on all cores (ranges are too small to thread well)
-    std::vector<SearchConst> recs(n);
-    {
-        const Tables& T = tables();
-        const int mode = search_mode(d);
-        const double rmax = d->radii[d->n_radii - 1];
-        parallel_for(n, [&](size_t s) { make_search_const(d, static_cast<int>(s), rmax, mode, T, recs[s]); }, 64);
+    const uint32_t tps = static_cast<uint32_t>((cps + cvg::kTile - 1) / cvg::kTile);
+    const uint64_t sig[4] = {n, cps, static_cast<uint64_t>(d->delta_basis), static_cast<uint64_t>(d->path)};
+    const bool hinted = std::equal(sig, sig + 4, ctx->hint_sig);
+    cvg_plan p;
+    p.external_out = true;
+    if (int e = plan_build_safe(ctx, d, &p)) {
+        plan_release(&p);
+        return e;
     }
-    const double t_recs = now_ms();
+    const double t_built = now_ms();
+    struct Cleanup {
+        cvg_ctx* ctx;
+        cvg_plan* p;
+        std::vector<void*> host;
+        std::vector<cudaEvent_t> events;
+        void* dev = nullptr;
+        ~Cleanup() {
+            cudaStreamSynchronize(ctx->copy_stream);
+            cudaStreamSynchronize(ctx->tail_stream);
+            cudaStreamSynchronize(ctx->stream);
+            for (void* h : host) ctx->host.release(h);
+            for (cudaEvent_t e : events) ctx->events.push_back(e);
+            ctx->dev.release(dev);
+            plan_release(p);
+        }
+    } cl{ctx, &p, {}, {}, nullptr};
+    auto event = [&]() -> cudaEvent_t {
+        cudaEvent_t e = nullptr;
+        if (!ctx->events.empty()) {
+            e = ctx->events.back();
+            ctx->events.pop_back();
+        } else if (cudaEventCreate(&e) != cudaSuccess) {
+            return nullptr;
+        }
+        cl.events.push_back(e);
+        return e;
+    };
+    // device pair buffer: the previous total of this shape (+25%), else
+    // plan_reserve's default; a view that overflows reruns the batch at the
+    // exact size
+    {
+        const uint64_t fit = static_cast<uint64_t>(ctx->total_mem / 4 / 10);
+        const uint64_t cap = hinted ? ctx->hint_pairs + ctx->hint_pairs / 4 + (1u << 16)
+                                    : std::min<uint64_t>(p.candidates, std::max<uint64_t>(fit, 1u << 20));
+        if (int e = plan_reserve(&p, cap)) return e;
+    }
+
+    // ---- per-view workspace: [Stats | total | tickets] x K | cum[K+1] | status | claim ----
+    const std::vector<size_t> lo = ramp_bounds(n, K);
+    constexpr size_t kHdr = 512;
+    size_t status_words = 0;
+    for (int c = 0; c < K; ++c) {
+        status_words += ((lo[c + 1] - lo[c]) * tps + cvg::kScanTile - 1) / cvg::kScanTile;
+    }
+    const size_t o_cum = kHdr * K, o_st = o_cum + 8 * (K + 1), o_claim = o_st + 8 * status_words;
+    const size_t vbytes = o_claim + 4 * n;
+    auto* stage = static_cast<unsigned char*>(ctx->host.alloc(vbytes));
+    auto* tails = static_cast<unsigned char*>(ctx->host.alloc(kHdr * K));
+    cl.host = {stage, tails};
+    cl.dev = ctx->dev.alloc(vbytes);
     r->n_searches = d->n_searches;
     r->counts = static_cast<uint64_t*>(ctx->host.alloc(sizeof(uint64_t) * n));
     r->offsets = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (n + 1)));
-    auto* tails = static_cast<ChunkTail*>(ctx->host.alloc(sizeof(ChunkTail) * K));
-    if (!r->counts || !r->offsets || !tails) {
-        ctx->host.release(tails);
-        return fail(CVG_ENOMEM, "host allocation failed");
+    if (!stage || !tails || !cl.dev || !r->counts || !r->offsets) return fail(CVG_ENOMEM, "allocation failed");
+    auto* dv = static_cast<unsigned char*>(cl.dev);
+    std::memset(stage, 0, o_claim);
+    auto* claim = reinterpret_cast<uint32_t*>(stage + o_claim);
+    std::vector<LaunchArgs> views(K, p.args);
+    size_t st_off = 0;
+    for (int c = 0; c < K; ++c) {
+        LaunchArgs& V = views[c];
+        const size_t b = lo[c], e = lo[c + 1];
+        V.search_begin = static_cast<uint32_t>(b);
+        V.range_searches = static_cast<uint32_t>(e - b);
+        V.tile_begin = static_cast<uint64_t>(b) * tps;
+        V.n_tiles = static_cast<uint64_t>(e - b) * tps;
+        V.stats = reinterpret_cast<cvg::Stats*>(dv + kHdr * c);
+        V.total = reinterpret_cast<unsigned long long*>(dv + kHdr * c + 256);
+        V.ticket = reinterpret_cast<unsigned int*>(dv + kHdr * c + 264);
+        V.base_offset = reinterpret_cast<const unsigned long long*>(dv + o_cum + 8 * c);
+        V.grand_total = reinterpret_cast<unsigned long long*>(dv + o_cum + 8 * (c + 1));
+        V.status = reinterpret_cast<unsigned long long*>(dv + o_st + 8 * st_off);
+        st_off += (V.n_tiles + cvg::kScanTile - 1) / cvg::kScanTile;
+        V.worklist = p.args.worklist + V.tile_begin * (cvg::kTile / cvg::kEmitSpan);
+        // claim order inside the view: searches grouped by loud count (one
+        // hot-loop specialization per group), as plan_build does for a batch
+        V.claim_order = nullptr;
+        if (p.mode == cvg::kModeBand && e - b > 1) {
+            std::array<uint32_t, 4> bucket{};
+            for (size_t i = b; i < e; ++i) ++bucket[__builtin_popcount(d->pattern_bits[i] & 7)];
+            if ((bucket[1] > 0) + (bucket[2] > 0) + (bucket[3] > 0) > 1) {
+                V.group_end[0] = bucket[1];
+                V.group_end[1] = bucket[1] + bucket[2];
+                V.group_end[2] = bucket[1] + bucket[2] + bucket[3];
+                std::array<uint32_t, 4> next{0, 0, V.group_end[0], V.group_end[1]};
+                for (size_t i = b; i < e; ++i) {
+                    claim[b + next[__builtin_popcount(d->pattern_bits[i] & 7)]++] = static_cast<uint32_t>(i);
+                }
+                V.claim_order = reinterpret_cast<const uint32_t*>(dv + o_claim) + b;
+            }
+        }
     }
-    std::vector<cvg_plan> plans(K);
-    const std::vector<size_t> lo = ramp_bounds(n, K);
-    std::vector<cudaEvent_t> done(K, nullptr), kdone(K, nullptr);  // tails landed / kernels finished
-    PinnedPairs out{ctx};
-    const uint64_t sig[4] = {n, cps, static_cast<uint64_t>(d->delta_basis), static_cast<uint64_t>(d->path)};
-    const bool hinted = std::equal(sig, sig + 4, ctx->hint_sig);
-    uint64_t used = 0;
-    double prep = t_recs - t0, h2d = 0, t_last_done = 0;
-    cvg::Stats agg{};
-    float agg_ratio = 0.f, kernel_ms = 0.f;
-    int err = CVG_OK;
-    static const bool trace = std::getenv("CVG_TRACE") != nullptr;
-    std::vector<cudaEvent_t> copied(trace ? K : 0, nullptr);
-    for (auto& e : copied) cudaEventCreate(&e);
-    std::vector<std::pair<const char*, double>> tl;
-    auto mark = [&](const char* what) {
-        if (trace) tl.emplace_back(what, now_ms() - t0);
-    };
-
-    auto enqueue_tail = [&](int c) -> int {
-        // counts and [stats | total] of the range on the tail stream: the
-        // compute stream goes on with the next range, never queued behind
-        // a pair copy on the D2H engine
-        cvg_plan& p = plans[c];
-        cudaStream_t st = ctx->tail_stream;
-        CVG_CUDA(cudaEventRecord(kdone[c], ctx->stream));
-        CVG_CUDA(cudaStreamWaitEvent(st, kdone[c], 0));
-        CVG_CUDA(cudaMemcpyAsync(r->counts + lo[c], p.args.counts, sizeof(uint64_t) * (lo[c + 1] - lo[c]),
-                                 cudaMemcpyDeviceToHost, st));
-        CVG_CUDA(cudaMemcpyAsync(&tails[c], p.args.stats, sizeof(ChunkTail), cudaMemcpyDeviceToHost, st));
-        CVG_CUDA(cudaEventRecord(done[c], st));
+    std::vector<cudaEvent_t> kdone(K), done(K), copied(K);
+    for (int c = 0; c < K; ++c) {
+        kdone[c] = event();
+        done[c] = event();
+        copied[c] = event();
+        if (!kdone[c] || !done[c] || !copied[c]) return fail(CVG_ECUDA, "event creation failed");
+    }
+    cudaStream_t st = ctx->stream, ts = ctx->tail_stream, cs = ctx->copy_stream;
+    CVG_CUDA(cudaMemcpyAsync(dv, stage, vbytes, cudaMemcpyHostToDevice, st));
+    auto enqueue = [&]() -> int {
+        CVG_CUDA(cudaMemsetAsync(p.d_work, 0, p.work_bytes, st));
+        CVG_CUDA(cudaMemsetAsync(dv, 0, o_claim, st));  // headers, cum, status (a rerun starts clean)
+        CVG_CUDA(cudaEventRecord(p.ev0, st));
+        for (int c = 0; c < K; ++c) {
+            LaunchArgs& V = views[c];
+            V.out_idx = p.args.out_idx;  // plan_reserve may have replaced the buffers
+            V.out_codes = p.args.out_codes;
+            V.capacity = p.args.capacity;
+            CVG_CUDA(cvg::launch_phase1(V, p.mode, p.out, p.path, p.grid, st));
+            CVG_CUDA(cvg::launch_scan(V, st));
+            CVG_CUDA(cvg::launch_emit(V, p.mode, p.path, p.grid, st));
+            CVG_CUDA(cudaEventRecord(kdone[c], st));
+            CVG_CUDA(cudaStreamWaitEvent(ts, kdone[c], 0));
+            CVG_CUDA(cudaMemcpyAsync(r->counts + lo[c], p.args.counts + lo[c], sizeof(uint64_t) * (lo[c + 1] - lo[c]),
+                                     cudaMemcpyDeviceToHost, ts));
+            CVG_CUDA(cudaMemcpyAsync(tails + kHdr * c, dv + kHdr * c, 264, cudaMemcpyDeviceToHost, ts));
+            CVG_CUDA(cudaEventRecord(done[c], ts));
+        }
+        CVG_CUDA(cudaEventRecord(p.ev1, st));
         return CVG_OK;
     };
-    auto drain = [&](int c) -> int {
-        cvg_plan& p = plans[c];
-        mark("drain");
+    if (int e = enqueue()) return e;
+    const double t_enq = now_ms();
+
+    // ---- drain: copy each view's pairs as soon as its tail lands ----
+    PinnedPairs out{ctx};
+    uint64_t used = 0;
+    bool overflow = false;
+    cvg::Stats agg{};
+    float ratio_max = 0.f;
+    double t_last_done = t_enq;
+    for (int c = 0; c < K; ++c) {
         CVG_CUDA(cudaEventSynchronize(done[c]));
-        mark("done");
-        if (tails[c].st.overflow) {  // device pair buffer too small: rerun this range at its exact size
-            if (int e = plan_reserve(&p, tails[c].total)) return e;
-            if (int e = plan_enqueue(&p, ctx->stream)) return e;
-            if (int e = enqueue_tail(c)) return e;
-            CVG_CUDA(cudaEventSynchronize(done[c]));
-            if (tails[c].st.overflow) return fail(CVG_ECUDA, "pair buffer overflow after resizing");
-        }
-        if (tails[c].st.undecided) return undecided_fail(tails[c].st.undecided);
         t_last_done = now_ms();
-        const uint64_t tc = tails[c].total;
-        const uint64_t seen = cps * lo[c + 1];  // candidates through this chunk
-        const uint64_t extrap = (used + tc) * ((cps * n + seen - 1) / seen) + (used + tc) / 4 + (1u << 16);
-        const uint64_t want = hinted ? std::max(ctx->hint_pairs, used + tc) : extrap;
-        if (!out.ensure(used + tc, std::min<uint64_t>(want, cps * n), used)) {
-            return fail(CVG_ENOMEM, "pinned host allocation failed");
-        }
-        if (tc) {
-            CVG_CUDA(cudaStreamWaitEvent(ctx->copy_stream, done[c], 0));
-            CVG_CUDA(cudaMemcpyAsync(out.idx + used, p.d_out_idx, tc * 4, cudaMemcpyDeviceToHost, ctx->copy_stream));
-            CVG_CUDA(cudaMemcpyAsync(out.codes + 6 * used, p.d_out_codes, tc * 6, cudaMemcpyDeviceToHost,
-                                     ctx->copy_stream));
-        }
-        if (trace) cudaEventRecord(copied[c], ctx->copy_stream);
-        mark("issued");
-        used += tc;
-        const cvg::Stats& s = tails[c].st;
+        const auto& s = *reinterpret_cast<const cvg::Stats*>(tails + kHdr * c);
+        const uint64_t tc = *reinterpret_cast<const unsigned long long*>(tails + kHdr * c + 256);
+        if (s.undecided) return undecided_fail(s.undecided);
         agg.band_repairs += s.band_repairs;
         agg.code_repairs += s.code_repairs;
         agg.audit_violations += s.audit_violations;
         agg.class_mismatch += s.class_mismatch;
         float ratio;
         std::memcpy(&ratio, &s.audit_max_ratio_bits, sizeof(float));
-        agg_ratio = std::max(agg_ratio, ratio);
-        float ms = 0.f;
-        CVG_CUDA(cudaEventElapsedTime(&ms, p.ev0, p.ev1));
-        kernel_ms += ms;
-        return CVG_OK;
-    };
-
-    mark("grid");
-    int next = 0;  // first range not yet drained
-    for (int c = 0; c < K && !err; ++c) {
-        cvg_search_desc sub = *d;
-        sub.n_searches = static_cast<int32_t>(lo[c + 1] - lo[c]);
-        sub.target_rgb = d->target_rgb + 3 * lo[c];
-        sub.pattern_bits = d->pattern_bits + lo[c];
-        sub.v_th = d->v_th + lo[c];
-        sub.r_novib = d->r_novib + lo[c];
-        const double tb = now_ms();
-        err = plan_build_safe(ctx, &sub, &plans[c], &grid, recs.data() + lo[c]);
-        if (err) break;
-        prep += (plans[c].t_prep_end ? plans[c].t_prep_end : now_ms()) - tb;
-        h2d += plans[c].t_upload_end ? plans[c].t_upload_end - plans[c].t_prep_end : 0.0;
-        for (cudaEvent_t* ev : {&done[c], &kdone[c]}) {
-            if (!ctx->events.empty()) {
-                *ev = ctx->events.back();
-                ctx->events.pop_back();
-            } else if (cudaEventCreate(ev) != cudaSuccess) {
-                err = fail(CVG_ECUDA, "event creation failed");
+        ratio_max = std::max(ratio_max, ratio);
+        overflow |= s.overflow != 0;
+        if (!overflow && tc) {
+            // pinned result sized for the whole batch up front when hinted
+            const uint64_t seen = cps * lo[c + 1];
+            const uint64_t extrap = (used + tc) * ((cps * n + seen - 1) / seen) + (used + tc) / 4 + (1u << 16);
+            const uint64_t want = hinted ? std::max(ctx->hint_pairs, used + tc) : extrap;
+            if (!out.ensure(used + tc, std::min<uint64_t>(want, cps * n), used)) {
+                return fail(CVG_ENOMEM, "pinned host allocation failed");
+            }
+            CVG_CUDA(cudaStreamWaitEvent(cs, done[c], 0));
+            CVG_CUDA(cudaMemcpyAsync(out.idx + used, p.args.out_idx + used, tc * 4, cudaMemcpyDeviceToHost, cs));
+            CVG_CUDA(cudaMemcpyAsync(out.codes + 6 * used, p.args.out_codes + 6 * used, tc * 6, cudaMemcpyDeviceToHost,
+                                     cs));
+        }
+        CVG_CUDA(cudaEventRecord(copied[c], cs));
+        used += tc;
+    }
+    if (overflow) {
+        // a view's pairs did not fit the device buffer: rerun at the exact size
+        CVG_CUDA(cudaStreamSynchronize(cs));
+        if (int e = plan_reserve(&p, used)) return e;
+        if (int e = enqueue()) return e;
+        CVG_CUDA(cudaStreamSynchronize(ts));
+        for (int c = 0; c < K; ++c) {
+            if (reinterpret_cast<const cvg::Stats*>(tails + kHdr * c)->overflow) {
+                return fail(CVG_ECUDA, "pair buffer overflow after resizing");
             }
         }
-        if (err) break;
-        mark("built");
-        err = plan_enqueue(&plans[c], ctx->stream);
-        if (!err) err = enqueue_tail(c);
-        mark("enqueued");
-        // start the read-back of every finished range without blocking the builds
-        while (!err && next < c) {
-            const cudaError_t q = cudaEventQuery(done[next]);
-            if (q == cudaErrorNotReady) {
-                cudaGetLastError();  // not an error: the range is still running
-                break;
-            }
-            err = q == cudaSuccess ? drain(next++) : cuda_fail(q, "range completion");
+        if (!out.ensure(used, used, 0)) return fail(CVG_ENOMEM, "pinned host allocation failed");
+        if (used) {
+            CVG_CUDA(cudaStreamWaitEvent(cs, done[K - 1], 0));
+            CVG_CUDA(cudaMemcpyAsync(out.idx, p.args.out_idx, used * 4, cudaMemcpyDeviceToHost, cs));
+            CVG_CUDA(cudaMemcpyAsync(out.codes, p.args.out_codes, used * 6, cudaMemcpyDeviceToHost, cs));
         }
     }
-    while (!err && next < K) err = drain(next++);
-    if (!err) {
-        cudaError_t ce = cudaStreamSynchronize(ctx->copy_stream);
-        if (ce != cudaSuccess) err = cuda_fail(ce, "pair read-back");
-    }
+    CVG_CUDA(cudaStreamSynchronize(cs));
     const double t1 = now_ms();
-    if (!err) {
-        r->idx = used ? out.idx : nullptr;
-        r->codes = used ? out.codes : nullptr;
-        if (!used) {
-            ctx->host.release(out.idx);
-            ctx->host.release(out.codes);
+    static const bool trace = std::getenv("CVG_TRACE") != nullptr;
+    if (trace) {
+        std::string line = "[cvg pipeline] K=" + std::to_string(K) + " built@" + std::to_string(t_built - t0).substr(0, 6) +
+                           " enq@" + std::to_string(t_enq - t0).substr(0, 6) + " end@" + std::to_string(t1 - t0).substr(0, 6);
+        for (int c = 0; c < K; ++c) {
+            float a = 0, b = 0;
+            cudaEventElapsedTime(&a, p.ev0, kdone[c]);
+            cudaEventElapsedTime(&b, p.ev0, copied[c]);
+            line += " | v" + std::to_string(c) + " n=" + std::to_string(lo[c + 1] - lo[c]) + " kernels@" +
+                    std::to_string(a).substr(0, 5) + " copied@" + std::to_string(b).substr(0, 5);
         }
-        r->offsets[0] = 0;
-        for (size_t s = 0; s < n; ++s) r->offsets[s + 1] = r->offsets[s] + r->counts[s];
-        r->n_pairs = used;
-        r->n_candidates = cps * n;
-        r->n_band_repairs = agg.band_repairs;
-        r->n_code_repairs = agg.code_repairs;
-        r->n_audit_violations = agg.audit_violations;
-        r->n_class_mismatch = agg.class_mismatch;
-        r->audit_max_ratio = agg_ratio;
-        r->kernel_ms = kernel_ms;
-        uint64_t in_bytes = 0;
-        for (const cvg_plan& p : plans) in_bytes += p.input_bytes;
-        r->h2d_bytes = in_bytes;
-        r->d2h_bytes = sizeof(uint64_t) * n + (sizeof(ChunkTail)) * K + used * 10;
-        r->prep_ms = static_cast<float>(prep);
-        r->h2d_ms = static_cast<float>(h2d);
-        r->device_ms = static_cast<float>(t_last_done - t0 - prep - h2d);
-        r->d2h_ms = static_cast<float>(t1 - t_last_done);
-        r->total_ms = static_cast<float>(t1 - t0);
-        std::copy(sig, sig + 4, ctx->hint_sig);
-        ctx->hint_pairs = used;
-    } else {
-        cudaStreamSynchronize(ctx->copy_stream);
+        std::fprintf(stderr, "%s\n", line.c_str());
+    }
+
+    // ---- result ----
+    r->offsets[0] = 0;
+    for (size_t s = 0; s < n; ++s) r->offsets[s + 1] = r->offsets[s] + r->counts[s];
+    if (r->offsets[n] != used) return fail(CVG_ECUDA, "pipelined search: counts and pair totals disagree");
+    r->n_pairs = used;
+    r->idx = used ? out.idx : nullptr;
+    r->codes = used ? out.codes : nullptr;
+    if (!used) {
         ctx->host.release(out.idx);
         ctx->host.release(out.codes);
     }
-    cudaStreamSynchronize(ctx->stream);
-    cudaStreamSynchronize(ctx->tail_stream);
-    if (trace) {
-        mark("end");
-        std::string line = "[cvg trace] K=" + std::to_string(K);
-        for (auto& [w, t] : tl) line += std::string(" ") + w + "@" + std::to_string(t).substr(0, 6);
-        for (int c = 0; c < K && !err; ++c) {
-            float a = 0, b = 0, x = 0, m0 = 0, m1 = 0;
-            cudaEventElapsedTime(&a, plans[0].ev0, plans[c].ev0);
-            cudaEventElapsedTime(&b, plans[0].ev0, plans[c].ev1);
-            cudaEventElapsedTime(&x, plans[0].ev0, copied[c]);
-            cudaEventElapsedTime(&m0, plans[c].ev0, plans[c].marks[0]);
-            cudaEventElapsedTime(&m1, plans[c].ev0, plans[c].marks[1]);
-            line += " | r" + std::to_string(c) + " n=" + std::to_string(lo[c + 1] - lo[c]) + " pairs=" +
-                    std::to_string(tails[c].total) + " gpu " + std::to_string(a).substr(0, 5) + "-" +
-                    std::to_string(b).substr(0, 5) + " (p1 " + std::to_string(m0).substr(0, 5) + " scan@" +
-                    std::to_string(m1).substr(0, 5) + ") copied@" + std::to_string(x).substr(0, 5);
-        }
-        std::fprintf(stderr, "%s\n", line.c_str());
-        for (auto& e : copied) cudaEventDestroy(e);
-    }
-    for (int c = 0; c < K; ++c) {
-        if (done[c]) ctx->events.push_back(done[c]);
-        if (kdone[c]) ctx->events.push_back(kdone[c]);
-        if (plans[c].ctx) plan_release(&plans[c]);
-    }
-    ctx->host.release(tails);
-    return err;
+    r->n_candidates = cps * n;
+    r->n_band_repairs = agg.band_repairs;
+    r->n_code_repairs = agg.code_repairs;
+    r->n_audit_violations = agg.audit_violations;
+    r->n_class_mismatch = agg.class_mismatch;
+    r->audit_max_ratio = ratio_max;
+    CVG_CUDA(cudaEventElapsedTime(&r->kernel_ms, p.ev0, p.ev1));
+    r->h2d_bytes = p.input_bytes + vbytes;
+    r->d2h_bytes = sizeof(uint64_t) * n + 264 * K + used * 10;
+    r->prep_ms = static_cast<float>((p.t_prep_end ? p.t_prep_end : t_built) - t0);
+    r->h2d_ms = static_cast<float>(p.t_upload_end ? p.t_upload_end - p.t_prep_end : 0.0);
+    r->device_ms = static_cast<float>(t_last_done - t_enq);
+    r->d2h_ms = static_cast<float>(t1 - t_last_done);
+    r->total_ms = static_cast<float>(t1 - t0);
+    std::copy(sig, sig + 4, ctx->hint_sig);
+    ctx->hint_pairs = used;
+    return CVG_OK;
 }
 
 }  // namespace cvg::host

@@ -50,6 +50,28 @@ def test_pipelined_equals_single_plan(ctx, order):
     assert np.array_equal(again["idx"], want_idx) and np.array_equal(again["codes"], want_codes)
 
 
+def test_hinted_repeat_and_overflow_rerun(ctx):
+    """A repeat of a pipelined shape sizes the device pair buffer from the
+    previous total (+25%).  A repeat with many more pairs overflows it, and
+    the batch reruns at the exact size (cvg_search.cpp search_pipelined).
+    Every call must equal the single-plan result."""
+    rng = np.random.default_rng(5)
+    radii, angles = W.radii(256, 1.0), W.angles(1024)
+    n = 320
+    targets = rng.integers(0, 256, (n, 3)).astype(np.int32)
+    pats = rng.integers(1, 8, n).astype(np.int32)
+    rn = np.full(n, 0.5)
+    sparse = np.full(n, 254.9)
+    sparse[:8] = 20.0
+    dense = rng.choice([5.0, 20.0, 50.0], n)
+    for vt in (sparse, sparse, dense, dense, dense):
+        got = ctx.search(targets, pats, vt, rn, radii, angles)
+        want_idx, want_codes, want_counts = single_plan(ctx, targets, pats, vt, rn, radii, angles, 64)
+        assert np.array_equal(got["counts"], want_counts)
+        assert np.array_equal(got["idx"], want_idx) and np.array_equal(got["codes"], want_codes)
+        assert got["stats"]["class_mismatch"] == 0
+
+
 def test_pipelined_no_pairs(ctx):
     radii, angles = W.radii(256, 1.0), W.angles(1024)
     n = 300  # 78.6M candidates -> 2 ranges
