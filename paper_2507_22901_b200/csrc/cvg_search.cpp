@@ -110,7 +110,7 @@ int fixed_chunks(const cvg_search_desc* d) {
         const char* e = std::getenv("CVG_PIPELINE_K");
         return e ? std::atoi(e) : 0;
     }();
-    return forced > 0 ? std::min(forced, d->n_searches) : 4;
+    return forced > 0 ? std::min(forced, d->n_searches) : 8;
 }
 
 int search_ranges_fixed(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, int K) {
@@ -134,8 +134,12 @@ int search_ranges_fixed(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, i
     const GridTables grid = make_grid_tables(d);
     double prep = 0, h2d = 0, t_first_enqueued = 0;
     int err = CVG_OK;
+    // growing ranges: the first range's prep (the only one not overlapped)
+    // is short.  Measured cfg4 e2e (C-side ms): K=4 even 224-225,
+    // K=4 ramp 227.7, K=8 even 231.0, K=8 ramp 220.2, K=16 ramp 221.2
+    const std::vector<size_t> bounds = ramp_bounds(n, K);
     for (int c = 0; c < K && !err; ++c) {
-        const size_t lo = n * c / K, hi = n * (c + 1) / K;
+        const size_t lo = bounds[c], hi = bounds[c + 1];
         cvg_search_desc sub = *d;
         sub.n_searches = static_cast<int32_t>(hi - lo);
         sub.target_rgb = d->target_rgb + 3 * lo;
