@@ -184,6 +184,11 @@ CVG_API void cvg_d65_white(double out[3]);
 CVG_API int cvg_pair_signal(const double lab[3], double radius, double angle, const double* white_point,
                             double sp[3], double sm[3]);
 CVG_API void cvg_quant_thresholds(double out[256]);
+/* The kernels' FP32 code table: 4097 buckets of linear [0, 1] x {threshold t,
+ * code below (int32 bits)}; 8194 floats.  Exposed so tests can check it on
+ * the host. */
+CVG_API void cvg_code_table(float out[8194]);
+CVG_API float cvg_code_slack(void);
 
 /* FP32 FFMA issue-rate microbenchmark (roofline denominator); returns
  * lane-FFMA per second measured on `device`, 0 on failure. */

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <array>
+#include <bit>
 #include <atomic>
 #include <condition_variable>
 #include <functional>
@@ -115,8 +116,13 @@ void to_linear(const double lab[3], const double* wp, double lin[3]);
 // found by bisection over the glibc-pow quantizer (convert_kernel.hpp:127-141).
 struct Tables {
     double thr[256];
-    float thr3[256][4];  // {tf[g], tf[g+1], tf[g+2], 0}: tf[0] = -inf, tf[c] = float(thr[c]), tf[256..] = +inf
-    uint8_t guess[cvg::kGuessBuckets + 1];
+    // Code table over kGuessBuckets + 1 round-to-nearest buckets of linear
+    // [0, 1] (bucket i: x * 4096 in [i - 1/2, i + 1/2]), each widened by
+    // cvg::kCodeSlack on both sides.  Entry {t, c}: c = number of float
+    // thresholds tf = float(thr[1..255]) below the widened bucket, t = the one
+    // tf inside it (+inf if none, NaN if two or more).  For x in the bucket and
+    // E = eps_code <= kCodeSlack, |x - t| > E proves code(x64) = c + (x >= t).
+    float ctab[cvg::kGuessBuckets + 1][2];
     Tables() {
         thr[0] = 0.0;
         for (int code = 1; code <= 255; ++code) {
@@ -127,19 +133,23 @@ struct Tables {
             }
             thr[code] = hi;
         }
-        float tf[258];
-        tf[0] = -INFINITY;
-        for (int c = 1; c < 256; ++c) tf[c] = static_cast<float>(thr[c]);
-        tf[256] = tf[257] = INFINITY;
-        for (int g = 0; g < 256; ++g) {
-            thr3[g][0] = tf[g];
-            thr3[g][1] = tf[g + 1];
-            thr3[g][2] = tf[g + 2];
-            thr3[g][3] = 0.0f;
+        for (int i = 0; i <= cvg::kGuessBuckets; ++i) {
+            const double lo = (i - 0.5) / cvg::kGuessBuckets - cvg::kCodeSlack;
+            const double hi = (i + 0.5) / cvg::kGuessBuckets + cvg::kCodeSlack;
+            int below = 0, inside = 0;
+            float t = INFINITY;
+            for (int c = 1; c < 256; ++c) {
+                const double tf = static_cast<float>(thr[c]);
+                if (tf < lo) {
+                    ++below;
+                } else if (tf <= hi) {
+                    ++inside;
+                    t = static_cast<float>(tf);
+                }
+            }
+            ctab[i][0] = inside > 1 ? NAN : t;
+            ctab[i][1] = std::bit_cast<float>(below);
         }
-        // Round-to-nearest buckets: bucket i holds x * 4096 in [i - 1/2, i + 1/2);
-        // guess = code at the bucket's lower edge (<= 1 threshold per bucket).
-        for (int i = 0; i <= cvg::kGuessBuckets; ++i) guess[i] = static_cast<uint8_t>(code((i - 0.5) / 4096.0));
     }
     int code(double x) const {
         if (x <= 0.0) return 0;

@@ -27,6 +27,7 @@
 // Result: per-search counts and pair lists bit-identical to the reference.
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 
 
@@ -108,9 +109,11 @@ __device__ __forceinline__ void load_consts(const SearchConst* S, Consts& c) {
 struct CodeConsts {
     float fx0, fz0, rcube;
     float mx[3], mz[3], cy[3], ec[3];
+    uint32_t tab;  // code_fast's table address (ctab_addr), computed once per kernel
 };
 
-__device__ __forceinline__ void load_code_consts(const SearchConst* S, CodeConsts& c) {
+__device__ __forceinline__ void load_code_consts(const SearchConst* S, CodeConsts& c, uint32_t tab) {
+    c.tab = tab;
     c.fx0 = __ldg(&S->fx0);
     c.fz0 = __ldg(&S->fz0);
     c.rcube = __ldg(&S->rcube);
@@ -119,7 +122,8 @@ __device__ __forceinline__ void load_code_consts(const SearchConst* S, CodeConst
         c.mx[q] = __ldg(&S->mx[q]);
         c.mz[q] = __ldg(&S->mz[q]);
         c.cy[q] = __ldg(&S->cy[q]);
-        c.ec[q] = __ldg(&S->eps_code[q]);
+        const float e = __ldg(&S->eps_code[q]);
+        c.ec[q] = e <= kCodeSlack ? e : INFINITY;  // beyond the table's slack: every code goes to FP64
     }
 }
 
@@ -273,7 +277,14 @@ __device__ __forceinline__ float finv_fast(float f) {
 // The six linear endpoint values (plus: vp, minus: vm) minus an additive
 // offset folded into `add` (cy for the values themselves, cy - centre for the
 // band statistic).  f = f0 +- r*s' is one FFMA; f^-1 two FMULs (+ select).
-template <bool kCubeOnly>
+__device__ __forceinline__ float fma_sat(float a, float b, float c) {
+    float d;
+    asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+    return d;
+}
+
+// kSat: the values saturated to [0, 1] in the last FFMA (code_fast input).
+template <bool kCubeOnly, bool kSat = false>
 __device__ __forceinline__ void fast_linear(float fx0, float fz0, const float* mx, const float* mz, const float* add,
                                             float r, float2 sc, float* vp, float* vm) {
     const float fxp = fmaf(r, sc.x, fx0);
@@ -286,8 +297,13 @@ __device__ __forceinline__ void fast_linear(float fx0, float fz0, const float* m
     const float gzm = finv_fast<kCubeOnly>(fzm);
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
-        vp[q] = fmaf(mx[q], gxp, fmaf(mz[q], gzp, add[q]));
-        vm[q] = fmaf(mx[q], gxm, fmaf(mz[q], gzm, add[q]));
+        if (kSat) {
+            vp[q] = fma_sat(mx[q], gxp, fmaf(mz[q], gzp, add[q]));
+            vm[q] = fma_sat(mx[q], gxm, fmaf(mz[q], gzm, add[q]));
+        } else {
+            vp[q] = fmaf(mx[q], gxp, fmaf(mz[q], gzp, add[q]));
+            vm[q] = fmaf(mx[q], gxm, fmaf(mz[q], gzm, add[q]));
+        }
     }
 }
 
@@ -367,19 +383,31 @@ __device__ __forceinline__ bool band_certain(const Consts& C, float minl, float 
     return (minl > C.lp) & (maxq < C.qp);
 }
 
-// Linear value -> code through the float tables, verified against the bound:
-// the bucket of x (round-to-nearest, x saturated to [0, 1]) gives g; one
-// 16-byte load gives thr[g..g+2]; c = g + (x >= thr[g+1]); ok iff
-// thr[c] + E < x < thr[c+1] - E, which proves code(x64) == c.
-__device__ __forceinline__ int code_fast(float x, float E, const float4* t3, const uint8_t* guess, bool& ok) {
-    const float b = fmaf(__saturatef(x), static_cast<float>(kGuessBuckets), 8388608.0f);  // 2^23 + round(x * 4096)
-    const int g = guess[__float_as_int(b) - 0x4B000000];
-    const float4 T = t3[g];
-    const bool up = x >= T.y;
-    const float lo = up ? T.y : T.x;
-    const float hi = up ? T.z : T.y;
-    ok = (__fsub_rn(x, lo) > E) & (__fsub_rn(hi, x) > E);
-    return g + up;
+// Linear value -> code through the code table, verified against the bound:
+// the bucket of xs (round-to-nearest) gives {t, c}, the only float threshold
+// within kCodeSlack of the bucket and the count below it; c + (xs >= t) is
+// the code, and ok iff |xs - t| > E, which proves code(x64) == it (E =
+// eps_code <= kCodeSlack; NaN t: never ok).  xs is the FP32 value saturated
+// to [0, 1]: the table has no threshold within kCodeSlack of 0 or 1, so a
+// value below 0 (above 1) gets code 0 (255) exactly as its FP64 twin does.
+// `tab` = shared address of the table minus 8 * bits(2^23).
+__device__ __forceinline__ int code_fast(float xs, float E, uint32_t tab, bool& ok) {
+    const float b = fmaf(xs, static_cast<float>(kGuessBuckets), 8388608.0f);  // bits: 0x4B000000 + round(xs * 4096)
+    float t;
+    int c;
+    asm("ld.shared.v2.b32 {%0, %1}, [%2];" : "=f"(t), "=r"(c) : "r"(tab + (__float_as_uint(b) << 3)));
+    ok = fabsf(__fsub_rn(xs, t)) > E;
+    int up;
+    asm("set.ge.s32.f32 %0, %1, %2;" : "=r"(up) : "f"(xs), "f"(t));  // -1 or 0
+    return c - up;
+}
+
+// Passed through a shuffle, so that it is opaque to ptxas and each lookup is
+// one LEA off this register (else ptxas re-derives the shared base and the
+// constant inside the loop, two more instructions per lookup).
+__device__ __forceinline__ uint32_t ctab_addr(const float2* ctab) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(ctab)) - (0x4B000000u << 3);
+    return __shfl_sync(0xffffffffu, a, 0);
 }
 
 // Exact code from a nearby guess (the FP32 code is off by at most one).
@@ -391,20 +419,24 @@ __device__ __forceinline__ int code_exact_from(double x, int c, const double* th
     return c;
 }
 
-// Shared tables: exact and float quantization thresholds + code guesses.
+// Shared tables: exact quantization thresholds + the FP32 code table.
 struct Smem {
-    float4 t3[256];     // {tf[g], tf[g+1], tf[g+2], 0}
     double thr_d[256];
     uint32_t first[kWarpsPerBlock];  // FIRST mode: tile offset of the warp's first passing candidate
-    uint8_t guess[kGuessBuckets + 16];
+    float2 ctab[kGuessBuckets + 2];  // code table (cvg_host.h Tables::ctab); last: kernels without codes omit it
 };
 
+// Dynamic shared memory of phase 1: the code table only where it quantizes.
+template <int kMode>
+constexpr size_t phase1_smem() { return kMode == kModeCodes ? sizeof(Smem) : offsetof(Smem, ctab); }
+
+template <bool kCodes>
 __device__ __forceinline__ void load_tables(Smem& sm, const LaunchArgs& A) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         sm.thr_d[i] = A.thr_d[i];
-        sm.t3[i] = reinterpret_cast<const float4*>(A.thr3)[i];
     }
-    for (int i = threadIdx.x; i <= kGuessBuckets; i += blockDim.x) sm.guess[i] = A.guess[i];
+    if (kCodes)
+        for (int i = threadIdx.x; i <= kGuessBuckets; i += blockDim.x) sm.ctab[i] = reinterpret_cast<const float2*>(A.ctab)[i];
     __syncthreads();
 }
 
@@ -454,16 +486,16 @@ __device__ __forceinline__ void codes_fast(const Smem& sm, const SearchConst* S,
                                            bool active, int* cp, int* cm, unsigned long long& repairs) {
     float vp[3], vm[3];
     if (__all_sync(kFull, r < C.rcube)) {  // every lane's row stays on the cube branch
-        fast_linear<true>(C.fx0, C.fz0, C.mx, C.mz, C.cy, r, sc, vp, vm);
+        fast_linear<true, true>(C.fx0, C.fz0, C.mx, C.mz, C.cy, r, sc, vp, vm);
     } else {
-        fast_linear<false>(C.fx0, C.fz0, C.mx, C.mz, C.cy, r, sc, vp, vm);
+        fast_linear<false, true>(C.fx0, C.fz0, C.mx, C.mz, C.cy, r, sc, vp, vm);
     }
     bool all_ok = true;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         bool ok1, ok2;
-        cp[q] = code_fast(vp[q], C.ec[q], sm.t3, sm.guess, ok1);
-        cm[q] = code_fast(vm[q], C.ec[q], sm.t3, sm.guess, ok2);
+        cp[q] = code_fast(vp[q], C.ec[q], C.tab, ok1);
+        cm[q] = code_fast(vm[q], C.ec[q], C.tab, ok2);
         all_ok &= ok1 & ok2;
     }
     if (__any_sync(kFull, !all_ok) && !all_ok) {
@@ -506,8 +538,8 @@ __device__ __forceinline__ void candidate_codes(const Smem& sm, const SearchCons
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         bool ok1, ok2;
-        const int fp = code_fast(vp[q], C.ec[q], sm.t3, sm.guess, ok1);
-        const int fm = code_fast(vm[q], C.ec[q], sm.t3, sm.guess, ok2);
+        const int fp = code_fast(__saturatef(vp[q]), C.ec[q], C.tab, ok1);
+        const int fm = code_fast(__saturatef(vm[q]), C.ec[q], C.tab, ok2);
         all_ok &= ok1 & ok2;
         cp[q] = code_exact(lp[q], sm.thr_d);
         cm[q] = code_exact(lm[q], sm.thr_d);
@@ -708,7 +740,8 @@ template <int kMode, int kOut, int kPath>
 __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    load_tables(sm, A);
+    load_tables<kMode == kModeCodes>(sm, A);  // phase 1 needs codes only in FrameDiff x Quantized
+    const uint32_t tab = ctab_addr(sm.ctab);
     const unsigned lane = threadIdx.x & 31;
     const unsigned lane_lt = (1u << lane) - 1u;
     Counters ct;
@@ -780,7 +813,7 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
             }
         } else {
             CodeConsts CC;
-            load_code_consts(S, CC);
+            load_code_consts(S, CC, tab);
             for (uint32_t base = i0; base < i1; base += 32) {
                 const bool active = base + lane < i1;
                 const uint32_t i = active ? base + lane : i1 - 1;
@@ -901,7 +934,8 @@ template <int kMode, int kPath>
 __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    load_tables(sm, A);
+    load_tables<true>(sm, A);
+    const uint32_t tab = ctab_addr(sm.ctab);
     const unsigned lane = threadIdx.x & 31;
     const uint32_t n_work = *reinterpret_cast<volatile unsigned int*>(&A.ticket[3]);
     const unsigned long long base0 = A.base_offset ? *A.base_offset : 0ull;
@@ -925,7 +959,7 @@ __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
             const uint32_t i0 = (t - s * A.tiles_per_search) * static_cast<uint32_t>(kTile);
             const SearchConst* S = search_const(A, s);
             CodeConsts CC;
-            load_code_consts(S, CC);
+            load_code_consts(S, CC, tab);
             if (kPath == kPathFast) {
                 // Software pipeline: list entries two iterations ahead, the
                 // candidate's radius/trig loads one iteration ahead.
@@ -1026,7 +1060,7 @@ __global__ void ffma_peak_kernel(float* out, int iters, float a, float b) {
 template <int kMode, int kOut, int kPath>
 cudaError_t phase1_t(const LaunchArgs& a, int grid, cudaStream_t st) {
     // The dynamic shared-memory sizes are opted into by occupancy_t (plan creation).
-    phase1_kernel<kMode, kOut, kPath><<<grid, kBlock, sizeof(Smem), st>>>(a);
+    phase1_kernel<kMode, kOut, kPath><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);
     return cudaGetLastError();
 }
 
@@ -1062,10 +1096,11 @@ template <int kMode, int kOut, int kPath>
 int occupancy_t() {
     auto f1 = phase1_kernel<kMode, kOut, kPath>;
     auto f3 = emit_kernel<kMode, emit_path(kMode, kPath)>;
-    cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Smem)));
+    cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(phase1_smem<kMode>()));
     cudaFuncSetAttribute(f3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Smem)));
     int blocks = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f1, kBlock, sizeof(Smem)) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f1, kBlock, phase1_smem<kMode>()) != cudaSuccess)
+        return 0;
     return blocks;
 }
 

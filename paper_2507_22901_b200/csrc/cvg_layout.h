@@ -12,7 +12,8 @@ namespace cvg {
 constexpr int kTile = 4096;
 constexpr int kWarpsPerBlock = 8;
 constexpr int kBlock = 32 * kWarpsPerBlock;
-constexpr int kGuessBuckets = 4096;  // code-guess buckets over linear [0, 1]
+constexpr int kGuessBuckets = 4096;  // code-table buckets over linear [0, 1]
+constexpr float kCodeSlack = 1.0f / 65536;  // code-table bucket widening (>= every usable eps_code)
 constexpr int kEmitSpan = 256;      // pairs per emit work item (tile sub-range)
 constexpr int kScanItems = 8;        // tile counts per thread in the offset scan
 constexpr int kScanTile = kBlock * kScanItems;
@@ -83,8 +84,7 @@ struct LaunchArgs {
     const float* trig_f;       // [na][2] = (sin/500, cos/200) as float
     const double* trig_d;      // [na][2] = (sin, cos), glibc doubles (search.cpp:414-419)
     const double* thr_d;       // [256] QuantTable thresholds (convert_kernel.hpp:123-141)
-    const float* thr3;         // [256][4] {tf[g], tf[g+1], tf[g+2], 0}, tf = thresholds as float, tf[0] = -inf
-    const uint8_t* guess;      // [kGuessBuckets + 1] code((i - 1/2) / 4096): round-to-nearest buckets
+    const float* ctab;         // [kGuessBuckets + 1][2] code table {t, bits(c)} (cvg_host.h Tables)
     double minv[9];            // kXyzToRgb (convert_kernel.hpp:47), row-major
     int32_t n_searches;
     int32_t nr;

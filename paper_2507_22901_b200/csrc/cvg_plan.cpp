@@ -279,7 +279,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         }
     }
 
-    // ---- one constant blob: [sc | sc_index | claim | radii | trig | thresholds | guess] ----
+    // ---- one constant blob: [sc | sc_index | claim | radii | trig | thresholds | code table] ----
     Layout L;
     const size_t o_sc = L.take(sizeof(SearchConst) * n_sc);
     const size_t o_si = L.take(sizeof(uint32_t) * sc_index.size());
@@ -289,8 +289,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     const size_t o_td = L.take(sizeof(double) * trig_d.size());
     const size_t o_tf = L.take(sizeof(float) * trig_f.size());
     const size_t o_thd = L.take(sizeof(double) * 256);
-    const size_t o_thf = L.take(sizeof(float) * 256 * 4);
-    const size_t o_gs = L.take(cvg::kGuessBuckets + 1);
+    const size_t o_ctab = L.take(sizeof(T.ctab));
     const size_t bytes = L.off;
     p->input_bytes = bytes;
     p->t_prep_end = now_ms();
@@ -326,8 +325,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     std::memcpy(stage + o_td, trig_d.data(), sizeof(double) * trig_d.size());
     std::memcpy(stage + o_tf, trig_f.data(), sizeof(float) * trig_f.size());
     std::memcpy(stage + o_thd, T.thr, sizeof(double) * 256);
-    std::memcpy(stage + o_thf, T.thr3, sizeof(float) * 256 * 4);
-    std::memcpy(stage + o_gs, T.guess, cvg::kGuessBuckets + 1);
+    std::memcpy(stage + o_ctab, T.ctab, sizeof(T.ctab));
     LaunchArgs& A = p->args;
     std::memset(&A, 0, sizeof(A));
     A.sc = at<const SearchConst>(p->d_const, o_sc);
@@ -339,8 +337,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.trig_d = at<const double>(p->d_const, o_td);
     A.trig_f = at<const float>(p->d_const, o_tf);
     A.thr_d = at<const double>(p->d_const, o_thd);
-    A.thr3 = at<const float>(p->d_const, o_thf);
-    A.guess = at<const uint8_t>(p->d_const, o_gs);
+    A.ctab = at<const float>(p->d_const, o_ctab);
     // No sync: the staging block stays with the plan until it is released,
     // which happens after the stream has passed this copy.
     cudaError_t e = cudaMemcpyAsync(p->d_const, stage, bytes, cudaMemcpyHostToDevice, ctx->stream);
@@ -876,6 +873,8 @@ void cvg_d65_white(double out[3]) {
 }
 
 void cvg_quant_thresholds(double out[256]) { std::memcpy(out, tables().thr, sizeof(double) * 256); }
+void cvg_code_table(float out[8194]) { std::memcpy(out, tables().ctab, sizeof(tables().ctab)); }
+float cvg_code_slack(void) { return cvg::kCodeSlack; }
 
 double cvg_measure_ffma_peak(int device, float* ms_out) { return cvg::measure_ffma_peak(device, ms_out); }
 

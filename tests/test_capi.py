@@ -263,3 +263,44 @@ def test_select_best_margin_and_ties():
     assert cv.select_best([a, b, c, d], th).angle == 0.05
     with pytest.raises(ValueError):
         cv.select_best([], th)
+
+
+def _code64(x, thr):
+    """QuantTable::code (convert_kernel.hpp:143-154) as 'thresholds at or below x'."""
+    c = np.searchsorted(thr[1:], x, side="right")
+    return np.where(x <= 0.0, 0, np.where(x >= 1.0, 255, c))
+
+
+@pytest.mark.parametrize("E", [2.0 ** -22, 1e-6, 2.0 ** -16])
+def test_code_table_proof(lib, E):
+    """The kernels' FP32 code lookup (cvg_kernels.cu code_fast) restated in
+    numpy over the exported table: wherever it claims a verified code
+    (|xs - t| > E), every FP64 value within eps = E - 2^-23 of the FP32 value
+    has that code (QuantTable::code, convert_kernel.hpp:143-154).  Probes: every
+    float threshold +- 64 ulps and 2M uniform values in [-0.1, 1.1]."""
+    tab = np.zeros(8194, np.float32)
+    lib.cvg_code_table(tab.ctypes.data_as(C.POINTER(C.c_float)))
+    lib.cvg_code_slack.restype = C.c_float
+    assert E <= lib.cvg_code_slack() + 1e-12
+    thr = np.zeros(256, np.float64)
+    lib.cvg_quant_thresholds(thr.ctypes.data_as(C.POINTER(C.c_double)))
+    t_tab = tab[0::2]
+    c_tab = tab[1::2].view(np.int32)
+    assert np.all(np.diff(c_tab) >= 0) and c_tab[0] == 0 and c_tab[-1] == 255
+    tf = thr[1:].astype(np.float32)
+    near = (tf[:, None].view(np.int32) + np.arange(-64, 65, dtype=np.int32)[None, :]).view(np.float32).ravel()
+    rng = np.random.default_rng(5)
+    x = np.concatenate([near, rng.uniform(-0.1, 1.1, 2_000_000).astype(np.float32),
+                        np.float32([0.0, 1.0, -1e-9, 1.0 + 1e-7])])
+    xs = np.clip(x, np.float32(0), np.float32(1))
+    b = np.rint(xs.astype(np.float64) * 4096).astype(np.int64)  # fmaf(xs, 4096, 2^23): round half even
+    t = t_tab[b]
+    with np.errstate(invalid="ignore"):
+        ok = np.abs(xs - t) > np.float32(E)
+        code = c_tab[b] + (xs >= t)
+    eps = E - 2.0 ** -23
+    x64 = x.astype(np.float64)
+    lo, hi = _code64(x64 - eps, thr), _code64(x64 + eps, thr)
+    assert np.array_equal(code[ok], lo[ok]) and np.array_equal(code[ok], hi[ok])
+    # the unverified share is the +-E windows around the 255 thresholds
+    assert ok[len(near):].mean() > 1.0 - 600 * E
