@@ -188,6 +188,9 @@ CVG_API void cvg_quant_thresholds(double out[256]);
  * code below (int32 bits)}; 8194 floats.  Exposed so tests can check it on
  * the host. */
 CVG_API void cvg_code_table(float out[8194]);
+/* The Continuous x FrameDiff prefilter's signal bounds: 4097 buckets x
+ * {L, U}, L <= signal_value(x) <= U over bucket i = [(i - 1/2), (i + 1/2)] / 4096. */
+CVG_API void cvg_signal_table(float out[8194]);
 CVG_API float cvg_code_slack(void);
 
 /* FP32 FFMA issue-rate microbenchmark (roofline denominator); returns

@@ -108,6 +108,7 @@ double f_lab_inv(double u);
 double eotf(double u);
 double oetf(double x);
 int quantize(double linear);
+double signal_value(double linear);  // 255 * oetf(clamp(x, 0, 1)) (convert_kernel.hpp:109-112)
 const double* white_or_d65(const double* wp);
 void to_lab(const int32_t c[3], const double* wp, double lab[3]);
 void to_linear(const double lab[3], const double* wp, double lin[3]);
@@ -123,6 +124,11 @@ struct Tables {
     // tf inside it (+inf if none, NaN if two or more).  For x in the bucket and
     // E = eps_code <= kCodeSlack, |x - t| > E proves code(x64) = c + (x >= t).
     float ctab[cvg::kGuessBuckets + 1][2];
+    // Signal table (Continuous x FrameDiff prefilter) over the same buckets:
+    // {L, U} with L <= signal_value(x) <= U for every double x in
+    // [(i - 1/2) / 4096, (i + 1/2) / 4096] (signal_value is monotone; the
+    // bounds are rounded outward to float with a 1e-9 allowance for glibc pow).
+    float stab[cvg::kGuessBuckets + 1][2];
     Tables() {
         thr[0] = 0.0;
         for (int code = 1; code <= 255; ++code) {
@@ -149,6 +155,13 @@ struct Tables {
             }
             ctab[i][0] = inside > 1 ? NAN : t;
             ctab[i][1] = std::bit_cast<float>(below);
+            const double sl = signal_value((i - 0.5) / cvg::kGuessBuckets) - 1e-9;
+            const double su = signal_value((i + 0.5) / cvg::kGuessBuckets) + 1e-9;
+            float fl = static_cast<float>(sl), fu = static_cast<float>(su);
+            if (fl > sl) fl = std::nextafter(fl, -INFINITY);
+            if (fu < su) fu = std::nextafter(fu, INFINITY);
+            stab[i][0] = fl;
+            stab[i][1] = fu;
         }
     }
     int code(double x) const {

@@ -241,6 +241,69 @@ __device__ __forceinline__ bool signal_pass(const SearchConst* S, const double* 
     return ok;
 }
 
+// ---- Continuous x FrameDiff FP32 prefilter ------------------------------
+__device__ __forceinline__ float add_rm_sat(float a, float b) {
+    float d;
+    asm("add.rm.sat.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ float add_rp_sat(float a, float b) {
+    float d;
+    asm("add.rp.sat.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+
+// Per-search constants of the prefilter: the bound on |v32 - v64| and each
+// channel's threshold widened to [tl, th] (margin 2^-12 covers the float
+// rounding of the threshold and the difference's double rounding).
+struct SigConsts {
+    float e[3], th[3], tl[3];
+};
+
+__device__ __forceinline__ void load_sig_consts(const SearchConst* S, SigConsts& g) {
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const double T = __ldg(&S->lo[q]);
+        g.e[q] = __ldg(&S->eps[q]);
+        g.th[q] = __double2float_ru(T + 0x1p-12);
+        g.tl[q] = __double2float_rd(T - 0x1p-12);
+    }
+}
+
+// Bounds [lo, hi] on signal_value(v64) for |v - v64| <= e: the buckets of
+// sat(v - e) (rounded down) and sat(v + e) (rounded up) in the signal table
+// (Tables::stab, signal_value monotone).  `tab` as in code_fast.
+__device__ __forceinline__ void signal_bounds(float v, float e, uint32_t tab, float& lo, float& hi) {
+    const float bl = fmaf(add_rm_sat(v, -e), static_cast<float>(kGuessBuckets), 8388608.0f);
+    const float bh = fmaf(add_rp_sat(v, e), static_cast<float>(kGuessBuckets), 8388608.0f);
+    asm("ld.shared.f32 %0, [%1];" : "=f"(lo) : "r"(tab + (__float_as_uint(bl) << 3)));
+    asm("ld.shared.f32 %0, [%1];" : "=f"(hi) : "r"(tab + (__float_as_uint(bh) << 3) + 4u));
+}
+
+// classify_pair on continuous FrameDiff deltas (search.cpp:146-173) from the
+// bounds: with d in [dmin, dmax], a channel is surely above its threshold if
+// dmin > th and surely at or below it if dmax <= tl.  The candidate surely
+// fails if any channel surely fails, surely passes if every channel surely
+// passes; otherwise `unsure` (the FP64 path decides).
+__device__ __forceinline__ bool signal_prefilter(const SigConsts& G, const float* vp, const float* vm, uint32_t tab,
+                                                 uint32_t flags, bool& unsure) {
+    bool fail = false, all = true;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        float pl, ph, ml, mh;
+        signal_bounds(vp[q], G.e[q], tab, pl, ph);
+        signal_bounds(vm[q], G.e[q], tab, ml, mh);
+        const float dlo = __fsub_rd(pl, mh), dhi = __fsub_ru(ph, ml);
+        const float dmin = fmaxf(fmaxf(dlo, -dhi), 0.0f), dmax = fmaxf(-dlo, dhi);
+        const bool above = dmin > G.th[q], below = dmax <= G.tl[q];
+        const bool loud = (flags >> q) & 1;
+        fail |= loud ? below : above;
+        all &= loud ? above : below;
+    }
+    unsure = !fail & !all;
+    return all;
+}
+
 // classify_pair (search.cpp:146-157) on integer codes, with the integer form
 // of the thresholds (d > v_th <=> d >= k1, d <= low <=> d <= q0).
 __device__ __forceinline__ bool classify_codes(const SearchConst* S, const int* cp, const int* cm,
@@ -423,20 +486,27 @@ __device__ __forceinline__ int code_exact_from(double x, int c, const double* th
 struct Smem {
     double thr_d[256];
     uint32_t first[kWarpsPerBlock];  // FIRST mode: tile offset of the warp's first passing candidate
-    float2 ctab[kGuessBuckets + 2];  // code table (cvg_host.h Tables::ctab); last: kernels without codes omit it
+    // code table (cvg_host.h Tables::ctab); phase 1 of kModeSignal holds the
+    // signal table (Tables::stab) here instead.  Last: kernels without a
+    // table omit it.
+    float2 ctab[kGuessBuckets + 2];
 };
 
 // Dynamic shared memory of phase 1: the code table only where it quantizes.
 template <int kMode>
-constexpr size_t phase1_smem() { return kMode == kModeCodes ? sizeof(Smem) : offsetof(Smem, ctab); }
+constexpr size_t phase1_smem() { return kMode == kModeBand ? offsetof(Smem, ctab) : sizeof(Smem); }
 
-template <bool kCodes>
+enum Table : int { kTabNone = 0, kTabCode = 1, kTabSignal = 2 };
+
+template <int kTab>
 __device__ __forceinline__ void load_tables(Smem& sm, const LaunchArgs& A) {
     for (int i = threadIdx.x; i < 256; i += blockDim.x) {
         sm.thr_d[i] = A.thr_d[i];
     }
-    if (kCodes)
-        for (int i = threadIdx.x; i <= kGuessBuckets; i += blockDim.x) sm.ctab[i] = reinterpret_cast<const float2*>(A.ctab)[i];
+    if (kTab != kTabNone) {
+        const float2* src = reinterpret_cast<const float2*>(kTab == kTabCode ? A.ctab : A.stab);
+        for (int i = threadIdx.x; i <= kGuessBuckets; i += blockDim.x) sm.ctab[i] = src[i];
+    }
     __syncthreads();
 }
 
@@ -557,14 +627,32 @@ __device__ __forceinline__ void candidate_codes(const Smem& sm, const SearchCons
 // Phase-1 decision of one candidate, any mode/path (the generic loop).
 template <int kMode, int kPath>
 __device__ __forceinline__ bool candidate_pass(const Smem& sm, const SearchConst* S, const Consts& C,
-                                               const CodeConsts& CC, const LaunchArgs& A, uint32_t k, uint32_t m,
-                                               bool active, Counters& ct) {
-    if (kMode == kModeSignal) {  // every path: FP64 linear values + device pow with its margin
-        double lp[3], lm[3];
-        exact_linear(S, A, k, m, lp, lm);
-        bool undecided;
-        const bool pass = signal_pass(S, lp, lm, C.flags, undecided);
-        if (active) ct.undecided += undecided;
+                                               const CodeConsts& CC, const SigConsts& SG, const LaunchArgs& A,
+                                               uint32_t k, uint32_t m, bool active, Counters& ct) {
+    if (kMode == kModeSignal) {
+        // FP32 prefilter on signal bounds; unsure lanes (and every lane of
+        // the EXACT / AUDIT paths) decide on FP64 linear values + device pow
+        // with its margin.
+        bool pass = false, unsure = true;
+        if (kPath != kPathExact) {
+            const float r = __ldg(&A.radii_f[k]);
+            const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + m);
+            float vp[3], vm[3];
+            fast_linear<false>(CC.fx0, CC.fz0, CC.mx, CC.mz, CC.cy, r, sc, vp, vm);
+            pass = signal_prefilter(SG, vp, vm, CC.tab, C.flags, unsure);
+        }
+        if (kPath != kPathFast || (__any_sync(kFull, unsure) && unsure)) {
+            double lp[3], lm[3];
+            exact_linear(S, A, k, m, lp, lm);
+            bool undecided;
+            const bool ex = signal_pass(S, lp, lm, C.flags, undecided);
+            if (active) {
+                ct.undecided += undecided;
+                if (kPath != kPathExact) ct.repairs += unsure;
+                if (kPath == kPathAudit) ct.violations += !unsure && ex != pass;
+            }
+            pass = ex;
+        }
         return active && pass;
     }
     if (kMode == kModeCodes) {
@@ -711,6 +799,125 @@ __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, 
     }
 }
 
+// ---- Quantized x FrameDiff hot loop ---------------------------------------
+// Code bounds instead of exact codes: a code whose FP32 value lies within E
+// of its bucket's threshold is c or c + 1 (code_fast), so its computed value
+// is off by at most one; with widths w, d = |cp - cm| lies in [d - w, d + w].
+// A channel surely passes or fails unless its threshold falls inside that
+// range (classify_pair, search.cpp:146-157, frame_deltas :138-144); only
+// candidates that are neither sure pass nor sure fail take FP64 codes.
+// E beyond kCodeSlack (ec = inf): width 256, every channel unsure.
+struct FrameConsts {
+    int k1, q0;
+    int wc[3];
+};
+
+__device__ __forceinline__ void frame_chunk(const CodeConsts& CC, const FrameConsts& F, uint32_t flags, float r,
+                                            float2 sc, bool& att, bool& sure) {
+    float vp[3], vm[3];
+    fast_linear<false, true>(CC.fx0, CC.fz0, CC.mx, CC.mz, CC.cy, r, sc, vp, vm);
+    bool fail = false, all = true;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        bool okp, okm;
+        const int cp = code_fast(vp[q], CC.ec[q], CC.tab, okp);
+        const int cm = code_fast(vm[q], CC.ec[q], CC.tab, okm);
+        const int w = (okp ? 0 : F.wc[q]) + (okm ? 0 : F.wc[q]);
+        const int d = abs(cp - cm);
+        const int dmin = d - w, dmax = d + w;  // dmin < 0 is as good as 0 below
+        const bool loud = (flags >> q) & 1;
+        fail |= loud ? (dmax < F.k1) : (dmin > F.q0);
+        all &= loud ? (dmin >= F.k1) : (dmax <= F.q0);
+    }
+    att = !fail;
+    sure = all;
+}
+
+template <int kOut>
+__device__ __forceinline__ void frame_settle(const Smem& sm, const SearchConst* S, const LaunchArgs& A, uint32_t flags,
+                                             uint32_t k, uint32_t m, bool att, bool sure, uint32_t off,
+                                             uint16_t* list, uint32_t& cnt, uint32_t* first, Counters& ct,
+                                             unsigned lane_lt) {
+    bool pass = sure;
+    if (att & !sure) {
+        double lp[3], lm[3];
+        exact_linear(S, A, k, m, lp, lm);
+        int cp[3], cm[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            cp[q] = code_exact(lp[q], sm.thr_d);
+            cm[q] = code_exact(lm[q], sm.thr_d);
+        }
+        pass = classify_codes(S, cp, cm, flags);
+        ++ct.repairs;
+    }
+    append<kOut>(pass, off, list, cnt, first, lane_lt);
+}
+
+// `nch` full chunks of radius row k from angle m0 (na % 32 == 0), two chunks
+// per vote.
+template <int kOut>
+__device__ __forceinline__ void frame_row(const Smem& sm, const SearchConst* S, const CodeConsts& CC,
+                                          const FrameConsts& F, uint32_t flags, const LaunchArgs& A, uint32_t k,
+                                          float r, uint32_t m0, uint32_t nch, uint32_t off, uint16_t* list,
+                                          uint32_t& cnt, uint32_t* first, Counters& ct, unsigned lane,
+                                          unsigned lane_lt) {
+    constexpr uint32_t G = 2;
+    const float2* __restrict__ trig = reinterpret_cast<const float2*>(A.trig_f);
+    const uint32_t mb = m0 + lane;
+    uint32_t ix = mb;
+    const uint32_t iend = mb + 32u * (nch - nch % G);
+#pragma unroll 1
+    for (; ix != iend; ix += 32 * G) {
+        float2 sv[G];
+        bool at[G], su[G];
+#pragma unroll
+        for (uint32_t g = 0; g < G; ++g) sv[g] = __ldg(trig + ix + 32 * g);
+        bool any = false;
+#pragma unroll
+        for (uint32_t g = 0; g < G; ++g) {
+            frame_chunk(CC, F, flags, r, sv[g], at[g], su[g]);
+            any |= at[g];
+        }
+        if (__any_sync(kFull, any)) {
+            const uint32_t d = ix - mb;
+#pragma unroll
+            for (uint32_t g = 0; g < G; ++g)
+                frame_settle<kOut>(sm, S, A, flags, k, ix + 32 * g, at[g], su[g], off + lane + d + 32 * g, list, cnt,
+                                   first, ct, lane_lt);
+        }
+    }
+    if (nch % G) {
+        bool at, su;
+        frame_chunk(CC, F, flags, r, __ldg(trig + ix), at, su);
+        if (__any_sync(kFull, at))
+            frame_settle<kOut>(sm, S, A, flags, k, ix, at, su, off + lane + (ix - mb), list, cnt, first, ct, lane_lt);
+    }
+}
+
+template <int kOut>
+__device__ __forceinline__ void frame_tile(const Smem& sm, const SearchConst* S, const CodeConsts& CC,
+                                           uint32_t flags, const LaunchArgs& A, uint32_t i0, uint32_t i1,
+                                           uint16_t* list, uint32_t& cnt, uint32_t* first, Counters& ct,
+                                           unsigned lane, unsigned lane_lt) {
+    FrameConsts F;
+    F.k1 = __ldg(&S->k1);
+    F.q0 = __ldg(&S->q0);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) F.wc[q] = CC.ec[q] == INFINITY ? 256 : 1;
+    uint32_t k = div_na(i0, A);
+    uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
+    uint32_t i = i0;
+    while (i < i1) {
+        const uint32_t seg = min(i1 - i, static_cast<uint32_t>(A.na) - m0);
+        const float r = __ldg(&A.radii_f[k]);
+        frame_row<kOut>(sm, S, CC, F, flags, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);
+        i += seg;
+        m0 = 0;
+        ++k;
+    }
+}
+
 template <int kL, int kOut>
 __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t i0,
                                           uint32_t i1, uint16_t* list, uint32_t& cnt, uint32_t* first, Counters& ct,
@@ -740,7 +947,8 @@ template <int kMode, int kOut, int kPath>
 __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    load_tables<kMode == kModeCodes>(sm, A);  // phase 1 needs codes only in FrameDiff x Quantized
+    // phase 1 quantizes only in FrameDiff x Quantized; Continuous x FrameDiff prefilters on signal bounds
+    load_tables<kMode == kModeCodes ? kTabCode : (kMode == kModeSignal ? kTabSignal : kTabNone)>(sm, A);
     const uint32_t tab = ctab_addr(sm.ctab);
     const unsigned lane = threadIdx.x & 31;
     const unsigned lane_lt = (1u << lane) - 1u;
@@ -811,15 +1019,21 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
             } else {
                 band_tile<1, kOut>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
             }
+        } else if (kMode == kModeCodes && kPath == kPathFast && A.aligned) {
+            CodeConsts CC;
+            load_code_consts(S, CC, tab);
+            frame_tile<kOut>(sm, S, CC, C.flags, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
         } else {
             CodeConsts CC;
             load_code_consts(S, CC, tab);
+            SigConsts SG;
+            if (kMode == kModeSignal) load_sig_consts(S, SG);
             for (uint32_t base = i0; base < i1; base += 32) {
                 const bool active = base + lane < i1;
                 const uint32_t i = active ? base + lane : i1 - 1;
                 const uint32_t k = div_na(i, A);
                 const uint32_t m = i - k * static_cast<uint32_t>(A.na);
-                const bool pass = candidate_pass<kMode, kPath>(sm, S, C, CC, A, k, m, active, ct);
+                const bool pass = candidate_pass<kMode, kPath>(sm, S, C, CC, SG, A, k, m, active, ct);
                 append<kOut>(pass, i - i0, list, cnt, first, lane_lt);
             }
         }
@@ -934,7 +1148,7 @@ template <int kMode, int kPath>
 __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    load_tables<true>(sm, A);
+    load_tables<kTabCode>(sm, A);
     const uint32_t tab = ctab_addr(sm.ctab);
     const unsigned lane = threadIdx.x & 31;
     const uint32_t n_work = *reinterpret_cast<volatile unsigned int*>(&A.ticket[3]);
@@ -1113,15 +1327,15 @@ using OccFn = int (*)();
 const LaunchFn kLaunch[kModes][3][3] = {
     {CVG_ROW(kModeBand, kPathFast), CVG_ROW(kModeBand, kPathExact), CVG_ROW(kModeBand, kPathAudit)},
     {CVG_ROW(kModeCodes, kPathFast), CVG_ROW(kModeCodes, kPathExact), CVG_ROW(kModeCodes, kPathAudit)},
-    // continuous FrameDiff: one FP64 decision path (all three paths run it)
-    {CVG_ROW(kModeSignal, kPathExact), CVG_ROW(kModeSignal, kPathExact), CVG_ROW(kModeSignal, kPathExact)},
+    // continuous FrameDiff: FP32 signal-bound prefilter + FP64 decisions (EXACT: FP64 only)
+    {CVG_ROW(kModeSignal, kPathFast), CVG_ROW(kModeSignal, kPathExact), CVG_ROW(kModeSignal, kPathAudit)},
 };
 using Phase1Fn = cudaError_t (*)(const LaunchArgs&, int, cudaStream_t);
 #define CVG_P1(M, P) {phase1_t<M, kOutPairs, P>, phase1_t<M, kOutCounts, P>, phase1_t<M, kOutFirst, P>}
 const Phase1Fn kPhase1[kModes][3][3] = {
     {CVG_P1(kModeBand, kPathFast), CVG_P1(kModeBand, kPathExact), CVG_P1(kModeBand, kPathAudit)},
     {CVG_P1(kModeCodes, kPathFast), CVG_P1(kModeCodes, kPathExact), CVG_P1(kModeCodes, kPathAudit)},
-    {CVG_P1(kModeSignal, kPathExact), CVG_P1(kModeSignal, kPathExact), CVG_P1(kModeSignal, kPathExact)},
+    {CVG_P1(kModeSignal, kPathFast), CVG_P1(kModeSignal, kPathExact), CVG_P1(kModeSignal, kPathAudit)},
 };
 using EmitFn = cudaError_t (*)(const LaunchArgs&, int, int, cudaStream_t);
 const EmitFn kEmit[kModes][3] = {
@@ -1133,7 +1347,7 @@ const EmitFn kEmit[kModes][3] = {
 const OccFn kOcc[kModes][3][3] = {
     {CVG_OCC(kModeBand, kPathFast), CVG_OCC(kModeBand, kPathExact), CVG_OCC(kModeBand, kPathAudit)},
     {CVG_OCC(kModeCodes, kPathFast), CVG_OCC(kModeCodes, kPathExact), CVG_OCC(kModeCodes, kPathAudit)},
-    {CVG_OCC(kModeSignal, kPathExact), CVG_OCC(kModeSignal, kPathExact), CVG_OCC(kModeSignal, kPathExact)},
+    {CVG_OCC(kModeSignal, kPathFast), CVG_OCC(kModeSignal, kPathExact), CVG_OCC(kModeSignal, kPathAudit)},
 };
 
 }  // namespace

@@ -85,6 +85,7 @@ struct LaunchArgs {
     const double* trig_d;      // [na][2] = (sin, cos), glibc doubles (search.cpp:414-419)
     const double* thr_d;       // [256] QuantTable thresholds (convert_kernel.hpp:123-141)
     const float* ctab;         // [kGuessBuckets + 1][2] code table {t, bits(c)} (cvg_host.h Tables)
+    const float* stab;         // [kGuessBuckets + 1][2] signal bounds {L, U} (kModeSignal plans only)
     double minv[9];            // kXyzToRgb (convert_kernel.hpp:47), row-major
     int32_t n_searches;
     int32_t nr;

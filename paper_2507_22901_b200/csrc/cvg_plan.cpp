@@ -290,6 +290,8 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     const size_t o_tf = L.take(sizeof(float) * trig_f.size());
     const size_t o_thd = L.take(sizeof(double) * 256);
     const size_t o_ctab = L.take(sizeof(T.ctab));
+    const bool signal = p->mode == cvg::kModeSignal;
+    const size_t o_stab = signal ? L.take(sizeof(T.stab)) : 0;
     const size_t bytes = L.off;
     p->input_bytes = bytes;
     p->t_prep_end = now_ms();
@@ -326,6 +328,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     std::memcpy(stage + o_tf, trig_f.data(), sizeof(float) * trig_f.size());
     std::memcpy(stage + o_thd, T.thr, sizeof(double) * 256);
     std::memcpy(stage + o_ctab, T.ctab, sizeof(T.ctab));
+    if (signal) std::memcpy(stage + o_stab, T.stab, sizeof(T.stab));
     LaunchArgs& A = p->args;
     std::memset(&A, 0, sizeof(A));
     A.sc = at<const SearchConst>(p->d_const, o_sc);
@@ -338,6 +341,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.trig_f = at<const float>(p->d_const, o_tf);
     A.thr_d = at<const double>(p->d_const, o_thd);
     A.ctab = at<const float>(p->d_const, o_ctab);
+    A.stab = signal ? at<const float>(p->d_const, o_stab) : nullptr;
     // No sync: the staging block stays with the plan until it is released,
     // which happens after the stream has passed this copy.
     cudaError_t e = cudaMemcpyAsync(p->d_const, stage, bytes, cudaMemcpyHostToDevice, ctx->stream);
@@ -874,6 +878,7 @@ void cvg_d65_white(double out[3]) {
 
 void cvg_quant_thresholds(double out[256]) { std::memcpy(out, tables().thr, sizeof(double) * 256); }
 void cvg_code_table(float out[8194]) { std::memcpy(out, tables().ctab, sizeof(tables().ctab)); }
+void cvg_signal_table(float out[8194]) { std::memcpy(out, tables().stab, sizeof(tables().stab)); }
 float cvg_code_slack(void) { return cvg::kCodeSlack; }
 
 double cvg_measure_ffma_peak(int device, float* ms_out) { return cvg::measure_ffma_peak(device, ms_out); }

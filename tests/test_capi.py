@@ -304,3 +304,28 @@ def test_code_table_proof(lib, E):
     assert np.array_equal(code[ok], lo[ok]) and np.array_equal(code[ok], hi[ok])
     # the unverified share is the +-E windows around the 255 thresholds
     assert ok[len(near):].mean() > 1.0 - 600 * E
+
+
+def test_signal_table_bounds(lib):
+    """The Continuous x FrameDiff prefilter's table (cvg_kernels.cu
+    signal_bounds): for every double x in bucket i = [(i - 1/2), (i + 1/2)] / 4096,
+    L[i] <= signal_value(x) <= U[i] (convert_kernel.hpp:109-112), and the
+    bounds are tight enough to decide almost every candidate."""
+    tab = np.zeros(8194, np.float32)
+    lib.cvg_signal_table(tab.ctypes.data_as(C.POINTER(C.c_float)))
+    L, U = tab[0::2].astype(np.float64), tab[1::2].astype(np.float64)
+
+    def signal(x):
+        x = np.clip(x, 0.0, 1.0)
+        return 255.0 * np.where(x <= 0.0031308, 12.92 * x, 1.055 * np.power(x, 1.0 / 2.4) - 0.055)
+
+    rng = np.random.default_rng(11)
+    i = np.arange(4097)
+    edges = np.concatenate([(i - 0.5) / 4096, (i + 0.5) / 4096])
+    x = np.concatenate([rng.uniform(-0.05, 1.05, 1_000_000), edges, np.nextafter(edges, 2), np.nextafter(edges, -2)])
+    b = np.clip(np.rint(np.clip(x, 0, 1) * 4096), 0, 4096).astype(np.int64)
+    inside = (np.clip(x, 0, 1) >= (b - 0.5) / 4096) & (np.clip(x, 0, 1) <= (b + 0.5) / 4096)
+    s = signal(x)
+    assert np.all(L[b][inside] <= s[inside]) and np.all(s[inside] <= U[b][inside])
+    assert np.all(np.diff(L) >= 0) and np.all(np.diff(U) >= 0) and L[0] <= 0.0 and U[-1] >= 255.0
+    assert (U - L).max() < 1.0 and np.median(U - L) < 0.05

@@ -299,7 +299,7 @@ def test_continuous_api_deltas_match_oracle(cv, ctx, oracle):
             assert [pair.deltas.dr, pair.deltas.dg, pair.deltas.db] == d.tolist()
 
 
-@pytest.mark.parametrize("path", ["fast", "exact"])
+@pytest.mark.parametrize("path", ["fast", "exact", "audit"])
 @pytest.mark.parametrize("out", ["pairs", "counts", "first"])
 def test_continuous_frame_diff_bit_exact(ctx, oracle, path, out):
     """DeltaMode::Continuous x FrameDiff (search.cpp:146-173): |s(p) - s(m)|
@@ -313,6 +313,10 @@ def test_continuous_frame_diff_bit_exact(ctx, oracle, path, out):
                 t.append(tg); p.append(pat); v.append(vt); r.append(rn)
     wl = W.Workload("cfd", np.array(t, np.int32), np.array(p, np.int32), np.array(v), np.array(r), radii, angles)
     res = run(ctx, wl, path=path, mode=1, basis=1, output=out)
+    # the FP32 signal-bound prefilter never decides against the FP64 path
+    assert res["stats"]["audit_violations"] == 0
+    if path == "fast":
+        assert res["stats"]["band_repairs"] < wl.candidates // 20  # the prefilter decides most candidates
     total = 0
     for s in range(wl.n_searches):
         oi, oc, _ = oracle.search(wl.targets[s], int(wl.patterns[s]), wl.v_th[s], wl.r_novib[s], radii, angles,
