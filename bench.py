@@ -352,6 +352,7 @@ def run_ours(args):
     # per-launch kernel time over the timed steps: events inside the plan
     # cover only the search kernel; re-measure a few steps for the roofline
     kern, phases = [], []
+    plan.set_phase_marks(True)  # events between the kernels (off in the timed steps: they block the PDL overlap)
     for _ in range(min(args.steps, 20)):
         flush.zero_()
         plan.run(stream.cuda_stream)

@@ -164,6 +164,10 @@ CVG_API int cvg_plan_last_kernel_ms(cvg_plan* plan, float* ms);
  * offset scan, pair emit (scan/emit are 0 outside CVG_OUT_PAIRS; the FIRST
  * epilogue is counted in phase 1) */
 CVG_API int cvg_plan_last_phase_ms(cvg_plan* plan, float* phase1_ms, float* scan_ms, float* emit_ms);
+/* Record events between the three kernels of the next runs, so that
+ * cvg_plan_last_phase_ms can split a run (default off: the kernels then
+ * launch with programmatic dependent launch and overlap their hand-off). */
+CVG_API int cvg_plan_set_phase_marks(cvg_plan* plan, int on);
 /* bytes of device-resident input the plan uploaded (constants + grid tables) */
 CVG_API uint64_t cvg_plan_input_bytes(const cvg_plan* plan);
 /* number of kernel launches one cvg_plan_run enqueues */

@@ -688,6 +688,7 @@ PYBIND11_MODULE(_core, m) {
         .def_property_readonly("launches", [](const Plan& p) { return cvg_plan_launches(p.plan); })
         .def_property_readonly("candidates", [](const Plan& p) { return cvg_plan_candidates(p.plan); })
         .def_property_readonly("input_bytes", [](const Plan& p) { return cvg_plan_input_bytes(p.plan); })
+        .def("set_phase_marks", [](Plan& p, bool on) { check(cvg_plan_set_phase_marks(p.plan, on ? 1 : 0)); })
         .def("last_phase_ms", [](Plan& p) {
             float a = 0.f, b = 0.f, c = 0.f;
             check(cvg_plan_last_phase_ms(p.plan, &a, &b, &c));

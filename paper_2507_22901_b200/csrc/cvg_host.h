@@ -431,6 +431,8 @@ struct cvg_plan {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // PAIRS: [0] after phase 1, [1] after the scan (pipelined searches use [2], [3] per view)
     cudaEvent_t marks[4] = {nullptr, nullptr, nullptr, nullptr};
+    bool phase_marks = false;  // record marks between the kernels (breaks their PDL overlap)
+    bool marked = false;       // the last run recorded them
     bool external_out = false;  // the caller supplies the pair buffers (streamed search): no reserve
     bool ran = false;
     cudaStream_t last_stream = nullptr;

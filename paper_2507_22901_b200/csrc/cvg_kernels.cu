@@ -67,6 +67,12 @@ __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long 
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Programmatic dependent launch: scan and emit launch while their
+// predecessor drains (its CTAs trigger when they run out of work) and wait
+// here for its completion and memory before touching its outputs.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ const SearchConst* search_const(const LaunchArgs& A, uint32_t s) {
     return A.sc + (A.sc_index ? __ldg(&A.sc_index[s]) : s);
 }
@@ -1053,6 +1059,7 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         }
         c = __shfl_sync(kFull, t_claim, 0);
     }
+    pdl_trigger();  // no tiles left for this warp: the scan may launch once every CTA has said so
     flush_counters(ct, A, lane);
 }
 
@@ -1062,6 +1069,8 @@ __global__ void __launch_bounds__(kBlock) scan_kernel(const LaunchArgs A) {
     __shared__ uint32_t s_block;
     __shared__ unsigned long long s_warp[kWarpsPerBlock];
     __shared__ unsigned long long s_prefix;
+    pdl_trigger();  // emit CTAs may launch (and load their tables) while the scan runs
+    pdl_wait();     // phase 1 complete: tile counts and tickets visible
     if (threadIdx.x == 0) s_block = atomicAdd(&A.ticket[1], 1u);
     __syncthreads();
     const uint32_t b = s_block;
@@ -1148,8 +1157,9 @@ template <int kMode, int kPath>
 __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    load_tables<kTabCode>(sm, A);
+    load_tables<kTabCode>(sm, A);  // constant inputs only: before the wait
     const uint32_t tab = ctab_addr(sm.ctab);
+    pdl_wait();  // scan (and so phase 1) complete
     const unsigned lane = threadIdx.x & 31;
     const uint32_t n_work = *reinterpret_cast<volatile unsigned int*>(&A.ticket[3]);
     const unsigned long long base0 = A.base_offset ? *A.base_offset : 0ull;
@@ -1282,17 +1292,32 @@ cudaError_t phase1_t(const LaunchArgs& a, int grid, cudaStream_t st) {
 // quantizes passing pairs on the FP32 code path with FP64 repair).
 constexpr int emit_path(int mode, int path) { return mode == kModeSignal ? kPathFast : path; }
 
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// before its stream predecessor completes; it calls pdl_wait() first.
+cudaError_t launch_pdl(void (*kernel)(LaunchArgs), unsigned grid, unsigned threads, size_t smem, cudaStream_t st,
+                       const LaunchArgs& a) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 template <int kMode, int kPath>
 cudaError_t emit_t(const LaunchArgs& a, int grid, int threads, cudaStream_t st) {
-    emit_kernel<kMode, kPath><<<grid, threads, sizeof(Smem), st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(emit_kernel<kMode, kPath>, grid, threads, sizeof(Smem), st, a);
 }
 
 cudaError_t scan_l(const LaunchArgs& a, cudaStream_t st) {
     const unsigned scan_blocks = static_cast<unsigned>((a.n_tiles + kScanTile - 1) / kScanTile);
     if (scan_blocks == 0) return cudaSuccess;
-    scan_kernel<<<scan_blocks, kBlock, 0, st>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(scan_kernel, scan_blocks, kBlock, 0, st, a);
 }
 
 template <int kMode, int kOut, int kPath>

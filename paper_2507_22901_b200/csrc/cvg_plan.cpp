@@ -475,7 +475,8 @@ int plan_enqueue(cvg_plan* p, cudaStream_t st) {
     CVG_CUDA(cudaMemsetAsync(p->d_work, 0, p->work_bytes, st));
     if (p->out == cvg::kOutFirst) CVG_CUDA(cudaMemsetAsync(p->d_first, 0xff, static_cast<size_t>(p->n) * 4, st));
     CVG_CUDA(cudaEventRecord(p->ev0, st));
-    CVG_CUDA(cvg::launch_search(p->args, p->mode, p->out, p->path, p->grid, st, p->marks));
+    p->marked = p->phase_marks;
+    CVG_CUDA(cvg::launch_search(p->args, p->mode, p->out, p->path, p->grid, st, p->marked ? p->marks : nullptr));
     if (p->out == cvg::kOutFirst) CVG_CUDA(cvg::launch_first_codes(p->args, st));
     CVG_CUDA(cudaEventRecord(p->ev1, st));
     return CVG_OK;
@@ -777,9 +778,16 @@ int cvg_plan_last_phase_ms(cvg_plan* p, float* phase1_ms, float* scan_ms, float*
     CVG_CUDA(cudaEventSynchronize(p->ev1));
     if (p->out != cvg::kOutPairs) return cudaEventElapsedTime(phase1_ms, p->ev0, p->ev1) == cudaSuccess
                                              ? CVG_OK : fail(CVG_ECUDA, "event timing failed");
+    if (!p->marked) return fail(CVG_EINVAL, "the last run recorded no phase marks (cvg_plan_set_phase_marks)");
     CVG_CUDA(cudaEventElapsedTime(phase1_ms, p->ev0, p->marks[0]));
     CVG_CUDA(cudaEventElapsedTime(scan_ms, p->marks[0], p->marks[1]));
     CVG_CUDA(cudaEventElapsedTime(emit_ms, p->marks[1], p->ev1));
+    return CVG_OK;
+}
+
+int cvg_plan_set_phase_marks(cvg_plan* p, int on) {
+    if (!p) return fail(CVG_EINVAL, "null plan");
+    p->phase_marks = on != 0;
     return CVG_OK;
 }
 
