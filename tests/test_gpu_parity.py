@@ -27,10 +27,10 @@ def split(res, s):
     return res["idx"][a:b], res["codes"][a:b]
 
 
-def oracle_records(oracle, wl, s, basis=0, white=None, workers=4):
+def oracle_records(oracle, wl, s, basis=0, white=None, workers=4, mode=0):
     idx, codes, _ = oracle.search(wl.targets[s], int(wl.patterns[s]), wl.v_th[s], wl.r_novib[s], wl.radii,
                                   wl.angles, delta_basis=basis, white=white, method=1, workers=workers,
-                                  want_deltas=False)
+                                  want_deltas=False, delta_mode=mode)
     return idx, codes
 
 
@@ -403,13 +403,14 @@ def test_edge_grids_vs_oracle(ctx, oracle, gname, path):
         for pat, vt, rn in ((7, 50.0, 0.5), (5, 100.0, 0.25), (2, 20.0, 1.0), (1, 300.0, 0.5), (6, 0.5, 1.0)):
             t.append(tg); p.append(pat); v.append(vt); r.append(rn)
     wl = W.Workload("edge", np.array(t, np.int32), np.array(p, np.int32), np.array(v), np.array(r), radii, angles)
-    for basis in (0, 1):
-        res = run(ctx, wl, path=path, basis=basis)
+    # Quantized x {TargetSwing, FrameDiff}, Continuous x FrameDiff (its FP32 prefilter)
+    for mode, basis in ((0, 0), (0, 1), (1, 1)):
+        res = run(ctx, wl, path=path, basis=basis, mode=mode)
         for s in range(wl.n_searches):
             idx, codes = split(res, s)
-            oi, oc = oracle_records(oracle, wl, s, basis=basis, workers=1)
-            assert np.array_equal(idx, oi), (gname, s, basis)
-            assert np.array_equal(codes, oc), (gname, s, basis)
+            oi, oc = oracle_records(oracle, wl, s, basis=basis, workers=1, mode=mode)
+            assert np.array_equal(idx, oi), (gname, s, mode, basis)
+            assert np.array_equal(codes, oc), (gname, s, mode, basis)
         assert_clean(res, path)
 
 
