@@ -740,6 +740,57 @@ __device__ __forceinline__ void band_settle(const SearchConst* S, const Consts& 
     append<kOut>(pass, off, list, cnt, first, lane_lt);
 }
 
+// Slow path of a group of G chunks (some lane needs attention): the certain
+// passes, FP64 repair of the unsure lanes behind one vote, then the ordered
+// appends.  COUNTS / FIRST append with one ballot per chunk and, while the
+// tile has no pass yet, a warp-uniform search for the first passing lane.
+template <int kOut, uint32_t G>
+__device__ __forceinline__ void band_settle_group(const SearchConst* S, const Consts& C, const LaunchArgs& A,
+                                                  uint32_t k, uint32_t ix, const float* lv, const float* qv,
+                                                  uint32_t off, uint16_t* list, uint32_t& cnt, uint32_t* first,
+                                                  Counters& ct, unsigned lane_lt) {
+    bool pass[G], uns[G], any_uns = false;
+#pragma unroll
+    for (uint32_t g = 0; g < G; ++g) {
+        pass[g] = band_certain(C, lv[g], qv[g]);
+        uns[g] = band_attention(C, lv[g], qv[g]) & !pass[g];
+        any_uns |= uns[g];
+    }
+    if (__any_sync(kFull, any_uns)) {
+#pragma unroll
+        for (uint32_t g = 0; g < G; ++g) {
+            if (uns[g]) {
+                double lp[3], lm[3];
+                exact_linear(S, A, k, ix + 32 * g, lp, lm);
+                pass[g] = exact_band(S, lp, lm, C.flags);
+                ++ct.repairs;
+            }
+        }
+    }
+    if (kOut == kOutPairs) {
+#pragma unroll
+        for (uint32_t g = 0; g < G; ++g) append<kOut>(pass[g], off + 32 * g, list, cnt, first, lane_lt);
+    } else {
+        unsigned b[G];
+        uint32_t n = 0;
+#pragma unroll
+        for (uint32_t g = 0; g < G; ++g) {
+            b[g] = __ballot_sync(kFull, pass[g]);
+            n += __popc(b[g]);
+        }
+        if (kOut == kOutFirst && cnt == 0 && n) {
+#pragma unroll
+            for (uint32_t g = 0; g < G; ++g) {
+                if (b[g]) {
+                    if (pass[g] && (b[g] & lane_lt) == 0) *first = off + 32 * g;
+                    break;
+                }
+            }
+        }
+        cnt += n;
+    }
+}
+
 template <int kL, bool kCubeOnly>
 __device__ __forceinline__ void band_chunk(const Consts& C, float r, float2 sc, float& minl, float& maxq) {
     if (kCubeOnly) {
@@ -786,14 +837,8 @@ __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, 
             band_chunk<kL, kCubeOnly>(C, r, sv[g], lv[g], qv[g]);
             att |= band_attention(C, lv[g], qv[g]);
         }
-        if (__any_sync(kFull, att)) {
-            const uint32_t d = ix - mb;
-#pragma unroll
-            for (uint32_t g = 0; g < G; ++g) {
-                band_settle<kOut>(S, C, A, k, ix + 32 * g, lv[g], qv[g], off + lane + d + 32 * g, list, cnt, first, ct,
-                                  lane_lt);
-            }
-        }
+        if (__any_sync(kFull, att))
+            band_settle_group<kOut, G>(S, C, A, k, ix, lv, qv, off + lane + (ix - mb), list, cnt, first, ct, lane_lt);
     }
 #pragma unroll 1
     for (uint32_t j = nch % G; j; --j, ix += 32) {
