@@ -1,28 +1,29 @@
 // cvg_kernels.cu -- fused color-pair search for B200 (sm_100a).
 //
-// One persistent kernel per batch of searches.  Each warp claims 2048-
-// candidate tiles (a contiguous range of one search's canonical index
-// i = k*na + m) from a global ticket and, per tile:
+// Three kernels per batch of searches (one stream, K2/K3 by programmatic
+// dependent launch):
 //
-//   phase 1  synthesizes every candidate in registers from (target, r_k,
-//            theta_m) -- no per-candidate HBM traffic besides the L1/L2-
-//            resident trig table -- runs the Lab -> linear RGB conversion and
-//            the band test of the reference batch path (search.cpp:230-278,
-//            291-329) in FP32 with a proven per-channel error bound, and sends
-//            the rare candidates whose decision lies inside that bound through
-//            the FP64 op-for-op restatement (bit-identical to the reference).
-//            Passing candidates are compacted into a per-warp shared-memory
-//            list with ballot/popc (the reference's pass-2 extraction,
-//            search.cpp:379-397).
-//   look-back  the warp publishes its tile count and reads its predecessors'
-//            (decoupled look-back), giving the tile's output offset in the
-//            global canonical order -- one pass, no count kernel, and output
-//            order independent of scheduling (search.cpp:448-455, test
-//            tests/test_search.cpp:206-235).
-//   phase 2  the warp walks its compacted list 32 pairs at a time (all lanes
-//            busy), recomputes the six linear values, quantizes them through
-//            the float threshold table with the same bound (FP64 repair when
-//            unsure) and writes idx + 6 code bytes with coalesced stores.
+//   K1 phase1_kernel  persistent; each warp claims 4096-candidate tiles (a
+//            contiguous range of one search's canonical index i = k*na + m)
+//            from a global ticket.  It synthesizes every candidate in
+//            registers from (target, r_k, theta_m) -- no per-candidate HBM
+//            traffic besides the L1/L2-resident trig table -- runs the Lab ->
+//            linear RGB conversion and the band test of the reference batch
+//            path (search.cpp:230-278, 291-329) in FP32 with a proven
+//            per-channel error bound, and sends the rare candidates whose
+//            decision lies inside that bound through the FP64 op-for-op
+//            restatement (bit-identical to the reference).  Passing offsets
+//            are appended to the tile's ordered list with ballot/popc (the
+//            reference's pass-2 extraction, search.cpp:379-397), or counted
+//            (COUNTS / FIRST).  The FrameDiff modes have their own decisions
+//            (code bounds; FP32 signal bounds) with the same FP64 fallback.
+//   K2 scan_kernel  exclusive scan of the tile counts (chained, decoupled
+//            look-back): each tile's output offset in the global canonical
+//            order, independent of scheduling (search.cpp:448-455).
+//   K3 emit_kernel  warps walk the lists 32 pairs at a time (all lanes busy),
+//            recompute the six linear values, quantize them through the code
+//            table with the same bound (FP64 repair when unsure) and write
+//            idx + 6 code bytes with coalesced stores.
 //
 // Result: per-search counts and pair lists bit-identical to the reference.
 #include <cuda_runtime.h>
@@ -990,7 +991,7 @@ __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C,
     }
 }
 
-// K1: decide every candidate.  Warps claim 2048-candidate tiles (contiguous
+// K1: decide every candidate.  Warps claim 4096-candidate tiles (contiguous
 // canonical ranges of one search) from a ticket, prefetching the next ticket.
 // PAIRS: tile count + ordered passing offsets to scratch; COUNTS: per-search
 // counts; FIRST: counts + first passing index.

@@ -451,6 +451,20 @@ def test_plan_overflow_then_reserve(ctx):
         plan.run()
     assert plan.sync() == 3785016
     assert plan.launches == 3  # phase 1, offset scan, emit
+    # kernels chained by programmatic dependent launch: no per-kernel split
+    # unless phase marks are requested (events between the kernels)
+    with pytest.raises(ValueError, match="phase marks"):
+        plan.last_phase_ms()
+    plan.set_phase_marks(True)
+    plan.run()
+    assert plan.sync() == 3785016
+    p1, sc, em = plan.last_phase_ms()
+    assert p1 > 0 and sc > 0 and em > 0
+    assert abs((p1 + sc + em) - plan.last_kernel_ms()) < 0.05 * plan.last_kernel_ms()
+    plan.set_phase_marks(False)
+    plan.run()
+    assert plan.sync() == 3785016
+    assert sha_by_search(plan.fetch()) == golden("workloads.json")["cfg1"]["sha256"]
 
 
 def test_huge_single_search_linearity(ctx):
