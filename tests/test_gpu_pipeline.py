@@ -24,10 +24,12 @@ def single_plan(ctx, targets, pats, vt, rn, radii, angles, step):
     return np.concatenate(idx), np.concatenate(codes), np.concatenate(counts)
 
 
+@pytest.mark.parametrize("na", [1024, 1000])
 @pytest.mark.parametrize("order", ["sparse_first", "dense_first", "mixed"])
-def test_pipelined_equals_single_plan(ctx, order):
+def test_pipelined_equals_single_plan(ctx, order, na):
+    """na = 1000: tiles straddle radius rows."""
     rng = np.random.default_rng({"sparse_first": 1, "dense_first": 2, "mixed": 3}[order])
-    radii, angles = W.radii(256, 1.0), W.angles(1024)
+    radii, angles = W.radii(256, 1.0), W.angles(na)
     n = 320  # 83.9M candidates -> 2 ranges (sizes 1:2)
     targets = rng.integers(0, 256, (n, 3)).astype(np.int32)
     pats = rng.integers(1, 8, n).astype(np.int32)
