@@ -28,6 +28,7 @@
 // Result: per-search counts and pair lists bit-identical to the reference.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstddef>
 #include <cstdint>
 
@@ -1327,8 +1328,17 @@ __global__ void ffma_peak_kernel(float* out, int iters, float a, float b) {
     if (r == 1234.5f) out[0] = r;
 }
 
+// Persistent grids, but never more blocks than there is work for: one warp
+// per tile (phase 1) or per emit item at most.  Small batches (one search of
+// a few tiles) then skip launching and table-loading hundreds of idle blocks.
+inline int work_grid(int grid, uint64_t units, int warps) {
+    const uint64_t need = (units + static_cast<uint64_t>(warps) - 1) / static_cast<uint64_t>(warps);
+    return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(grid), need)));
+}
+
 template <int kMode, int kOut, int kPath>
 cudaError_t phase1_t(const LaunchArgs& a, int grid, cudaStream_t st) {
+    grid = work_grid(grid, a.n_tiles, kWarpsPerBlock);
     // The dynamic shared-memory sizes are opted into by occupancy_t (plan creation).
     phase1_kernel<kMode, kOut, kPath><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);
     return cudaGetLastError();
@@ -1357,6 +1367,7 @@ cudaError_t launch_pdl(void (*kernel)(LaunchArgs), unsigned grid, unsigned threa
 
 template <int kMode, int kPath>
 cudaError_t emit_t(const LaunchArgs& a, int grid, int threads, cudaStream_t st) {
+    grid = work_grid(grid, a.n_tiles * (kTile / kEmitSpan), threads / 32);
     return launch_pdl(emit_kernel<kMode, kPath>, grid, threads, sizeof(Smem), st, a);
 }
 
