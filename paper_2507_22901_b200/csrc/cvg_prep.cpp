@@ -321,8 +321,21 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
     std::memset(&S, 0, sizeof(S));
     const double* wp = white_or_d65(d->white_point);
     const int32_t* t = d->target_rgb + 3 * s;
+    // srgb_to_lab of the target (color.cpp:57-70: 3 glibc pow + 3 cbrt, most
+    // of a record's cost); batches repeat a target over consecutive searches,
+    // so each thread remembers its last one
+    thread_local int32_t last_t[3] = {-1, -1, -1};
+    thread_local double last_wp[3] = {0, 0, 0}, last_lab[3];
     double lab[3];
-    to_lab(t, wp, lab);
+    if (t[0] == last_t[0] && t[1] == last_t[1] && t[2] == last_t[2] && wp[0] == last_wp[0] && wp[1] == last_wp[1] &&
+        wp[2] == last_wp[2]) {
+        std::memcpy(lab, last_lab, sizeof(lab));
+    } else {
+        to_lab(t, wp, lab);
+        std::memcpy(last_t, t, sizeof(last_t));
+        std::memcpy(last_wp, wp, sizeof(last_wp));
+        std::memcpy(last_lab, lab, sizeof(lab));
+    }
     // search.cpp:345-355
     const auto& m = kXyzToRgb.m;
     const double fy = (lab[0] + 16.0) / 116.0;
