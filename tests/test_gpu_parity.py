@@ -263,6 +263,36 @@ def test_frame_diff_basis(cv, ctx):
     assert len(fd) != len(cv.batch_search(*args))
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("out", ["pairs", "counts", "first"])
+def test_frame_diff_aligned_grid_outputs(ctx, oracle, mode, out):
+    """FrameDiff on an aligned grid (na % 32 == 0): the FAST path's own row
+    loops -- code bounds (Quantized, frame_tile) and FP32 signal bounds
+    (Continuous) -- in every output mode, against the oracle search by search."""
+    radii, angles = W.radii(48, 2.5), W.angles(256)
+    rng = np.random.default_rng(17 + mode)
+    n = 40
+    t = rng.integers(0, 256, (n, 3)).astype(np.int32)
+    t[:4] = [[0, 0, 0], [255, 255, 255], [8, 8, 8], [255, 0, 128]]
+    p = rng.integers(1, 8, n).astype(np.int32)
+    v = rng.choice([20.0, 50.0, 100.0, 150.5], n)
+    r = rng.choice([0.125, 0.25, 0.5, 1.0], n)
+    wl = W.Workload("fd", t, p, v, r, radii, angles)
+    res = run(ctx, wl, basis=1, mode=mode, output=out)
+    assert res["stats"]["class_mismatch"] == 0
+    total = 0
+    for s in range(n):
+        oi, oc = oracle_records(oracle, wl, s, basis=1, workers=1, mode=mode)
+        total += len(oi)
+        assert res["counts"][s] == len(oi), s
+        if out == "pairs":
+            idx, codes = split(res, s)
+            assert np.array_equal(idx, oi) and np.array_equal(codes, oc), s
+        elif out == "first" and len(oi):
+            assert res["first_idx"][s] == oi[0] and np.array_equal(res["first_codes"][s], oc[0]), s
+    assert total > 1000
+
+
 @pytest.mark.parametrize("path", ["fast", "audit", "exact"])
 def test_continuous_target_swing_bit_exact(ctx, oracle, path):
     """DeltaMode::Continuous x TargetSwing (search.cpp:161-180): signal-space
