@@ -129,6 +129,13 @@ struct Tables {
     // [(i - 1/2) / 4096, (i + 1/2) / 4096] (signal_value is monotone; the
     // bounds are rounded outward to float with a 1e-9 allowance for glibc pow).
     float stab[cvg::kGuessBuckets + 1][2];
+    // FrameDiff linear-space bounds (QuantTable thresholds, clamped values):
+    // |code(p) - code(m)| >= k1 needs |x_p - x_m| > fd_loud[k1] =
+    // min_c (thr[c + k1 - 1] - thr[c]); |code(p) - code(m)| <= q0 needs
+    // |x_p - x_m| < fd_quiet[q0] = max_c (thr[min(c + q0 + 1, 256)] - thr[c]),
+    // thr[256] = 1 (x clamped to [0, 1]).  k1 = 256 / q0 = 255: +inf.
+    double fd_loud[257];
+    double fd_quiet[256];
     Tables() {
         thr[0] = 0.0;
         for (int code = 1; code <= 255; ++code) {
@@ -162,6 +169,17 @@ struct Tables {
             if (fu < su) fu = std::nextafter(fu, INFINITY);
             stab[i][0] = fl;
             stab[i][1] = fu;
+        }
+        for (int k1 = 1; k1 <= 256; ++k1) {
+            double d = INFINITY;
+            for (int c = 1; k1 <= 255 && c + k1 - 1 <= 255; ++c) d = std::min(d, thr[c + k1 - 1] - thr[c]);
+            fd_loud[k1] = d;
+        }
+        fd_loud[0] = -INFINITY;  // unused (k1 >= 1)
+        for (int q0 = 0; q0 <= 255; ++q0) {
+            double d = 0.0;
+            for (int c = 0; q0 < 255 && c <= 255; ++c) d = std::max(d, (c + q0 + 1 >= 256 ? 1.0 : thr[c + q0 + 1]) - thr[c]);
+            fd_quiet[q0] = q0 >= 255 ? INFINITY : d;
         }
     }
     int code(double x) const {

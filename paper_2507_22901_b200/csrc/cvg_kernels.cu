@@ -266,6 +266,7 @@ __device__ __forceinline__ float add_rp_sat(float a, float b) {
 // rounding of the threshold and the difference's double rounding).
 struct SigConsts {
     float e[3], th[3], tl[3];
+    float flo[3], fhi[3];  // SearchConst::fd_bounds: linear-space sure-fail bounds (frame_signal_bounds)
 };
 
 __device__ __forceinline__ void load_sig_consts(const SearchConst* S, SigConsts& g) {
@@ -275,6 +276,8 @@ __device__ __forceinline__ void load_sig_consts(const SearchConst* S, SigConsts&
         g.e[q] = __ldg(&S->eps[q]);
         g.th[q] = __double2float_ru(T + 0x1p-12);
         g.tl[q] = __double2float_rd(T - 0x1p-12);
+        g.flo[q] = __ldg(&S->fd_bounds[2 * q]);
+        g.fhi[q] = __ldg(&S->fd_bounds[2 * q + 1]);
     }
 }
 
@@ -647,7 +650,21 @@ __device__ __forceinline__ bool candidate_pass(const Smem& sm, const SearchConst
             const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + m);
             float vp[3], vm[3];
             fast_linear<false>(CC.fx0, CC.fz0, CC.mx, CC.mz, CC.cy, r, sc, vp, vm);
+            // a channel whose clamped linear difference is outside its
+            // linear-space bounds surely fails: skip the signal bounds when
+            // every lane has one
+            bool lf = false;
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                const float d = fabsf(__fsub_rn(__saturatef(vp[q]), __saturatef(vm[q])));
+                lf |= (d <= SG.flo[q]) | (d >= SG.fhi[q]);
+            }
+            if (__all_sync(kFull, lf) && kPath == kPathFast) return false;
             pass = signal_prefilter(SG, vp, vm, CC.tab, C.flags, unsure);
+            if (lf) {
+                pass = false;
+                unsure = false;
+            }
         }
         if (kPath != kPathFast || (__any_sync(kFull, unsure) && unsure)) {
             double lp[3], lm[3];
@@ -863,12 +880,24 @@ __device__ __forceinline__ void band_row(const SearchConst* S, const Consts& C, 
 struct FrameConsts {
     int k1, q0;
     int wc[3];
+    float lo[3], hi[3];  // SearchConst::fd_bounds: linear-space sure-fail bounds per channel
 };
 
-__device__ __forceinline__ void frame_chunk(const CodeConsts& CC, const FrameConsts& F, uint32_t flags, float r,
-                                            float2 sc, bool& att, bool& sure) {
-    float vp[3], vm[3];
-    fast_linear<false, true>(CC.fx0, CC.fz0, CC.mx, CC.mz, CC.cy, r, sc, vp, vm);
+// Linear-space prefilter: true if some channel surely fails (|v_p - v_m| of
+// the saturated FP32 values at or below its loud bound, or at or above its
+// quiet bound; make_search_const), so the candidate needs no codes.
+__device__ __forceinline__ bool frame_surely_fails(const FrameConsts& F, const float* vp, const float* vm) {
+    bool fail = false;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const float d = fabsf(__fsub_rn(vp[q], vm[q]));
+        fail |= (d <= F.lo[q]) | (d >= F.hi[q]);
+    }
+    return fail;
+}
+
+__device__ __forceinline__ void frame_chunk(const CodeConsts& CC, const FrameConsts& F, uint32_t flags,
+                                            const float* vp, const float* vm, bool& att, bool& sure) {
     bool fail = false, all = true;
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
@@ -908,7 +937,9 @@ __device__ __forceinline__ void frame_settle(const Smem& sm, const SearchConst* 
 }
 
 // `nch` full chunks of radius row k from angle m0 (na % 32 == 0), two chunks
-// per vote.
+// per vote.  The six saturated values of both chunks go through the
+// linear-space prefilter first; the code lookups run only when some lane of
+// the pair of chunks may pass.
 template <int kOut>
 __device__ __forceinline__ void frame_row(const Smem& sm, const SearchConst* S, const CodeConsts& CC,
                                           const FrameConsts& F, uint32_t flags, const LaunchArgs& A, uint32_t k,
@@ -923,13 +954,20 @@ __device__ __forceinline__ void frame_row(const Smem& sm, const SearchConst* S, 
 #pragma unroll 1
     for (; ix != iend; ix += 32 * G) {
         float2 sv[G];
-        bool at[G], su[G];
 #pragma unroll
         for (uint32_t g = 0; g < G; ++g) sv[g] = __ldg(trig + ix + 32 * g);
-        bool any = false;
+        float vp[G][3], vm[G][3];
+        bool maybe = false;
 #pragma unroll
         for (uint32_t g = 0; g < G; ++g) {
-            frame_chunk(CC, F, flags, r, sv[g], at[g], su[g]);
+            fast_linear<false, true>(CC.fx0, CC.fz0, CC.mx, CC.mz, CC.cy, r, sv[g], vp[g], vm[g]);
+            maybe |= !frame_surely_fails(F, vp[g], vm[g]);
+        }
+        if (!__any_sync(kFull, maybe)) continue;
+        bool at[G], su[G], any = false;
+#pragma unroll
+        for (uint32_t g = 0; g < G; ++g) {
+            frame_chunk(CC, F, flags, vp[g], vm[g], at[g], su[g]);
             any |= at[g];
         }
         if (__any_sync(kFull, any)) {
@@ -941,8 +979,10 @@ __device__ __forceinline__ void frame_row(const Smem& sm, const SearchConst* S, 
         }
     }
     if (nch % G) {
+        float vp[3], vm[3];
+        fast_linear<false, true>(CC.fx0, CC.fz0, CC.mx, CC.mz, CC.cy, r, __ldg(trig + ix), vp, vm);
         bool at, su;
-        frame_chunk(CC, F, flags, r, __ldg(trig + ix), at, su);
+        frame_chunk(CC, F, flags, vp, vm, at, su);
         if (__any_sync(kFull, at))
             frame_settle<kOut>(sm, S, A, flags, k, ix, at, su, off + lane + (ix - mb), list, cnt, first, ct, lane_lt);
     }
@@ -957,7 +997,11 @@ __device__ __forceinline__ void frame_tile(const Smem& sm, const SearchConst* S,
     F.k1 = __ldg(&S->k1);
     F.q0 = __ldg(&S->q0);
 #pragma unroll
-    for (int q = 0; q < 3; ++q) F.wc[q] = CC.ec[q] == INFINITY ? 256 : 1;
+    for (int q = 0; q < 3; ++q) {
+        F.wc[q] = CC.ec[q] == INFINITY ? 256 : 1;
+        F.lo[q] = __ldg(&S->fd_bounds[2 * q]);
+        F.hi[q] = __ldg(&S->fd_bounds[2 * q + 1]);
+    }
     uint32_t k = div_na(i0, A);
     uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
     uint32_t i = i0;

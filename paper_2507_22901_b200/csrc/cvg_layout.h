@@ -33,7 +33,11 @@ struct alignas(16) SearchConst {
     float mxs[3];      // band form, channels permuted loud-first: mx / h_c   (h_c: band half-width)
     float mzs[3];      //            mz / h_c
     float cys[3];      //            (cy - centre_c) / h_c
-    float cube[6];     // cube-only rows, sum/difference form: {fx0^3, 3 fx0^2, 3 fx0, fz0^3, 3 fz0^2, 3 fz0}
+    union {
+        float cube[6];       // cube-only rows, sum/difference form: {fx0^3, 3 fx0^2, 3 fx0, fz0^3, 3 fz0^2, 3 fz0}
+        float fd_bounds[6];  // Quantized x FrameDiff: per channel {lo, hi}; the channel surely fails if the
+                             // saturated FP32 |v_p - v_m| <= lo or >= hi (make_search_const)
+    };
     float qa, qp, lp;  // attention: max quiet M' <= qa; certain pass: max quiet M' < qp and min loud M' > lp
     float eps[3];      // proven bound |lin32 - lin64| per channel (linear units)
     float eps_code[3]; // eps + float rounding of the code thresholds

@@ -264,6 +264,43 @@ SignalBand signal_band_cached(int target, double T) {
     return b;
 }
 
+// Continuous x FrameDiff linear-space bounds for a channel threshold T on
+// d = |s(x_p) - s(x_m)| (search.cpp:161-173).  s = signal_value is increasing
+// and concave on [0, 1] with s(0) = 0 and s(1) = 255, so for dx = |x_p - x_m|
+//   d <= s(dx)               (subadditivity): dx <= a, s(a) <= T - 1e-6,
+//                            gives d < T, and a loud channel fails;
+//   d >= 255 - s(1 - dx)     (the flattest end): dx >= 1 - b with
+//                            s(b) <= 255 - T - 1e-6 gives d > T, and a quiet
+//                            channel fails.
+// Returns {a, 1 - b} (largest such a, b by bisection over the reference's own
+// signal_value, glibc pow); a = -1: no loud region, a = 2: a loud channel
+// never passes; 1 - b = 2: a quiet channel never fails.  Memoized per T.
+std::pair<double, double> frame_signal_bounds(double T) {
+    static std::mutex mu;
+    static std::map<double, std::pair<double, double>> cache;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        const auto it = cache.find(T);
+        if (it != cache.end()) return it->second;
+    }
+    auto largest_below = [](double v) {  // largest x in [0, 1] with s(x) <= v (v in [0, 255))
+        double lo = 0.0, hi = 1.0;
+        for (int i = 0; i < 80; ++i) {
+            const double mid = 0.5 * (lo + hi);
+            (signal_value(mid) <= v ? lo : hi) = mid;
+        }
+        return lo;
+    };
+    const double la = T - 1e-6, lq = 255.0 - T - 1e-6;
+    const double a = la <= 0.0 ? -1.0 : (la >= 255.0 ? 2.0 : largest_below(la));
+    const double q = lq < 0.0 ? 2.0 : 1.0 - largest_below(lq);
+    const std::pair<double, double> r{a, q};
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() >= 4096) cache.clear();
+    cache.emplace(T, r);
+    return r;
+}
+
 struct BoundTerms {
     double err;  // |g32 - f^-1(f)| bound
     double gmax; // max |f^-1(f)|
@@ -461,6 +498,39 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
     S.lp = round_up_f(1.0 + eps_l);
     S.qa = round_up_f(1.0 + eps_q);
     S.qp = round_down_f(1.0 - eps_q);
+    if (mode == cvg::kModeSignal) {
+        // Continuous x FrameDiff: the same prefilter on the signal's
+        // linear-space bounds (frame_signal_bounds), before the signal table
+        for (int c = 0; c < 3; ++c) {
+            const double m = 2.0 * S.eps[c] + std::ldexp(1.0, -22) + 1e-9;
+            const auto [a, q] = frame_signal_bounds(S.lo[c]);
+            if (bits[c]) {
+                S.fd_bounds[2 * c] = a > 1.5 ? INFINITY : (a < 0.0 ? -1.0f : round_down_f(a - m));
+                S.fd_bounds[2 * c + 1] = INFINITY;
+            } else {
+                S.fd_bounds[2 * c] = -1.0f;
+                S.fd_bounds[2 * c + 1] = q > 1.5 ? INFINITY : round_up_f(q + m);
+            }
+        }
+    }
+    if (mode == cvg::kModeCodes) {
+        // FrameDiff prefilter bounds (frame_row): |sat(v32) - sat(v64)| <= eps
+        // per endpoint and the FP32 difference rounds by <= 2^-24, so a
+        // channel whose |d32| is at most fd_loud - 2 eps - 2^-22 (loud) or at
+        // least fd_quiet + 2 eps + 2^-22 (quiet) surely fails.
+        for (int c = 0; c < 3; ++c) {
+            const double m = 2.0 * S.eps[c] + std::ldexp(1.0, -22);
+            if (bits[c]) {
+                const double lo = T.fd_loud[k1];
+                S.fd_bounds[2 * c] = std::isinf(lo) ? INFINITY : round_down_f(lo - m);
+                S.fd_bounds[2 * c + 1] = INFINITY;
+            } else {
+                const double hi = T.fd_quiet[q0];
+                S.fd_bounds[2 * c] = -1.0f;
+                S.fd_bounds[2 * c + 1] = std::isinf(hi) ? INFINITY : round_up_f(hi + m);
+            }
+        }
+    }
 }
 
 }  // namespace cvg::host

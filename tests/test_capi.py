@@ -329,3 +329,69 @@ def test_signal_table_bounds(lib):
     assert np.all(L[b][inside] <= s[inside]) and np.all(s[inside] <= U[b][inside])
     assert np.all(np.diff(L) >= 0) and np.all(np.diff(U) >= 0) and L[0] <= 0.0 and U[-1] >= 255.0
     assert (U - L).max() < 1.0 and np.median(U - L) < 0.05
+
+
+def test_frame_diff_linear_bounds(lib):
+    """The Quantized x FrameDiff linear-space prefilter (cvg_host.h
+    Tables::fd_loud / fd_quiet, cvg_kernels.cu frame_surely_fails): with
+    D_loud(k1) = min_c thr[c+k1-1] - thr[c] and D_quiet(q0) = max_c
+    thr[min(c+q0+1, 256)] - thr[c] (thr[256] = 1), clamped values with
+    |x_p - x_m| <= D_loud(k1) never have |code_p - code_m| >= k1, and values with
+    |x_p - x_m| > D_quiet(q0) never have |code_p - code_m| <= q0 (frame_deltas,
+    search.cpp:138-144, on QuantTable codes)."""
+    thr = np.zeros(256, np.float64)
+    lib.cvg_quant_thresholds(thr.ctypes.data_as(C.POINTER(C.c_double)))
+    ext = np.concatenate([thr, [1.0]])
+    rng = np.random.default_rng(23)
+    xp = np.clip(rng.uniform(-0.05, 1.05, 400_000), 0, 1)
+    # differences concentrated near the bounds as well as spread out
+    xm = np.clip(xp + rng.normal(0, 0.2, xp.size) * rng.choice([1e-3, 1e-2, 1e-1, 1.0], xp.size), 0, 1)
+    d = np.abs(xp - xm)
+    code = lambda x: _code64(x, thr)  # noqa: E731
+    dc = np.abs(code(xp) - code(xm))
+    for k1 in (1, 2, 11, 51, 101, 151, 201, 255):
+        dl = min(thr[c + k1 - 1] - thr[c] for c in range(1, 257 - k1))
+        assert not np.any((d <= dl) & (dc >= k1)), k1
+    for q0 in (0, 1, 6, 12, 25, 50, 100, 200, 254):
+        dq = max(ext[min(c + q0 + 1, 256)] - thr[c] for c in range(256))
+        assert not np.any((d > dq) & (dc <= q0)), q0
+
+
+def test_continuous_frame_diff_linear_bounds():
+    """The Continuous x FrameDiff linear-space prefilter (cvg_prep.cpp
+    frame_signal_bounds): signal_value s is increasing and concave on [0, 1],
+    so |x_p - x_m| <= a with s(a) <= T - 1e-6 gives |s_p - s_m| < T, and
+    |x_p - x_m| >= 1 - b with s(b) <= 255 - T - 1e-6 gives |s_p - s_m| > T
+    (convert_kernel.hpp:109-112, search.cpp:161-173).  Checked on clamped
+    random pairs, concentrated near each bound."""
+    def s(x):
+        x = np.clip(x, 0.0, 1.0)
+        return 255.0 * np.where(x <= 0.0031308, 12.92 * x, 1.055 * np.power(x, 1.0 / 2.4) - 0.055)
+
+    def largest_below(v):
+        lo, hi = 0.0, 1.0
+        for _ in range(80):
+            mid = 0.5 * (lo + hi)
+            if s(mid) <= v:
+                lo = mid
+            else:
+                hi = mid
+        return lo
+
+    rng = np.random.default_rng(29)
+    for T in (3.0, 6.25, 12.5, 25.0, 50.0, 100.0, 150.0, 200.0, 250.0):
+        a = largest_below(T - 1e-6)
+        q = 1.0 - largest_below(255.0 - T - 1e-6)
+        x = rng.uniform(0, 1, 300_000)
+        for dx, want in ((a, "below"), (q, "above")):
+            d = dx * (1 + rng.choice([-1e-3, -1e-9, 0.0], x.size)) if want == "below" else \
+                dx * (1 + rng.choice([1e-3, 1e-9, 0.0], x.size))
+            y = np.clip(x + d * rng.choice([-1, 1], x.size), 0, 1)
+            real = np.abs(np.clip(x, 0, 1) - y)
+            ds = np.abs(s(x) - s(y))
+            if want == "below":
+                sel = real <= a
+                assert np.all(ds[sel] < T), T
+            else:
+                sel = real >= q
+                assert np.all(ds[sel] > T), T
