@@ -67,13 +67,15 @@ T* at(void* base, size_t off) {
 
 // sc_index[s] -> record of search s; uniq[u] -> first search with record u.
 // sc_index stays empty when every search is distinct (identity mapping).
-void dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, std::vector<int32_t>& uniq) {
+// Returns true if every search has the same (pattern, v_th, r_novib).
+bool dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, std::vector<int32_t>& uniq) {
     const int n = d->n_searches;
     sc_index.clear();
     uniq.clear();
-    if (n <= 0) return;
-    // uniform classifier? (chunked so the 8M-search screen runs on all cores)
-    const size_t parts = n >= (1 << 20) ? 64 : 1;
+    if (n <= 0) return true;
+    // uniform classifier? (chunked so a per-pixel screen runs on all cores;
+    // 16K searches per chunk at least)
+    const size_t parts = std::min<size_t>(64, std::max<size_t>(1, static_cast<size_t>(n) >> 14));
     std::vector<char> same(parts, 1);
     parallel_for(
         parts,
@@ -103,7 +105,7 @@ void dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, s
         // record is its first search (atomic min), so the result is
         // independent of the thread count.
         std::vector<uint64_t> bits(1u << 18, 0);
-        const size_t chunks = n >= (1 << 20) ? 64 : 1;
+        const size_t chunks = parts;
         parallel_for(
             chunks,
             [&](size_t c) {
@@ -175,6 +177,7 @@ void dedup_searches(const cvg_search_desc* d, std::vector<uint32_t>& sc_index, s
     if (static_cast<int>(uniq.size()) == n) {
         sc_index.clear();  // all distinct: records are in search order
     }
+    return uniform;
 }
 
 GridTables make_grid_tables(const cvg_search_desc* d) {
@@ -238,8 +241,9 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     std::vector<uint32_t> sc_index;
     std::vector<int32_t> uniq;  // representative search of each record
     size_t n_sc = static_cast<size_t>(p->n);
+    bool uniform = false;  // one classifier for the whole batch (one loud count: no claim groups)
     if (!pre) {
-        dedup_searches(d, sc_index, uniq);
+        uniform = dedup_searches(d, sc_index, uniq);
         n_sc = uniq.size();
     }
     mark("dedup");
@@ -263,7 +267,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         const char* e = std::getenv("CVG_CLAIM_GROUP");  // A/B switch; default on
         return !e || std::atoi(e) != 0;
     }();
-    if (group_claims && p->mode == cvg::kModeBand && p->n > 1) {
+    if (group_claims && p->mode == cvg::kModeBand && p->n > 1 && !uniform) {
         std::array<uint32_t, 4> bucket{};
         for (int32_t i = 0; i < p->n; ++i) ++bucket[__builtin_popcount(d->pattern_bits[i] & 7)];
         int kinds = 0;
