@@ -277,9 +277,13 @@ private:
             // A search runs several short parallel sections back to back:
             // poll for the next batch for a while before sleeping on the
             // condition variable (a futex wake-up costs tens of microseconds).
+            static const int spin_us = [] {
+                const char* e = std::getenv("CVG_POOL_SPIN_US");
+                return e ? std::atoi(e) : 200;
+            }();
             const auto t0 = std::chrono::steady_clock::now();
             while (published_.load(std::memory_order_acquire) == seen &&
-                   std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(200)) {
+                   std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(spin_us)) {
                 __builtin_ia32_pause();
             }
             Batch b;
@@ -484,6 +488,7 @@ GridTables make_grid_tables(const cvg_search_desc* d);
 int ensure_device(cvg_ctx* ctx);
 void plan_free_outputs(cvg_plan* p);
 int plan_reserve(cvg_plan* p, uint64_t cap);
+void plan_set_density(cvg_plan* p, uint64_t expected_pairs);
 int plan_build_safe(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTables* grid = nullptr,
                     const SearchConst* pre = nullptr);
 void plan_release(cvg_plan* p);

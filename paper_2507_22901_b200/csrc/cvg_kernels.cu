@@ -1139,7 +1139,7 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
             if (kOut == kOutPairs) {
                 A.tile_count[t] = cnt;
                 // emit work items: (tile, 256-pair sub-range), any order
-                const uint32_t subs = (cnt + kEmitSpan - 1) / kEmitSpan;
+                const uint32_t subs = (cnt + (1u << A.emit_shift) - 1) >> A.emit_shift;
                 if (subs) {
                     const uint32_t w = atomicAdd(&A.ticket[3], subs);
                     for (uint32_t j = 0; j < subs; ++j) A.worklist[w + j] = (t << 4) | j;
@@ -1263,8 +1263,8 @@ __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
         if (lane == 0) q_claim = atomicAdd(&A.ticket[2], 1u);
         const uint32_t item = A.worklist[q];
         const uint32_t t = item >> 4;
-        const uint32_t p0 = (item & 15u) * kEmitSpan;
-        const uint32_t cnt = min(A.tile_count[t] - p0, static_cast<uint32_t>(kEmitSpan));
+        const uint32_t p0 = (item & 15u) << A.emit_shift;
+        const uint32_t cnt = min(A.tile_count[t] - p0, 1u << A.emit_shift);
         const unsigned long long base = base0 + A.tile_base[t] + p0;
         const uint16_t* list = A.scratch + static_cast<size_t>(t) * kTile + p0;
         if (base + cnt > A.capacity) {

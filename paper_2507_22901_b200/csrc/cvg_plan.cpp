@@ -31,6 +31,15 @@ void plan_free_outputs(cvg_plan* p) {
     p->capacity = 0;
 }
 
+// Emit item size from the expected pair count: batches averaging >= 256
+// pairs per tile (cfg2: ~750) take 512-pair items, half the item set-ups
+// (cfg2 emit 3.32 -> 3.04 ms); sparse batches keep 256 so that the last
+// items stay short (cfg1: 512 everywhere measured 0.051 -> 0.054 ms).
+void plan_set_density(cvg_plan* p, uint64_t expected_pairs) {
+    const uint64_t tiles = p->args.n_tiles ? p->args.n_tiles : 1;
+    p->args.emit_shift = expected_pairs >= 256 * tiles ? 9u : 8u;
+}
+
 int plan_reserve(cvg_plan* p, uint64_t cap) {
     if (p->out != cvg::kOutPairs || p->empty) return CVG_OK;
     if (cap == 0) cap = 1;
@@ -361,6 +370,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.tiles_per_search = tps;
     A.cand_per_search = static_cast<uint32_t>(cps);
     A.na_magic = p->na > 1 ? (UINT64_MAX / static_cast<uint64_t>(p->na)) + 1 : 0;
+    A.emit_shift = 8;  // kEmitSpan until an expected pair count says otherwise (plan_set_density)
     A.n_tiles = n_tiles;
 
     // ---- per-run workspace --------------------------------------------------
@@ -698,6 +708,7 @@ int cvg_plan_reserve(cvg_plan* p, uint64_t cap) {
     if (!p) return fail(CVG_EINVAL, "null plan");
     std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
     if (int e = ensure_device(p->ctx)) return e;
+    plan_set_density(p, cap);  // the caller's expected pair count
     return plan_reserve(p, cap);
 }
 

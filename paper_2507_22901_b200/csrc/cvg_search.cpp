@@ -285,6 +285,7 @@ int search_pipelined(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, int 
         const uint64_t fit = static_cast<uint64_t>(ctx->total_mem / 4 / 10);
         const uint64_t cap = hinted ? ctx->hint_pairs + ctx->hint_pairs / 4 + (1u << 16)
                                     : std::min<uint64_t>(p.candidates, std::max<uint64_t>(fit, 1u << 20));
+        if (hinted) plan_set_density(&p, ctx->hint_pairs);
         if (int e = plan_reserve(&p, cap)) return e;
     }
 
