@@ -351,6 +351,37 @@ def run_ours(args):
 
     # per-launch kernel time over the timed steps: events inside the plan
     # cover only the search kernel; re-measure a few steps for the roofline
+    # ---- CVG_PATH_PRUNED, reported apart (not the headline): whole radius
+    # rows decided by a certified FP64 bound, so its candidates/s counts
+    # candidates decided, not each one evaluated ----
+    pruned = None
+    if wl.output in ("pairs", "counts", "first") and rank == 0 and world == 1:
+        pp = ctx.plan(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, output=wl.output,
+                      path="pruned")
+        pp.run(stream.cuda_stream)
+        got_p = pp.sync()
+        if wl.output == "pairs":
+            pp.reserve(max(got_p, 1))
+        for _ in range(args.warmup):
+            flush.zero_()
+            pp.run(stream.cuda_stream)
+        torch.cuda.synchronize()
+        p_ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            pp.run(stream.cuda_stream)
+            b.record(stream)
+            torch.cuda.synchronize()
+            p_ms.append(a.elapsed_time(b))
+        assert pp.sync() == got_p and (wl.output != "pairs" or got_p == n_pairs)
+        pruned = {"value": round(wl.candidates * args.steps / (sum(p_ms) * 1e-3) / 1e9, 4), "unit": UNIT,
+                  "ms_per_step": round(sum(p_ms) / args.steps, 4), "path": "pruned (CVG_PATH_PRUNED)",
+                  "note": "same results; radius rows proven empty by a certified FP64 bound are decided "
+                          "without per-candidate evaluation, so this counts candidates decided per second"}
+        del pp
+
     kern, phases = [], []
     plan.set_phase_marks(True)  # events between the kernels (off in the timed steps: they block the PDL overlap)
     for _ in range(min(args.steps, 20)):
@@ -441,6 +472,7 @@ def run_ours(args):
                 "api": "cvg_search (C-ABI host call)", "breakdown_ms": phase_med},
         "gpu_launches": plan.launches * args.steps,
         **({"gather": gather} if gather else {}),
+        **({"pruned": pruned} if pruned else {}),
         "clocks": clk.summary(),
         "roofline": roofline,
         "cpu_baseline": cpu,

@@ -59,6 +59,9 @@ extern "C" {
 #define CVG_PATH_FAST 0  /* FP32 with a proven error bound + FP64 repair of near-boundary values */
 #define CVG_PATH_EXACT 1 /* FP64 op-for-op restatement for every candidate (serial_search) */
 #define CVG_PATH_AUDIT 2 /* both; counts bound violations (tests) */
+#define CVG_PATH_PRUNED 3 /* FAST, plus whole radius rows decided by a certified FP64 bound
+                             (TargetSwing, aligned grids): same results; candidates of a
+                             pruned row are decided without being evaluated one by one */
 
 typedef struct cvg_ctx cvg_ctx;
 typedef struct cvg_plan cvg_plan;

@@ -46,6 +46,7 @@ int path_mode(const std::string& s) {
     if (s == "fast") return CVG_PATH_FAST;
     if (s == "exact") return CVG_PATH_EXACT;
     if (s == "audit") return CVG_PATH_AUDIT;
+    if (s == "pruned") return CVG_PATH_PRUNED;
     throw std::invalid_argument("path must be 'fast', 'exact' or 'audit'");
 }
 

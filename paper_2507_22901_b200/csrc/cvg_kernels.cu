@@ -1015,6 +1015,37 @@ __device__ __forceinline__ void frame_tile(const Smem& sm, const SearchConst* S,
     }
 }
 
+// CVG_PATH_PRUNED: true if every candidate of radius row k surely fails,
+// proven in FP64 from the reference's own operation sequence
+// (search.cpp:243-262): with |sin|, |cos| <= 1, fx of every candidate lies in
+// [fy + (ta - r)/500, fy + (ta + r)/500] and fz in [fy - (tb + r)/200,
+// fy - (tb - r)/200] (each rounded operation is monotone), X = wx f^-1(fx) and
+// Z = wz f^-1(fz) are monotone, and lin_c = (Minv[c][0] X + cy_c) +
+// Minv[c][2] Z takes its extremes at the corners.  A loud channel whose whole
+// range lies inside its band [lo, hi) (1e-12 of slack for the f^-1 branch
+// switch) never passes (exact_band), so neither does any candidate.
+__device__ __noinline__ bool row_surely_fails(const SearchConst* S, const LaunchArgs& A, uint32_t k) {
+    const double r = __ldg(&A.radii_d[k]);
+    const double fy = __ldg(&S->fy), ta = __ldg(&S->ta), tb = __ldg(&S->tb);
+    const double wx = __ldg(&S->wx), wz = __ldg(&S->wz);
+    const double x0 = __dmul_rn(wx, finv_exact(__dadd_rn(fy, __dmul_rn(__dsub_rn(ta, r), kInv500))));
+    const double x1 = __dmul_rn(wx, finv_exact(__dadd_rn(fy, __dmul_rn(__dadd_rn(ta, r), kInv500))));
+    const double z0 = __dmul_rn(wz, finv_exact(__dsub_rn(fy, __dmul_rn(__dadd_rn(tb, r), kInv200))));
+    const double z1 = __dmul_rn(wz, finv_exact(__dsub_rn(fy, __dmul_rn(__dsub_rn(tb, r), kInv200))));
+    const uint32_t flags = __ldg(&S->flags);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        if (!((flags >> q) & 1u)) continue;
+        const double a0 = __dmul_rn(A.minv[3 * q], x0), a1 = __dmul_rn(A.minv[3 * q], x1);
+        const double b0 = __dmul_rn(A.minv[3 * q + 2], z0), b1 = __dmul_rn(A.minv[3 * q + 2], z1);
+        const double cy = __ldg(&S->cy64[q]);
+        const double vmin = __dadd_rn(__dadd_rn(fmin(a0, a1), cy), fmin(b0, b1));
+        const double vmax = __dadd_rn(__dadd_rn(fmax(a0, a1), cy), fmax(b0, b1));
+        if (vmin - 1e-12 >= __ldg(&S->lo[q]) && vmax + 1e-12 < __ldg(&S->hi[q])) return true;
+    }
+    return false;
+}
+
 template <int kL, int kOut>
 __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t i0,
                                           uint32_t i1, uint16_t* list, uint32_t& cnt, uint32_t* first, Counters& ct,
@@ -1025,7 +1056,9 @@ __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C,
     while (i < i1) {
         const uint32_t seg = min(i1 - i, static_cast<uint32_t>(A.na) - m0);
         const float r = __ldg(&A.radii_f[k]);
-        if (r < C.rcube) {
+        if (A.prune && row_surely_fails(S, A, k)) {
+            // no candidate of this row passes: nothing to append
+        } else if (r < C.rcube) {
             band_row<kL, true, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);
         } else {
             band_row<kL, false, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);

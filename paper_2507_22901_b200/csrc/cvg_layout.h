@@ -116,6 +116,7 @@ struct LaunchArgs {
     uint16_t* scratch;             // [n_tiles * kTile] per-tile passing offsets (PAIRS)
     uint32_t* worklist;            // [n_tiles * kTile / kEmitSpan] emit items tile << 4 | sub, any order
     uint32_t emit_shift;           // log2 of the pairs per emit item: 8 (kEmitSpan), 9 for dense batches
+    uint32_t prune;                // CVG_PATH_PRUNED: skip radius rows that row_surely_fails proves empty
     unsigned long long* total;     // [1] sum of tile_count (PAIRS)
     uint32_t* out_idx;           // [capacity]
     uint8_t* out_codes;          // [capacity * 6]

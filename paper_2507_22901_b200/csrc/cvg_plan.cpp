@@ -229,7 +229,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     p->ctx = ctx;
     p->mode = search_mode(d);
     p->out = d->output;
-    p->path = d->path;
+    p->path = d->path == CVG_PATH_PRUNED ? CVG_PATH_FAST : d->path;  // pruning is a flag of the FAST path
     p->n = d->n_searches;
     p->nr = d->n_radii;
     p->na = d->n_angles;
@@ -371,6 +371,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.cand_per_search = static_cast<uint32_t>(cps);
     A.na_magic = p->na > 1 ? (UINT64_MAX / static_cast<uint64_t>(p->na)) + 1 : 0;
     A.emit_shift = 8;  // kEmitSpan until an expected pair count says otherwise (plan_set_density)
+    A.prune = d->path == CVG_PATH_PRUNED ? 1u : 0u;
     A.n_tiles = n_tiles;
 
     // ---- per-run workspace --------------------------------------------------

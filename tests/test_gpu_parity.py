@@ -54,7 +54,7 @@ def assert_clean(res, path):
         assert st["audit_max_ratio"] < 1.0, st
 
 
-@pytest.mark.parametrize("path", ["fast", "exact", "audit"])
+@pytest.mark.parametrize("path", ["fast", "exact", "audit", "pruned"])
 def test_cfg0_bit_exact(ctx, oracle, path):
     wl = W.cfg0()
     res = run(ctx, wl, path=path)
@@ -85,7 +85,7 @@ def test_reference_small_grid_cases(ctx, path, basis):
     assert_clean(res, path)
 
 
-@pytest.mark.parametrize("path", ["fast", "audit"])
+@pytest.mark.parametrize("path", ["fast", "audit", "pruned"])
 def test_cfg1_full_sweep(ctx, path):
     wl = W.cfg1()
     res = run(ctx, wl, path=path)
@@ -102,19 +102,21 @@ def test_cfg1_counts_mode_matches_pairs(ctx):
     assert res["counts"].tolist() == golden("workloads.json")["cfg1"]["counts"]
 
 
-def test_cfg3_dense_targets(ctx):
+@pytest.mark.parametrize("path", ["fast", "pruned"])
+def test_cfg3_dense_targets(ctx, path):
     wl = W.cfg3()
-    res = run(ctx, wl)
+    res = run(ctx, wl, path=path)
     g = golden("workloads.json")["cfg3"]
     assert res["counts"].tolist() == g["counts"]
     assert sha_by_search(res) == g["sha256"]
     assert_clean(res, "fast")
 
 
-def test_cfg4_first_pair_mode_crop(ctx):
+@pytest.mark.parametrize("path", ["fast", "pruned"])
+def test_cfg4_first_pair_mode_crop(ctx, path):
     g = golden("workloads.json")["cfg4_256x144"]
     wl = W.cfg4(g["width"], g["height"])
-    res = run(ctx, wl, output="first")
+    res = run(ctx, wl, output="first", path=path)
     import hashlib
 
     m = hashlib.sha256()
@@ -425,7 +427,7 @@ EDGE_TARGETS = [[0, 0, 0], [255, 255, 255], [8, 8, 8], [255, 0, 0], [0, 255, 255
 
 
 @pytest.mark.parametrize("gname", sorted(EDGE_GRIDS))
-@pytest.mark.parametrize("path", ["fast", "audit"])
+@pytest.mark.parametrize("path", ["fast", "audit", "pruned"])
 def test_edge_grids_vs_oracle(ctx, oracle, gname, path):
     radii, angles = EDGE_GRIDS[gname]
     t, p, v, r = [], [], [], []

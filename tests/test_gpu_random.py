@@ -74,3 +74,16 @@ def test_dark_targets_linear_branch(ctx, oracle):
             oi, oc, _ = oracle.search(targets[s], pat, 5.0, 0.5, radii, angles, method=1, want_deltas=False)
             assert np.array_equal(res["idx"][a:b], oi) and np.array_equal(res["codes"][a:b], oc)
     del rng
+
+
+@pytest.mark.parametrize("s", range(6))
+@pytest.mark.parametrize("basis", [0, 1])
+def test_random_aligned_grids_pruned(ctx, oracle, s, basis):
+    """CVG_PATH_PRUNED on aligned grids (the band hot loop with row pruning;
+    FrameDiff batches ignore the flag): every record equals the oracle's,
+    dark and bright targets, radii from tiny to beyond the gamut."""
+    rng = np.random.default_rng(1000 + s)
+    nr = int(rng.integers(1, 48))
+    na = int(rng.choice([32, 64, 96, 256, 512]))
+    rmax = float(rng.choice([0.5, 5.0, 40.0, 130.0, 300.0]))
+    check_batch(ctx, oracle, rng, nr, na, rmax, n=16, basis=basis, path="pruned")
