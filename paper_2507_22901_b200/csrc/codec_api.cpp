@@ -188,7 +188,7 @@ FramePair embed_blocks(const Image& base, const BlockLayout& layout, const Thres
     std::vector<int32_t> xy(2 * n);
     const bool empty_grid = grid.radii.empty() || grid.angles.empty();
     ResultGuard g;
-    if (!specs.empty() && !empty_grid) run(specs, grid, opts, CVG_OUT_PAIRS, CVG_PATH_FAST, g);
+    if (!specs.empty() && !empty_grid) run(specs, grid, opts, CVG_OUT_PAIRS, CVG_PATH_PRUNED, g);
     for (size_t i = 0; i < first_bad; ++i) {
         const BlockSpec& b = layout.blocks[i];
         const uint64_t lo = empty_grid ? 0 : g.r.offsets[i], hi = empty_grid ? 0 : g.r.offsets[i + 1];

@@ -315,7 +315,7 @@ std::vector<ColorPair> serial_search(const SrgbColor& target, const VibrationGri
 
 std::vector<ColorPair> batch_search(const SrgbColor& target, const VibrationGrid& grid, const BitPattern& pattern,
                                     const Thresholds& th, const SearchOptions& opts) {
-    return search_one(target, grid, pattern, th, opts, CVG_PATH_FAST);
+    return search_one(target, grid, pattern, th, opts, CVG_PATH_PRUNED);  // FAST + certified row pruning: same pairs
 }
 
 double classification_margin(const ColorPair& pair, const Thresholds& th) {
@@ -348,7 +348,7 @@ std::vector<std::vector<ColorPair>> batch_search_many(const std::vector<SearchSp
     std::vector<std::vector<ColorPair>> out(specs.size());
     if (specs.empty() || grid.radii.empty() || grid.angles.empty()) return out;
     ResultGuard g;
-    run(specs, grid, opts, CVG_OUT_PAIRS, CVG_PATH_FAST, g);
+    run(specs, grid, opts, CVG_OUT_PAIRS, CVG_PATH_PRUNED, g);
     for (size_t s = 0; s < specs.size(); ++s) out[s] = materialize(g.r, s, specs[s].target, grid, opts);
     return out;
 }
@@ -359,7 +359,7 @@ std::vector<std::uint64_t> batch_count_many(const std::vector<SearchSpec>& specs
     std::vector<std::uint64_t> out(specs.size(), 0);
     if (specs.empty() || grid.radii.empty() || grid.angles.empty()) return out;
     ResultGuard g;
-    run(specs, grid, opts, CVG_OUT_COUNTS, CVG_PATH_FAST, g);
+    run(specs, grid, opts, CVG_OUT_COUNTS, CVG_PATH_PRUNED, g);
     for (size_t s = 0; s < specs.size(); ++s) out[s] = g.r.counts[s];
     return out;
 }
