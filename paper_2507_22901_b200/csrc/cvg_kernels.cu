@@ -1024,7 +1024,7 @@ __device__ __forceinline__ void frame_tile(const Smem& sm, const SearchConst* S,
 // Minv[c][2] Z takes its extremes at the corners.  A loud channel whose whole
 // range lies inside its band [lo, hi) (1e-12 of slack for the f^-1 branch
 // switch) never passes (exact_band), so neither does any candidate.
-__device__ __noinline__ bool row_surely_fails(const SearchConst* S, const LaunchArgs& A, uint32_t k) {
+__device__ __forceinline__ bool row_surely_fails(const SearchConst* S, const LaunchArgs& A, uint32_t k) {
     const double r = __ldg(&A.radii_d[k]);
     const double fy = __ldg(&S->fy), ta = __ldg(&S->ta), tb = __ldg(&S->tb);
     const double wx = __ldg(&S->wx), wz = __ldg(&S->wz);
@@ -1046,17 +1046,30 @@ __device__ __noinline__ bool row_surely_fails(const SearchConst* S, const Launch
     return false;
 }
 
+// Rows k0 .. k0 + n - 1 (n <= 32) that row_surely_fails proves empty, one
+// row per lane, as a bit mask (one warp-wide FP64 pass per tile).
+__device__ __noinline__ uint32_t rows_surely_fail(const SearchConst* S, const LaunchArgs& A, uint32_t k0, uint32_t n) {
+    const uint32_t lane = threadIdx.x & 31;
+    return __ballot_sync(kFull, lane < n && row_surely_fails(S, A, k0 + lane));
+}
+
 template <int kL, int kOut>
 __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t i0,
                                           uint32_t i1, uint16_t* list, uint32_t& cnt, uint32_t* first, Counters& ct,
                                           unsigned lane, unsigned lane_lt) {
     uint32_t k = div_na(i0, A);
     uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
+    // CVG_PATH_PRUNED: the tile's first 32 rows tested at once
+    uint32_t skip = 0;
+    if (A.prune) {
+        const uint32_t rows = (m0 + (i1 - i0) + static_cast<uint32_t>(A.na) - 1) / static_cast<uint32_t>(A.na);
+        skip = rows_surely_fail(S, A, k, min(rows, 32u));
+    }
     uint32_t i = i0;
     while (i < i1) {
         const uint32_t seg = min(i1 - i, static_cast<uint32_t>(A.na) - m0);
         const float r = __ldg(&A.radii_f[k]);
-        if (A.prune && row_surely_fails(S, A, k)) {
+        if (skip & 1u) {
             // no candidate of this row passes: nothing to append
         } else if (r < C.rcube) {
             band_row<kL, true, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);
@@ -1066,6 +1079,7 @@ __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C,
         i += seg;
         m0 = 0;
         ++k;
+        skip >>= 1;
     }
 }
 
