@@ -1053,7 +1053,7 @@ __device__ __noinline__ uint32_t rows_surely_fail(const SearchConst* S, const La
     return __ballot_sync(kFull, lane < n && row_surely_fails(S, A, k0 + lane));
 }
 
-template <int kL, int kOut>
+template <int kL, int kOut, bool kPrune>
 __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t i0,
                                           uint32_t i1, uint16_t* list, uint32_t& cnt, uint32_t* first, Counters& ct,
                                           unsigned lane, unsigned lane_lt) {
@@ -1061,7 +1061,7 @@ __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C,
     uint32_t m0 = i0 - k * static_cast<uint32_t>(A.na);
     // CVG_PATH_PRUNED: the tile's first 32 rows tested at once
     uint32_t skip = 0;
-    if (A.prune) {
+    if (kPrune) {
         const uint32_t rows = (m0 + (i1 - i0) + static_cast<uint32_t>(A.na) - 1) / static_cast<uint32_t>(A.na);
         skip = rows_surely_fail(S, A, k, min(rows, 32u));
     }
@@ -1069,7 +1069,7 @@ __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C,
     while (i < i1) {
         const uint32_t seg = min(i1 - i, static_cast<uint32_t>(A.na) - m0);
         const float r = __ldg(&A.radii_f[k]);
-        if (skip & 1u) {
+        if (kPrune && (skip & 1u)) {
             // no candidate of this row passes: nothing to append
         } else if (r < C.rcube) {
             band_row<kL, true, kOut>(S, C, A, k, r, m0, seg >> 5, i - i0, list, cnt, first, ct, lane, lane_lt);
@@ -1079,7 +1079,7 @@ __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C,
         i += seg;
         m0 = 0;
         ++k;
-        skip >>= 1;
+        if (kPrune) skip >>= 1;
     }
 }
 
@@ -1087,7 +1087,9 @@ __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C,
 // canonical ranges of one search) from a ticket, prefetching the next ticket.
 // PAIRS: tile count + ordered passing offsets to scratch; COUNTS: per-search
 // counts; FIRST: counts + first passing index.
-template <int kMode, int kOut, int kPath>
+// kPrune (CVG_PATH_PRUNED, band mode): its own instantiation, so that the
+// unpruned loops keep their register allocation (a run-time flag cost 1-2%).
+template <int kMode, int kOut, int kPath, bool kPrune = false>
 __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -1157,11 +1159,11 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         if (kMode == kModeBand && kPath == kPathFast && A.aligned) {
             const uint32_t nl = (C.flags >> 10) & 3u;
             if (nl == 3) {
-                band_tile<3, kOut>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
+                band_tile<3, kOut, kPrune>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
             } else if (nl == 2) {
-                band_tile<2, kOut>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
+                band_tile<2, kOut, kPrune>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
             } else {
-                band_tile<1, kOut>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
+                band_tile<1, kOut, kPrune>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);
             }
         } else if (kMode == kModeCodes && kPath == kPathFast && A.aligned) {
             CodeConsts CC;
@@ -1427,11 +1429,15 @@ inline int work_grid(int grid, uint64_t units, int warps) {
     return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(grid), need)));
 }
 
-template <int kMode, int kOut, int kPath>
+template <int kMode, int kOut, int kPath, bool kPrune = false>
 cudaError_t phase1_t(const LaunchArgs& a, int grid, cudaStream_t st) {
     grid = work_grid(grid, a.n_tiles, kWarpsPerBlock);
+    if (kMode == kModeBand && kPath == kPathFast && !kPrune && a.prune) {
+        phase1_kernel<kMode, kOut, kPath, true><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);
+        return cudaGetLastError();
+    }
     // The dynamic shared-memory sizes are opted into by occupancy_t (plan creation).
-    phase1_kernel<kMode, kOut, kPath><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);
+    phase1_kernel<kMode, kOut, kPath, kPrune><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);
     return cudaGetLastError();
 }
 
