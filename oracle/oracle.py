@@ -47,6 +47,32 @@ def _cpu_has_avx512() -> bool:
     return False
 
 
+def _cpu_flags() -> set:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("flags"):
+                    return set(line.split(":", 1)[1].split())
+    except OSError:
+        pass
+    return set()
+
+
+def reference_library() -> str:
+    """Path of the reference build for this host: the -march=native build
+    (BASELINE.md section 3's flags) when this CPU has every flag of the host
+    it was built on (_ref/native_cpu_flags.txt), else x86-64-v4 / -v3."""
+    native = os.path.join(HERE, "_ref", "libcolorvibe_ref_native.so")
+    flags_file = os.path.join(HERE, "_ref", "native_cpu_flags.txt")
+    if os.path.exists(native) and os.path.exists(flags_file):
+        with open(flags_file) as f:
+            built = set(f.readline().split())
+        if built and built <= _cpu_flags():
+            return native
+    v = "v4" if _cpu_has_avx512() else "v3"
+    return os.path.join(HERE, "_ref", f"libcolorvibe_ref_{v}.so")
+
+
 def _ptr(a, t):
     return None if a is None else a.ctypes.data_as(t)
 
@@ -153,15 +179,38 @@ class Reference(_Lib):
     prefix = "cvr_"
 
     def __init__(self, path: str | None = None):
-        if path is None:
-            v = "v4" if _cpu_has_avx512() else "v3"
-            path = os.path.join(HERE, "_ref", f"libcolorvibe_ref_{v}.so")
-        super().__init__(path)
+        super().__init__(path or reference_library())
         self.lib.cvr_last_error.restype = C.c_char_p
         self.lib.cvr_srgb_to_lab.argtypes = [_ip, _dp]
         f = self.lib.cvr_search_many
         f.restype = C.c_int64
         f.argtypes = [C.c_int, _ip, _ip, _dp, _dp, _dp, C.c_int, _dp, C.c_int, C.c_int, _u64p]
+        f = self.lib.cvr_search_memo
+        f.restype = C.c_int64
+        f.argtypes = [C.c_int64, _ip, C.c_int, C.c_double, C.c_double, _dp, C.c_int, _dp, C.c_int, C.c_int,
+                      _u64p, _up, _bp]
+        self.lib.cvr_batch_search_addr.restype = C.c_void_p
+
+    def batch_search_addr(self) -> int:
+        """Address colorvibe::batch_search resolves to inside this library."""
+        return self.lib.cvr_batch_search_addr()
+
+    def search_memo(self, rgb, pattern_bits: int, v_th: float, r_novib: float, radii, angles, threads: int = 0):
+        """Per-pixel batch memoized by color:
+        (counts u64[n], first_idx u32[n], first_codes u8[n, 6], n_unique)."""
+        t = np.ascontiguousarray(rgb, np.int32).reshape(-1, 3)
+        r = np.ascontiguousarray(radii, np.float64)
+        a = np.ascontiguousarray(angles, np.float64)
+        n = len(t)
+        counts = np.zeros(n, np.uint64)
+        first = np.zeros(n, np.uint32)
+        codes = np.zeros((n, 6), np.uint8)
+        u = self.lib.cvr_search_memo(n, _ptr(t, _ip), int(pattern_bits), float(v_th), float(r_novib),
+                                     _ptr(r, _dp), len(r), _ptr(a, _dp), len(a), int(threads or os.cpu_count() or 1),
+                                     _ptr(counts, _u64p), _ptr(first, _up), _ptr(codes, _bp))
+        if u < 0:
+            raise ValueError(self.last_error())
+        return counts, first, codes, int(u)
 
     def last_error(self) -> str:
         return self.lib.cvr_last_error().decode()

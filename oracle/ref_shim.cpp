@@ -9,10 +9,12 @@
 // reference's own colorvibe::batch_search (search.cpp:403-456).
 
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "colorvibe/search.hpp"
@@ -147,6 +149,98 @@ int64_t cvr_search_many(int n, const int32_t* rgb, const int32_t* pattern_bits,
             total += static_cast<int64_t>(pairs.size());
         }
         return total;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return -1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -2;
+    }
+}
+
+// Address of colorvibe::batch_search as THIS library binds it.  The library
+// is linked with -Bsymbolic (oracle/Makefile), so the reference's own
+// definition is used even when libcolorvibe_gpu.so (which exports the same
+// mangled symbol) is loaded into the same process first with RTLD_GLOBAL;
+// tests/test_oracle.py checks this with dladdr.
+void* cvr_batch_search_addr() {
+    using Fn = std::vector<ColorPair> (*)(const SrgbColor&, const VibrationGrid&, const BitPattern&,
+                                          const Thresholds&, const SearchOptions&);
+    return reinterpret_cast<void*>(static_cast<Fn>(&batch_search));
+}
+
+// cfg4's CPU baseline as BASELINE.md section 3 plans it: dedupe the pixels
+// by color -- with one pattern and one threshold pair for the batch, results
+// depend only on it -- evaluate each unique color with the reference
+// batch_search (workers = 1 per call) on an outer pool of `threads`
+// std::threads, then scatter count + first canonical pair to every pixel.
+// Writes counts[n], first_idx[n] (0xFFFFFFFF if none), first_codes[6n];
+// returns the number of unique colors, or a negative error.
+int64_t cvr_search_memo(int64_t n, const int32_t* rgb, int pattern_bits, double v_th,
+                        double r_novib, const double* radii, int nr, const double* angles, int na,
+                        int threads, uint64_t* counts, uint32_t* first_idx, uint8_t* first_codes) {
+    try {
+        const VibrationGrid grid = grid_of(radii, nr, angles, na);
+        std::vector<int32_t> slot(size_t(1) << 24, -1);  // key = rgb
+        std::vector<uint32_t> keys;
+        std::vector<int32_t> of(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) {
+            const int32_t* c = rgb + 3 * i;
+            if ((c[0] | c[1] | c[2]) & ~0xff) throw std::invalid_argument("color channel out of range");
+            const uint32_t key = (static_cast<uint32_t>(c[0]) << 16) | (static_cast<uint32_t>(c[1]) << 8) |
+                                 static_cast<uint32_t>(c[2]);
+            int32_t& u = slot[key];
+            if (u < 0) {
+                u = static_cast<int32_t>(keys.size());
+                keys.push_back(key);
+            }
+            of[static_cast<size_t>(i)] = u;
+        }
+        const size_t nu = keys.size();
+        std::vector<uint64_t> ucount(nu);
+        std::vector<uint32_t> ufirst(nu, 0xffffffffu);
+        std::vector<uint8_t> ucodes(6 * nu, 0);
+        std::atomic<size_t> next{0};
+        std::string err;
+        std::atomic<bool> failed{false};
+        auto work = [&] {
+            SearchOptions o;
+            o.workers = 1;
+            try {
+                for (size_t u; (u = next.fetch_add(1)) < nu && !failed.load();) {
+                    const uint32_t key = keys[u];
+                    const auto pairs = batch_search(
+                        SrgbColor{int((key >> 16) & 0xff), int((key >> 8) & 0xff), int(key & 0xff)}, grid,
+                        pattern_of(pattern_bits), Thresholds{v_th, r_novib}, o);
+                    ucount[u] = pairs.size();
+                    if (!pairs.empty()) {
+                        const ColorPair& p = pairs.front();
+                        const auto k = std::lower_bound(grid.radii.begin(), grid.radii.end(), p.radius) -
+                                       grid.radii.begin();
+                        const auto m = std::lower_bound(grid.angles.begin(), grid.angles.end(), p.angle) -
+                                       grid.angles.begin();
+                        ufirst[u] = static_cast<uint32_t>(static_cast<uint64_t>(k) * na + m);
+                        uint8_t* c = &ucodes[6 * u];
+                        c[0] = p.plus.r; c[1] = p.plus.g; c[2] = p.plus.b;
+                        c[3] = p.minus.r; c[4] = p.minus.g; c[5] = p.minus.b;
+                    }
+                }
+            } catch (const std::exception& e) {
+                if (!failed.exchange(true)) err = e.what();
+            }
+        };
+        std::vector<std::thread> pool;
+        for (int t = 1; t < std::max(1, threads); ++t) pool.emplace_back(work);
+        work();
+        for (auto& t : pool) t.join();
+        if (failed) throw std::invalid_argument(err);
+        for (int64_t i = 0; i < n; ++i) {
+            const size_t u = static_cast<size_t>(of[static_cast<size_t>(i)]);
+            counts[i] = ucount[u];
+            first_idx[i] = ufirst[u];
+            std::memcpy(first_codes + 6 * i, &ucodes[6 * u], 6);
+        }
+        return static_cast<int64_t>(nu);
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
         return -1;

@@ -6,14 +6,14 @@ reference's own src/color.cpp + src/search.cpp compiled where they lie under
 build container (where /root/reference exists):
 
     python tests/golden/make_golden.py            # everything but cfg2
-    python tests/golden/make_golden.py --cfg2     # + cfg2 per-target counts (minutes)
+    python tests/golden/make_golden.py --cfg2     # + cfg2 per-target counts and record sha256 (minutes)
     python tests/golden/make_golden.py --cfg4     # + full-size cfg4 per-pixel count/first hash
 
 Outputs (all small, committed):
   known_answers.json    thresholds, kXyzToRgb, d65 white, target Lab, code probes
   small_cases.json      reference test_search.cpp grid cases: count + sha256 per case
   workloads.json        cfg0 / cfg1 / cfg3 per-search counts + record sha256,
-                        cfg2 per-target counts, cfg4 (256x144 crop) count/first sha256
+                        cfg2 per-target counts + 10-byte-record sha256, cfg4 (256x144 crop) count/first sha256
   matrix_aggregated.csv feasibility aggregate over SearchConfig::defaults()
                         (same bytes as the reference's tests/golden file)
 """
@@ -98,6 +98,41 @@ def workload_records(ref: Reference, wl: W.Workload, workers: int) -> dict:
     return {"counts": counts, "total": int(sum(counts)), "sha256": shas.hexdigest()}
 
 
+def records10_sha_update(m, idx: np.ndarray, codes: np.ndarray) -> None:
+    """Feeds records in the 10-byte wire layout (u32 LE idx, then the 6 code
+    bytes) to hash m -- streamable, so cfg2's 444M pairs hash row chunk by
+    row chunk."""
+    rec = np.empty((len(idx), 10), np.uint8)
+    rec[:, :4] = np.ascontiguousarray(idx, "<u4").view(np.uint8).reshape(-1, 4)
+    rec[:, 4:] = codes
+    m.update(rec.tobytes())
+
+
+def cfg2_records(ref: Reference, workers: int, chunk: int = 256) -> dict:
+    """cfg2 per-target counts and per-target record sha256 (10-byte layout),
+    from the reference batch_search run on row chunks [k_lo, k_lo+chunk) of
+    the grid: rows are independent (search.cpp:230-278) and a search's list
+    is the concatenation of its row slices in row order (search.cpp:433-455),
+    so idx = (k_lo + k) * na + m of the chunk's record k * na + m."""
+    wl = W.cfg2()
+    na = len(wl.angles)
+    counts, shas = [], []
+    for s in range(wl.n_searches):
+        m, n = hashlib.sha256(), 0
+        for k_lo in range(0, len(wl.radii), chunk):
+            idx, codes, _ = ref.search(wl.targets[s], int(wl.patterns[s]), wl.v_th[s], wl.r_novib[s],
+                                       wl.radii[k_lo:k_lo + chunk], wl.angles, method=1, workers=workers,
+                                       want_deltas=False)
+            records10_sha_update(m, idx.astype(np.uint64) + np.uint64(k_lo * na), codes)
+            n += len(idx)
+        counts.append(n)
+        shas.append(m.hexdigest())
+        print(f"cfg2 target {s}: {n} pairs", flush=True)
+    return {"counts": counts, "total": int(sum(counts)), "sha256_records10": shas,
+            "layout": "per target: sha256 over 10-byte records (u32 LE idx = k*na+m, plus rgb, minus rgb) "
+                      "in canonical order; reference batch_search on 256-row chunks"}
+
+
 def cfg4_small(ref: Reference, width=256, height=144) -> dict:
     """cfg4 pipeline (same generator, any size): per-pixel count and first
     canonical pair, memoized by color (results depend only on it)."""
@@ -144,6 +179,7 @@ def aggregated_matrix(ref: Reference) -> str:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg2", action="store_true")
+    ap.add_argument("--cfg2-only", action="store_true", help="regenerate only the cfg2 entry")
     ap.add_argument("--cfg4", action="store_true", help="full 3840x2160 per-pixel config (memoized by color)")
     ap.add_argument("--workers", type=int, default=os.cpu_count() or 1)
     args = ap.parse_args()
@@ -157,6 +193,12 @@ def main():
         f.write(aggregated_matrix(ref))
     path = os.path.join(HERE, "workloads.json")
     wj = json.load(open(path)) if os.path.exists(path) else {}
+    if args.cfg2_only:
+        wj["cfg2"] = cfg2_records(ref, args.workers)
+        with open(path, "w") as f:
+            json.dump(wj, f, indent=1)
+        print(f"cfg2 fixture written in {time.time() - t0:.1f}s")
+        return
     wj["cfg0"] = workload_records(ref, W.cfg0(), args.workers)
     wj["cfg1"] = workload_records(ref, W.cfg1(), args.workers)
     wj["cfg3"] = workload_records(ref, W.cfg3(), args.workers)
@@ -164,10 +206,7 @@ def main():
     if args.cfg4:
         wj["cfg4"] = cfg4_small(ref, 3840, 2160)
     if args.cfg2:
-        wl = W.cfg2()
-        counts = ref.search_many(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles,
-                                 workers=args.workers)
-        wj["cfg2"] = {"counts": [int(c) for c in counts], "total": int(counts.sum())}
+        wj["cfg2"] = cfg2_records(ref, args.workers)
     with open(path, "w") as f:
         json.dump(wj, f, indent=1)
     print(f"golden fixtures written in {time.time() - t0:.1f}s")

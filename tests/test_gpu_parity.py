@@ -10,7 +10,7 @@ import threading
 import numpy as np
 import pytest
 
-from cvtest_util import golden, sha_records
+from cvtest_util import golden, records10_sha, sha_records
 from paper_2507_22901_b200 import workloads as W
 from paper_2507_22901_b200.workloads import uniform_grid
 
@@ -162,18 +162,24 @@ def test_cfg4_full_image_first_pair(ctx):
 
 
 @pytest.mark.slow
-def test_cfg2_fine_grid_counts_and_rows(ctx, oracle):
+def test_cfg2_fine_grid_full_pair_set(ctx, oracle):
+    """cfg2 (2.4G candidates, 444M pairs): per-target counts AND the full
+    ordered record set of every target against the reference's own
+    batch_search (tests/golden/make_golden.py --cfg2: 10-byte-record sha256
+    per target), plus a few rows against the oracle directly."""
     wl = W.cfg2()
     res = run(ctx, wl)
-    g = golden("workloads.json").get("cfg2")
-    if g:
-        assert res["counts"].tolist() == g["counts"]
+    g = golden("workloads.json")["cfg2"]
+    assert res["counts"].tolist() == g["counts"]
+    assert res["n_pairs"] == g["total"] == 444092662
     assert_clean(res, "fast")
+    for s in range(wl.n_searches):
+        idx, codes = split(res, s)
+        assert records10_sha(idx, codes) == g["sha256_records10"][s], f"cfg2 target {s} pair set differs"
     na = len(wl.angles)
     rows = [0, 1, 777, 2048, 4095]
     for s in (0, 3, 8):
         idx, codes = split(res, s)
-        assert np.all(np.diff(idx.astype(np.int64)) > 0)  # canonical order, no duplicates
         sub = W.Workload("sub", wl.targets[s:s + 1], wl.patterns[s:s + 1], wl.v_th[s:s + 1],
                          wl.r_novib[s:s + 1], wl.radii[rows], wl.angles)
         oi, oc = oracle_records(oracle, sub, 0, workers=8)
@@ -182,6 +188,27 @@ def test_cfg2_fine_grid_counts_and_rows(ctx, oracle):
         kk = np.searchsorted(np.array(rows), k[sel])
         assert np.array_equal(kk * na + idx[sel] % na, oi)
         assert np.array_equal(codes[sel], oc)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["cfg2", "cfg3", "cfg4"])
+def test_audit_bound_holds_on_large_configs(ctx, name):
+    """AUDIT path (every candidate in FP32 and FP64) on the grids that stress
+    the error bound most: cfg2 (r <= 128 on a 65536-angle grid), cfg3 (4096
+    lattice targets incl. near-black), cfg4 (8.3M pixels, r <= 126, the
+    linear branch of f^-1).  No FP32 decision claimed certain may be wrong,
+    and every |lin32 - lin64| must stay inside its proven bound."""
+    wl = W.ALL[name]()
+    out = {"cfg2": "counts", "cfg3": "pairs", "cfg4": "first"}[name]
+    res = run(ctx, wl, output=out, path="audit")
+    g = golden("workloads.json")[name]
+    assert int(res["counts"].sum()) == g["total"]
+    if name != "cfg4":
+        assert res["counts"].tolist() == g["counts"]
+    st = res["stats"]
+    assert st["audit_violations"] == 0, st
+    assert 0.0 < st["audit_max_ratio"] < 1.0, st
+    assert st["class_mismatch"] == 0, st
 
 
 # ---- reference API through the Python binding (test_search.cpp pins) -------

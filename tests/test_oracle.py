@@ -4,6 +4,8 @@ Golden fixtures were produced by the reference itself (tests/golden/make_golden.
 over oracle/_ref, i.e. the reference's src/color.cpp + src/search.cpp).  When
 the reference build is present the oracle is also compared to it directly.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -125,3 +127,59 @@ def test_oracle_equals_reference_custom_white(oracle, reference):
     b = reference.search([120, 60, 200], 5, 50.0, 0.5, radii, angles, white=wp, workers=1)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+_BIND_CHECK = r"""
+import ctypes, ctypes.util, os, sys
+sys.path.insert(0, {root!r})
+# the product library first, GLOBAL: it exports the same mangled
+# colorvibe::batch_search as the reference checker
+ctypes.CDLL({gpu!r}, mode=ctypes.RTLD_GLOBAL)
+from oracle.oracle import Reference
+ref = Reference()
+
+class Dl_info(ctypes.Structure):
+    _fields_ = [("dli_fname", ctypes.c_char_p), ("dli_fbase", ctypes.c_void_p),
+                ("dli_sname", ctypes.c_char_p), ("dli_saddr", ctypes.c_void_p)]
+
+libdl = ctypes.CDLL(ctypes.util.find_library("dl") or "libc.so.6")
+info = Dl_info()
+assert libdl.dladdr(ctypes.c_void_p(ref.batch_search_addr()), ctypes.byref(info))
+print(os.path.realpath(info.dli_fname.decode()), os.path.realpath(ref.path))
+"""
+
+
+def test_reference_binds_its_own_search():
+    """The reference checker must run the REFERENCE's batch_search even when
+    libcolorvibe_gpu.so, which exports the identical C++ symbol, was loaded
+    first with RTLD_GLOBAL (-Bsymbolic link, oracle/Makefile): otherwise the
+    parity tests could compare the product with itself."""
+    import subprocess
+    import sys
+
+    from cvtest_util import ROOT
+
+    gpu = os.path.join(ROOT, "paper_2507_22901_b200", "libcolorvibe_gpu.so")
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.exists(gpu) or not os.path.isdir(ref_dir):
+        pytest.skip("libraries not built")
+    out = subprocess.run([sys.executable, "-c", _BIND_CHECK.format(root=ROOT, gpu=gpu)], capture_output=True,
+                         text=True, check=True).stdout.split()
+    assert out[0] == out[1] and "/oracle/_ref/" in out[0], out
+
+
+def test_reference_memo_matches_crop_golden(reference):
+    """bench.py's cfg4 CPU baseline (memoized by color)
+    against the reference-generated 256x144 per-pixel golden."""
+    import hashlib
+
+    from cvtest_util import golden
+    from paper_2507_22901_b200 import workloads as W
+
+    g = golden("workloads.json")["cfg4_256x144"]
+    wl = W.cfg4(g["width"], g["height"])
+    counts, first, codes, nu = reference.search_memo(wl.targets, 7, 50.0, 0.5, wl.radii, wl.angles, threads=4)
+    assert nu == g["unique_colors"]
+    m = hashlib.sha256()
+    m.update(counts.tobytes()); m.update(first.tobytes()); m.update(codes.tobytes())
+    assert int(counts.sum()) == g["total"] and m.hexdigest() == g["sha256"]
