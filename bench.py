@@ -1,34 +1,51 @@
 #!/usr/bin/env python3
 """Benchmark: candidate color pairs evaluated per second on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--impl ours|reference]
 
 One step = one pass of the hot path (colorvibe::batch_search, reference
-src/search.cpp:403-456) over one batch of synthetic input: by default
-BASELINE.json configs[1], the 756-search sweep on the 256 x 1024 grid
-(198,180,864 candidates), evaluated in ONE launch of the fused kernel.
+src/search.cpp:403-456) over one batch of synthetic input.  The headline
+workload is the largest single-GPU configuration of BASELINE.json: cfg4, the
+per-pixel batch (3840x2160 pixels, one search each, 64 radii x 256 angles,
+135,895,449,600 candidates, per-pixel count + first canonical pair).  The
+other configs (cfg0..cfg3) are measured in the same run (N = 1) and reported
+inside the same JSON line under "configs".
 
 Prints ONE JSON line (rank 0):
-  value   -- Gcand/s with inputs resident in HBM (device plan; CUDA events on
-             the launching stream around each step, L2 flushed between steps)
-  e2e     -- same metric through the C-ABI host call `cvg_search` (host
-             arrays in; per-target prep, H2D, kernel, D2H of counts + every
-             pair record out), wall-clocked per call
-  roofline-- FP32-issue roofline of the fused kernel (SURVEY.md §8(d):
-             W = 50 FP32 instructions per candidate) vs the FFMA issue peak
-             measured in this run
+  value    -- Gcand/s, whole job, inputs resident in HBM (device plan; CUDA
+              events on the launching stream around each step, L2 flushed
+              between steps, max over ranks)
+  e2e      -- same metric through the C-ABI host call `cvg_search` (host
+              arrays in: validation, per-target prep, H2D, kernels, D2H of
+              every result), wall-clocked per call, max over ranks
+  memoized -- cfg4 only, LABELLED APART: the same per-pixel result with each
+              distinct color searched once (CVG_PATH_MEMO), nominal
+              candidates / wall time; beside it the reference memoized the
+              same way
+  roofline -- FP32-issue roofline of the fused kernel (SURVEY.md section 8(d):
+              W = 50 FP32 instructions per candidate) vs the FFMA issue peak
+              measured in this run
   cpu_baseline -- the reference's own batch_search (oracle/_ref, built from
-             the reference sources) on all host cores, same workload
+              the reference sources) on the host cores
 
-Multi-GPU (torchrun, one process per GPU): weak scaling -- every rank
-evaluates its own full copy of the workload; there is no data-path exchange
-(the searches are independent), value = all ranks' candidates / max-over-
-ranks device time.  `--impl reference` runs the reference CPU arm on rank 0.
+Multi-GPU (torchrun, one process per GPU, NCCL): the batch is PARTITIONED
+(SURVEY.md section 8(e)): contiguous search ranges for the many-search
+configs (cfg1, cfg3, cfg4), radius-row slices for the few-search ones (cfg0,
+cfg2).  A timed step is the local search plus the NCCL all_gather of the
+per-search results (cfg4: counts + first pair of every pixel; else counts);
+value = the global batch's candidates / max-over-ranks time (strong
+scaling: the total work is fixed).  The pair-list gather (send/recv into
+offset slices on rank 0) is timed apart under "gather".
+
+`--impl reference` runs the reference CPU arm on rank 0 and imports nothing
+from the product package (the workload generators are loaded by path).
 """
 from __future__ import annotations
 
 import argparse
 import contextlib
+import hashlib
+import importlib.util
 import json
 import os
 import statistics
@@ -44,18 +61,37 @@ import numpy as np  # noqa: E402
 W_INSTR = 50  # algorithmic FP32 instructions per candidate
 METRIC = "candidate color pairs evaluated/sec"
 UNIT = "Gcand/s"
+CONFIGS = ["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"]
+HEADLINE = "cfg4"
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg1", choices=["cfg0", "cfg1", "cfg2", "cfg3", "cfg4"])
+    ap.add_argument("--config", default=HEADLINE, choices=CONFIGS)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-others", action="store_true", help="skip the other configs (N = 1)")
     return ap.parse_args()
+
+
+def load_workloads():
+    """paper_2507_22901_b200/workloads.py loaded BY PATH: it needs only
+    numpy, and importing it this way does not import the package (whose
+    __init__ loads the native extension) -- the reference arm stays free of
+    the product's libraries."""
+    path = os.path.join(ROOT, "paper_2507_22901_b200", "workloads.py")
+    spec = importlib.util.spec_from_file_location("_cvg_bench_workloads", path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod  # dataclasses resolve the module by name
+    spec.loader.exec_module(mod)
+    return mod
+
+
+W = load_workloads()
 
 
 @contextlib.contextmanager
@@ -77,22 +113,35 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def workload(name):
-    from paper_2507_22901_b200 import workloads as W
+def partition(wl, world):
+    """Same rule as paper_2507_22901_b200.distributed.partition (kept here so
+    the reference arm needs no package import)."""
+    if world > 1 and wl.n_searches < 4 * world and len(wl.radii) >= world:
+        return "rows"
+    return "searches"
 
-    return W.ALL[name]()
+
+def shard(wl, rank, world):
+    """This rank's share of `wl`: a contiguous search range, or (rows) radius
+    rows [k_lo, k_hi) of every search (reference row slices, search.cpp:433-455)."""
+    if world == 1:
+        return wl
+    if partition(wl, world) == "rows":
+        nr = len(wl.radii)
+        k_lo, k_hi = nr * rank // world, nr * (rank + 1) // world
+        return W.Workload(wl.name, wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii[k_lo:k_hi], wl.angles,
+                          wl.output, wl.note)
+    return wl.shard(rank, world)
 
 
-def config_dict(wl, n, extra=None):
-    d = {"workload": f"{wl.name} (BASELINE.json configs[{wl.name[-1]}])", "searches": wl.n_searches,
-         "grid": f"{len(wl.radii)} radii x {len(wl.angles)} angles", "candidates_per_step": wl.candidates,
-         "targets": {"cfg3": "16^3 lattice", "cfg4": "3840x2160 Voronoi image, one search per pixel"}.get(
-             wl.name, "Table-1 colors"), "output": wl.output,
-         "parallelism": f"dp{n} (each rank its own {wl.name}-sized batch, no data-path collective)" if n > 1
-         else "single", "l2": "flushed between steps (256 MiB write)"}
-    if extra:
-        d.update(extra)
-    return d
+def config_dict(wl, world):
+    """The workload, identical in both arms (the driver compares them)."""
+    return {"workload": f"{wl.name} (BASELINE.json configs[{wl.name[-1]}])", "searches": wl.n_searches,
+            "grid": f"{len(wl.radii)} radii x {len(wl.angles)} angles", "candidates_per_step": wl.candidates,
+            "targets": {"cfg3": "16^3 lattice", "cfg4": "3840x2160 Voronoi image, one search per pixel"}.get(
+                wl.name, "Table-1 colors"), "output": wl.output,
+            "parallelism": (f"partitioned over {world} GPUs by {partition(wl, world)}" if world > 1 else "single"),
+            "l2": "flushed between steps (256 MiB write)"}
 
 
 # ---------------------------------------------------------------------------
@@ -153,43 +202,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-
-CPU_SAMPLE_SEARCHES = {"cfg4": 20000, "cfg2": 1}  # bounded CPU samples (full cfg0/1/3)
-
-
-def cpu_sample(wl):
-    """Bounded CPU sample of a workload: the first searches (cfg4: 20,000
-    pixels, no color memoization; cfg2: one target on 512 of its 4096 radius
-    rows), so the reference arm finishes in seconds."""
-    n = CPU_SAMPLE_SEARCHES.get(wl.name)
-    if n is None:
-        return wl, f"full {wl.name} ({wl.n_searches} searches)"
-    sub = wl.shard(0, max(1, wl.n_searches // n)) if wl.n_searches > n else wl
-    sub = type(wl)(wl.name, sub.targets[:n], sub.patterns[:n], sub.v_th[:n], sub.r_novib[:n], sub.radii,
-                   sub.angles, wl.output, wl.note)
-    if wl.name == "cfg2":
-        sub.radii = wl.radii[::8]
-        return sub, f"cfg2 target 0, every 8th radius row ({sub.candidates} candidates)"
-    return sub, f"first {n} pixels of {wl.name} ({sub.candidates} candidates, no color memoization)"
-
-
-def cpu_reference_arm(wl, steps, warmup, cores=None):
-    """The reference's own batch_search (oracle/_ref) once per search, all host
-    threads, full workload per step.  Returns (Gcand/s, seconds/step, cores)."""
-    from oracle.oracle import Reference
-
-    ref = Reference()
-    cores = cores or os.cpu_count() or 1
-    for _ in range(warmup):
-        ref.search_many(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, workers=cores)
-    times = []
-    for _ in range(steps):
-        t0 = time.perf_counter()
-        counts = ref.search_many(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, workers=cores)
-        times.append(time.perf_counter() - t0)
-    total = sum(times)
-    return wl.candidates * steps / total / 1e9, total / steps, cores, int(counts.sum()), ref.path
-
+# reference CPU side (oracle/_ref: the reference's own color.cpp + search.cpp)
 
 def cpu_model():
     try:
@@ -201,32 +214,132 @@ def cpu_model():
     return "unknown"
 
 
+CPU_SAMPLE = {"cfg4": 65536, "cfg2": 1}  # bounded CPU samples (cfg0/1/3 run in full)
+
+
+def cpu_sample(wl):
+    """Bounded CPU sample of a workload, so the reference arm finishes in
+    seconds per step: cfg4 = 65,536 pixels spread evenly over the image (every
+    ~127th pixel, no color memoization); cfg2 = target 0 on every 8th radius
+    row; cfg0/1/3 = the full workload."""
+    if wl.name == "cfg4":
+        n = CPU_SAMPLE["cfg4"]
+        sel = np.linspace(0, wl.n_searches - 1, n).astype(np.int64)
+        sub = W.Workload(wl.name, wl.targets[sel], wl.patterns[sel], wl.v_th[sel], wl.r_novib[sel], wl.radii,
+                         wl.angles, wl.output, wl.note)
+        return sub, f"{n} pixels evenly spread over the image ({sub.candidates} candidates, each evaluated)"
+    if wl.name == "cfg2":
+        sub = W.Workload(wl.name, wl.targets[:1], wl.patterns[:1], wl.v_th[:1], wl.r_novib[:1], wl.radii[::8],
+                         wl.angles, wl.output, wl.note)
+        return sub, f"cfg2 target 0, every 8th radius row ({sub.candidates} candidates)"
+    return wl, f"full {wl.name} ({wl.n_searches} searches)"
+
+
+def cpu_run(ref, wl, steps, warmup, cores):
+    """The reference batch_search once per search, on all host threads:
+    per-search batches as the reference's own sweep calls it (one call per
+    search, workers = all threads; feasibility.cpp:273-275); the per-pixel
+    batch (cfg4, 16K-candidate searches, where a thread spawn per call would
+    dominate) on an outer pool of all threads with workers = 1 per pixel
+    (BASELINE.md section 3), every pixel searched.  Returns (Gcand/s,
+    s/step, pairs)."""
+    if wl.name == "cfg4":
+        def one():
+            return ref.search_memo(wl.targets, int(wl.patterns[0]), float(wl.v_th[0]), float(wl.r_novib[0]),
+                                   wl.radii, wl.angles, threads=cores, memo=False)[0]
+    else:
+        def one():
+            return ref.search_many(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles,
+                                   workers=cores)
+    for _ in range(warmup):
+        one()
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        counts = one()
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    return wl.candidates * steps / total / 1e9, total / steps, int(counts.sum())
+
+
+def cpu_memoized(ref, wl, cores, reps=3):
+    """BASELINE.md section 3's cfg4 CPU plan: dedupe pixels by color, each
+    unique color through the reference batch_search (workers = 1) on an
+    outer pool of `cores` threads, scatter; best of `reps` wall times."""
+    best, out = None, None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = ref.search_memo(wl.targets, int(wl.patterns[0]), float(wl.v_th[0]), float(wl.r_novib[0]),
+                              wl.radii, wl.angles, threads=cores)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    counts, first, codes, nu = out
+    return {"wall_s": round(best, 4), "nominal_value": round(wl.candidates / best / 1e9, 4), "unit": UNIT,
+            "unique_colors": nu, "threads": cores, "total_pairs": int(counts.sum()),
+            "result_sha256": first_hash(counts, first, codes),
+            "note": "MEMOIZED (not the metric): each distinct color searched once, results scattered to its "
+                    "pixels; nominal candidates / wall time, best of 3 (BASELINE.md section 3)"}
+
+
+def first_hash(counts, first, codes):
+    m = hashlib.sha256()
+    m.update(np.ascontiguousarray(counts, np.uint64).tobytes())
+    m.update(np.ascontiguousarray(first, np.uint32).tobytes())
+    m.update(np.ascontiguousarray(codes, np.uint8).tobytes())
+    return m.hexdigest()
+
+
+def cpu_baseline(wl, steps=2, warmup=1):
+    from oracle.oracle import Reference
+
+    ref = Reference()
+    cores = os.cpu_count() or 1
+    cwl, sample = cpu_sample(wl)
+    v, sec, pairs = cpu_run(ref, cwl, steps, warmup, cores)
+    out = {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "reference",
+           "sample": f"{sample}; mean of {steps} steps after {warmup} warm-up; workers={cores}; {cpu_model()}; "
+                     f"{os.path.relpath(ref.path, ROOT)}",
+           "pairs": pairs, "s_per_step": round(sec, 4)}
+    if wl.name == "cfg4":
+        out["memoized"] = cpu_memoized(ref, wl, cores)
+    return out, cwl is wl, pairs
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    wl, sample = cpu_sample(workload(args.config))
-    steps = max(1, min(args.steps, 20))
-    warm = max(0, min(args.warmup, 2))
-    v, sec, cores, pairs, path = cpu_reference_arm(wl, steps, warm)
+    from oracle.oracle import Reference
+
+    wl = W.ALL[args.config]()
+    ref = Reference()
+    cores = os.cpu_count() or 1
+    cwl, sample = cpu_sample(wl)
+    v, sec, pairs = cpu_run(ref, cwl, args.steps, args.warmup, cores)
     out = {
-        "metric": METRIC, "value": round(v, 6), "unit": UNIT, "n_gpus": world, "device": "cpu (host cores)",
-        "steps": steps, "warmup": warm,
-        "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": config_dict(wl, 1, {"cpu": cpu_model(), "library": os.path.relpath(path, ROOT)}),
+        "metric": METRIC, "value": round(v, 6), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference", "config": config_dict(wl, world),
+        "device": "cpu (host cores)", "cpu": cpu_model(), "library": os.path.relpath(ref.path, ROOT),
         "pairs_per_step": pairs,
         "cpu_baseline": {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "reference",
                          "sample": f"{sample}: one reference batch_search call per search per step, "
-                                   f"workers={cores}"},
+                                   + ("outer pool of " if wl.name == "cfg4" else "workers=") + f"{cores}"
+                                   + (" threads, workers=1 per call" if wl.name == "cfg4" else "")},
         "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if wl.name == "cfg4":
+        out["memoized"] = cpu_memoized(ref, wl, cores)
     print(json.dumps(out), flush=True)
 
 
-def ncu_traffic(config="cfg1"):
-    """DRAM bytes (read + write) per launch of phase1_kernel from one committed
-    `ncu --set full` capture (profiles/ncu_summary.json), or None."""
+# ---------------------------------------------------------------------------
+# our arm
+
+def ncu_traffic(config):
+    """DRAM bytes (read + write) per launch of phase1_kernel from the
+    committed `ncu --set full` capture summary (profiles/ncu_summary.json)."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
@@ -236,62 +349,232 @@ def ncu_traffic(config="cfg1"):
         return None
 
 
-def time_gather(dist, plan, wl, n_pairs, world, stream, reps=5):
-    """The multi-GPU exchange step of SURVEY §8(e), timed apart from the
-    search (scaling is weak: no collective in the timed step): NCCL
-    all_gather of every rank's per-search counts, and (PAIRS) of its packed
-    pair records (u32 idx + 6 code bytes, padded to the largest rank).  Device
-    events around each collective, max over ranks.  The gathered counts are
-    checked against the local ones (every rank ran the same batch)."""
+class ResultGather:
+    """The exchange inside a multi-GPU step: NCCL
+    all_gather of each rank's per-search results into the global layout.
+    searches partition: counts (and, FIRST, first idx + codes) of equal-size
+    padded shards; rows partition: per-search counts of every rank."""
+
+    def __init__(self, dist, plan, wl, lwl, by, world):
+        import torch
+
+        self.dist, self.plan, self.by = dist, plan, by
+        self.first = wl.output == "first"
+        n_local = lwl.n_searches
+        self.width = n_local if by == "rows" else -(-wl.n_searches // world)  # ceil
+        dev = "cuda"
+        self.counts = torch.zeros(self.width, dtype=torch.int64, device=dev)
+        self.g_counts = torch.empty(world * self.width, dtype=torch.int64, device=dev)
+        if self.first:
+            self.fidx = torch.zeros(self.width, dtype=torch.int32, device=dev)
+            self.fcodes = torch.zeros((self.width, 6), dtype=torch.uint8, device=dev)
+            self.g_fidx = torch.empty(world * self.width, dtype=torch.int32, device=dev)
+            self.g_fcodes = torch.empty((world * self.width, 6), dtype=torch.uint8, device=dev)
+        self.bytes_per_rank = self.width * (8 + (10 if self.first else 0))
+
+    def __call__(self, stream):
+        self.plan.copy_outputs(self.counts.data_ptr(), 0, 0, 0, stream.cuda_stream)
+        if self.first:
+            self.plan.copy_first(self.fidx.data_ptr(), self.fcodes.data_ptr(), stream.cuda_stream)
+        self.dist.all_gather_into_tensor(self.g_counts, self.counts)
+        if self.first:
+            self.dist.all_gather_into_tensor(self.g_fidx, self.fidx)
+            self.dist.all_gather_into_tensor(self.g_fcodes, self.fcodes)
+
+
+def time_plan(plan, stream, steps, warmup, flush, after=None, clk=None, dist=None):
+    """K device-timed steps (CUDA events on the launching stream around the
+    plan run + `after`), L2 flushed between steps outside the events.
+    Returns total ms (max over ranks) and the per-step list."""
     import torch
 
-    n = wl.n_searches
-    counts = torch.empty(n, dtype=torch.int64, device="cuda")
-    pairs = wl.output == "pairs"
-    idx = torch.empty(max(n_pairs, 1), dtype=torch.int32, device="cuda") if pairs else None
-    codes = torch.empty((max(n_pairs, 1), 6), dtype=torch.uint8, device="cuda") if pairs else None
+    for _ in range(warmup):
+        flush.zero_()
+        plan.run(stream.cuda_stream)
+        if after:
+            after(stream)
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ctxm = clk if clk is not None else contextlib.nullcontext()
+    with ctxm:
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for i in range(steps):
+            flush.zero_()
+            starts[i].record(stream)
+            plan.run(stream.cuda_stream)
+            if after:
+                after(stream)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), step_ms
+
+
+def time_e2e(ctx, lwl, steps, dist, path="fast"):
+    """`steps` wall-clocked calls of the C-ABI host search (ctx.search ->
+    cvg_search) on this rank's share; max over ranks."""
+    import torch
+
+    for _ in range(2):  # the second call allocates with the first call's shape hint
+        res = ctx.search(lwl.targets, lwl.patterns, lwl.v_th, lwl.r_novib, lwl.radii, lwl.angles,
+                         output=lwl.output, path=path)
+    h2d, d2h = int(res["stats"]["h2d_bytes"]), int(res["stats"]["d2h_bytes"])
+    del res
+    if dist:
+        dist.barrier()
+    times, phases = [], []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        r = ctx.search(lwl.targets, lwl.patterns, lwl.v_th, lwl.r_novib, lwl.radii, lwl.angles, output=lwl.output,
+                       path=path)
+        _ = int(r["n_pairs"])
+        times.append(time.perf_counter() - t0)
+        phases.append({k: r["stats"][k] for k in ("prep_ms", "h2d_ms", "device_ms", "d2h_ms", "total_ms")})
+        last = r
+    t = torch.tensor([sum(times)], dtype=torch.float64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    med = {k: round(statistics.median(p[k] for p in phases), 4) for k in phases[0]}
+    return float(t.item()) / steps, h2d, d2h, med, last
+
+
+def pair_gather(dist, plan, lwl, n_pairs_local, world, by, reps=3):
+    """PAIRS configs at N > 1, timed apart from the step: size exchange, then
+    every rank's packed records sent into their offset slice on rank 0
+    (distributed.gather_records: exact-size sends, nothing received
+    elsewhere).  Device events, max over ranks."""
+    import torch
+
+    from paper_2507_22901_b200.distributed import gather_records
+
+    n = max(n_pairs_local, 1)
+    idx = torch.empty(n, dtype=torch.int32, device="cuda")
+    codes = torch.empty((n, 6), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
     plan.run(stream.cuda_stream)
     plan.sync()
-    plan.copy_outputs(counts.data_ptr(), idx.data_ptr() if pairs else 0, codes.data_ptr() if pairs else 0,
-                      n_pairs if pairs else 0, stream.cuda_stream)
-    sizes = torch.tensor([n_pairs], dtype=torch.int64, device="cuda")
-    out_c = [torch.empty_like(counts) for _ in range(world)]
+    plan.copy_outputs(0, idx.data_ptr(), codes.data_ptr(), n_pairs_local, stream.cuda_stream)
+    rec = torch.empty((n_pairs_local, 10), dtype=torch.uint8, device="cuda")
+    rec[:, :4] = idx[:n_pairs_local].view(torch.uint8).view(-1, 4)
+    rec[:, 4:] = codes[:n_pairs_local]
+    size = torch.tensor([n_pairs_local], dtype=torch.int64, device="cuda")
+    sizes_t = torch.empty(world, dtype=torch.int64, device="cuda")
+    ms = []
+    for _ in range(reps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dist.all_gather_into_tensor(sizes_t, size)
+        sizes = [int(x) for x in sizes_t.cpu()]
+        out = gather_records(rec, sizes, None, 0)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms.append(a.elapsed_time(b))
+    v = torch.tensor([statistics.median(ms)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(v, op=dist.ReduceOp.MAX)
+    total = sum(sizes)
+    if out is not None:
+        assert out.shape[0] == total
+    return {"collective": "size all_gather + NCCL send/recv into offset slices on rank 0",
+            "partition": by, "pairs_total": total, "bytes_total": 10 * total,
+            "ms": round(float(v.item()), 4),
+            "gbs": round(10 * total / (float(v.item()) * 1e-3) / 1e9, 1) if v.item() > 0 else None}
 
-    def timed(fn):
-        ms = []
-        for _ in range(reps):
-            dist.barrier()
-            torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            fn()
-            b.record(stream)
-            torch.cuda.synchronize()
-            ms.append(a.elapsed_time(b))
-        v = torch.tensor([statistics.median(ms)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        return float(v.item())
 
-    out = {"collective": "NCCL all_gather over NVLink", "counts_bytes_per_rank": 8 * n,
-           "counts_all_gather_ms": round(timed(lambda: dist.all_gather(out_c, counts)), 4)}
-    assert all(torch.equal(x, counts) for x in out_c), "gathered counts differ between ranks"
-    if pairs:
-        all_sizes = [torch.empty_like(sizes) for _ in range(world)]
-        dist.all_gather(all_sizes, sizes)
-        width = int(max(int(x.item()) for x in all_sizes))
-        rec = torch.zeros((max(width, 1), 10), dtype=torch.uint8, device="cuda")
-        rec[:n_pairs, :4] = idx[:n_pairs].view(torch.uint8).view(-1, 4)
-        rec[:n_pairs, 4:] = codes[:n_pairs]
-        out_r = [torch.empty_like(rec) for _ in range(world)]
+def measure_config(cv, ctx, wl, args, rank, world, local, dist, flush, clk=None, full=True):
+    """value / e2e / phases (and, at N = 1, pruned + memoized) of one config."""
+    import torch
 
-        def pairs_gather():
-            dist.all_gather(all_sizes, sizes)
-            dist.all_gather(out_r, rec)
+    stream = torch.cuda.current_stream()
+    by = partition(wl, world)
+    lwl = shard(wl, rank, world)
+    plan = ctx.plan(lwl.targets, lwl.patterns, lwl.v_th, lwl.r_novib, lwl.radii, lwl.angles, output=lwl.output)
+    plan.run(stream.cuda_stream)
+    n_pairs = plan.sync()
+    if lwl.output == "pairs":
+        plan.reserve(max(n_pairs, 1))
+    gather = ResultGather(dist, plan, wl, lwl, by, world) if dist and world > 1 else None
+    steps = args.steps if full else max(3, min(args.steps, 10))
+    total_ms, _ = time_plan(plan, stream, steps, args.warmup, flush, after=gather, clk=clk, dist=dist)
+    assert plan.sync() == n_pairs
+    value = wl.candidates * steps / (total_ms * 1e-3) / 1e9
+    out = {"value": round(value, 4), "unit": UNIT, "ms_per_step": round(total_ms / steps, 4), "steps": steps,
+           "pairs_per_step": n_pairs if world == 1 else None, "gpu_launches_per_step": plan.launches}
+    if gather:
+        out["step_collective"] = {"op": "NCCL all_gather_into_tensor of per-search "
+                                        + ("counts + first pairs" if gather.first else "counts"),
+                                  "bytes_per_rank": gather.bytes_per_rank}
 
-        out["pairs_bytes_per_rank"] = 10 * n_pairs
-        out["pairs_all_gather_ms"] = round(timed(pairs_gather), 4)
-        out["pairs_all_gather_gbs"] = round(10 * n_pairs * world / (out["pairs_all_gather_ms"] * 1e-3) / 1e9, 1)
-        assert all(torch.equal(x[:n_pairs], rec[:n_pairs]) for x in out_r)
+    # per-kernel split (events between the kernels: off in the timed steps)
+    kern, phases = [], []
+    plan.set_phase_marks(True)
+    for _ in range(min(steps, 10)):
+        flush.zero_()
+        plan.run(stream.cuda_stream)
+        kern.append(plan.last_kernel_ms())
+        phases.append(plan.last_phase_ms())
+    plan.set_phase_marks(False)
+    out["kernel_ms"] = round(statistics.median(kern), 4)
+    out["phase_ms"] = [round(statistics.median(p[i] for p in phases), 4) for i in range(3)]
+
+    e2e_steps = args.e2e_steps or (max(3, min(args.steps, 20)) if full else 3)
+    e2e_s, h2d, d2h, med, _ = time_e2e(ctx, lwl, e2e_steps, dist)
+    out["e2e"] = {"value": round(wl.candidates / e2e_s / 1e9, 4), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                  "d2h_bytes_per_step": d2h, "s_per_step": round(e2e_s, 5), "steps": e2e_steps,
+                  "api": "cvg_search (C-ABI host call, host arrays in, every result out)", "breakdown_ms": med}
+
+    if lwl.output == "pairs" and gather:
+        out["gather"] = pair_gather(dist, plan, lwl, n_pairs, world, by)
+
+    if world == 1 and full:
+        # CVG_PATH_PRUNED, reported apart: radius rows proven empty by a
+        # certified FP64 bound are decided without per-candidate evaluation
+        pp = ctx.plan(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, output=wl.output,
+                      path="pruned")
+        pp.run(stream.cuda_stream)
+        got = pp.sync()
+        if wl.output == "pairs":
+            pp.reserve(max(got, 1))
+        p_ms, _ = time_plan(pp, stream, steps, args.warmup, flush)
+        assert pp.sync() == got and (wl.output != "pairs" or got == n_pairs)
+        out["pruned"] = {"value": round(wl.candidates * steps / (p_ms * 1e-3) / 1e9, 4), "unit": UNIT,
+                         "ms_per_step": round(p_ms / steps, 4), "path": "pruned (CVG_PATH_PRUNED)",
+                         "note": "same results; counts candidates DECIDED per second (not the metric)"}
+        del pp
+    if world == 1 and full and wl.output in ("first", "counts"):
+        out["memoized"] = memoized_gpu(ctx, wl, args, dist)
+    out["_plan"] = plan
+    return out
+
+
+def memoized_gpu(ctx, wl, args, dist):
+    """CVG_PATH_MEMO through the same host call (labelled apart: distinct
+    searches only, results scattered on the device), checked equal to the
+    per-candidate path."""
+    steps = max(3, min(args.steps, 10))
+    e2e_s, h2d, d2h, med, r = time_e2e(ctx, wl, steps, dist, path="memo")
+    full = ctx.search(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, output=wl.output)
+    same = bool(np.array_equal(r["counts"], full["counts"]))
+    if wl.output == "first":
+        same &= bool(np.array_equal(r["first_idx"], full["first_idx"]) and
+                     np.array_equal(r["first_codes"], full["first_codes"]))
+    assert same, "memoized result differs from the per-candidate result"
+    out = {"wall_s": round(e2e_s, 5), "nominal_value": round(wl.candidates / e2e_s / 1e9, 4), "unit": UNIT,
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "breakdown_ms": med, "steps": steps,
+           "api": "cvg_search, path=CVG_PATH_MEMO", "identical_to_per_candidate": same,
+           "note": "MEMOIZED (not the metric): each distinct color searched once on the device, results scattered "
+                   "to its pixels; nominal candidates / wall time"}
+    if wl.output == "first":
+        out["result_sha256"] = first_hash(r["counts"], r["first_idx"], r["first_codes"])
     return out
 
 
@@ -309,173 +592,90 @@ def run_ours(args):
         with stdout_to_stderr():  # NCCL prints its version banner on stdout; the JSON line must stand alone
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
             dist.barrier()  # communicator is created here: keep its banner off stdout too
-    wl = workload(args.config)
+    wl = W.ALL[args.config]()
     ctx = cv.Context(local)
-    stream = torch.cuda.current_stream()
-
-    # ---------------- device-resident plan: `value` ----------------
-    plan = ctx.plan(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, output=wl.output)
-    plan.run(stream.cuda_stream)
-    n_pairs = plan.sync()
-    if wl.output == "pairs":
-        plan.reserve(max(n_pairs, 1))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    for _ in range(args.warmup):
-        flush.zero_()
-        plan.run(stream.cuda_stream)
-    torch.cuda.synchronize()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    with ClockSampler(local) as clk:
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        for i in range(args.steps):
-            flush.zero_()  # L2 flush outside the timed events
-            starts[i].record(stream)
-            plan.run(stream.cuda_stream)
-            ends[i].record(stream)
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = sum(step_ms)
-    got = plan.sync()
-    assert got == n_pairs, (got, n_pairs)
-    kms = plan.last_kernel_ms()  # search kernel alone (last step)
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
-    value = wl.candidates * world * args.steps / (max_ms * 1e-3) / 1e9
 
-    # per-launch kernel time over the timed steps: events inside the plan
-    # cover only the search kernel; re-measure a few steps for the roofline
-    # ---- CVG_PATH_PRUNED, reported apart (not the headline): whole radius
-    # rows decided by a certified FP64 bound, so its candidates/s counts
-    # candidates decided, not each one evaluated ----
-    pruned = None
-    if wl.output in ("pairs", "counts", "first") and rank == 0 and world == 1:
-        pp = ctx.plan(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, output=wl.output,
-                      path="pruned")
-        pp.run(stream.cuda_stream)
-        got_p = pp.sync()
-        if wl.output == "pairs":
-            pp.reserve(max(got_p, 1))
-        for _ in range(args.warmup):
-            flush.zero_()
-            pp.run(stream.cuda_stream)
-        torch.cuda.synchronize()
-        p_ms = []
-        for _ in range(args.steps):
-            flush.zero_()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            pp.run(stream.cuda_stream)
-            b.record(stream)
-            torch.cuda.synchronize()
-            p_ms.append(a.elapsed_time(b))
-        assert pp.sync() == got_p and (wl.output != "pairs" or got_p == n_pairs)
-        pruned = {"value": round(wl.candidates * args.steps / (sum(p_ms) * 1e-3) / 1e9, 4), "unit": UNIT,
-                  "ms_per_step": round(sum(p_ms) / args.steps, 4), "path": "pruned (CVG_PATH_PRUNED)",
-                  "note": "same results; radius rows proven empty by a certified FP64 bound are decided "
-                          "without per-candidate evaluation, so this counts candidates decided per second"}
-        del pp
+    clk = ClockSampler(local)  # sampled during the headline's timed steps
+    head = measure_config(cv, ctx, wl, args, rank, world, local, dist, flush, clk=clk)
+    head.pop("_plan")
 
-    kern, phases = [], []
-    plan.set_phase_marks(True)  # events between the kernels (off in the timed steps: they block the PDL overlap)
-    for _ in range(min(args.steps, 20)):
-        flush.zero_()
-        plan.run(stream.cuda_stream)
-        kern.append(plan.last_kernel_ms())
-        phases.append(plan.last_phase_ms())
-    kern_ms = statistics.median(kern)
-    phase_ms = [statistics.median(p[i] for p in phases) for i in range(3)]
-
-    # ---------------- e2e through the C-ABI host call ----------------
-    e2e_steps = args.e2e_steps or max(3, min(args.steps, 20))
-    # warm-up: two calls, so that the shape-hinted buffers of the second call
-    # (sized from the first call's pair total) are allocated before timing
-    for _ in range(2):
-        res = ctx.search(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, output=wl.output)
-    assert int(res["n_pairs"]) == n_pairs
-    h2d = int(res["stats"]["h2d_bytes"])
-    d2h = int(res["stats"]["d2h_bytes"])
-    del res
-    if dist:
-        dist.barrier()
-    e2e_times, phases = [], []
-    for _ in range(e2e_steps):
-        t0 = time.perf_counter()
-        r = ctx.search(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, output=wl.output)
-        _ = int(r["n_pairs"])
-        e2e_times.append(time.perf_counter() - t0)
-        phases.append({k: r["stats"][k] for k in ("prep_ms", "h2d_ms", "device_ms", "d2h_ms", "total_ms")})
-        del r
-    phase_med = {k: round(statistics.median(p[k] for p in phases), 4) for k in phases[0]}
-    e2e_s = sum(e2e_times)
-    t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-    gather = None
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        gather = time_gather(dist, plan, wl, n_pairs, world, stream)
-    e2e_value = wl.candidates * world * e2e_steps / float(t.item()) / 1e9
+    others = {}
+    if world == 1 and not args.no_others:
+        for name in CONFIGS:
+            if name == wl.name:
+                continue
+            owl = W.ALL[name]()
+            o = measure_config(cv, ctx, owl, args, rank, world, local, dist, flush, full=False)
+            o.pop("_plan")
+            p1 = o["phase_ms"][0] if o["phase_ms"][0] > 0 else o["kernel_ms"]
+            o["roofline_frac_phase1"] = None  # filled below with the measured peak
+            o["_p1"] = p1
+            o["candidates_per_step"] = owl.candidates
+            others[name] = o
 
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
 
-    # ---------------- roofline ----------------
-    # algorithmic output bytes: 10 B per pair + 8 B count per search (pairs);
-    # count + first pair (8 + 4 + 6 B) per search (first)
-    out_bytes = n_pairs * 10 + wl.n_searches * 8 if wl.output == "pairs" else wl.n_searches * 18
+    # ---------------- roofline (dominant kernel: phase 1) ----------------
     peak_lane, _ = cv.measure_ffma_peak(local)
-    # dominant kernel: phase 1 decides every candidate (the W = 50 algorithmic
-    # FP32 instructions of SURVEY §8d); the whole 3-kernel step is reported too
-    p1_ms = phase_ms[0] if phase_ms[0] > 0 else kern_ms
-    achieved = wl.candidates * W_INSTR / (p1_ms * 1e-3) / 1e12
     peak = peak_lane / 1e12
-    step_achieved = wl.candidates * W_INSTR / (kern_ms * 1e-3) / 1e12
+    p1_ms = head["phase_ms"][0] if head["phase_ms"][0] > 0 else head["kernel_ms"]
+    # per launch on this rank's share (N > 1: the local shard)
+    lcand = shard(wl, rank, world).candidates
+    achieved = lcand * W_INSTR / (p1_ms * 1e-3) / 1e12
+    step_achieved = lcand * W_INSTR / (head["kernel_ms"] * 1e-3) / 1e12
+    n_pairs = head.get("pairs_per_step") or 0
+    out_bytes = n_pairs * 10 + wl.n_searches * 8 if wl.output == "pairs" else wl.n_searches * 18
     roofline = {"bound": "fp32_issue", "kernel": "phase1_kernel", "achieved": round(achieved, 3),
                 "peak": round(peak, 3), "unit": "Tinstr/s", "frac": round(achieved / peak, 4) if peak else None,
                 "traffic": ncu_traffic(wl.name), "kernel_ms": round(p1_ms, 4),
-                "step_kernels_ms": {"phase1": round(phase_ms[0], 4), "scan": round(phase_ms[1], 4),
-                                    "emit": round(phase_ms[2], 4), "total": round(kern_ms, 4)},
+                "step_kernels_ms": {"phase1": head["phase_ms"][0], "scan": head["phase_ms"][1],
+                                    "emit": head["phase_ms"][2], "total": head["kernel_ms"]},
                 "step_frac": round(step_achieved / peak, 4) if peak else None,
                 "instr_per_candidate": W_INSTR,
                 "peak_source": "FFMA issue microbenchmark measured in this run (cvg_measure_ffma_peak)",
                 "hbm": {"bytes_per_launch": out_bytes,
-                        "achieved_gbs": round(out_bytes / (kern_ms * 1e-3) / 1e9, 2)}}
+                        "achieved_gbs": round(out_bytes / (head["kernel_ms"] * 1e-3) / 1e9, 2)}}
+    for name, o in others.items():
+        o["roofline_frac_phase1"] = round(o["candidates_per_step"] * W_INSTR / (o.pop("_p1") * 1e-3) / 1e12 / peak, 4) \
+            if peak else None
 
     # ---------------- CPU baseline (reference, bounded sample) ----------------
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         try:
-            cwl, sample = cpu_sample(wl)
-            v, sec, cores, pairs, _ = cpu_reference_arm(cwl, 2, 1)
-            cpu = {"value": round(v, 6), "unit": UNIT, "cores": cores, "kind": "reference",
-                   "sample": f"{sample}, mean of 2 steps after 1 warm-up, workers={cores}, {cpu_model()}",
-                   "pairs": pairs, "s_per_step": round(sec, 4)}
-            if cwl is wl:
+            cpu, full, pairs = cpu_baseline(wl)
+            if full:
                 assert pairs == n_pairs, (pairs, n_pairs)
+            if "memoized" in cpu and "memoized" in head and "result_sha256" in head["memoized"]:
+                # same per-pixel result on both sides
+                assert cpu["memoized"]["result_sha256"] == head["memoized"]["result_sha256"]
+            for name, o in others.items():
+                c, _, _ = cpu_baseline(W.ALL[name]())
+                c.pop("memoized", None)
+                o["cpu_baseline"] = {k: c[k] for k in ("value", "unit", "cores", "sample")}
         except FileNotFoundError as e:
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
+    steps = head["steps"]
     out = {
-        "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(max_ms / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64repair", "data": "synthetic",
-        "config": config_dict(wl, world, {"pairs_per_step": n_pairs}),
-        "e2e": {"value": round(e2e_value, 4), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "s_per_step": round(float(t.item()) / e2e_steps, 5), "steps": e2e_steps,
-                "api": "cvg_search (C-ABI host call)", "breakdown_ms": phase_med},
-        "gpu_launches": plan.launches * args.steps,
-        **({"gather": gather} if gather else {}),
-        **({"pruned": pruned} if pruned else {}),
+        "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32+f64repair",
+        "data": "synthetic", "config": config_dict(wl, world),
+        "e2e": head["e2e"],
+        "gpu_launches": head["gpu_launches_per_step"] * steps,
+        **({"step_collective": head["step_collective"]} if "step_collective" in head else {}),
+        **({"gather": head["gather"]} if "gather" in head else {}),
+        **({"memoized": head["memoized"]} if "memoized" in head else {}),
+        **({"pruned": head["pruned"]} if "pruned" in head else {}),
         "clocks": clk.summary(),
         "roofline": roofline,
         "cpu_baseline": cpu,
+        **({"configs": others} if others else {}),
     }
     print(json.dumps(out), flush=True)
     if dist:
@@ -484,6 +684,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3 (timing rules)")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -62,6 +62,12 @@ extern "C" {
 #define CVG_PATH_PRUNED 3 /* FAST, plus whole radius rows decided by a certified FP64 bound
                              (TargetSwing, aligned grids): same results; candidates of a
                              pruned row are decided without being evaluated one by one */
+#define CVG_PATH_MEMO 4   /* COUNTS / FIRST only: FAST over the DISTINCT searches of the batch
+                             (target, pattern, v_th, r_novib), each search's count / first pair
+                             then scattered from its representative on the device.  Same
+                             results (they depend only on those four values); a per-pixel batch
+                             of 8.3M pixels with ~22K distinct colors evaluates ~22K searches.
+                             Reported apart from the per-candidate figures (memoized). */
 
 typedef struct cvg_ctx cvg_ctx;
 typedef struct cvg_plan cvg_plan;
@@ -93,7 +99,9 @@ typedef struct {
 } cvg_search_desc;
 
 /*
- * Host-side result (library-owned; release with cvg_result_free).
+ * Host-side result (library-owned; release with cvg_result_free).  Its
+ * buffers are pinned blocks of the context's pool; a result may outlive its
+ * context (cvg_destroy hands the blocks of live results over to them).
  * Pair p: idx[p] = k * n_angles + m (radius index k, angle index m),
  * codes[6p .. 6p+5] = plus r,g,b then minus r,g,b.  Pairs of search s are
  * [offsets[s], offsets[s+1]).  FIRST mode fills first_idx/first_codes instead
@@ -161,6 +169,11 @@ CVG_API int cvg_plan_device_outputs(cvg_plan* plan, uint64_t** counts, uint32_t*
  * For collectives on framework tensors (e.g. NCCL all_gather of results). */
 CVG_API int cvg_plan_copy_outputs(cvg_plan* plan, uint64_t* counts, uint32_t* idx, uint8_t* codes,
                                   uint64_t n_pairs, void* stream);
+/* FIRST plans: copies the last run's per-search first pair (u32 idx, 6 code
+ * bytes) into caller device buffers, enqueued on `stream`. */
+CVG_API int cvg_plan_copy_first(cvg_plan* plan, uint32_t* first_idx, uint8_t* first_codes, void* stream);
+/* searches the plan's kernels evaluate (MEMO: the distinct ones; else all) */
+CVG_API int32_t cvg_plan_evaluated_searches(const cvg_plan* plan);
 /* device time (ms) of the search kernel(s) of the plan's last completed run */
 CVG_API int cvg_plan_last_kernel_ms(cvg_plan* plan, float* ms);
 /* per-kernel device time (ms) of the last run: phase 1 (candidate decisions),

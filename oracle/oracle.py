@@ -188,16 +188,19 @@ class Reference(_Lib):
         f = self.lib.cvr_search_memo
         f.restype = C.c_int64
         f.argtypes = [C.c_int64, _ip, C.c_int, C.c_double, C.c_double, _dp, C.c_int, _dp, C.c_int, C.c_int,
-                      _u64p, _up, _bp]
+                      C.c_int, _u64p, _up, _bp]
         self.lib.cvr_batch_search_addr.restype = C.c_void_p
 
     def batch_search_addr(self) -> int:
         """Address colorvibe::batch_search resolves to inside this library."""
         return self.lib.cvr_batch_search_addr()
 
-    def search_memo(self, rgb, pattern_bits: int, v_th: float, r_novib: float, radii, angles, threads: int = 0):
-        """Per-pixel batch memoized by color:
-        (counts u64[n], first_idx u32[n], first_codes u8[n, 6], n_unique)."""
+    def search_memo(self, rgb, pattern_bits: int, v_th: float, r_novib: float, radii, angles, threads: int = 0,
+                    memo: bool = True):
+        """Per-pixel batch on an outer pool of `threads` (reference
+        batch_search with workers = 1 per pixel), memoized by color
+         unless memo=False:
+        (counts u64[n], first_idx u32[n], first_codes u8[n, 6], n_searched)."""
         t = np.ascontiguousarray(rgb, np.int32).reshape(-1, 3)
         r = np.ascontiguousarray(radii, np.float64)
         a = np.ascontiguousarray(angles, np.float64)
@@ -207,7 +210,7 @@ class Reference(_Lib):
         codes = np.zeros((n, 6), np.uint8)
         u = self.lib.cvr_search_memo(n, _ptr(t, _ip), int(pattern_bits), float(v_th), float(r_novib),
                                      _ptr(r, _dp), len(r), _ptr(a, _dp), len(a), int(threads or os.cpu_count() or 1),
-                                     _ptr(counts, _u64p), _ptr(first, _up), _ptr(codes, _bp))
+                                     int(bool(memo)), _ptr(counts, _u64p), _ptr(first, _up), _ptr(codes, _bp))
         if u < 0:
             raise ValueError(self.last_error())
         return counts, first, codes, int(u)

@@ -175,13 +175,15 @@ void* cvr_batch_search_addr() {
 // batch_search (workers = 1 per call) on an outer pool of `threads`
 // std::threads, then scatter count + first canonical pair to every pixel.
 // Writes counts[n], first_idx[n] (0xFFFFFFFF if none), first_codes[6n];
-// returns the number of unique colors, or a negative error.
+// returns the number of unique colors, or a negative error.  memo = 0: no
+// dedup, every pixel is searched (the same outer pool; the per-candidate
+// CPU rate of the per-pixel batch).
 int64_t cvr_search_memo(int64_t n, const int32_t* rgb, int pattern_bits, double v_th,
                         double r_novib, const double* radii, int nr, const double* angles, int na,
-                        int threads, uint64_t* counts, uint32_t* first_idx, uint8_t* first_codes) {
+                        int threads, int memo, uint64_t* counts, uint32_t* first_idx, uint8_t* first_codes) {
     try {
         const VibrationGrid grid = grid_of(radii, nr, angles, na);
-        std::vector<int32_t> slot(size_t(1) << 24, -1);  // key = rgb
+        std::vector<int32_t> slot(memo ? size_t(1) << 24 : 0, -1);  // key = rgb
         std::vector<uint32_t> keys;
         std::vector<int32_t> of(static_cast<size_t>(n));
         for (int64_t i = 0; i < n; ++i) {
@@ -189,6 +191,11 @@ int64_t cvr_search_memo(int64_t n, const int32_t* rgb, int pattern_bits, double 
             if ((c[0] | c[1] | c[2]) & ~0xff) throw std::invalid_argument("color channel out of range");
             const uint32_t key = (static_cast<uint32_t>(c[0]) << 16) | (static_cast<uint32_t>(c[1]) << 8) |
                                  static_cast<uint32_t>(c[2]);
+            if (!memo) {
+                of[static_cast<size_t>(i)] = static_cast<int32_t>(keys.size());
+                keys.push_back(key);
+                continue;
+            }
             int32_t& u = slot[key];
             if (u < 0) {
                 u = static_cast<int32_t>(keys.size());

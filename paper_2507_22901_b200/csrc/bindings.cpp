@@ -29,9 +29,13 @@ void check(int status) {
     throw std::runtime_error(msg);
 }
 
-// Owns a cvg_result; NumPy arrays view its buffers (zero copy).
+struct Context;
+
+// Owns a cvg_result; NumPy arrays view its buffers (zero copy).  It keeps
+// the context alive: the buffers are blocks of the context's pinned pool.
 struct ResultHolder {
     cvg_result r{};
+    std::shared_ptr<Context> owner;
     ~ResultHolder() { cvg_result_free(&r); }
 };
 
@@ -47,7 +51,8 @@ int path_mode(const std::string& s) {
     if (s == "exact") return CVG_PATH_EXACT;
     if (s == "audit") return CVG_PATH_AUDIT;
     if (s == "pruned") return CVG_PATH_PRUNED;
-    throw std::invalid_argument("path must be 'fast', 'exact' or 'audit'");
+    if (s == "memo") return CVG_PATH_MEMO;
+    throw std::invalid_argument("path must be 'fast', 'exact', 'audit', 'pruned' or 'memo'");
 }
 
 using I32 = py::array_t<int32_t, py::array::c_style | py::array::forcecast>;
@@ -333,6 +338,7 @@ PYBIND11_MODULE(_core, m) {
                 Desc d(std::move(rgb), std::move(bits), std::move(vth), std::move(rn), std::move(radii),
                        std::move(angles), mode, basis, white, output, path);
                 auto h = std::make_shared<ResultHolder>();
+                h->owner = self;
                 int st;
                 {
                     py::gil_scoped_release nogil;
@@ -678,6 +684,7 @@ PYBIND11_MODULE(_core, m) {
         .def("reserve", [](Plan& p, uint64_t cap) { check(cvg_plan_reserve(p.plan, cap)); })
         .def("fetch", [](Plan& p) {
             auto h = std::make_shared<ResultHolder>();
+            h->owner = p.ctx;
             int st;
             {
                 py::gil_scoped_release nogil;
@@ -707,6 +714,13 @@ PYBIND11_MODULE(_core, m) {
                                              n_pairs, reinterpret_cast<void*>(stream)));
              },
              py::arg("counts"), py::arg("idx"), py::arg("codes"), py::arg("n_pairs"), py::arg("stream") = 0)
+        .def("copy_first",
+             [](Plan& p, uintptr_t idx, uintptr_t codes, uintptr_t stream) {
+                 check(cvg_plan_copy_first(p.plan, reinterpret_cast<uint32_t*>(idx), reinterpret_cast<uint8_t*>(codes),
+                                           reinterpret_cast<void*>(stream)));
+             },
+             py::arg("idx"), py::arg("codes"), py::arg("stream") = 0)
+        .def_property_readonly("evaluated_searches", [](const Plan& p) { return cvg_plan_evaluated_searches(p.plan); })
         .def("device_outputs", [](Plan& p) {
             uint64_t* counts = nullptr;
             uint32_t* idx = nullptr;

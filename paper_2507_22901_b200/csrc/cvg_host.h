@@ -402,6 +402,15 @@ struct Pool {
         cached += it->second;
     }
 
+    // Hands an outstanding block to its holder: the pool forgets it (its
+    // destructor will not free it); the holder frees it with the raw API.
+    bool detach(void* p) {
+        auto it = sizes.find(p);
+        if (it == sizes.end()) return false;
+        sizes.erase(it);
+        return true;
+    }
+
     void trim() {
         for (auto& kv : free_blocks) {
             if (device) cudaFree(kv.second); else cudaFreeHost(kv.second);
@@ -473,6 +482,17 @@ struct cvg_plan {
     uint64_t* h_counts = nullptr;  // pinned per-search counts for cvg_plan_sync
     int32_t n_unique = 0;
     double t_prep_end = 0, t_upload_end = 0;
+    // CVG_PATH_MEMO: the kernels run the n_exec distinct searches (records in
+    // representative order); scatter_kernel expands their counts / first
+    // pairs to all n searches through map (= sc_index, device)
+    bool memo = false;
+    int32_t n_exec = 0;
+    const uint32_t* d_map = nullptr;
+    void* d_memo = nullptr;
+    // where the per-search results of a run land (args.* unless memo)
+    unsigned long long* res_counts = nullptr;
+    uint32_t* res_first_idx = nullptr;
+    uint8_t* res_first_codes = nullptr;
 };
 
 namespace cvg::host {

@@ -24,6 +24,9 @@ cudaError_t launch_emit(const LaunchArgs& a, int mode, int path, int grid, cudaS
 // dynamic shared memory size on the current device (call before launching).
 int search_blocks_per_sm(int mode, int out, int path);
 cudaError_t launch_first_codes(const LaunchArgs& a, cudaStream_t st);
+// CVG_PATH_MEMO: out[s] = in[map[s]] for counts (and first pairs when fi_in is set), s < n.
+cudaError_t launch_scatter(const uint32_t* map, int n, const unsigned long long* counts_in, const uint32_t* fi_in,
+                           const uint8_t* fc_in, unsigned long long* counts, uint32_t* fi, uint8_t* fc, cudaStream_t st);
 size_t search_smem_bytes();
 
 // Codec passes (cvg_codec.cu).  Block positions xy[2i], xy[2i+1]; colors

@@ -1406,6 +1406,25 @@ __global__ void first_codes_kernel(const LaunchArgs A) {
     }
 }
 
+// CVG_PATH_MEMO epilogue: every search takes the result of its distinct
+// representative (results depend only on target, pattern and thresholds).
+__global__ void scatter_kernel(const uint32_t* __restrict__ map, int n, const unsigned long long* __restrict__ counts_in,
+                               const uint32_t* __restrict__ fi_in, const uint8_t* __restrict__ fc_in,
+                               unsigned long long* __restrict__ counts, uint32_t* __restrict__ fi,
+                               uint8_t* __restrict__ fc) {
+    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gridDim.x * blockDim.x) {
+        const uint32_t u = __ldg(&map[s]);
+        counts[s] = __ldg(&counts_in[u]);
+        if (fi_in) {
+            fi[s] = __ldg(&fi_in[u]);
+            const uint8_t* a = fc_in + 6 * static_cast<size_t>(u);
+            uint8_t* b = fc + 6 * static_cast<size_t>(s);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) b[q] = __ldg(&a[q]);
+        }
+    }
+}
+
 // FP32 issue-rate microbenchmark: 8 independent FFMA chains per thread.
 __global__ void ffma_peak_kernel(float* out, int iters, float a, float b) {
     float x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3;
@@ -1551,6 +1570,15 @@ cudaError_t launch_first_codes(const LaunchArgs& a, cudaStream_t st) {
     const int blocks = (a.n_searches + threads - 1) / threads;
     if (blocks == 0) return cudaSuccess;
     first_codes_kernel<<<blocks, threads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scatter(const uint32_t* map, int n, const unsigned long long* counts_in, const uint32_t* fi_in,
+                           const uint8_t* fc_in, unsigned long long* counts, uint32_t* fi, uint8_t* fc, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const int threads = 256;
+    const int blocks = std::min((n + threads - 1) / threads, 148 * 8);
+    scatter_kernel<<<blocks, threads, 0, st>>>(map, n, counts_in, fi_in, fc_in, counts, fi, fc);
     return cudaGetLastError();
 }
 

@@ -229,7 +229,9 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     p->ctx = ctx;
     p->mode = search_mode(d);
     p->out = d->output;
-    p->path = d->path == CVG_PATH_PRUNED ? CVG_PATH_FAST : d->path;  // pruning is a flag of the FAST path
+    // pruning is a flag of the FAST path; so is memoization (distinct searches only)
+    p->path = (d->path == CVG_PATH_PRUNED || d->path == CVG_PATH_MEMO) ? CVG_PATH_FAST : d->path;
+    p->memo = d->path == CVG_PATH_MEMO && !pre;
     p->n = d->n_searches;
     p->nr = d->n_radii;
     p->na = d->n_angles;
@@ -239,8 +241,6 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     if (p->empty) return CVG_OK;  // search.cpp:409-411
 
     const uint32_t tps = static_cast<uint32_t>((cps + cvg::kTile - 1) / cvg::kTile);
-    const uint64_t n_tiles = static_cast<uint64_t>(tps) * static_cast<uint64_t>(p->n);
-    if (n_tiles >= (1ull << 28)) return fail(CVG_EINVAL, "batch too large for one plan (split the searches)");
 
     // ---- host tables ----
     // Per-search constants, deduplicated: searches with the same (target,
@@ -257,6 +257,12 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     }
     mark("dedup");
     p->n_unique = static_cast<int32_t>(n_sc);
+    if (p->memo && sc_index.empty()) p->memo = false;  // all distinct: nothing to memoize
+    // the searches the kernels run: all of them, or (memo) one per record
+    p->n_exec = p->memo ? static_cast<int32_t>(n_sc) : p->n;
+    const uint64_t n_tiles = static_cast<uint64_t>(tps) * static_cast<uint64_t>(p->n_exec);
+    if (n_tiles >= (1ull << 28)) return fail(CVG_EINVAL, "batch too large for one plan (split the searches)");
+    auto exec_bits = [&](int32_t i) { return d->pattern_bits[p->memo ? uniq[i] : i] & 7; };
     GridTables own;
     if (!grid) {
         own = make_grid_tables(d);
@@ -276,9 +282,9 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         const char* e = std::getenv("CVG_CLAIM_GROUP");  // A/B switch; default on
         return !e || std::atoi(e) != 0;
     }();
-    if (group_claims && p->mode == cvg::kModeBand && p->n > 1 && !uniform) {
+    if (group_claims && p->mode == cvg::kModeBand && p->n_exec > 1 && !uniform) {
         std::array<uint32_t, 4> bucket{};
-        for (int32_t i = 0; i < p->n; ++i) ++bucket[__builtin_popcount(d->pattern_bits[i] & 7)];
+        for (int32_t i = 0; i < p->n_exec; ++i) ++bucket[__builtin_popcount(exec_bits(i))];
         int kinds = 0;
         for (uint32_t b : bucket) kinds += b > 0;
         if (kinds > 1) {
@@ -287,8 +293,8 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
             group_end[1] = bucket[1] + bucket[2];
             group_end[2] = bucket[1] + bucket[2] + bucket[3];
             std::array<uint32_t, 4> next{0, 0, group_end[0], group_end[1]};
-            claim.resize(p->n);
-            for (int32_t i = 0; i < p->n; ++i) claim[next[__builtin_popcount(d->pattern_bits[i] & 7)]++] = i;
+            claim.resize(p->n_exec);
+            for (int32_t i = 0; i < p->n_exec; ++i) claim[next[__builtin_popcount(exec_bits(i))]++] = i;
         }
     }
 
@@ -345,7 +351,8 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     LaunchArgs& A = p->args;
     std::memset(&A, 0, sizeof(A));
     A.sc = at<const SearchConst>(p->d_const, o_sc);
-    A.sc_index = sc_index.empty() ? nullptr : at<const uint32_t>(p->d_const, o_si);
+    A.sc_index = sc_index.empty() || p->memo ? nullptr : at<const uint32_t>(p->d_const, o_si);
+    p->d_map = p->memo ? at<const uint32_t>(p->d_const, o_si) : nullptr;
     A.claim_order = claim.empty() ? nullptr : at<const uint32_t>(p->d_const, o_co);
     for (int g = 0; g < 3; ++g) A.group_end[g] = group_end[g];
     A.radii_d = at<const double>(p->d_const, o_rd);
@@ -363,7 +370,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     mark("upload");
 
     for (int i = 0; i < 9; ++i) A.minv[i] = kXyzToRgb.m[i / 3][i % 3];
-    A.n_searches = p->n;
+    A.n_searches = p->n_exec;
     A.nr = p->nr;
     A.na = p->na;
     A.aligned = (p->na % 32) == 0;
@@ -388,7 +395,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     Layout W;
     const size_t o_st = W.take(sizeof(unsigned long long) * scan_blocks);
     const size_t o_tk = W.take(sizeof(unsigned int) * 8);
-    const size_t o_ct = W.take(sizeof(unsigned long long) * p->n);
+    const size_t o_ct = W.take(sizeof(unsigned long long) * p->n_exec);
     const size_t o_ss = W.take(sizeof(cvg::Stats));
     const size_t o_to = W.take(sizeof(unsigned long long));  // stats+total read back as one ChunkTail
     p->work_bytes = W.off;  // memset span
@@ -406,7 +413,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.total = at<unsigned long long>(p->d_work, o_to);
     A.worklist = at<uint32_t>(p->d_work, o_wl);
     A.search_begin = 0;
-    A.range_searches = static_cast<uint32_t>(p->n);
+    A.range_searches = static_cast<uint32_t>(p->n_exec);
     A.tile_begin = 0;
     A.base_offset = nullptr;
     A.grand_total = nullptr;
@@ -417,13 +424,29 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     }
     if (p->out == cvg::kOutFirst) {
         Layout F;
-        const size_t o_fi = F.take(sizeof(uint32_t) * p->n);
-        const size_t o_fc = F.take(static_cast<size_t>(p->n) * 6);
+        const size_t o_fi = F.take(sizeof(uint32_t) * p->n_exec);
+        const size_t o_fc = F.take(static_cast<size_t>(p->n_exec) * 6);
         p->first_bytes = F.off;
         p->d_first = ctx->dev.alloc(p->first_bytes);
         if (!p->d_first) return fail(CVG_ENOMEM, "device allocation of the first-pair buffer failed");
         A.first_idx = at<uint32_t>(p->d_first, o_fi);
         A.first_codes = at<uint8_t>(p->d_first, o_fc);
+    }
+    p->res_counts = A.counts;
+    p->res_first_idx = A.first_idx;
+    p->res_first_codes = A.first_codes;
+    if (p->memo) {
+        // every search's result, scattered from its record's
+        Layout M;
+        const size_t o_mc = M.take(sizeof(unsigned long long) * p->n);
+        const bool first = p->out == cvg::kOutFirst;
+        const size_t o_mi = M.take(first ? sizeof(uint32_t) * p->n : 0);
+        const size_t o_mf = M.take(first ? static_cast<size_t>(p->n) * 6 : 0);
+        p->d_memo = ctx->dev.alloc(M.off);
+        if (!p->d_memo) return fail(CVG_ENOMEM, "device allocation of the memoized results failed");
+        p->res_counts = at<unsigned long long>(p->d_memo, o_mc);
+        p->res_first_idx = first ? at<uint32_t>(p->d_memo, o_mi) : nullptr;
+        p->res_first_codes = first ? at<uint8_t>(p->d_memo, o_mf) : nullptr;
     }
 
     const uint64_t want = (n_tiles + cvg::kWarpsPerBlock - 1) / cvg::kWarpsPerBlock;
@@ -472,6 +495,8 @@ void plan_release(cvg_plan* p) {
     p->ctx->dev.release(p->d_work);
     p->ctx->dev.release(p->d_first);
     p->ctx->dev.release(p->d_scratch);
+    p->ctx->dev.release(p->d_memo);
+    p->d_memo = nullptr;
     if (p->stage) cudaStreamSynchronize(p->ctx->stream);  // the constant upload may still be in flight
     for (cudaEvent_t* ev : {&p->ev0, &p->ev1, &p->marks[0], &p->marks[1], &p->marks[2], &p->marks[3]}) {
         if (*ev) p->ctx->events.push_back(*ev);
@@ -488,11 +513,17 @@ int plan_enqueue(cvg_plan* p, cudaStream_t st) {
     p->ran = true;
     if (p->empty) return CVG_OK;
     CVG_CUDA(cudaMemsetAsync(p->d_work, 0, p->work_bytes, st));
-    if (p->out == cvg::kOutFirst) CVG_CUDA(cudaMemsetAsync(p->d_first, 0xff, static_cast<size_t>(p->n) * 4, st));
+    if (p->out == cvg::kOutFirst) CVG_CUDA(cudaMemsetAsync(p->d_first, 0xff, static_cast<size_t>(p->n_exec) * 4, st));
     CVG_CUDA(cudaEventRecord(p->ev0, st));
     p->marked = p->phase_marks;
     CVG_CUDA(cvg::launch_search(p->args, p->mode, p->out, p->path, p->grid, st, p->marked ? p->marks : nullptr));
     if (p->out == cvg::kOutFirst) CVG_CUDA(cvg::launch_first_codes(p->args, st));
+    if (p->memo) {
+        const bool first = p->out == cvg::kOutFirst;
+        CVG_CUDA(cvg::launch_scatter(p->d_map, p->n, p->args.counts, first ? p->args.first_idx : nullptr,
+                                     first ? p->args.first_codes : nullptr, p->res_counts, p->res_first_idx,
+                                     p->res_first_codes, st));
+    }
     CVG_CUDA(cudaEventRecord(p->ev1, st));
     return CVG_OK;
 }
@@ -503,7 +534,7 @@ int plan_collect(cvg_plan* p, uint64_t* counts, HostStats& hs) {
         return CVG_OK;
     }
     cudaStream_t st = p->last_stream;
-    CVG_CUDA(cudaMemcpyAsync(counts, p->args.counts, sizeof(uint64_t) * p->n, cudaMemcpyDeviceToHost, st));
+    CVG_CUDA(cudaMemcpyAsync(counts, p->res_counts, sizeof(uint64_t) * p->n, cudaMemcpyDeviceToHost, st));
     CVG_CUDA(cudaMemcpyAsync(&hs.st, p->args.stats, sizeof(cvg::Stats), cudaMemcpyDeviceToHost, st));
     CVG_CUDA(cudaStreamSynchronize(st));
     CVG_CUDA(cudaEventElapsedTime(&hs.ms, p->ev0, p->ev1));
@@ -589,15 +620,17 @@ int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
         r->first_codes = static_cast<uint8_t*>(ctx->host.alloc(n * 6));
         if (!r->first_idx || !r->first_codes) return fail(CVG_ENOMEM, "pinned host allocation failed");
         cudaStream_t st = p->last_stream;
-        CVG_CUDA(cudaMemcpyAsync(r->first_idx, p->args.first_idx, n * 4, cudaMemcpyDeviceToHost, st));
-        CVG_CUDA(cudaMemcpyAsync(r->first_codes, p->args.first_codes, n * 6, cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaMemcpyAsync(r->first_idx, p->res_first_idx, n * 4, cudaMemcpyDeviceToHost, st));
+        CVG_CUDA(cudaMemcpyAsync(r->first_codes, p->res_first_codes, n * 6, cudaMemcpyDeviceToHost, st));
         CVG_CUDA(cudaStreamSynchronize(st));
     }
     return CVG_OK;
 }
 
 // cvg_result keeps a pointer to its context in a side table so that
-// cvg_result_free can return pinned blocks to the right pool.
+// cvg_result_free can return pinned blocks to the right pool.  A result may
+// outlive its context: cvg_destroy detaches the blocks still held by results
+// (owner nullptr) and cvg_result_free then releases them with cudaFreeHost.
 std::mutex g_owner_mu;
 std::map<const void*, cvg_ctx*> g_owner;
 
@@ -661,9 +694,10 @@ void cvg_destroy(cvg_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     {
+        // results still alive keep their pinned blocks (they outlive the pool)
         std::lock_guard<std::mutex> lk(g_owner_mu);
-        for (auto it = g_owner.begin(); it != g_owner.end();) {
-            it = it->second == ctx ? g_owner.erase(it) : std::next(it);
+        for (auto& kv : g_owner) {
+            if (kv.second == ctx && ctx->host.detach(const_cast<void*>(kv.first))) kv.second = nullptr;
         }
     }
     cudaStreamSynchronize(ctx->copy_stream);
@@ -758,7 +792,7 @@ int cvg_plan_copy_outputs(cvg_plan* p, uint64_t* counts, uint32_t* idx, uint8_t*
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (counts) {
-        CVG_CUDA(cudaMemcpyAsync(counts, p->args.counts, sizeof(uint64_t) * p->n, cudaMemcpyDeviceToDevice, st));
+        CVG_CUDA(cudaMemcpyAsync(counts, p->res_counts, sizeof(uint64_t) * p->n, cudaMemcpyDeviceToDevice, st));
     }
     if (idx && n_pairs) CVG_CUDA(cudaMemcpyAsync(idx, p->d_out_idx, 4 * n_pairs, cudaMemcpyDeviceToDevice, st));
     if (codes && n_pairs) CVG_CUDA(cudaMemcpyAsync(codes, p->d_out_codes, 6 * n_pairs, cudaMemcpyDeviceToDevice, st));
@@ -767,7 +801,7 @@ int cvg_plan_copy_outputs(cvg_plan* p, uint64_t* counts, uint32_t* idx, uint8_t*
 
 int cvg_plan_device_outputs(cvg_plan* p, uint64_t** counts, uint32_t** idx, uint8_t** codes, uint64_t* capacity) {
     if (!p) return fail(CVG_EINVAL, "null plan");
-    if (counts) *counts = reinterpret_cast<uint64_t*>(p->args.counts);
+    if (counts) *counts = reinterpret_cast<uint64_t*>(p->res_counts);
     if (idx) *idx = static_cast<uint32_t*>(p->d_out_idx);
     if (codes) *codes = static_cast<uint8_t*>(p->d_out_codes);
     if (capacity) *capacity = p->capacity;
@@ -785,6 +819,21 @@ int cvg_plan_last_kernel_ms(cvg_plan* p, float* ms) {
 }
 
 uint64_t cvg_plan_input_bytes(const cvg_plan* p) { return p ? p->input_bytes : 0; }
+
+int32_t cvg_plan_evaluated_searches(const cvg_plan* p) { return p ? (p->empty ? 0 : p->n_exec) : 0; }
+
+int cvg_plan_copy_first(cvg_plan* p, uint32_t* first_idx, uint8_t* first_codes, void* stream) {
+    if (!p) return fail(CVG_EINVAL, "null plan");
+    if (p->out != cvg::kOutFirst) return fail(CVG_EINVAL, "not a FIRST plan");
+    std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
+    if (int e = ensure_device(p->ctx)) return e;
+    if (p->empty || !p->n) return CVG_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t n = static_cast<size_t>(p->n);
+    if (first_idx) CVG_CUDA(cudaMemcpyAsync(first_idx, p->res_first_idx, 4 * n, cudaMemcpyDeviceToDevice, st));
+    if (first_codes) CVG_CUDA(cudaMemcpyAsync(first_codes, p->res_first_codes, 6 * n, cudaMemcpyDeviceToDevice, st));
+    return CVG_OK;
+}
 
 int cvg_plan_last_phase_ms(cvg_plan* p, float* phase1_ms, float* scan_ms, float* emit_ms) {
     if (!p || !phase1_ms || !scan_ms || !emit_ms) return fail(CVG_EINVAL, "null plan or output");
@@ -823,15 +872,19 @@ void cvg_result_free(cvg_result* r) {
                       static_cast<void*>(r->first_codes)}) {
         if (!ptr) continue;
         cvg_ctx* owner = nullptr;
+        bool orphan = false;
         {
             std::lock_guard<std::mutex> lk(g_owner_mu);
             auto it = g_owner.find(ptr);
             if (it != g_owner.end()) {
                 owner = it->second;
+                orphan = owner == nullptr;
                 g_owner.erase(it);
             }
         }
-        if (owner) {
+        if (orphan) {
+            cudaFreeHost(ptr);  // its context was destroyed first
+        } else if (owner) {
             std::lock_guard<std::recursive_mutex> lk(owner->mu);
             owner->host.release(ptr);
         }

@@ -133,7 +133,10 @@ int validate_desc(const cvg_search_desc* d) {
         return fail(CVG_EINVAL, "unknown delta_basis");
     }
     if (d->output < CVG_OUT_PAIRS || d->output > CVG_OUT_FIRST) return fail(CVG_EINVAL, "unknown output mode");
-    if (d->path < CVG_PATH_FAST || d->path > CVG_PATH_PRUNED) return fail(CVG_EINVAL, "unknown path");
+    if (d->path < CVG_PATH_FAST || d->path > CVG_PATH_MEMO) return fail(CVG_EINVAL, "unknown path");
+    if (d->path == CVG_PATH_MEMO && d->output == CVG_OUT_PAIRS) {
+        return fail(CVG_EINVAL, "CVG_PATH_MEMO returns per-search counts / first pairs (CVG_OUT_COUNTS or CVG_OUT_FIRST)");
+    }
     // Fast screen: branch-free, vectorizable pass over the whole batch.  Only
     // if it finds a problem does the ordered per-search loop below run, to
     // report the first failure with the reference's message and order.

@@ -501,7 +501,10 @@ int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out) {
         if (tiles >= per_range) K_min = static_cast<int>(std::min<uint64_t>((tiles + per_range - 1) / per_range,
                                                                              static_cast<uint64_t>(desc->n_searches)));
     }
-    if (const int K = std::max({pipeline_chunks(desc), fixed_chunks(desc), K_min}); K > 1) {
+    // memoized batches run as one plan: the color dedup must see the whole batch
+    if (desc->path == CVG_PATH_MEMO) K_min = 1;
+    if (const int K = desc->path == CVG_PATH_MEMO ? 1 : std::max({pipeline_chunks(desc), fixed_chunks(desc), K_min});
+        K > 1) {
         int e;
         try {
             e = desc->output == CVG_OUT_PAIRS ? search_pipelined(ctx, desc, out, K)

@@ -8,7 +8,8 @@ search, as the reference's threads do (src/search.cpp:433-455), and a
 search's list is the rank-order concatenation of its row slices.  The
 only exchange is the final gather of per-search counts (fixed size, one
 `all_gather`) and, when a caller needs one contiguous list, the variable-size
-pair records (size exchange + padded `all_gather`).  Canonical order is kept
+pair records (size exchange, then exact-size send/recv into offset slices
+on the destination rank only).  Canonical order is kept
 because rank r holds searches [lo_r, hi_r) and ranks concatenate in order --
 the multi-GPU analogue of the reference's ordered slice concatenation
 (src/search.cpp:433-455).
@@ -134,10 +135,53 @@ def _row_destinations(shard: ShardResult, r: int) -> np.ndarray:
     local = np.cumsum(C[r]) - C[r]                        # where it sits in rank r's list
     return np.repeat(start - local, C[r]) + np.arange(int(C[r].sum()))
 
+def pack_records(idx, codes):
+    """(n, 10) uint8 records: u32 LE idx, then the 6 code bytes (the wire
+    layout of the pair gather)."""
+    n = len(idx)
+    rec = np.empty((n, 10), np.uint8)
+    if n:
+        rec[:, :4] = np.ascontiguousarray(idx, "<u4").view(np.uint8).reshape(-1, 4)
+        rec[:, 4:] = codes
+    return rec
+
+
+def gather_records(rec, sizes: list, group=None, dst: int = 0):
+    """Variable-size gather of every rank's (sizes[r], 10) uint8 record
+    tensor into ONE (sum(sizes), 10) tensor on `dst`, rank r's records at
+    offset sum(sizes[:r]) (grouped send/recv into
+    offset slices).  Only dst allocates and receives; the other ranks only
+    send their exact-size buffer.  `rec` lives on the backend's device (CUDA
+    for NCCL, CPU for gloo).  Returns the tensor on dst, None elsewhere."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    assert rec.shape[0] == sizes[rank], (rec.shape, sizes)
+    to_global = (lambda r: dist.get_global_rank(group, r)) if group is not None else (lambda r: r)
+    if rank != dst:
+        if sizes[rank]:
+            dist.send(rec.contiguous(), to_global(dst), group=group)
+        return None
+    out = torch.empty((sum(sizes), 10), dtype=torch.uint8, device=rec.device)
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    ops = []
+    for r in range(world):
+        if r == dst or not sizes[r]:
+            continue
+        ops.append(dist.P2POp(dist.irecv, out[offs[r]:offs[r + 1]], to_global(r), group=group))
+    reqs = dist.batch_isend_irecv(ops) if ops else []
+    if sizes[dst]:
+        out[offs[dst]:offs[dst + 1]].copy_(rec)
+    for q in reqs:
+        q.wait()
+    return out
+
+
 def gather_pairs(shard: ShardResult, group=None, dst: int = 0):
-    """Variable-size gather of every rank's records onto `dst` in canonical
-    order (size exchange, then a padded all_gather).  Returns (idx, codes) on
-    dst, None elsewhere."""
+    """Gather of every rank's records onto `dst` in canonical order
+    (gather_records: exact-size sends into offset slices, nothing received
+    on the other ranks).  Returns (idx, codes) on dst, None elsewhere."""
     import torch
     import torch.distributed as dist
 
@@ -146,24 +190,18 @@ def gather_pairs(shard: ShardResult, group=None, dst: int = 0):
     n_local = len(shard.idx)
     sizes = _rank_sizes(shard, world)
     assert sizes[rank] == n_local, (sizes, n_local)
-    width = max(sizes) if sizes else 0
-    rec = torch.zeros((max(width, 1), 10), dtype=torch.uint8, device=dev)
-    if n_local:
-        packed = np.zeros((n_local, 10), np.uint8)
-        packed[:, :4] = np.ascontiguousarray(shard.idx, np.uint32).view(np.uint8).reshape(-1, 4)
-        packed[:, 4:] = shard.codes
-        rec[:n_local] = torch.from_numpy(packed)
-    out = [torch.empty_like(rec) for _ in range(world)]
-    dist.all_gather(out, rec, group=group)
+    rec = torch.from_numpy(pack_records(shard.idx, shard.codes)).to(dev)
+    out = gather_records(rec, sizes, group, dst)
     if rank != dst:
         return None
-    parts = [out[r][: sizes[r]].cpu().numpy() for r in range(world)]
+    allrec = out.cpu().numpy()
     if shard.by == "rows":
-        allrec = np.zeros((sum(sizes), 10), np.uint8)
+        # rank r's block of search s lands after ranks < r's blocks of s
+        placed = np.empty_like(allrec)
+        offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
         for r in range(world):
-            allrec[_row_destinations(shard, r)] = parts[r]
-    else:
-        allrec = np.concatenate(parts) if parts else np.zeros((0, 10), np.uint8)
+            placed[_row_destinations(shard, r)] = allrec[offs[r]:offs[r + 1]]
+        allrec = placed
     idx = np.ascontiguousarray(allrec[:, :4]).view(np.uint32).reshape(-1)
     codes = np.ascontiguousarray(allrec[:, 4:])
     return idx, codes

@@ -547,3 +547,71 @@ def test_huge_single_search_linearity(ctx):
     assert int(full["counts"][0]) == total > 0
     assert int(full["first_idx"][0]) == first
     assert full["first_codes"][0].tolist() == first_codes
+
+
+# ---- CVG_PATH_MEMO (distinct searches only, scattered on the device) --------
+
+@pytest.mark.parametrize("out", ["first", "counts"])
+def test_memo_path_crop_matches_golden(ctx, out):
+    g = golden("workloads.json")["cfg4_256x144"]
+    wl = W.cfg4(g["width"], g["height"])
+    res = run(ctx, wl, output=out, path="memo")
+    full = run(ctx, wl, output=out)
+    assert np.array_equal(res["counts"], full["counts"])
+    assert int(res["counts"].sum()) == g["total"]
+    if out == "first":
+        import hashlib
+
+        m = hashlib.sha256()
+        m.update(res["counts"].astype(np.uint64).tobytes())
+        m.update(np.ascontiguousarray(res["first_idx"], np.uint32).tobytes())
+        m.update(np.ascontiguousarray(res["first_codes"], np.uint8).tobytes())
+        assert m.hexdigest() == g["sha256"]
+
+
+def test_memo_path_mixed_classifiers(ctx, oracle):
+    """Repeated searches with different patterns / thresholds: the record key
+    is (color, pattern, v_th, r_novib), not the color alone."""
+    radii, angles = W.radii(40, 2.5), W.angles(128)
+    rng = np.random.default_rng(5)
+    base_t = rng.integers(0, 256, (12, 3)).astype(np.int32)
+    n = 300
+    pick = rng.integers(0, 12, n)
+    t = base_t[pick]
+    p = np.where(pick % 2 == 0, 7, 5).astype(np.int32)
+    v = np.where(pick % 3 == 0, 50.0, 100.0)
+    r = np.full(n, 0.5)
+    wl = W.Workload("memo", t, p, v, r, radii, angles, output="first")
+    res = run(ctx, wl, output="first", path="memo")
+    full = run(ctx, wl, output="first")
+    assert np.array_equal(res["counts"], full["counts"])
+    assert np.array_equal(res["first_idx"], full["first_idx"])
+    assert np.array_equal(res["first_codes"], full["first_codes"])
+    for s in range(0, n, 37):
+        oi, oc = oracle_records(oracle, wl, s, workers=1)
+        assert res["counts"][s] == len(oi)
+        if len(oi):
+            assert res["first_idx"][s] == oi[0] and np.array_equal(res["first_codes"][s], oc[0])
+
+
+def test_memo_path_rejects_pairs(ctx):
+    wl = W.cfg0()
+    with pytest.raises(ValueError):
+        run(ctx, wl, output="pairs", path="memo")
+
+
+def test_result_outlives_its_context(cv):
+    """Result arrays view the context's pinned pool; dropping the context
+    first must not free them (use-after-free)."""
+    import gc
+
+    wl = W.cfg0()
+    c = cv.Context(0)
+    res = c.search(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles)
+    idx, codes = res["idx"], res["codes"]
+    del c, res
+    gc.collect()
+    c2 = cv.Context(0)  # reuses the freed pinned memory if the result did not keep it
+    junk = c2.search(wl.targets, wl.patterns, wl.v_th + 7.0, wl.r_novib, wl.radii, wl.angles)
+    assert sha_records(idx, codes) == golden("workloads.json")["cfg0"]["sha256"]
+    del junk, c2
