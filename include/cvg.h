@@ -54,6 +54,10 @@ extern "C" {
 #define CVG_OUT_PAIRS 0  /* every passing pair, canonical (search, radius, angle) order */
 #define CVG_OUT_COUNTS 1 /* per-search pair count only */
 #define CVG_OUT_FIRST 2  /* per-search count + first pair in canonical order (per-pixel mode) */
+#define CVG_OUT_BEST 3   /* per-search count + select_best's pair (search.cpp:458-489): the largest
+                            classification_margin, ties to the first in canonical order; chosen
+                            on the device (first_idx / first_codes hold it).  DeltaMode::Quantized
+                            only (continuous deltas need glibc pow: CVG_EUNSUPPORTED) */
 
 /* evaluation path (all give identical results) */
 #define CVG_PATH_FAST 0  /* FP32 with a proven error bound + FP64 repair of near-boundary values */
@@ -104,8 +108,8 @@ typedef struct {
  * context (cvg_destroy hands the blocks of live results over to them).
  * Pair p: idx[p] = k * n_angles + m (radius index k, angle index m),
  * codes[6p .. 6p+5] = plus r,g,b then minus r,g,b.  Pairs of search s are
- * [offsets[s], offsets[s+1]).  FIRST mode fills first_idx/first_codes instead
- * (first_idx = 0xFFFFFFFF when a search has no pair).
+ * [offsets[s], offsets[s+1]).  FIRST and BEST modes fill first_idx/first_codes
+ * instead (first_idx = 0xFFFFFFFF when a search has no pair).
  */
 typedef struct {
     int32_t n_searches;
@@ -114,8 +118,8 @@ typedef struct {
     uint64_t* offsets;     /* [n_searches + 1] (PAIRS) */
     uint32_t* idx;         /* [n_pairs] (PAIRS) */
     uint8_t* codes;        /* [n_pairs * 6] (PAIRS) */
-    uint32_t* first_idx;   /* [n_searches] (FIRST) */
-    uint8_t* first_codes;  /* [n_searches * 6] (FIRST) */
+    uint32_t* first_idx;   /* [n_searches] (FIRST / BEST) */
+    uint8_t* first_codes;  /* [n_searches * 6] (FIRST / BEST) */
     /* diagnostics */
     uint64_t n_candidates;
     uint64_t n_band_repairs;  /* candidates whose band decision went to FP64 */

@@ -43,7 +43,8 @@ int out_mode(const std::string& s) {
     if (s == "pairs") return CVG_OUT_PAIRS;
     if (s == "counts") return CVG_OUT_COUNTS;
     if (s == "first") return CVG_OUT_FIRST;
-    throw std::invalid_argument("output must be 'pairs', 'counts' or 'first'");
+    if (s == "best") return CVG_OUT_BEST;
+    throw std::invalid_argument("output must be 'pairs', 'counts', 'first' or 'best'");
 }
 
 int path_mode(const std::string& s) {
@@ -111,7 +112,7 @@ py::dict result_dict(std::shared_ptr<ResultHolder> h, int output) {
             out["idx"] = py::array_t<uint32_t>(0);
             out["codes"] = py::array_t<uint8_t>(std::vector<py::ssize_t>{0, 6});
         }
-    } else if (output == CVG_OUT_FIRST) {
+    } else if (output == CVG_OUT_FIRST || output == CVG_OUT_BEST) {
         if (n) {
             out["first_idx"] = py::array_t<uint32_t>({n}, {sizeof(uint32_t)}, r.first_idx, base);
             out["first_codes"] = py::array_t<uint8_t>({n, py::ssize_t(6)}, {py::ssize_t(6), py::ssize_t(1)}, r.first_codes, base);

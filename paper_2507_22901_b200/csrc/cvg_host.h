@@ -486,6 +486,10 @@ struct cvg_plan {
     // representative order); scatter_kernel expands their counts / first
     // pairs to all n searches through map (= sc_index, device)
     bool memo = false;
+    // CVG_OUT_BEST: the PAIRS kernels, then best_kernel (select_best per
+    // search on the device pair buffer) into the first_* arrays
+    bool best = false;
+    const double* d_bands = nullptr;  // BEST: (v_th, low_band) per search
     int32_t n_exec = 0;
     const uint32_t* d_map = nullptr;
     void* d_memo = nullptr;

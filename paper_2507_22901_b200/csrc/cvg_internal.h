@@ -24,6 +24,10 @@ cudaError_t launch_emit(const LaunchArgs& a, int mode, int path, int grid, cudaS
 // dynamic shared memory size on the current device (call before launching).
 int search_blocks_per_sm(int mode, int out, int path);
 cudaError_t launch_first_codes(const LaunchArgs& a, cudaStream_t st);
+// CVG_OUT_BEST epilogue after the PAIRS kernels: per search, the pair of
+// largest classification_margin (first in canonical order on ties) from the
+// device pair buffer into a.first_idx / a.first_codes.  bands = (v_th, low) per search.
+cudaError_t launch_best(const LaunchArgs& a, const double* bands, cudaStream_t st);
 // CVG_PATH_MEMO: out[s] = in[map[s]] for counts (and first pairs when fi_in is set), s < n.
 cudaError_t launch_scatter(const uint32_t* map, int n, const unsigned long long* counts_in, const uint32_t* fi_in,
                            const uint8_t* fc_in, unsigned long long* counts, uint32_t* fi, uint8_t* fc, cudaStream_t st);

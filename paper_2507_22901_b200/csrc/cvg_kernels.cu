@@ -1406,6 +1406,84 @@ __global__ void first_codes_kernel(const LaunchArgs A) {
     }
 }
 
+// CVG_OUT_BEST epilogue: select_best (search.cpp:458-489) on the device.
+// classification_margin (search.cpp:458-466) of a pair is min over channels
+// of (d > v_th ? d - v_th : low - d) in double, with d the integer channel
+// delta (channel_deltas / frame_deltas, search.cpp:125-144).  A passing pair
+// has margin >= +0, so the IEEE bits of the margin order as unsigned
+// integers; the best pair is the largest margin, the first in canonical
+// order among equals (the reference keeps the first maximum of its scan).
+// One block per search: pass 1 the block's max margin, pass 2 the smallest
+// position that reaches it.
+constexpr int kBestThreads = 256;
+
+__device__ __forceinline__ unsigned long long pair_margin_bits(const LaunchArgs& A, unsigned long long o,
+                                                               const int* t, bool frame_diff, double v_th,
+                                                               double low) {
+    const uint16_t* c16 = reinterpret_cast<const uint16_t*>(A.out_codes + 6 * o);
+    const uint32_t w0 = c16[0], w1 = c16[1], w2 = c16[2];
+    const int p[3] = {static_cast<int>(w0 & 0xff), static_cast<int>(w0 >> 8), static_cast<int>(w1 & 0xff)};
+    const int m[3] = {static_cast<int>(w1 >> 8), static_cast<int>(w2 & 0xff), static_cast<int>(w2 >> 8)};
+    double mg = INFINITY;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const int di = frame_diff ? abs(p[q] - m[q]) : max(abs(p[q] - t[q]), abs(m[q] - t[q]));
+        const double d = static_cast<double>(di);
+        const double g = d > v_th ? __dsub_rn(d, v_th) : __dsub_rn(low, d);
+        mg = fmin(mg, g);
+    }
+    return static_cast<unsigned long long>(__double_as_longlong(mg));
+}
+
+template <typename T, typename Op>
+__device__ __forceinline__ T block_reduce(T v, T* red, Op op) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = op(v, __shfl_xor_sync(kFull, v, o));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    v = red[0];
+    for (int w = 1; w < kBestThreads / 32; ++w) v = op(v, red[w]);
+    return v;
+}
+
+__global__ void __launch_bounds__(kBestThreads) best_kernel(const LaunchArgs A, const double* __restrict__ bands) {
+    __shared__ unsigned long long red[kBestThreads / 32];
+    pdl_wait();  // emit complete
+    for (uint32_t s = blockIdx.x; s < static_cast<uint32_t>(A.n_searches); s += gridDim.x) {
+        const unsigned long long cnt = A.counts[s];
+        if (cnt == 0) {
+            if (threadIdx.x == 0) A.first_idx[s] = 0xffffffffu;
+            if (threadIdx.x < 6) A.first_codes[6 * static_cast<size_t>(s) + threadIdx.x] = 0;
+            continue;
+        }
+        const unsigned long long base = A.tile_base[static_cast<uint64_t>(s) * A.tiles_per_search];
+        const SearchConst* S = search_const(A, s);
+        const int t[3] = {__ldg(&S->t[0]), __ldg(&S->t[1]), __ldg(&S->t[2])};
+        const bool frame_diff = (__ldg(&S->flags) >> 8) & 1u;
+        const double v_th = __ldg(&bands[2 * s]), low = __ldg(&bands[2 * s + 1]);
+        unsigned long long best = 0;
+        for (unsigned long long q = threadIdx.x; q < cnt; q += kBestThreads) {
+            best = max(best, pair_margin_bits(A, base + q, t, frame_diff, v_th, low));
+        }
+        best = block_reduce(best, red, [](unsigned long long a, unsigned long long b) { return max(a, b); });
+        unsigned long long pos = ~0ull;
+        for (unsigned long long q = threadIdx.x; q < cnt; q += kBestThreads) {
+            if (pair_margin_bits(A, base + q, t, frame_diff, v_th, low) == best) {
+                pos = q;
+                break;  // q grows: this thread's first hit is its smallest
+            }
+        }
+        pos = block_reduce(pos, red, [](unsigned long long a, unsigned long long b) { return min(a, b); });
+        if (threadIdx.x == 0) A.first_idx[s] = A.out_idx[base + pos];
+        if (threadIdx.x < 6) {
+            A.first_codes[6 * static_cast<size_t>(s) + threadIdx.x] = A.out_codes[6 * (base + pos) + threadIdx.x];
+        }
+        __syncthreads();  // red is reused by the next search
+    }
+}
+
 // CVG_PATH_MEMO epilogue: every search takes the result of its distinct
 // representative (results depend only on target, pattern and thresholds).
 __global__ void scatter_kernel(const uint32_t* __restrict__ map, int n, const unsigned long long* __restrict__ counts_in,
@@ -1479,6 +1557,19 @@ cudaError_t launch_pdl(void (*kernel)(LaunchArgs), unsigned grid, unsigned threa
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
+cudaError_t launch_pdl_bands(unsigned grid, const LaunchArgs& a, const double* bands, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kBestThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, best_kernel, a, bands);
 }
 
 template <int kMode, int kPath>
@@ -1571,6 +1662,12 @@ cudaError_t launch_first_codes(const LaunchArgs& a, cudaStream_t st) {
     if (blocks == 0) return cudaSuccess;
     first_codes_kernel<<<blocks, threads, 0, st>>>(a);
     return cudaGetLastError();
+}
+
+cudaError_t launch_best(const LaunchArgs& a, const double* bands, cudaStream_t st) {
+    if (a.n_searches <= 0) return cudaSuccess;
+    const unsigned blocks = static_cast<unsigned>(std::min(a.n_searches, 148 * 16));
+    return launch_pdl_bands(blocks, a, bands, st);
 }
 
 cudaError_t launch_scatter(const uint32_t* map, int n, const unsigned long long* counts_in, const uint32_t* fi_in,

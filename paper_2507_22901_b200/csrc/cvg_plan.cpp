@@ -228,7 +228,8 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     mark("tables");
     p->ctx = ctx;
     p->mode = search_mode(d);
-    p->out = d->output;
+    p->best = d->output == CVG_OUT_BEST;
+    p->out = p->best ? CVG_OUT_PAIRS : d->output;  // BEST runs the PAIRS kernels, then best_kernel
     // pruning is a flag of the FAST path; so is memoization (distinct searches only)
     p->path = (d->path == CVG_PATH_PRUNED || d->path == CVG_PATH_MEMO) ? CVG_PATH_FAST : d->path;
     p->memo = d->path == CVG_PATH_MEMO && !pre;
@@ -311,6 +312,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     const size_t o_ctab = L.take(sizeof(T.ctab));
     const bool signal = p->mode == cvg::kModeSignal;
     const size_t o_stab = signal ? L.take(sizeof(T.stab)) : 0;
+    const size_t o_bands = p->best ? L.take(sizeof(double) * 2 * p->n) : 0;
     const size_t bytes = L.off;
     p->input_bytes = bytes;
     p->t_prep_end = now_ms();
@@ -348,6 +350,15 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     std::memcpy(stage + o_thd, T.thr, sizeof(double) * 256);
     std::memcpy(stage + o_ctab, T.ctab, sizeof(T.ctab));
     if (signal) std::memcpy(stage + o_stab, T.stab, sizeof(T.stab));
+    if (p->best) {
+        // (v_th, low_band) per search for classification_margin (search.hpp:29-35: low = v_th * r_novib)
+        auto* bands = reinterpret_cast<double*>(stage + o_bands);
+        for (int32_t s = 0; s < p->n; ++s) {
+            bands[2 * s] = d->v_th[s];
+            bands[2 * s + 1] = d->v_th[s] * d->r_novib[s];
+        }
+        p->d_bands = at<const double>(p->d_const, o_bands);
+    }
     LaunchArgs& A = p->args;
     std::memset(&A, 0, sizeof(A));
     A.sc = at<const SearchConst>(p->d_const, o_sc);
@@ -422,7 +433,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         if (!p->d_scratch) return fail(CVG_ENOMEM, "device allocation of the tile lists failed");
         A.scratch = static_cast<uint16_t*>(p->d_scratch);
     }
-    if (p->out == cvg::kOutFirst) {
+    if (p->out == cvg::kOutFirst || p->best) {
         Layout F;
         const size_t o_fi = F.take(sizeof(uint32_t) * p->n_exec);
         const size_t o_fc = F.take(static_cast<size_t>(p->n_exec) * 6);
@@ -518,6 +529,7 @@ int plan_enqueue(cvg_plan* p, cudaStream_t st) {
     p->marked = p->phase_marks;
     CVG_CUDA(cvg::launch_search(p->args, p->mode, p->out, p->path, p->grid, st, p->marked ? p->marks : nullptr));
     if (p->out == cvg::kOutFirst) CVG_CUDA(cvg::launch_first_codes(p->args, st));
+    if (p->best) CVG_CUDA(cvg::launch_best(p->args, p->d_bands, st));
     if (p->memo) {
         const bool first = p->out == cvg::kOutFirst;
         CVG_CUDA(cvg::launch_scatter(p->d_map, p->n, p->args.counts, first ? p->args.first_idx : nullptr,
@@ -598,7 +610,7 @@ int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
     r->kernel_ms = hs.ms;
     r->h2d_bytes = p->input_bytes;
     r->d2h_bytes = sizeof(uint64_t) * n + sizeof(cvg::Stats);
-    if (p->out == cvg::kOutPairs) {
+    if (p->out == cvg::kOutPairs && !p->best) {
         r->d2h_bytes += total * 10;
         r->offsets = static_cast<uint64_t*>(std::malloc(sizeof(uint64_t) * (n + 1)));
         if (!r->offsets) return fail(CVG_ENOMEM, "host allocation failed");
@@ -614,7 +626,7 @@ int plan_fetch_impl(cvg_plan* p, cvg_result* r, bool allow_rerun) {
             CVG_CUDA(cudaStreamSynchronize(st));
         }
         r->d2h_ms = static_cast<float>(now_ms() - t_counts);
-    } else if (p->out == cvg::kOutFirst && n) {
+    } else if ((p->out == cvg::kOutFirst || p->best) && n) {
         r->d2h_bytes += n * 10;
         r->first_idx = static_cast<uint32_t*>(ctx->host.alloc(n * 4));
         r->first_codes = static_cast<uint8_t*>(ctx->host.alloc(n * 6));
@@ -824,7 +836,7 @@ int32_t cvg_plan_evaluated_searches(const cvg_plan* p) { return p ? (p->empty ? 
 
 int cvg_plan_copy_first(cvg_plan* p, uint32_t* first_idx, uint8_t* first_codes, void* stream) {
     if (!p) return fail(CVG_EINVAL, "null plan");
-    if (p->out != cvg::kOutFirst) return fail(CVG_EINVAL, "not a FIRST plan");
+    if (p->out != cvg::kOutFirst && !p->best) return fail(CVG_EINVAL, "not a FIRST / BEST plan");
     std::lock_guard<std::recursive_mutex> lk(p->ctx->mu);
     if (int e = ensure_device(p->ctx)) return e;
     if (p->empty || !p->n) return CVG_OK;
@@ -858,7 +870,8 @@ int cvg_plan_set_phase_marks(cvg_plan* p, int on) {
 
 int cvg_plan_launches(const cvg_plan* p) {
     if (!p || p->empty) return 0;
-    return p->out == cvg::kOutPairs ? 3 : p->out == cvg::kOutFirst ? 2 : 1;
+    // phase 1 [+ scan + emit] [+ first codes] [+ best] [+ memo scatter]
+    return (p->out == cvg::kOutPairs ? 3 : p->out == cvg::kOutFirst ? 2 : 1) + (p->best ? 1 : 0) + (p->memo ? 1 : 0);
 }
 
 uint64_t cvg_plan_candidates(const cvg_plan* p) { return p ? p->candidates : 0; }

@@ -132,9 +132,13 @@ int validate_desc(const cvg_search_desc* d) {
     if (d->delta_basis != CVG_BASIS_TARGET_SWING && d->delta_basis != CVG_BASIS_FRAME_DIFF) {
         return fail(CVG_EINVAL, "unknown delta_basis");
     }
-    if (d->output < CVG_OUT_PAIRS || d->output > CVG_OUT_FIRST) return fail(CVG_EINVAL, "unknown output mode");
+    if (d->output < CVG_OUT_PAIRS || d->output > CVG_OUT_BEST) return fail(CVG_EINVAL, "unknown output mode");
     if (d->path < CVG_PATH_FAST || d->path > CVG_PATH_MEMO) return fail(CVG_EINVAL, "unknown path");
-    if (d->path == CVG_PATH_MEMO && d->output == CVG_OUT_PAIRS) {
+    if (d->output == CVG_OUT_BEST && d->delta_mode != CVG_DELTA_QUANTIZED) {
+        return fail(CVG_EUNSUPPORTED, "CVG_OUT_BEST ranks integer (Quantized) deltas; continuous deltas need the "
+                                      "host's glibc pow (select_best over CVG_OUT_PAIRS)");
+    }
+    if (d->path == CVG_PATH_MEMO && (d->output == CVG_OUT_PAIRS || d->output == CVG_OUT_BEST)) {
         return fail(CVG_EINVAL, "CVG_PATH_MEMO returns per-search counts / first pairs (CVG_OUT_COUNTS or CVG_OUT_FIRST)");
     }
     // Fast screen: branch-free, vectorizable pass over the whole batch.  Only

@@ -502,8 +502,9 @@ int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out) {
                                                                              static_cast<uint64_t>(desc->n_searches)));
     }
     // memoized batches run as one plan: the color dedup must see the whole batch
-    if (desc->path == CVG_PATH_MEMO) K_min = 1;
-    if (const int K = desc->path == CVG_PATH_MEMO ? 1 : std::max({pipeline_chunks(desc), fixed_chunks(desc), K_min});
+    // and BEST runs one plan (select_best reads each search's whole list on the device)
+    const bool single = desc->path == CVG_PATH_MEMO || desc->output == CVG_OUT_BEST;
+    if (const int K = single ? 1 : std::max({pipeline_chunks(desc), fixed_chunks(desc), K_min});
         K > 1) {
         int e;
         try {
