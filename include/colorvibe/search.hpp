@@ -11,6 +11,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <string_view>
 #include <utility>
@@ -137,5 +138,33 @@ std::vector<std::vector<ColorPair>> batch_search_many(const std::vector<SearchSp
 /// Pair counts only (no list materialization).
 std::vector<std::uint64_t> batch_count_many(const std::vector<SearchSpec>& specs, const VibrationGrid& grid,
                                             const SearchOptions& opts = {});
+
+// ---- B200 extension: lazy result -------------------------------------------
+/// The pairs of one search, kept as the packed records the device returned
+/// (u32 idx = k * n_angles + m, then plus r,g,b and minus r,g,b) in pinned
+/// host memory; ColorPair (80 B, search.hpp:58-79) is built on access, so a
+/// search with hundreds of millions of pairs costs 10 B per pair until
+/// elements are read.  at(i) / to_vector() equal batch_search(...)[i] / (...).
+class PairView {
+public:
+    PairView() = default;
+    std::size_t size() const;
+    bool empty() const { return size() == 0; }
+    ColorPair at(std::size_t i) const;  // std::out_of_range past the end
+    ColorPair operator[](std::size_t i) const { return at(i); }
+    std::vector<ColorPair> to_vector() const;
+    const std::uint32_t* idx() const;    // [size()] packed records
+    const std::uint8_t* codes() const;   // [6 * size()]
+    struct Impl;
+
+private:
+    std::shared_ptr<const Impl> impl_;
+    friend PairView batch_search_view(const SrgbColor&, const VibrationGrid&, const BitPattern&, const Thresholds&,
+                                      const SearchOptions&);
+};
+
+/// batch_search returning a PairView instead of materializing the list.
+PairView batch_search_view(const SrgbColor& target, const VibrationGrid& grid, const BitPattern& pattern,
+                           const Thresholds& th, const SearchOptions& opts = {});
 
 }  // namespace colorvibe

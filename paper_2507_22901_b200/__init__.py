@@ -19,6 +19,10 @@ embed_blocks, decode_blocks, layout_to_json, decode_report_json (+
 layout_from_json); painting and block sums run on the device
 (csrc/cvg_codec.cu).
 
+Lazy results: `batch_search_view(...)` returns a PairView (packed 10-byte
+records in pinned memory, ColorPair built on access, equal to the list
+batch_search returns).
+
 Extras for batched/pipeline use: `Context.search(...)` (NumPy in, NumPy out,
 one launch for many searches), `Context.plan(...)` (device-resident repeated
 runs), `batch_search_many`, `batch_count_many`.
@@ -84,6 +88,7 @@ from ._core import (  # noqa: E402
     DeltaBasis,
     DeltaMode,
     LabColor,
+    PairView,
     Plan,
     SearchOptions,
     SearchSpec,
@@ -95,6 +100,7 @@ from ._core import (  # noqa: E402
     batch_search,
     batch_search_many,
     batch_search_opts,
+    batch_search_view,
     channel_deltas,
     classification_margin,
     classify_pair,
@@ -117,9 +123,9 @@ from ._core import (  # noqa: E402
 LIBRARY_PATH = _os.path.join(_here, "libcolorvibe_gpu.so")
 
 __all__ = [
-    "BitPattern", "ChannelDeltas", "ColorPair", "Context", "DeltaBasis", "DeltaMode", "LabColor", "Plan",
+    "BitPattern", "ChannelDeltas", "ColorPair", "Context", "DeltaBasis", "DeltaMode", "LabColor", "PairView", "Plan",
     "SearchOptions", "SearchSpec", "SrgbColor", "Thresholds", "VibrationGrid", "WhitePoint",
-    "batch_count_many", "batch_search", "batch_search_many", "batch_search_opts", "channel_deltas",
+    "batch_count_many", "batch_search", "batch_search_many", "batch_search_opts", "batch_search_view", "channel_deltas",
     "classification_margin", "classify_pair", "d65_white", "displaced_pair", "frame_deltas", "in_gamut",
     "lab_to_srgb", "lab_to_srgb_clipped", "measure_ffma_peak", "quant_thresholds", "select_best",
     "serial_search", "serial_search_opts", "srgb_to_lab", "srgb_to_linear", "version", "LIBRARY_PATH",

@@ -301,6 +301,72 @@ PYBIND11_MODULE(_core, m) {
         },
         py::arg("target"), py::arg("grid"), py::arg("pattern"), py::arg("thresholds"), py::arg("workers") = 0,
         py::call_guard<py::gil_scoped_release>());
+    // Lazy result (B200 extension): the packed records stay in pinned host
+    // memory; ColorPair objects are built on access.  Compares equal to the
+    // list batch_search returns.
+    py::class_<PairView>(m, "PairView")
+        .def("__len__", &PairView::size)
+        .def("__getitem__", [](const PairView& v, py::ssize_t i) {
+            const py::ssize_t n = static_cast<py::ssize_t>(v.size());
+            if (i < 0) i += n;
+            if (i < 0 || i >= n) throw py::index_error("PairView index out of range");
+            return v.at(static_cast<size_t>(i));
+        })
+        .def("__getitem__", [](const PairView& v, const py::slice& sl) {
+            size_t start = 0, stop = 0, step = 0, len = 0;
+            if (!sl.compute(v.size(), &start, &stop, &step, &len)) throw py::error_already_set();
+            std::vector<ColorPair> out;
+            out.reserve(len);
+            for (size_t j = 0; j < len; ++j) out.push_back(v.at(start + j * step));
+            return out;
+        })
+        .def("__iter__", [](py::object self) {
+            return py::iter(py::module_::import("builtins").attr("map")(self.attr("__getitem__"),
+                                                                        py::module_::import("builtins").attr("range")(
+                                                                            py::len(self))));
+        })
+        .def("__eq__", [](const PairView& v, py::object other) {
+            if (py::isinstance<PairView>(other)) {
+                const PairView& o = other.cast<const PairView&>();
+                if (o.size() != v.size()) return false;
+                for (size_t i = 0; i < v.size(); ++i) if (!(v.at(i) == o.at(i))) return false;
+                return true;
+            }
+            if (!py::isinstance<py::sequence>(other)) return false;
+            py::sequence seq = other;
+            if (static_cast<size_t>(py::len(seq)) != v.size()) return false;
+            for (size_t i = 0; i < v.size(); ++i) {
+                py::object x = seq[i];
+                if (!py::isinstance<ColorPair>(x) || !(x.cast<const ColorPair&>() == v.at(i))) return false;
+            }
+            return true;
+        })
+        .def("__bool__", [](const PairView& v) { return !v.empty(); })
+        .def("__repr__", [](const PairView& v) { return "PairView(" + std::to_string(v.size()) + " pairs)"; })
+        .def("to_list", &PairView::to_vector, py::call_guard<py::gil_scoped_release>())
+        .def_property_readonly("idx", [](py::object self) {
+            const PairView& v = self.cast<const PairView&>();
+            const py::ssize_t n = static_cast<py::ssize_t>(v.size());
+            if (!n) return py::array_t<uint32_t>(0);
+            return py::array_t<uint32_t>({n}, {sizeof(uint32_t)}, v.idx(), self);  // zero-copy
+        })
+        .def_property_readonly("codes", [](py::object self) {
+            const PairView& v = self.cast<const PairView&>();
+            const py::ssize_t n = static_cast<py::ssize_t>(v.size());
+            if (!n) return py::array_t<uint8_t>(std::vector<py::ssize_t>{0, 6});
+            return py::array_t<uint8_t>({n, py::ssize_t(6)}, {py::ssize_t(6), py::ssize_t(1)}, v.codes(), self);
+        });
+    m.def(
+        "batch_search_view",
+        [](const SrgbColor& target, const VibrationGrid& grid, const BitPattern& pattern, const Thresholds& th,
+           int workers, py::object options) {
+            SearchOptions opts = options.is_none() ? SearchOptions{} : options.cast<SearchOptions>();
+            opts.workers = workers;
+            py::gil_scoped_release nogil;
+            return batch_search_view(target, grid, pattern, th, opts);
+        },
+        py::arg("target"), py::arg("grid"), py::arg("pattern"), py::arg("thresholds"), py::arg("workers") = 0,
+        py::arg("options") = py::none());
     // Options-aware forms of the C++ API (search.hpp:126-130 take SearchOptions).
     m.def("batch_search_opts", &batch_search, py::arg("target"), py::arg("grid"), py::arg("pattern"),
           py::arg("thresholds"), py::arg("options"), py::call_guard<py::gil_scoped_release>());

@@ -79,44 +79,50 @@ void run(const std::vector<SearchSpec>& specs, const VibrationGrid& grid, const 
     check(cvg_search(default_ctx(), &d, &g.r));
 }
 
+// ColorPair of record (i, c) of a search around `target` (Continuous: `lab`
+// is the target's Lab, deltas from the host's glibc signal values).
+ColorPair make_pair(uint32_t i, const uint8_t* c, const SrgbColor& target, const double* radii, const double* angles,
+                    uint32_t na, const SearchOptions& opts, const double* lab) {
+    const bool swing = opts.delta_basis == DeltaBasis::TargetSwing;
+    const bool continuous = opts.delta_mode == DeltaMode::Continuous;
+    const double wp[3] = {opts.white_point.x, opts.white_point.y, opts.white_point.z};
+    ColorPair cp;
+    cp.target = target;
+    cp.plus = SrgbColor{c[0], c[1], c[2]};
+    cp.minus = SrgbColor{c[3], c[4], c[5]};
+    cp.radius = radii[i / na];
+    cp.angle = angles[i % na];
+    if (continuous) {
+        // continuous_deltas (search.cpp:161-180) on the host's glibc signal values
+        double sp[3], sm[3];
+        check(cvg_pair_signal(lab, cp.radius, cp.angle, wp, sp, sm));
+        const double t[3] = {static_cast<double>(target.r), static_cast<double>(target.g),
+                             static_cast<double>(target.b)};
+        double d[3];
+        for (int q = 0; q < 3; ++q) {
+            d[q] = swing ? std::max(std::abs(sp[q] - t[q]), std::abs(sm[q] - t[q])) : std::abs(sp[q] - sm[q]);
+        }
+        cp.deltas = ChannelDeltas{d[0], d[1], d[2]};
+    } else {
+        cp.deltas = swing ? channel_deltas(target, cp.plus, cp.minus) : frame_deltas(cp.plus, cp.minus);
+    }
+    return cp;
+}
+
 std::vector<ColorPair> materialize(const cvg_result& r, size_t s, const SrgbColor& target, const VibrationGrid& grid,
                                    const SearchOptions& opts) {
     std::vector<ColorPair> out;
     const uint64_t b = r.offsets[s], e = r.offsets[s + 1];
     out.reserve(e - b);
     const uint32_t na = static_cast<uint32_t>(grid.angles.size());
-    const bool swing = opts.delta_basis == DeltaBasis::TargetSwing;
-    const bool continuous = opts.delta_mode == DeltaMode::Continuous;
-    const double wp[3] = {opts.white_point.x, opts.white_point.y, opts.white_point.z};
     double lab[3] = {0, 0, 0};
-    if (continuous) {
+    if (opts.delta_mode == DeltaMode::Continuous) {
         const int32_t rgb[3] = {target.r, target.g, target.b};
+        const double wp[3] = {opts.white_point.x, opts.white_point.y, opts.white_point.z};
         check(cvg_srgb_to_lab(rgb, wp, lab));
     }
     for (uint64_t p = b; p < e; ++p) {
-        const uint32_t i = r.idx[p];
-        const uint8_t* c = r.codes + 6 * p;
-        ColorPair cp;
-        cp.target = target;
-        cp.plus = SrgbColor{c[0], c[1], c[2]};
-        cp.minus = SrgbColor{c[3], c[4], c[5]};
-        cp.radius = grid.radii[i / na];
-        cp.angle = grid.angles[i % na];
-        if (continuous) {
-            // continuous_deltas (search.cpp:161-180) on the host's glibc signal values
-            double sp[3], sm[3];
-            check(cvg_pair_signal(lab, cp.radius, cp.angle, wp, sp, sm));
-            const double t[3] = {static_cast<double>(target.r), static_cast<double>(target.g),
-                                 static_cast<double>(target.b)};
-            double d[3];
-            for (int c = 0; c < 3; ++c) {
-                d[c] = swing ? std::max(std::abs(sp[c] - t[c]), std::abs(sm[c] - t[c])) : std::abs(sp[c] - sm[c]);
-            }
-            cp.deltas = ChannelDeltas{d[0], d[1], d[2]};
-        } else {
-            cp.deltas = swing ? channel_deltas(target, cp.plus, cp.minus) : frame_deltas(cp.plus, cp.minus);
-        }
-        out.push_back(cp);
+        out.push_back(make_pair(r.idx[p], r.codes + 6 * p, target, grid.radii.data(), grid.angles.data(), na, opts, lab));
     }
     return out;
 }
@@ -316,6 +322,61 @@ std::vector<ColorPair> serial_search(const SrgbColor& target, const VibrationGri
 std::vector<ColorPair> batch_search(const SrgbColor& target, const VibrationGrid& grid, const BitPattern& pattern,
                                     const Thresholds& th, const SearchOptions& opts) {
     return search_one(target, grid, pattern, th, opts, CVG_PATH_PRUNED);  // FAST + certified row pruning: same pairs
+}
+
+// ---- PairView ----------------------------------------------------------------
+
+struct PairView::Impl {
+    cvg_result r{};
+    SrgbColor target{};
+    std::vector<double> radii, angles;
+    SearchOptions opts{};
+    double lab[3] = {0, 0, 0};
+    ~Impl() { cvg_result_free(&r); }
+};
+
+std::size_t PairView::size() const { return impl_ ? static_cast<std::size_t>(impl_->r.n_pairs) : 0; }
+
+const std::uint32_t* PairView::idx() const { return impl_ ? impl_->r.idx : nullptr; }
+
+const std::uint8_t* PairView::codes() const { return impl_ ? impl_->r.codes : nullptr; }
+
+ColorPair PairView::at(std::size_t i) const {
+    if (i >= size()) throw std::out_of_range("PairView index out of range");
+    const Impl& m = *impl_;
+    return make_pair(m.r.idx[i], m.r.codes + 6 * i, m.target, m.radii.data(), m.angles.data(),
+                     static_cast<uint32_t>(m.angles.size()), m.opts, m.lab);
+}
+
+std::vector<ColorPair> PairView::to_vector() const {
+    std::vector<ColorPair> out;
+    out.reserve(size());
+    for (std::size_t i = 0; i < size(); ++i) out.push_back(at(i));
+    return out;
+}
+
+PairView batch_search_view(const SrgbColor& target, const VibrationGrid& grid, const BitPattern& pattern,
+                           const Thresholds& th, const SearchOptions& opts) {
+    validate_one(target, grid, pattern, th);
+    PairView v;
+    auto impl = std::make_shared<PairView::Impl>();
+    impl->target = target;
+    impl->opts = opts;
+    if (!grid.radii.empty() && !grid.angles.empty()) {
+        ResultGuard g;
+        run({SearchSpec{target, pattern, th}}, grid, opts, CVG_OUT_PAIRS, CVG_PATH_PRUNED, g);
+        impl->r = g.r;  // the view owns the result from here
+        g.r = cvg_result{};
+        impl->radii = grid.radii;
+        impl->angles = grid.angles;
+        if (opts.delta_mode == DeltaMode::Continuous) {
+            const int32_t rgb[3] = {target.r, target.g, target.b};
+            const double wp[3] = {opts.white_point.x, opts.white_point.y, opts.white_point.z};
+            check(cvg_srgb_to_lab(rgb, wp, impl->lab));
+        }
+    }
+    v.impl_ = std::move(impl);
+    return v;
 }
 
 double classification_margin(const ColorPair& pair, const Thresholds& th) {

@@ -1083,6 +1083,106 @@ __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C,
     }
 }
 
+// ---- Column tiles (COUNTS / FIRST, band FAST path) -------------------------
+// Lane l evaluates radius row k = 32 kb + l at every angle of the tile's
+// block, the warp walking the angles in ascending order, kColG angles per
+// iteration: the trig values are warp-uniform (one broadcast LDG.128 per two
+// angles), the radius is a per-lane register for the whole tile, and there
+// is no per-row set-up.  Certain passes are tallied per lane (no ballot);
+// each lane keeps its first passing angle (angles ascend, so the first hit
+// is the lane's smallest).  Lanes inside the FP32 bound but not certain are
+// decided in FP64 behind one vote per iteration.  Every candidate is
+// evaluated exactly as in the row-major loop (band_chunk, same bound), only
+// the walk order differs -- the outputs (counts, first canonical pair) do
+// not depend on it.
+constexpr uint32_t kColG = 4;
+
+template <int kL, bool kCubeOnly, int kOut>
+__device__ __forceinline__ void col_run(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
+                                        bool row_ok, float r, uint32_t m0, uint32_t m1, uint32_t& cnt,
+                                        uint32_t& fm, Counters& ct) {
+    const float4* __restrict__ trig4 = reinterpret_cast<const float4*>(A.trig_f);
+    const float2* __restrict__ trig = reinterpret_cast<const float2*>(A.trig_f);
+    uint32_t m = m0;
+    const uint32_t mend = m0 + (m1 - m0) / kColG * kColG;
+#pragma unroll 1
+    for (; m != mend; m += kColG) {
+        float2 sv[kColG];
+#pragma unroll
+        for (uint32_t g = 0; g < kColG; g += 2) {
+            const float4 t = __ldg(trig4 + ((m + g) >> 1));  // m0 even (block starts at kColW * mb)
+            sv[g] = make_float2(t.x, t.y);
+            sv[g + 1] = make_float2(t.z, t.w);
+        }
+        float lv[kColG], qv[kColG];
+        bool uns = false;
+#pragma unroll
+        for (uint32_t g = 0; g < kColG; ++g) {
+            band_chunk<kL, kCubeOnly>(C, r, sv[g], lv[g], qv[g]);
+            const bool cert = band_certain(C, lv[g], qv[g]) & row_ok;
+            cnt += cert;
+            if (kOut == kOutFirst) fm = cert ? min(fm, m + g) : fm;
+            uns |= band_attention(C, lv[g], qv[g]) & !band_certain(C, lv[g], qv[g]);
+        }
+        uns &= row_ok;
+        if (__any_sync(kFull, uns) && uns) {
+#pragma unroll 1
+            for (uint32_t g = 0; g < kColG; ++g) {
+                if (band_attention(C, lv[g], qv[g]) & !band_certain(C, lv[g], qv[g])) {
+                    double lp[3], lm[3];
+                    exact_linear(S, A, k, m + g, lp, lm);
+                    const bool pass = exact_band(S, lp, lm, C.flags);
+                    ++ct.repairs;
+                    cnt += pass;
+                    if (kOut == kOutFirst && pass) fm = min(fm, m + g);
+                }
+            }
+        }
+    }
+#pragma unroll 1
+    for (; m < m1; ++m) {
+        float l1, q1;
+        band_chunk<kL, kCubeOnly>(C, r, __ldg(trig + m), l1, q1);
+        bool pass = band_certain(C, l1, q1);
+        const bool u = band_attention(C, l1, q1) & !pass & row_ok;
+        if (__any_sync(kFull, u) && u) {
+            double lp[3], lm[3];
+            exact_linear(S, A, k, m, lp, lm);
+            pass = exact_band(S, lp, lm, C.flags);
+            ++ct.repairs;
+        }
+        pass &= row_ok;
+        cnt += pass;
+        if (kOut == kOutFirst && pass) fm = min(fm, m);
+    }
+}
+
+// One column tile: rows [32 kb, 32 kb + 32) x angles [kColW mb, ...) of
+// search s; per-search count and first canonical pair updated here.
+template <int kL, int kOut>
+__device__ __forceinline__ void col_tile(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t s,
+                                         uint32_t kb, uint32_t mb, unsigned lane, Counters& ct) {
+    const uint32_t k = 32 * kb + lane;
+    const bool row_ok = k < static_cast<uint32_t>(A.nr);
+    const uint32_t kl = min(32 * kb + 31, static_cast<uint32_t>(A.nr) - 1);  // the block's largest radius
+    const float r = row_ok ? __ldg(&A.radii_f[k]) : 0.0f;
+    const uint32_t m0 = static_cast<uint32_t>(kColW) * mb;
+    const uint32_t m1 = min(m0 + static_cast<uint32_t>(kColW), static_cast<uint32_t>(A.na));
+    uint32_t cnt = 0, fm = 0xffffffffu;
+    if (__ldg(&A.radii_f[kl]) < C.rcube) {  // no row of the block reaches the linear branch of f^-1
+        col_run<kL, true, kOut>(S, C, A, k, row_ok, r, m0, m1, cnt, fm, ct);
+    } else {
+        col_run<kL, false, kOut>(S, C, A, k, row_ok, r, m0, m1, cnt, fm, ct);
+    }
+    const uint32_t total = __reduce_add_sync(kFull, cnt);
+    if (kOut == kOutFirst) {
+        const uint32_t mine = fm != 0xffffffffu ? k * static_cast<uint32_t>(A.na) + fm : 0xffffffffu;
+        const uint32_t first = __reduce_min_sync(kFull, mine);
+        if (lane == 0 && total) atomicMin(&A.first_idx[s], first);
+    }
+    if (lane == 0 && total) atomicAdd(&A.counts[s], static_cast<unsigned long long>(total));
+}
+
 // K1: decide every candidate.  Warps claim 4096-candidate tiles (contiguous
 // canonical ranges of one search) from a ticket, prefetching the next ticket.
 // PAIRS: tile count + ordered passing offsets to scratch; COUNTS: per-search
@@ -1156,7 +1256,21 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         uint32_t* first = &sm.first[threadIdx.x >> 5];
         Consts C;
         load_consts(S, C);
-        if (kMode == kModeBand && kPath == kPathFast && A.aligned) {
+        constexpr bool kColsOk = kMode == kModeBand && kPath == kPathFast && kOut != kOutPairs && !kPrune;
+        if (kColsOk && A.cols) {
+            if constexpr (kColsOk) {
+                const uint32_t kb = lt / A.col_mb, mb = lt - kb * A.col_mb;
+                const uint32_t nl = (C.flags >> 10) & 3u;
+                if (nl == 3) {
+                    col_tile<3, kOut>(S, C, A, s, kb, mb, lane, ct);
+                } else if (nl == 2) {
+                    col_tile<2, kOut>(S, C, A, s, kb, mb, lane, ct);
+                } else {
+                    col_tile<1, kOut>(S, C, A, s, kb, mb, lane, ct);
+                }
+            }
+            // counts / first pair already recorded: cnt stays 0
+        } else if (kMode == kModeBand && kPath == kPathFast && A.aligned) {
             const uint32_t nl = (C.flags >> 10) & 3u;
             if (nl == 3) {
                 band_tile<3, kOut, kPrune>(S, C, A, i0, i1, list, cnt, first, ct, lane, lane_lt);

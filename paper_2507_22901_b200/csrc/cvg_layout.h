@@ -14,6 +14,7 @@ constexpr int kWarpsPerBlock = 8;
 constexpr int kBlock = 32 * kWarpsPerBlock;
 constexpr int kGuessBuckets = 4096;  // code-table buckets over linear [0, 1]
 constexpr float kCodeSlack = 1.0f / 65536;  // code-table bucket widening (>= every usable eps_code)
+constexpr int kColW = kTile / 32;  // angles per column tile (32 rows x 128 angles)
 constexpr int kEmitSpan = 256;      // pairs per emit work item (tile sub-range)
 constexpr int kScanItems = 8;        // tile counts per thread in the offset scan
 constexpr int kScanTile = kBlock * kScanItems;
@@ -117,6 +118,12 @@ struct LaunchArgs {
     uint32_t* worklist;            // [n_tiles * kTile / kEmitSpan] emit items tile << 4 | sub, any order
     uint32_t emit_shift;           // log2 of the pairs per emit item: 8 (kEmitSpan), 9 for dense batches
     uint32_t prune;                // CVG_PATH_PRUNED: skip radius rows that row_surely_fails proves empty
+    // Column tiles (COUNTS / FIRST, band FAST path): tile lt of a search is
+    // radius rows [32 kb, 32 kb + 32) x angles [kColW mb, kColW mb + kColW),
+    // kb = lt / col_mb, mb = lt % col_mb; lane l owns row 32 kb + l and the
+    // warp walks the angles (warp-uniform trig).  0 = row-major tiles.
+    uint32_t cols;
+    uint32_t col_mb;               // angle blocks per search
     unsigned long long* total;     // [1] sum of tile_count (PAIRS)
     uint32_t* out_idx;           // [capacity]
     uint8_t* out_codes;          // [capacity * 6]

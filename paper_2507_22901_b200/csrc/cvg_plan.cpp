@@ -241,7 +241,20 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     p->empty = p->candidates == 0;
     if (p->empty) return CVG_OK;  // search.cpp:409-411
 
-    const uint32_t tps = static_cast<uint32_t>((cps + cvg::kTile - 1) / cvg::kTile);
+    // Column tiles (32 rows x kColW angles, lane per row) for COUNTS / FIRST
+    // on the band FAST path when there are rows enough to fill the lanes
+    // (cfg4: 64 x 256 grid); else row-major tiles of kTile canonical
+    // candidates.  CVG_COLS=0 turns them off (A/B).
+    static const int cols_env = [] {
+        const char* e = std::getenv("CVG_COLS");
+        return e ? std::atoi(e) : 1;
+    }();
+    const bool cols = cols_env != 0 && d->output != CVG_OUT_PAIRS && d->output != CVG_OUT_BEST &&
+                      search_mode(d) == cvg::kModeBand && (d->path == CVG_PATH_FAST || d->path == CVG_PATH_MEMO) &&
+                      p->nr >= 24;
+    const uint32_t col_mb = static_cast<uint32_t>((p->na + cvg::kColW - 1) / cvg::kColW);
+    const uint32_t tps = cols ? static_cast<uint32_t>((p->nr + 31) / 32) * col_mb
+                              : static_cast<uint32_t>((cps + cvg::kTile - 1) / cvg::kTile);
 
     // ---- host tables ----
     // Per-search constants, deduplicated: searches with the same (target,
@@ -390,6 +403,8 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.na_magic = p->na > 1 ? (UINT64_MAX / static_cast<uint64_t>(p->na)) + 1 : 0;
     A.emit_shift = 8;  // kEmitSpan until an expected pair count says otherwise (plan_set_density)
     A.prune = d->path == CVG_PATH_PRUNED ? 1u : 0u;
+    A.cols = cols ? 1u : 0u;
+    A.col_mb = col_mb;
     A.n_tiles = n_tiles;
 
     // ---- per-run workspace --------------------------------------------------

@@ -615,3 +615,81 @@ def test_result_outlives_its_context(cv):
     junk = c2.search(wl.targets, wl.patterns, wl.v_th + 7.0, wl.r_novib, wl.radii, wl.angles)
     assert sha_records(idx, codes) == golden("workloads.json")["cfg0"]["sha256"]
     del junk, c2
+
+
+# ---- PairView (lazy ColorPair materialization, module.cpp:121-131) ----------
+
+def test_pair_view_equals_list(cv, ctx):
+    grid = cv.VibrationGrid.uniform(1.0, 91.0, 10.0, 0.0, 350.0, 10.0)
+    fd = cv.SearchOptions()
+    fd.delta_basis = cv.DeltaBasis.FRAME_DIFF
+    co = cv.SearchOptions()
+    co.delta_mode = cv.DeltaMode.CONTINUOUS
+    for t in ([170, 170, 170], [240, 100, 240], [8, 8, 8]):
+        for p in ("101", "111", "010"):
+            args = (cv.SrgbColor(*t), grid, cv.BitPattern(p), cv.Thresholds(50.0, 0.5))
+            lst = cv.batch_search(*args)
+            v = cv.batch_search_view(*args)
+            assert len(v) == len(lst) and v == lst and v.to_list() == lst and list(v) == lst
+            assert bool(v) == bool(lst)
+            if lst:
+                assert v[0] == lst[0] and v[-1] == lst[-1] and v[1:4] == lst[1:4]
+                assert v.idx.dtype == np.uint32 and v.codes.shape == (len(lst), 6)
+            for opts in (fd, co):
+                assert cv.batch_search_view(*args, options=opts) == cv.batch_search_opts(*args, opts)
+    with pytest.raises(IndexError):
+        cv.batch_search_view(cv.SrgbColor(170, 170, 170), grid, cv.BitPattern("111"), cv.Thresholds(50.0, 0.5))[10 ** 6]
+    with pytest.raises(ValueError):
+        cv.batch_search_view(cv.SrgbColor(300, 0, 0), grid, cv.BitPattern("111"), cv.Thresholds(50.0, 0.5))
+
+
+@pytest.mark.slow
+def test_pair_view_cfg2_target_not_list_bound(cv, ctx):
+    """A cfg2 target through the Python API (46M pairs): the view holds the
+    10-byte records (reference-pinned sha), no 80-byte objects are built."""
+    import time
+
+    wl = W.cfg2()
+    grid = cv.VibrationGrid()
+    grid.radii = wl.radii.tolist()
+    grid.angles = wl.angles.tolist()
+    t0 = time.perf_counter()
+    v = cv.batch_search_view(cv.SrgbColor(*wl.targets[0].tolist()), grid, cv.BitPattern("111"),
+                             cv.Thresholds(50.0, 0.5))
+    dt = time.perf_counter() - t0
+    g = golden("workloads.json")["cfg2"]
+    assert len(v) == g["counts"][0]
+    assert records10_sha(v.idx, v.codes) == g["sha256_records10"][0]
+    p = v[len(v) // 2]
+    assert p.radius == wl.radii[v.idx[len(v) // 2] // len(wl.angles)]
+    assert dt < 10.0, dt  # list materialization of 46M ColorPair objects takes minutes
+
+
+# ---- column tiles (COUNTS / FIRST, band FAST path: lane per radius row) -----
+
+@pytest.mark.parametrize("nr,na", [(24, 7), (40, 100), (33, 130), (64, 256), (70, 384), (100, 33)])
+@pytest.mark.parametrize("out", ["counts", "first"])
+def test_column_tiles_edge_shapes(ctx, oracle, nr, na, out):
+    """Partial row blocks (nr % 32), partial angle blocks (na % 128), odd na,
+    against the oracle search by search; same answer with row-major tiles
+    (path 'pruned' keeps row-major tiles)."""
+    radii, angles = W.radii(nr, 126.0 / max(nr - 1, 1)), W.angles(na)
+    rng = np.random.default_rng(nr * 1000 + na)
+    n = 24
+    t = rng.integers(0, 256, (n, 3)).astype(np.int32)
+    t[:3] = [[0, 0, 0], [255, 255, 255], [8, 8, 8]]
+    p = rng.integers(1, 8, n).astype(np.int32)
+    v = rng.choice([30.0, 50.0, 100.0], n)
+    r = rng.choice([0.25, 0.5, 1.0], n)
+    wl = W.Workload("cols", t, p, v, r, radii, angles, output=out)
+    res = run(ctx, wl, output=out)
+    rowm = run(ctx, wl, output=out, path="pruned")
+    assert np.array_equal(res["counts"], rowm["counts"])
+    for s in range(n):
+        oi, oc = oracle_records(oracle, wl, s, workers=1)
+        assert res["counts"][s] == len(oi), s
+        if out == "first":
+            if len(oi):
+                assert res["first_idx"][s] == oi[0] and np.array_equal(res["first_codes"][s], oc[0]), s
+            else:
+                assert res["first_idx"][s] == 0xFFFFFFFF
