@@ -1083,104 +1083,138 @@ __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C,
     }
 }
 
-// ---- Column tiles (COUNTS / FIRST, band FAST path) -------------------------
-// Lane l evaluates radius row k = 32 kb + l at every angle of the tile's
-// block, the warp walking the angles in ascending order, kColG angles per
-// iteration: the trig values are warp-uniform (one broadcast LDG.128 per two
-// angles), the radius is a per-lane register for the whole tile, and there
-// is no per-row set-up.  Certain passes are tallied per lane (no ballot);
-// each lane keeps its first passing angle (angles ascend, so the first hit
-// is the lane's smallest).  Lanes inside the FP32 bound but not certain are
-// decided in FP64 behind one vote per iteration.  Every candidate is
-// evaluated exactly as in the row-major loop (band_chunk, same bound), only
-// the walk order differs -- the outputs (counts, first canonical pair) do
-// not depend on it.
-constexpr uint32_t kColG = 4;
+// ---- Strip tiles (COUNTS / FIRST, band FAST path) --------------------------
+// A strip is 32 consecutive angles (lane l owns angle m0 + l, its trig in
+// registers for the whole strip) walked down R radius rows, kStripG rows per
+// iteration: the radii are warp-uniform (one broadcast LDG.128 per four
+// rows) and a row costs no set-up.  The f^-1 branch is chosen per group of
+// rows from the strip's own largest |sin| and |cos| (cube-only while r of the
+// group's last row stays under the strip's bound), so only strips near the
+// axes pay for the linear branch.  Certain passes are tallied per lane (no
+// ballot); each lane keeps its first passing row (rows ascend, so the first
+// hit is the lane's smallest).  Lanes inside the FP32 bound but not certain
+// are decided in FP64 behind one vote per iteration.  Every candidate is
+// evaluated by the same band_chunk under the same proven bound as in the
+// row-major loop; only the walk order differs, and the outputs (counts,
+// first canonical pair) do not depend on it.
+constexpr uint32_t kStripG = 4;
 
+// Rows [k, kend) (kend - k a multiple of kStripG, k % 4 == 0) of the strip,
+// one f^-1 form for all of them.  Fast path: the attention test only, one
+// vote per group; a group with some lane that may pass settles: certain
+// passes tallied per lane, the lane's first passing row kept, unsure lanes
+// decided in FP64.
 template <int kL, bool kCubeOnly, int kOut>
-__device__ __forceinline__ void col_run(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t k,
-                                        bool row_ok, float r, uint32_t m0, uint32_t m1, uint32_t& cnt,
-                                        uint32_t& fm, Counters& ct) {
-    const float4* __restrict__ trig4 = reinterpret_cast<const float4*>(A.trig_f);
-    const float2* __restrict__ trig = reinterpret_cast<const float2*>(A.trig_f);
-    uint32_t m = m0;
-    const uint32_t mend = m0 + (m1 - m0) / kColG * kColG;
+__device__ __forceinline__ void strip_rows(const SearchConst* S, const Consts& C, const LaunchArgs& A, float2 sc,
+                                           bool m_ok, uint32_t m, uint32_t k, uint32_t kend, uint32_t& cnt,
+                                           uint32_t& fk, Counters& ct) {
+    const float4* __restrict__ r4p = reinterpret_cast<const float4*>(A.radii_f);
 #pragma unroll 1
-    for (; m != mend; m += kColG) {
-        float2 sv[kColG];
+    for (; k != kend; k += kStripG) {
+        const float4 r4 = __ldg(r4p + (k >> 2));
+        const float rr[kStripG] = {r4.x, r4.y, r4.z, r4.w};
+        float lv[kStripG], qv[kStripG];
+        bool att = false;
 #pragma unroll
-        for (uint32_t g = 0; g < kColG; g += 2) {
-            const float4 t = __ldg(trig4 + ((m + g) >> 1));  // m0 even (block starts at kColW * mb)
-            sv[g] = make_float2(t.x, t.y);
-            sv[g + 1] = make_float2(t.z, t.w);
+        for (uint32_t g = 0; g < kStripG; ++g) {
+            band_chunk<kL, kCubeOnly>(C, rr[g], sc, lv[g], qv[g]);
+            att |= band_attention(C, lv[g], qv[g]);
         }
-        float lv[kColG], qv[kColG];
-        bool uns = false;
+        att &= m_ok;
+        if (__any_sync(kFull, att) && att) {
 #pragma unroll
-        for (uint32_t g = 0; g < kColG; ++g) {
-            band_chunk<kL, kCubeOnly>(C, r, sv[g], lv[g], qv[g]);
-            const bool cert = band_certain(C, lv[g], qv[g]) & row_ok;
-            cnt += cert;
-            if (kOut == kOutFirst) fm = cert ? min(fm, m + g) : fm;
-            uns |= band_attention(C, lv[g], qv[g]) & !band_certain(C, lv[g], qv[g]);
-        }
-        uns &= row_ok;
-        if (__any_sync(kFull, uns) && uns) {
-#pragma unroll 1
-            for (uint32_t g = 0; g < kColG; ++g) {
-                if (band_attention(C, lv[g], qv[g]) & !band_certain(C, lv[g], qv[g])) {
+            for (uint32_t g = 0; g < kStripG; ++g) {
+                bool pass = band_certain(C, lv[g], qv[g]);
+                if (band_attention(C, lv[g], qv[g]) & !pass) {
                     double lp[3], lm[3];
-                    exact_linear(S, A, k, m + g, lp, lm);
-                    const bool pass = exact_band(S, lp, lm, C.flags);
+                    exact_linear(S, A, k + g, m, lp, lm);
+                    pass = exact_band(S, lp, lm, C.flags);
                     ++ct.repairs;
-                    cnt += pass;
-                    if (kOut == kOutFirst && pass) fm = min(fm, m + g);
                 }
+                cnt += pass;
+                if (kOut == kOutFirst && pass) fk = min(fk, k + g);
             }
         }
     }
+}
+
+// Rows [k0, k1) of the strip at angles m0 + lane.
+template <int kL, int kOut>
+__device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t m0,
+                                          uint32_t k0, uint32_t k1, unsigned lane, uint32_t& cnt, uint32_t& fk,
+                                          Counters& ct) {
+    const uint32_t m = m0 + lane;
+    const bool m_ok = m < static_cast<uint32_t>(A.na);
+    const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + (m_ok ? m : A.na - 1));
+    // The strip's cube-only bound rb: no candidate of a row with r < rb
+    // leaves the cube branch of f^-1 (r |s'| < fx0 - u0 and r |c'| < fz0 -
+    // u0 over the strip's angles, with margins as make_search_const's rcube).
+    float gs = fabsf(sc.x), gc = fabsf(sc.y);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        gs = fmaxf(gs, __shfl_xor_sync(kFull, gs, o));
+        gc = fmaxf(gc, __shfl_xor_sync(kFull, gc, o));
+    }
+    const float ex = fmaf(C.fx0 - kU0f, 1.0f - 4e-6f, -1e-6f), ez = fmaf(C.fz0 - kU0f, 1.0f - 4e-6f, -1e-6f);
+    const float rb = fminf(ex / fmaxf(gs, 1e-30f), ez / fmaxf(gc, 1e-30f)) * (1.0f - 1e-6f);
+    // kc: the first row (from k0, in steps of kStripG) whose group reaches rb;
+    // radii ascend, so rows [k0, kc) are cube-only
+    const uint32_t kend = k0 + (k1 - k0) / kStripG * kStripG;  // k0 % 4 == 0
+    uint32_t kc = kend;
+    for (uint32_t kk = k0; kk < kend; kk += 32 * kStripG) {
+        const uint32_t kl = kk + kStripG * lane + kStripG - 1;  // last row of lane's group
+        const unsigned b = __ballot_sync(kFull, kl < kend && !(__ldg(&A.radii_f[kl]) < rb));
+        if (b) {
+            kc = kk + kStripG * static_cast<uint32_t>(__ffs(b) - 1);
+            break;
+        }
+    }
+    strip_rows<kL, true, kOut>(S, C, A, sc, m_ok, m, k0, kc, cnt, fk, ct);
+    strip_rows<kL, false, kOut>(S, C, A, sc, m_ok, m, kc, kend, cnt, fk, ct);
 #pragma unroll 1
-    for (; m < m1; ++m) {
+    for (uint32_t k = kend; k < k1; ++k) {
+        const float r = __ldg(&A.radii_f[k]);
         float l1, q1;
-        band_chunk<kL, kCubeOnly>(C, r, __ldg(trig + m), l1, q1);
+        band_chunk<kL, false>(C, r, sc, l1, q1);
         bool pass = band_certain(C, l1, q1);
-        const bool u = band_attention(C, l1, q1) & !pass & row_ok;
+        const bool u = band_attention(C, l1, q1) & !pass & m_ok;
         if (__any_sync(kFull, u) && u) {
             double lp[3], lm[3];
             exact_linear(S, A, k, m, lp, lm);
             pass = exact_band(S, lp, lm, C.flags);
             ++ct.repairs;
         }
-        pass &= row_ok;
+        pass &= m_ok;
         cnt += pass;
-        if (kOut == kOutFirst && pass) fm = min(fm, m);
+        if (kOut == kOutFirst && pass) fk = min(fk, k);
     }
 }
 
-// One column tile: rows [32 kb, 32 kb + 32) x angles [kColW mb, ...) of
-// search s; per-search count and first canonical pair updated here.
+// One strip tile of search s: strips [lt' * strip_per_tile, ...) of row
+// block kb (lt = kb * tiles_per_block + lt'); per-search count and first
+// canonical pair recorded here.
 template <int kL, int kOut>
-__device__ __forceinline__ void col_tile(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t s,
-                                         uint32_t kb, uint32_t mb, unsigned lane, Counters& ct) {
-    const uint32_t k = 32 * kb + lane;
-    const bool row_ok = k < static_cast<uint32_t>(A.nr);
-    const uint32_t kl = min(32 * kb + 31, static_cast<uint32_t>(A.nr) - 1);  // the block's largest radius
-    const float r = row_ok ? __ldg(&A.radii_f[k]) : 0.0f;
-    const uint32_t m0 = static_cast<uint32_t>(kColW) * mb;
-    const uint32_t m1 = min(m0 + static_cast<uint32_t>(kColW), static_cast<uint32_t>(A.na));
-    uint32_t cnt = 0, fm = 0xffffffffu;
-    if (__ldg(&A.radii_f[kl]) < C.rcube) {  // no row of the block reaches the linear branch of f^-1
-        col_run<kL, true, kOut>(S, C, A, k, row_ok, r, m0, m1, cnt, fm, ct);
-    } else {
-        col_run<kL, false, kOut>(S, C, A, k, row_ok, r, m0, m1, cnt, fm, ct);
+__device__ __forceinline__ void strip_tile(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t s,
+                                           uint32_t lt, unsigned lane, Counters& ct) {
+    const uint32_t kb = lt / A.strip_tiles, st = lt - kb * A.strip_tiles;
+    const uint32_t k0 = kb * A.strip_rows;
+    const uint32_t k1 = min(k0 + A.strip_rows, static_cast<uint32_t>(A.nr));
+    const uint32_t n_strips = (static_cast<uint32_t>(A.na) + 31) / 32;
+    const uint32_t s0 = st * A.strips_per_tile, s1 = min(s0 + A.strips_per_tile, n_strips);
+    uint32_t cnt = 0, first = 0xffffffffu;
+    for (uint32_t q = s0; q < s1; ++q) {
+        uint32_t fk = 0xffffffffu;
+        strip_run<kL, kOut>(S, C, A, 32 * q, k0, k1, lane, cnt, fk, ct);
+        if (kOut == kOutFirst) {
+            const uint32_t mine = fk != 0xffffffffu ? fk * static_cast<uint32_t>(A.na) + 32 * q + lane : 0xffffffffu;
+            first = min(first, __reduce_min_sync(kFull, mine));
+        }
     }
     const uint32_t total = __reduce_add_sync(kFull, cnt);
-    if (kOut == kOutFirst) {
-        const uint32_t mine = fm != 0xffffffffu ? k * static_cast<uint32_t>(A.na) + fm : 0xffffffffu;
-        const uint32_t first = __reduce_min_sync(kFull, mine);
-        if (lane == 0 && total) atomicMin(&A.first_idx[s], first);
+    if (lane == 0 && total) {
+        atomicAdd(&A.counts[s], static_cast<unsigned long long>(total));
+        if (kOut == kOutFirst) atomicMin(&A.first_idx[s], first);
     }
-    if (lane == 0 && total) atomicAdd(&A.counts[s], static_cast<unsigned long long>(total));
 }
 
 // K1: decide every candidate.  Warps claim 4096-candidate tiles (contiguous
@@ -1189,7 +1223,7 @@ __device__ __forceinline__ void col_tile(const SearchConst* S, const Consts& C, 
 // counts; FIRST: counts + first passing index.
 // kPrune (CVG_PATH_PRUNED, band mode): its own instantiation, so that the
 // unpruned loops keep their register allocation (a run-time flag cost 1-2%).
-template <int kMode, int kOut, int kPath, bool kPrune = false>
+template <int kMode, int kOut, int kPath, bool kPrune = false, bool kStrips = false>
 __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -1256,18 +1290,17 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         uint32_t* first = &sm.first[threadIdx.x >> 5];
         Consts C;
         load_consts(S, C);
-        constexpr bool kColsOk = kMode == kModeBand && kPath == kPathFast && kOut != kOutPairs && !kPrune;
-        if (kColsOk && A.cols) {
-            if constexpr (kColsOk) {
-                const uint32_t kb = lt / A.col_mb, mb = lt - kb * A.col_mb;
-                const uint32_t nl = (C.flags >> 10) & 3u;
-                if (nl == 3) {
-                    col_tile<3, kOut>(S, C, A, s, kb, mb, lane, ct);
-                } else if (nl == 2) {
-                    col_tile<2, kOut>(S, C, A, s, kb, mb, lane, ct);
-                } else {
-                    col_tile<1, kOut>(S, C, A, s, kb, mb, lane, ct);
-                }
+        // kStrips (COUNTS / FIRST, band FAST path, LaunchArgs::strips): its
+        // own instantiation, so that the row-major loops keep their registers
+        constexpr bool kStripsOk = kMode == kModeBand && kPath == kPathFast && kOut != kOutPairs && !kPrune;
+        if constexpr (kStrips && kStripsOk) {
+            const uint32_t nl = (C.flags >> 10) & 3u;
+            if (nl == 3) {
+                strip_tile<3, kOut>(S, C, A, s, lt, lane, ct);
+            } else if (nl == 2) {
+                strip_tile<2, kOut>(S, C, A, s, lt, lane, ct);
+            } else {
+                strip_tile<1, kOut>(S, C, A, s, lt, lane, ct);
             }
             // counts / first pair already recorded: cnt stays 0
         } else if (kMode == kModeBand && kPath == kPathFast && A.aligned) {
@@ -1645,6 +1678,10 @@ cudaError_t phase1_t(const LaunchArgs& a, int grid, cudaStream_t st) {
     grid = work_grid(grid, a.n_tiles, kWarpsPerBlock);
     if (kMode == kModeBand && kPath == kPathFast && !kPrune && a.prune) {
         phase1_kernel<kMode, kOut, kPath, true><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);
+        return cudaGetLastError();
+    }
+    if (kMode == kModeBand && kPath == kPathFast && kOut != kOutPairs && !kPrune && a.strips) {
+        phase1_kernel<kMode, kOut, kPath, false, true><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);
         return cudaGetLastError();
     }
     // The dynamic shared-memory sizes are opted into by occupancy_t (plan creation).

@@ -14,7 +14,6 @@ constexpr int kWarpsPerBlock = 8;
 constexpr int kBlock = 32 * kWarpsPerBlock;
 constexpr int kGuessBuckets = 4096;  // code-table buckets over linear [0, 1]
 constexpr float kCodeSlack = 1.0f / 65536;  // code-table bucket widening (>= every usable eps_code)
-constexpr int kColW = kTile / 32;  // angles per column tile (32 rows x 128 angles)
 constexpr int kEmitSpan = 256;      // pairs per emit work item (tile sub-range)
 constexpr int kScanItems = 8;        // tile counts per thread in the offset scan
 constexpr int kScanTile = kBlock * kScanItems;
@@ -118,12 +117,14 @@ struct LaunchArgs {
     uint32_t* worklist;            // [n_tiles * kTile / kEmitSpan] emit items tile << 4 | sub, any order
     uint32_t emit_shift;           // log2 of the pairs per emit item: 8 (kEmitSpan), 9 for dense batches
     uint32_t prune;                // CVG_PATH_PRUNED: skip radius rows that row_surely_fails proves empty
-    // Column tiles (COUNTS / FIRST, band FAST path): tile lt of a search is
-    // radius rows [32 kb, 32 kb + 32) x angles [kColW mb, kColW mb + kColW),
-    // kb = lt / col_mb, mb = lt % col_mb; lane l owns row 32 kb + l and the
-    // warp walks the angles (warp-uniform trig).  0 = row-major tiles.
-    uint32_t cols;
-    uint32_t col_mb;               // angle blocks per search
+    // Strip tiles (COUNTS / FIRST, band FAST path): a strip is 32 angles x
+    // strip_rows radius rows (lane l owns angle 32 q + l, the warp walks the
+    // rows).  Tile lt of a search = row block kb = lt / strip_tiles, strips
+    // [(lt % strip_tiles) * strips_per_tile, +strips_per_tile).  0 = row-major tiles.
+    uint32_t strips;
+    uint32_t strip_rows;           // rows per row block (multiple of 4, or nr)
+    uint32_t strips_per_tile;
+    uint32_t strip_tiles;          // tiles per row block
     unsigned long long* total;     // [1] sum of tile_count (PAIRS)
     uint32_t* out_idx;           // [capacity]
     uint8_t* out_codes;          // [capacity * 6]

@@ -241,20 +241,22 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     p->empty = p->candidates == 0;
     if (p->empty) return CVG_OK;  // search.cpp:409-411
 
-    // Column tiles (32 rows x kColW angles, lane per row) for COUNTS / FIRST
-    // on the band FAST path when there are rows enough to fill the lanes
-    // (cfg4: 64 x 256 grid); else row-major tiles of kTile canonical
-    // candidates.  CVG_COLS=0 turns them off (A/B).
-    static const int cols_env = [] {
-        const char* e = std::getenv("CVG_COLS");
+    // Strip tiles (32 angles x up to 512 rows, lane per angle, uniform
+    // radii) for COUNTS / FIRST on the band FAST path; a tile holds ~16K
+    // candidates (cfg4: one whole 64 x 256 search).  Else row-major tiles of
+    // kTile canonical candidates.  CVG_STRIPS=0 turns them off (A/B).
+    static const int strips_env = [] {
+        const char* e = std::getenv("CVG_STRIPS");
         return e ? std::atoi(e) : 1;
     }();
-    const bool cols = cols_env != 0 && d->output != CVG_OUT_PAIRS && d->output != CVG_OUT_BEST &&
-                      search_mode(d) == cvg::kModeBand && (d->path == CVG_PATH_FAST || d->path == CVG_PATH_MEMO) &&
-                      p->nr >= 24;
-    const uint32_t col_mb = static_cast<uint32_t>((p->na + cvg::kColW - 1) / cvg::kColW);
-    const uint32_t tps = cols ? static_cast<uint32_t>((p->nr + 31) / 32) * col_mb
-                              : static_cast<uint32_t>((cps + cvg::kTile - 1) / cvg::kTile);
+    const bool strips = strips_env != 0 && d->output != CVG_OUT_PAIRS && d->output != CVG_OUT_BEST &&
+                        search_mode(d) == cvg::kModeBand && (d->path == CVG_PATH_FAST || d->path == CVG_PATH_MEMO);
+    const uint32_t strip_rows = static_cast<uint32_t>(std::min(p->nr, 512));
+    const uint32_t n_strips = static_cast<uint32_t>((p->na + 31) / 32);
+    const uint32_t strips_per_tile = std::max<uint32_t>(1, 16384u / (32u * strip_rows));
+    const uint32_t strip_tiles = (n_strips + strips_per_tile - 1) / strips_per_tile;
+    const uint32_t tps = strips ? static_cast<uint32_t>((p->nr + strip_rows - 1) / strip_rows) * strip_tiles
+                                : static_cast<uint32_t>((cps + cvg::kTile - 1) / cvg::kTile);
 
     // ---- host tables ----
     // Per-search constants, deduplicated: searches with the same (target,
@@ -403,8 +405,10 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.na_magic = p->na > 1 ? (UINT64_MAX / static_cast<uint64_t>(p->na)) + 1 : 0;
     A.emit_shift = 8;  // kEmitSpan until an expected pair count says otherwise (plan_set_density)
     A.prune = d->path == CVG_PATH_PRUNED ? 1u : 0u;
-    A.cols = cols ? 1u : 0u;
-    A.col_mb = col_mb;
+    A.strips = strips ? 1u : 0u;
+    A.strip_rows = strip_rows;
+    A.strips_per_tile = strips_per_tile;
+    A.strip_tiles = strip_tiles;
     A.n_tiles = n_tiles;
 
     // ---- per-run workspace --------------------------------------------------

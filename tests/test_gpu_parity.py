@@ -665,11 +665,11 @@ def test_pair_view_cfg2_target_not_list_bound(cv, ctx):
     assert dt < 10.0, dt  # list materialization of 46M ColorPair objects takes minutes
 
 
-# ---- column tiles (COUNTS / FIRST, band FAST path: lane per radius row) -----
+# ---- strip tiles (COUNTS / FIRST, band FAST path: lane per angle) ----------
 
 @pytest.mark.parametrize("nr,na", [(24, 7), (40, 100), (33, 130), (64, 256), (70, 384), (100, 33)])
 @pytest.mark.parametrize("out", ["counts", "first"])
-def test_column_tiles_edge_shapes(ctx, oracle, nr, na, out):
+def test_strip_tiles_edge_shapes(ctx, oracle, nr, na, out):
     """Partial row blocks (nr % 32), partial angle blocks (na % 128), odd na,
     against the oracle search by search; same answer with row-major tiles
     (path 'pruned' keeps row-major tiles)."""
