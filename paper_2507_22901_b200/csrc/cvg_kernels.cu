@@ -449,6 +449,49 @@ __device__ __forceinline__ void band_cube(const Consts& C, float r, float2 sc, f
     band_stats_m<kL>(C, M, minl, maxq);
 }
 
+// Strip form of the cube-only band statistic.  In band_cube, with ux = r s'
+// and uz = r c' (s' = sin/500, c' = cos/200 of the lane's angle),
+//   A_c = mxs_c (fx0^3 + 3 fx0 ux^2) + mzs_c (fz0^3 + 3 fz0 uz^2) + cys_c
+//       = K0_c + r^2 K2_c,
+//   B_c = mxs_c ux (3 fx0^2 + ux^2) - mzs_c uz (3 fz0^2 + uz^2)
+//       = r L1_c + r^3 L3_c,
+// K0_c per search, K2_c, L1_c, L3_c per search and angle: computed once per
+// strip (strip_setup), so a candidate costs 2 + 3 operations per channel
+// plus |A| + |B| instead of the 25 of band_cube.  r, r^2, r^3 are
+// warp-uniform row tables.  make_search_const bounds this FP32 sequence too
+// (20u per term magnitude) and the band thresholds cover it; the AUDIT path
+// checks it against FP64 on every cube-only candidate.
+struct StripConsts {
+    float k0[3], k2[3], l1[3], l3[3];
+};
+
+__device__ __forceinline__ void strip_setup(const Consts& C, float2 sc, StripConsts& Q) {
+    const float s2 = __fmul_rn(sc.x, sc.x), c2 = __fmul_rn(sc.y, sc.y);
+    const float px = __fmul_rn(C.cube[2], s2), pz = __fmul_rn(C.cube[5], c2);  // 3 f0 s'^2
+    const float s1x = __fmul_rn(C.cube[1], sc.x), s1z = __fmul_rn(C.cube[4], sc.y);  // 3 f0^2 s'
+    const float s3x = __fmul_rn(s2, sc.x), s3z = __fmul_rn(c2, sc.y);  // s'^3
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        Q.k0[q] = fmaf(C.mxs[q], C.cube[0], fmaf(C.mzs[q], C.cube[3], C.cys[q]));
+        Q.k2[q] = fmaf(C.mxs[q], px, __fmul_rn(C.mzs[q], pz));
+        Q.l1[q] = fmaf(C.mxs[q], s1x, -__fmul_rn(C.mzs[q], s1z));
+        Q.l3[q] = fmaf(C.mxs[q], s3x, -__fmul_rn(C.mzs[q], s3z));
+    }
+}
+
+template <int kL>
+__device__ __forceinline__ void strip_stat(const Consts& C, const StripConsts& Q, float r, float r2, float r3,
+                                           float& minl, float& maxq) {
+    float M[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const float a = fmaf(Q.k2[q], r2, Q.k0[q]);
+        const float b = fmaf(Q.l3[q], r3, __fmul_rn(Q.l1[q], r));
+        M[q] = fabsf(a) + fabsf(b);
+    }
+    band_stats_m<kL>(C, M, minl, maxq);
+}
+
 __device__ __forceinline__ bool band_attention(const Consts& C, float minl, float maxq) {
     return (minl >= C.la) & (maxq <= C.qa);
 }
@@ -708,6 +751,15 @@ __device__ __forceinline__ bool candidate_pass(const Smem& sm, const SearchConst
             const bool pass2 = band_certain(C, l2, q2);
             const bool unsure2 = band_attention(C, l2, q2) & !pass2;
             if (active) ct.violations += !unsure2 && ex != pass2;
+            // and the strip form (strip tiles, COUNTS / FIRST)
+            StripConsts Q;
+            strip_setup(C, sc, Q);
+            const double rd = __ldg(&A.radii_d[k]);
+            float l3, q3;
+            strip_stat<0>(C, Q, r, static_cast<float>(rd * rd), static_cast<float>(rd * rd * rd), l3, q3);
+            const bool pass3 = band_certain(C, l3, q3);
+            const bool unsure3 = band_attention(C, l3, q3) & !pass3;
+            if (active) ct.violations += !unsure3 && ex != pass3;
         }
         if (active) {
             ct.violations += !unsure && ex != pass;
@@ -1099,40 +1151,64 @@ __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C,
 // first canonical pair) do not depend on it.
 constexpr uint32_t kStripG = 4;
 
+
 // Rows [k, kend) (kend - k a multiple of kStripG, k % 4 == 0) of the strip,
 // one f^-1 form for all of them.  Fast path: the attention test only, one
 // vote per group; a group with some lane that may pass settles: certain
 // passes tallied per lane, the lane's first passing row kept, unsure lanes
 // decided in FP64.
 template <int kL, bool kCubeOnly, int kOut>
-__device__ __forceinline__ void strip_rows(const SearchConst* S, const Consts& C, const LaunchArgs& A, float2 sc,
-                                           bool m_ok, uint32_t m, uint32_t k, uint32_t kend, uint32_t& cnt,
-                                           uint32_t& fk, Counters& ct) {
+__device__ __forceinline__ void strip_rows(const SearchConst* S, const Consts& C, const StripConsts& Q,
+                                           const LaunchArgs& A, float2 sc, bool m_ok, uint32_t m, uint32_t k,
+                                           uint32_t kend, uint32_t& cnt, uint32_t& fk, Counters& ct) {
     const float4* __restrict__ r4p = reinterpret_cast<const float4*>(A.radii_f);
+    const float4* __restrict__ r24p = reinterpret_cast<const float4*>(A.radii2_f);
+    const float4* __restrict__ r34p = reinterpret_cast<const float4*>(A.radii3_f);
 #pragma unroll 1
     for (; k != kend; k += kStripG) {
         const float4 r4 = __ldg(r4p + (k >> 2));
         const float rr[kStripG] = {r4.x, r4.y, r4.z, r4.w};
         float lv[kStripG], qv[kStripG];
         bool att = false;
+        if (kCubeOnly) {
+            const float4 q2 = __ldg(r24p + (k >> 2)), q3 = __ldg(r34p + (k >> 2));
+            const float r2[kStripG] = {q2.x, q2.y, q2.z, q2.w}, r3[kStripG] = {q3.x, q3.y, q3.z, q3.w};
 #pragma unroll
-        for (uint32_t g = 0; g < kStripG; ++g) {
-            band_chunk<kL, kCubeOnly>(C, rr[g], sc, lv[g], qv[g]);
-            att |= band_attention(C, lv[g], qv[g]);
+            for (uint32_t g = 0; g < kStripG; ++g) {
+                strip_stat<kL>(C, Q, rr[g], r2[g], r3[g], lv[g], qv[g]);
+                att |= band_attention(C, lv[g], qv[g]);
+            }
+        } else {
+#pragma unroll
+            for (uint32_t g = 0; g < kStripG; ++g) {
+                band_chunk<kL, false>(C, rr[g], sc, lv[g], qv[g]);
+                att |= band_attention(C, lv[g], qv[g]);
+            }
         }
         att &= m_ok;
         if (__any_sync(kFull, att) && att) {
+            // certain passes counted per lane (the lane's first passing row
+            // kept); the unsure lanes, rare, behind one more vote
+            bool uns = false;
 #pragma unroll
             for (uint32_t g = 0; g < kStripG; ++g) {
-                bool pass = band_certain(C, lv[g], qv[g]);
-                if (band_attention(C, lv[g], qv[g]) & !pass) {
-                    double lp[3], lm[3];
-                    exact_linear(S, A, k + g, m, lp, lm);
-                    pass = exact_band(S, lp, lm, C.flags);
-                    ++ct.repairs;
+                const bool cert = band_certain(C, lv[g], qv[g]);
+                cnt += cert;
+                if (kOut == kOutFirst && cert) fk = min(fk, k + g);
+                uns |= band_attention(C, lv[g], qv[g]) & !cert;
+            }
+            if (uns) {
+#pragma unroll 1
+                for (uint32_t g = 0; g < kStripG; ++g) {
+                    if (band_attention(C, lv[g], qv[g]) & !band_certain(C, lv[g], qv[g])) {
+                        double lp[3], lm[3];
+                        exact_linear(S, A, k + g, m, lp, lm);
+                        const bool pass = exact_band(S, lp, lm, C.flags);
+                        ++ct.repairs;
+                        cnt += pass;
+                        if (kOut == kOutFirst && pass) fk = min(fk, k + g);
+                    }
                 }
-                cnt += pass;
-                if (kOut == kOutFirst && pass) fk = min(fk, k + g);
             }
         }
     }
@@ -1148,15 +1224,12 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C,
     const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + (m_ok ? m : A.na - 1));
     // The strip's cube-only bound rb: no candidate of a row with r < rb
     // leaves the cube branch of f^-1 (r |s'| < fx0 - u0 and r |c'| < fz0 -
-    // u0 over the strip's angles, with margins as make_search_const's rcube).
-    float gs = fabsf(sc.x), gc = fabsf(sc.y);
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        gs = fmaxf(gs, __shfl_xor_sync(kFull, gs, o));
-        gc = fmaxf(gc, __shfl_xor_sync(kFull, gc, o));
-    }
+    // u0 over the strip's angles, with margins as make_search_const's
+    // rcube).  strip_inv[q] = 1 / the strip's largest |s'|, |c'| (host,
+    // rounded down; +inf for an all-zero column).
+    const float2 inv = __ldg(reinterpret_cast<const float2*>(A.strip_inv) + (m0 >> 5));
     const float ex = fmaf(C.fx0 - kU0f, 1.0f - 4e-6f, -1e-6f), ez = fmaf(C.fz0 - kU0f, 1.0f - 4e-6f, -1e-6f);
-    const float rb = fminf(ex / fmaxf(gs, 1e-30f), ez / fmaxf(gc, 1e-30f)) * (1.0f - 1e-6f);
+    const float rb = fminf(ex * inv.x, ez * inv.y) * (1.0f - 1e-6f);
     // kc: the first row (from k0, in steps of kStripG) whose group reaches rb;
     // radii ascend, so rows [k0, kc) are cube-only
     const uint32_t kend = k0 + (k1 - k0) / kStripG * kStripG;  // k0 % 4 == 0
@@ -1169,8 +1242,10 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C,
             break;
         }
     }
-    strip_rows<kL, true, kOut>(S, C, A, sc, m_ok, m, k0, kc, cnt, fk, ct);
-    strip_rows<kL, false, kOut>(S, C, A, sc, m_ok, m, kc, kend, cnt, fk, ct);
+    StripConsts Q;
+    strip_setup(C, sc, Q);
+    strip_rows<kL, true, kOut>(S, C, Q, A, sc, m_ok, m, k0, kc, cnt, fk, ct);
+    strip_rows<kL, false, kOut>(S, C, Q, A, sc, m_ok, m, kc, kend, cnt, fk, ct);
 #pragma unroll 1
     for (uint32_t k = kend; k < k1; ++k) {
         const float r = __ldg(&A.radii_f[k]);

@@ -125,6 +125,9 @@ struct LaunchArgs {
     uint32_t strip_rows;           // rows per row block (multiple of 4, or nr)
     uint32_t strips_per_tile;
     uint32_t strip_tiles;          // tiles per row block
+    const float* strip_inv;        // [n_strips][2]: 1 / the strip's largest |sin/500|, |cos/200| (rounded down)
+    const float* radii2_f;         // [nr]: float(r^2), float(r^3) of the double radii (strip form)
+    const float* radii3_f;
     unsigned long long* total;     // [1] sum of tile_count (PAIRS)
     uint32_t* out_idx;           // [capacity]
     uint8_t* out_codes;          // [capacity * 6]

@@ -328,6 +328,9 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     const bool signal = p->mode == cvg::kModeSignal;
     const size_t o_stab = signal ? L.take(sizeof(T.stab)) : 0;
     const size_t o_bands = p->best ? L.take(sizeof(double) * 2 * p->n) : 0;
+    const size_t o_sinv = strips ? L.take(sizeof(float) * 2 * n_strips) : 0;
+    const size_t o_r2 = strips ? L.take(sizeof(float) * p->nr) : 0;
+    const size_t o_r3 = strips ? L.take(sizeof(float) * p->nr) : 0;
     const size_t bytes = L.off;
     p->input_bytes = bytes;
     p->t_prep_end = now_ms();
@@ -365,6 +368,33 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     std::memcpy(stage + o_thd, T.thr, sizeof(double) * 256);
     std::memcpy(stage + o_ctab, T.ctab, sizeof(T.ctab));
     if (signal) std::memcpy(stage + o_stab, T.stab, sizeof(T.stab));
+    if (strips) {
+        // r^2 and r^3 of the double radii, rounded once to float (strip form)
+        auto* r2 = reinterpret_cast<float*>(stage + o_r2);
+        auto* r3 = reinterpret_cast<float*>(stage + o_r3);
+        for (int k = 0; k < p->nr; ++k) {
+            const double r = d->radii[k];
+            r2[k] = static_cast<float>(r * r);
+            r3[k] = static_cast<float>(r * r * r);
+        }
+        // per strip of 32 angles: 1 / max |s'|, 1 / max |c'| over the float
+        // trig values the kernel uses, rounded down (FLT_MAX for an all-zero
+        // column: 0 * FLT_MAX stays 0 in the kernel's bound)
+        auto* inv = reinterpret_cast<float*>(stage + o_sinv);
+        for (uint32_t q = 0; q < n_strips; ++q) {
+            float gs = 0.f, gc = 0.f;
+            for (int m = 32 * static_cast<int>(q); m < std::min(p->na, 32 * static_cast<int>(q) + 32); ++m) {
+                gs = std::max(gs, std::fabs(trig_f[2 * m]));
+                gc = std::max(gc, std::fabs(trig_f[2 * m + 1]));
+            }
+            for (int c = 0; c < 2; ++c) {
+                const double g = c ? gc : gs;
+                float v = g > 0 ? static_cast<float>(1.0 / g) : FLT_MAX;
+                if (g > 0 && static_cast<double>(v) > 1.0 / g) v = std::nextafter(v, 0.0f);
+                inv[2 * q + c] = std::min(v, FLT_MAX);
+            }
+        }
+    }
     if (p->best) {
         // (v_th, low_band) per search for classification_margin (search.hpp:29-35: low = v_th * r_novib)
         auto* bands = reinterpret_cast<double*>(stage + o_bands);
@@ -409,6 +439,9 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.strip_rows = strip_rows;
     A.strips_per_tile = strips_per_tile;
     A.strip_tiles = strip_tiles;
+    A.strip_inv = strips ? at<const float>(p->d_const, o_sinv) : nullptr;
+    A.radii2_f = strips ? at<const float>(p->d_const, o_r2) : nullptr;
+    A.radii3_f = strips ? at<const float>(p->d_const, o_r3) : nullptr;
     A.n_tiles = n_tiles;
 
     // ---- per-run workspace --------------------------------------------------

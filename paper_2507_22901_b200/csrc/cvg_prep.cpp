@@ -497,8 +497,26 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
         const auto [e_a, a_max] = lin_err_of(cx.a, cz.a, std::fabs(mx / hh), std::fabs(mz / hh), (cy - cc) / hh);
         const auto [e_b, b_max] = lin_err_of(cx.b, cz.b, std::fabs(mx / hh), std::fabs(mz / hh), 0.0);
         const double e_ab = e_a + e_b + u * (a_max + b_max + e_a + e_b);
-        const double m_max = std::max(d_max, a_max + b_max);
-        const double e_m = 1.05 * (std::max(e_d, e_ab) + 4 * std::ldexp(1.0, -53) * (m_max + 2.0)) + 1e-12 / hh;
+        // strip form (the kernel's strip_stat, cube-only rows of a strip):
+        // A_c = fma(K2_c, r^2, K0_c), B_c = fma(L3_c, r^3, fl(L1_c * r)) with
+        // K0_c = mxs fx0^3 + mzs fz0^3 + cys, K2_c = mxs 3fx0 s'^2 + mzs 3fz0 c'^2,
+        // L1_c = mxs 3fx0^2 s' - mzs 3fz0^2 c', L3_c = mxs s'^3 - mzs c'^3, all
+        // in FP32 from the float constants and the float trig / r, r^2, r^3
+        // tables.  Term by term (u = 2^-24; strip_setup's operation order):
+        // |err K0| <= 4u TA0, |err K2 r^2| <= 10u TA2, final rounding u |A|
+        // (TA = TA0 + TA2 the magnitudes of the cube and U^2 parts), and
+        // |err fl(L1 r)| <= 8u TB1, |err L3 r^3| <= 9u TB3, rounding u |B|;
+        // bounded here by 20u TA and 20u TB.
+        const double fxa = std::fabs(fx0), fza = std::fabs(fz0);
+        const double uxm = rmax * kInv500, uzm = rmax * kInv200;
+        const double amx = std::fabs(mx / hh), amz = std::fabs(mz / hh);
+        const double ta_s = amx * (fxa * fxa * fxa + 3.0 * fxa * uxm * uxm) +
+                            amz * (fza * fza * fza + 3.0 * fza * uzm * uzm) + std::fabs((cy - cc) / hh);
+        const double tb_s = amx * uxm * (3.0 * fxa * fxa + uxm * uxm) + amz * uzm * (3.0 * fza * fza + uzm * uzm);
+        const double e_as = 20.0 * u * ta_s, e_bs = 20.0 * u * tb_s;
+        const double e_abs = e_as + e_bs + u * (ta_s + tb_s + e_as + e_bs);
+        const double m_max = std::max({d_max, a_max + b_max, ta_s + tb_s});
+        const double e_m = 1.05 * (std::max({e_d, e_ab, e_abs}) + 4 * std::ldexp(1.0, -53) * (m_max + 2.0)) + 1e-12 / hh;
         (bits[c] ? eps_l : eps_q) = std::max(bits[c] ? eps_l : eps_q, e_m);
     }
     S.la = round_down_f(1.0 - eps_l);
