@@ -393,8 +393,8 @@ __device__ __forceinline__ void fast_linear(float fx0, float fz0, const float* m
 //   certain pass:                            minl >  lp and maxq <  qp
 // and only attention-but-not-certain candidates go to the FP64 path.
 // kL = loud count (1..3), 0 = read it from the flags at run time.
-template <int kL>
-__device__ __forceinline__ void band_stats_m(const Consts& C, const float* M, float& minl, float& maxq) {
+template <int kL, class CT>
+__device__ __forceinline__ void band_stats_m(const CT& C, const float* M, float& minl, float& maxq) {
     const int L = kL ? kL : static_cast<int>((C.flags >> 10) & 3u);
     minl = INFINITY;
     maxq = -INFINITY;
@@ -465,6 +465,21 @@ struct StripConsts {
     float k0[3], k2[3], l1[3], l3[3];
 };
 
+// The band thresholds alone (the cube-only strip loop holds no other search
+// constant, so the linear-form constants are not live across it).
+struct ThrConsts {
+    float la, qa, lp, qp;
+    uint32_t flags;
+};
+
+// A copy of a pointer the compiler cannot see through: loads through it are
+// not merged with earlier loads through the original (forces a reload).
+template <class T>
+__device__ __forceinline__ const T* opaque_ptr(const T* p) {
+    asm volatile("" : "+l"(p));
+    return p;
+}
+
 __device__ __forceinline__ void strip_setup(const Consts& C, float2 sc, StripConsts& Q) {
     const float s2 = __fmul_rn(sc.x, sc.x), c2 = __fmul_rn(sc.y, sc.y);
     const float px = __fmul_rn(C.cube[2], s2), pz = __fmul_rn(C.cube[5], c2);  // 3 f0 s'^2
@@ -479,8 +494,8 @@ __device__ __forceinline__ void strip_setup(const Consts& C, float2 sc, StripCon
     }
 }
 
-template <int kL>
-__device__ __forceinline__ void strip_stat(const Consts& C, const StripConsts& Q, float r, float r2, float r3,
+template <int kL, class CT>
+__device__ __forceinline__ void strip_stat(const CT& C, const StripConsts& Q, float r, float r2, float r3,
                                            float& minl, float& maxq) {
     float M[3];
 #pragma unroll
@@ -492,11 +507,13 @@ __device__ __forceinline__ void strip_stat(const Consts& C, const StripConsts& Q
     band_stats_m<kL>(C, M, minl, maxq);
 }
 
-__device__ __forceinline__ bool band_attention(const Consts& C, float minl, float maxq) {
+template <class CT>
+__device__ __forceinline__ bool band_attention(const CT& C, float minl, float maxq) {
     return (minl >= C.la) & (maxq <= C.qa);
 }
 
-__device__ __forceinline__ bool band_certain(const Consts& C, float minl, float maxq) {
+template <class CT>
+__device__ __forceinline__ bool band_certain(const CT& C, float minl, float maxq) {
     return (minl > C.lp) & (maxq < C.qp);
 }
 
@@ -1153,25 +1170,27 @@ constexpr uint32_t kStripG = 4;
 
 
 // Rows [k, kend) (kend - k a multiple of kStripG, k % 4 == 0) of the strip,
-// one f^-1 form for all of them.  Fast path: the attention test only, one
-// vote per group; a group with some lane that may pass settles: certain
-// passes tallied per lane, the lane's first passing row kept, unsure lanes
-// decided in FP64.
-template <int kL, bool kCubeOnly, int kOut>
-__device__ __forceinline__ void strip_rows(const SearchConst* S, const Consts& C, const StripConsts& Q,
+// one f^-1 form for all of them: kCubeOnly = the strip form (strip_stat,
+// constants Q and thresholds T only), else band_chunk (full constants C).
+// Fast path: the attention test only, one vote per group; a group with some
+// lane that may pass settles: certain passes tallied per lane, the lane's
+// first passing row kept, unsure lanes decided in FP64.
+template <int kL, bool kCubeOnly, int kOut, class CT>
+__device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, const StripConsts& Q,
                                            const LaunchArgs& A, float2 sc, bool m_ok, uint32_t m, uint32_t k,
                                            uint32_t kend, uint32_t& cnt, uint32_t& fk, Counters& ct) {
-    const float4* __restrict__ r4p = reinterpret_cast<const float4*>(A.radii_f);
-    const float4* __restrict__ r24p = reinterpret_cast<const float4*>(A.radii2_f);
-    const float4* __restrict__ r34p = reinterpret_cast<const float4*>(A.radii3_f);
+    // radius groups: {r[4j..4j+3]}, {r^2}, {r^3} as three consecutive float4
+    const float4* __restrict__ rg = reinterpret_cast<const float4*>(A.radius_groups) + 3 * (k >> 2);
 #pragma unroll 1
-    for (; k != kend; k += kStripG) {
-        const float4 r4 = __ldg(r4p + (k >> 2));
+    for (; k != kend; k += kStripG, rg += 3) {
+        const float4 r4 = __ldg(rg);
         const float rr[kStripG] = {r4.x, r4.y, r4.z, r4.w};
         float lv[kStripG], qv[kStripG];
         bool att = false;
-        if (kCubeOnly) {
-            const float4 q2 = __ldg(r24p + (k >> 2)), q3 = __ldg(r34p + (k >> 2));
+        if constexpr (kCubeOnly) {
+            // lanes past the last angle hold zero strip constants: every
+            // channel's statistic is 0, so no loud channel leaves its band
+            const float4 q2 = __ldg(rg + 1), q3 = __ldg(rg + 2);
             const float r2[kStripG] = {q2.x, q2.y, q2.z, q2.w}, r3[kStripG] = {q3.x, q3.y, q3.z, q3.w};
 #pragma unroll
             for (uint32_t g = 0; g < kStripG; ++g) {
@@ -1184,11 +1203,11 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const Consts& C
                 band_chunk<kL, false>(C, rr[g], sc, lv[g], qv[g]);
                 att |= band_attention(C, lv[g], qv[g]);
             }
+            att &= m_ok;
         }
-        att &= m_ok;
         if (__any_sync(kFull, att) && att) {
             // certain passes counted per lane (the lane's first passing row
-            // kept); the unsure lanes, rare, behind one more vote
+            // kept); the unsure lanes, rare, decided in FP64
             bool uns = false;
 #pragma unroll
             for (uint32_t g = 0; g < kStripG; ++g) {
@@ -1198,12 +1217,12 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const Consts& C
                 uns |= band_attention(C, lv[g], qv[g]) & !cert;
             }
             if (uns) {
-#pragma unroll 1
-                for (uint32_t g = 0; g < kStripG; ++g) {
+#pragma unroll
+                for (uint32_t g = 0; g < kStripG; ++g) {  // unrolled: lv / qv stay in registers
                     if (band_attention(C, lv[g], qv[g]) & !band_certain(C, lv[g], qv[g])) {
                         double lp[3], lm[3];
                         exact_linear(S, A, k + g, m, lp, lm);
-                        const bool pass = exact_band(S, lp, lm, C.flags);
+                        const bool pass = exact_band(S, lp, lm, __ldg(&S->flags));
                         ++ct.repairs;
                         cnt += pass;
                         if (kOut == kOutFirst && pass) fk = min(fk, k + g);
@@ -1214,37 +1233,50 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const Consts& C
     }
 }
 
-// Rows [k0, k1) of the strip at angles m0 + lane.
+// Rows [k0, k1) of the strip at angles m0 + lane.  The full constants are
+// loaded for the strip set-up and again (through an opaque pointer, so the
+// two loads are not merged) for the linear rows: during the cube-only rows
+// only the strip constants and the thresholds are live.
 template <int kL, int kOut>
-__device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t m0,
-                                          uint32_t k0, uint32_t k1, unsigned lane, uint32_t& cnt, uint32_t& fk,
-                                          Counters& ct) {
+__device__ __forceinline__ void strip_run(const SearchConst* S, const LaunchArgs& A, uint32_t m0, uint32_t k0,
+                                          uint32_t k1, unsigned lane, uint32_t& cnt, uint32_t& fk, Counters& ct) {
     const uint32_t m = m0 + lane;
     const bool m_ok = m < static_cast<uint32_t>(A.na);
     const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + (m_ok ? m : A.na - 1));
-    // The strip's cube-only bound rb: no candidate of a row with r < rb
-    // leaves the cube branch of f^-1 (r |s'| < fx0 - u0 and r |c'| < fz0 -
-    // u0 over the strip's angles, with margins as make_search_const's
-    // rcube).  strip_inv[q] = 1 / the strip's largest |s'|, |c'| (host,
-    // rounded down; +inf for an all-zero column).
-    const float2 inv = __ldg(reinterpret_cast<const float2*>(A.strip_inv) + (m0 >> 5));
-    const float ex = fmaf(C.fx0 - kU0f, 1.0f - 4e-6f, -1e-6f), ez = fmaf(C.fz0 - kU0f, 1.0f - 4e-6f, -1e-6f);
-    const float rb = fminf(ex * inv.x, ez * inv.y) * (1.0f - 1e-6f);
-    // kc: the first row (from k0, in steps of kStripG) whose group reaches rb;
-    // radii ascend, so rows [k0, kc) are cube-only
     const uint32_t kend = k0 + (k1 - k0) / kStripG * kStripG;  // k0 % 4 == 0
-    uint32_t kc = kend;
-    for (uint32_t kk = k0; kk < kend; kk += 32 * kStripG) {
-        const uint32_t kl = kk + kStripG * lane + kStripG - 1;  // last row of lane's group
-        const unsigned b = __ballot_sync(kFull, kl < kend && !(__ldg(&A.radii_f[kl]) < rb));
-        if (b) {
-            kc = kk + kStripG * static_cast<uint32_t>(__ffs(b) - 1);
-            break;
-        }
-    }
     StripConsts Q;
-    strip_setup(C, sc, Q);
-    strip_rows<kL, true, kOut>(S, C, Q, A, sc, m_ok, m, k0, kc, cnt, fk, ct);
+    ThrConsts T;
+    uint32_t kc = kend;
+    {
+        Consts C;
+        load_consts(S, C);
+        T = ThrConsts{C.la, C.qa, C.lp, C.qp, C.flags};
+        // The strip's cube-only bound rb: no candidate of a row with r < rb
+        // leaves the cube branch of f^-1 (r |s'| < fx0 - u0 and r |c'| <
+        // fz0 - u0 over the strip's angles, with margins as
+        // make_search_const's rcube).  strip_inv[q] = 1 / the strip's
+        // largest |s'|, |c'| (host, rounded down; FLT_MAX for an all-zero
+        // column).
+        const float2 inv = __ldg(reinterpret_cast<const float2*>(A.strip_inv) + (m0 >> 5));
+        const float ex = fmaf(C.fx0 - kU0f, 1.0f - 4e-6f, -1e-6f), ez = fmaf(C.fz0 - kU0f, 1.0f - 4e-6f, -1e-6f);
+        const float rb = fminf(ex * inv.x, ez * inv.y) * (1.0f - 1e-6f);
+        // kc: the first row (from k0, in steps of kStripG) whose group
+        // reaches rb; radii ascend, so rows [k0, kc) are cube-only
+        for (uint32_t kk = k0; kk < kend; kk += 32 * kStripG) {
+            const uint32_t kl = kk + kStripG * lane + kStripG - 1;  // last row of lane's group
+            const unsigned b = __ballot_sync(kFull, kl < kend && !(__ldg(&A.radii_f[kl]) < rb));
+            if (b) {
+                kc = kk + kStripG * static_cast<uint32_t>(__ffs(b) - 1);
+                break;
+            }
+        }
+        strip_setup(C, sc, Q);
+        if (!m_ok) Q = StripConsts{};  // the partial strip's idle lanes never pass (strip_rows)
+    }
+    strip_rows<kL, true, kOut>(S, T, Q, A, sc, m_ok, m, k0, kc, cnt, fk, ct);
+    if (kc == k1) return;
+    Consts C;
+    load_consts(opaque_ptr(S), C);
     strip_rows<kL, false, kOut>(S, C, Q, A, sc, m_ok, m, kc, kend, cnt, fk, ct);
 #pragma unroll 1
     for (uint32_t k = kend; k < k1; ++k) {
@@ -1269,8 +1301,8 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C,
 // block kb (lt = kb * tiles_per_block + lt'); per-search count and first
 // canonical pair recorded here.
 template <int kL, int kOut>
-__device__ __forceinline__ void strip_tile(const SearchConst* S, const Consts& C, const LaunchArgs& A, uint32_t s,
-                                           uint32_t lt, unsigned lane, Counters& ct) {
+__device__ __forceinline__ void strip_tile(const SearchConst* S, const LaunchArgs& A, uint32_t s, uint32_t lt,
+                                           unsigned lane, Counters& ct) {
     const uint32_t kb = lt / A.strip_tiles, st = lt - kb * A.strip_tiles;
     const uint32_t k0 = kb * A.strip_rows;
     const uint32_t k1 = min(k0 + A.strip_rows, static_cast<uint32_t>(A.nr));
@@ -1279,7 +1311,7 @@ __device__ __forceinline__ void strip_tile(const SearchConst* S, const Consts& C
     uint32_t cnt = 0, first = 0xffffffffu;
     for (uint32_t q = s0; q < s1; ++q) {
         uint32_t fk = 0xffffffffu;
-        strip_run<kL, kOut>(S, C, A, 32 * q, k0, k1, lane, cnt, fk, ct);
+        strip_run<kL, kOut>(S, A, 32 * q, k0, k1, lane, cnt, fk, ct);
         if (kOut == kOutFirst) {
             const uint32_t mine = fk != 0xffffffffu ? fk * static_cast<uint32_t>(A.na) + 32 * q + lane : 0xffffffffu;
             first = min(first, __reduce_min_sync(kFull, mine));
@@ -1369,13 +1401,13 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         // own instantiation, so that the row-major loops keep their registers
         constexpr bool kStripsOk = kMode == kModeBand && kPath == kPathFast && kOut != kOutPairs && !kPrune;
         if constexpr (kStrips && kStripsOk) {
-            const uint32_t nl = (C.flags >> 10) & 3u;
+            const uint32_t nl = (__ldg(&S->flags) >> 10) & 3u;
             if (nl == 3) {
-                strip_tile<3, kOut>(S, C, A, s, lt, lane, ct);
+                strip_tile<3, kOut>(S, A, s, lt, lane, ct);
             } else if (nl == 2) {
-                strip_tile<2, kOut>(S, C, A, s, lt, lane, ct);
+                strip_tile<2, kOut>(S, A, s, lt, lane, ct);
             } else {
-                strip_tile<1, kOut>(S, C, A, s, lt, lane, ct);
+                strip_tile<1, kOut>(S, A, s, lt, lane, ct);
             }
             // counts / first pair already recorded: cnt stays 0
         } else if (kMode == kModeBand && kPath == kPathFast && A.aligned) {

@@ -126,8 +126,8 @@ struct LaunchArgs {
     uint32_t strips_per_tile;
     uint32_t strip_tiles;          // tiles per row block
     const float* strip_inv;        // [n_strips][2]: 1 / the strip's largest |sin/500|, |cos/200| (rounded down)
-    const float* radii2_f;         // [nr]: float(r^2), float(r^3) of the double radii (strip form)
-    const float* radii3_f;
+    const float* radius_groups;    // [ceil(nr/4)][3][4]: per 4 rows float(r), float(r^2), float(r^3)
+                                   // of the double radii (strip form; padded with the last radius)
     unsigned long long* total;     // [1] sum of tile_count (PAIRS)
     uint32_t* out_idx;           // [capacity]
     uint8_t* out_codes;          // [capacity * 6]

@@ -329,8 +329,8 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     const size_t o_stab = signal ? L.take(sizeof(T.stab)) : 0;
     const size_t o_bands = p->best ? L.take(sizeof(double) * 2 * p->n) : 0;
     const size_t o_sinv = strips ? L.take(sizeof(float) * 2 * n_strips) : 0;
-    const size_t o_r2 = strips ? L.take(sizeof(float) * p->nr) : 0;
-    const size_t o_r3 = strips ? L.take(sizeof(float) * p->nr) : 0;
+    const size_t n_rgroups = static_cast<size_t>((p->nr + 3) / 4);
+    const size_t o_rg = strips ? L.take(sizeof(float) * 12 * n_rgroups) : 0;
     const size_t bytes = L.off;
     p->input_bytes = bytes;
     p->t_prep_end = now_ms();
@@ -369,13 +369,16 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     std::memcpy(stage + o_ctab, T.ctab, sizeof(T.ctab));
     if (signal) std::memcpy(stage + o_stab, T.stab, sizeof(T.stab));
     if (strips) {
-        // r^2 and r^3 of the double radii, rounded once to float (strip form)
-        auto* r2 = reinterpret_cast<float*>(stage + o_r2);
-        auto* r3 = reinterpret_cast<float*>(stage + o_r3);
-        for (int k = 0; k < p->nr; ++k) {
-            const double r = d->radii[k];
-            r2[k] = static_cast<float>(r * r);
-            r3[k] = static_cast<float>(r * r * r);
+        // radius groups of 4 rows: r, r^2, r^3 of the double radii, each
+        // rounded once to float (strip form); padded with the last radius
+        auto* rg = reinterpret_cast<float*>(stage + o_rg);
+        for (size_t j = 0; j < n_rgroups; ++j) {
+            for (int i = 0; i < 4; ++i) {
+                const double r = d->radii[std::min<size_t>(4 * j + i, static_cast<size_t>(p->nr - 1))];
+                rg[12 * j + i] = static_cast<float>(r);
+                rg[12 * j + 4 + i] = static_cast<float>(r * r);
+                rg[12 * j + 8 + i] = static_cast<float>(r * r * r);
+            }
         }
         // per strip of 32 angles: 1 / max |s'|, 1 / max |c'| over the float
         // trig values the kernel uses, rounded down (FLT_MAX for an all-zero
@@ -440,8 +443,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.strips_per_tile = strips_per_tile;
     A.strip_tiles = strip_tiles;
     A.strip_inv = strips ? at<const float>(p->d_const, o_sinv) : nullptr;
-    A.radii2_f = strips ? at<const float>(p->d_const, o_r2) : nullptr;
-    A.radii3_f = strips ? at<const float>(p->d_const, o_r3) : nullptr;
+    A.radius_groups = strips ? at<const float>(p->d_const, o_rg) : nullptr;
     A.n_tiles = n_tiles;
 
     // ---- per-run workspace --------------------------------------------------
