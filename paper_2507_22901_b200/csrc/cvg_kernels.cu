@@ -1153,6 +1153,9 @@ __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C,
 }
 
 // ---- Strip tiles (COUNTS / FIRST, band FAST path) --------------------------
+#ifndef CVG_STRIP_G
+#define CVG_STRIP_G 4
+#endif
 // A strip is 32 consecutive angles (lane l owns angle m0 + l, its trig in
 // registers for the whole strip) walked down R radius rows, kStripG rows per
 // iteration: the radii are warp-uniform (one broadcast LDG.128 per four
@@ -1166,7 +1169,7 @@ __device__ __forceinline__ void band_tile(const SearchConst* S, const Consts& C,
 // evaluated by the same band_chunk under the same proven bound as in the
 // row-major loop; only the walk order differs, and the outputs (counts,
 // first canonical pair) do not depend on it.
-constexpr uint32_t kStripG = 4;
+constexpr uint32_t kStripG = CVG_STRIP_G;  // rows per iteration: 4 or 8 (radius groups of 4)
 
 
 // Rows [k, kend) (kend - k a multiple of kStripG, k % 4 == 0) of the strip,
@@ -1182,16 +1185,23 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
     // radius groups: {r[4j..4j+3]}, {r^2}, {r^3} as three consecutive float4
     const float4* __restrict__ rg = reinterpret_cast<const float4*>(A.radius_groups) + 3 * (k >> 2);
 #pragma unroll 1
-    for (; k != kend; k += kStripG, rg += 3) {
-        const float4 r4 = __ldg(rg);
-        const float rr[kStripG] = {r4.x, r4.y, r4.z, r4.w};
+    for (; k != kend; k += kStripG, rg += 3 * (kStripG / 4)) {
+        float rr[kStripG], r2[kStripG], r3[kStripG];
+#pragma unroll
+        for (uint32_t h = 0; h < kStripG / 4; ++h) {
+            const float4 r4 = __ldg(rg + 3 * h);
+            rr[4 * h] = r4.x, rr[4 * h + 1] = r4.y, rr[4 * h + 2] = r4.z, rr[4 * h + 3] = r4.w;
+            if constexpr (kCubeOnly) {
+                const float4 q2 = __ldg(rg + 3 * h + 1), q3 = __ldg(rg + 3 * h + 2);
+                r2[4 * h] = q2.x, r2[4 * h + 1] = q2.y, r2[4 * h + 2] = q2.z, r2[4 * h + 3] = q2.w;
+                r3[4 * h] = q3.x, r3[4 * h + 1] = q3.y, r3[4 * h + 2] = q3.z, r3[4 * h + 3] = q3.w;
+            }
+        }
         float lv[kStripG], qv[kStripG];
         bool att = false;
         if constexpr (kCubeOnly) {
             // lanes past the last angle hold zero strip constants: every
             // channel's statistic is 0, so no loud channel leaves its band
-            const float4 q2 = __ldg(rg + 1), q3 = __ldg(rg + 2);
-            const float r2[kStripG] = {q2.x, q2.y, q2.z, q2.w}, r3[kStripG] = {q3.x, q3.y, q3.z, q3.w};
 #pragma unroll
             for (uint32_t g = 0; g < kStripG; ++g) {
                 strip_stat<kL>(C, Q, rr[g], r2[g], r3[g], lv[g], qv[g]);
@@ -1238,8 +1248,9 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
 // two loads are not merged) for the linear rows: during the cube-only rows
 // only the strip constants and the thresholds are live.
 template <int kL, int kOut>
-__device__ __forceinline__ void strip_run(const SearchConst* S, const LaunchArgs& A, uint32_t m0, uint32_t k0,
-                                          uint32_t k1, unsigned lane, uint32_t& cnt, uint32_t& fk, Counters& ct) {
+__device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0, const LaunchArgs& A, uint32_t m0,
+                                          uint32_t k0, uint32_t k1, unsigned lane, uint32_t& cnt, uint32_t& fk,
+                                          Counters& ct) {
     const uint32_t m = m0 + lane;
     const bool m_ok = m < static_cast<uint32_t>(A.na);
     const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + (m_ok ? m : A.na - 1));
@@ -1248,8 +1259,7 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const LaunchArgs
     ThrConsts T;
     uint32_t kc = kend;
     {
-        Consts C;
-        load_consts(S, C);
+        const Consts& C = C0;
         T = ThrConsts{C.la, C.qa, C.lp, C.qp, C.flags};
         // The strip's cube-only bound rb: no candidate of a row with r < rb
         // leaves the cube branch of f^-1 (r |s'| < fx0 - u0 and r |c'| <
@@ -1275,8 +1285,7 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const LaunchArgs
     }
     strip_rows<kL, true, kOut>(S, T, Q, A, sc, m_ok, m, k0, kc, cnt, fk, ct);
     if (kc == k1) return;
-    Consts C;
-    load_consts(opaque_ptr(S), C);
+    const Consts& C = C0;
     strip_rows<kL, false, kOut>(S, C, Q, A, sc, m_ok, m, kc, kend, cnt, fk, ct);
 #pragma unroll 1
     for (uint32_t k = kend; k < k1; ++k) {
@@ -1309,9 +1318,11 @@ __device__ __forceinline__ void strip_tile(const SearchConst* S, const LaunchArg
     const uint32_t n_strips = (static_cast<uint32_t>(A.na) + 31) / 32;
     const uint32_t s0 = st * A.strips_per_tile, s1 = min(s0 + A.strips_per_tile, n_strips);
     uint32_t cnt = 0, first = 0xffffffffu;
+    Consts C;
+    load_consts(S, C);
     for (uint32_t q = s0; q < s1; ++q) {
         uint32_t fk = 0xffffffffu;
-        strip_run<kL, kOut>(S, A, 32 * q, k0, k1, lane, cnt, fk, ct);
+        strip_run<kL, kOut>(S, C, A, 32 * q, k0, k1, lane, cnt, fk, ct);
         if (kOut == kOutFirst) {
             const uint32_t mine = fk != 0xffffffffu ? fk * static_cast<uint32_t>(A.na) + 32 * q + lane : 0xffffffffu;
             first = min(first, __reduce_min_sync(kFull, mine));
