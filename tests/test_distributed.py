@@ -1,4 +1,5 @@
-"""Multi-rank partitioning on CPU: world_size 2 over gloo.
+"""Multi-rank partitioning: world_size 2 over gloo (CPU oracle, and the real
+device search on one GPU under -m gpu).
 
 Each rank evaluates its contiguous share of a batch (here with the CPU oracle
 standing in for the per-GPU search -- the partition/gather logic is what is
@@ -116,3 +117,75 @@ def test_partition_rule():
     assert partition(1, 256, 8) == "rows"         # cfg0
     assert partition(1, 256, 1) == "searches"
     assert partition(4, 3, 8) == "searches"       # fewer rows than ranks
+
+
+# ---- the sharded search on the GPU ------------------------------------------
+
+def _gpu_search(shard):
+    import paper_2507_22901_b200 as cv
+
+    ctx = _gpu_search.ctx = getattr(_gpu_search, "ctx", None) or cv.Context(0)
+    return ctx.search(shard.targets, shard.patterns, shard.v_th, shard.r_novib, shard.radii, shard.angles)
+
+
+def _gpu_worker(rank, world, port, q, name):
+    import hashlib
+
+    import torch.distributed as dist
+
+    from paper_2507_22901_b200.distributed import gather_pairs, search_sharded
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        wl = W.ALL[name]()
+        try:
+            res = search_sharded(wl, _gpu_search)
+        except Exception as e:  # noqa: BLE001 -- reported to the parent instead of hanging it
+            q.put((rank, "error", repr(e), None))
+            raise
+        got = gather_pairs(res)
+        sha = None
+        if got is not None:
+            m = hashlib.sha256()
+            for s in range(wl.n_searches):
+                a, b = int(res.offsets[s]), int(res.offsets[s + 1])
+                m.update(np.ascontiguousarray(got[0][a:b], np.uint32).tobytes())
+                m.update(np.ascontiguousarray(got[1][a:b], np.uint8).tobytes())
+            sha = m.hexdigest()
+        q.put((rank, res.by, res.counts.tolist(), sha))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["cfg0", "cfg1"])
+def test_sharded_gpu_search_matches_golden(name):
+    """search_sharded with the REAL device search (Context.search) in two
+    processes sharing cuda:0 (gloo collectives on the host: the two ranks'
+    kernels never wait on each other), gathered on rank 0: cfg1 partitions
+    by search ranges, cfg0 (one search) by radius rows; counts and the
+    gathered records equal the reference goldens."""
+    import multiprocessing as mp
+
+    import torch
+    from cvtest_util import golden
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, q, name)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = sorted(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(o[1] != "error" for o in outs), outs
+    g = golden("workloads.json")[name]
+    assert outs[0][1] == ("rows" if name == "cfg0" else "searches")
+    for _, _, counts, _ in outs:
+        assert counts == g["counts"]
+    assert outs[0][3] == g["sha256"]
