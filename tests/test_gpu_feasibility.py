@@ -113,3 +113,53 @@ def test_benchmark_small_workload(cv, ctx):  # test_bench.cpp:23-49
 def test_benchmark_defaults_parity_pass(cv, ctx):  # run_benchmark(benchmark_defaults) = 408,364
     r = cv.run_benchmark(cv.SearchConfig.benchmark_defaults(), 1)
     assert r.result_parity and r.pairs_found == 408364
+
+
+def _host_select_best(res, targets, v_th, r_novib, basis):
+    """select_best (search.cpp:458-489) over each search's PAIRS records in
+    double: the first maximum of classification_margin in canonical order."""
+    best = []
+    for s in range(len(res["counts"])):
+        a, b = int(res["offsets"][s]), int(res["offsets"][s + 1])
+        if a == b:
+            best.append(None)
+            continue
+        c = res["codes"][a:b].astype(np.int64)
+        t = np.asarray(targets[s], np.int64)
+        if basis == 0:
+            d = np.maximum(np.abs(c[:, :3] - t), np.abs(c[:, 3:] - t)).astype(np.float64)
+        else:
+            d = np.abs(c[:, :3] - c[:, 3:]).astype(np.float64)
+        low = v_th[s] * r_novib[s]
+        g = np.where(d > v_th[s], d - v_th[s], low - d)
+        m = g.min(axis=1)
+        j = int(np.argmax(m))  # first maximum
+        best.append((int(res["idx"][a + j]), res["codes"][a + j].tolist()))
+    return best
+
+
+@pytest.mark.parametrize("basis", [0, 1])
+def test_best_output_mode_matches_host_select_best(ctx, basis):
+    """CVG_OUT_BEST (select_best on the device) on the 756-search cfg1 sweep
+    against select_best's rule applied to the full pair lists."""
+    from paper_2507_22901_b200 import workloads as W
+
+    wl = W.cfg1()
+    args = (wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles)
+    full = ctx.search(*args, delta_basis=basis)
+    best = ctx.search(*args, output="best", delta_basis=basis)
+    assert np.array_equal(best["counts"], full["counts"])
+    want = _host_select_best(full, wl.targets, wl.v_th, wl.r_novib, basis)
+    for s, w in enumerate(want):
+        if w is None:
+            assert best["first_idx"][s] == 0xFFFFFFFF
+        else:
+            assert (int(best["first_idx"][s]), best["first_codes"][s].tolist()) == w, s
+
+
+def test_best_output_rejects_continuous(ctx):
+    from paper_2507_22901_b200 import workloads as W
+
+    wl = W.cfg0()
+    with pytest.raises(RuntimeError):
+        ctx.search(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, output="best", delta_mode=1)
