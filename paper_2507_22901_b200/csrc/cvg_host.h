@@ -493,6 +493,7 @@ struct cvg_plan {
     int32_t n_exec = 0;
     const uint32_t* d_map = nullptr;
     void* d_memo = nullptr;
+    void* d_masks = nullptr;  // PAIRS on strip tiles: pass words (LaunchArgs::masks)
     // where the per-search results of a run land (args.* unless memo)
     unsigned long long* res_counts = nullptr;
     uint32_t* res_first_idx = nullptr;

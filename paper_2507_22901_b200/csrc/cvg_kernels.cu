@@ -1178,10 +1178,15 @@ constexpr uint32_t kStripG = CVG_STRIP_G;  // rows per iteration: 4 or 8 (radius
 // Fast path: the attention test only, one vote per group; a group with some
 // lane that may pass settles: certain passes tallied per lane, the lane's
 // first passing row kept, unsure lanes decided in FP64.
+// PAIRS: `cnt` is the lane's pending pass word (bit l = angle m0 + l) of row
+// 32 b + lane of the current 32-row block; each 32-row block's words are
+// stored to the strip's column of the pass-mask array (mcol[k], coalesced)
+// when the block ends.
 template <int kL, bool kCubeOnly, int kOut, class CT>
 __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, const StripConsts& Q,
                                            const LaunchArgs& A, float2 sc, bool m_ok, uint32_t m, uint32_t k,
-                                           uint32_t kend, uint32_t& cnt, uint32_t& fk, Counters& ct) {
+                                           uint32_t kend, uint32_t& cnt, uint32_t& fk, Counters& ct,
+                                           uint32_t* mcol = nullptr) {
     // radius groups: {r[4j..4j+3]}, {r^2}, {r^3} as three consecutive float4
     const float4* __restrict__ rg = reinterpret_cast<const float4*>(A.radius_groups) + 3 * (k >> 2);
 #pragma unroll 1
@@ -1215,7 +1220,37 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
             }
             att &= m_ok;
         }
-        if (__any_sync(kFull, att) && att) {
+        if constexpr (kOut == kOutPairs) {
+            if (__any_sync(kFull, att)) {
+                bool pass[kStripG], uns = false;
+#pragma unroll
+                for (uint32_t g = 0; g < kStripG; ++g) {
+                    pass[g] = band_certain(C, lv[g], qv[g]) & m_ok;
+                    uns |= band_attention(C, lv[g], qv[g]) & !pass[g] & m_ok;
+                }
+                if (uns) {
+#pragma unroll
+                    for (uint32_t g = 0; g < kStripG; ++g) {
+                        if (band_attention(C, lv[g], qv[g]) & !band_certain(C, lv[g], qv[g]) & m_ok) {
+                            double lp[3], lm[3];
+                            exact_linear(S, A, k + g, m, lp, lm);
+                            pass[g] = exact_band(S, lp, lm, __ldg(&S->flags));
+                            ++ct.repairs;
+                        }
+                    }
+                }
+                const uint32_t lane = threadIdx.x & 31;
+#pragma unroll
+                for (uint32_t g = 0; g < kStripG; ++g) {
+                    const uint32_t w = __ballot_sync(kFull, pass[g]);
+                    if (lane == ((k + g) & 31u)) cnt = w;
+                }
+            }
+            if (((k + kStripG) & 31u) == 0) {  // the 32-row block is complete
+                mcol[(k & ~31u) + (threadIdx.x & 31)] = cnt;
+                cnt = 0;
+            }
+        } else if (__any_sync(kFull, att) && att) {
             // certain passes counted per lane (the lane's first passing row
             // kept); the unsure lanes, rare, decided in FP64
             bool uns = false;
@@ -1250,7 +1285,7 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
 template <int kL, int kOut>
 __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0, const LaunchArgs& A, uint32_t m0,
                                           uint32_t k0, uint32_t k1, unsigned lane, uint32_t& cnt, uint32_t& fk,
-                                          Counters& ct) {
+                                          Counters& ct, uint32_t* mcol = nullptr) {
     const uint32_t m = m0 + lane;
     const bool m_ok = m < static_cast<uint32_t>(A.na);
     const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + (m_ok ? m : A.na - 1));
@@ -1283,10 +1318,15 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0
         strip_setup(C, sc, Q);
         if (!m_ok) Q = StripConsts{};  // the partial strip's idle lanes never pass (strip_rows)
     }
-    strip_rows<kL, true, kOut>(S, T, Q, A, sc, m_ok, m, k0, kc, cnt, fk, ct);
-    if (kc == k1) return;
+    strip_rows<kL, true, kOut>(S, T, Q, A, sc, m_ok, m, k0, kc, cnt, fk, ct, mcol);
+    if (kc == k1) {
+        if constexpr (kOut == kOutPairs) {
+            if (k1 & 31u) mcol[((k1 - 1) & ~31u) + lane] = cnt;  // the last, partial 32-row block
+        }
+        return;
+    }
     const Consts& C = C0;
-    strip_rows<kL, false, kOut>(S, C, Q, A, sc, m_ok, m, kc, kend, cnt, fk, ct);
+    strip_rows<kL, false, kOut>(S, C, Q, A, sc, m_ok, m, kc, kend, cnt, fk, ct, mcol);
 #pragma unroll 1
     for (uint32_t k = kend; k < k1; ++k) {
         const float r = __ldg(&A.radii_f[k]);
@@ -1301,8 +1341,19 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0
             ++ct.repairs;
         }
         pass &= m_ok;
-        cnt += pass;
-        if (kOut == kOutFirst && pass) fk = min(fk, k);
+        if constexpr (kOut == kOutPairs) {
+            const uint32_t w = __ballot_sync(kFull, pass);
+            if (lane == (k & 31u)) cnt = w;
+        } else {
+            cnt += pass;
+            if (kOut == kOutFirst && pass) fk = min(fk, k);
+        }
+    }
+    if constexpr (kOut == kOutPairs) {
+        if ((k1 & 31u) || kend != k1) {  // the last block's rows were not stored yet (rows >= k1 stay 0)
+            mcol[((k1 - 1) & ~31u) + lane] = cnt;
+            cnt = 0;
+        }
     }
 }
 
@@ -1320,6 +1371,15 @@ __device__ __forceinline__ void strip_tile(const SearchConst* S, const LaunchArg
     uint32_t cnt = 0, first = 0xffffffffu;
     Consts C;
     load_consts(S, C);
+    if constexpr (kOut == kOutPairs) {
+        // pass words of strip q: column q of search s's mask block (rows padded to 32)
+        uint32_t* mblk = A.masks + static_cast<size_t>(s) * n_strips * A.mask_rows;
+        for (uint32_t q = s0; q < s1; ++q) {
+            uint32_t w = 0, fk = 0;
+            strip_run<kL, kOut>(S, C, A, 32 * q, k0, k1, lane, w, fk, ct, mblk + static_cast<size_t>(q) * A.mask_rows);
+        }
+        return;
+    }
     for (uint32_t q = s0; q < s1; ++q) {
         uint32_t fk = 0xffffffffu;
         strip_run<kL, kOut>(S, C, A, 32 * q, k0, k1, lane, cnt, fk, ct);
@@ -1355,7 +1415,8 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
     uint32_t t_claim = 0;
     if (lane == 0) t_claim = atomicAdd(&A.ticket[0], 1u);
     uint32_t c = __shfl_sync(kFull, t_claim, 0);
-    while (c < A.n_tiles) {
+    const uint32_t n_claims = A.n_claims;
+    while (c < n_claims) {
         if (lane == 0) t_claim = atomicAdd(&A.ticket[0], 1u);  // next tile, consumed at the end
         // Claim order for searches of many tiles: outermost radius tiles of
         // every search first, the innermost last.  Outer rows are the costly
@@ -1366,9 +1427,10 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         // search's constants.  Tile t (search s, tile lt) keeps its storage
         // slot s * tps + lt either way.
         uint32_t s, lt;
+        const uint32_t cps = A.claim_per_search;  // tiles (or strip tiles) per search
         if (A.claim_order) {
             // group g of loud-count-sorted positions, outer-first inside it
-            const uint32_t tps = A.tiles_per_search;
+            const uint32_t tps = cps;
             uint32_t g0 = 0, g1 = A.group_end[0];
             if (c >= g1 * tps) {
                 g0 = g1;
@@ -1390,13 +1452,13 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
                 pos = g0 + sr;
             }
             s = __ldg(&A.claim_order[pos]);
-        } else if (A.tiles_per_search >= 16) {
+        } else if (cps >= 16) {
             const uint32_t q = c / A.range_searches;
             s = A.search_begin + (c - q * A.range_searches);
-            lt = A.tiles_per_search - 1 - q;
+            lt = cps - 1 - q;
         } else {
-            const uint32_t sr = c / A.tiles_per_search;
-            lt = c - sr * A.tiles_per_search;
+            const uint32_t sr = c / cps;
+            lt = c - sr * cps;
             s = A.search_begin + sr;
         }
         const uint32_t t = s * A.tiles_per_search + lt;
@@ -1410,7 +1472,7 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         load_consts(S, C);
         // kStrips (COUNTS / FIRST, band FAST path, LaunchArgs::strips): its
         // own instantiation, so that the row-major loops keep their registers
-        constexpr bool kStripsOk = kMode == kModeBand && kPath == kPathFast && kOut != kOutPairs && !kPrune;
+        constexpr bool kStripsOk = kMode == kModeBand && kPath == kPathFast && !kPrune;
         if constexpr (kStrips && kStripsOk) {
             const uint32_t nl = (__ldg(&S->flags) >> 10) & 3u;
             if (nl == 3) {
@@ -1420,7 +1482,10 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
             } else {
                 strip_tile<1, kOut>(S, A, s, lt, lane, ct);
             }
-            // counts / first pair already recorded: cnt stays 0
+            // counts / first pair recorded; PAIRS: pass words written, the
+            // tile lists come from lists_kernel
+            c = __shfl_sync(kFull, t_claim, 0);
+            continue;
         } else if (kMode == kModeBand && kPath == kPathFast && A.aligned) {
             const uint32_t nl = (C.flags >> 10) & 3u;
             if (nl == 3) {
@@ -1466,6 +1531,106 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
     }
     pdl_trigger();  // no tiles left for this warp: the scan may launch once every CTA has said so
     flush_counters(ct, A, lane);
+}
+
+// K1b (PAIRS on strip tiles): the canonical tile lists from the pass words.
+// A unit is search s, lst_unit_rows rows (8, or the rows of one whole-row
+// tile when that is more) and strips [128 cb, +128) (all strips when a tile
+// holds whole rows): at most 1024 words, read as full 32-byte column
+// segments (lst_unit_rows consecutive rows of a strip) into a padded shared
+// block, then appended row by row, strips ascending, to the ordered list of
+// their canonical tile (whole-row tiles: lst_rpt rows each; else lst_tpr
+// tiles per row).  Small units keep many warps resident: the expansion is a
+// latency-bound chain of shuffles.  Writes tile_count, the emit work items
+// and the per-search counts: scan and emit then run exactly as after the
+// row-major loop.
+constexpr uint32_t kListWords = 1024;
+
+__global__ void __launch_bounds__(kBlock) lists_kernel(const LaunchArgs A) {
+    __shared__ uint32_t blk[kWarpsPerBlock][kListWords + 32];
+    pdl_wait();  // phase 1 complete: every pass word written
+    const unsigned lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned lane_lt = (1u << lane) - 1u;
+    uint32_t* Wb = blk[warp];
+    const uint32_t nq = static_cast<uint32_t>(A.na) >> 5;
+    const uint32_t ur = A.lst_unit_rows;                     // rows per unit (divides 32)
+    const uint32_t n_kb = (static_cast<uint32_t>(A.nr) + ur - 1) / ur;
+    const uint32_t n_cb = A.lst_tpr ? A.lst_tpr : 1u;
+    const uint32_t cwu = min(nq, 128u);
+    const uint32_t stride = cwu + 1;                         // shared row stride (bank-conflict free)
+    const uint32_t ups = n_kb * n_cb;
+    const uint32_t n_units = A.range_searches * ups;
+    const uint32_t per_load = 32u / ur;                      // strips per load instruction
+    uint32_t u_claim = 0;
+    if (lane == 0) u_claim = atomicAdd(&A.ticket[4], 1u);
+    uint32_t u = __shfl_sync(kFull, u_claim, 0);
+    while (u < n_units) {
+        if (lane == 0) u_claim = atomicAdd(&A.ticket[4], 1u);
+        const uint32_t sr = u / ups, r = u - sr * ups;
+        const uint32_t s = A.search_begin + sr;
+        const uint32_t kb = r / n_cb, cb = r - kb * n_cb;
+        const uint32_t k0 = ur * kb, rows = min(ur, static_cast<uint32_t>(A.nr) - k0);
+        const uint32_t* mblk = A.masks + static_cast<size_t>(s) * nq * A.mask_rows;
+        // load: lane -> (strip qs + lane / ur, row k0 + lane % ur)
+        {
+            const uint32_t kr = lane % ur, qo = lane / ur;
+            const uint32_t* col = mblk + static_cast<size_t>(128u * cb + qo) * A.mask_rows + k0 + kr;
+#pragma unroll 4
+            for (uint32_t qs = 0; qs < cwu; qs += per_load) {
+                if (qs + qo < cwu) Wb[kr * stride + qs + qo] = __ldg(col + static_cast<size_t>(qs) * A.mask_rows);
+            }
+        }
+        __syncwarp();
+        uint32_t tcnt = 0;  // lane j: count of the unit's tile slot j
+        for (uint32_t j = 0; j < rows; ++j) {
+            const uint32_t row = k0 + j;
+            const uint32_t slot = A.lst_rpt ? j / A.lst_rpt : j;
+            const uint32_t lt = A.lst_rpt ? row / A.lst_rpt : row * A.lst_tpr + cb;
+            uint16_t* list = A.scratch + static_cast<size_t>(s * A.tiles_per_search + lt) * kTile;
+            for (uint32_t qc = 0; qc < cwu; qc += 32) {
+                const uint32_t W = qc + lane < cwu ? Wb[j * stride + qc + lane] : 0u;
+                if (!__any_sync(kFull, W != 0u)) continue;
+                // word index of strip qc + l inside the tile
+                const uint32_t wbase = A.lst_rpt ? (row % A.lst_rpt) * nq + qc : qc;
+                uint32_t cnt = __shfl_sync(kFull, tcnt, slot);
+                const uint32_t pc = __popc(W);
+                uint32_t incl = pc;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= static_cast<unsigned>(o)) incl += y;
+                }
+                uint32_t nz = __ballot_sync(kFull, W != 0);
+                while (nz) {
+                    const int q = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    const uint32_t Wq = __shfl_sync(kFull, W, q);
+                    const uint32_t oq = __shfl_sync(kFull, incl - pc, q);
+                    if ((Wq >> lane) & 1u) {
+                        list[cnt + oq + __popc(Wq & lane_lt)] = static_cast<uint16_t>(32u * (wbase + q) + lane);
+                    }
+                }
+                cnt += __shfl_sync(kFull, incl, 31);
+                if (lane == slot) tcnt = cnt;
+            }
+        }
+        __syncwarp();
+        const uint32_t n_slots = A.lst_rpt ? (rows + A.lst_rpt - 1) / A.lst_rpt : rows;
+        if (lane < n_slots) {
+            const uint32_t lt = A.lst_rpt ? k0 / A.lst_rpt + lane : (k0 + lane) * A.lst_tpr + cb;
+            const uint32_t t = s * A.tiles_per_search + lt;
+            A.tile_count[t] = tcnt;
+            const uint32_t subs = (tcnt + (1u << A.emit_shift) - 1) >> A.emit_shift;
+            if (subs) {
+                const uint32_t w = atomicAdd(&A.ticket[3], subs);
+                for (uint32_t q = 0; q < subs; ++q) A.worklist[w + q] = (t << 4) | q;
+            }
+        }
+        const uint32_t total = __reduce_add_sync(kFull, lane < n_slots ? tcnt : 0u);
+        if (lane == 0 && total) atomicAdd(&A.counts[s], static_cast<unsigned long long>(total));
+        u = __shfl_sync(kFull, u_claim, 0);
+    }
+    pdl_trigger();
 }
 
 // K2: exclusive scan of tile_count -> tile_base (single pass, chained scan
@@ -1791,16 +1956,26 @@ inline int work_grid(int grid, uint64_t units, int warps) {
     return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(static_cast<uint64_t>(grid), need)));
 }
 
+cudaError_t launch_pdl(void (*kernel)(LaunchArgs), unsigned grid, unsigned threads, size_t smem, cudaStream_t st,
+                       const LaunchArgs& a);
+
 template <int kMode, int kOut, int kPath, bool kPrune = false>
 cudaError_t phase1_t(const LaunchArgs& a, int grid, cudaStream_t st) {
-    grid = work_grid(grid, a.n_tiles, kWarpsPerBlock);
+    grid = work_grid(grid, a.n_claims, kWarpsPerBlock);
     if (kMode == kModeBand && kPath == kPathFast && !kPrune && a.prune) {
         phase1_kernel<kMode, kOut, kPath, true><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);
         return cudaGetLastError();
     }
-    if (kMode == kModeBand && kPath == kPathFast && kOut != kOutPairs && !kPrune && a.strips) {
+    if (kMode == kModeBand && kPath == kPathFast && !kPrune && a.strips) {
         phase1_kernel<kMode, kOut, kPath, false, true><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);
-        return cudaGetLastError();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess || kOut != kOutPairs) return e;
+        // PAIRS: the canonical tile lists from the pass words
+        const uint32_t units = a.range_searches * ((a.nr + a.lst_unit_rows - 1) / a.lst_unit_rows) *
+                               (a.lst_tpr ? a.lst_tpr : 1u);
+        // latency-bound expansion: as many resident warps as fit (6 blocks per SM)
+        return launch_pdl(lists_kernel, static_cast<unsigned>(work_grid(grid * 6 / 4, units, kWarpsPerBlock)), kBlock,
+                          0, st, a);
     }
     // The dynamic shared-memory sizes are opted into by occupancy_t (plan creation).
     phase1_kernel<kMode, kOut, kPath, kPrune><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);

@@ -99,6 +99,17 @@ struct LaunchArgs {
     uint32_t cand_per_search;  // nr * na (< 2^32)
     uint64_t na_magic;         // ceil(2^64 / na): k = umul64hi(i, na_magic)
     uint64_t n_tiles;              // tiles of this range view
+    // Work units the phase-1 warps claim: tiles, or strip tiles.
+    uint32_t n_claims;             // units of this range view
+    uint32_t claim_per_search;
+    // PAIRS on strip tiles: pass words, column-major per search:
+    // masks[(s * n_strips + q) * mask_rows + k] (bit l = angle 32 q + l);
+    // lists_kernel builds the canonical tile lists from them
+    uint32_t* masks;
+    uint32_t mask_rows;            // n_radii rounded up to 32
+    uint32_t lst_rpt;              // tiles of whole rows: rows per tile (0 otherwise)
+    uint32_t lst_tpr;              // rows of whole tiles: tiles per row (0 otherwise)
+    uint32_t lst_unit_rows;        // rows per lists_kernel unit: max(8, lst_rpt)
     // Range view: the launch covers searches [search_begin, search_begin +
     // range_searches) = tiles [tile_begin, tile_begin + n_tiles).  A plan may
     // run two views on two streams so that one range's scan and emit fill

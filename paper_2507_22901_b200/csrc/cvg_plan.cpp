@@ -249,14 +249,24 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         const char* e = std::getenv("CVG_STRIPS");
         return e ? std::atoi(e) : 1;
     }();
-    const bool strips = strips_env != 0 && d->output != CVG_OUT_PAIRS && d->output != CVG_OUT_BEST &&
-                        search_mode(d) == cvg::kModeBand && (d->path == CVG_PATH_FAST || d->path == CVG_PATH_MEMO);
-    const uint32_t strip_rows = static_cast<uint32_t>(std::min(p->nr, 512));
+    // PAIRS (and BEST, on the PAIRS kernels) on strip tiles need canonical
+    // tiles of whole strips within a 32-row block: n_angles % 32 == 0 and
+    // either tiles of <= 32 whole rows (n_strips | 128, n_strips >= 4) or
+    // rows of whole tiles (128 | n_strips)
+    const bool pairs_out = d->output == CVG_OUT_PAIRS || d->output == CVG_OUT_BEST;
     const uint32_t n_strips = static_cast<uint32_t>((p->na + 31) / 32);
+    const bool lists_ok = p->na % 32 == 0 && ((n_strips >= 4 && 128 % n_strips == 0) || n_strips % 128 == 0);
+    const bool strips = strips_env != 0 && search_mode(d) == cvg::kModeBand &&
+                        (d->path == CVG_PATH_FAST || d->path == CVG_PATH_MEMO) && (!pairs_out || lists_ok);
+    const uint32_t strip_rows = static_cast<uint32_t>(std::min(p->nr, 512));  // 512: a multiple of 32
     const uint32_t strips_per_tile = std::max<uint32_t>(1, 16384u / (32u * strip_rows));
     const uint32_t strip_tiles = (n_strips + strips_per_tile - 1) / strips_per_tile;
-    const uint32_t tps = strips ? static_cast<uint32_t>((p->nr + strip_rows - 1) / strip_rows) * strip_tiles
-                                : static_cast<uint32_t>((cps + cvg::kTile - 1) / cvg::kTile);
+    const uint32_t tps = strips && !pairs_out
+                             ? static_cast<uint32_t>((p->nr + strip_rows - 1) / strip_rows) * strip_tiles
+                             : static_cast<uint32_t>((cps + cvg::kTile - 1) / cvg::kTile);
+    const uint32_t claim_per_search =
+        strips ? static_cast<uint32_t>((p->nr + strip_rows - 1) / strip_rows) * strip_tiles : tps;
+    const uint32_t mask_rows = static_cast<uint32_t>((p->nr + 31) / 32 * 32);
 
     // ---- host tables ----
     // Per-search constants, deduplicated: searches with the same (target,
@@ -277,6 +287,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     // the searches the kernels run: all of them, or (memo) one per record
     p->n_exec = p->memo ? static_cast<int32_t>(n_sc) : p->n;
     const uint64_t n_tiles = static_cast<uint64_t>(tps) * static_cast<uint64_t>(p->n_exec);
+    const uint64_t n_claims = static_cast<uint64_t>(claim_per_search) * static_cast<uint64_t>(p->n_exec);
     if (n_tiles >= (1ull << 28)) return fail(CVG_EINVAL, "batch too large for one plan (split the searches)");
     auto exec_bits = [&](int32_t i) { return d->pattern_bits[p->memo ? uniq[i] : i] & 7; };
     GridTables own;
@@ -439,6 +450,12 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.emit_shift = 8;  // kEmitSpan until an expected pair count says otherwise (plan_set_density)
     A.prune = d->path == CVG_PATH_PRUNED ? 1u : 0u;
     A.strips = strips ? 1u : 0u;
+    A.n_claims = static_cast<uint32_t>(n_claims);
+    A.claim_per_search = claim_per_search;
+    A.mask_rows = mask_rows;
+    A.lst_rpt = strips && pairs_out && n_strips <= 128 ? 128u / n_strips : 0u;
+    A.lst_tpr = strips && pairs_out && n_strips > 128 ? n_strips / 128u : 0u;
+    A.lst_unit_rows = std::max<uint32_t>(8u, A.lst_rpt);
     A.strip_rows = strip_rows;
     A.strips_per_tile = strips_per_tile;
     A.strip_tiles = strip_tiles;
@@ -486,6 +503,11 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         p->d_scratch = ctx->dev.alloc(static_cast<size_t>(n_tiles) * cvg::kTile * sizeof(uint16_t));
         if (!p->d_scratch) return fail(CVG_ENOMEM, "device allocation of the tile lists failed");
         A.scratch = static_cast<uint16_t*>(p->d_scratch);
+        if (strips) {  // pass words of the strip tiles (every word is written each run)
+            p->d_masks = ctx->dev.alloc(static_cast<size_t>(p->n_exec) * n_strips * mask_rows * sizeof(uint32_t));
+            if (!p->d_masks) return fail(CVG_ENOMEM, "device allocation of the pass masks failed");
+            A.masks = static_cast<uint32_t*>(p->d_masks);
+        }
     }
     if (p->out == cvg::kOutFirst || p->best) {
         Layout F;
@@ -514,7 +536,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         p->res_first_codes = first ? at<uint8_t>(p->d_memo, o_mf) : nullptr;
     }
 
-    const uint64_t want = (n_tiles + cvg::kWarpsPerBlock - 1) / cvg::kWarpsPerBlock;
+    const uint64_t want = (n_claims + cvg::kWarpsPerBlock - 1) / cvg::kWarpsPerBlock;
     static const int cap_per_sm = [] {
         const char* e = std::getenv("CVG_BLOCKS_PER_SM");  // tuning override (occupancy experiments)
         return e ? std::atoi(e) : 0;
@@ -562,6 +584,8 @@ void plan_release(cvg_plan* p) {
     p->ctx->dev.release(p->d_scratch);
     p->ctx->dev.release(p->d_memo);
     p->d_memo = nullptr;
+    p->ctx->dev.release(p->d_masks);
+    p->d_masks = nullptr;
     if (p->stage) cudaStreamSynchronize(p->ctx->stream);  // the constant upload may still be in flight
     for (cudaEvent_t* ev : {&p->ev0, &p->ev1, &p->marks[0], &p->marks[1], &p->marks[2], &p->marks[3]}) {
         if (*ev) p->ctx->events.push_back(*ev);

@@ -318,6 +318,7 @@ int search_pipelined(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, int 
         V.range_searches = static_cast<uint32_t>(e - b);
         V.tile_begin = static_cast<uint64_t>(b) * tps;
         V.n_tiles = static_cast<uint64_t>(e - b) * tps;
+        V.n_claims = static_cast<uint32_t>((e - b) * p.args.claim_per_search);
         V.stats = reinterpret_cast<cvg::Stats*>(dv + kHdr * c);
         V.total = reinterpret_cast<unsigned long long*>(dv + kHdr * c + 256);
         V.ticket = reinterpret_cast<unsigned int*>(dv + kHdr * c + 264);

@@ -28,3 +28,8 @@ for _ in range(a.runs):
     plan.run(0)
     plan.sync()
 print(a.config, "pairs", n, "kernel_ms", plan.last_kernel_ms())
+if (a.output or wl.output) == "pairs":
+    plan.set_phase_marks(True)
+    plan.run(0)
+    plan.sync()
+    print(a.config, "phases_ms (phase1[+lists], scan, emit)", [round(x, 4) for x in plan.last_phase_ms()])
