@@ -531,9 +531,8 @@ __device__ __forceinline__ int code_fast(float xs, float E, uint32_t tab, bool& 
     int c;
     asm("ld.shared.v2.b32 {%0, %1}, [%2];" : "=f"(t), "=r"(c) : "r"(tab + (__float_as_uint(b) << 3)));
     ok = fabsf(__fsub_rn(xs, t)) > E;
-    int up;
-    asm("set.ge.s32.f32 %0, %1, %2;" : "=r"(up) : "f"(xs), "f"(t));  // -1 or 0
-    return c - up;
+    if (xs >= t) ++c;  // one predicated add
+    return c;
 }
 
 // Passed through a shuffle, so that it is opaque to ptxas and each lookup is
@@ -1719,6 +1718,52 @@ __device__ __forceinline__ void store_pair(const LaunchArgs& A, unsigned long lo
     c16[2] = static_cast<uint16_t>(cm[1] | (cm[2] << 8));
 }
 
+// FAST path of one emit work item: `cnt` pairs of the tile's list from
+// `list`, written to out_idx / out_codes (the item's slice).  Software
+// pipeline: list entries two iterations ahead, the candidate's radius / trig
+// loads one iteration ahead.  kOneRow: the tile lies inside radius row kt
+// (no per-pair division, no radius load).
+template <bool kOneRow>
+__device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, const CodeConsts& CC,
+                                         const LaunchArgs& A, const uint16_t* list, uint32_t cnt, uint32_t i0,
+                                         uint32_t kt, uint32_t* out_idx, uint8_t* out_codes, unsigned lane,
+                                         Counters& ct) {
+    const float2* trig = reinterpret_cast<const float2*>(A.trig_f);
+    const uint32_t last = cnt - 1;
+    const float rt = __ldg(&A.radii_f[kt]);
+    uint32_t off_n = list[min(32 + lane, last)];
+    uint32_t i = i0 + list[min(lane, last)];
+    uint32_t k = kOneRow ? kt : div_na(i, A);
+    uint32_t m = i - k * static_cast<uint32_t>(A.na);
+    float r = kOneRow ? rt : __ldg(&A.radii_f[k]);
+    float2 sc = __ldg(trig + m);
+#pragma unroll 1
+    for (uint32_t p = 0; p < cnt; p += 32) {
+        const uint32_t i_n = i0 + off_n;
+        const uint32_t k_n = kOneRow ? kt : div_na(i_n, A);
+        const uint32_t m_n = i_n - k_n * static_cast<uint32_t>(A.na);
+        const float r_n = kOneRow ? rt : __ldg(&A.radii_f[k_n]);
+        const float2 sc_n = __ldg(trig + m_n);
+        off_n = list[min(p + 64 + lane, last)];
+        const uint32_t qq = p + lane;
+        const bool active = qq < cnt;
+        int cp[3], cm[3];
+        codes_fast(sm, S, CC, A, k, m, r, sc, active, cp, cm, ct.code_repairs);
+        if (active) {
+            out_idx[qq] = i;
+            uint16_t* c16 = reinterpret_cast<uint16_t*>(out_codes + 6 * qq);
+            c16[0] = static_cast<uint16_t>(cp[0] | (cp[1] << 8));
+            c16[1] = static_cast<uint16_t>(cp[2] | (cm[0] << 8));
+            c16[2] = static_cast<uint16_t>(cm[1] | (cm[2] << 8));
+        }
+        i = i_n;
+        k = k_n;
+        m = m_n;
+        r = r_n;
+        sc = sc_n;
+    }
+}
+
 // K3: codes + coalesced writes of every passing pair at its final offset.
 // Warps claim (tile, 256-pair sub-range) items from the phase-1 worklist
 // (next claim prefetched), so no warp holds more than 8 chunks of work; the
@@ -1755,40 +1800,16 @@ __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
             CodeConsts CC;
             load_code_consts(S, CC, tab);
             if (kPath == kPathFast) {
-                // Software pipeline: list entries two iterations ahead, the
-                // candidate's radius/trig loads one iteration ahead.
-                const float2* trig = reinterpret_cast<const float2*>(A.trig_f);
-                const uint32_t last = cnt - 1;
                 // a tile inside one radius row (n_angles >= 4096): k is the
                 // tile's row for every pair, no per-pair division or radius load
                 const uint32_t kt = div_na(i0, A);
                 const uint32_t mt = i0 - kt * static_cast<uint32_t>(A.na);
-                const bool one_row = mt + static_cast<uint32_t>(kTile) <= static_cast<uint32_t>(A.na);
-                const float rt = __ldg(&A.radii_f[kt]);
-                uint32_t off_n = list[min(32 + lane, last)];
-                uint32_t i = i0 + list[min(lane, last)];
-                uint32_t k = one_row ? kt : div_na(i, A);
-                uint32_t m = i - k * static_cast<uint32_t>(A.na);
-                float r = one_row ? rt : __ldg(&A.radii_f[k]);
-                float2 sc = __ldg(trig + m);
-#pragma unroll 1
-                for (uint32_t p = 0; p < cnt; p += 32) {
-                    const uint32_t i_n = i0 + off_n;
-                    const uint32_t k_n = one_row ? kt : div_na(i_n, A);
-                    const uint32_t m_n = i_n - k_n * static_cast<uint32_t>(A.na);
-                    const float r_n = one_row ? rt : __ldg(&A.radii_f[k_n]);
-                    const float2 sc_n = __ldg(trig + m_n);
-                    off_n = list[min(p + 64 + lane, last)];
-                    const uint32_t qq = p + lane;
-                    const bool active = qq < cnt;
-                    int cp[3], cm[3];
-                    codes_fast(sm, S, CC, A, k, m, r, sc, active, cp, cm, ct.code_repairs);
-                    if (active) store_pair(A, base + qq, i, cp, cm);
-                    i = i_n;
-                    k = k_n;
-                    m = m_n;
-                    r = r_n;
-                    sc = sc_n;
+                uint32_t* out_idx = A.out_idx + base;
+                uint8_t* out_codes = A.out_codes + 6 * base;
+                if (mt + static_cast<uint32_t>(kTile) <= static_cast<uint32_t>(A.na)) {
+                    emit_run<true>(sm, S, CC, A, list, cnt, i0, kt, out_idx, out_codes, lane, ct);
+                } else {
+                    emit_run<false>(sm, S, CC, A, list, cnt, i0, kt, out_idx, out_codes, lane, ct);
                 }
             } else {
 #pragma unroll 1
