@@ -258,8 +258,25 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     const bool lists_ok = p->na % 32 == 0 && ((n_strips >= 4 && 128 % n_strips == 0) || n_strips % 128 == 0);
     const bool strips = strips_env != 0 && search_mode(d) == cvg::kModeBand &&
                         (d->path == CVG_PATH_FAST || d->path == CVG_PATH_MEMO) && (!pairs_out || lists_ok);
-    const uint32_t strip_rows = static_cast<uint32_t>(std::min(p->nr, 512));  // 512: a multiple of 32
-    const uint32_t strips_per_tile = std::max<uint32_t>(1, 16384u / (32u * strip_rows));
+    // ~16K candidates per strip tile (a strip's set-up amortized over up to
+    // 512 rows), made finer for small batches until there are claims for
+    // every resident warp twice over (cfg0: one search of 256 x 1024)
+    uint32_t strip_rows = static_cast<uint32_t>(std::min(p->nr, 512));  // 512: a multiple of 32
+    uint32_t strips_per_tile = std::max<uint32_t>(1, 16384u / (32u * strip_rows));
+    {
+        const uint64_t want = 2ull * static_cast<uint64_t>(ctx->sms) * 32;
+        auto claims = [&] {
+            return static_cast<uint64_t>(p->n) * ((p->nr + strip_rows - 1) / strip_rows) *
+                   ((n_strips + strips_per_tile - 1) / strips_per_tile);
+        };
+        while (claims() < want && (strips_per_tile > 1 || strip_rows > 32)) {
+            if (strips_per_tile > 1) {
+                strips_per_tile /= 2;
+            } else {
+                strip_rows = std::max<uint32_t>(32, (strip_rows / 2 + 31) / 32 * 32);
+            }
+        }
+    }
     const uint32_t strip_tiles = (n_strips + strips_per_tile - 1) / strips_per_tile;
     const uint32_t tps = strips && !pairs_out
                              ? static_cast<uint32_t>((p->nr + strip_rows - 1) / strip_rows) * strip_tiles
