@@ -10,3 +10,7 @@ for c in cfg1 cfg3 cfg2; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"phase1|lists|scan|emit" -s 8 -c 4 -o $O/full_$c python tools/prof_plan.py $c --runs 3 > $O/ncu_$c.log 2>&1; echo $c=$?
 done
 ls -la $O
+# summaries on the box (the .ncu-rep files exceed gpurun's copy-back limit)
+for c in cfg4 cfg1 cfg3 cfg2; do python tools/ncu_summary.py $O/full_$c.ncu-rep --blocks -o $O/ncu_full_$c.json; done
+python tools/ncu_summary.py --launches $O/launches_cfg4.csv -o $O/ncu_launches_cfg4.json
+rm -f $O/*.ncu-rep
