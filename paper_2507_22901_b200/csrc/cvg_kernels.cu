@@ -494,6 +494,11 @@ __device__ __forceinline__ void strip_setup(const Consts& C, float2 sc, StripCon
     }
 }
 
+// One slot's statistic |A_c| + |B_c| of the strip form.
+__device__ __forceinline__ float strip_chan(const StripConsts& Q, int q, float r, float r2, float r3) {
+    return fabsf(fmaf(Q.k2[q], r2, Q.k0[q])) + fabsf(fmaf(Q.l3[q], r3, __fmul_rn(Q.l1[q], r)));
+}
+
 template <int kL, class CT>
 __device__ __forceinline__ void strip_stat(const CT& C, const StripConsts& Q, float r, float r2, float r3,
                                            float& minl, float& maxq) {
@@ -1201,6 +1206,20 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
                 r3[4 * h] = q3.x, r3[4 * h + 1] = q3.y, r3[4 * h + 2] = q3.z, r3[4 * h + 3] = q3.w;
             }
         }
+        // slot 0 first (the most selective loud channel, make_search_const):
+        // a group where no candidate can leave its band needs nothing more
+        bool go = true;
+        float M0[kStripG];
+        if constexpr (kCubeOnly) {
+            float mx0 = 0.0f;
+#pragma unroll
+            for (uint32_t g = 0; g < kStripG; ++g) {
+                M0[g] = strip_chan(Q, 0, rr[g], r2[g], r3[g]);
+                mx0 = fmaxf(mx0, M0[g]);
+            }
+            go = __any_sync(kFull, mx0 >= C.la);
+        }
+        if (go) {
         float lv[kStripG], qv[kStripG];
         bool att = false;
         if constexpr (kCubeOnly) {
@@ -1208,7 +1227,8 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
             // channel's statistic is 0, so no loud channel leaves its band
 #pragma unroll
             for (uint32_t g = 0; g < kStripG; ++g) {
-                strip_stat<kL>(C, Q, rr[g], r2[g], r3[g], lv[g], qv[g]);
+                const float M[3] = {M0[g], strip_chan(Q, 1, rr[g], r2[g], r3[g]), strip_chan(Q, 2, rr[g], r2[g], r3[g])};
+                band_stats_m<kL>(C, M, lv[g], qv[g]);
                 att |= band_attention(C, lv[g], qv[g]);
             }
         } else {
@@ -1245,10 +1265,6 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
                     if (lane == ((k + g) & 31u)) cnt = w;
                 }
             }
-            if (((k + kStripG) & 31u) == 0) {  // the 32-row block is complete
-                mcol[(k & ~31u) + (threadIdx.x & 31)] = cnt;
-                cnt = 0;
-            }
         } else if (__any_sync(kFull, att) && att) {
             // certain passes counted per lane (the lane's first passing row
             // kept); the unsure lanes, rare, decided in FP64
@@ -1272,6 +1288,13 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
                         if (kOut == kOutFirst && pass) fk = min(fk, k + g);
                     }
                 }
+            }
+        }
+        }
+        if constexpr (kOut == kOutPairs) {
+            if (((k + kStripG) & 31u) == 0) {  // the 32-row block is complete
+                mcol[(k & ~31u) + (threadIdx.x & 31)] = cnt;
+                cnt = 0;
             }
         }
     }

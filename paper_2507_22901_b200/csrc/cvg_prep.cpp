@@ -448,8 +448,27 @@ void make_search_const(const cvg_search_desc* d, int s, double rmax, int mode, c
     int slot_of[3], n_loud = 0;
     for (int c = 0; c < 3; ++c) n_loud += bits[c];
     {
-        int nl = 0, nq = n_loud;
-        for (int c = 0; c < 3; ++c) slot_of[c] = bits[c] ? nl++ : nq++;
+        // Loud channels ordered most selective first: the strip loop tests
+        // slot 0 alone first and skips the other channels when no candidate
+        // of a group can leave slot 0's band.  Selectivity estimate: the
+        // band statistic of the target itself plus its first-order growth
+        // over half the radius range, in band units (small = rarely > 1).
+        double sigma[3];
+        for (int c = 0; c < 3; ++c) {
+            const double mx = m[c][0] * wp[0], mz = m[c][2] * wp[2];
+            const double lo = std::isinf(S.lo[c]) ? -10.0 : S.lo[c], hi = std::isinf(S.hi[c]) ? 10.0 : S.hi[c];
+            const double hh = std::max(0.5 * (hi - lo), 1e-30), cc = 0.5 * (lo + hi);
+            const double centre = (mx * fx0 * fx0 * fx0 + mz * fz0 * fz0 * fz0 + S.cy64[c] - cc) / hh;
+            const double growth = (std::fabs(mx) * 3.0 * fx0 * fx0 * kInv500 + std::fabs(mz) * 3.0 * fz0 * fz0 * kInv200) *
+                                  0.5 * rmax / hh;
+            sigma[c] = std::fabs(centre) + growth;
+        }
+        int order[3] = {0, 1, 2};
+        std::stable_sort(order, order + 3, [&](int a, int b) {
+            if (bits[a] != bits[b]) return bits[a] > bits[b];  // loud first
+            return bits[a] ? sigma[a] < sigma[b] : false;
+        });
+        for (int j = 0; j < 3; ++j) slot_of[order[j]] = j;
     }
     S.flags |= static_cast<uint32_t>(n_loud) << 10;
     for (int c = 0; c < 3; ++c) {
