@@ -1210,12 +1210,27 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
         // a group where no candidate can leave its band needs nothing more
         bool go = true;
         float M0[kStripG];
+        float gv[kStripG][4];  // linear rows: f^-1 of the four endpoint coordinates (x+, x-, z+, z-)
         if constexpr (kCubeOnly) {
             float mx0 = 0.0f;
 #pragma unroll
             for (uint32_t g = 0; g < kStripG; ++g) {
                 M0[g] = strip_chan(Q, 0, rr[g], r2[g], r3[g]);
                 mx0 = fmaxf(mx0, M0[g]);
+            }
+            go = __any_sync(kFull, mx0 >= C.la);
+        } else {
+            float mx0 = 0.0f;
+#pragma unroll
+            for (uint32_t g = 0; g < kStripG; ++g) {
+                gv[g][0] = finv_fast<false>(fmaf(rr[g], sc.x, C.fx0));
+                gv[g][1] = finv_fast<false>(fmaf(-rr[g], sc.x, C.fx0));
+                gv[g][2] = finv_fast<false>(fmaf(-rr[g], sc.y, C.fz0));
+                gv[g][3] = finv_fast<false>(fmaf(rr[g], sc.y, C.fz0));
+                const float dp = fmaf(C.mxs[0], gv[g][0], fmaf(C.mzs[0], gv[g][2], C.cys[0]));
+                const float dm = fmaf(C.mxs[0], gv[g][1], fmaf(C.mzs[0], gv[g][3], C.cys[0]));
+                M0[g] = fmaxf(fabsf(dp), fabsf(dm));
+                mx0 = fmaxf(mx0, m_ok ? M0[g] : 0.0f);
             }
             go = __any_sync(kFull, mx0 >= C.la);
         }
@@ -1232,9 +1247,18 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
                 att |= band_attention(C, lv[g], qv[g]);
             }
         } else {
+            // the endpoint form (fast_linear + band_stats) of the remaining slots
 #pragma unroll
             for (uint32_t g = 0; g < kStripG; ++g) {
-                band_chunk<kL, false>(C, rr[g], sc, lv[g], qv[g]);
+                float M[3];
+                M[0] = M0[g];
+#pragma unroll
+                for (int q = 1; q < 3; ++q) {
+                    const float dp = fmaf(C.mxs[q], gv[g][0], fmaf(C.mzs[q], gv[g][2], C.cys[q]));
+                    const float dm = fmaf(C.mxs[q], gv[g][1], fmaf(C.mzs[q], gv[g][3], C.cys[q]));
+                    M[q] = fmaxf(fabsf(dp), fabsf(dm));
+                }
+                band_stats_m<kL>(C, M, lv[g], qv[g]);
                 att |= band_attention(C, lv[g], qv[g]);
             }
             att &= m_ok;
