@@ -569,7 +569,7 @@ struct Smem {
 
 // Dynamic shared memory of phase 1: the code table only where it quantizes.
 template <int kMode>
-constexpr size_t phase1_smem() { return kMode == kModeBand ? offsetof(Smem, ctab) : sizeof(Smem); }
+__host__ __device__ constexpr size_t phase1_smem() { return kMode == kModeBand ? offsetof(Smem, ctab) : sizeof(Smem); }
 
 enum Table : int { kTabNone = 0, kTabCode = 1, kTabSignal = 2 };
 
