@@ -1186,7 +1186,10 @@ constexpr uint32_t kStripG = CVG_STRIP_G;  // rows per iteration: 4 or 8 (radius
 // 32 b + lane of the current 32-row block; each 32-row block's words are
 // stored to the strip's column of the pass-mask array (mcol[k], coalesced)
 // when the block ends.
-template <int kL, bool kCubeOnly, int kOut, class CT>
+// kCubeOnly: the strip form (rows below the strip's cube bound); else the
+// endpoint form, with x on the cube branch when kXCube (every row of the
+// range below the x half of the bound: no select for the x endpoints).
+template <int kL, bool kCubeOnly, int kOut, class CT, bool kXCube = false>
 __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, const StripConsts& Q,
                                            const LaunchArgs& A, float2 sc, bool m_ok, uint32_t m, uint32_t k,
                                            uint32_t kend, uint32_t& cnt, uint32_t& fk, Counters& ct,
@@ -1223,8 +1226,8 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
             float mx0 = 0.0f;
 #pragma unroll
             for (uint32_t g = 0; g < kStripG; ++g) {
-                gv[g][0] = finv_fast<false>(fmaf(rr[g], sc.x, C.fx0));
-                gv[g][1] = finv_fast<false>(fmaf(-rr[g], sc.x, C.fx0));
+                gv[g][0] = finv_fast<kXCube>(fmaf(rr[g], sc.x, C.fx0));
+                gv[g][1] = finv_fast<kXCube>(fmaf(-rr[g], sc.x, C.fx0));
                 gv[g][2] = finv_fast<false>(fmaf(-rr[g], sc.y, C.fz0));
                 gv[g][3] = finv_fast<false>(fmaf(rr[g], sc.y, C.fz0));
                 const float dp = fmaf(C.mxs[0], gv[g][0], fmaf(C.mzs[0], gv[g][2], C.cys[0]));
@@ -1372,7 +1375,15 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0
         return;
     }
     const Consts& C = C0;
-    strip_rows<kL, false, kOut>(S, C, Q, A, sc, m_ok, m, kc, kend, cnt, fk, ct, mcol);
+    // x stays on the cube branch in every remaining row (r |s'| below
+    // fx0 - u0 with the rcube margins): the endpoint form without the x select
+    const float rbx = fmaf(C.fx0 - kU0f, 1.0f - 4e-6f, -1e-6f) *
+                      __ldg(reinterpret_cast<const float2*>(A.strip_inv) + (m0 >> 5)).x * (1.0f - 1e-6f);
+    if (kend > kc && __ldg(&A.radii_f[kend - 1]) < rbx) {
+        strip_rows<kL, false, kOut, Consts, true>(S, C, Q, A, sc, m_ok, m, kc, kend, cnt, fk, ct, mcol);
+    } else {
+        strip_rows<kL, false, kOut>(S, C, Q, A, sc, m_ok, m, kc, kend, cnt, fk, ct, mcol);
+    }
 #pragma unroll 1
     for (uint32_t k = kend; k < k1; ++k) {
         const float r = __ldg(&A.radii_f[k]);
