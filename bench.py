@@ -536,9 +536,10 @@ def measure_config(cv, ctx, wl, args, rank, world, local, dist, flush, clk=None,
     if lwl.output == "pairs" and gather:
         out["gather"] = pair_gather(dist, plan, lwl, n_pairs, world, by)
 
-    if world == 1 and full:
+    if world == 1 and full and wl.output == "pairs":
         # CVG_PATH_PRUNED, reported apart: radius rows proven empty by a
         # certified FP64 bound are decided without per-candidate evaluation
+        # (row-major tiles; for COUNTS / FIRST the strip path outruns it)
         pp = ctx.plan(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles, output=wl.output,
                       path="pruned")
         pp.run(stream.cuda_stream)
