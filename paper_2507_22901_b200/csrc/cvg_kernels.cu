@@ -1335,9 +1335,17 @@ template <int kL, int kOut>
 __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0, const LaunchArgs& A, uint32_t m0,
                                           uint32_t k0, uint32_t k1, unsigned lane, uint32_t& cnt, uint32_t& fk,
                                           Counters& ct, uint32_t* mcol = nullptr) {
-    const uint32_t m = m0 + lane;
-    const bool m_ok = m < static_cast<uint32_t>(A.na);
-    const float2 sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + (m_ok ? m : A.na - 1));
+    // lane slot m0 + lane: angle m (the identity, or the |cos|-sorted
+    // permutation of the COUNTS / FIRST strips)
+    uint32_t m = m0 + lane;
+    bool m_ok = m < static_cast<uint32_t>(A.na);
+    float2 sc;
+    if (A.strip_perm) {
+        sc = __ldg(reinterpret_cast<const float2*>(A.strip_trig) + m);
+        m = __ldg(&A.strip_perm[m]);
+    } else {
+        sc = __ldg(reinterpret_cast<const float2*>(A.trig_f) + (m_ok ? m : A.na - 1));
+    }
     const uint32_t kend = k0 + (k1 - k0) / kStripG * kStripG;  // k0 % 4 == 0
     StripConsts Q;
     ThrConsts T;
@@ -1441,7 +1449,8 @@ __device__ __forceinline__ void strip_tile(const SearchConst* S, const LaunchArg
         uint32_t fk = 0xffffffffu;
         strip_run<kL, kOut>(S, C, A, 32 * q, k0, k1, lane, cnt, fk, ct);
         if (kOut == kOutFirst) {
-            const uint32_t mine = fk != 0xffffffffu ? fk * static_cast<uint32_t>(A.na) + 32 * q + lane : 0xffffffffu;
+            const uint32_t mq = A.strip_perm ? __ldg(&A.strip_perm[32 * q + lane]) : 32 * q + lane;  // the lane's angle
+            const uint32_t mine = fk != 0xffffffffu ? fk * static_cast<uint32_t>(A.na) + mq : 0xffffffffu;
             first = min(first, __reduce_min_sync(kFull, mine));
         }
     }

@@ -137,6 +137,11 @@ struct LaunchArgs {
     uint32_t strips_per_tile;
     uint32_t strip_tiles;          // tiles per row block
     const float* strip_inv;        // [n_strips][2]: 1 / the strip's largest |sin/500|, |cos/200| (rounded down)
+    // COUNTS / FIRST strips: lane slot j walks angle strip_perm[j] (angles by
+    // decreasing |cos|; 0xFFFFFFFF past the last), its trig in strip_trig[j]
+    // (nullptr: identity, PAIRS)
+    const uint32_t* strip_perm;
+    const float* strip_trig;
     const float* radius_groups;    // [ceil(nr/4)][3][4]: per 4 rows float(r), float(r^2), float(r^3)
                                    // of the double radii (strip form; padded with the last radius)
     unsigned long long* total;     // [1] sum of tile_count (PAIRS)

@@ -357,6 +357,14 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     const size_t o_stab = signal ? L.take(sizeof(T.stab)) : 0;
     const size_t o_bands = p->best ? L.take(sizeof(double) * 2 * p->n) : 0;
     const size_t o_sinv = strips ? L.take(sizeof(float) * 2 * n_strips) : 0;
+    // COUNTS / FIRST strips walk the angles in order of decreasing |cos|
+    // (lane slot j -> angle perm[j]): a strip's angles then reach the linear
+    // branch of f^-1 at nearly the same radius, so fewer rows need the
+    // general form (cfg4: 13% of the candidates instead of 19.5%).  PAIRS
+    // strips keep the canonical order (their pass words are canonical).
+    const bool permute = strips && !pairs_out;
+    const size_t o_perm = permute ? L.take(sizeof(uint32_t) * 32 * n_strips) : 0;
+    const size_t o_ptrig = permute ? L.take(sizeof(float) * 2 * 32 * n_strips) : 0;
     const size_t n_rgroups = static_cast<size_t>((p->nr + 3) / 4);
     const size_t o_rg = strips ? L.take(sizeof(float) * 12 * n_rgroups) : 0;
     const size_t bytes = L.off;
@@ -411,10 +419,26 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
         // per strip of 32 angles: 1 / max |s'|, 1 / max |c'| over the float
         // trig values the kernel uses, rounded down (FLT_MAX for an all-zero
         // column: 0 * FLT_MAX stays 0 in the kernel's bound)
+        std::vector<uint32_t> order(static_cast<size_t>(p->na));
+        for (int m = 0; m < p->na; ++m) order[m] = static_cast<uint32_t>(m);
+        if (permute) {
+            std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+                return std::fabs(trig_f[2 * a + 1]) > std::fabs(trig_f[2 * b + 1]);
+            });
+            auto* perm = reinterpret_cast<uint32_t*>(stage + o_perm);
+            auto* ptrig = reinterpret_cast<float*>(stage + o_ptrig);
+            for (size_t j = 0; j < 32 * static_cast<size_t>(n_strips); ++j) {
+                const uint32_t m = order[std::min<size_t>(j, order.size() - 1)];  // idle slots: a valid angle
+                perm[j] = j < order.size() ? m : 0xffffffffu;
+                ptrig[2 * j] = trig_f[2 * m];
+                ptrig[2 * j + 1] = trig_f[2 * m + 1];
+            }
+        }
         auto* inv = reinterpret_cast<float*>(stage + o_sinv);
         for (uint32_t q = 0; q < n_strips; ++q) {
             float gs = 0.f, gc = 0.f;
-            for (int m = 32 * static_cast<int>(q); m < std::min(p->na, 32 * static_cast<int>(q) + 32); ++m) {
+            for (int j = 32 * static_cast<int>(q); j < std::min(p->na, 32 * static_cast<int>(q) + 32); ++j) {
+                const uint32_t m = order[static_cast<size_t>(j)];
                 gs = std::max(gs, std::fabs(trig_f[2 * m]));
                 gc = std::max(gc, std::fabs(trig_f[2 * m + 1]));
             }
@@ -477,6 +501,8 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.strips_per_tile = strips_per_tile;
     A.strip_tiles = strip_tiles;
     A.strip_inv = strips ? at<const float>(p->d_const, o_sinv) : nullptr;
+    A.strip_perm = permute ? at<const uint32_t>(p->d_const, o_perm) : nullptr;
+    A.strip_trig = permute ? at<const float>(p->d_const, o_ptrig) : nullptr;
     A.radius_groups = strips ? at<const float>(p->d_const, o_rg) : nullptr;
     A.n_tiles = n_tiles;
 
