@@ -530,14 +530,17 @@ __device__ __forceinline__ bool band_certain(const CT& C, float minl, float maxq
 // to [0, 1]: the table has no threshold within kCodeSlack of 0 or 1, so a
 // value below 0 (above 1) gets code 0 (255) exactly as its FP64 twin does.
 // `tab` = shared address of the table minus 8 * bits(2^23).
+// The increment is the sign bit of d = t - xs (one LEA.HI): when ok, d != 0
+// and sign(d) = (xs > t) = (xs >= t); when not ok the result is c or c + 1
+// either way, which is all the callers assume of an unverified code.
 __device__ __forceinline__ int code_fast(float xs, float E, uint32_t tab, bool& ok) {
     const float b = fmaf(xs, static_cast<float>(kGuessBuckets), 8388608.0f);  // bits: 0x4B000000 + round(xs * 4096)
     float t;
     int c;
     asm("ld.shared.v2.b32 {%0, %1}, [%2];" : "=f"(t), "=r"(c) : "r"(tab + (__float_as_uint(b) << 3)));
-    ok = fabsf(__fsub_rn(xs, t)) > E;
-    if (xs >= t) ++c;  // one predicated add
-    return c;
+    const float d = __fsub_rn(t, xs);
+    ok = fabsf(d) > E;
+    return c + static_cast<int>(__float_as_uint(d) >> 31);
 }
 
 // Passed through a shuffle, so that it is opaque to ptxas and each lookup is
@@ -1796,32 +1799,36 @@ __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, c
                                          uint32_t kt, uint32_t* out_idx, uint8_t* out_codes, unsigned lane,
                                          Counters& ct) {
     const float2* trig = reinterpret_cast<const float2*>(A.trig_f);
-    const uint32_t last = cnt - 1;
     const float rt = __ldg(&A.radii_f[kt]);
-    uint32_t off_n = list[min(32 + lane, last)];
-    uint32_t i = i0 + list[min(lane, last)];
+    // per-lane cursors (one add each per iteration instead of re-deriving
+    // 64-bit addresses from the item base); entries past the item read as
+    // offset 0, a valid candidate whose codes are computed and not written
+    const uint16_t* pl = list + 64 + lane;
+    uint32_t* po = out_idx + lane;
+    uint16_t* pc = reinterpret_cast<uint16_t*>(out_codes) + 3 * lane;
+    const int cnt_l = static_cast<int>(cnt) - static_cast<int>(lane);  // iteration p is active iff p < cnt_l
+    uint32_t off_n = 32 < cnt_l ? list[32 + lane] : 0u;
+    uint32_t i = i0 + (0 < cnt_l ? list[lane] : 0u);
     uint32_t k = kOneRow ? kt : div_na(i, A);
     uint32_t m = i - k * static_cast<uint32_t>(A.na);
     float r = kOneRow ? rt : __ldg(&A.radii_f[k]);
     float2 sc = __ldg(trig + m);
 #pragma unroll 1
-    for (uint32_t p = 0; p < cnt; p += 32) {
+    for (int p = 0; p < static_cast<int>(cnt); p += 32, pl += 32, po += 32, pc += 96) {
         const uint32_t i_n = i0 + off_n;
         const uint32_t k_n = kOneRow ? kt : div_na(i_n, A);
         const uint32_t m_n = i_n - k_n * static_cast<uint32_t>(A.na);
         const float r_n = kOneRow ? rt : __ldg(&A.radii_f[k_n]);
         const float2 sc_n = __ldg(trig + m_n);
-        off_n = list[min(p + 64 + lane, last)];
-        const uint32_t qq = p + lane;
-        const bool active = qq < cnt;
+        off_n = p + 64 < cnt_l ? *pl : 0u;
+        const bool active = p < cnt_l;
         int cp[3], cm[3];
         codes_fast(sm, S, CC, A, k, m, r, sc, active, cp, cm, ct.code_repairs);
         if (active) {
-            out_idx[qq] = i;
-            uint16_t* c16 = reinterpret_cast<uint16_t*>(out_codes + 6 * qq);
-            c16[0] = static_cast<uint16_t>(cp[0] | (cp[1] << 8));
-            c16[1] = static_cast<uint16_t>(cp[2] | (cm[0] << 8));
-            c16[2] = static_cast<uint16_t>(cm[1] | (cm[2] << 8));
+            *po = i;
+            pc[0] = static_cast<uint16_t>(__byte_perm(cp[0], cp[1], 0x40));
+            pc[1] = static_cast<uint16_t>(__byte_perm(cp[2], cm[0], 0x40));
+            pc[2] = static_cast<uint16_t>(__byte_perm(cm[1], cm[2], 0x40));
         }
         i = i_n;
         k = k_n;
