@@ -1796,8 +1796,8 @@ __device__ __forceinline__ void store_pair(const LaunchArgs& A, unsigned long lo
 template <bool kOneRow>
 __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, const CodeConsts& CC,
                                          const LaunchArgs& A, const uint16_t* list, uint32_t cnt, uint32_t i0,
-                                         uint32_t kt, uint32_t* out_idx, uint8_t* out_codes, unsigned lane,
-                                         Counters& ct) {
+                                         uint32_t kt, uint32_t mt, uint32_t* out_idx, uint8_t* out_codes,
+                                         unsigned lane, Counters& ct) {
     const float2* trig = reinterpret_cast<const float2*>(A.trig_f);
     const float rt = __ldg(&A.radii_f[kt]);
     // per-lane cursors (one add each per iteration instead of re-deriving
@@ -1806,18 +1806,21 @@ __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, c
     const uint16_t* pl = list + 64 + lane;
     uint32_t* po = out_idx + lane;
     uint16_t* pc = reinterpret_cast<uint16_t*>(out_codes) + 3 * lane;
-    const int cnt_l = static_cast<int>(cnt) - static_cast<int>(lane);  // iteration p is active iff p < cnt_l
+    // through shuffles: ptxas would otherwise re-derive both (and mt's
+    // division) inside the loop to save the two registers
+    const int cnt_l = __shfl_sync(kFull, static_cast<int>(cnt) - static_cast<int>(lane), lane);  // active iff p < cnt_l
+    mt = __shfl_sync(kFull, mt, 0);
     uint32_t off_n = 32 < cnt_l ? list[32 + lane] : 0u;
     uint32_t i = i0 + (0 < cnt_l ? list[lane] : 0u);
     uint32_t k = kOneRow ? kt : div_na(i, A);
-    uint32_t m = i - k * static_cast<uint32_t>(A.na);
+    uint32_t m = kOneRow ? i - i0 + mt : i - k * static_cast<uint32_t>(A.na);
     float r = kOneRow ? rt : __ldg(&A.radii_f[k]);
     float2 sc = __ldg(trig + m);
 #pragma unroll 1
     for (int p = 0; p < static_cast<int>(cnt); p += 32, pl += 32, po += 32, pc += 96) {
         const uint32_t i_n = i0 + off_n;
         const uint32_t k_n = kOneRow ? kt : div_na(i_n, A);
-        const uint32_t m_n = i_n - k_n * static_cast<uint32_t>(A.na);
+        const uint32_t m_n = kOneRow ? mt + off_n : i_n - k_n * static_cast<uint32_t>(A.na);
         const float r_n = kOneRow ? rt : __ldg(&A.radii_f[k_n]);
         const float2 sc_n = __ldg(trig + m_n);
         off_n = p + 64 < cnt_l ? *pl : 0u;
@@ -1843,7 +1846,7 @@ __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, c
 // (next claim prefetched), so no warp holds more than 8 chunks of work; the
 // item's list entries are read one chunk ahead.
 template <int kMode, int kPath>
-__global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
+__global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
     load_tables<kTabCode>(sm, A);  // constant inputs only: before the wait
@@ -1881,9 +1884,9 @@ __global__ void __launch_bounds__(kBlock, 3) emit_kernel(const LaunchArgs A) {
                 uint32_t* out_idx = A.out_idx + base;
                 uint8_t* out_codes = A.out_codes + 6 * base;
                 if (mt + static_cast<uint32_t>(kTile) <= static_cast<uint32_t>(A.na)) {
-                    emit_run<true>(sm, S, CC, A, list, cnt, i0, kt, out_idx, out_codes, lane, ct);
+                    emit_run<true>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes, lane, ct);
                 } else {
-                    emit_run<false>(sm, S, CC, A, list, cnt, i0, kt, out_idx, out_codes, lane, ct);
+                    emit_run<false>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes, lane, ct);
                 }
             } else {
 #pragma unroll 1
