@@ -574,6 +574,11 @@ struct Smem {
 template <int kMode>
 __host__ __device__ constexpr size_t phase1_smem() { return kMode == kModeBand ? offsetof(Smem, ctab) : sizeof(Smem); }
 
+// Dynamic shared memory of the emit kernel: the tables + each warp's repair
+// queue (emit_run).
+constexpr int kRepairQueueSlots = 64;
+constexpr size_t emit_smem() { return sizeof(Smem) + kWarpsPerBlock * kRepairQueueSlots * sizeof(uint2); }
+
 enum Table : int { kTabNone = 0, kTabCode = 1, kTabSignal = 2 };
 
 template <int kTab>
@@ -629,9 +634,9 @@ __device__ __forceinline__ void audit_ratio(const SearchConst* S, const float* v
 // exact: values whose code is not proven by the bound go to FP64 (all six
 // values recomputed op-for-op, codes walked from the FP32 guess).  Called by
 // all 32 lanes (warp vote inside).
-__device__ __forceinline__ void codes_fast(const Smem& sm, const SearchConst* S, const CodeConsts& C,
-                                           const LaunchArgs& A, uint32_t k, uint32_t m, float r, float2 sc,
-                                           bool active, int* cp, int* cm, unsigned long long& repairs) {
+// FP32 codes of the six endpoint channels (code_fast each); true iff all six
+// are proven.  Called by all 32 lanes (warp vote inside).
+__device__ __forceinline__ bool codes_guess(const CodeConsts& C, float r, float2 sc, int* cp, int* cm) {
     float vp[3], vm[3];
     if (__all_sync(kFull, r < C.rcube)) {  // every lane's row stays on the cube branch
         fast_linear<true, true>(C.fx0, C.fz0, C.mx, C.mz, C.cy, r, sc, vp, vm);
@@ -646,6 +651,13 @@ __device__ __forceinline__ void codes_fast(const Smem& sm, const SearchConst* S,
         cm[q] = code_fast(vm[q], C.ec[q], C.tab, ok2);
         all_ok &= ok1 & ok2;
     }
+    return all_ok;
+}
+
+__device__ __forceinline__ void codes_fast(const Smem& sm, const SearchConst* S, const CodeConsts& C,
+                                           const LaunchArgs& A, uint32_t k, uint32_t m, float r, float2 sc,
+                                           bool active, int* cp, int* cm, unsigned long long& repairs) {
+    const bool all_ok = codes_guess(C, r, sc, cp, cm);
     if (__any_sync(kFull, !all_ok) && !all_ok) {
         double lp[3], lm[3];
         exact_linear_inl(S, A, k, m, lp, lm);
@@ -1792,14 +1804,48 @@ __device__ __forceinline__ void store_pair(const LaunchArgs& A, unsigned long lo
 // `list`, written to out_idx / out_codes (the item's slice).  Software
 // pipeline: list entries two iterations ahead, the candidate's radius / trig
 // loads one iteration ahead.  kOneRow: the tile lies inside radius row kt
-// (no per-pair division, no radius load).
+// (angle = mt + list offset: no per-pair division, no radius load).
+// Candidates whose FP32 codes are not all proven (~0.4%) do not take the FP64
+// path where they occur (a whole warp pass for one lane): their item-local
+// index and FP32 guesses go to the warp's queue in shared memory, and each
+// 32 queued pairs are repaired together by the full warp (emit_repair).
+constexpr int kRepairQueue = kRepairQueueSlots;  // per warp: < 32 waiting + one iteration's 32
+
+template <bool kOneRow>
+__device__ __forceinline__ void emit_repair(const Smem& sm, const SearchConst* S, const LaunchArgs& A,
+                                         const uint16_t* list, uint32_t i0, uint32_t kt, uint32_t mt,
+                                         uint8_t* out_codes, const uint2* q, uint32_t n, unsigned lane,
+                                         unsigned long long& repairs) {
+    if (lane >= n) return;
+    const uint2 e = q[lane];
+    const uint32_t qq = (e.x >> 24) | ((e.y >> 24) << 8);
+    const uint32_t off = list[qq];
+    const uint32_t i = i0 + off;
+    const uint32_t k = kOneRow ? kt : div_na(i, A);
+    const uint32_t m = kOneRow ? mt + off : i - k * static_cast<uint32_t>(A.na);
+    double lp[3], lm[3];
+    exact_linear_inl(S, A, k, m, lp, lm);
+    int cp[3], cm[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        cp[c] = code_exact_from(lp[c], (e.x >> (8 * c)) & 0xff, sm.thr_d);
+        cm[c] = code_exact_from(lm[c], (e.y >> (8 * c)) & 0xff, sm.thr_d);
+    }
+    uint16_t* pc = reinterpret_cast<uint16_t*>(out_codes) + 3 * qq;
+    pc[0] = static_cast<uint16_t>(__byte_perm(cp[0], cp[1], 0x40));
+    pc[1] = static_cast<uint16_t>(__byte_perm(cp[2], cm[0], 0x40));
+    pc[2] = static_cast<uint16_t>(__byte_perm(cm[1], cm[2], 0x40));
+    ++repairs;
+}
+
 template <bool kOneRow>
 __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, const CodeConsts& CC,
                                          const LaunchArgs& A, const uint16_t* list, uint32_t cnt, uint32_t i0,
                                          uint32_t kt, uint32_t mt, uint32_t* out_idx, uint8_t* out_codes,
-                                         unsigned lane, Counters& ct) {
+                                         uint2* queue, unsigned lane, Counters& ct) {
     const float2* trig = reinterpret_cast<const float2*>(A.trig_f);
     const float rt = __ldg(&A.radii_f[kt]);
+    const unsigned lane_lt = (1u << lane) - 1u;
     // per-lane cursors (one add each per iteration instead of re-deriving
     // 64-bit addresses from the item base); entries past the item read as
     // offset 0, a valid candidate whose codes are computed and not written
@@ -1816,6 +1862,7 @@ __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, c
     uint32_t m = kOneRow ? i - i0 + mt : i - k * static_cast<uint32_t>(A.na);
     float r = kOneRow ? rt : __ldg(&A.radii_f[k]);
     float2 sc = __ldg(trig + m);
+    uint32_t nq = 0;
 #pragma unroll 1
     for (int p = 0; p < static_cast<int>(cnt); p += 32, pl += 32, po += 32, pc += 96) {
         const uint32_t i_n = i0 + off_n;
@@ -1826,18 +1873,41 @@ __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, c
         off_n = p + 64 < cnt_l ? *pl : 0u;
         const bool active = p < cnt_l;
         int cp[3], cm[3];
-        codes_fast(sm, S, CC, A, k, m, r, sc, active, cp, cm, ct.code_repairs);
+        const bool ok = codes_guess(CC, r, sc, cp, cm);
         if (active) {
             *po = i;
-            pc[0] = static_cast<uint16_t>(__byte_perm(cp[0], cp[1], 0x40));
-            pc[1] = static_cast<uint16_t>(__byte_perm(cp[2], cm[0], 0x40));
-            pc[2] = static_cast<uint16_t>(__byte_perm(cm[1], cm[2], 0x40));
+            if (ok) {
+                pc[0] = static_cast<uint16_t>(__byte_perm(cp[0], cp[1], 0x40));
+                pc[1] = static_cast<uint16_t>(__byte_perm(cp[2], cm[0], 0x40));
+                pc[2] = static_cast<uint16_t>(__byte_perm(cm[1], cm[2], 0x40));
+            }
+        }
+        const unsigned rep = __ballot_sync(kFull, active & !ok);
+        if (rep) {
+            if (active & !ok) {
+                const uint32_t qq = p + lane;
+                queue[nq + __popc(rep & lane_lt)] =
+                    make_uint2(cp[0] | (cp[1] << 8) | (cp[2] << 16) | (qq << 24),
+                               cm[0] | (cm[1] << 8) | (cm[2] << 16) | ((qq >> 8) << 24));
+            }
+            nq += __popc(rep);
+            if (nq >= 32) {
+                nq -= 32;
+                __syncwarp();
+                emit_repair<kOneRow>(sm, S, A, list, i0, kt, mt, out_codes, queue + nq, 32, lane, ct.code_repairs);
+                __syncwarp();
+            }
         }
         i = i_n;
         k = k_n;
         m = m_n;
         r = r_n;
         sc = sc_n;
+    }
+    if (nq) {
+        __syncwarp();
+        emit_repair<kOneRow>(sm, S, A, list, i0, kt, mt, out_codes, queue, nq, lane, ct.code_repairs);
+        __syncwarp();
     }
 }
 
@@ -1849,6 +1919,7 @@ template <int kMode, int kPath>
 __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+    uint2* queue = reinterpret_cast<uint2*>(smem_raw + sizeof(Smem)) + (threadIdx.x >> 5) * kRepairQueue;
     load_tables<kTabCode>(sm, A);  // constant inputs only: before the wait
     const uint32_t tab = ctab_addr(sm.ctab);
     pdl_wait();  // scan (and so phase 1) complete
@@ -1884,9 +1955,9 @@ __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
                 uint32_t* out_idx = A.out_idx + base;
                 uint8_t* out_codes = A.out_codes + 6 * base;
                 if (mt + static_cast<uint32_t>(kTile) <= static_cast<uint32_t>(A.na)) {
-                    emit_run<true>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes, lane, ct);
+                    emit_run<true>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes, queue, lane, ct);
                 } else {
-                    emit_run<false>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes, lane, ct);
+                    emit_run<false>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes, queue, lane, ct);
                 }
             } else {
 #pragma unroll 1
@@ -2117,7 +2188,7 @@ cudaError_t launch_pdl_bands(unsigned grid, const LaunchArgs& a, const double* b
 template <int kMode, int kPath>
 cudaError_t emit_t(const LaunchArgs& a, int grid, int threads, cudaStream_t st) {
     grid = work_grid(grid, a.n_tiles * (kTile / kEmitSpan), threads / 32);
-    return launch_pdl(emit_kernel<kMode, kPath>, grid, threads, sizeof(Smem), st, a);
+    return launch_pdl(emit_kernel<kMode, kPath>, grid, threads, emit_smem(), st, a);
 }
 
 cudaError_t scan_l(const LaunchArgs& a, cudaStream_t st) {
@@ -2142,7 +2213,7 @@ int occupancy_t() {
     auto f1 = phase1_kernel<kMode, kOut, kPath>;
     auto f3 = emit_kernel<kMode, emit_path(kMode, kPath)>;
     cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(phase1_smem<kMode>()));
-    cudaFuncSetAttribute(f3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sizeof(Smem)));
+    cudaFuncSetAttribute(f3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(emit_smem()));
     int blocks = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f1, kBlock, phase1_smem<kMode>()) != cudaSuccess)
         return 0;
