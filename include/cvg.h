@@ -178,6 +178,10 @@ CVG_API int cvg_plan_copy_outputs(cvg_plan* plan, uint64_t* counts, uint32_t* id
 CVG_API int cvg_plan_copy_first(cvg_plan* plan, uint32_t* first_idx, uint8_t* first_codes, void* stream);
 /* searches the plan's kernels evaluate (MEMO: the distinct ones; else all) */
 CVG_API int32_t cvg_plan_evaluated_searches(const cvg_plan* plan);
+/* 1 if the plan's PAIRS emit uses twin tiles: on a grid symmetric under
+ * theta -> theta + pi (proven on the host), each pair of tiles whose pass
+ * words are identical is quantized once and written twice */
+CVG_API int cvg_plan_twin_tiles(const cvg_plan* plan);
 /* device time (ms) of the search kernel(s) of the plan's last completed run */
 CVG_API int cvg_plan_last_kernel_ms(cvg_plan* plan, float* ms);
 /* per-kernel device time (ms) of the last run: phase 1 (candidate decisions),

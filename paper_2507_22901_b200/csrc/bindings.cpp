@@ -788,6 +788,7 @@ PYBIND11_MODULE(_core, m) {
              },
              py::arg("idx"), py::arg("codes"), py::arg("stream") = 0)
         .def_property_readonly("evaluated_searches", [](const Plan& p) { return cvg_plan_evaluated_searches(p.plan); })
+        .def_property_readonly("twin_tiles", [](const Plan& p) { return cvg_plan_twin_tiles(p.plan) != 0; })
         .def("device_outputs", [](Plan& p) {
             uint64_t* counts = nullptr;
             uint32_t* idx = nullptr;

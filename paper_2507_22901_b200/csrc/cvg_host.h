@@ -489,6 +489,7 @@ struct cvg_plan {
     // CVG_OUT_BEST: the PAIRS kernels, then best_kernel (select_best per
     // search on the device pair buffer) into the first_* arrays
     bool best = false;
+    bool twin = false;  // PAIRS: twin tiles (LaunchArgs::twin)
     const double* d_bands = nullptr;  // BEST: (v_th, low_band) per search
     int32_t n_exec = 0;
     const uint32_t* d_map = nullptr;

@@ -1627,6 +1627,39 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
 // row-major loop.
 constexpr uint32_t kListWords = 1024;
 
+// Appends the set bits of one 32-word chunk (lane l: word W of strip
+// wbase + l, bit b = angle 32 (wbase + l) + b of the tile) to `list` after
+// `cnt` entries, in canonical order; returns the new count (warp-uniform).
+__device__ __forceinline__ uint32_t expand_chunk(uint32_t W, uint32_t wbase, uint16_t* list, uint32_t cnt,
+                                                 unsigned lane, unsigned lane_lt) {
+    const uint32_t pc = __popc(W);
+    uint32_t incl = pc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= static_cast<unsigned>(o)) incl += y;
+    }
+    uint32_t nz = __ballot_sync(kFull, W != 0);
+    while (nz) {
+        const int q = __ffs(nz) - 1;
+        nz &= nz - 1;
+        const uint32_t Wq = __shfl_sync(kFull, W, q);
+        const uint32_t oq = __shfl_sync(kFull, incl - pc, q);
+        if ((Wq >> lane) & 1u) {
+            list[cnt + oq + __popc(Wq & lane_lt)] = static_cast<uint16_t>(32u * (wbase + q) + lane);
+        }
+    }
+    return cnt + __shfl_sync(kFull, incl, 31);
+}
+
+// Twin tiles (A.twin, rows of whole tiles): the units cover the first half of
+// each row's tiles; each unit also reads the words of the twin column (same
+// rows, angles + na/2) with the same coalesced loads and compares them in
+// registers.  A row whose twin words are all identical is one list for two
+// tiles (twin[t] = 1, the twin gets the count and no list of its own); a row
+// with any difference (a decision the FP64 repair settled differently for
+// the two angles) builds the twin's list from its own words, and the twin is
+// emitted on its own.
 __global__ void __launch_bounds__(kBlock) lists_kernel(const LaunchArgs A) {
     __shared__ uint32_t blk[kWarpsPerBlock][kListWords + 32];
     pdl_wait();  // phase 1 complete: every pass word written
@@ -1634,14 +1667,16 @@ __global__ void __launch_bounds__(kBlock) lists_kernel(const LaunchArgs A) {
     const unsigned lane_lt = (1u << lane) - 1u;
     uint32_t* Wb = blk[warp];
     const uint32_t nq = static_cast<uint32_t>(A.na) >> 5;
-    const uint32_t ur = A.lst_unit_rows;                     // rows per unit (divides 32)
+    const uint32_t ur = A.lst_unit_rows;                     // rows per unit (divides 32; 8 with twins)
     const uint32_t n_kb = (static_cast<uint32_t>(A.nr) + ur - 1) / ur;
-    const uint32_t n_cb = A.lst_tpr ? A.lst_tpr : 1u;
+    const uint32_t hcb = A.twin ? A.twin_tiles : 0u;         // twin column offset (0: no twins)
+    const uint32_t n_cb = A.lst_tpr ? A.lst_tpr - hcb : 1u;
     const uint32_t cwu = min(nq, 128u);
     const uint32_t stride = cwu + 1;                         // shared row stride (bank-conflict free)
     const uint32_t ups = n_kb * n_cb;
     const uint32_t n_units = A.range_searches * ups;
     const uint32_t per_load = 32u / ur;                      // strips per load instruction
+    const size_t twin_col = static_cast<size_t>(128u * hcb) * A.mask_rows;
     uint32_t u_claim = 0;
     if (lane == 0) u_claim = atomicAdd(&A.ticket[4], 1u);
     uint32_t u = __shfl_sync(kFull, u_claim, 0);
@@ -1652,62 +1687,81 @@ __global__ void __launch_bounds__(kBlock) lists_kernel(const LaunchArgs A) {
         const uint32_t kb = r / n_cb, cb = r - kb * n_cb;
         const uint32_t k0 = ur * kb, rows = min(ur, static_cast<uint32_t>(A.nr) - k0);
         const uint32_t* mblk = A.masks + static_cast<size_t>(s) * nq * A.mask_rows;
+        uint32_t split = 0;  // twins: bit j = row k0 + j differs from its twin row
         // load: lane -> (strip qs + lane / ur, row k0 + lane % ur)
         {
             const uint32_t kr = lane % ur, qo = lane / ur;
             const uint32_t* col = mblk + static_cast<size_t>(128u * cb + qo) * A.mask_rows + k0 + kr;
+            uint32_t diff = 0;
 #pragma unroll 4
             for (uint32_t qs = 0; qs < cwu; qs += per_load) {
-                if (qs + qo < cwu) Wb[kr * stride + qs + qo] = __ldg(col + static_cast<size_t>(qs) * A.mask_rows);
+                if (qs + qo < cwu) {
+                    const uint32_t w = __ldg(col + static_cast<size_t>(qs) * A.mask_rows);
+                    Wb[kr * stride + qs + qo] = w;
+                    if (hcb) diff |= w ^ __ldg(col + twin_col + static_cast<size_t>(qs) * A.mask_rows);
+                }
+            }
+            if (hcb) {  // ur == 8: lanes j, j + 8, j + 16, j + 24 hold row j
+                const unsigned dm = __ballot_sync(kFull, diff != 0u);
+                split = (dm | dm >> 8 | dm >> 16 | dm >> 24) & 0xffu;
+                if (A.twin_split_test) split |= 0xaau & ((1u << rows) - 1u);
             }
         }
         __syncwarp();
-        uint32_t tcnt = 0;  // lane j: count of the unit's tile slot j
+        uint32_t tcnt = 0;   // lane j: count of the unit's tile slot j
+        uint32_t tcnt2 = 0;  // twins: lane j: count of slot j's twin when its row differs
         for (uint32_t j = 0; j < rows; ++j) {
             const uint32_t row = k0 + j;
             const uint32_t slot = A.lst_rpt ? j / A.lst_rpt : j;
             const uint32_t lt = A.lst_rpt ? row / A.lst_rpt : row * A.lst_tpr + cb;
             uint16_t* list = A.scratch + static_cast<size_t>(s * A.tiles_per_search + lt) * kTile;
+            // word index of strip qc + l inside the tile
+            const uint32_t wrow = A.lst_rpt ? (row % A.lst_rpt) * nq : 0u;
             for (uint32_t qc = 0; qc < cwu; qc += 32) {
                 const uint32_t W = qc + lane < cwu ? Wb[j * stride + qc + lane] : 0u;
                 if (!__any_sync(kFull, W != 0u)) continue;
-                // word index of strip qc + l inside the tile
-                const uint32_t wbase = A.lst_rpt ? (row % A.lst_rpt) * nq + qc : qc;
                 uint32_t cnt = __shfl_sync(kFull, tcnt, slot);
-                const uint32_t pc = __popc(W);
-                uint32_t incl = pc;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= static_cast<unsigned>(o)) incl += y;
-                }
-                uint32_t nz = __ballot_sync(kFull, W != 0);
-                while (nz) {
-                    const int q = __ffs(nz) - 1;
-                    nz &= nz - 1;
-                    const uint32_t Wq = __shfl_sync(kFull, W, q);
-                    const uint32_t oq = __shfl_sync(kFull, incl - pc, q);
-                    if ((Wq >> lane) & 1u) {
-                        list[cnt + oq + __popc(Wq & lane_lt)] = static_cast<uint16_t>(32u * (wbase + q) + lane);
-                    }
-                }
-                cnt += __shfl_sync(kFull, incl, 31);
+                cnt = expand_chunk(W, wrow + qc, list, cnt, lane, lane_lt);
                 if (lane == slot) tcnt = cnt;
+            }
+            if ((split >> j) & 1u) {  // rare: the twin row gets its own list
+                uint16_t* list2 = list + static_cast<size_t>(hcb) * kTile;
+                const uint32_t* col2 = mblk + twin_col + static_cast<size_t>(128u * cb) * A.mask_rows + row;
+                uint32_t cnt2 = 0;
+                for (uint32_t qc = 0; qc < cwu; qc += 32) {
+                    const uint32_t W = qc + lane < cwu ? __ldg(col2 + static_cast<size_t>(qc + lane) * A.mask_rows) : 0u;
+                    if (!__any_sync(kFull, W != 0u)) continue;
+                    cnt2 = expand_chunk(W, qc, list2, cnt2, lane, lane_lt);
+                }
+                if (lane == slot) tcnt2 = cnt2;
             }
         }
         __syncwarp();
         const uint32_t n_slots = A.lst_rpt ? (rows + A.lst_rpt - 1) / A.lst_rpt : rows;
+        uint32_t mine = 0;
         if (lane < n_slots) {
             const uint32_t lt = A.lst_rpt ? k0 / A.lst_rpt + lane : (k0 + lane) * A.lst_tpr + cb;
             const uint32_t t = s * A.tiles_per_search + lt;
             A.tile_count[t] = tcnt;
-            const uint32_t subs = (tcnt + (1u << A.emit_shift) - 1) >> A.emit_shift;
-            if (subs) {
-                const uint32_t w = atomicAdd(&A.ticket[3], subs);
+            mine = tcnt;
+            uint32_t subs = (tcnt + (1u << A.emit_shift) - 1) >> A.emit_shift;
+            uint32_t subs2 = 0, c2 = 0;
+            if (hcb) {
+                const bool tw = !((split >> lane) & 1u);
+                c2 = tw ? tcnt : tcnt2;
+                A.tile_count[t + hcb] = c2;
+                A.twin[t] = tw ? 1u : 0u;
+                A.twin[t + hcb] = 0u;
+                if (!tw) subs2 = (c2 + (1u << A.emit_shift) - 1) >> A.emit_shift;
+                mine += c2;
+            }
+            if (subs + subs2) {
+                const uint32_t w = atomicAdd(&A.ticket[3], subs + subs2);
                 for (uint32_t q = 0; q < subs; ++q) A.worklist[w + q] = (t << 4) | q;
+                for (uint32_t q = 0; q < subs2; ++q) A.worklist[w + subs + q] = ((t + hcb) << 4) | q;
             }
         }
-        const uint32_t total = __reduce_add_sync(kFull, lane < n_slots ? tcnt : 0u);
+        const uint32_t total = __reduce_add_sync(kFull, mine);
         if (lane == 0 && total) atomicAdd(&A.counts[s], static_cast<unsigned long long>(total));
         u = __shfl_sync(kFull, u_claim, 0);
     }
@@ -1811,11 +1865,21 @@ __device__ __forceinline__ void store_pair(const LaunchArgs& A, unsigned long lo
 // 32 queued pairs are repaired together by the full warp (emit_repair).
 constexpr int kRepairQueue = kRepairQueueSlots;  // per warp: < 32 waiting + one iteration's 32
 
-template <bool kOneRow>
+__device__ __forceinline__ void store_codes16(uint8_t* codes, uint32_t qq, const int* p, const int* m) {
+    uint16_t* pc = reinterpret_cast<uint16_t*>(codes) + 3 * qq;
+    pc[0] = static_cast<uint16_t>(__byte_perm(p[0], p[1], 0x40));
+    pc[1] = static_cast<uint16_t>(__byte_perm(p[2], m[0], 0x40));
+    pc[2] = static_cast<uint16_t>(__byte_perm(m[1], m[2], 0x40));
+}
+
+// kTwin: the pair is also the twin tile's pair qq (angle m + twin_m, the
+// endpoints swapped); its codes come from its own FP64 values (the FP32
+// guesses, swapped, are the walk's starting points).
+template <bool kOneRow, bool kTwin>
 __device__ __forceinline__ void emit_repair(const Smem& sm, const SearchConst* S, const LaunchArgs& A,
                                          const uint16_t* list, uint32_t i0, uint32_t kt, uint32_t mt,
-                                         uint8_t* out_codes, const uint2* q, uint32_t n, unsigned lane,
-                                         unsigned long long& repairs) {
+                                         uint8_t* out_codes, uint8_t* out_codes2, const uint2* q, uint32_t n,
+                                         unsigned lane, unsigned long long& repairs) {
     if (lane >= n) return;
     const uint2 e = q[lane];
     const uint32_t qq = (e.x >> 24) | ((e.y >> 24) << 8);
@@ -1831,18 +1895,30 @@ __device__ __forceinline__ void emit_repair(const Smem& sm, const SearchConst* S
         cp[c] = code_exact_from(lp[c], (e.x >> (8 * c)) & 0xff, sm.thr_d);
         cm[c] = code_exact_from(lm[c], (e.y >> (8 * c)) & 0xff, sm.thr_d);
     }
-    uint16_t* pc = reinterpret_cast<uint16_t*>(out_codes) + 3 * qq;
-    pc[0] = static_cast<uint16_t>(__byte_perm(cp[0], cp[1], 0x40));
-    pc[1] = static_cast<uint16_t>(__byte_perm(cp[2], cm[0], 0x40));
-    pc[2] = static_cast<uint16_t>(__byte_perm(cm[1], cm[2], 0x40));
+    store_codes16(out_codes, qq, cp, cm);
     ++repairs;
+    if (kTwin) {
+        exact_linear_inl(S, A, k, m + A.twin_m, lp, lm);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            cp[c] = code_exact_from(lp[c], (e.y >> (8 * c)) & 0xff, sm.thr_d);
+            cm[c] = code_exact_from(lm[c], (e.x >> (8 * c)) & 0xff, sm.thr_d);
+        }
+        store_codes16(out_codes2, qq, cp, cm);
+        ++repairs;
+    }
 }
 
-template <bool kOneRow>
+// kTwin (one-row tiles only): every pair is written twice, as itself at
+// out_idx / out_codes and as the twin tile's pair at out_idx2 / out_codes2
+// (idx + twin_m, plus and minus codes swapped).  The caller widened CC.ec by
+// kTwinSlack, so a verified code is the exact code of both records.
+template <bool kOneRow, bool kTwin = false>
 __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, const CodeConsts& CC,
                                          const LaunchArgs& A, const uint16_t* list, uint32_t cnt, uint32_t i0,
                                          uint32_t kt, uint32_t mt, uint32_t* out_idx, uint8_t* out_codes,
-                                         uint2* queue, unsigned lane, Counters& ct) {
+                                         uint32_t* out_idx2, uint8_t* out_codes2, uint2* queue, unsigned lane,
+                                         Counters& ct) {
     const float2* trig = reinterpret_cast<const float2*>(A.trig_f);
     const float rt = __ldg(&A.radii_f[kt]);
     const unsigned lane_lt = (1u << lane) - 1u;
@@ -1852,6 +1928,9 @@ __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, c
     const uint16_t* pl = list + 64 + lane;
     uint32_t* po = out_idx + lane;
     uint16_t* pc = reinterpret_cast<uint16_t*>(out_codes) + 3 * lane;
+    uint32_t* po2 = kTwin ? out_idx2 + lane : nullptr;
+    uint16_t* pc2 = kTwin ? reinterpret_cast<uint16_t*>(out_codes2) + 3 * lane : nullptr;
+    const uint32_t tm = kTwin ? A.twin_m : 0u;
     // through shuffles: ptxas would otherwise re-derive both (and mt's
     // division) inside the loop to save the two registers
     const int cnt_l = __shfl_sync(kFull, static_cast<int>(cnt) - static_cast<int>(lane), lane);  // active iff p < cnt_l
@@ -1876,11 +1955,21 @@ __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, c
         const bool ok = codes_guess(CC, r, sc, cp, cm);
         if (active) {
             *po = i;
+            if (kTwin) *po2 = i + tm;
             if (ok) {
                 pc[0] = static_cast<uint16_t>(__byte_perm(cp[0], cp[1], 0x40));
                 pc[1] = static_cast<uint16_t>(__byte_perm(cp[2], cm[0], 0x40));
                 pc[2] = static_cast<uint16_t>(__byte_perm(cm[1], cm[2], 0x40));
+                if (kTwin) {
+                    pc2[0] = static_cast<uint16_t>(__byte_perm(cm[0], cm[1], 0x40));
+                    pc2[1] = static_cast<uint16_t>(__byte_perm(cm[2], cp[0], 0x40));
+                    pc2[2] = static_cast<uint16_t>(__byte_perm(cp[1], cp[2], 0x40));
+                }
             }
+        }
+        if (kTwin) {
+            po2 += 32;
+            pc2 += 96;
         }
         const unsigned rep = __ballot_sync(kFull, active & !ok);
         if (rep) {
@@ -1894,7 +1983,8 @@ __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, c
             if (nq >= 32) {
                 nq -= 32;
                 __syncwarp();
-                emit_repair<kOneRow>(sm, S, A, list, i0, kt, mt, out_codes, queue + nq, 32, lane, ct.code_repairs);
+                emit_repair<kOneRow, kTwin>(sm, S, A, list, i0, kt, mt, out_codes, out_codes2, queue + nq, 32, lane,
+                                            ct.code_repairs);
                 __syncwarp();
             }
         }
@@ -1906,7 +1996,8 @@ __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, c
     }
     if (nq) {
         __syncwarp();
-        emit_repair<kOneRow>(sm, S, A, list, i0, kt, mt, out_codes, queue, nq, lane, ct.code_repairs);
+        emit_repair<kOneRow, kTwin>(sm, S, A, list, i0, kt, mt, out_codes, out_codes2, queue, nq, lane,
+                                    ct.code_repairs);
         __syncwarp();
     }
 }
@@ -1939,7 +2030,11 @@ __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
         const uint32_t cnt = min(A.tile_count[t] - p0, 1u << A.emit_shift);
         const unsigned long long base = base0 + A.tile_base[t] + p0;
         const uint16_t* list = A.scratch + static_cast<size_t>(t) * kTile + p0;
-        if (base + cnt > A.capacity) {
+        // twin tiles (band FAST plans only): this item also writes the twin's
+        // records, further along the same search
+        const bool twin = kMode == kModeBand && kPath == kPathFast && A.twin && A.twin[t];
+        const unsigned long long base2 = twin ? base0 + A.tile_base[t + A.twin_tiles] + p0 : base;
+        if (base2 + cnt > A.capacity) {
             if (lane == 0) ++ct.overflow;
         } else {
             const uint32_t s = t / A.tiles_per_search;
@@ -1954,10 +2049,22 @@ __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
                 const uint32_t mt = i0 - kt * static_cast<uint32_t>(A.na);
                 uint32_t* out_idx = A.out_idx + base;
                 uint8_t* out_codes = A.out_codes + 6 * base;
-                if (mt + static_cast<uint32_t>(kTile) <= static_cast<uint32_t>(A.na)) {
-                    emit_run<true>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes, queue, lane, ct);
+                if (twin) {
+                    // one quantization, two records (the twin's codes proven
+                    // with the bound widened by kTwinSlack)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const float e = __ldg(&S->eps_code[c]) + kTwinSlack;
+                        CC.ec[c] = e <= kCodeSlack ? e : INFINITY;
+                    }
+                    emit_run<true, true>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes,
+                                         A.out_idx + base2, A.out_codes + 6 * base2, queue, lane, ct);
+                } else if (mt + static_cast<uint32_t>(kTile) <= static_cast<uint32_t>(A.na)) {
+                    emit_run<true>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes, nullptr, nullptr, queue,
+                                   lane, ct);
                 } else {
-                    emit_run<false>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes, queue, lane, ct);
+                    emit_run<false>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes, nullptr, nullptr, queue,
+                                    lane, ct);
                 }
             } else {
 #pragma unroll 1

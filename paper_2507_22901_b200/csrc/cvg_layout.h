@@ -17,6 +17,10 @@ constexpr float kCodeSlack = 1.0f / 65536;  // code-table bucket widening (>= ev
 constexpr int kEmitSpan = 256;      // pairs per emit work item (tile sub-range)
 constexpr int kScanItems = 8;        // tile counts per thread in the offset scan
 constexpr int kScanTile = kBlock * kScanItems;
+// Twin tiles: |lin64(k, m) - lin64 of the swapped twin endpoint| <= 2^-33 is
+// proven on the host (plan_build); the emit widens its code-verification
+// bound by this much for the twin's records.
+constexpr float kTwinSlack = 1.0f / 4294967296.0f;  // 2^-32
 
 // Per-search constants, one 288-byte record per (target, pattern, thresholds).
 // The FP32 half feeds the fast path; the FP64 half is the bit-exact restatement
@@ -144,6 +148,17 @@ struct LaunchArgs {
     const float* strip_trig;
     const float* radius_groups;    // [ceil(nr/4)][3][4]: per 4 rows float(r), float(r^2), float(r^3)
                                    // of the double radii (strip form; padded with the last radius)
+    // Twin tiles (PAIRS on rows of whole tiles, grid symmetric under
+    // theta -> theta + pi; plan_build proves it): candidate (k, m + na/2) is
+    // candidate (k, m) with the endpoints swapped.  lists_kernel compares the
+    // pass words of tile t (first half of a row) and its twin t + twin_tiles
+    // word for word; twin[t] = 1 when they are identical, and the emit then
+    // quantizes each pair of t once and writes both records (codes swapped).
+    // nullptr = off.
+    uint8_t* twin;                 // [n_tiles]
+    uint32_t twin_tiles;           // lst_tpr / 2
+    uint32_t twin_m;               // na / 2
+    uint32_t twin_split_test;      // test hook: treat odd rows as differing (both lists built)
     unsigned long long* total;     // [1] sum of tile_count (PAIRS)
     uint32_t* out_idx;           // [capacity]
     uint8_t* out_codes;          // [capacity * 6]

@@ -207,6 +207,46 @@ GridTables make_grid_tables(const cvg_search_desc* d) {
     return g;
 }
 
+// Twin tiles: the grid maps onto itself under theta -> theta + pi,
+// so candidate (k, m + na/2) is candidate (k, m) with its endpoints swapped.
+// The reference's sin/cos of the twin angles are not exactly the negated ones;
+// this bounds what that changes in the FP64 linear values (search.cpp:243-262)
+// of every search of the plan: the derivative of a linear value in sin (cos) is
+// M_c0 wx f^-1'(fx) r / 500 (M_c2 wz f^-1'(fz) r / 200), f^-1' <= max(3 u^2,
+// 116 / kappa) for |u| <= the largest |fx| (|fz|), plus the FP64 rounding of
+// both evaluations (< 2^-46 of the terms' magnitude).  Twins are used only
+// when that is <= 2^-33; the emit widens its code bound by 2^-32 (kTwinSlack).
+bool twin_grid(const std::vector<double>& trig_d, int na, const double* radii, int nr, const SearchConst* recs,
+               size_t n_sc) {
+    if (na < 2 || na % 2 != 0 || nr < 1) return false;
+    const int h = na / 2;
+    double ds = 0.0, dc = 0.0;
+    for (int m = 0; m < h; ++m) {
+        ds = std::max(ds, std::fabs(trig_d[2 * m] + trig_d[2 * (m + h)]));
+        dc = std::max(dc, std::fabs(trig_d[2 * m + 1] + trig_d[2 * (m + h) + 1]));
+    }
+    if (!(ds <= 1e-12 && dc <= 1e-12)) return false;  // also NaN
+    double rmax = 0.0;
+    for (int k = 0; k < nr; ++k) rmax = std::max(rmax, std::fabs(radii[k]));
+    double fy = 0.0, ta = 0.0, tb = 0.0, wx = 0.0, wz = 0.0, cy = 0.0;
+    for (size_t u = 0; u < n_sc; ++u) {
+        const SearchConst& r = recs[u];
+        fy = std::max(fy, std::fabs(r.fy));
+        ta = std::max(ta, std::fabs(r.ta));
+        tb = std::max(tb, std::fabs(r.tb));
+        wx = std::max(wx, std::fabs(r.wx));
+        wz = std::max(wz, std::fabs(r.wz));
+        for (int q = 0; q < 3; ++q) cy = std::max(cy, std::fabs(r.cy64[q]));
+    }
+    constexpr double kM = 3.25;  // >= every |kXyzToRgb| entry (convert_kernel.hpp:47)
+    const double fxm = fy + (ta + rmax) / 500.0, fzm = fy + (tb + rmax) / 200.0;
+    const double ls = kM * wx * std::max(3.0 * fxm * fxm, 0.13) * rmax / 500.0;
+    const double lc = kM * wz * std::max(3.0 * fzm * fzm, 0.13) * rmax / 200.0;
+    const double mag = kM * (wx * fxm * fxm * fxm + wz * fzm * fzm * fzm) + cy + 1.0;
+    const double delta = 2.0 * (ls * ds + lc * dc) + std::ldexp(mag, -46);
+    return std::isfinite(delta) && delta <= std::ldexp(1.0, -33);
+}
+
 int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTables* grid = nullptr,
                const SearchConst* pre = nullptr) {
     const double tb0 = now_ms();
@@ -527,6 +567,17 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     const size_t o_tc = W.take(sizeof(uint32_t) * (pairs ? n_tiles : 0));
     const size_t o_tb = W.take(sizeof(unsigned long long) * (pairs ? n_tiles : 0));
     const size_t o_wl = W.take(sizeof(uint32_t) * (pairs ? n_tiles * (cvg::kTile / cvg::kEmitSpan) : 0));
+    // Twin tiles: PAIRS strip plans whose rows hold an even number of whole
+    // tiles, on a grid twin_grid proves symmetric.  CVG_TWIN=0 turns them off
+    // (A/B); CVG_TWIN_SPLIT_TEST=1 builds both lists of every odd row (tests).
+    const int twin_env = [] {
+        const char* e = std::getenv("CVG_TWIN");
+        return e ? std::atoi(e) : 1;
+    }();
+    const bool twin = pairs && strips && twin_env != 0 && A.lst_tpr >= 2 && A.lst_tpr % 2 == 0 &&
+                      A.lst_unit_rows == 8 &&
+                      twin_grid(trig_d, p->na, d->radii, p->nr, at<const SearchConst>(stage, o_sc), n_sc);
+    const size_t o_tw = W.take(twin ? n_tiles : 0);
     p->d_work = ctx->dev.alloc(W.off);
     if (!p->d_work) return fail(CVG_ENOMEM, "device allocation of the workspace failed");
     A.status = at<unsigned long long>(p->d_work, o_st);
@@ -537,6 +588,14 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.tile_base = at<unsigned long long>(p->d_work, o_tb);
     A.total = at<unsigned long long>(p->d_work, o_to);
     A.worklist = at<uint32_t>(p->d_work, o_wl);
+    A.twin = twin ? at<uint8_t>(p->d_work, o_tw) : nullptr;
+    A.twin_tiles = twin ? A.lst_tpr / 2 : 0u;
+    A.twin_m = twin ? static_cast<uint32_t>(p->na / 2) : 0u;
+    A.twin_split_test = [] {
+        const char* e = std::getenv("CVG_TWIN_SPLIT_TEST");
+        return e && std::atoi(e) != 0 ? 1u : 0u;
+    }();
+    p->twin = twin;
     A.search_begin = 0;
     A.range_searches = static_cast<uint32_t>(p->n_exec);
     A.tile_begin = 0;
@@ -954,6 +1013,8 @@ int cvg_plan_last_kernel_ms(cvg_plan* p, float* ms) {
 uint64_t cvg_plan_input_bytes(const cvg_plan* p) { return p ? p->input_bytes : 0; }
 
 int32_t cvg_plan_evaluated_searches(const cvg_plan* p) { return p ? (p->empty ? 0 : p->n_exec) : 0; }
+
+int cvg_plan_twin_tiles(const cvg_plan* p) { return p && p->twin ? 1 : 0; }
 
 int cvg_plan_copy_first(cvg_plan* p, uint32_t* first_idx, uint8_t* first_codes, void* stream) {
     if (!p) return fail(CVG_EINVAL, "null plan");

@@ -693,3 +693,58 @@ def test_strip_tiles_edge_shapes(ctx, oracle, nr, na, out):
                 assert res["first_idx"][s] == oi[0] and np.array_equal(res["first_codes"][s], oc[0]), s
             else:
                 assert res["first_idx"][s] == 0xFFFFFFFF
+
+
+# ---- twin tiles (PAIRS, rows of whole tiles, grid symmetric under +pi) -----
+
+def _twin_workload(na, angles=None, nr=36, n=6, seed=7):
+    rng = np.random.default_rng(seed)
+    t = rng.integers(60, 250, (n, 3)).astype(np.int32)
+    t[0] = [170, 170, 170]
+    t[1] = [8, 8, 8]  # near black: the linear branch of f^-1
+    p = rng.integers(1, 8, n).astype(np.int32)
+    p[0] = 7
+    v = rng.choice([50.0, 100.0], n)
+    r = rng.choice([0.25, 0.5], n)
+    return W.Workload("twin", t, p, v, r, W.radii(nr, 128.0 / (nr - 1)),
+                      W.angles(na) if angles is None else angles)
+
+
+@pytest.mark.parametrize("na", [8192, 16384])
+def test_twin_tiles_match_oracle(ctx, oracle, na, monkeypatch):
+    """Twin tiles on: every search's records equal the oracle's; the same
+    with both lists built for every odd row (the split path a differing twin
+    row takes) and with twins off."""
+    wl = _twin_workload(na)
+    plan = ctx.plan(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles)
+    assert plan.twin_tiles
+    res = run(ctx, wl)
+    assert_clean(res, "fast")
+    assert res["n_pairs"] > 0
+    for s in range(wl.n_searches):
+        oi, oc = oracle_records(oracle, wl, s, workers=8)
+        idx, codes = split(res, s)
+        assert np.array_equal(idx, oi), s
+        assert np.array_equal(codes, oc), s
+    want = sha_by_search(res)
+    monkeypatch.setenv("CVG_TWIN_SPLIT_TEST", "1")
+    assert sha_by_search(run(ctx, wl)) == want
+    monkeypatch.delenv("CVG_TWIN_SPLIT_TEST")
+    monkeypatch.setenv("CVG_TWIN", "0")
+    plan0 = ctx.plan(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles)
+    assert not plan0.twin_tiles
+    assert sha_by_search(run(ctx, wl)) == want
+
+
+def test_twin_tiles_off_on_asymmetric_grid(ctx, oracle):
+    """Angles over half a circle: no twin tiles; results still exact."""
+    na = 8192
+    angles = np.pi * np.arange(na) / na
+    wl = _twin_workload(na, angles=angles, nr=20)
+    plan = ctx.plan(wl.targets, wl.patterns, wl.v_th, wl.r_novib, wl.radii, wl.angles)
+    assert not plan.twin_tiles
+    res = run(ctx, wl)
+    for s in range(wl.n_searches):
+        oi, oc = oracle_records(oracle, wl, s, workers=8)
+        idx, codes = split(res, s)
+        assert np.array_equal(idx, oi) and np.array_equal(codes, oc), s
