@@ -1639,14 +1639,23 @@ __device__ __forceinline__ uint32_t expand_chunk(uint32_t W, uint32_t wbase, uin
         const uint32_t y = __shfl_up_sync(kFull, incl, o);
         if (lane >= static_cast<unsigned>(o)) incl += y;
     }
+    const uint32_t excl = cnt + incl - pc;
     uint32_t nz = __ballot_sync(kFull, W != 0);
+    // two words per iteration: their shuffles are independent, so the two
+    // latency chains overlap
     while (nz) {
-        const int q = __ffs(nz) - 1;
+        const int q1 = __ffs(nz) - 1;
         nz &= nz - 1;
-        const uint32_t Wq = __shfl_sync(kFull, W, q);
-        const uint32_t oq = __shfl_sync(kFull, incl - pc, q);
-        if ((Wq >> lane) & 1u) {
-            list[cnt + oq + __popc(Wq & lane_lt)] = static_cast<uint16_t>(32u * (wbase + q) + lane);
+        const int q2 = nz ? __ffs(nz) - 1 : q1;
+        const bool two = nz != 0;
+        nz &= nz - 1;
+        const uint32_t W1 = __shfl_sync(kFull, W, q1);
+        const uint32_t o1 = __shfl_sync(kFull, excl, q1);
+        const uint32_t W2 = __shfl_sync(kFull, W, q2);
+        const uint32_t o2 = __shfl_sync(kFull, excl, q2);
+        if ((W1 >> lane) & 1u) list[o1 + __popc(W1 & lane_lt)] = static_cast<uint16_t>(32u * (wbase + q1) + lane);
+        if (two && ((W2 >> lane) & 1u)) {
+            list[o2 + __popc(W2 & lane_lt)] = static_cast<uint16_t>(32u * (wbase + q2) + lane);
         }
     }
     return cnt + __shfl_sync(kFull, incl, 31);

@@ -38,6 +38,10 @@ void plan_free_outputs(cvg_plan* p) {
 void plan_set_density(cvg_plan* p, uint64_t expected_pairs) {
     const uint64_t tiles = p->args.n_tiles ? p->args.n_tiles : 1;
     p->args.emit_shift = expected_pairs >= 256 * tiles ? 9u : 8u;
+    if (const char* e = std::getenv("CVG_EMIT_SHIFT")) {  // A/B override (8..12)
+        const int v = std::atoi(e);
+        if (v >= 8 && v <= 12) p->args.emit_shift = static_cast<uint32_t>(v);
+    }
 }
 
 int plan_reserve(cvg_plan* p, uint64_t cap) {
