@@ -1056,8 +1056,9 @@ int cvg_plan_set_phase_marks(cvg_plan* p, int on) {
 
 int cvg_plan_launches(const cvg_plan* p) {
     if (!p || p->empty) return 0;
-    // phase 1 [+ scan + emit] [+ first codes] [+ best] [+ memo scatter]
-    return (p->out == cvg::kOutPairs ? 3 : p->out == cvg::kOutFirst ? 2 : 1) + (p->best ? 1 : 0) + (p->memo ? 1 : 0);
+    // phase 1 [+ tile lists (strip plans) + scan + emit] [+ first codes] [+ best] [+ memo scatter]
+    const int pairs = p->out == cvg::kOutPairs ? (p->args.masks ? 4 : 3) : 0;
+    return (pairs ? pairs : p->out == cvg::kOutFirst ? 2 : 1) + (p->best ? 1 : 0) + (p->memo ? 1 : 0);
 }
 
 uint64_t cvg_plan_candidates(const cvg_plan* p) { return p ? p->candidates : 0; }

@@ -509,7 +509,7 @@ def test_plan_overflow_then_reserve(ctx):
     for _ in range(3):  # repeated runs reuse the device buffers
         plan.run()
     assert plan.sync() == 3785016
-    assert plan.launches == 3  # phase 1, offset scan, emit
+    assert plan.launches == 4  # phase 1, tile lists (strip tiles), offset scan, emit
     # kernels chained by programmatic dependent launch: no per-kernel split
     # unless phase marks are requested (events between the kernels)
     with pytest.raises(ValueError, match="phase marks"):
