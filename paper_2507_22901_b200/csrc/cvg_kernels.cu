@@ -1342,11 +1342,37 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
     }
 }
 
+// strip_run's bulk skip: the largest g <= n such that rows [k0, k0 + kStripG g)
+// hold no lane whose slot-0 strip statistic can reach la (bisection on the
+// bound described there; warp-uniform result).
+__device__ __forceinline__ uint32_t skip_groups(const float* radius_groups, uint32_t k0, uint32_t n, float k0s,
+                                             float k2s, float l1s, float l3s, float la) {
+    auto below = [&](uint32_t groups) {  // rows [k0, k0 + kStripG * groups) skippable?
+        const uint32_t ke = k0 + kStripG * groups - 1;  // last row of the range
+        const float* g = radius_groups + 12 * (ke >> 2) + (ke & 3u);
+        const float rb = __ldg(g), r2b = __ldg(g + 4), r3b = __ldg(g + 8);
+        const float a = fmaxf(fabsf(k0s), fabsf(fmaf(k2s, r2b, k0s)));
+        const float b = fmaf(fabsf(l3s), r3b, fabsf(l1s) * rb);
+        return __all_sync(kFull, (a + b) * (1.0f + 1.0f / 1048576.0f) < la);
+    };
+    if (n == 0 || !below(1)) return 0u;
+    uint32_t lo = 1, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (below(mid)) {
+            lo = mid;
+        } else {
+            hi = mid - 1;
+        }
+    }
+    return lo;
+}
+
 // Rows [k0, k1) of the strip at angles m0 + lane.  The full constants are
 // loaded for the strip set-up and again (through an opaque pointer, so the
 // two loads are not merged) for the linear rows: during the cube-only rows
 // only the strip constants and the thresholds are live.
-template <int kL, int kOut>
+template <int kL, int kOut, bool kSkip>
 __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0, const LaunchArgs& A, uint32_t m0,
                                           uint32_t k0, uint32_t k1, unsigned lane, uint32_t& cnt, uint32_t& fk,
                                           Counters& ct, uint32_t* mcol = nullptr) {
@@ -1390,7 +1416,32 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0
         strip_setup(C, sc, Q);
         if (!m_ok) Q = StripConsts{};  // the partial strip's idle lanes never pass (strip_rows)
     }
-    strip_rows<kL, true, kOut>(S, T, Q, A, sc, m_ok, m, k0, kc, cnt, fk, ct, mcol);
+    // Bulk skip of the inner rows (slot 0): rows [k0, ks) where no lane's
+    // slot-0 statistic can reach la -- exactly the groups strip_rows would
+    // stop after slot 0 -- found by bisection over the row groups.  Over rows
+    // up to radius rb (float r, r^2, r^3 of the radii, ascending) the strip
+    // form's slot-0 value is at most
+    //     max(|K0|, |K0 + rb^2 K2|) + rb |L1| + rb^3 |L3|
+    // (A = K0 + r^2 K2 is linear in r^2, so |A| peaks at an end of the range;
+    // B = r L1 + r^3 L3 by the triangle inequality), non-decreasing in rb.
+    // The 2^-20 relative margin covers the FP32 rounding of both this bound
+    // and the per-candidate value (a few operations of 2^-24 each).
+    // The first group is tested first: where it cannot be skipped (the pass
+    // region starts at the centre) the search costs one step.  kSkip: its
+    // own instantiation; the PAIRS kernels of small strips (cfg1, cfg3) ran
+    // 10-17% slower with this code present even when it skipped nothing.
+    uint32_t ks = k0;
+    if constexpr (kSkip) {
+        const uint32_t lo = A.bulk_skip && kc > k0
+                                ? skip_groups(A.radius_groups, k0, (kc - k0) / kStripG, Q.k0[0], Q.k2[0], Q.l1[0],
+                                              Q.l3[0], T.la)
+                                : 0u;
+        ks = k0 + kStripG * lo;
+        if constexpr (kOut == kOutPairs) {
+            for (uint32_t b = k0; b + 32 <= ks; b += 32) mcol[b + lane] = 0u;  // whole skipped 32-row blocks
+        }
+    }
+    strip_rows<kL, true, kOut>(S, T, Q, A, sc, m_ok, m, ks, kc, cnt, fk, ct, mcol);
     if (kc == k1) {
         if constexpr (kOut == kOutPairs) {
             if (k1 & 31u) mcol[((k1 - 1) & ~31u) + lane] = cnt;  // the last, partial 32-row block
@@ -1440,7 +1491,7 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0
 // One strip tile of search s: strips [lt' * strip_per_tile, ...) of row
 // block kb (lt = kb * tiles_per_block + lt'); per-search count and first
 // canonical pair recorded here.
-template <int kL, int kOut>
+template <int kL, int kOut, bool kSkip>
 __device__ __forceinline__ void strip_tile(const SearchConst* S, const LaunchArgs& A, uint32_t s, uint32_t lt,
                                            unsigned lane, Counters& ct) {
     const uint32_t kb = lt / A.strip_tiles, st = lt - kb * A.strip_tiles;
@@ -1456,13 +1507,14 @@ __device__ __forceinline__ void strip_tile(const SearchConst* S, const LaunchArg
         uint32_t* mblk = A.masks + static_cast<size_t>(s) * n_strips * A.mask_rows;
         for (uint32_t q = s0; q < s1; ++q) {
             uint32_t w = 0, fk = 0;
-            strip_run<kL, kOut>(S, C, A, 32 * q, k0, k1, lane, w, fk, ct, mblk + static_cast<size_t>(q) * A.mask_rows);
+            strip_run<kL, kOut, kSkip>(S, C, A, 32 * q, k0, k1, lane, w, fk, ct,
+                                       mblk + static_cast<size_t>(q) * A.mask_rows);
         }
         return;
     }
     for (uint32_t q = s0; q < s1; ++q) {
         uint32_t fk = 0xffffffffu;
-        strip_run<kL, kOut>(S, C, A, 32 * q, k0, k1, lane, cnt, fk, ct);
+        strip_run<kL, kOut, kSkip>(S, C, A, 32 * q, k0, k1, lane, cnt, fk, ct);
         if (kOut == kOutFirst) {
             const uint32_t mq = A.strip_perm ? __ldg(&A.strip_perm[32 * q + lane]) : 32 * q + lane;  // the lane's angle
             const uint32_t mine = fk != 0xffffffffu ? fk * static_cast<uint32_t>(A.na) + mq : 0xffffffffu;
@@ -1482,7 +1534,9 @@ __device__ __forceinline__ void strip_tile(const SearchConst* S, const LaunchArg
 // counts; FIRST: counts + first passing index.
 // kPrune (CVG_PATH_PRUNED, band mode): its own instantiation, so that the
 // unpruned loops keep their register allocation (a run-time flag cost 1-2%).
-template <int kMode, int kOut, int kPath, bool kPrune = false, bool kStrips = false>
+// kStrips: 0 = row-major tiles, 1 = strip tiles, 2 = strip tiles with the
+// bulk skip of the inner rows (strip_run).
+template <int kMode, int kOut, int kPath, bool kPrune = false, int kStrips = 0>
 __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
@@ -1554,14 +1608,14 @@ __global__ void __launch_bounds__(kBlock, 4) phase1_kernel(const LaunchArgs A) {
         // kStrips (COUNTS / FIRST, band FAST path, LaunchArgs::strips): its
         // own instantiation, so that the row-major loops keep their registers
         constexpr bool kStripsOk = kMode == kModeBand && kPath == kPathFast && !kPrune;
-        if constexpr (kStrips && kStripsOk) {
+        if constexpr (kStrips != 0 && kStripsOk) {
             const uint32_t nl = (__ldg(&S->flags) >> 10) & 3u;
             if (nl == 3) {
-                strip_tile<3, kOut>(S, A, s, lt, lane, ct);
+                strip_tile<3, kOut, kStrips == 2>(S, A, s, lt, lane, ct);
             } else if (nl == 2) {
-                strip_tile<2, kOut>(S, A, s, lt, lane, ct);
+                strip_tile<2, kOut, kStrips == 2>(S, A, s, lt, lane, ct);
             } else {
-                strip_tile<1, kOut>(S, A, s, lt, lane, ct);
+                strip_tile<1, kOut, kStrips == 2>(S, A, s, lt, lane, ct);
             }
             // counts / first pair recorded; PAIRS: pass words written, the
             // tile lists come from lists_kernel
@@ -2252,7 +2306,13 @@ cudaError_t phase1_t(const LaunchArgs& a, int grid, cudaStream_t st) {
         return cudaGetLastError();
     }
     if (kMode == kModeBand && kPath == kPathFast && !kPrune && a.strips) {
-        phase1_kernel<kMode, kOut, kPath, false, true><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);
+        // the bulk skip: always for COUNTS / FIRST; PAIRS when the plan asks
+        // (plan_build: strips of 512 rows)
+        if (kOut == kOutPairs && !a.bulk_skip) {
+            phase1_kernel<kMode, kOut, kPath, false, 1><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);
+        } else {
+            phase1_kernel<kMode, kOut, kPath, false, 2><<<grid, kBlock, phase1_smem<kMode>(), st>>>(a);
+        }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess || kOut != kOutPairs) return e;
         // PAIRS: the canonical tile lists from the pass words

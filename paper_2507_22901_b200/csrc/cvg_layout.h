@@ -146,6 +146,7 @@ struct LaunchArgs {
     // (nullptr: identity, PAIRS)
     const uint32_t* strip_perm;
     const float* strip_trig;
+    uint32_t bulk_skip;            // strip tiles: bisect the inner rows no lane can pass (strip_run)
     const float* radius_groups;    // [ceil(nr/4)][3][4]: per 4 rows float(r), float(r^2), float(r^3)
                                    // of the double radii (strip form; padded with the last radius)
     // Twin tiles (PAIRS on rows of whole tiles, grid symmetric under

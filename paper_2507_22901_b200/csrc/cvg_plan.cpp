@@ -548,6 +548,14 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.strip_perm = permute ? at<const uint32_t>(p->d_const, o_perm) : nullptr;
     A.strip_trig = permute ? at<const float>(p->d_const, o_ptrig) : nullptr;
     A.radius_groups = strips ? at<const float>(p->d_const, o_rg) : nullptr;
+    // Bulk skip of the inner rows of strip tiles (strip_run): COUNTS / FIRST
+    // always; PAIRS on strips of 512 rows (cfg2: phase 1 + lists 1.86 ->
+    // 1.49 ms), not on short strips (cfg1 / cfg3: its instantiation is 10-17%
+    // slower there).  CVG_BULK_SKIP=0/1 forces it off / on (A/B).
+    A.bulk_skip = [&] {
+        if (const char* e = std::getenv("CVG_BULK_SKIP")) return static_cast<uint32_t>(std::atoi(e) != 0);
+        return static_cast<uint32_t>(!pairs_out || strip_rows >= 512);
+    }();
     A.n_tiles = n_tiles;
 
     // ---- per-run workspace --------------------------------------------------

@@ -5,7 +5,8 @@ import argparse
 import os
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+# CVG_PKG_ROOT: import the package from another build tree (A/B of two builds in one run)
+sys.path.insert(0, os.environ.get("CVG_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2507_22901_b200 as cv  # noqa: E402
 from paper_2507_22901_b200 import workloads as W  # noqa: E402
