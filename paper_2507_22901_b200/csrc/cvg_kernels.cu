@@ -1751,6 +1751,7 @@ __global__ void __launch_bounds__(kBlock) lists_kernel(const LaunchArgs A) {
         const uint32_t k0 = ur * kb, rows = min(ur, static_cast<uint32_t>(A.nr) - k0);
         const uint32_t* mblk = A.masks + static_cast<size_t>(s) * nq * A.mask_rows;
         uint32_t split = 0;  // twins: bit j = row k0 + j differs from its twin row
+        uint32_t nzacc = 0;  // OR of the lane's words (and twin words)
         // load: lane -> (strip qs + lane / ur, row k0 + lane % ur)
         {
             const uint32_t kr = lane % ur, qo = lane / ur;
@@ -1761,7 +1762,12 @@ __global__ void __launch_bounds__(kBlock) lists_kernel(const LaunchArgs A) {
                 if (qs + qo < cwu) {
                     const uint32_t w = __ldg(col + static_cast<size_t>(qs) * A.mask_rows);
                     Wb[kr * stride + qs + qo] = w;
-                    if (hcb) diff |= w ^ __ldg(col + twin_col + static_cast<size_t>(qs) * A.mask_rows);
+                    nzacc |= w;
+                    if (hcb) {
+                        const uint32_t w2 = __ldg(col + twin_col + static_cast<size_t>(qs) * A.mask_rows);
+                        diff |= w ^ w2;
+                        nzacc |= w2;
+                    }
                 }
             }
             if (hcb) {  // ur == 8: lanes j, j + 8, j + 16, j + 24 hold row j
@@ -1773,7 +1779,10 @@ __global__ void __launch_bounds__(kBlock) lists_kernel(const LaunchArgs A) {
         __syncwarp();
         uint32_t tcnt = 0;   // lane j: count of the unit's tile slot j
         uint32_t tcnt2 = 0;  // twins: lane j: count of slot j's twin when its row differs
-        for (uint32_t j = 0; j < rows; ++j) {
+        // an all-zero unit (sparse batches: most of them) writes its zero
+        // counts without walking its rows
+        const uint32_t n_rows = __any_sync(kFull, nzacc != 0u) ? rows : 0u;
+        for (uint32_t j = 0; j < n_rows; ++j) {
             const uint32_t row = k0 + j;
             const uint32_t slot = A.lst_rpt ? j / A.lst_rpt : j;
             const uint32_t lt = A.lst_rpt ? row / A.lst_rpt : row * A.lst_tpr + cb;
