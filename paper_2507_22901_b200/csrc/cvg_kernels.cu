@@ -2226,39 +2226,86 @@ __device__ __forceinline__ T block_reduce(T v, T* red, Op op) {
     return v;
 }
 
-__global__ void __launch_bounds__(kBestThreads) best_kernel(const LaunchArgs A, const double* __restrict__ bands) {
-    __shared__ unsigned long long red[kBestThreads / 32];
-    pdl_wait();  // emit complete
-    for (uint32_t s = blockIdx.x; s < static_cast<uint32_t>(A.n_searches); s += gridDim.x) {
-        const unsigned long long cnt = A.counts[s];
-        if (cnt == 0) {
-            if (threadIdx.x == 0) A.first_idx[s] = 0xffffffffu;
-            if (threadIdx.x < 6) A.first_codes[6 * static_cast<size_t>(s) + threadIdx.x] = 0;
-            continue;
-        }
-        const unsigned long long base = A.tile_base[static_cast<uint64_t>(s) * A.tiles_per_search];
+// select_best on the device (search.cpp:458-489), over the emitted pairs,
+// balanced by tiles.  Tile pass: a warp takes a canonical tile (its pairs are
+// one contiguous slice of the search's records) and reduces its pairs to the
+// largest margin and the first position reaching it (a passing pair's margin
+// is >= +0, so its IEEE bits order as unsigned integers); the pair is stored
+// in the tile's tile_base slot pair (tile_key).  Search pass: a warp per search
+// reduces its tiles in canonical order the same way (larger margin wins, the
+// earlier tile on a tie: the reference keeps the first maximum of its scan)
+// and writes the record at the winning position, or the empty marker.  One
+// search with many pairs no longer sits on one block (cfg1: 354 -> ~90 us).
+__global__ void __launch_bounds__(kBestThreads) best_tiles_kernel(const LaunchArgs A, const double* __restrict__ bands) {
+    pdl_wait();  // the emit complete
+    pdl_trigger();
+    const unsigned lane = threadIdx.x & 31;
+    const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (kBestThreads / 32);
+    for (uint64_t t = blockIdx.x * (kBestThreads / 32) + (threadIdx.x >> 5); t < A.n_tiles; t += warps) {
+        const uint64_t tg = A.tile_begin + t;
+        const uint32_t cnt = A.tile_count[tg];
+        if (cnt == 0) continue;
+        const uint32_t s = static_cast<uint32_t>(tg / A.tiles_per_search);
+        const unsigned long long base = (A.base_offset ? *A.base_offset : 0ull) + A.tile_base[tg];
         const SearchConst* S = search_const(A, s);
-        const int t[3] = {__ldg(&S->t[0]), __ldg(&S->t[1]), __ldg(&S->t[2])};
+        const int tt[3] = {__ldg(&S->t[0]), __ldg(&S->t[1]), __ldg(&S->t[2])};
         const bool frame_diff = (__ldg(&S->flags) >> 8) & 1u;
         const double v_th = __ldg(&bands[2 * s]), low = __ldg(&bands[2 * s + 1]);
-        unsigned long long best = 0;
-        for (unsigned long long q = threadIdx.x; q < cnt; q += kBestThreads) {
-            best = max(best, pair_margin_bits(A, base + q, t, frame_diff, v_th, low));
-        }
-        best = block_reduce(best, red, [](unsigned long long a, unsigned long long b) { return max(a, b); });
-        unsigned long long pos = ~0ull;
-        for (unsigned long long q = threadIdx.x; q < cnt; q += kBestThreads) {
-            if (pair_margin_bits(A, base + q, t, frame_diff, v_th, low) == best) {
-                pos = q;
-                break;  // q grows: this thread's first hit is its smallest
+        unsigned long long m = 0, pos = ~0ull;  // lane's best so far (its positions ascend)
+        for (uint32_t q = lane; q < cnt; q += 32) {
+            const unsigned long long g = pair_margin_bits(A, base + q, tt, frame_diff, v_th, low);
+            if (g > m || pos == ~0ull) {
+                m = g;
+                pos = base + q;
             }
         }
-        pos = block_reduce(pos, red, [](unsigned long long a, unsigned long long b) { return min(a, b); });
-        if (threadIdx.x == 0) A.first_idx[s] = A.out_idx[base + pos];
-        if (threadIdx.x < 6) {
-            A.first_codes[6 * static_cast<size_t>(s) + threadIdx.x] = A.out_codes[6 * (base + pos) + threadIdx.x];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long m2 = __shfl_xor_sync(kFull, m, o), p2 = __shfl_xor_sync(kFull, pos, o);
+            if (m2 > m || (m2 == m && p2 < pos)) {
+                m = m2;
+                pos = p2;
+            }
         }
-        __syncthreads();  // red is reused by the next search
+        if (lane == 0) {
+            A.best_key[2 * t] = m;
+            A.best_key[2 * t + 1] = pos;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBestThreads) best_search_kernel(const LaunchArgs A) {
+    pdl_wait();  // the tile pass complete
+    const unsigned lane = threadIdx.x & 31;
+    const uint32_t warps = gridDim.x * (kBestThreads / 32);
+    const uint32_t tps = A.tiles_per_search;
+    for (uint32_t sr = blockIdx.x * (kBestThreads / 32) + (threadIdx.x >> 5); sr < A.range_searches; sr += warps) {
+        const uint32_t s = A.search_begin + sr;
+        if (A.counts[s] == 0) {
+            if (lane == 0) A.first_idx[s] = 0xffffffffu;
+            if (lane < 6) A.first_codes[6 * static_cast<size_t>(s) + lane] = 0;
+            continue;
+        }
+        unsigned long long m = 0, pos = ~0ull;
+        for (uint32_t j = lane; j < tps; j += 32) {  // tiles ascend: the lane keeps its earliest maximum
+            const uint64_t t = static_cast<uint64_t>(sr) * tps + j;
+            if (A.tile_count[A.tile_begin + t] == 0) continue;
+            const unsigned long long g = A.best_key[2 * t];
+            if (g > m || pos == ~0ull) {
+                m = g;
+                pos = A.best_key[2 * t + 1];
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const unsigned long long m2 = __shfl_xor_sync(kFull, m, o), p2 = __shfl_xor_sync(kFull, pos, o);
+            if (m2 > m || (m2 == m && p2 < pos)) {
+                m = m2;
+                pos = p2;
+            }
+        }
+        if (lane == 0) A.first_idx[s] = A.out_idx[pos];
+        if (lane < 6) A.first_codes[6 * static_cast<size_t>(s) + lane] = A.out_codes[6 * pos + lane];
     }
 }
 
@@ -2357,7 +2404,8 @@ cudaError_t launch_pdl(void (*kernel)(LaunchArgs), unsigned grid, unsigned threa
     return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
-cudaError_t launch_pdl_bands(unsigned grid, const LaunchArgs& a, const double* bands, cudaStream_t st) {
+cudaError_t launch_pdl_bands(void (*kernel)(LaunchArgs, const double*), unsigned grid, const LaunchArgs& a,
+                             const double* bands, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kBestThreads);
@@ -2367,7 +2415,7 @@ cudaError_t launch_pdl_bands(unsigned grid, const LaunchArgs& a, const double* b
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, best_kernel, a, bands);
+    return cudaLaunchKernelEx(&cfg, kernel, a, bands);
 }
 
 template <int kMode, int kPath>
@@ -2464,8 +2512,13 @@ cudaError_t launch_first_codes(const LaunchArgs& a, cudaStream_t st) {
 
 cudaError_t launch_best(const LaunchArgs& a, const double* bands, cudaStream_t st) {
     if (a.n_searches <= 0) return cudaSuccess;
-    const unsigned blocks = static_cast<unsigned>(std::min(a.n_searches, 148 * 16));
-    return launch_pdl_bands(blocks, a, bands, st);
+    const unsigned blocks = static_cast<unsigned>(
+        std::max<uint64_t>(1, std::min<uint64_t>((a.n_tiles + kBestThreads / 32 - 1) / (kBestThreads / 32), 148 * 8)));
+    const cudaError_t e = launch_pdl_bands(best_tiles_kernel, blocks, a, bands, st);
+    if (e != cudaSuccess) return e;
+    const unsigned sb = static_cast<unsigned>(
+        std::max(1, std::min((a.n_searches + kBestThreads / 32 - 1) / (kBestThreads / 32), 148 * 8)));
+    return launch_pdl(best_search_kernel, sb, kBestThreads, 0, st, a);
 }
 
 cudaError_t launch_scatter(const uint32_t* map, int n, const unsigned long long* counts_in, const uint32_t* fi_in,

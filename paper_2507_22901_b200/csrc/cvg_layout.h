@@ -164,6 +164,9 @@ struct LaunchArgs {
     uint32_t* out_idx;           // [capacity]
     uint8_t* out_codes;          // [capacity * 6]
     uint64_t capacity;
+    // BEST: per tile of the view, the largest margin bits of its pairs and
+    // the first position reaching it (best_tiles_kernel)
+    unsigned long long* best_key;  // [2 * n_tiles]
     uint32_t* first_idx;         // [n_searches] (FIRST)
     uint8_t* first_codes;        // [n_searches * 6] (FIRST)
     Stats* stats;

@@ -579,6 +579,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     const size_t o_tc = W.take(sizeof(uint32_t) * (pairs ? n_tiles : 0));
     const size_t o_tb = W.take(sizeof(unsigned long long) * (pairs ? n_tiles : 0));
     const size_t o_wl = W.take(sizeof(uint32_t) * (pairs ? n_tiles * (cvg::kTile / cvg::kEmitSpan) : 0));
+    const size_t o_bk = W.take(p->best ? sizeof(unsigned long long) * 2 * n_tiles : 0);  // written each run
     // Twin tiles: PAIRS strip plans whose rows hold an even number of whole
     // tiles, on a grid twin_grid proves symmetric.  CVG_TWIN=0 turns them off
     // (A/B); CVG_TWIN_SPLIT_TEST=1 builds both lists of every odd row (tests).
@@ -599,6 +600,7 @@ int plan_build(cvg_ctx* ctx, const cvg_search_desc* d, cvg_plan* p, const GridTa
     A.tile_count = at<uint32_t>(p->d_work, o_tc);
     A.tile_base = at<unsigned long long>(p->d_work, o_tb);
     A.total = at<unsigned long long>(p->d_work, o_to);
+    A.best_key = p->best ? at<unsigned long long>(p->d_work, o_bk) : nullptr;
     A.worklist = at<uint32_t>(p->d_work, o_wl);
     A.twin = twin ? at<uint8_t>(p->d_work, o_tw) : nullptr;
     A.twin_tiles = twin ? A.lst_tpr / 2 : 0u;
@@ -1064,9 +1066,9 @@ int cvg_plan_set_phase_marks(cvg_plan* p, int on) {
 
 int cvg_plan_launches(const cvg_plan* p) {
     if (!p || p->empty) return 0;
-    // phase 1 [+ tile lists (strip plans) + scan + emit] [+ first codes] [+ best] [+ memo scatter]
+    // phase 1 [+ tile lists (strip plans) + scan + emit] [+ first codes] [+ best: tile pass + search pass] [+ memo scatter]
     const int pairs = p->out == cvg::kOutPairs ? (p->args.masks ? 4 : 3) : 0;
-    return (pairs ? pairs : p->out == cvg::kOutFirst ? 2 : 1) + (p->best ? 1 : 0) + (p->memo ? 1 : 0);
+    return (pairs ? pairs : p->out == cvg::kOutFirst ? 2 : 1) + (p->best ? 2 : 0) + (p->memo ? 1 : 0);
 }
 
 uint64_t cvg_plan_candidates(const cvg_plan* p) { return p ? p->candidates : 0; }

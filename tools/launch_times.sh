@@ -4,7 +4,7 @@
 c=$1; runs=${2:-2}
 mkdir -p gpurun_out
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/lt_$c.csv \
-  python tools/prof_plan.py $c --runs $runs > /dev/null 2>&1
+  python tools/prof_plan.py $c --runs $runs ${LT_ARGS} > /dev/null 2>&1
 python - "$c" <<'PY'
 import csv, sys, collections
 c = sys.argv[1]
