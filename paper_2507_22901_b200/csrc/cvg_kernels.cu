@@ -1694,6 +1694,13 @@ __device__ __forceinline__ uint32_t expand_chunk(uint32_t W, uint32_t wbase, uin
         if (lane >= static_cast<unsigned>(o)) incl += y;
     }
     const uint32_t excl = cnt + incl - pc;
+    if (__all_sync(kFull, W == 0xffffffffu)) {
+        // every candidate of the chunk passes (dense batches: most non-empty
+        // chunks): the list is the chunk's offsets in order
+#pragma unroll 8
+        for (uint32_t q = 0; q < 32; ++q) list[cnt + 32u * q + lane] = static_cast<uint16_t>(32u * (wbase + q) + lane);
+        return cnt + 1024u;
+    }
     uint32_t nz = __ballot_sync(kFull, W != 0);
     // two words per iteration: their shuffles are independent, so the two
     // latency chains overlap
