@@ -1992,7 +1992,10 @@ __device__ __forceinline__ void emit_repair(const Smem& sm, const SearchConst* S
 // out_idx / out_codes and as the twin tile's pair at out_idx2 / out_codes2
 // (idx + twin_m, plus and minus codes swapped).  The caller widened CC.ec by
 // kTwinSlack, so a verified code is the exact code of both records.
-template <bool kOneRow, bool kTwin = false>
+// kSeq (one-row tiles): the item's list is one run of consecutive offsets
+// (dense batches: pass regions are long arcs), so offsets are computed, not
+// loaded, and the trig loads do not wait on the list.
+template <bool kOneRow, bool kTwin = false, bool kSeq = false>
 __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, const CodeConsts& CC,
                                          const LaunchArgs& A, const uint16_t* list, uint32_t cnt, uint32_t i0,
                                          uint32_t kt, uint32_t mt, uint32_t* out_idx, uint8_t* out_codes,
@@ -2014,8 +2017,10 @@ __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, c
     // division) inside the loop to save the two registers
     const int cnt_l = __shfl_sync(kFull, static_cast<int>(cnt) - static_cast<int>(lane), lane);  // active iff p < cnt_l
     mt = __shfl_sync(kFull, mt, 0);
-    uint32_t off_n = 32 < cnt_l ? list[32 + lane] : 0u;
-    uint32_t i = i0 + (0 < cnt_l ? list[lane] : 0u);
+    const uint32_t off0 = kSeq ? list[0] : 0u;
+    const uint32_t off_last = kSeq ? off0 + cnt - 1 : 0u;
+    uint32_t off_n = kSeq ? min(off0 + 32 + lane, off_last) : (32 < cnt_l ? list[32 + lane] : 0u);
+    uint32_t i = i0 + (kSeq ? min(off0 + lane, off_last) : (0 < cnt_l ? list[lane] : 0u));
     uint32_t k = kOneRow ? kt : div_na(i, A);
     uint32_t m = kOneRow ? i - i0 + mt : i - k * static_cast<uint32_t>(A.na);
     float r = kOneRow ? rt : __ldg(&A.radii_f[k]);
@@ -2028,7 +2033,7 @@ __device__ __forceinline__ void emit_run(const Smem& sm, const SearchConst* S, c
         const uint32_t m_n = kOneRow ? mt + off_n : i_n - k_n * static_cast<uint32_t>(A.na);
         const float r_n = kOneRow ? rt : __ldg(&A.radii_f[k_n]);
         const float2 sc_n = __ldg(trig + m_n);
-        off_n = p + 64 < cnt_l ? *pl : 0u;
+        off_n = kSeq ? min(off0 + p + 64 + lane, off_last) : (p + 64 < cnt_l ? *pl : 0u);
         const bool active = p < cnt_l;
         int cp[3], cm[3];
         const bool ok = codes_guess(CC, r, sc, cp, cm);
@@ -2136,8 +2141,14 @@ __global__ void __launch_bounds__(kBlock, 4) emit_kernel(const LaunchArgs A) {
                         const float e = __ldg(&S->eps_code[c]) + kTwinSlack;
                         CC.ec[c] = e <= kCodeSlack ? e : INFINITY;
                     }
-                    emit_run<true, true>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes,
-                                         A.out_idx + base2, A.out_codes + 6 * base2, queue, lane, ct);
+                    const bool seq = list[cnt - 1] - list[0] == cnt - 1;  // lists ascend strictly
+                    if (seq) {
+                        emit_run<true, true, true>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes,
+                                                   A.out_idx + base2, A.out_codes + 6 * base2, queue, lane, ct);
+                    } else {
+                        emit_run<true, true>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes,
+                                             A.out_idx + base2, A.out_codes + 6 * base2, queue, lane, ct);
+                    }
                 } else if (mt + static_cast<uint32_t>(kTile) <= static_cast<uint32_t>(A.na)) {
                     emit_run<true>(sm, S, CC, A, list, cnt, i0, kt, mt, out_idx, out_codes, nullptr, nullptr, queue,
                                    lane, ct);
