@@ -1696,9 +1696,22 @@ __device__ __forceinline__ uint32_t expand_chunk(uint32_t W, uint32_t wbase, uin
     const uint32_t excl = cnt + incl - pc;
     if (__all_sync(kFull, W == 0xffffffffu)) {
         // every candidate of the chunk passes (dense batches: most non-empty
-        // chunks): the list is the chunk's offsets in order
-#pragma unroll 8
-        for (uint32_t q = 0; q < 32; ++q) list[cnt + 32u * q + lane] = static_cast<uint16_t>(32u * (wbase + q) + lane);
+        // chunks): the list is the ramp 32 wbase + e, e < 1024, written as
+        // 16-byte stores between a short head and tail
+        uint16_t* dst = list + cnt;
+        const uint32_t base = 32u * wbase;
+        const uint32_t head = (8u - ((static_cast<uint32_t>(reinterpret_cast<uintptr_t>(dst)) >> 1) & 7u)) & 7u;
+        if (lane < head) dst[lane] = static_cast<uint16_t>(base + lane);
+        uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+        const uint32_t nb = (1024u - head) >> 3;
+#pragma unroll 4
+        for (uint32_t j = lane; j < nb; j += 32) {
+            const uint32_t v = base + head + 8u * j;
+            d4[j] = make_uint4(v | (v + 1) << 16, (v + 2) | (v + 3) << 16, (v + 4) | (v + 5) << 16,
+                               (v + 6) | (v + 7) << 16);
+        }
+        const uint32_t t0 = head + 8u * nb;
+        if (t0 + lane < 1024u) dst[t0 + lane] = static_cast<uint16_t>(base + t0 + lane);
         return cnt + 1024u;
     }
     uint32_t nz = __ballot_sync(kFull, W != 0);
