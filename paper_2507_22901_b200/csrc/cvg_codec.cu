@@ -23,6 +23,12 @@ namespace {
 
 constexpr int kBlockThreads = 256;  // 8 warps; the fill and the block sums run one task per warp
 
+// Programmatic dependent launch: the fill is launched while the copy drains;
+// its blocks set up their geometry and wait (griddepcontrol.wait: the copy
+// grid complete and its writes visible) before their first store.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Painting, in two passes over device memory:
 //  1. copy2_kernel: frame_a = frame_b = base, a flat 16-byte copy (read once,
 //     write twice: the 9 B/pixel minimum) with four loads in flight per thread;
@@ -35,6 +41,7 @@ __global__ void __launch_bounds__(256) copy2_kernel(const uint4* __restrict__ ba
                                                     uint4* __restrict__ fb, long long n16,
                                                     const uint8_t* __restrict__ base_b, uint8_t* __restrict__ fa_b,
                                                     uint8_t* __restrict__ fb_b, long long n_bytes) {
+    pdl_trigger();  // the fill may launch now (it waits for this grid before storing)
     const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
     long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     for (; i + 3 * stride < n16; i += 4 * stride) {
@@ -96,7 +103,10 @@ __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uin
                                                    const uint32_t* __restrict__ plus,
                                                    const uint32_t* __restrict__ minus) {
     const int task = static_cast<int>(blockIdx.x) * (kBlockThreads / 32) + static_cast<int>(threadIdx.x >> 5);
-    if (task >= n_tasks) return;
+    if (task >= n_tasks) {
+        pdl_wait();
+        return;
+    }
     const int blk = task / slices, slice = task - blk * slices;
     const int bx = __ldg(&xy[2 * blk]), by = __ldg(&xy[2 * blk + 1]);
     const uint32_t pc = __ldg(&plus[blk]), mc = __ldg(&minus[blk]);
@@ -129,6 +139,7 @@ __global__ void __launch_bounds__(256) fill_kernel(uint8_t* __restrict__ fa, uin
         geometry(s0, ws, nw, ph0, nh, t_beg, nt);
         tch = static_cast<int>(t_beg - s0) % 3;
     }
+    pdl_wait();  // the copy pass complete: these bytes are ours now
     for (int r = r0 + g; r < r1; r += groups) {
         const long long s = 3 * (static_cast<long long>(by + r) * width + bx);
         long long wrow;
@@ -314,8 +325,8 @@ int lane_group_log2(int items) {
 
 // Row slices of a block (one warp task each) so that >= 16 warps per SM are
 // in flight in total.
-int rows_per_slice(int n_blocks, int block_h, int sms, unsigned* slices_out) {
-    const long long want = (static_cast<long long>(sms) * 16 + n_blocks - 1) / n_blocks;
+int rows_per_slice(int n_blocks, int block_h, int sms, unsigned* slices_out, int warps_per_sm = 16) {
+    const long long want = (static_cast<long long>(sms) * warps_per_sm + n_blocks - 1) / n_blocks;
     long long slices = want < block_h ? want : block_h;
     if (slices < 1) slices = 1;
     const int rps = static_cast<int>((block_h + slices - 1) / slices);
@@ -341,21 +352,28 @@ cudaError_t launch_paint(const uint8_t* base, uint8_t* fa, uint8_t* fb, int widt
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || n_blocks <= 0) return e;
     unsigned slices = 1;
-    const int rps = rows_per_slice(n_blocks, block_h, sms, &slices);
+    // the fill is store-latency bound: ~48 warps per SM in flight (16 measured slower)
+    const int rps = rows_per_slice(n_blocks, block_h, sms, &slices, 48);
     if ((reinterpret_cast<uintptr_t>(fa) | reinterpret_cast<uintptr_t>(fb)) & 3) return cudaErrorMisalignedAddress;
     const int lg = lane_group_log2((3 * block_w) / 4 + 1);
     const long long tasks = static_cast<long long>(n_blocks) * slices;
     if (tasks > (1ll << 31) - 1) return cudaErrorInvalidConfiguration;
     const int nt = static_cast<int>(tasks);
     const unsigned grid2 = static_cast<unsigned>((tasks + 7) / 8);
-    if (width % 4 == 0) {
-        fill_kernel<true><<<grid2, kBlockThreads, 0, st>>>(fa, fb, width, block_w, block_h, static_cast<int>(slices),
-                                                           rps, lg, nt, xy, plus, minus);
-    } else {
-        fill_kernel<false><<<grid2, kBlockThreads, 0, st>>>(fa, fb, width, block_w, block_h, static_cast<int>(slices),
-                                                            rps, lg, nt, xy, plus, minus);
-    }
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid2);
+    cfg.blockDim = dim3(kBlockThreads);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const int sl = static_cast<int>(slices);
+    return width % 4 == 0 ? cudaLaunchKernelEx(&cfg, fill_kernel<true>, fa, fb, width, block_w, block_h, sl, rps, lg,
+                                               nt, xy, plus, minus)
+                          : cudaLaunchKernelEx(&cfg, fill_kernel<false>, fa, fb, width, block_w, block_h, sl, rps,
+                                               lg, nt, xy, plus, minus);
 }
 
 cudaError_t launch_block_sums(const uint8_t* fa, const uint8_t* fb, int width, int height, int block_w, int block_h,

@@ -28,6 +28,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.environ.get("CVG_PKG_ROOT") or ROOT)  # CVG_PKG_ROOT: A/B another build
 
 
 def main():
