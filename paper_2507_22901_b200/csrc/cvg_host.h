@@ -197,6 +197,7 @@ int validate_color(const int32_t* c);
 int validate_grid(const double* radii, int nr, const double* angles, int na);
 int validate_thresholds(double v_th, double r_novib);
 int validate_desc(const cvg_search_desc* d);
+int validate_header(const cvg_search_desc* d);  // validate_desc without the per-search scan
 
 // Process-wide worker threads for parallel_for: spawning threads per call
 // costs ~10 us each, more than the host work of a sweep-sized batch.  The

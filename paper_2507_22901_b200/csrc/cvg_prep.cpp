@@ -120,7 +120,8 @@ bool batch_clean(const cvg_search_desc* d) {
     return true;
 }
 
-int validate_desc(const cvg_search_desc* d) {
+// The descriptor's scalar fields (no per-search arrays scanned).
+int validate_header(const cvg_search_desc* d) {
     if (!d) return fail(CVG_EINVAL, "null search descriptor");
     if (d->n_searches < 0) return fail(CVG_EINVAL, "n_searches must be >= 0");
     if (d->n_searches > 0 && (!d->target_rgb || !d->pattern_bits || !d->v_th || !d->r_novib)) {
@@ -141,6 +142,11 @@ int validate_desc(const cvg_search_desc* d) {
     if (d->path == CVG_PATH_MEMO && (d->output == CVG_OUT_PAIRS || d->output == CVG_OUT_BEST)) {
         return fail(CVG_EINVAL, "CVG_PATH_MEMO returns per-search counts / first pairs (CVG_OUT_COUNTS or CVG_OUT_FIRST)");
     }
+    return CVG_OK;
+}
+
+int validate_desc(const cvg_search_desc* d) {
+    if (int e = validate_header(d)) return e;
     // Fast screen: branch-free, vectorizable pass over the whole batch.  Only
     // if it finds a problem does the ordered per-search loop below run, to
     // report the first failure with the reference's message and order.

@@ -131,7 +131,7 @@ int search_ranges_fixed(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, i
     }
     std::vector<cvg_plan> plans(K);
     std::vector<cudaEvent_t> kdone(K, nullptr);
-    const GridTables grid = make_grid_tables(d);
+    GridTables grid;  // built once range 0 has validated the grid
     double prep = 0, h2d = 0, t_first_enqueued = 0;
     int err = CVG_OK;
     // growing ranges: the first range's prep (the only one not overlapped)
@@ -147,6 +147,9 @@ int search_ranges_fixed(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, i
         sub.v_th = d->v_th + lo;
         sub.r_novib = d->r_novib + lo;
         const double tb = now_ms();
+        err = validate_desc(&sub);  // cvg_search left the per-search scan to the ranges
+        if (err) break;
+        if (c == 0) grid = make_grid_tables(d);
         err = plan_build_safe(ctx, &sub, &plans[c], &grid);
         if (err) break;
         prep += (plans[c].t_prep_end ? plans[c].t_prep_end : now_ms()) - tb;
@@ -489,7 +492,17 @@ extern "C" {
 int cvg_search(cvg_ctx* ctx, const cvg_search_desc* desc, cvg_result* out) {
     if (!ctx || !out) return fail(CVG_EINVAL, "null context or result");
     result_zero(out);
-    if (int e = validate_desc(desc)) return e;
+    if (int e = validate_header(desc)) return e;
+    // Search ranges (COUNTS / FIRST) validate range by range, each just
+    // before its plan is built, so that the scan of range c + 1 overlaps
+    // range c's kernels (cfg4: ~4 ms of an 88 ms call).  The ranges run in
+    // order, so the first failure reported is the batch's first, with the
+    // reference's message; the other paths validate the whole batch here.
+    const bool ranged_fixed = desc->output != CVG_OUT_PAIRS && desc->path != CVG_PATH_MEMO &&
+                              desc->output != CVG_OUT_BEST && fixed_chunks(desc) > 1;
+    if (!ranged_fixed) {
+        if (int e = validate_desc(desc)) return e;
+    }
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
     if (int e = ensure_device(ctx)) return e;
     // A plan holds < 2^28 tiles (32-bit tile ids with 16 emit items each):

@@ -748,3 +748,30 @@ def test_twin_tiles_off_on_asymmetric_grid(ctx, oracle):
         oi, oc = oracle_records(oracle, wl, s, workers=8)
         idx, codes = split(res, s)
         assert np.array_equal(idx, oi) and np.array_equal(codes, oc), s
+
+
+def test_ranged_batch_validates_range_by_range(ctx):
+    """A COUNTS batch of >= 2^20 searches runs as search ranges, each
+    validated just before its plan: a bad search in a late range still fails
+    the call with the message the whole-batch check gives, and the context
+    keeps working."""
+    n = (1 << 20) + 7
+    rng = np.random.default_rng(5)
+    t = rng.integers(0, 256, (n, 3)).astype(np.int32)
+    p = rng.integers(1, 8, n).astype(np.int32)
+    v = np.full(n, 100.0)
+    r = np.full(n, 0.25)
+    radii, angles = W.radii(4, 20.0), W.angles(32)
+    ok = ctx.search(t, p, v, r, radii, angles, output="counts")
+    assert len(ok["counts"]) == n
+    for field, idx, val in (("patterns", n - 3, 0), ("v_th", n - 1, -1.0), ("targets", 5, 300)):
+        tt, pp, vv = t.copy(), p.copy(), v.copy()
+        {"patterns": pp, "v_th": vv, "targets": tt}[field][idx] = val
+        with pytest.raises(ValueError) as big:
+            ctx.search(tt, pp, vv, r, radii, angles, output="counts")
+        one = slice(idx, idx + 1)
+        with pytest.raises(ValueError) as small:
+            ctx.search(tt[one], pp[one], vv[one], r[one], radii, angles, output="counts")
+        assert str(big.value) == str(small.value), field
+    again = ctx.search(t, p, v, r, radii, angles, output="counts")
+    assert np.array_equal(again["counts"], ok["counts"])
