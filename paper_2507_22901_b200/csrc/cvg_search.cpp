@@ -161,13 +161,27 @@ int search_ranges_fixed(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, i
             err = fail(CVG_ECUDA, "event creation failed");
             break;
         }
-        err = plan_enqueue(&plans[c], ctx->stream);
+        // ranges alternate between two streams: range c + 1's phase-1 blocks
+        // take the SMs that range c's tail leaves idle (CVG_RANGE_STREAMS=1: one)
+        static const bool two = [] {
+            const char* e = std::getenv("CVG_RANGE_STREAMS");
+            return !e || std::atoi(e) != 1;
+        }();
+        cudaStream_t ps = two && (c & 1) ? ctx->tail_stream : ctx->stream;
+        if (ps != ctx->stream) {  // the plan's constants were uploaded on ctx->stream
+            if (cudaEventRecord(kdone[c], ctx->stream) != cudaSuccess ||
+                cudaStreamWaitEvent(ps, kdone[c], 0) != cudaSuccess) {
+                err = fail(CVG_ECUDA, "range stream ordering failed");
+                break;
+            }
+        }
+        err = plan_enqueue(&plans[c], ps);
         if (err) break;
         if (c == 0) t_first_enqueued = now_ms();
         const cvg_plan& p = plans[c];
         auto copy = [&]() -> int {
             cudaStream_t cs = ctx->copy_stream;
-            CVG_CUDA(cudaEventRecord(kdone[c], ctx->stream));
+            CVG_CUDA(cudaEventRecord(kdone[c], ps));
             CVG_CUDA(cudaStreamWaitEvent(cs, kdone[c], 0));
             CVG_CUDA(cudaMemcpyAsync(r->counts + lo, p.args.counts, sizeof(uint64_t) * (hi - lo),
                                      cudaMemcpyDeviceToHost, cs));
@@ -224,6 +238,7 @@ int search_ranges_fixed(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, i
         (void)t_enqueued;
     }
     cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->tail_stream);
     for (int c = 0; c < K; ++c) {
         if (kdone[c]) ctx->events.push_back(kdone[c]);
         if (plans[c].ctx) plan_release(&plans[c]);
