@@ -775,3 +775,30 @@ def test_ranged_batch_validates_range_by_range(ctx):
         assert str(big.value) == str(small.value), field
     again = ctx.search(t, p, v, r, radii, angles, output="counts")
     assert np.array_equal(again["counts"], ok["counts"])
+
+
+@pytest.mark.parametrize("out", ["counts", "first"])
+def test_strip_bulk_skip_random_grids_vs_exact(ctx, out):
+    """The strip tiles' bulk skip of the inner rows (a bound on the strip
+    form, bisection over row groups) on random targets, patterns, thresholds
+    and irregular radius grids up to r = 150 (deep into the linear branch of
+    f^-1): FAST (strip tiles + skip) equals EXACT (FP64 op-for-op, row-major
+    tiles) search by search."""
+    rng = np.random.default_rng(11)
+    for trial in range(3):
+        nr = int(rng.integers(20, 140))
+        radii = np.sort(rng.uniform(0.0, 150.0, nr))
+        radii = np.unique(radii)
+        na = int(rng.choice([64, 96, 128, 256]))
+        n = 96
+        t = rng.integers(0, 256, (n, 3)).astype(np.int32)
+        p = rng.integers(1, 8, n).astype(np.int32)
+        v = rng.uniform(20.0, 200.0, n)
+        r = rng.uniform(0.1, 1.0, n)
+        wl = W.Workload("skip", t, p, v, r, radii, W.angles(na), output=out)
+        fast = run(ctx, wl, output=out)
+        exact = run(ctx, wl, output=out, path="exact")
+        assert np.array_equal(fast["counts"], exact["counts"]), trial
+        if out == "first":
+            assert np.array_equal(fast["first_idx"], exact["first_idx"]), trial
+            assert np.array_equal(fast["first_codes"], exact["first_codes"]), trial
