@@ -211,6 +211,14 @@ CVG_API void cvg_d65_white(double out[3]);
  * 109-112): materializes DeltaMode::Continuous deltas of emitted pairs */
 CVG_API int cvg_pair_signal(const double lab[3], double radius, double angle, const double* white_point,
                             double sp[3], double sm[3]);
+/* Both endpoints of the pair (radius, angle) around `lab`, evaluated on the
+ * host exactly as the reference's serial_search does per candidate
+ * (search.cpp:184-218: displaced_pair, lab_to_linear, quantize_signal /
+ * signal_value): codes sp/sm and pre-quantization signals gp/gm.  The scalar
+ * "previous method" of the API (colorvibe::serial_search), never used by the
+ * device search. */
+CVG_API int cvg_pair_eval(const double lab[3], double radius, double angle, const double* white_point,
+                          int32_t sp[3], int32_t sm[3], double gp[3], double gm[3]);
 CVG_API void cvg_quant_thresholds(double out[256]);
 /* The kernels' FP32 code table: 4097 buckets of linear [0, 1] x {threshold t,
  * code below (int32 bits)}; 8194 floats.  Exposed so tests can check it on

@@ -314,9 +314,43 @@ bool classify_pair(const ChannelDeltas& d, const BitPattern& pattern, const Thre
     return r_ok && g_ok && b_ok;
 }
 
+// The reference's scalar "previous method" (search.cpp:184-218), kept as
+// what it is in the reference: one candidate after another on the host, the
+// baseline the batched search is measured against (run_benchmark's serial
+// column).  It is not a fallback: batch_search and every other
+// search entry point run on the device only.
 std::vector<ColorPair> serial_search(const SrgbColor& target, const VibrationGrid& grid, const BitPattern& pattern,
                                      const Thresholds& th, const SearchOptions& opts) {
-    return search_one(target, grid, pattern, th, opts, CVG_PATH_EXACT);
+    validate_one(target, grid, pattern, th);
+    const double wp[3] = {opts.white_point.x, opts.white_point.y, opts.white_point.z};
+    const int32_t rgb[3] = {target.r, target.g, target.b};
+    double lab[3];
+    check(cvg_srgb_to_lab(rgb, wp, lab));
+    const bool quantized = opts.delta_mode == DeltaMode::Quantized;
+    const bool swing = opts.delta_basis == DeltaBasis::TargetSwing;
+    const double t[3] = {static_cast<double>(target.r), static_cast<double>(target.g), static_cast<double>(target.b)};
+    std::vector<ColorPair> hits;
+    for (double radius : grid.radii) {
+        for (double angle : grid.angles) {
+            int32_t p[3], m[3];
+            double gp[3], gm[3];
+            check(cvg_pair_eval(lab, radius, angle, wp, p, m, gp, gm));
+            const SrgbColor sp{p[0], p[1], p[2]}, sm{m[0], m[1], m[2]};
+            ChannelDeltas d;
+            if (quantized) {
+                d = swing ? channel_deltas(target, sp, sm) : frame_deltas(sp, sm);
+            } else {
+                // continuous_deltas (search.cpp:161-180)
+                double e[3];
+                for (int q = 0; q < 3; ++q) {
+                    e[q] = swing ? std::max(std::abs(gp[q] - t[q]), std::abs(gm[q] - t[q])) : std::abs(gp[q] - gm[q]);
+                }
+                d = ChannelDeltas{e[0], e[1], e[2]};
+            }
+            if (classify_pair(d, pattern, th)) hits.push_back(ColorPair{target, sp, sm, radius, angle, d});
+        }
+    }
+    return hits;
 }
 
 std::vector<ColorPair> batch_search(const SrgbColor& target, const VibrationGrid& grid, const BitPattern& pattern,

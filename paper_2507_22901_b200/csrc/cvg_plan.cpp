@@ -1137,6 +1137,27 @@ int cvg_lab_to_srgb(const double lab[3], const double* wp, int32_t rgb[3]) {
     return 1;
 }
 
+int cvg_pair_eval(const double lab[3], double radius, double angle, const double* wp, int32_t sp[3], int32_t sm[3],
+                  double gp[3], double gm[3]) {
+    if (!lab || !sp || !sm || !gp || !gm) return fail(CVG_EINVAL, "null argument");
+    // displaced_pair (search.cpp:113-123) -> lab_to_linear (convert_kernel.hpp:
+    // 94-105) -> quantize_signal / signal_value (:109-117), per candidate
+    const double da = radius * std::sin(angle);
+    const double db = radius * std::cos(angle);
+    const double plus[3] = {lab[0], lab[1] + da, lab[2] + db};
+    const double minus[3] = {lab[0], lab[1] - da, lab[2] - db};
+    double lp[3], lm[3];
+    to_linear(plus, white_or_d65(wp), lp);
+    to_linear(minus, white_or_d65(wp), lm);
+    for (int c = 0; c < 3; ++c) {
+        sp[c] = quantize(lp[c]);
+        sm[c] = quantize(lm[c]);
+        gp[c] = signal_value(lp[c]);
+        gm[c] = signal_value(lm[c]);
+    }
+    return CVG_OK;
+}
+
 int cvg_pair_signal(const double lab[3], double radius, double angle, const double* wp, double sp[3],
                     double sm[3]) {
     if (!lab || !sp || !sm) return fail(CVG_EINVAL, "null argument");
