@@ -50,6 +50,54 @@ std::vector<size_t> ramp_bounds(size_t n, int K) {
     return lo;
 }
 
+// Range boundaries for the COUNTS / FIRST ranges: a small first range (its
+// prep is the only one the device waits for), sizes doubling up to a plateau
+// (the host prepares ~2.5x faster than the device computes, so range c + 1
+// is ready before range c ends), and a taper so that the last range's
+// read-back, the only one not overlapped, is small.  Weights per range; the
+// batch is cut in proportion.  CVG_RANGE_SHAPE=0: the linear ramp above.
+std::vector<size_t> shaped_bounds(size_t n, int K) {
+    static const int shape = [] {
+        const char* e = std::getenv("CVG_RANGE_SHAPE");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (shape == 0 || K < 6) return ramp_bounds(n, K);
+    std::vector<double> w(K);
+    static const std::vector<double> forced = [] {  // tuning override: CVG_RANGE_WEIGHTS="1,2,4,4,2,1"
+        std::vector<double> v;
+        if (const char* e = std::getenv("CVG_RANGE_WEIGHTS")) {
+            for (const char* q = e; *q;) {
+                char* end = nullptr;
+                const double x = std::strtod(q, &end);
+                if (end == q) break;
+                if (x > 0) v.push_back(x);
+                q = *end == ',' ? end + 1 : end;
+            }
+        }
+        return v;
+    }();
+    if (static_cast<int>(forced.size()) == K) {
+        w = forced;
+    } else {
+        const int up = std::min(5, K / 3), down = std::min(4, K / 3);
+        double top = 1.0;
+        for (int c = 0; c < up; ++c, top *= 2.0) w[c] = top;
+        for (int c = up; c < K - down; ++c) w[c] = top;
+        double t = top;
+        for (int c = K - down; c < K; ++c) w[c] = (t *= 0.5);
+    }
+    double sum = 0.0;
+    for (double x : w) sum += x;
+    std::vector<size_t> lo(K + 1);
+    double acc = 0.0;
+    for (int c = 0; c <= K; ++c) {
+        const size_t b = c == K ? n : static_cast<size_t>(static_cast<double>(n) * (acc / sum));
+        lo[c] = std::max(static_cast<size_t>(c), std::min(n - (K - c), b));  // every range holds a search
+        if (c < K) acc += w[c];
+    }
+    return lo;
+}
+
 struct ChunkTail {
     union {
         cvg::Stats st;
@@ -137,7 +185,9 @@ int search_ranges_fixed(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, i
     // growing ranges: the first range's prep (the only one not overlapped)
     // is short.  Measured cfg4 e2e (C-side ms): K=4 even 224-225,
     // K=4 ramp 227.7, K=8 even 231.0, K=8 ramp 220.2, K=16 ramp 221.2
-    const std::vector<size_t> bounds = ramp_bounds(n, K);
+    // shaped ranges, K = 8 (weights 1,2,4,4,4,4,2,1): cfg4 call 86.4 -> 84.2 ms against the
+    // linear ramp (tools/sweep_ranges_cfg4.sh, tools/sweep_range_weights_cfg4.sh)
+    const std::vector<size_t> bounds = shaped_bounds(n, K);
     for (int c = 0; c < K && !err; ++c) {
         const size_t lo = bounds[c], hi = bounds[c + 1];
         cvg_search_desc sub = *d;
