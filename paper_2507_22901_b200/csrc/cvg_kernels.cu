@@ -1203,7 +1203,9 @@ constexpr uint32_t kStripG = CVG_STRIP_G;  // rows per iteration: 4 or 8 (radius
 // when the block ends.
 // kCubeOnly: the strip form (rows below the strip's cube bound); else the
 // endpoint form, with x on the cube branch when kXCube (every row of the
-// range below the x half of the bound: no select for the x endpoints).
+// range below the x half of the bound: no select for the x endpoints; the
+// caller also passes cos >= 0 with fz0 on the cube branch, so the z endpoint
+// fz0 + r cos needs no select).
 template <int kL, bool kCubeOnly, int kOut, class CT, bool kXCube = false>
 __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, const StripConsts& Q,
                                            const LaunchArgs& A, float2 sc, bool m_ok, uint32_t m, uint32_t k,
@@ -1244,7 +1246,7 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
                 gv[g][0] = finv_fast<kXCube>(fmaf(rr[g], sc.x, C.fx0));
                 gv[g][1] = finv_fast<kXCube>(fmaf(-rr[g], sc.x, C.fx0));
                 gv[g][2] = finv_fast<false>(fmaf(-rr[g], sc.y, C.fz0));
-                gv[g][3] = finv_fast<false>(fmaf(rr[g], sc.y, C.fz0));
+                gv[g][3] = finv_fast<kXCube>(fmaf(rr[g], sc.y, C.fz0));  // kXCube: sc.y >= 0, fz0 on the cube branch
                 const float dp = fmaf(C.mxs[0], gv[g][0], fmaf(C.mzs[0], gv[g][2], C.cys[0]));
                 const float dm = fmaf(C.mxs[0], gv[g][1], fmaf(C.mzs[0], gv[g][3], C.cys[0]));
                 M0[g] = fmaxf(fabsf(dp), fabsf(dm));
@@ -1453,8 +1455,14 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0
     // fx0 - u0 with the rcube margins): the endpoint form without the x select
     const float rbx = fmaf(C.fx0 - kU0f, 1.0f - 4e-6f, -1e-6f) *
                       __ldg(reinterpret_cast<const float2*>(A.strip_inv) + (m0 >> 5)).x * (1.0f - 1e-6f);
-    if (kend > kc && __ldg(&A.radii_f[kend - 1]) < rbx) {
-        strip_rows<kL, false, kOut, Consts, true>(S, C, Q, A, sc, m_ok, m, kc, kend, cnt, fk, ct, mcol);
+    // ... and with the lane's endpoints swapped where cos < 0 (the statistic
+    // max(|d+|, |d-|) is symmetric in the endpoints, and the swapped FFMAs
+    // compute the same values: fma(-r, -s, f0) = fma(r, s, f0)), the "-"
+    // endpoint's z = fz0 + r |c'| >= fz0 stays on the cube branch whenever
+    // fz0 itself is: no select for it either
+    if (kend > kc && __ldg(&A.radii_f[kend - 1]) < rbx && C.fz0 > kU0f) {
+        const float2 scs = make_float2(sc.y < 0.0f ? -sc.x : sc.x, fabsf(sc.y));
+        strip_rows<kL, false, kOut, Consts, true>(S, C, Q, A, scs, m_ok, m, kc, kend, cnt, fk, ct, mcol);
     } else {
         strip_rows<kL, false, kOut>(S, C, Q, A, sc, m_ok, m, kc, kend, cnt, fk, ct, mcol);
     }
