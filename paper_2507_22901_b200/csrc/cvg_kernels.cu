@@ -1213,6 +1213,9 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
                                            uint32_t* mcol = nullptr) {
     // radius groups: {r[4j..4j+3]}, {r^2}, {r^3} as three consecutive float4
     const float4* __restrict__ rg = reinterpret_cast<const float4*>(A.radius_groups) + 3 * (k >> 2);
+    // linear rows: a partial strip's idle lanes never ask for the other slots
+    // (one masked threshold instead of a select per row)
+    const float la_lane = m_ok ? C.la : 3.0e38f;
 #pragma unroll 1
     for (; k != kend; k += kStripG, rg += 3 * (kStripG / 4)) {
         float rr[kStripG], r2[kStripG], r3[kStripG];
@@ -1250,9 +1253,9 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
                 const float dp = fmaf(C.mxs[0], gv[g][0], fmaf(C.mzs[0], gv[g][2], C.cys[0]));
                 const float dm = fmaf(C.mxs[0], gv[g][1], fmaf(C.mzs[0], gv[g][3], C.cys[0]));
                 M0[g] = fmaxf(fabsf(dp), fabsf(dm));
-                mx0 = fmaxf(mx0, m_ok ? M0[g] : 0.0f);
+                mx0 = fmaxf(mx0, M0[g]);
             }
-            go = __any_sync(kFull, mx0 >= C.la);
+            go = __any_sync(kFull, mx0 >= la_lane);
         }
         if (go) {
         float lv[kStripG], qv[kStripG];
