@@ -199,9 +199,16 @@ int search_ranges_fixed(cvg_ctx* ctx, const cvg_search_desc* d, cvg_result* r, i
         const double tb = now_ms();
         err = validate_desc(&sub);  // cvg_search left the per-search scan to the ranges
         if (err) break;
+        const double tv = now_ms();
         if (c == 0) grid = make_grid_tables(d);
+        const double tg = now_ms();
         err = plan_build_safe(ctx, &sub, &plans[c], &grid);
         if (err) break;
+        static const bool trace = std::getenv("CVG_TRACE") != nullptr;
+        if (trace) {
+            std::fprintf(stderr, "[cvg range %d] start@%.3f validate %.3f grid %.3f build %.3f (n = %zu)\n", c, tb - t0,
+                         tv - tb, tg - tv, now_ms() - tg, hi - lo);
+        }
         prep += (plans[c].t_prep_end ? plans[c].t_prep_end : now_ms()) - tb;
         h2d += plans[c].t_upload_end ? plans[c].t_upload_end - plans[c].t_prep_end : 0.0;
         if (!ctx->events.empty()) {
