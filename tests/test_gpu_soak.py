@@ -1,0 +1,97 @@
+"""Time-boxed randomized soak of the FAST device paths (strip tiles with the
+|cos|-sorted walk, the bulk skip, the endpoint-swapped linear rows, PAIRS
+masks + lists + emit, twin tiles) against the EXACT path (FP64 op-for-op,
+row-major tiles) on the same inputs, with a sample of searches also checked
+against the CPU oracle.  Each case draws fresh seeded batches until its time
+box is spent: CVG_SOAK_SECONDS (default 6 s per case; the round-end evidence
+run in profiles/ used 120).  Any mismatch prints the seed and the search.
+"""
+import os
+import time
+
+import numpy as np
+import pytest
+
+from paper_2507_22901_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+BOX = float(os.environ.get("CVG_SOAK_SECONDS", "6"))
+
+
+def draw(rng, pairs):
+    """One random batch: grid shape, radius range and thresholds chosen to
+    land on every branch (cube-only, linear rows, saturated codes, partial
+    strips, irregular angles)."""
+    if pairs:
+        na = int(rng.choice([128, 256, 512, 1024, 4096, 8192]))  # whole strips, canonical tiles (plan_build)
+        nr = int(rng.integers(1, 80 if na <= 1024 else 24))
+        n = int(rng.integers(1, 40 if na <= 1024 else 6))
+    else:
+        na = int(rng.choice([1, 7, 31, 32, 33, 64, 96, 100, 128, 250, 256, 512]))
+        nr = int(rng.integers(1, 160))
+        n = int(rng.integers(1, 400))
+    rmax = float(rng.choice([0.5, 3.0, 20.0, 60.0, 128.0, 150.0, 300.0]))
+    kind = int(rng.integers(0, 3))
+    if kind == 0:
+        radii = W.radii(nr, rmax / max(nr, 1))
+    elif kind == 1:
+        radii = np.unique(np.sort(rng.uniform(0.0, rmax, nr)))
+    else:
+        radii = np.unique(np.round(np.sort(rng.uniform(0.0, rmax, nr)), 3))
+    if pairs or rng.integers(0, 2):
+        angles = W.angles(na)
+    else:
+        angles = np.unique(rng.uniform(0.0, 2 * np.pi, na))
+        angles = angles[angles < 2 * np.pi]
+    dark = rng.integers(0, 4) == 0
+    t = rng.integers(0, 24 if dark else 256, (n, 3)).astype(np.int32)
+    p = rng.integers(1, 8, n).astype(np.int32)
+    v = rng.choice([0.5, 1.0, 7.0, 20.0, 50.0, 100.0, 150.0, 254.9, 255.0, 300.0], n).astype(np.float64)
+    if rng.integers(0, 2):
+        v = rng.uniform(0.5, 260.0, n)
+    r = rng.choice([1.0, 0.5, 0.25, 0.125, 0.01], n).astype(np.float64)
+    return t, p, v, r, radii.astype(np.float64), angles.astype(np.float64)
+
+
+def check_oracle(oracle, res, b, s, basis, what):
+    t, p, v, r, radii, angles = b
+    oi, oc, _ = oracle.search(t[s], int(p[s]), v[s], r[s], radii, angles, delta_basis=basis, method=1,
+                              want_deltas=False)
+    assert int(res["counts"][s]) == len(oi), what
+    if "offsets" in res:
+        a, e = int(res["offsets"][s]), int(res["offsets"][s + 1])
+        assert np.array_equal(res["idx"][a:e], oi) and np.array_equal(res["codes"][a:e], oc), what
+    elif "first_idx" in res and len(oi):
+        assert int(res["first_idx"][s]) == int(oi[0]), what
+        assert np.array_equal(np.asarray(res["first_codes"][s]).ravel(), np.asarray(oc[0]).ravel()), what
+
+
+@pytest.mark.parametrize("out", ["counts", "first", "pairs"])
+def test_soak_fast_vs_exact(ctx, oracle, out):
+    t_end = time.monotonic() + BOX
+    seed0 = {"counts": 1_000_000, "first": 2_000_000, "pairs": 3_000_000}[out]
+    trials = cand = 0
+    while time.monotonic() < t_end or trials < 3:
+        seed = seed0 + trials
+        rng = np.random.default_rng(seed)
+        b = draw(rng, out == "pairs")
+        basis = 0  # strip tiles are the TargetSwing band path
+        fast = ctx.search(*b, output=out, path="fast", delta_basis=basis)
+        exact = ctx.search(*b, output=out, path="exact", delta_basis=basis)
+        what = (out, seed)
+        assert fast["stats"]["class_mismatch"] == 0, what
+        assert np.array_equal(fast["counts"], exact["counts"]), what
+        if out == "first":
+            assert np.array_equal(fast["first_idx"], exact["first_idx"]), what
+            assert np.array_equal(fast["first_codes"], exact["first_codes"]), what
+        if out == "pairs":
+            assert np.array_equal(fast["offsets"], exact["offsets"]), what
+            assert np.array_equal(fast["idx"], exact["idx"]), what
+            assert np.array_equal(fast["codes"], exact["codes"]), what
+        n = len(b[1])
+        for s in rng.choice(n, size=min(n, 2), replace=False):
+            check_oracle(oracle, fast, b, int(s), basis, what + (int(s),))
+        trials += 1
+        cand += n * len(b[4]) * len(b[5])
+    print(f"soak {out}: {trials} batches, {cand} candidates, 0 mismatches")
