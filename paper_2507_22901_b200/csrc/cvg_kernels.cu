@@ -1348,17 +1348,28 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
 }
 
 // strip_run's bulk skip: the largest g <= n such that rows [k0, k0 + kStripG g)
-// hold no lane whose slot-0 strip statistic can reach la (bisection on the
-// bound described there; warp-uniform result).
-__device__ __forceinline__ uint32_t skip_groups(const float* radius_groups, uint32_t k0, uint32_t n, float k0s,
-                                             float k2s, float l1s, float l3s, float la) {
+// hold no lane whose loud strip statistics can all reach la (bisection on the
+// bound described there; warp-uniform result).  A lane needs every loud
+// channel (slots 0 .. kL-1) at la or more, so it is out while the smallest of
+// its loud channels' bounds stays below: different lanes of a strip are
+// limited by different channels (each channel has its own null direction).
+template <int kL>
+__device__ __forceinline__ uint32_t skip_groups(const float* radius_groups, uint32_t k0, uint32_t n,
+                                             const StripConsts& Q, float la) {
+    // (a + b) (1 + 2^-20) < la, with the margin folded into the threshold
+    const float las = la * (1.0f - 1.0f / 524288.0f);
     auto below = [&](uint32_t groups) {  // rows [k0, k0 + kStripG * groups) skippable?
         const uint32_t ke = k0 + kStripG * groups - 1;  // last row of the range
         const float* g = radius_groups + 12 * (ke >> 2) + (ke & 3u);
         const float rb = __ldg(g), r2b = __ldg(g + 4), r3b = __ldg(g + 8);
-        const float a = fmaxf(fabsf(k0s), fabsf(fmaf(k2s, r2b, k0s)));
-        const float b = fmaf(fabsf(l3s), r3b, fabsf(l1s) * rb);
-        return __all_sync(kFull, (a + b) * (1.0f + 1.0f / 1048576.0f) < la);
+        float ub = 3.0e38f;
+#pragma unroll
+        for (int q = 0; q < kL; ++q) {
+            const float a = fmaxf(fabsf(Q.k0[q]), fabsf(fmaf(Q.k2[q], r2b, Q.k0[q])));
+            const float b = fabsf(Q.l3[q] * r3b) + fabsf(Q.l1[q] * rb);  // r >= 0
+            ub = fminf(ub, a + b);
+        }
+        return __all_sync(kFull, ub < las);
     };
     if (n == 0 || !below(1)) return 0u;
     uint32_t lo = 1, hi = n;
@@ -1421,14 +1432,15 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0
         strip_setup(C, sc, Q);
         if (!m_ok) Q = StripConsts{};  // the partial strip's idle lanes never pass (strip_rows)
     }
-    // Bulk skip of the inner rows (slot 0): rows [k0, ks) where no lane's
-    // slot-0 statistic can reach la -- exactly the groups strip_rows would
-    // stop after slot 0 -- found by bisection over the row groups.  Over rows
-    // up to radius rb (float r, r^2, r^3 of the radii, ascending) the strip
-    // form's slot-0 value is at most
+    // Bulk skip of the inner rows: rows [k0, ks) where no lane can have all
+    // its loud statistics at la or more -- groups strip_rows would leave
+    // without a pass or a repair -- found by bisection over the row groups.
+    // Over rows up to radius rb (float r, r^2, r^3 of the radii, ascending)
+    // the strip form's value of a slot is at most
     //     max(|K0|, |K0 + rb^2 K2|) + rb |L1| + rb^3 |L3|
     // (A = K0 + r^2 K2 is linear in r^2, so |A| peaks at an end of the range;
-    // B = r L1 + r^3 L3 by the triangle inequality), non-decreasing in rb.
+    // B = r L1 + r^3 L3 by the triangle inequality), non-decreasing in rb, and
+    // so is a lane's smallest bound over its loud slots.
     // The 2^-20 relative margin covers the FP32 rounding of both this bound
     // and the per-candidate value (a few operations of 2^-24 each).
     // The first group is tested first: where it cannot be skipped (the pass
@@ -1438,8 +1450,7 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0
     uint32_t ks = k0;
     if constexpr (kSkip) {
         const uint32_t lo = A.bulk_skip && kc > k0
-                                ? skip_groups(A.radius_groups, k0, (kc - k0) / kStripG, Q.k0[0], Q.k2[0], Q.l1[0],
-                                              Q.l3[0], T.la)
+                                ? skip_groups<kL>(A.radius_groups, k0, (kc - k0) / kStripG, Q, T.la)
                                 : 0u;
         ks = k0 + kStripG * lo;
         if constexpr (kOut == kOutPairs) {
