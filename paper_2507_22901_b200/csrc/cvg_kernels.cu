@@ -1355,7 +1355,7 @@ __device__ __forceinline__ void strip_rows(const SearchConst* S, const CT& C, co
 // limited by different channels (each channel has its own null direction).
 template <int kL>
 __device__ __forceinline__ uint32_t skip_groups(const float* radius_groups, uint32_t k0, uint32_t n,
-                                             const StripConsts& Q, float la) {
+                                             const StripConsts& Q, float la, uint32_t guess) {
     // (a + b) (1 + 2^-20) < la, with the margin folded into the threshold
     const float las = la * (1.0f - 1.0f / 524288.0f);
     auto below = [&](uint32_t groups) {  // rows [k0, k0 + kStripG * groups) skippable?
@@ -1371,8 +1371,41 @@ __device__ __forceinline__ uint32_t skip_groups(const float* radius_groups, uint
         }
         return __all_sync(kFull, ub < las);
     };
-    if (n == 0 || !below(1)) return 0u;
-    uint32_t lo = 1, hi = n;
+    // lo: groups proven skippable; nothing beyond hi is.  The first probe sits
+    // at the previous strip's answer (consecutive strips of a tile have
+    // neighbouring |cos|) and the next ones gallop away from it in doubling
+    // steps until they bracket the answer: where it still holds the search
+    // costs two steps.  Without one (guess = 0: a tile's first strip, or
+    // nothing skipped last time) the first group is tested first: where it
+    // cannot be skipped (the pass region starts at the centre) the search
+    // costs one step.
+    if (n == 0) return 0u;
+    uint32_t lo = 0, hi = n;
+    const uint32_t g = min(max(guess, 1u), n);
+    if (below(g)) {
+        lo = g;
+        if (guess != 0) {
+            for (uint32_t step = 1; lo < hi; step *= 2) {
+                const uint32_t p = min(lo + step, hi);
+                if (below(p)) {
+                    lo = p;
+                } else {
+                    hi = p - 1;
+                    break;
+                }
+            }
+        }
+    } else {
+        hi = g - 1;
+        for (uint32_t step = 1; lo < hi; step *= 2) {
+            const uint32_t p = hi > step ? hi - step + 1 : 1u;
+            if (below(p)) {
+                lo = p;
+                break;
+            }
+            hi = p - 1;
+        }
+    }
     while (lo < hi) {
         const uint32_t mid = (lo + hi + 1) >> 1;
         if (below(mid)) {
@@ -1391,7 +1424,7 @@ __device__ __forceinline__ uint32_t skip_groups(const float* radius_groups, uint
 template <int kL, int kOut, bool kSkip>
 __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0, const LaunchArgs& A, uint32_t m0,
                                           uint32_t k0, uint32_t k1, unsigned lane, uint32_t& cnt, uint32_t& fk,
-                                          Counters& ct, uint32_t* mcol = nullptr) {
+                                          Counters& ct, uint32_t& guess, uint32_t* mcol = nullptr) {
     // lane slot m0 + lane: angle m (the identity, or the |cos|-sorted
     // permutation of the COUNTS / FIRST strips)
     uint32_t m = m0 + lane;
@@ -1450,8 +1483,12 @@ __device__ __forceinline__ void strip_run(const SearchConst* S, const Consts& C0
     uint32_t ks = k0;
     if constexpr (kSkip) {
         const uint32_t lo = A.bulk_skip && kc > k0
-                                ? skip_groups<kL>(A.radius_groups, k0, (kc - k0) / kStripG, Q, T.la)
+                                ? skip_groups<kL>(A.radius_groups, k0, (kc - k0) / kStripG, Q, T.la,
+                                                  kOut == kOutPairs ? 0u : guess)
                                 : 0u;
+        // PAIRS skips on 512-row strips only (one strip per tile): no hint to
+        // carry, and its instantiation keeps the plain search
+        if constexpr (kOut != kOutPairs) guess = lo;
         ks = k0 + kStripG * lo;
         if constexpr (kOut == kOutPairs) {
             for (uint32_t b = k0; b + 32 <= ks; b += 32) mcol[b + lane] = 0u;  // whole skipped 32-row blocks
@@ -1522,6 +1559,7 @@ __device__ __forceinline__ void strip_tile(const SearchConst* S, const LaunchArg
     const uint32_t n_strips = (static_cast<uint32_t>(A.na) + 31) / 32;
     const uint32_t s0 = st * A.strips_per_tile, s1 = min(s0 + A.strips_per_tile, n_strips);
     uint32_t cnt = 0, first = 0xffffffffu;
+    uint32_t guess = 0;  // bulk skip: the previous strip's skipped groups (warp-uniform; 0 = no hint)
     Consts C;
     load_consts(S, C);
     if constexpr (kOut == kOutPairs) {
@@ -1529,14 +1567,14 @@ __device__ __forceinline__ void strip_tile(const SearchConst* S, const LaunchArg
         uint32_t* mblk = A.masks + static_cast<size_t>(s) * n_strips * A.mask_rows;
         for (uint32_t q = s0; q < s1; ++q) {
             uint32_t w = 0, fk = 0;
-            strip_run<kL, kOut, kSkip>(S, C, A, 32 * q, k0, k1, lane, w, fk, ct,
+            strip_run<kL, kOut, kSkip>(S, C, A, 32 * q, k0, k1, lane, w, fk, ct, guess,
                                        mblk + static_cast<size_t>(q) * A.mask_rows);
         }
         return;
     }
     for (uint32_t q = s0; q < s1; ++q) {
         uint32_t fk = 0xffffffffu;
-        strip_run<kL, kOut, kSkip>(S, C, A, 32 * q, k0, k1, lane, cnt, fk, ct);
+        strip_run<kL, kOut, kSkip>(S, C, A, 32 * q, k0, k1, lane, cnt, fk, ct, guess);
         if (kOut == kOutFirst) {
             const uint32_t mq = A.strip_perm ? __ldg(&A.strip_perm[32 * q + lane]) : 32 * q + lane;  // the lane's angle
             const uint32_t mine = fk != 0xffffffffu ? fk * static_cast<uint32_t>(A.na) + mq : 0xffffffffu;
